@@ -1,0 +1,302 @@
+/*
+ * runq_b200.h — C ABI of the B200-native compressed-execution path.
+ *
+ * Drop-in boundary for the reference engine's hot path (arXiv 2506.10092,
+ * `runq`, /root/reference/proj). Each entry point names the reference
+ * interface it replaces (file:line under proj/core). The reference API is C++
+ * (value-semantics columns, exceptions); this ABI keeps the same operator
+ * set, argument meaning and output encodings, but
+ *   - columns/masks/arrays live in device memory behind opaque handles,
+ *   - errors are int status codes with a thread-local message
+ *     (rq_last_error) instead of exceptions (error.hpp:11-32),
+ *   - no C++ or torch types cross the boundary.
+ *
+ * Ownership: every handle returned through an out-parameter is owned by the
+ * caller and released with the matching *_free. Handles are immutable and
+ * share device buffers internally (reference-counted), so an operator that
+ * keeps its input's positions (arith_scalar, filter with a full-cover mask)
+ * does not copy them. All work is enqueued on the context's CUDA stream;
+ * calls that must know an output size (materialising intersections,
+ * compactions) synchronise that stream once.
+ *
+ * Threading: one context per host thread. Handles may be read from any
+ * context on the same device.
+ */
+#ifndef RUNQ_B200_H
+#define RUNQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (runq::Error / OverflowError / ResourceError, error.hpp:11-26) ---- */
+enum rq_status {
+  RQ_OK = 0,
+  RQ_INVALID = 1,  /* runq::Error: precondition / size mismatch / int div by zero */
+  RQ_OVERFLOW = 2, /* runq::OverflowError (kernels.cpp:21-31) */
+  RQ_RESOURCE = 3, /* runq::ResourceError (primitives.cpp:172-178) or device OOM */
+  RQ_CUDA = 4,     /* CUDA runtime failure */
+  RQ_NCCL = 5      /* NCCL failure */
+};
+
+/* ---- dtypes: runq::DType order (dtype.hpp:11) ---- */
+enum rq_dtype { RQ_I8 = 0, RQ_I16 = 1, RQ_I32 = 2, RQ_I64 = 3, RQ_F32 = 4, RQ_F64 = 5 };
+
+/* ---- encodings: runq::Encoding / runq::MaskEncoding (column.hpp:13-14) ---- */
+enum rq_encoding {
+  RQ_ENC_PLAIN = 0,
+  RQ_ENC_RLE = 1,
+  RQ_ENC_INDEX = 2,
+  RQ_ENC_PLAIN_INDEX = 3,
+  RQ_ENC_RLE_INDEX = 4
+};
+enum rq_mask_encoding {
+  RQ_MASK_PLAIN = 0,
+  RQ_MASK_RLE = 1,
+  RQ_MASK_INDEX = 2,
+  RQ_MASK_COMPOSITE = 3
+};
+
+/* ---- operators: runq::compute::BinOp (align.hpp:70) ---- */
+enum rq_binop {
+  RQ_ADD = 0, RQ_SUB = 1, RQ_MUL = 2, RQ_DIV = 3,
+  RQ_LT = 4, RQ_LE = 5, RQ_EQ = 6, RQ_NE = 7, RQ_GE = 8, RQ_GT = 9
+};
+
+/* ---- aggregate functions: runq::agg::AggFn (groupby.hpp:7) ---- */
+enum rq_aggfn {
+  RQ_SUM = 0, RQ_COUNT = 1, RQ_MIN = 2, RQ_MAX = 3, RQ_AVG = 4, RQ_STD = 5, RQ_VAR = 6
+};
+
+typedef struct rq_ctx_s* rq_ctx_t;   /* device + stream + allocator + pinned scratch */
+typedef struct rq_arr_s* rq_arr_t;   /* typed device array (runq::Array, array.hpp:16) */
+typedef struct rq_col_s* rq_col_t;   /* runq::Column (column.hpp:78) */
+typedef struct rq_mask_s* rq_mask_t; /* runq::MaskColumn (column.hpp:133) */
+
+/* Scalar literal: runq::compute::Scalar = variant<int64_t,double> (align.hpp:76). */
+typedef struct rq_scalar {
+  int32_t is_float;
+  int32_t _pad;
+  int64_t i;
+  double f;
+} rq_scalar;
+
+/*
+ * Host-side column image used by rq_col_upload / rq_col_download.
+ * Field use per encoding (column.hpp:22-76):
+ *   PLAIN       : dtype = storage dtype, logical, has_center/center, n rows, v
+ *   RLE         : dtype of v, n runs, v, s, e, total_size
+ *   INDEX       : dtype of v, n points, v, p, total_size
+ *   PLAIN_INDEX : base as PLAIN (dtype/logical/center/n/v); outliers in
+ *                 dtype2 (== logical), n2, v2, p2
+ *   RLE_INDEX   : runs as RLE (dtype/n/v/s/e); points in dtype2, n2, v2, p2
+ * For download, call rq_col_describe first (fills everything but the
+ * pointers), allocate, then rq_col_download copies into the pointers.
+ */
+typedef struct rq_host_column {
+  int32_t encoding;
+  int32_t dtype;
+  int32_t logical;
+  int32_t has_center;
+  int64_t center;
+  int64_t total_size;
+  int64_t n;
+  void* v;
+  int64_t* s;
+  int64_t* e;
+  int64_t* p;
+  int32_t dtype2;
+  int32_t _pad;
+  int64_t n2;
+  void* v2;
+  int64_t* p2;
+} rq_host_column;
+
+/*
+ * Host-side mask image (column.hpp:111-131):
+ *   PLAIN     : n bytes in bits (total_size == n)
+ *   RLE       : n runs in s, e
+ *   INDEX     : n positions in p
+ *   COMPOSITE : runs n in s, e; points n2 in p2
+ */
+typedef struct rq_host_mask {
+  int32_t encoding;
+  int32_t _pad;
+  int64_t total_size;
+  int64_t n;
+  uint8_t* bits;
+  int64_t* s;
+  int64_t* e;
+  int64_t* p;
+  int64_t n2;
+  int64_t* p2;
+} rq_host_mask;
+
+/* ---------------------------------------------------------------------- */
+/* errors / context                                                         */
+/* ---------------------------------------------------------------------- */
+
+/* Message of the last failing call on this host thread ("" if none). */
+const char* rq_last_error(void);
+/* Build/version string: compile target, git-independent. */
+const char* rq_version(void);
+
+int rq_ctx_create(int device, rq_ctx_t* out);
+int rq_ctx_destroy(rq_ctx_t ctx);
+int rq_ctx_synchronize(rq_ctx_t ctx);
+/* The context's CUDA stream (cudaStream_t) for interop. */
+void* rq_ctx_stream(rq_ctx_t ctx);
+/* Kernel launches issued by this context so far (evidence counter). */
+int64_t rq_ctx_launches(rq_ctx_t ctx);
+
+/* ---------------------------------------------------------------------- */
+/* arrays (runq::Array, array.hpp:16-99; positions are RQ_I64 arrays)       */
+/* ---------------------------------------------------------------------- */
+
+int rq_arr_upload(rq_ctx_t ctx, int32_t dtype, const void* host, int64_t n, rq_arr_t* out);
+/* Wraps caller-owned device memory without copying; caller keeps it alive. */
+int rq_arr_wrap_device(rq_ctx_t ctx, int32_t dtype, void* dev, int64_t n, rq_arr_t* out);
+int rq_arr_info(rq_arr_t a, int32_t* dtype, int64_t* n);
+void* rq_arr_device_ptr(rq_arr_t a);
+int rq_arr_download(rq_ctx_t ctx, rq_arr_t a, void* host);
+int rq_arr_free(rq_arr_t a);
+
+/* ---------------------------------------------------------------------- */
+/* columns and masks                                                        */
+/* ---------------------------------------------------------------------- */
+
+int rq_col_upload(rq_ctx_t ctx, const rq_host_column* h, rq_col_t* out);
+int rq_col_describe(rq_col_t c, rq_host_column* h);
+int rq_col_download(rq_ctx_t ctx, rq_col_t c, rq_host_column* h);
+int rq_col_free(rq_col_t c);
+int rq_col_encoding(rq_col_t c);
+int64_t rq_col_total_size(rq_col_t c);
+/* runq::Column::value_type (column.cpp:88-97) */
+int rq_col_value_type(rq_col_t c);
+/* Builds columns from device arrays (shared, not copied). */
+int rq_col_make_rle(rq_ctx_t ctx, rq_arr_t v, rq_arr_t s, rq_arr_t e, int64_t total_size,
+                    rq_col_t* out);
+int rq_col_make_index(rq_ctx_t ctx, rq_arr_t v, rq_arr_t p, int64_t total_size, rq_col_t* out);
+int rq_col_make_plain(rq_ctx_t ctx, rq_arr_t values, int32_t logical, int32_t has_center,
+                      int64_t center, rq_col_t* out);
+/* Part arrays of a column: which = 0:v 1:s 2:e 3:p 4:v2 5:p2 (new handles). */
+int rq_col_part(rq_col_t c, int which, rq_arr_t* out);
+
+int rq_mask_upload(rq_ctx_t ctx, const rq_host_mask* h, rq_mask_t* out);
+int rq_mask_describe(rq_mask_t m, rq_host_mask* h);
+int rq_mask_download(rq_ctx_t ctx, rq_mask_t m, rq_host_mask* h);
+int rq_mask_free(rq_mask_t m);
+/* runq::MaskColumn::true_count (column.cpp:112-128); device reduction. */
+int rq_mask_true_count(rq_ctx_t ctx, rq_mask_t m, int64_t* out);
+
+/* ---------------------------------------------------------------------- */
+/* encoding primitives: runq::enc (primitives.hpp:28-92)                    */
+/* ---------------------------------------------------------------------- */
+
+/* enc::range_intersect (primitives.cpp:15-46): fragments s,e + idx1,idx2. */
+int rq_range_intersect(rq_ctx_t ctx, rq_arr_t s1, rq_arr_t e1, rq_arr_t s2, rq_arr_t e2,
+                       rq_arr_t* s, rq_arr_t* e, rq_arr_t* idx1, rq_arr_t* idx2);
+/* enc::idx_in_rle (primitives.cpp:48-61). */
+int rq_idx_in_rle(rq_ctx_t ctx, rq_arr_t p, rq_arr_t s, rq_arr_t e, rq_arr_t* p_out,
+                  rq_arr_t* run_of, rq_arr_t* idx_of);
+/* enc::rle_contain_idx (primitives.cpp:63-86); identical results. */
+int rq_rle_contain_idx(rq_ctx_t ctx, rq_arr_t p, rq_arr_t s, rq_arr_t e, rq_arr_t* p_out,
+                       rq_arr_t* run_of, rq_arr_t* idx_of);
+/* enc::idx_in_idx (primitives.cpp:88-100). */
+int rq_idx_in_idx(rq_ctx_t ctx, rq_arr_t p1, rq_arr_t p2, rq_arr_t* p_out, rq_arr_t* idx1,
+                  rq_arr_t* idx2);
+/* enc::plain_mask_to_rle / plain_mask_to_index (primitives.cpp:349-368). */
+int rq_plain_mask_to_rle(rq_ctx_t ctx, rq_mask_t plain, rq_mask_t* out);
+int rq_plain_mask_to_index(rq_ctx_t ctx, rq_mask_t plain, rq_mask_t* out);
+/* enc::compact_rle (primitives.cpp:370-379). */
+int rq_compact_rle(rq_ctx_t ctx, rq_col_t rle, rq_col_t* out);
+
+/* kernels::bucketize (kernels.cpp:10-19): searchsorted of x in boundaries. */
+int rq_bucketize(rq_ctx_t ctx, rq_arr_t x, rq_arr_t boundaries, int32_t right, rq_arr_t* out);
+
+/* ---------------------------------------------------------------------- */
+/* column model helpers (column.hpp:178-189, align.hpp:43-48)               */
+/* ---------------------------------------------------------------------- */
+
+/* decode_values (column.cpp:283-309): bit-width-reduced unpack to logical
+ * dtype (+center), Plain+Index overlay. Plain and Plain+Index only. */
+int rq_decode_values(rq_ctx_t ctx, rq_col_t c, rq_arr_t* out);
+/* compute::normalize_basic (align.cpp:102-115). */
+int rq_normalize_basic(rq_ctx_t ctx, rq_col_t c, rq_col_t* out);
+
+/* ---------------------------------------------------------------------- */
+/* align-compute: runq::compute (align.hpp:59-95)                           */
+/* ---------------------------------------------------------------------- */
+
+/* compute::align (align.cpp:219-231). shape_kind: 0 dense, 1 run, 2 point.
+ * Run shapes return s,e; point shapes return p; dense returns neither. */
+int rq_align(rq_ctx_t ctx, rq_col_t a, rq_col_t b, int32_t* shape_kind, rq_arr_t* s,
+             rq_arr_t* e, rq_arr_t* p, rq_arr_t* v1, rq_arr_t* v2);
+/* compute::arith (align.cpp:495-508). */
+int rq_arith(rq_ctx_t ctx, rq_col_t a, rq_col_t b, int32_t op, rq_col_t* out);
+/* compute::compare (align.cpp:510-523). */
+int rq_compare(rq_ctx_t ctx, rq_col_t a, rq_col_t b, int32_t op, rq_mask_t* out);
+/* compute::arith_scalar (align.cpp:571-596). */
+int rq_arith_scalar(rq_ctx_t ctx, rq_col_t a, rq_scalar k, int32_t op, int32_t reversed,
+                    rq_col_t* out);
+/* compute::compare_scalar (align.cpp:598-652): predicate -> RLE/Index/Plain/Composite mask. */
+int rq_compare_scalar(rq_ctx_t ctx, rq_col_t a, rq_scalar k, int32_t op, int32_t reversed,
+                      rq_mask_t* out);
+/* compute::filter (align.cpp:755-771). */
+int rq_filter(rq_ctx_t ctx, rq_col_t a, rq_mask_t m, rq_col_t* out);
+
+/* masks::and_mask (mask_ops.cpp:183-209). */
+int rq_mask_and(rq_ctx_t ctx, rq_mask_t a, rq_mask_t b, rq_mask_t* out);
+
+/* ---------------------------------------------------------------------- */
+/* aggregation: runq::agg (groupby.hpp:22-50)                               */
+/* ---------------------------------------------------------------------- */
+
+/* agg::aggregate_all (groupby.cpp:164-172). Result is one element of dtype
+ * *out_dtype (RQ_I64 or RQ_F64) written to *out_i64 or *out_f64. */
+int rq_aggregate_all(rq_ctx_t ctx, rq_col_t data, int32_t fn, int32_t* out_dtype,
+                     int64_t* out_i64, double* out_f64);
+
+/* agg::group_aggregate (groupby.cpp:144-162). keys[n_keys], data[n_data] with
+ * fns[n_data]. Outputs: n_groups, key arrays (device, ascending lexicographic)
+ * out_keys[n_keys] and aggregate arrays out_vals[n_data]. */
+int rq_group_aggregate(rq_ctx_t ctx, const rq_col_t* keys, int32_t n_keys, const rq_col_t* data,
+                       const int32_t* fns, int32_t n_data, int64_t* n_groups, rq_arr_t* out_keys,
+                       rq_arr_t* out_vals);
+
+/* ---------------------------------------------------------------------- */
+/* fused entry points (no reference counterpart: one kernel for an operator
+ * chain whose intermediate the reference materialises)                     */
+/* ---------------------------------------------------------------------- */
+
+/* aggregate_all(arith(a, b, op), fn) without materialising arith's output
+ * (align.cpp:495-508 + groupby.cpp:164-172). fn in {SUM, COUNT, AVG}. */
+int rq_aggregate_binop(rq_ctx_t ctx, rq_col_t a, rq_col_t b, int32_t op, int32_t fn,
+                       int32_t* out_dtype, int64_t* out_i64, double* out_f64);
+
+/* aggregate_all(arith(filter(a,m), filter(b,m), op), fn) with
+ * m = compare_scalar(c, k, cmp) — the filtered-aggregate query shape of
+ * runner.cpp:243-336 — in one pass over the compressed inputs. */
+int rq_filtered_aggregate_binop(rq_ctx_t ctx, rq_col_t c, rq_scalar k, int32_t cmp,
+                                rq_col_t a, rq_col_t b, int32_t op, int32_t fn,
+                                int32_t* out_dtype, int64_t* out_i64, double* out_f64);
+
+/* ---------------------------------------------------------------------- */
+/* row-range sharding (multi-GPU; no reference counterpart)                 */
+/* ---------------------------------------------------------------------- */
+
+/* Slices a host column image to rows [lo, hi) as a standalone shard: runs
+ * crossing a cut are split with their value duplicated, positions are
+ * rebased to the shard (p - lo) and total_size = hi - lo. Pure host function
+ * (no device work); output arrays are allocated with malloc and released
+ * with rq_host_column_free. */
+int rq_shard_host_column(const rq_host_column* in, int64_t lo, int64_t hi, rq_host_column* out);
+void rq_host_column_free(rq_host_column* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RUNQ_B200_H */

@@ -1,0 +1,295 @@
+/*
+ * runq_oracle.c — TEST INFRASTRUCTURE ONLY: plain-C restatement of the
+ * reference's hot-path algorithms. See runq_oracle.h for the contract and
+ * how this restatement is pinned (golden vectors + live reference library).
+ * Never linked into or called by the product path.
+ */
+#include "runq_oracle.h"
+
+#include <stddef.h>
+#include <string.h>
+
+/* runq::DType codes (dtype.hpp:11) */
+enum { I8 = 0, I16 = 1, I32 = 2, I64 = 3, F32 = 4, F64 = 5 };
+/* runq::compute::BinOp codes (align.hpp:70) */
+enum { ADD = 0, SUB = 1, MUL = 2, DIV = 3, LT = 4, LE = 5, EQ = 6, NE = 7, GE = 8, GT = 9 };
+
+static int64_t lower_bound(const int64_t* b, int64_t nb, int64_t x) {
+  int64_t lo = 0, hi = nb;
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (b[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+static int64_t upper_bound(const int64_t* b, int64_t nb, int64_t x) {
+  int64_t lo = 0, hi = nb;
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (b[mid] <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+/* kernels.cpp:10-19 */
+void orq_bucketize(const int64_t* x, int64_t nx, const int64_t* b, int64_t nb, int right,
+                   int64_t* out) {
+  for (int64_t i = 0; i < nx; ++i)
+    out[i] = right ? upper_bound(b, nb, x[i]) : lower_bound(b, nb, x[i]);
+}
+
+/* primitives.cpp:15-46: the list with fewer runs drives; for driver run i,
+ * the overlapping runs of the other list are [lower_bound(e_other, s_i),
+ * upper_bound(s_other, e_i)); fragments in driver order then other order;
+ * idx outputs reported per argument. */
+int64_t orq_range_intersect(const int64_t* s1, const int64_t* e1, int64_t n1, const int64_t* s2,
+                            const int64_t* e2, int64_t n2, int64_t* s, int64_t* e, int64_t* idx1,
+                            int64_t* idx2) {
+  int swapped = n1 > n2;
+  const int64_t *ds = s1, *de = e1, *os = s2, *oe = e2;
+  int64_t dn = n1, on = n2;
+  if (swapped) {
+    ds = s2; de = e2; dn = n2;
+    os = s1; oe = e1; on = n1;
+  }
+  int64_t k = 0;
+  for (int64_t i = 0; i < dn; ++i) {
+    int64_t jb = lower_bound(oe, on, ds[i]);
+    int64_t je = upper_bound(os, on, de[i]);
+    for (int64_t j = jb; j < je; ++j) {
+      s[k] = ds[i] > os[j] ? ds[i] : os[j];
+      e[k] = de[i] < oe[j] ? de[i] : oe[j];
+      idx1[k] = swapped ? j : i;
+      idx2[k] = swapped ? i : j;
+      ++k;
+    }
+  }
+  return k;
+}
+
+/* primitives.cpp:48-61: bin = upper_bound(s, p) - 1, keep if p <= e[bin]. */
+int64_t orq_idx_in_rle(const int64_t* p, int64_t np, const int64_t* s, const int64_t* e,
+                       int64_t nr, int64_t* p_out, int64_t* run_of, int64_t* idx_of) {
+  int64_t k = 0;
+  for (int64_t i = 0; i < np; ++i) {
+    int64_t b = upper_bound(s, nr, p[i]) - 1;
+    if (b >= 0 && p[i] <= e[b]) {
+      p_out[k] = p[i];
+      run_of[k] = b;
+      idx_of[k] = i;
+      ++k;
+    }
+  }
+  return k;
+}
+
+/* primitives.cpp:63-86: per run, the covered position-index range is
+ * [lower_bound(p, s_r), upper_bound(p, e_r) - 1]; expand in run order. */
+int64_t orq_rle_contain_idx(const int64_t* p, int64_t np, const int64_t* s, const int64_t* e,
+                            int64_t nr, int64_t* p_out, int64_t* run_of, int64_t* idx_of) {
+  int64_t k = 0;
+  for (int64_t r = 0; r < nr; ++r) {
+    int64_t lo = lower_bound(p, np, s[r]);
+    int64_t hi = upper_bound(p, np, e[r]) - 1;
+    for (int64_t q = lo; q <= hi; ++q) {
+      p_out[k] = p[q];
+      run_of[k] = r;
+      idx_of[k] = q;
+      ++k;
+    }
+  }
+  return k;
+}
+
+/* primitives.cpp:88-100: bin = upper_bound(p2, p1[i]) - 1, keep on equality. */
+int64_t orq_idx_in_idx(const int64_t* p1, int64_t n1, const int64_t* p2, int64_t n2,
+                       int64_t* p_out, int64_t* idx1, int64_t* idx2) {
+  int64_t k = 0;
+  for (int64_t i = 0; i < n1; ++i) {
+    int64_t b = upper_bound(p2, n2, p1[i]) - 1;
+    if (b >= 0 && p1[i] == p2[b]) {
+      p_out[k] = p1[i];
+      idx1[k] = i;
+      idx2[k] = b;
+      ++k;
+    }
+  }
+  return k;
+}
+
+/* primitives.cpp:349-360 */
+int64_t orq_plain_mask_to_rle(const uint8_t* bits, int64_t n, int64_t* s, int64_t* e) {
+  int64_t k = 0;
+  int prev = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int bit = bits[i] != 0;
+    if (bit && !prev) s[k] = i;
+    if (!bit && prev) e[k++] = i - 1;
+    prev = bit;
+  }
+  if (prev) e[k++] = n - 1;
+  return k;
+}
+
+/* primitives.cpp:362-368 */
+int64_t orq_plain_mask_to_index(const uint8_t* bits, int64_t n, int64_t* p) {
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (bits[i]) p[k++] = i;
+  return k;
+}
+
+/* primitives.cpp:370-379: s' = exclusive cumsum of lengths, e' = s' + l - 1. */
+int64_t orq_compact_rle(const int64_t* s, const int64_t* e, int64_t nr, int64_t* s_out,
+                        int64_t* e_out) {
+  int64_t at = 0;
+  for (int64_t i = 0; i < nr; ++i) {
+    int64_t l = e[i] - s[i] + 1;
+    s_out[i] = at;
+    e_out[i] = at + l - 1;
+    at += l;
+  }
+  return at;
+}
+
+static int64_t load_int(int dtype, const void* v, int64_t i) {
+  switch (dtype) {
+    case I8: return ((const int8_t*)v)[i];
+    case I16: return ((const int16_t*)v)[i];
+    case I32: return ((const int32_t*)v)[i];
+    default: return ((const int64_t*)v)[i];
+  }
+}
+
+static int64_t wrap_to(int dtype, int64_t x) {
+  switch (dtype) {
+    case I8: return (int8_t)(uint8_t)x;
+    case I16: return (int16_t)(uint16_t)x;
+    case I32: return (int32_t)(uint32_t)x;
+    default: return x;
+  }
+}
+
+/* column.cpp:283-297: cast storage to the logical type, then
+ * x = T(x + center) at the logical width. */
+void orq_decode_plain_int(int dtype, const void* values, int64_t n, int logical,
+                          int has_center, int64_t center, int64_t* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t x = wrap_to(logical, load_int(dtype, values, i));
+    if (has_center) x = wrap_to(logical, (int64_t)((uint64_t)x + (uint64_t)center));
+    out[i] = x;
+  }
+}
+
+static int cmp_i64(int64_t x, int op, int64_t y) {
+  switch (op) {
+    case LT: return x < y;
+    case LE: return x <= y;
+    case EQ: return x == y;
+    case NE: return x != y;
+    case GE: return x >= y;
+    default: return x > y;
+  }
+}
+
+static uint64_t arith_u64(int64_t x, int op, int64_t y) {
+  switch (op) {
+    case ADD: return (uint64_t)x + (uint64_t)y;
+    case SUB: return (uint64_t)x - (uint64_t)y;
+    default: return (uint64_t)x * (uint64_t)y;
+  }
+}
+
+/* align.cpp compare_scalar, `case Encoding::Rle`: per-run flag, keep the
+ * passing runs' s/e unmerged. */
+int64_t orq_rle_compare_scalar_i64(const int64_t* v, const int64_t* s, const int64_t* e,
+                                   int64_t nr, int op, int64_t k, int64_t* s_out,
+                                   int64_t* e_out) {
+  int64_t m = 0;
+  for (int64_t i = 0; i < nr; ++i) {
+    if (cmp_i64(v[i], op, k)) {
+      s_out[m] = s[i];
+      e_out[m] = e[i];
+      ++m;
+    }
+  }
+  return m;
+}
+
+/* Fragments of the RLE x RLE positional intersection enumerated by a
+ * two-pointer walk (same set and order as primitives.cpp:15-46), each
+ * contributing (va op vb) * len to the int64 SUM (groupby.cpp:82-89). */
+int64_t orq_sum_rle_binop_i64(const int64_t* va, const int64_t* sa, const int64_t* ea,
+                              int64_t ra, const int64_t* vb, const int64_t* sb, const int64_t* eb,
+                              int64_t rb, int op) {
+  uint64_t acc = 0;
+  int64_t i = 0, j = 0;
+  while (i < ra && j < rb) {
+    int64_t lo = sa[i] > sb[j] ? sa[i] : sb[j];
+    int64_t hi = ea[i] < eb[j] ? ea[i] : eb[j];
+    if (lo <= hi) acc += arith_u64(va[i], op, vb[j]) * (uint64_t)(hi - lo + 1);
+    if (ea[i] < eb[j]) ++i;
+    else if (eb[j] < ea[i]) ++j;
+    else { ++i; ++j; }
+  }
+  return (int64_t)acc;
+}
+
+/* Advances *r to the first run whose end is >= pos; returns the run index
+ * if it contains pos, else -1. */
+static int64_t run_at(const int64_t* s, const int64_t* e, int64_t nr, int64_t* r, int64_t pos) {
+  while (*r < nr && e[*r] < pos) ++*r;
+  if (*r < nr && s[*r] <= pos) return *r;
+  return -1;
+}
+
+int64_t orq_filtered_sum_rle_idx_rle(const int64_t* cv, const int64_t* cs, const int64_t* ce,
+                                     int64_t rc, int cmp, int64_t k, const int64_t* av,
+                                     const int64_t* as, const int64_t* ae, int64_t ra,
+                                     const int64_t* bv, const int64_t* bp, int64_t nb, int op) {
+  uint64_t acc = 0;
+  int64_t ic = 0, ia = 0;
+  for (int64_t q = 0; q < nb; ++q) {
+    int64_t pos = bp[q];
+    int64_t rcix = run_at(cs, ce, rc, &ic, pos);
+    if (rcix < 0 || !cmp_i64(cv[rcix], cmp, k)) continue;
+    int64_t raix = run_at(as, ae, ra, &ia, pos);
+    if (raix < 0) continue;
+    acc += arith_u64(av[raix], op, bv[q]);
+  }
+  return (int64_t)acc;
+}
+
+int64_t orq_filtered_sum_plain_idx_rle(int c_dtype, const void* c_values, int64_t n, int c_logical,
+                                       int c_has_center, int64_t c_center, int cmp, int64_t k,
+                                       const int64_t* av, const int64_t* as, const int64_t* ae,
+                                       int64_t ra, const int64_t* bv, const int64_t* bp,
+                                       int64_t nb, int op) {
+  uint64_t acc = 0;
+  int64_t ia = 0;
+  for (int64_t q = 0; q < nb; ++q) {
+    int64_t pos = bp[q];
+    if (pos < 0 || pos >= n) continue;
+    int64_t c = wrap_to(c_logical, load_int(c_dtype, c_values, pos));
+    if (c_has_center) c = wrap_to(c_logical, (int64_t)((uint64_t)c + (uint64_t)c_center));
+    if (!cmp_i64(c, cmp, k)) continue;
+    int64_t raix = run_at(as, ae, ra, &ia, pos);
+    if (raix < 0) continue;
+    acc += arith_u64(av[raix], op, bv[q]);
+  }
+  return (int64_t)acc;
+}
+
+double orq_sum_f64(const double* x, int64_t n) {
+  double sum = 0.0, comp = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double t = sum + x[i];
+    if ((sum >= 0 ? sum : -sum) >= (x[i] >= 0 ? x[i] : -x[i])) comp += (sum - t) + x[i];
+    else comp += (x[i] - t) + sum;
+    sum = t;
+  }
+  return sum + comp;
+}

@@ -1,0 +1,129 @@
+"""Loader and ctypes prototypes for the in-tree C ABI library.
+
+``librunq_b200.so`` is built in-tree by ``__graft_entry__.build()``
+(``paper_2506_10092_b200/csrc/Makefile``). There is no fallback: if the
+library is missing or a symbol is absent, importing the device API raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .host import HostColumn, HostMask, Scalar
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librunq_b200.so")
+
+_lib = None
+
+vp = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+P = C.POINTER
+
+# name -> (restype, argtypes). Mirrors include/runq_b200.h one to one.
+PROTOTYPES = {
+    "rq_last_error": (C.c_char_p, []),
+    "rq_version": (C.c_char_p, []),
+    "rq_ctx_create": (C.c_int, [C.c_int, P(vp)]),
+    "rq_ctx_destroy": (C.c_int, [vp]),
+    "rq_ctx_synchronize": (C.c_int, [vp]),
+    "rq_ctx_stream": (vp, [vp]),
+    "rq_ctx_launches": (i64, [vp]),
+    "rq_arr_upload": (C.c_int, [vp, i32, vp, i64, P(vp)]),
+    "rq_arr_wrap_device": (C.c_int, [vp, i32, vp, i64, P(vp)]),
+    "rq_arr_info": (C.c_int, [vp, P(i32), P(i64)]),
+    "rq_arr_device_ptr": (vp, [vp]),
+    "rq_arr_download": (C.c_int, [vp, vp, vp]),
+    "rq_arr_free": (C.c_int, [vp]),
+    "rq_col_upload": (C.c_int, [vp, P(HostColumn), P(vp)]),
+    "rq_col_describe": (C.c_int, [vp, P(HostColumn)]),
+    "rq_col_download": (C.c_int, [vp, vp, P(HostColumn)]),
+    "rq_col_free": (C.c_int, [vp]),
+    "rq_col_encoding": (C.c_int, [vp]),
+    "rq_col_total_size": (i64, [vp]),
+    "rq_col_value_type": (C.c_int, [vp]),
+    "rq_col_make_rle": (C.c_int, [vp, vp, vp, vp, i64, P(vp)]),
+    "rq_col_make_index": (C.c_int, [vp, vp, vp, i64, P(vp)]),
+    "rq_col_make_plain": (C.c_int, [vp, vp, i32, i32, i64, P(vp)]),
+    "rq_col_part": (C.c_int, [vp, C.c_int, P(vp)]),
+    "rq_mask_upload": (C.c_int, [vp, P(HostMask), P(vp)]),
+    "rq_mask_describe": (C.c_int, [vp, P(HostMask)]),
+    "rq_mask_download": (C.c_int, [vp, vp, P(HostMask)]),
+    "rq_mask_free": (C.c_int, [vp]),
+    "rq_mask_true_count": (C.c_int, [vp, vp, P(i64)]),
+    "rq_range_intersect": (C.c_int, [vp, vp, vp, vp, vp, P(vp), P(vp), P(vp), P(vp)]),
+    "rq_idx_in_rle": (C.c_int, [vp, vp, vp, vp, P(vp), P(vp), P(vp)]),
+    "rq_rle_contain_idx": (C.c_int, [vp, vp, vp, vp, P(vp), P(vp), P(vp)]),
+    "rq_idx_in_idx": (C.c_int, [vp, vp, vp, P(vp), P(vp), P(vp)]),
+    "rq_plain_mask_to_rle": (C.c_int, [vp, vp, P(vp)]),
+    "rq_plain_mask_to_index": (C.c_int, [vp, vp, P(vp)]),
+    "rq_compact_rle": (C.c_int, [vp, vp, P(vp)]),
+    "rq_bucketize": (C.c_int, [vp, vp, vp, i32, P(vp)]),
+    "rq_decode_values": (C.c_int, [vp, vp, P(vp)]),
+    "rq_normalize_basic": (C.c_int, [vp, vp, P(vp)]),
+    "rq_align": (C.c_int, [vp, vp, vp, P(i32), P(vp), P(vp), P(vp), P(vp), P(vp)]),
+    "rq_arith": (C.c_int, [vp, vp, vp, i32, P(vp)]),
+    "rq_compare": (C.c_int, [vp, vp, vp, i32, P(vp)]),
+    "rq_arith_scalar": (C.c_int, [vp, vp, Scalar, i32, i32, P(vp)]),
+    "rq_compare_scalar": (C.c_int, [vp, vp, Scalar, i32, i32, P(vp)]),
+    "rq_filter": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_mask_and": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_aggregate_all": (C.c_int, [vp, vp, i32, P(i32), P(i64), P(C.c_double)]),
+    "rq_group_aggregate": (C.c_int, [vp, P(vp), i32, P(vp), P(i32), i32, P(i64), P(vp), P(vp)]),
+    "rq_aggregate_binop": (C.c_int, [vp, vp, vp, i32, i32, P(i32), P(i64), P(C.c_double)]),
+    "rq_filtered_aggregate_binop": (C.c_int, [vp, vp, Scalar, i32, vp, vp, i32, i32, P(i32), P(i64),
+                                              P(C.c_double)]),
+    "rq_shard_host_column": (C.c_int, [P(HostColumn), i64, i64, P(HostColumn)]),
+    "rq_host_column_free": (None, [P(HostColumn)]),
+}
+
+
+class RqError(RuntimeError):
+    """runq::Error (error.hpp:11-14)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class RqOverflowError(RqError):
+    """runq::OverflowError (error.hpp:17-20)."""
+
+
+class RqResourceError(RqError):
+    """runq::ResourceError (error.hpp:23-26)."""
+
+
+class RqDeviceError(RqError):
+    """CUDA / NCCL failure."""
+
+
+def load():
+    """Loads the library (once). Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: the CUDA extension is not built (run __graft_entry__.build()); "
+            "there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in PROTOTYPES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status == 0:
+        return
+    msg = load().rq_last_error().decode(errors="replace")
+    if status == 2:
+        raise RqOverflowError(status, msg)
+    if status == 3:
+        raise RqResourceError(status, msg)
+    if status in (4, 5):
+        raise RqDeviceError(status, msg)
+    raise RqError(status, msg)

@@ -1,0 +1,390 @@
+// capi_ops.cpp — operator half of the C ABI (include/runq_b200.h).
+#include <cstdlib>
+#include <cstring>
+
+#include "rq_internal.hpp"
+
+using namespace rqb;
+
+namespace {
+
+CtxPtr ctx_of(rq_ctx_t c) {
+  if (!c || !c->ctx) fail("null context");
+  RQ_CUDA_CHECK(cudaSetDevice(c->ctx->device));
+  return c->ctx;
+}
+const DArr& arr_of(rq_arr_t a) {
+  if (!a) fail("null array handle");
+  return a->a;
+}
+const DCol& col_of(rq_col_t c) {
+  if (!c) fail("null column handle");
+  return c->c;
+}
+const DMask& mask_of(rq_mask_t m) {
+  if (!m) fail("null mask handle");
+  return m->m;
+}
+Scalar scal(rq_scalar k) {
+  Scalar s;
+  s.is_float = k.is_float != 0;
+  s.i = k.i;
+  s.f = k.f;
+  return s;
+}
+void put(rq_arr_t* out, const DArr& a) {
+  if (out) *out = wrap_arr(a);
+}
+void put_agg(const AggOut& r, int32_t* out_dtype, int64_t* out_i64, double* out_f64) {
+  if (out_dtype) *out_dtype = r.dtype;
+  if (out_i64) *out_i64 = r.i;
+  if (out_f64) *out_f64 = r.f;
+}
+void require_pos(const DArr& a, const char* what) {
+  if (a.dt != RQ_I64) fail(std::string(what) + ": positions must be i64");
+}
+
+}  // namespace
+
+extern "C" {
+
+int rq_range_intersect(rq_ctx_t c, rq_arr_t s1, rq_arr_t e1, rq_arr_t s2, rq_arr_t e2,
+                       rq_arr_t* s, rq_arr_t* e, rq_arr_t* idx1, rq_arr_t* idx2) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    Intersection r = range_intersect(ctx, arr_of(s1), arr_of(e1), arr_of(s2), arr_of(e2),
+                                     idx1 != nullptr, idx2 != nullptr);
+    put(s, r.s);
+    put(e, r.e);
+    put(idx1, r.idx1);
+    put(idx2, r.idx2);
+  });
+}
+
+int rq_idx_in_rle(rq_ctx_t c, rq_arr_t p, rq_arr_t s, rq_arr_t e, rq_arr_t* p_out,
+                  rq_arr_t* run_of, rq_arr_t* idx_of) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require_pos(arr_of(p), "idx_in_rle");
+    PointsInRuns r = points_in_runs(ctx, arr_of(p), arr_of(s), arr_of(e), run_of != nullptr,
+                                    idx_of != nullptr);
+    put(p_out, r.p_out);
+    put(run_of, r.run_of);
+    put(idx_of, r.idx_of);
+  });
+}
+
+int rq_rle_contain_idx(rq_ctx_t c, rq_arr_t p, rq_arr_t s, rq_arr_t e, rq_arr_t* p_out,
+                       rq_arr_t* run_of, rq_arr_t* idx_of) {
+  // primitives.hpp:43-46: same result set as idx_in_rle; one device kernel
+  return rq_idx_in_rle(c, p, s, e, p_out, run_of, idx_of);
+}
+
+int rq_idx_in_idx(rq_ctx_t c, rq_arr_t p1, rq_arr_t p2, rq_arr_t* p_out, rq_arr_t* idx1,
+                  rq_arr_t* idx2) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require_pos(arr_of(p1), "idx_in_idx");
+    require_pos(arr_of(p2), "idx_in_idx");
+    PointsIntersect r = points_intersect(ctx, arr_of(p1), arr_of(p2), idx1 != nullptr,
+                                         idx2 != nullptr);
+    put(p_out, r.p_out);
+    put(idx1, r.idx1);
+    put(idx2, r.idx2);
+  });
+}
+
+int rq_plain_mask_to_rle(rq_ctx_t c, rq_mask_t plain, rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    const DMask& m = mask_of(plain);
+    require(m.enc == RQ_MASK_PLAIN, "plain_mask_to_rle: plain mask required");
+    DMask r;
+    r.enc = RQ_MASK_RLE;
+    r.total = m.bits.n;
+    plain_mask_to_rle(ctx, m.bits, r.s, r.e);
+    *out = wrap_mask(std::move(r));
+  });
+}
+
+int rq_plain_mask_to_index(rq_ctx_t c, rq_mask_t plain, rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    const DMask& m = mask_of(plain);
+    require(m.enc == RQ_MASK_PLAIN, "plain_mask_to_index: plain mask required");
+    DMask r;
+    r.enc = RQ_MASK_INDEX;
+    r.total = m.bits.n;
+    r.p = plain_mask_to_index(ctx, m.bits);
+    *out = wrap_mask(std::move(r));
+  });
+}
+
+int rq_compact_rle(rq_ctx_t c, rq_col_t rle, rq_col_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    const DCol& in = col_of(rle);
+    require(in.enc == RQ_ENC_RLE, "compact_rle: rle column required");
+    DCol r;
+    r.enc = RQ_ENC_RLE;
+    r.v = in.v;
+    r.logical = in.v.dt;
+    int64_t covered = 0;
+    r.s = compact_positions(ctx, in.s, in.e, r.e, &covered);
+    r.total = covered;
+    *out = wrap_col(std::move(r));
+  });
+}
+
+int rq_bucketize(rq_ctx_t c, rq_arr_t x, rq_arr_t boundaries, int32_t right, rq_arr_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    put(out, bucketize(ctx, arr_of(x), arr_of(boundaries), right != 0));
+  });
+}
+
+int rq_decode_values(rq_ctx_t c, rq_col_t col, rq_arr_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    const DCol& in = col_of(col);
+    if (in.enc == RQ_ENC_PLAIN) put(out, decode_plain(ctx, in));
+    else if (in.enc == RQ_ENC_PLAIN_INDEX) put(out, decode_plain_index(ctx, in));
+    else fail("decode_values: plain or plain+index only");
+  });
+}
+
+int rq_normalize_basic(rq_ctx_t c, rq_col_t col, rq_col_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_col(normalize_basic(ctx, col_of(col)));
+  });
+}
+
+int rq_align(rq_ctx_t c, rq_col_t a, rq_col_t b, int32_t* shape_kind, rq_arr_t* s, rq_arr_t* e,
+             rq_arr_t* p, rq_arr_t* v1, rq_arr_t* v2) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    Aligned r = align(ctx, col_of(a), col_of(b));
+    if (shape_kind) *shape_kind = r.kind;
+    if (r.kind == 1) {
+      put(s, r.s);
+      put(e, r.e);
+    } else if (r.kind == 2) {
+      put(p, r.p);
+    }
+    put(v1, r.v1);
+    put(v2, r.v2);
+  });
+}
+
+int rq_arith(rq_ctx_t c, rq_col_t a, rq_col_t b, int32_t op, rq_col_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_col(arith(ctx, col_of(a), col_of(b), op));
+  });
+}
+
+int rq_compare(rq_ctx_t c, rq_col_t a, rq_col_t b, int32_t op, rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_mask(compare(ctx, col_of(a), col_of(b), op));
+  });
+}
+
+int rq_arith_scalar(rq_ctx_t c, rq_col_t a, rq_scalar k, int32_t op, int32_t reversed,
+                    rq_col_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_col(arith_scalar(ctx, col_of(a), scal(k), op, reversed != 0));
+  });
+}
+
+int rq_compare_scalar(rq_ctx_t c, rq_col_t a, rq_scalar k, int32_t op, int32_t reversed,
+                      rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_mask(compare_scalar(ctx, col_of(a), scal(k), op, reversed != 0));
+  });
+}
+
+int rq_filter(rq_ctx_t c, rq_col_t a, rq_mask_t m, rq_col_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_col(filter(ctx, col_of(a), mask_of(m)));
+  });
+}
+
+int rq_mask_and(rq_ctx_t c, rq_mask_t a, rq_mask_t b, rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_mask(mask_and(ctx, mask_of(a), mask_of(b)));
+  });
+}
+
+int rq_aggregate_all(rq_ctx_t c, rq_col_t data, int32_t fn, int32_t* out_dtype, int64_t* out_i64,
+                     double* out_f64) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    put_agg(aggregate_column(ctx, col_of(data), fn), out_dtype, out_i64, out_f64);
+  });
+}
+
+int rq_group_aggregate(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys, const rq_col_t* data,
+                       const int32_t* fns, int32_t n_data, int64_t* n_groups, rq_arr_t* out_keys,
+                       rq_arr_t* out_vals) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require(n_keys > 0, "group: empty key list");
+    std::vector<const DCol*> k, d;
+    std::vector<int> f;
+    for (int i = 0; i < n_keys; ++i) k.push_back(&col_of(keys[i]));
+    for (int i = 0; i < n_data; ++i) {
+      d.push_back(&col_of(data[i]));
+      f.push_back(fns[i]);
+    }
+    GroupAggOut r = group_aggregate(ctx, k, d, f);
+    if (n_groups) *n_groups = r.n_groups;
+    for (int i = 0; i < n_keys; ++i) out_keys[i] = wrap_arr(r.keys[static_cast<size_t>(i)]);
+    for (int i = 0; i < n_data; ++i) out_vals[i] = wrap_arr(r.vals[static_cast<size_t>(i)]);
+  });
+}
+
+int rq_aggregate_binop(rq_ctx_t c, rq_col_t a, rq_col_t b, int32_t op, int32_t fn,
+                       int32_t* out_dtype, int64_t* out_i64, double* out_f64) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    put_agg(aggregate_binop(ctx, col_of(a), col_of(b), op, fn), out_dtype, out_i64, out_f64);
+  });
+}
+
+int rq_filtered_aggregate_binop(rq_ctx_t c, rq_col_t pred, rq_scalar k, int32_t cmp, rq_col_t a,
+                                rq_col_t b, int32_t op, int32_t fn, int32_t* out_dtype,
+                                int64_t* out_i64, double* out_f64) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    put_agg(filtered_aggregate_binop(ctx, col_of(pred), scal(k), cmp, col_of(a), col_of(b), op, fn),
+            out_dtype, out_i64, out_f64);
+  });
+}
+
+// ---- host-side row-range sharding -------------------------------------------------
+
+namespace {
+
+void* dup_slice(const void* src, int64_t first, int64_t count, int width) {
+  const size_t bytes = static_cast<size_t>(count > 0 ? count : 0) * width;
+  void* p = std::malloc(bytes ? bytes : 1);
+  if (bytes) std::memcpy(p, static_cast<const char*>(src) + first * width, bytes);
+  return p;
+}
+
+int64_t lower_bound_h(const int64_t* a, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) / 2;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// RLE runs clipped to [lo, hi): first run with e >= lo .. last run with s < hi
+void slice_runs(const void* v, int width, const int64_t* s, const int64_t* e, int64_t n, int64_t lo,
+                int64_t hi, void** v_out, int64_t** s_out, int64_t** e_out, int64_t* n_out) {
+  const int64_t r0 = lower_bound_h(e, n, lo);
+  const int64_t r1 = lower_bound_h(s, n, hi);  // first run starting at/after hi
+  const int64_t cnt = r1 > r0 ? r1 - r0 : 0;
+  *v_out = dup_slice(v, r0, cnt, width);
+  *s_out = static_cast<int64_t*>(dup_slice(s, r0, cnt, 8));
+  *e_out = static_cast<int64_t*>(dup_slice(e, r0, cnt, 8));
+  if (cnt > 0) {
+    if ((*s_out)[0] < lo) (*s_out)[0] = lo;            // split run crossing the low cut
+    if ((*e_out)[cnt - 1] > hi - 1) (*e_out)[cnt - 1] = hi - 1;  // and the high cut
+  }
+  *n_out = cnt;
+}
+
+void slice_points(const void* v, int width, const int64_t* p, int64_t n, int64_t lo, int64_t hi,
+                  void** v_out, int64_t** p_out, int64_t* n_out) {
+  const int64_t a = lower_bound_h(p, n, lo);
+  const int64_t b = lower_bound_h(p, n, hi);
+  const int64_t cnt = b > a ? b - a : 0;
+  *v_out = dup_slice(v, a, cnt, width);
+  *p_out = static_cast<int64_t*>(dup_slice(p, a, cnt, 8));
+  *n_out = cnt;
+}
+
+}  // namespace
+
+// Row-range shard of a host column image: rows [lo, hi) of
+// the table become a standalone table of hi - lo rows. Runs crossing a cut
+// are split with their value duplicated; every position is rebased to the
+// shard (p - lo) and total_size = hi - lo, so all columns of a shard align
+// with each other, shard aggregates combine into the global aggregate, and
+// materialised shard outputs concatenate (after adding lo) into the global
+// result in shard order.
+int rq_shard_host_column(const rq_host_column* in, int64_t lo, int64_t hi, rq_host_column* out) {
+  return api_guard([&] {
+    require(in && out, "null argument");
+    require(0 <= lo && lo <= hi, "shard: bad row range");
+    std::memset(out, 0, sizeof(*out));
+    *out = *in;
+    out->v = out->v2 = nullptr;
+    out->s = out->e = out->p = out->p2 = nullptr;
+    out->total_size = hi - lo;
+    const int w = dt_width(in->dtype);
+    auto rebase = [&](int64_t* a, int64_t n) {
+      for (int64_t i = 0; i < n; ++i) a[i] -= lo;
+    };
+    switch (in->encoding) {
+      case RQ_ENC_PLAIN:
+      case RQ_ENC_PLAIN_INDEX: {
+        require(hi <= in->n, "shard: range beyond plain column");
+        out->n = hi - lo;
+        out->v = dup_slice(in->v, lo, hi - lo, w);
+        if (in->encoding == RQ_ENC_PLAIN_INDEX) {
+          slice_points(in->v2, dt_width(in->dtype2), in->p2, in->n2, lo, hi, &out->v2, &out->p2,
+                       &out->n2);
+          rebase(out->p2, out->n2);
+        }
+        break;
+      }
+      case RQ_ENC_RLE:
+        require(hi <= in->total_size, "shard: range beyond column");
+        slice_runs(in->v, w, in->s, in->e, in->n, lo, hi, &out->v, &out->s, &out->e, &out->n);
+        rebase(out->s, out->n);
+        rebase(out->e, out->n);
+        break;
+      case RQ_ENC_INDEX:
+        require(hi <= in->total_size, "shard: range beyond column");
+        slice_points(in->v, w, in->p, in->n, lo, hi, &out->v, &out->p, &out->n);
+        rebase(out->p, out->n);
+        break;
+      case RQ_ENC_RLE_INDEX:
+        require(hi <= in->total_size, "shard: range beyond column");
+        slice_runs(in->v, w, in->s, in->e, in->n, lo, hi, &out->v, &out->s, &out->e, &out->n);
+        rebase(out->s, out->n);
+        rebase(out->e, out->n);
+        slice_points(in->v2, dt_width(in->dtype2), in->p2, in->n2, lo, hi, &out->v2, &out->p2,
+                     &out->n2);
+        rebase(out->p2, out->n2);
+        break;
+      default:
+        fail("shard: unknown encoding");
+    }
+  });
+}
+
+void rq_host_column_free(rq_host_column* h) {
+  if (!h) return;
+  std::free(h->v);
+  std::free(h->s);
+  std::free(h->e);
+  std::free(h->p);
+  std::free(h->v2);
+  std::free(h->p2);
+  h->v = h->v2 = nullptr;
+  h->s = h->e = h->p = h->p2 = nullptr;
+}
+
+}  // extern "C"

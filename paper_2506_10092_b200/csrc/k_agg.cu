@@ -1,0 +1,460 @@
+// k_agg.cu — run-length-weighted aggregation (K2/K5 reductions).
+//
+// agg::aggregate_array (groupby.cpp:67-135) multiplies each slot's value by
+// its weight (run length for run shapes, 1 otherwise) and scatter-reduces.
+// Here the weight is computed inline from (s, e) and the product is folded
+// into per-thread accumulators; each CTA writes one partial record and a
+// single-CTA pass combines the partials in a fixed order (deterministic f64).
+// The fused RLE×RLE kernel (K2) runs the merge-path walk of range_intersect
+// and folds (va op vb)·len per fragment without materialising fragments —
+// the whole compute::arith → agg::aggregate_all chain (align.cpp:495-508,
+// groupby.cpp:164-172) in one pass over the compressed bytes.
+#include <cmath>
+#include <limits>
+
+#include "merge_walk.cuh"
+#include "rq_internal.hpp"
+
+namespace rqb {
+namespace dev {
+
+struct AggPart {
+  unsigned long long isum;  // Σ int64(v)·w, wrapping
+  double fsum;              // Σ f64(v)·f64(w)  (pass 2: Σ (v-mean)²·w)
+  long long cnt;            // Σ w
+  long long imin, imax;
+  double fmin, fmax;
+  double pad;
+};
+
+struct Acc {
+  uint64_t isum = 0;
+  double fsum = 0.0;
+  int64_t cnt = 0;
+  int64_t imin = INT64_MAX, imax = INT64_MIN;
+  double fmin = INFINITY, fmax = -INFINITY;
+
+  template <class T>
+  __device__ __forceinline__ void add(T x, int64_t w, bool pass2, double mean) {
+    if (pass2) {
+      const double d = static_cast<double>(x) - mean;
+      fsum += d * d * static_cast<double>(w);
+      return;
+    }
+    isum += static_cast<uint64_t>(static_cast<int64_t>(x)) * static_cast<uint64_t>(w);
+    fsum += static_cast<double>(x) * static_cast<double>(w);
+    cnt += w;
+    const int64_t xi = static_cast<int64_t>(x);
+    imin = xi < imin ? xi : imin;
+    imax = xi > imax ? xi : imax;
+    const double xf = static_cast<double>(x);
+    fmin = xf < fmin ? xf : fmin;
+    fmax = xf > fmax ? xf : fmax;
+  }
+};
+
+template <>
+__device__ __forceinline__ void Acc::add<double>(double x, int64_t w, bool pass2, double mean) {
+  if (pass2) {
+    const double d = x - mean;
+    fsum += d * d * static_cast<double>(w);
+    return;
+  }
+  fsum += x * static_cast<double>(w);
+  cnt += w;
+  fmin = x < fmin ? x : fmin;
+  fmax = x > fmax ? x : fmax;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ void block_store_acc(Acc a, AggPart* out) {
+  __shared__ uint64_t ru[BLOCK / 32 + 1];
+  __shared__ double rf[BLOCK / 32 + 1];
+  __shared__ int64_t ri[BLOCK / 32 + 1];
+  constexpr int NW = BLOCK / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t isum = block_sum<BLOCK>(a.isum, ru);
+  const double fsum = block_sum<BLOCK>(a.fsum, rf);
+  const uint64_t cnt = block_sum<BLOCK>(static_cast<uint64_t>(a.cnt), ru);
+  // min / max via warp reductions
+  int64_t imin = warp_min(a.imin), imax = warp_max(a.imax);
+  double fmin = warp_min(a.fmin), fmax = warp_max(a.fmax);
+  __shared__ int64_t smin[NW], smax[NW];
+  __shared__ double sfmin[NW], sfmax[NW];
+  if (lane == 0) {
+    smin[wid] = imin;
+    smax[wid] = imax;
+    sfmin[wid] = fmin;
+    sfmax[wid] = fmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < NW; ++w) {
+      imin = smin[w] < imin ? smin[w] : imin;
+      imax = smax[w] > imax ? smax[w] : imax;
+      fmin = sfmin[w] < fmin ? sfmin[w] : fmin;
+      fmax = sfmax[w] > fmax ? sfmax[w] : fmax;
+    }
+    AggPart p;
+    p.isum = isum;
+    p.fsum = fsum;
+    p.cnt = static_cast<long long>(cnt);
+    p.imin = imin;
+    p.imax = imax;
+    p.fmin = fmin;
+    p.fmax = fmax;
+    p.pad = 0;
+    *out = p;
+  }
+  (void)ri;
+}
+
+// Generic slot reduction. Weighted by run length when s != nullptr, unit
+// weight otherwise. Optional inline decode (bit-width-reduced plain storage:
+// wrap to logical width, add centre) — K9 fused into the reduction.
+struct SlotSpec {
+  const void* v;
+  int dt;
+  const int64_t* s;
+  const int64_t* e;
+  int64_t n;
+  int decode;  // 1: integer decode with logical/centre
+  int logical;
+  int has_center;
+  int64_t center;
+};
+
+template <class T, int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    k_reduce_slots(SlotSpec sp, int pass2, double mean, AggPart* __restrict__ parts) {
+  Acc acc;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * BLOCK + threadIdx.x; i < sp.n;
+       i += static_cast<int64_t>(gridDim.x) * BLOCK) {
+    T x;
+    if (sp.decode) {
+      int64_t r = wrap_to(sp.logical, ld_i64(sp.v, sp.dt, i));
+      if (sp.has_center)
+        r = wrap_to(sp.logical, static_cast<int64_t>(static_cast<uint64_t>(r) + static_cast<uint64_t>(sp.center)));
+      x = static_cast<T>(r);
+    } else {
+      x = ld_as<T>(sp.v, sp.dt, i);
+    }
+    const int64_t w = sp.s ? ldg64(sp.e, i) - ldg64(sp.s, i) + 1 : 1;
+    acc.add<T>(x, w, pass2 != 0, mean);
+  }
+  block_store_acc<BLOCK>(acc, parts + blockIdx.x);
+}
+
+// Combines `n` partials in a fixed order into parts_out[0].
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_combine(const AggPart* __restrict__ parts, int64_t n,
+                                                   AggPart* __restrict__ out) {
+  Acc acc;
+  for (int64_t i = threadIdx.x; i < n; i += BLOCK) {
+    const AggPart p = parts[i];
+    acc.isum += p.isum;
+    acc.fsum += p.fsum;
+    acc.cnt += p.cnt;
+    acc.imin = p.imin < acc.imin ? p.imin : acc.imin;
+    acc.imax = p.imax > acc.imax ? p.imax : acc.imax;
+    acc.fmin = p.fmin < acc.fmin ? p.fmin : acc.fmin;
+    acc.fmax = p.fmax > acc.fmax ? p.fmax : acc.fmax;
+  }
+  block_store_acc<BLOCK>(acc, out);
+}
+
+// K2: fused RLE×RLE intersection + (va op vb)·len reduction.
+template <int BLOCK, int ITEMS, bool GAPLESS, class T>
+__global__ void __launch_bounds__(BLOCK)
+    k_pair_reduce(MergeArgs m, const int64_t* __restrict__ s1, const int64_t* __restrict__ s2,
+                  const void* __restrict__ v1, int dt1, const void* __restrict__ v2, int dt2, int op,
+                  int pass2, double mean, AggPart* __restrict__ parts, int* __restrict__ err) {
+  using Tile = MergeTile<BLOCK, ITEMS>;
+  __shared__ int64_t sk[Tile::TILE];
+  Tile t;
+  t.load(m, blockIdx.x, sk);
+  Acc acc;
+  int lerr = 0;
+  int64_t prev = GAPLESS ? t.prev_key(sk, m) : 0;
+  t.walk(sk, [&](int64_t i, int64_t j, bool takeA, int64_t key) {
+    // the walk reports (A index, B index); one of them is the consumed key
+    const int64_t ia = i, jb = j;
+    const bool valid = takeA ? (jb < m.nb) : (ia < m.na);
+    int64_t len;
+    if (GAPLESS) {
+      len = key - prev;
+      prev = key;
+    } else {
+      const int64_t lo = valid ? max(ldg64(s1, ia), ldg64(s2, jb)) : key + 1;
+      len = key - lo + 1;
+    }
+    if (valid && len > 0) {
+      const T a = ld_as<T>(v1, dt1, ia);
+      const T b = ld_as<T>(v2, dt2, jb);
+      acc.add<T>(arith_t<T>(a, b, op, &lerr), len, pass2 != 0, mean);
+    }
+  });
+  if (lerr) atomicExch(err, 1);
+  __syncthreads();
+  block_store_acc<BLOCK>(acc, parts + blockIdx.x);
+}
+
+}  // namespace dev
+
+namespace {
+
+constexpr int RB = 256;
+
+struct AggHost {
+  uint64_t isum = 0;
+  double fsum = 0.0;
+  int64_t cnt = 0;
+  int64_t imin = INT64_MAX, imax = INT64_MIN;
+  double fmin = std::numeric_limits<double>::infinity();
+  double fmax = -std::numeric_limits<double>::infinity();
+};
+
+int grid_for(const CtxPtr& ctx, int64_t n) {
+  int64_t g = (n + RB * 4 - 1) / (RB * 4);
+  const int64_t cap = static_cast<int64_t>(ctx->sm_count) * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+AggHost combine(const CtxPtr& ctx, const DArr& parts, int64_t nparts) {
+  DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8);
+  dev::k_combine<RB><<<1, RB, 0, ctx->stream>>>(parts.as<dev::AggPart>(), nparts,
+                                                out.as<dev::AggPart>());
+  ctx->count_launch();
+  RQ_CUDA_CHECK(cudaGetLastError());
+  const auto* p = reinterpret_cast<const dev::AggPart*>(ctx->readback(out.raw(), sizeof(dev::AggPart)));
+  AggHost h;
+  h.isum = p->isum;
+  h.fsum = p->fsum;
+  h.cnt = p->cnt;
+  h.imin = p->imin;
+  h.imax = p->imax;
+  h.fmin = p->fmin;
+  h.fmax = p->fmax;
+  return h;
+}
+
+// runs the slot reduction over several parts (e.g. RLE+Index runs + points)
+AggHost reduce_specs(const CtxPtr& ctx, const std::vector<dev::SlotSpec>& specs, bool flt,
+                     bool pass2, double mean) {
+  int64_t total_blocks = 0;
+  std::vector<int> grids;
+  for (const auto& sp : specs) {
+    grids.push_back(grid_for(ctx, sp.n));
+    total_blocks += grids.back();
+  }
+  DArr parts = alloc_arr(ctx, RQ_I64, total_blocks * (sizeof(dev::AggPart) / 8));
+  int64_t off = 0;
+  for (size_t k = 0; k < specs.size(); ++k) {
+    auto* dst = parts.as<dev::AggPart>() + off;
+    if (flt)
+      dev::k_reduce_slots<double, RB><<<grids[k], RB, 0, ctx->stream>>>(specs[k], pass2, mean, dst);
+    else
+      dev::k_reduce_slots<int64_t, RB><<<grids[k], RB, 0, ctx->stream>>>(specs[k], pass2, mean, dst);
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+    off += grids[k];
+  }
+  return combine(ctx, parts, total_blocks);
+}
+
+// Final scalar per AggFn (groupby.cpp:67-135, kernels.cpp:97-125 sentinels).
+AggOut finish(int fn, bool flt, const AggHost& h, const AggHost* sq) {
+  AggOut o;
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  switch (fn) {
+    case RQ_SUM:
+      if (flt) {
+        o.dtype = RQ_F64;
+        o.f = h.fsum;
+      } else {
+        o.dtype = RQ_I64;
+        o.i = static_cast<int64_t>(h.isum);
+      }
+      break;
+    case RQ_COUNT:
+      o.dtype = RQ_I64;
+      o.i = h.cnt;
+      break;
+    case RQ_MIN:
+      if (flt) {
+        o.dtype = RQ_F64;
+        o.f = h.fmin;
+      } else {
+        o.dtype = RQ_I64;
+        o.i = h.imin;
+      }
+      break;
+    case RQ_MAX:
+      if (flt) {
+        o.dtype = RQ_F64;
+        o.f = h.fmax;
+      } else {
+        o.dtype = RQ_I64;
+        o.i = h.imax;
+      }
+      break;
+    case RQ_AVG:
+      o.dtype = RQ_F64;
+      o.f = h.cnt > 0 ? h.fsum / static_cast<double>(h.cnt) : nan;
+      break;
+    case RQ_VAR:
+    case RQ_STD: {
+      o.dtype = RQ_F64;
+      if (h.cnt == 0 || !sq) {
+        o.f = nan;
+        break;
+      }
+      const double var = sq->fsum / static_cast<double>(h.cnt);
+      o.f = fn == RQ_VAR ? var : std::sqrt(var);
+      break;
+    }
+    default:
+      fail("aggregate: unknown function");
+  }
+  return o;
+}
+
+dev::SlotSpec spec_of(const DArr& v, const DArr* s, const DArr* e) {
+  dev::SlotSpec sp{};
+  sp.v = v.raw();
+  sp.dt = v.dt;
+  sp.s = s ? s->pos() : nullptr;
+  sp.e = e ? e->pos() : nullptr;
+  sp.n = v.n;
+  return sp;
+}
+
+AggOut reduce_with_specs(const CtxPtr& ctx, const std::vector<dev::SlotSpec>& specs, bool flt,
+                         int fn) {
+  AggHost h = reduce_specs(ctx, specs, flt, false, 0.0);
+  if ((fn == RQ_VAR || fn == RQ_STD) && h.cnt > 0) {
+    const double mean = h.fsum / static_cast<double>(h.cnt);
+    AggHost sq = reduce_specs(ctx, specs, flt, true, mean);
+    return finish(fn, flt, h, &sq);
+  }
+  return finish(fn, flt, h, nullptr);
+}
+
+}  // namespace
+
+AggOut reduce_slots(const CtxPtr& ctx, const DArr& v, const DArr* s, const DArr* e, int fn) {
+  return reduce_with_specs(ctx, {spec_of(v, s, e)}, dt_float(v.dt), fn);
+}
+
+// agg::aggregate_all (groupby.cpp:164-172): normalize_basic then one group.
+// Composite parts are reduced in place (no expansion of RLE+Index to rows):
+// every aggregate is a fold over covered rows, so runs (weighted) and points
+// (unit) contribute to the same accumulators.
+AggOut aggregate_column(const CtxPtr& ctx, const DCol& c, int fn) {
+  require(fn >= RQ_SUM && fn <= RQ_VAR, "aggregate: unknown function");
+  switch (c.enc) {
+    case RQ_ENC_PLAIN: {
+      dev::SlotSpec sp = spec_of(c.v, nullptr, nullptr);
+      const bool flt = dt_float(c.logical) || dt_float(c.v.dt);
+      if (!flt && (c.has_center || c.v.dt != c.logical)) {
+        sp.decode = 1;
+        sp.logical = c.logical;
+        sp.has_center = c.has_center ? 1 : 0;
+        sp.center = c.center;
+        return reduce_with_specs(ctx, {sp}, false, fn);
+      }
+      if (flt && c.v.dt != c.logical) {
+        DArr dec = decode_plain(ctx, c);
+        return reduce_with_specs(ctx, {spec_of(dec, nullptr, nullptr)}, true, fn);
+      }
+      return reduce_with_specs(ctx, {sp}, flt, fn);
+    }
+    case RQ_ENC_RLE:
+      return reduce_with_specs(ctx, {spec_of(c.v, &c.s, &c.e)}, dt_float(c.v.dt), fn);
+    case RQ_ENC_INDEX:
+      return reduce_with_specs(ctx, {spec_of(c.v, nullptr, nullptr)}, dt_float(c.v.dt), fn);
+    case RQ_ENC_PLAIN_INDEX: {
+      DArr dec = decode_plain_index(ctx, c);
+      return reduce_with_specs(ctx, {spec_of(dec, nullptr, nullptr)}, dt_float(dec.dt), fn);
+    }
+    case RQ_ENC_RLE_INDEX: {
+      require(c.v.dt == c.v2.dt, "array dtype mismatch");  // to_rows merge (column.cpp:353-370)
+      std::vector<dev::SlotSpec> specs;
+      if (c.s.n) specs.push_back(spec_of(c.v, &c.s, &c.e));
+      if (c.p2.n) specs.push_back(spec_of(c.v2, nullptr, nullptr));
+      if (specs.empty()) specs.push_back(spec_of(c.v, &c.s, &c.e));
+      return reduce_with_specs(ctx, specs, dt_float(c.v.dt), fn);
+    }
+  }
+  fail("aggregate: unknown encoding");
+}
+
+namespace {
+
+constexpr int PB = 256, PI = 8;
+
+AggHost pair_reduce(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bool gapless,
+                    bool flt, bool pass2, double mean) {
+  constexpr int TILE = PB * PI;
+  const int64_t na = a.e.n, nb = b.e.n;
+  const int64_t ntiles = (na + nb + TILE - 1) / TILE;
+  DArr part = alloc_arr(ctx, RQ_I64, ntiles + 2);
+  {
+    const int64_t nparts = ntiles + 1;
+    const int blocks = static_cast<int>((nparts * 32 + 255) / 256);
+    dev::k_merge_partition<<<blocks, 256, 0, ctx->stream>>>(a.e.pos(), na, b.e.pos(), nb, TILE,
+                                                            nparts, part.as<int64_t>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  DArr parts = alloc_arr(ctx, RQ_I64, ntiles * (sizeof(dev::AggPart) / 8));
+  DArr err = alloc_arr(ctx, RQ_I32, 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(err.raw_mut(), 0, 4, ctx->stream));
+  dev::MergeArgs m{a.e.pos(), na, b.e.pos(), nb, part.as<int64_t>()};
+  auto* P = parts.as<dev::AggPart>();
+  const unsigned g = static_cast<unsigned>(ntiles);
+  if (gapless) {
+    if (flt) dev::k_pair_reduce<PB, PI, true, double><<<g, PB, 0, ctx->stream>>>(m, a.s.pos(), b.s.pos(), a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, op, pass2, mean, P, err.as<int>());
+    else dev::k_pair_reduce<PB, PI, true, int64_t><<<g, PB, 0, ctx->stream>>>(m, a.s.pos(), b.s.pos(), a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, op, pass2, mean, P, err.as<int>());
+  } else {
+    if (flt) dev::k_pair_reduce<PB, PI, false, double><<<g, PB, 0, ctx->stream>>>(m, a.s.pos(), b.s.pos(), a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, op, pass2, mean, P, err.as<int>());
+    else dev::k_pair_reduce<PB, PI, false, int64_t><<<g, PB, 0, ctx->stream>>>(m, a.s.pos(), b.s.pos(), a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, op, pass2, mean, P, err.as<int>());
+  }
+  ctx->count_launch();
+  RQ_CUDA_CHECK(cudaGetLastError());
+  AggHost h = combine(ctx, parts, ntiles);
+  if (!flt && op == RQ_DIV) {
+    const int64_t* e = ctx->readback(err.raw(), 8);
+    if (static_cast<int32_t>(e[0] & 0xffffffff)) fail("integer division by zero");
+  }
+  return h;
+}
+
+}  // namespace
+
+// aggregate_all(arith(a, b, op), fn) fused for RLE×RLE (K2); other encoding
+// pairs run the materialising operator chain on the device.
+AggOut aggregate_binop(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, int fn) {
+  require(op >= RQ_ADD && op <= RQ_DIV, "aggregate_binop: arithmetic operator required");
+  require(a.total == b.total, "align: total_size mismatch");
+  if (a.enc == RQ_ENC_RLE && b.enc == RQ_ENC_RLE && fn != RQ_MIN && fn != RQ_MAX) {
+    const bool flt = dt_float(a.v.dt) || dt_float(b.v.dt);
+    if (a.e.n == 0 || b.e.n == 0) {
+      AggHost h;
+      return finish(fn, flt, h, nullptr);
+    }
+    const bool gapless = col_gapless(ctx, a) && col_gapless(ctx, b);
+    AggHost h = pair_reduce(ctx, a, b, op, gapless, flt, false, 0.0);
+    if ((fn == RQ_VAR || fn == RQ_STD) && h.cnt > 0) {
+      AggHost sq = pair_reduce(ctx, a, b, op, gapless, flt, true, h.fsum / static_cast<double>(h.cnt));
+      return finish(fn, flt, h, &sq);
+    }
+    return finish(fn, flt, h, nullptr);
+  }
+  DCol r = arith(ctx, a, b, op);
+  return aggregate_column(ctx, r, fn);
+}
+
+}  // namespace rqb

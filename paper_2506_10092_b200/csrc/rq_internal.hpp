@@ -1,0 +1,321 @@
+// rq_internal.hpp — host-side internals of the B200 compressed-execution
+// library: device column model, context, allocation, error plumbing.
+//
+// Device layout: every column part is a separate
+// structure-of-arrays device buffer (runq::Array / PosVec in the reference,
+// array.hpp:16, column.hpp:22-76): values at their storage width, positions
+// int64. Buffers are 256-B aligned (cudaMallocAsync) so kernels may issue
+// 128-bit loads; buffers are reference counted so operators that keep an
+// input's positions share them instead of copying (the reference copies,
+// align.cpp:86-100).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/runq_b200.h"
+
+namespace rqb {
+
+// ---- errors -----------------------------------------------------------------
+
+struct RqError : std::runtime_error {
+  int code;
+  RqError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(const std::string& msg, int code = RQ_INVALID) {
+  throw RqError(code, msg);
+}
+inline void require(bool cond, const char* msg) {
+  if (!cond) fail(msg);
+}
+
+void cuda_fail(cudaError_t err, const char* what, const char* file, int line);
+#define RQ_CUDA_CHECK(x)                                          \
+  do {                                                            \
+    cudaError_t err__ = (x);                                      \
+    if (err__ != cudaSuccess) ::rqb::cuda_fail(err__, #x, __FILE__, __LINE__); \
+  } while (0)
+
+// ---- dtypes (runq::DType, dtype.hpp:11-71) -------------------------------------
+
+inline int dt_width(int32_t t) {
+  switch (t) {
+    case RQ_I8: return 1;
+    case RQ_I16: return 2;
+    case RQ_I32: return 4;
+    case RQ_F32: return 4;
+    default: return 8;
+  }
+}
+inline bool dt_float(int32_t t) { return t == RQ_F32 || t == RQ_F64; }
+inline bool dt_valid(int32_t t) { return t >= RQ_I8 && t <= RQ_F64; }
+// dtype_promote (dtype.hpp:69-71)
+inline int32_t dt_promote(int32_t a, int32_t b) {
+  return (dt_float(a) || dt_float(b)) ? RQ_F64 : RQ_I64;
+}
+
+// ---- context -------------------------------------------------------------------
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  int64_t launches = 0;
+  int64_t* pinned = nullptr;  // host-pinned readback slots
+  // decoupled look-back tile status (epoch-tagged, see device_common.cuh)
+  unsigned long long* tile_status = nullptr;
+  int64_t tile_status_cap = 0;
+  uint32_t epoch = 0;
+  // small device scratch for counters / reduction partials
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+
+  ~Ctx();
+  void* alloc(size_t bytes);
+  void free(void* p);
+  void sync();
+  // Copies `bytes` from device to the pinned slots and waits (one sync).
+  const int64_t* readback(const void* dev, size_t bytes);
+  // Ensures tile_status can hold `tiles` entries; returns the epoch to use.
+  uint32_t next_epoch(int64_t tiles);
+  void* get_scratch(size_t bytes);
+  void count_launch(int n = 1) { launches += n; }
+};
+
+using CtxPtr = std::shared_ptr<Ctx>;
+
+// ---- buffers and arrays ----------------------------------------------------------
+
+struct Buffer {
+  CtxPtr ctx;  // keeps the stream alive for the stream-ordered free
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  bool owned = true;
+  ~Buffer();
+};
+
+struct DArr {
+  int32_t dt = RQ_I64;
+  int64_t n = 0;
+  std::shared_ptr<Buffer> buf;
+
+  const void* raw() const { return buf ? buf->ptr : nullptr; }
+  void* raw_mut() const { return buf ? buf->ptr : nullptr; }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(raw_mut());
+  }
+  const int64_t* pos() const { return as<int64_t>(); }
+  size_t bytes() const { return static_cast<size_t>(n) * dt_width(dt); }
+};
+
+DArr alloc_arr(const CtxPtr& ctx, int32_t dt, int64_t n);
+DArr upload_arr(const CtxPtr& ctx, int32_t dt, const void* host, int64_t n);
+void download_arr(const CtxPtr& ctx, const DArr& a, void* host);
+// Device-side copy of the first n elements into a new array.
+DArr copy_prefix(const CtxPtr& ctx, const DArr& a, int64_t n);
+
+// ---- columns (runq::Column, column.hpp:22-107) --------------------------------------
+
+struct DCol {
+  int32_t enc = RQ_ENC_PLAIN;
+  int64_t total = 0;
+  // PLAIN / PLAIN_INDEX base: v = storage values, logical, center
+  // RLE / RLE_INDEX runs: v, s, e ; INDEX: v, p
+  DArr v;
+  int32_t logical = RQ_I64;
+  bool has_center = false;
+  int64_t center = 0;
+  DArr s, e, p;
+  // PLAIN_INDEX outliers / RLE_INDEX points
+  DArr v2, p2;
+  // RLE facts computed on demand: 1 if runs tile [0,total) with no gaps
+  mutable int gapless = -1;
+
+  int32_t value_type() const {  // column.cpp:88-97
+    switch (enc) {
+      case RQ_ENC_PLAIN: return logical;
+      case RQ_ENC_PLAIN_INDEX: return v2.dt;
+      default: return v.dt;
+    }
+  }
+  int64_t runs() const { return s.n; }
+};
+
+struct DMask {
+  int32_t enc = RQ_MASK_RLE;
+  int64_t total = 0;
+  DArr bits;    // PLAIN (uint8 per row, dt = I8)
+  DArr s, e;    // RLE / COMPOSITE runs
+  DArr p;       // INDEX / COMPOSITE points
+  mutable int64_t true_count = -1;
+};
+
+}  // namespace rqb
+
+// ---- opaque handle definitions -----------------------------------------------------
+
+struct rq_ctx_s {
+  rqb::CtxPtr ctx;
+};
+struct rq_arr_s {
+  rqb::DArr a;
+};
+struct rq_col_s {
+  rqb::DCol c;
+};
+struct rq_mask_s {
+  rqb::DMask m;
+};
+
+namespace rqb {
+
+void set_last_error(const std::string& msg);
+
+template <class F>
+int api_guard(F&& f) {
+  try {
+    f();
+    set_last_error("");
+    return RQ_OK;
+  } catch (const RqError& ex) {
+    set_last_error(ex.what());
+    return ex.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return RQ_RESOURCE;
+  } catch (const std::exception& ex) {
+    set_last_error(ex.what());
+    return RQ_INVALID;
+  }
+}
+
+inline rq_arr_t wrap_arr(DArr a) { return new rq_arr_s{std::move(a)}; }
+inline rq_col_t wrap_col(DCol c) { return new rq_col_s{std::move(c)}; }
+inline rq_mask_t wrap_mask(DMask m) { return new rq_mask_s{std::move(m)}; }
+
+// ---- operator entry points (ops.cpp / kernels) ----------------------------------------
+
+struct Scalar {
+  bool is_float = false;
+  int64_t i = 0;
+  double f = 0.0;
+};
+
+// primitives (k_merge.cu)
+struct Intersection {
+  DArr s, e, idx1, idx2;
+};
+Intersection range_intersect(const CtxPtr& ctx, const DArr& s1, const DArr& e1, const DArr& s2,
+                             const DArr& e2, bool want_idx1, bool want_idx2);
+struct PointsInRuns {
+  DArr p_out, run_of, idx_of;
+};
+PointsInRuns points_in_runs(const CtxPtr& ctx, const DArr& p, const DArr& s, const DArr& e,
+                            bool want_run_of, bool want_idx_of);
+struct PointsIntersect {
+  DArr p_out, idx1, idx2;
+};
+PointsIntersect points_intersect(const CtxPtr& ctx, const DArr& p1, const DArr& p2,
+                                 bool want_idx1, bool want_idx2);
+DArr bucketize(const CtxPtr& ctx, const DArr& x, const DArr& b, bool right);
+// merge of two disjoint sorted lists (keys + optional run ends + values)
+void merge_disjoint(const CtxPtr& ctx, const DArr& kA, const DArr* eA, const DArr* vA,
+                    const DArr& kB, const DArr* eB, const DArr* vB, DArr& k_out, DArr* e_out,
+                    DArr* v_out);
+// sorted de-duplicated union of two position lists
+DArr union_points(const CtxPtr& ctx, const DArr& p1, const DArr& p2);
+// byte-mask helpers
+DArr bytes_and(const CtxPtr& ctx, const DArr& a, const DArr& b);
+DArr bytes_copy01(const CtxPtr& ctx, const DArr& a);
+void set_bits(const CtxPtr& ctx, DArr& bits, const DArr& p);
+DArr zeros_bytes(const CtxPtr& ctx, int64_t n);
+
+// gathers / elementwise (k_dense.cu)
+DArr gather(const CtxPtr& ctx, const DArr& v, const DArr& idx);
+DArr decode_plain(const CtxPtr& ctx, const DCol& c);             // Plain -> logical values
+DArr decode_plain_index(const CtxPtr& ctx, const DCol& c);       // P+I -> logical values
+DArr arith_values(const CtxPtr& ctx, const DArr& a, const DArr& b, int op);
+DArr cmp_values(const CtxPtr& ctx, const DArr& a, const DArr& b, int op);  // uint8 flags
+DArr scalar_arith_values(const CtxPtr& ctx, const DArr& v, Scalar k, int op, bool reversed);
+DArr scalar_cmp_values(const CtxPtr& ctx, const DArr& v, Scalar k, int op, bool reversed);
+DArr cast_values(const CtxPtr& ctx, const DArr& v, int32_t to);
+// Plain (narrow, centered) compare -> uint8 mask bytes, decode fused (K6/K9)
+DArr plain_cmp_scalar(const CtxPtr& ctx, const DCol& c, Scalar k, int op, bool reversed);
+// set bits[p[i]] = flags[i] (P+I outlier overlay)
+void scatter_flags(const CtxPtr& ctx, DArr& bits, const DArr& p, const DArr& flags);
+DArr iota(const CtxPtr& ctx, int64_t n);
+
+// compaction (k_select.cu)
+// keep (s,e) of runs whose flag is set
+void select_runs(const CtxPtr& ctx, const DArr& flags, const DArr& s, const DArr& e, DArr& s_out,
+                 DArr& e_out);
+// keep p of points whose flag is set (optionally also their index)
+void select_points(const CtxPtr& ctx, const DArr& flags, const DArr& p, DArr& p_out,
+                   DArr* idx_out);
+// RLE-column compare_scalar fused: flags computed inline from v
+void rle_cmp_scalar_select(const CtxPtr& ctx, const DArr& v, const DArr& s, const DArr& e,
+                           Scalar k, int op, bool reversed, DArr& s_out, DArr& e_out);
+void index_cmp_scalar_select(const CtxPtr& ctx, const DArr& v, const DArr& p, Scalar k, int op,
+                             bool reversed, DArr& p_out);
+void plain_mask_to_rle(const CtxPtr& ctx, const DArr& bits, DArr& s, DArr& e);
+DArr plain_mask_to_index(const CtxPtr& ctx, const DArr& bits);
+// run expansion: positions of every row covered by runs (range_arange), and
+// optionally the source run of each row.
+void expand_runs(const CtxPtr& ctx, const DArr& s, const DArr& e, DArr* positions,
+                 DArr* run_idx);
+int64_t covered_rows(const CtxPtr& ctx, const DArr& s, const DArr& e);
+int64_t count_nonzero(const CtxPtr& ctx, const DArr& bits);
+bool runs_gapless(const CtxPtr& ctx, const DArr& s, const DArr& e, int64_t total);
+DArr compact_positions(const CtxPtr& ctx, const DArr& s, const DArr& e, DArr& e_out,
+                       int64_t* covered);
+
+// reductions (k_agg.cu)
+struct AggOut {
+  int32_t dtype = RQ_I64;
+  int64_t i = 0;
+  double f = 0.0;
+};
+// Aggregate over slots with weights (run lengths) — shape given as RLE runs
+// (s,e), or unit weights (points / dense) when s is empty.
+AggOut reduce_slots(const CtxPtr& ctx, const DArr& v, const DArr* s, const DArr* e, int fn);
+AggOut aggregate_column(const CtxPtr& ctx, const DCol& c, int fn);
+AggOut aggregate_binop(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, int fn);
+AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int cmp,
+                                const DCol& a, const DCol& b, int op, int fn);
+
+// high-level ops (ops.cpp)
+struct Aligned {
+  int kind = 0;  // 0 dense, 1 run, 2 point
+  DArr s, e, p;
+  DArr v1, v2;
+  int64_t total = 0;
+};
+Aligned align(const CtxPtr& ctx, const DCol& a, const DCol& b);
+DCol arith(const CtxPtr& ctx, const DCol& a, const DCol& b, int op);
+DMask compare(const CtxPtr& ctx, const DCol& a, const DCol& b, int op);
+DCol arith_scalar(const CtxPtr& ctx, const DCol& a, Scalar k, int op, bool reversed);
+DMask compare_scalar(const CtxPtr& ctx, const DCol& a, Scalar k, int op, bool reversed);
+DCol filter(const CtxPtr& ctx, const DCol& a, const DMask& m);
+DMask mask_and(const CtxPtr& ctx, const DMask& a, const DMask& b);
+DMask mask_or(const CtxPtr& ctx, const DMask& a, const DMask& b);
+DCol normalize_basic(const CtxPtr& ctx, const DCol& c);
+int64_t mask_true_count(const CtxPtr& ctx, const DMask& m);
+bool col_gapless(const CtxPtr& ctx, const DCol& c);
+
+struct GroupAggOut {
+  int64_t n_groups = 0;
+  std::vector<DArr> keys;
+  std::vector<DArr> vals;
+};
+GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
+                            const std::vector<const DCol*>& data, const std::vector<int>& fns);
+
+}  // namespace rqb

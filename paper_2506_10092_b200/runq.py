@@ -1,0 +1,503 @@
+"""Python face of the B200 compressed-execution path, mirroring the
+reference operator API (``runq::compute``, ``runq::enc``, ``runq::masks``,
+``runq::agg``, ``runq::kernels``; align.hpp:59-95, primitives.hpp:28-92,
+mask_ops.hpp:18, groupby.hpp:22-50, kernels.hpp:13-72) over the C ABI in
+``include/runq_b200.h``.
+
+Every function accepts host column images (``host.py``) or device handles.
+Host inputs are uploaded and results downloaded (value semantics, like the
+reference); device inputs stay resident and return device handles. All
+compute runs in the sm_100a kernels of ``librunq_b200.so``; there is no
+CPU fallback — the module raises at import if the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+from . import host as H
+from ._lib import check, load
+
+_L = load()
+
+
+class Context:
+    """rq_ctx_t: device, CUDA stream, stream-ordered pool, pinned readback."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(_L.rq_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def synchronize(self):
+        check(_L.rq_ctx_synchronize(self.handle))
+
+    @property
+    def stream(self) -> int:
+        return _L.rq_ctx_stream(self.handle) or 0
+
+    @property
+    def launches(self) -> int:
+        return int(_L.rq_ctx_launches(self.handle))
+
+    def close(self):
+        if self.handle:
+            _L.rq_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+class DeviceArray:
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+
+    @property
+    def info(self):
+        dt, n = C.c_int32(), C.c_int64()
+        check(_L.rq_arr_info(self.handle, C.byref(dt), C.byref(n)))
+        return int(dt.value), int(n.value)
+
+    @property
+    def dtype(self) -> int:
+        return self.info[0]
+
+    def __len__(self):
+        return self.info[1]
+
+    @property
+    def device_ptr(self) -> int:
+        return _L.rq_arr_device_ptr(self.handle) or 0
+
+    def download(self) -> np.ndarray:
+        dt, n = self.info
+        out = np.empty(n, dtype=H.DTYPES[dt])
+        check(_L.rq_arr_download(self.ctx.handle, self.handle, out.ctypes.data if n else None))
+        return out
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _L.rq_arr_free(self.handle)
+            self.handle = None
+
+
+class DeviceColumn:
+    """rq_col_t — a device-resident runq::Column."""
+
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+
+    @property
+    def encoding(self) -> int:
+        return _L.rq_col_encoding(self.handle)
+
+    @property
+    def total_size(self) -> int:
+        return int(_L.rq_col_total_size(self.handle))
+
+    @property
+    def value_type(self) -> int:
+        return _L.rq_col_value_type(self.handle)
+
+    def part(self, which: int) -> DeviceArray:
+        h = C.c_void_p()
+        check(_L.rq_col_part(self.handle, which, C.byref(h)))
+        return DeviceArray(h, self.ctx)
+
+    def download(self) -> H.Column:
+        img = H.HostColumn()
+        check(_L.rq_col_describe(self.handle, C.byref(img)))
+        arrs = H.alloc_for_image(img)
+        check(_L.rq_col_download(self.ctx.handle, self.handle, C.byref(img)))
+        return H.column_from_image(img, arrs)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _L.rq_col_free(self.handle)
+            self.handle = None
+
+
+class DeviceMask:
+    """rq_mask_t — a device-resident runq::MaskColumn."""
+
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+
+    def download(self) -> H.Mask:
+        img = H.HostMask()
+        check(_L.rq_mask_describe(self.handle, C.byref(img)))
+        arrs = H.alloc_for_mask_image(img)
+        check(_L.rq_mask_download(self.ctx.handle, self.handle, C.byref(img)))
+        return H.mask_from_image(img, arrs)
+
+    @property
+    def encoding(self) -> int:
+        img = H.HostMask()
+        check(_L.rq_mask_describe(self.handle, C.byref(img)))
+        return int(img.encoding)
+
+    def true_count(self) -> int:
+        n = C.c_int64()
+        check(_L.rq_mask_true_count(self.ctx.handle, self.handle, C.byref(n)))
+        return int(n.value)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _L.rq_mask_free(self.handle)
+            self.handle = None
+
+
+def upload(x, ctx: Context = None):
+    """Host column / mask / numpy array -> device handle."""
+    ctx = _ctx(ctx)
+    h = C.c_void_p()
+    if isinstance(x, (DeviceColumn, DeviceMask, DeviceArray)):
+        return x
+    if isinstance(x, np.ndarray):
+        a = np.ascontiguousarray(x)
+        check(_L.rq_arr_upload(ctx.handle, H.dtype_code(a), a.ctypes.data if a.size else None,
+                               a.shape[0], C.byref(h)))
+        return DeviceArray(h, ctx)
+    if isinstance(x, (H.PlainMask, H.RleMask, H.IndexMask, H.CompositeMask)):
+        img, keep = H.mask_image(x)
+        check(_L.rq_mask_upload(ctx.handle, C.byref(img), C.byref(h)))
+        return DeviceMask(h, ctx)
+    img, keep = H.column_image(x)
+    check(_L.rq_col_upload(ctx.handle, C.byref(img), C.byref(h)))
+    return DeviceColumn(h, ctx)
+
+
+def _is_host(*xs) -> bool:
+    return any(not isinstance(x, (DeviceColumn, DeviceMask, DeviceArray)) for x in xs)
+
+
+def _out(dev, host_mode: bool):
+    return dev.download() if host_mode else dev
+
+
+def _ctx_of(*xs) -> Context:
+    for x in xs:
+        if isinstance(x, (DeviceColumn, DeviceMask, DeviceArray)):
+            return x.ctx
+    return default_context()
+
+
+def _new():
+    return C.c_void_p()
+
+
+# ---------------------------------------------------------------------------
+# runq::enc (primitives.hpp:28-92) and runq::kernels (kernels.hpp:13-72)
+# ---------------------------------------------------------------------------
+
+
+class enc:
+    @staticmethod
+    def range_intersect(s1, e1, s2, e2):
+        """enc::range_intersect (primitives.cpp:15-46) -> (s, e, idx1, idx2)."""
+        host = _is_host(s1, e1, s2, e2)
+        ctx = _ctx_of(s1, e1, s2, e2)
+        a = [upload(np.asarray(x, np.int64) if not isinstance(x, DeviceArray) else x, ctx)
+             for x in (s1, e1, s2, e2)]
+        outs = [_new() for _ in range(4)]
+        check(_L.rq_range_intersect(ctx.handle, *[x.handle for x in a], *[C.byref(o) for o in outs]))
+        res = [DeviceArray(o, ctx) for o in outs]
+        return tuple(_out(r, host) for r in res)
+
+    @staticmethod
+    def _points(fn, p, s, e):
+        host = _is_host(p, s, e)
+        ctx = _ctx_of(p, s, e)
+        a = [upload(np.asarray(x, np.int64) if not isinstance(x, DeviceArray) else x, ctx)
+             for x in (p, s, e)]
+        outs = [_new() for _ in range(3)]
+        check(fn(ctx.handle, *[x.handle for x in a], *[C.byref(o) for o in outs]))
+        return tuple(_out(DeviceArray(o, ctx), host) for o in outs)
+
+    @staticmethod
+    def idx_in_rle(p, s, e):
+        """enc::idx_in_rle (primitives.cpp:48-61) -> (p_out, run_of, idx_of)."""
+        return enc._points(_L.rq_idx_in_rle, p, s, e)
+
+    @staticmethod
+    def rle_contain_idx(p, s, e):
+        """enc::rle_contain_idx (primitives.cpp:63-86) -> (p_out, run_of, idx_of)."""
+        return enc._points(_L.rq_rle_contain_idx, p, s, e)
+
+    @staticmethod
+    def idx_in_idx(p1, p2):
+        """enc::idx_in_idx (primitives.cpp:88-100) -> (p_out, idx1, idx2)."""
+        host = _is_host(p1, p2)
+        ctx = _ctx_of(p1, p2)
+        a = [upload(np.asarray(x, np.int64) if not isinstance(x, DeviceArray) else x, ctx)
+             for x in (p1, p2)]
+        outs = [_new() for _ in range(3)]
+        check(_L.rq_idx_in_idx(ctx.handle, *[x.handle for x in a], *[C.byref(o) for o in outs]))
+        return tuple(_out(DeviceArray(o, ctx), host) for o in outs)
+
+    @staticmethod
+    def plain_mask_to_rle(m):
+        """enc::plain_mask_to_rle (primitives.cpp:349-360)."""
+        host = _is_host(m)
+        ctx = _ctx_of(m)
+        dm = upload(m, ctx)
+        o = _new()
+        check(_L.rq_plain_mask_to_rle(ctx.handle, dm.handle, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
+    @staticmethod
+    def plain_mask_to_index(m):
+        """enc::plain_mask_to_index (primitives.cpp:362-368)."""
+        host = _is_host(m)
+        ctx = _ctx_of(m)
+        dm = upload(m, ctx)
+        o = _new()
+        check(_L.rq_plain_mask_to_index(ctx.handle, dm.handle, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
+    @staticmethod
+    def compact_rle(c):
+        """enc::compact_rle (primitives.cpp:370-379)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        o = _new()
+        check(_L.rq_compact_rle(ctx.handle, dc.handle, C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+
+class kernels:
+    @staticmethod
+    def bucketize(x, boundaries, right: bool):
+        """kernels::bucketize (kernels.cpp:10-19)."""
+        host = _is_host(x, boundaries)
+        ctx = _ctx_of(x, boundaries)
+        a = upload(np.asarray(x, np.int64) if not isinstance(x, DeviceArray) else x, ctx)
+        b = upload(np.asarray(boundaries, np.int64) if not isinstance(boundaries, DeviceArray) else boundaries, ctx)
+        o = _new()
+        check(_L.rq_bucketize(ctx.handle, a.handle, b.handle, 1 if right else 0, C.byref(o)))
+        return _out(DeviceArray(o, ctx), host)
+
+
+# ---------------------------------------------------------------------------
+# column model helpers
+# ---------------------------------------------------------------------------
+
+
+def decode_values(c):
+    """decode_values (column.cpp:283-309) for Plain / Plain+Index."""
+    host = _is_host(c)
+    ctx = _ctx_of(c)
+    dc = upload(c, ctx)
+    o = _new()
+    check(_L.rq_decode_values(ctx.handle, dc.handle, C.byref(o)))
+    return _out(DeviceArray(o, ctx), host)
+
+
+# ---------------------------------------------------------------------------
+# runq::compute (align.hpp:59-95)
+# ---------------------------------------------------------------------------
+
+
+class compute:
+    DENSE, RUN, POINT = 0, 1, 2
+
+    @staticmethod
+    def normalize_basic(c):
+        """compute::normalize_basic (align.cpp:102-115)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        o = _new()
+        check(_L.rq_normalize_basic(ctx.handle, dc.handle, C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
+    def align(a, b):
+        """compute::align (align.cpp:219-231) -> dict(kind, s, e, p, v1, v2, total_size)."""
+        host = _is_host(a, b)
+        ctx = _ctx_of(a, b)
+        da, db = upload(a, ctx), upload(b, ctx)
+        kind = C.c_int32()
+        outs = [_new() for _ in range(5)]
+        check(_L.rq_align(ctx.handle, da.handle, db.handle, C.byref(kind), *[C.byref(o) for o in outs]))
+        res = {"kind": int(kind.value), "total_size": da.total_size}
+        for name, o in zip(("s", "e", "p", "v1", "v2"), outs):
+            res[name] = _out(DeviceArray(o, ctx), host) if o.value else None
+        return res
+
+    @staticmethod
+    def arith(a, b, op):
+        """compute::arith (align.cpp:495-508)."""
+        op = H.BINOP_NAMES.get(op, op)
+        host = _is_host(a, b)
+        ctx = _ctx_of(a, b)
+        da, db = upload(a, ctx), upload(b, ctx)
+        o = _new()
+        check(_L.rq_arith(ctx.handle, da.handle, db.handle, op, C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
+    def compare(a, b, op):
+        """compute::compare (align.cpp:510-523)."""
+        op = H.BINOP_NAMES.get(op, op)
+        host = _is_host(a, b)
+        ctx = _ctx_of(a, b)
+        da, db = upload(a, ctx), upload(b, ctx)
+        o = _new()
+        check(_L.rq_compare(ctx.handle, da.handle, db.handle, op, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
+    @staticmethod
+    def binary_op(a, b, op):
+        """compute::binary_op (align.cpp:525-528)."""
+        op = H.BINOP_NAMES.get(op, op)
+        return compute.compare(a, b, op) if op >= H.LT else compute.arith(a, b, op)
+
+    @staticmethod
+    def arith_scalar(a, k, op, reversed: bool = False):
+        """compute::arith_scalar (align.cpp:571-596)."""
+        op = H.BINOP_NAMES.get(op, op)
+        host = _is_host(a)
+        ctx = _ctx_of(a)
+        da = upload(a, ctx)
+        o = _new()
+        check(_L.rq_arith_scalar(ctx.handle, da.handle, H.make_scalar(k), op, 1 if reversed else 0, C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
+    def compare_scalar(a, k, op, reversed: bool = False):
+        """compute::compare_scalar (align.cpp:598-652)."""
+        op = H.BINOP_NAMES.get(op, op)
+        host = _is_host(a)
+        ctx = _ctx_of(a)
+        da = upload(a, ctx)
+        o = _new()
+        check(_L.rq_compare_scalar(ctx.handle, da.handle, H.make_scalar(k), op, 1 if reversed else 0, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
+    @staticmethod
+    def scalar_op(a, k, op, reversed: bool = False):
+        """compute::scalar_op (align.cpp:654-657)."""
+        op = H.BINOP_NAMES.get(op, op)
+        if op >= H.LT:
+            return compute.compare_scalar(a, k, op, reversed)
+        return compute.arith_scalar(a, k, op, reversed)
+
+    @staticmethod
+    def filter(a, m):
+        """compute::filter (align.cpp:755-771)."""
+        host = _is_host(a, m)
+        ctx = _ctx_of(a, m)
+        da, dm = upload(a, ctx), upload(m, ctx)
+        o = _new()
+        check(_L.rq_filter(ctx.handle, da.handle, dm.handle, C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+
+class masks:
+    @staticmethod
+    def and_mask(a, b):
+        """masks::and_mask (mask_ops.cpp:183-209)."""
+        host = _is_host(a, b)
+        ctx = _ctx_of(a, b)
+        da, db = upload(a, ctx), upload(b, ctx)
+        o = _new()
+        check(_L.rq_mask_and(ctx.handle, da.handle, db.handle, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
+
+def _agg_result(dt, i, f):
+    return float(f.value) if dt.value == H.F64 else int(i.value)
+
+
+class agg:
+    SUM, COUNT, MIN, MAX, AVG, STD, VAR = range(7)
+
+    @staticmethod
+    def aggregate_all(data, fn):
+        """agg::aggregate_all (groupby.cpp:164-172) -> python int (i64) or float (f64)."""
+        fn = H.AGG_NAMES.get(fn, fn)
+        ctx = _ctx_of(data)
+        dd = upload(data, ctx)
+        dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+        check(_L.rq_aggregate_all(ctx.handle, dd.handle, fn, C.byref(dt), C.byref(i), C.byref(f)))
+        return _agg_result(dt, i, f)
+
+    @staticmethod
+    def group_aggregate(keys: Sequence, data: Sequence, fns: Sequence):
+        """agg::group_aggregate (groupby.cpp:144-162) -> (keys list, values list, n_groups)."""
+        fns = [H.AGG_NAMES.get(f, f) for f in fns]
+        host = _is_host(*keys, *data)
+        ctx = _ctx_of(*keys, *data)
+        dk = [upload(k, ctx) for k in keys]
+        dd = [upload(d, ctx) for d in data]
+        karr = (C.c_void_p * max(1, len(dk)))(*[k.handle.value for k in dk])
+        darr = (C.c_void_p * max(1, len(dd)))(*[d.handle.value for d in dd])
+        farr = (C.c_int32 * max(1, len(fns)))(*fns)
+        ok = (C.c_void_p * max(1, len(dk)))()
+        ov = (C.c_void_p * max(1, len(dd)))()
+        ng = C.c_int64()
+        check(_L.rq_group_aggregate(ctx.handle, karr, len(dk), darr, farr, len(dd), C.byref(ng), ok, ov))
+        ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
+        vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(dd))]
+        return ks, vs, int(ng.value)
+
+    @staticmethod
+    def aggregate_binop(a, b, op, fn):
+        """Fused aggregate_all(arith(a, b, op), fn) — one pass, no materialised fragments."""
+        op = H.BINOP_NAMES.get(op, op)
+        fn = H.AGG_NAMES.get(fn, fn)
+        ctx = _ctx_of(a, b)
+        da, db = upload(a, ctx), upload(b, ctx)
+        dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+        check(_L.rq_aggregate_binop(ctx.handle, da.handle, db.handle, op, fn, C.byref(dt), C.byref(i), C.byref(f)))
+        return _agg_result(dt, i, f)
+
+    @staticmethod
+    def filtered_aggregate_binop(c, k, cmp, a, b, op, fn):
+        """aggregate_all(arith(filter(a,m), filter(b,m), op), fn), m = compare_scalar(c, k, cmp)."""
+        op = H.BINOP_NAMES.get(op, op)
+        cmp = H.BINOP_NAMES.get(cmp, cmp)
+        fn = H.AGG_NAMES.get(fn, fn)
+        ctx = _ctx_of(c, a, b)
+        dc, da, db = upload(c, ctx), upload(a, ctx), upload(b, ctx)
+        dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+        check(_L.rq_filtered_aggregate_binop(ctx.handle, dc.handle, H.make_scalar(k), cmp, da.handle, db.handle,
+                                             op, fn, C.byref(dt), C.byref(i), C.byref(f)))
+        return _agg_result(dt, i, f)
+
+
+def shard_host_column(col: H.Column, lo: int, hi: int) -> H.Column:
+    """rq_shard_host_column: rows [lo, hi) as a standalone shard (host only)."""
+    img, keep = H.column_image(col)
+    out = H.HostColumn()
+    check(_L.rq_shard_host_column(C.byref(img), lo, hi, C.byref(out)))
+    try:
+        return H.column_from_malloc_image(out)
+    finally:
+        _L.rq_host_column_free(C.byref(out))
