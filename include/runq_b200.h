@@ -150,6 +150,11 @@ int rq_ctx_synchronize(rq_ctx_t ctx);
 void* rq_ctx_stream(rq_ctx_t ctx);
 /* Kernel launches issued by this context so far (evidence counter). */
 int64_t rq_ctx_launches(rq_ctx_t ctx);
+/* Per-kernel CUDA-event timing: when enabled, each tagged kernel launch is
+ * bracketed by events on the context stream (SURVEY.md §5 tracing). */
+int rq_ctx_set_profiling(rq_ctx_t ctx, int32_t enable);
+/* JSON {"tag": {"ms": total, "count": launches}, ...} into buf (syncs). */
+int rq_ctx_profile_report(rq_ctx_t ctx, int32_t reset, char* buf, int64_t cap);
 
 /* ---------------------------------------------------------------------- */
 /* arrays (runq::Array, array.hpp:16-99; positions are RQ_I64 arrays)       */
@@ -249,6 +254,10 @@ int rq_filter(rq_ctx_t ctx, rq_col_t a, rq_mask_t m, rq_col_t* out);
 
 /* masks::and_mask (mask_ops.cpp:183-209). */
 int rq_mask_and(rq_ctx_t ctx, rq_mask_t a, rq_mask_t b, rq_mask_t* out);
+/* masks::or_mask (mask_ops.cpp:211-237). */
+int rq_mask_or(rq_ctx_t ctx, rq_mask_t a, rq_mask_t b, rq_mask_t* out);
+/* masks::not_mask (mask_ops.cpp:239-265). */
+int rq_mask_not(rq_ctx_t ctx, rq_mask_t a, rq_mask_t* out);
 
 /* ---------------------------------------------------------------------- */
 /* aggregation: runq::agg (groupby.hpp:22-50)                               */

@@ -29,6 +29,8 @@ PROTOTYPES = {
     "rq_ctx_synchronize": (C.c_int, [vp]),
     "rq_ctx_stream": (vp, [vp]),
     "rq_ctx_launches": (i64, [vp]),
+    "rq_ctx_set_profiling": (C.c_int, [vp, i32]),
+    "rq_ctx_profile_report": (C.c_int, [vp, i32, C.c_char_p, i64]),
     "rq_arr_upload": (C.c_int, [vp, i32, vp, i64, P(vp)]),
     "rq_arr_wrap_device": (C.c_int, [vp, i32, vp, i64, P(vp)]),
     "rq_arr_info": (C.c_int, [vp, P(i32), P(i64)]),
@@ -68,6 +70,8 @@ PROTOTYPES = {
     "rq_compare_scalar": (C.c_int, [vp, vp, Scalar, i32, i32, P(vp)]),
     "rq_filter": (C.c_int, [vp, vp, vp, P(vp)]),
     "rq_mask_and": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_mask_or": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_mask_not": (C.c_int, [vp, vp, P(vp)]),
     "rq_aggregate_all": (C.c_int, [vp, vp, i32, P(i32), P(i64), P(C.c_double)]),
     "rq_group_aggregate": (C.c_int, [vp, P(vp), i32, P(vp), P(i32), i32, P(i64), P(vp), P(vp)]),
     "rq_aggregate_binop": (C.c_int, [vp, vp, vp, i32, i32, P(i32), P(i64), P(C.c_double)]),

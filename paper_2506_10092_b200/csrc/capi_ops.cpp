@@ -221,6 +221,20 @@ int rq_mask_and(rq_ctx_t c, rq_mask_t a, rq_mask_t b, rq_mask_t* out) {
   });
 }
 
+int rq_mask_or(rq_ctx_t c, rq_mask_t a, rq_mask_t b, rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_mask(mask_or(ctx, mask_of(a), mask_of(b)));
+  });
+}
+
+int rq_mask_not(rq_ctx_t c, rq_mask_t a, rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    *out = wrap_mask(mask_not(ctx, mask_of(a)));
+  });
+}
+
 int rq_aggregate_all(rq_ctx_t c, rq_col_t data, int32_t fn, int32_t* out_dtype, int64_t* out_i64,
                      double* out_f64) {
   return api_guard([&] {

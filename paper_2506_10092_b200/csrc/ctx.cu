@@ -21,9 +21,47 @@ void cuda_fail(cudaError_t err, const char* what, const char* file, int line) {
                           ": " + what);
 }
 
+cudaEvent_t Ctx::get_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  RQ_CUDA_CHECK(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::collect_profile() {
+  if (pending.empty()) return;
+  RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
+  for (auto& p : pending) {
+    float ms = 0;
+    RQ_CUDA_CHECK(cudaEventElapsedTime(&ms, p.a, p.b));
+    bool found = false;
+    for (auto& kv : kstats) {
+      if (kv.first == p.tag) {
+        kv.second.ms += ms;
+        kv.second.count += 1;
+        found = true;
+        break;
+      }
+    }
+    if (!found) kstats.push_back({p.tag, KStat{ms, 1}});
+    event_pool.push_back(p.a);
+    event_pool.push_back(p.b);
+  }
+  pending.clear();
+}
+
 Ctx::~Ctx() {
   cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  for (auto& p : pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : event_pool) cudaEventDestroy(e);
   if (tile_status) cudaFree(tile_status);
   if (scratch) cudaFree(scratch);
   if (pinned) cudaFreeHost(pinned);
@@ -211,6 +249,33 @@ int rq_ctx_synchronize(rq_ctx_t c) {
 void* rq_ctx_stream(rq_ctx_t c) { return (c && c->ctx) ? c->ctx->stream : nullptr; }
 
 int64_t rq_ctx_launches(rq_ctx_t c) { return (c && c->ctx) ? c->ctx->launches : -1; }
+
+int rq_ctx_set_profiling(rq_ctx_t c, int32_t enable) {
+  return api_guard([&] {
+    auto ctx = get_ctx(c);
+    ctx->collect_profile();
+    ctx->profiling = enable != 0;
+  });
+}
+
+int rq_ctx_profile_report(rq_ctx_t c, int32_t reset, char* buf, int64_t cap) {
+  return api_guard([&] {
+    auto ctx = get_ctx(c);
+    ctx->collect_profile();
+    std::string out = "{";
+    bool first = true;
+    for (auto& kv : ctx->kstats) {
+      if (!first) out += ",";
+      first = false;
+      out += "\"" + kv.first + "\":{\"ms\":" + std::to_string(kv.second.ms) +
+             ",\"count\":" + std::to_string(kv.second.count) + "}";
+    }
+    out += "}";
+    if (reset) ctx->kstats.clear();
+    require(buf != nullptr && cap > static_cast<int64_t>(out.size()), "profile report buffer too small");
+    std::memcpy(buf, out.c_str(), out.size() + 1);
+  });
+}
 
 // ---- arrays ---------------------------------------------------------------------
 

@@ -301,6 +301,27 @@ __device__ __forceinline__ int64_t warp_merge_path(const int64_t* __restrict__ A
   return lo + __popc(__ballot_sync(FULL, pred));
 }
 
+// Warp-cooperative 32-ary lower_bound (first index with a[i] >= key).
+__device__ __forceinline__ int64_t warp_lower_bound(const int64_t* __restrict__ a, int64_t n,
+                                                    int64_t key) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    int64_t x = lo + (static_cast<int64_t>(lane) + 1) * step - 1;
+    if (x > hi - 1) x = hi - 1;
+    const bool pred = __ldg(reinterpret_cast<const long long*>(a) + x) < key;
+    const int c = __popc(__ballot_sync(FULL, pred));
+    const int64_t nlo = c == 0 ? lo : __shfl_sync(FULL, x, c - 1) + 1;
+    const int64_t nhi = c == 32 ? hi : __shfl_sync(FULL, x, c);
+    lo = nlo;
+    hi = nhi;
+  }
+  const int64_t x = lo + lane;
+  const bool pred = x < hi && __ldg(reinterpret_cast<const long long*>(a) + x) < key;
+  return lo + __popc(__ballot_sync(FULL, pred));
+}
+
 // upper_bound / lower_bound over a sorted global int64 array
 __device__ __forceinline__ int64_t upper_bound_g(const int64_t* __restrict__ a, int64_t n,
                                                  int64_t x) {

@@ -180,6 +180,19 @@ __global__ void k_bytes_and(const uint8_t* __restrict__ a, const uint8_t* __rest
     out[i] = (a[i] && b[i]) ? 1 : 0;
 }
 
+__global__ void k_bytes_or(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t n,
+                           uint8_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = (a[i] || b[i]) ? 1 : 0;
+}
+
+__global__ void k_bytes_not(const uint8_t* __restrict__ a, int64_t n, uint8_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = a[i] ? 0 : 1;
+}
+
 __global__ void k_set_bits(uint8_t* __restrict__ bits, const int64_t* __restrict__ p, int64_t n) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -380,6 +393,23 @@ DArr bytes_and(const CtxPtr& ctx, const DArr& a, const DArr& b) {
   DArr out = alloc_arr(ctx, RQ_I8, a.n);
   if (a.n == 0) return out;
   dev::k_bytes_and<<<grid_for(ctx, a.n), 256, 0, ctx->stream>>>(a.as<uint8_t>(), b.as<uint8_t>(), a.n, out.as<uint8_t>());
+  check_launch(ctx);
+  return out;
+}
+
+DArr bytes_or(const CtxPtr& ctx, const DArr& a, const DArr& b) {
+  require(a.n == b.n, "or: length mismatch");
+  DArr out = alloc_arr(ctx, RQ_I8, a.n);
+  if (a.n == 0) return out;
+  dev::k_bytes_or<<<grid_for(ctx, a.n), 256, 0, ctx->stream>>>(a.as<uint8_t>(), b.as<uint8_t>(), a.n, out.as<uint8_t>());
+  check_launch(ctx);
+  return out;
+}
+
+DArr bytes_not(const CtxPtr& ctx, const DArr& a) {
+  DArr out = alloc_arr(ctx, RQ_I8, a.n);
+  if (a.n == 0) return out;
+  dev::k_bytes_not<<<grid_for(ctx, a.n), 256, 0, ctx->stream>>>(a.as<uint8_t>(), a.n, out.as<uint8_t>());
   check_launch(ctx);
   return out;
 }

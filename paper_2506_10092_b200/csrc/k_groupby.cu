@@ -480,9 +480,4 @@ AggOut filtered_aggregate_binop_chain(const CtxPtr& ctx, const DCol& c, Scalar k
   return aggregate_column(ctx, prod, fn);
 }
 
-AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int cmp,
-                                const DCol& a, const DCol& b, int op, int fn) {
-  return filtered_aggregate_binop_chain(ctx, c, k, cmp, a, b, op, fn);
-}
-
 }  // namespace rqb

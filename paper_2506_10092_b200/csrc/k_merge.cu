@@ -102,19 +102,23 @@ DArr merge_partition(const CtxPtr& ctx, const int64_t* A, int64_t na, const int6
 
 template <class Policy>
 int64_t merge_select(const CtxPtr& ctx, const int64_t* A, int64_t na, const int64_t* B,
-                     int64_t nb, const Policy& pol) {
+                     int64_t nb, const Policy& pol, const char* tag) {
   if (na + nb == 0) return 0;
-  int64_t ntiles = 0;
-  DArr part = merge_partition(ctx, A, na, B, nb, MTILE, ntiles);
-  dev::MergeArgs m{A, na, B, nb, part.as<int64_t>()};
-  dev::LookBack lb{ctx->tile_status, 0};
-  lb.epoch = ctx->next_epoch(ntiles);
+  int64_t ntiles = (na + nb + MTILE - 1) / MTILE;
+  dev::LookBack lb{nullptr, ctx->next_epoch(ntiles)};
   lb.status = ctx->tile_status;
-  int64_t* count = part.as<int64_t>() + ntiles + 1;
-  dev::k_merge_select<MB, MI, Policy>
-      <<<static_cast<unsigned>(ntiles), MB, 0, ctx->stream>>>(m, pol, lb, count);
-  ctx->count_launch();
-  RQ_CUDA_CHECK(cudaGetLastError());
+  DArr part;
+  int64_t* count;
+  {
+    KTimer timer(ctx, tag);
+    part = merge_partition(ctx, A, na, B, nb, MTILE, ntiles);
+    dev::MergeArgs m{A, na, B, nb, part.as<int64_t>()};
+    count = part.as<int64_t>() + ntiles + 1;
+    dev::k_merge_select<MB, MI, Policy>
+        <<<static_cast<unsigned>(ntiles), MB, 0, ctx->stream>>>(m, pol, lb, count);
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
   return *ctx->readback(count, 8);
 }
 
@@ -141,7 +145,7 @@ Intersection range_intersect(const CtxPtr& ctx, const DArr& s1, const DArr& e1, 
                            out.s.as<int64_t>(), out.e.as<int64_t>(),
                            want_idx1 ? out.idx1.as<int64_t>() : nullptr,
                            want_idx2 ? out.idx2.as<int64_t>() : nullptr};
-  const int64_t n = (s1.n == 0 || s2.n == 0) ? 0 : merge_select(ctx, e1.pos(), e1.n, e2.pos(), e2.n, pol);
+  const int64_t n = (s1.n == 0 || s2.n == 0) ? 0 : merge_select(ctx, e1.pos(), e1.n, e2.pos(), e2.n, pol, "range_intersect");
   set_len(out.s, n);
   set_len(out.e, n);
   if (want_idx1) set_len(out.idx1, n);
@@ -177,7 +181,7 @@ PointsInRuns points_in_runs(const CtxPtr& ctx, const DArr& p, const DArr& s, con
       n = *ctx->readback(cnt.raw(), 8);
     } else {
       dev::PointsInRunsPolicy pol{s.pos(), s.n, po, ro, io};
-      n = merge_select(ctx, p.pos(), p.n, e.pos(), e.n, pol);
+      n = merge_select(ctx, p.pos(), p.n, e.pos(), e.n, pol, "points_in_runs");
     }
   }
   set_len(out.p_out, n);
@@ -198,7 +202,7 @@ PointsIntersect points_intersect(const CtxPtr& ctx, const DArr& p1, const DArr& 
     dev::PointsEqPolicy pol{p2.pos(), p2.n, out.p_out.as<int64_t>(),
                             want_idx1 ? out.idx1.as<int64_t>() : nullptr,
                             want_idx2 ? out.idx2.as<int64_t>() : nullptr};
-    n = merge_select(ctx, p1.pos(), p1.n, p2.pos(), p2.n, pol);
+    n = merge_select(ctx, p1.pos(), p1.n, p2.pos(), p2.n, pol, "points_intersect");
   }
   set_len(out.p_out, n);
   if (want_idx1) set_len(out.idx1, n);
@@ -222,7 +226,7 @@ void merge_disjoint(const CtxPtr& ctx, const DArr& kA, const DArr* eA, const DAr
                            vA ? dt_width(vA->dt) : 8, k_out.as<int64_t>(),
                            e_out ? e_out->as<int64_t>() : nullptr,
                            v_out ? v_out->raw_mut() : nullptr};
-  const int64_t got = merge_select(ctx, kA.pos(), kA.n, kB.pos(), kB.n, pol);
+  const int64_t got = merge_select(ctx, kA.pos(), kA.n, kB.pos(), kB.n, pol, "merge_disjoint");
   require(got == n, "merge_disjoint: count mismatch");
 }
 
@@ -230,8 +234,26 @@ DArr union_points(const CtxPtr& ctx, const DArr& p1, const DArr& p2) {
   DArr out = alloc_arr(ctx, RQ_I64, p1.n + p2.n);
   if (p1.n + p2.n == 0) return out;
   dev::UnionPolicy pol{p1.pos(), out.as<int64_t>()};
-  const int64_t n = merge_select(ctx, p1.pos(), p1.n, p2.pos(), p2.n, pol);
+  const int64_t n = merge_select(ctx, p1.pos(), p1.n, p2.pos(), p2.n, pol, "union_points");
   set_len(out, n);
+  return out;
+}
+
+DArr points_not_in_runs(const CtxPtr& ctx, const DArr& p, const DArr& s, const DArr& e) {
+  DArr out = alloc_arr(ctx, RQ_I64, p.n);
+  if (p.n == 0) return out;
+  if (s.n == 0) return copy_prefix(ctx, p, p.n);
+  dev::PointsNotInRunsPolicy pol{s.pos(), s.n, out.as<int64_t>()};
+  const int64_t n = merge_select(ctx, p.pos(), p.n, e.pos(), e.n, pol, "points_not_in_runs");
+  set_len(out, n);
+  return out;
+}
+
+DArr merge_keys(const CtxPtr& ctx, const DArr& a, const DArr& b) {
+  DArr out = alloc_arr(ctx, RQ_I64, a.n + b.n);
+  if (a.n + b.n == 0) return out;
+  dev::MergeKeysPolicy pol{out.as<int64_t>()};
+  merge_select(ctx, a.pos(), a.n, b.pos(), b.n, pol, "merge_keys");
   return out;
 }
 

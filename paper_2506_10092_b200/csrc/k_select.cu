@@ -144,6 +144,47 @@ struct MaskFall {
   __device__ __forceinline__ void emit(int64_t o, int64_t i) const { out[o] = i; }
 };
 
+// complement_rle / complement_index (primitives.cpp:141-167): candidate gap i
+// in [0, n] spans [e_{i-1} + 1, s_i - 1] (with e_{-1} = -1, s_n = total);
+// kept when non-empty and inside [0, total).
+struct ComplementGaps {
+  const int64_t *s, *e;
+  int64_t n, total;
+  int64_t *s_out, *e_out;
+  __device__ __forceinline__ int64_t cs(int64_t i) const { return i == 0 ? 0 : ldg64(e, i - 1) + 1; }
+  __device__ __forceinline__ int64_t ce(int64_t i) const { return i == n ? total - 1 : ldg64(s, i) - 1; }
+  __device__ __forceinline__ bool flag(int64_t i) const {
+    const int64_t a = cs(i), b = ce(i);
+    return a <= b && a < total && b >= 0;
+  }
+  __device__ __forceinline__ void emit(int64_t o, int64_t i) const {
+    s_out[o] = cs(i);
+    e_out[o] = ce(i);
+  }
+};
+
+// range_union (primitives.cpp:102-123) over the independently merged start
+// list S and end list E: the reference pairs the k-th start with the k-th
+// end and breaks where S[i] > running max end + 1; E is sorted, so the
+// running max of E[0..i-1] is E[i-1].
+struct UnionStart {
+  const int64_t *S, *E;
+  int64_t* out;
+  __device__ __forceinline__ bool flag(int64_t i) const {
+    return i == 0 || ldg64(S, i) > ldg64(E, i - 1) + 1;
+  }
+  __device__ __forceinline__ void emit(int64_t o, int64_t i) const { out[o] = ldg64(S, i); }
+};
+struct UnionEnd {
+  const int64_t *S, *E;
+  int64_t n;
+  int64_t* out;
+  __device__ __forceinline__ bool flag(int64_t i) const {
+    return i == n - 1 || ldg64(S, i + 1) > ldg64(E, i) + 1;
+  }
+  __device__ __forceinline__ void emit(int64_t o, int64_t i) const { out[o] = ldg64(E, i); }
+};
+
 // ---- reductions over runs / bytes ----------------------------------------------------
 
 template <int BLOCK>
@@ -376,6 +417,28 @@ void plain_mask_to_rle(const CtxPtr& ctx, const DArr& bits, DArr& s, DArr& e) {
   require(ns == ne, "plain_mask_to_rle: start/end count mismatch");
   set_len(s, ns);
   set_len(e, ne);
+}
+
+void complement_runs(const CtxPtr& ctx, const DArr& s, const DArr& e, int64_t total, DArr& s_out,
+                     DArr& e_out) {
+  s_out = alloc_arr(ctx, RQ_I64, s.n + 1);
+  e_out = alloc_arr(ctx, RQ_I64, s.n + 1);
+  dev::ComplementGaps pol{s.pos(), e.pos(), s.n, total, s_out.as<int64_t>(), e_out.as<int64_t>()};
+  const int64_t n = run_select(ctx, s.n + 1, pol);
+  set_len(s_out, n);
+  set_len(e_out, n);
+}
+
+void union_from_merged(const CtxPtr& ctx, const DArr& S, const DArr& E, DArr& s_out, DArr& e_out) {
+  s_out = alloc_arr(ctx, RQ_I64, S.n);
+  e_out = alloc_arr(ctx, RQ_I64, S.n);
+  dev::UnionStart us{S.pos(), E.pos(), s_out.as<int64_t>()};
+  dev::UnionEnd ue{S.pos(), E.pos(), S.n, e_out.as<int64_t>()};
+  const int64_t ns = run_select(ctx, S.n, us);
+  const int64_t ne = run_select(ctx, S.n, ue);
+  require(ns == ne, "range_union: start/end count mismatch");
+  set_len(s_out, ns);
+  set_len(e_out, ne);
 }
 
 DArr plain_mask_to_index(const CtxPtr& ctx, const DArr& bits) {

@@ -226,6 +226,30 @@ struct MergeEmitPolicy {
   }
 };
 
+// Points NOT inside any run (subtract_runs, mask_ops.cpp:94-108): A = points,
+// B = run ends; complement of PointsInRunsPolicy's test.
+struct PointsNotInRunsPolicy {
+  const int64_t* s;
+  int64_t nr;
+  int64_t* p_out;
+  __device__ __forceinline__ bool test(int64_t, int64_t j, bool takeA, int64_t key) const {
+    return takeA && !(j < nr && ldg64(s, j) <= key);
+  }
+  __device__ __forceinline__ void emit(int64_t o, int64_t, int64_t, bool, int64_t key) const {
+    p_out[o] = key;
+  }
+};
+
+// Merge of two sorted lists keeping duplicates (range_union's std::merge of
+// the start lists and of the end lists, primitives.cpp:107-110).
+struct MergeKeysPolicy {
+  int64_t* out;
+  __device__ __forceinline__ bool test(int64_t, int64_t, bool, int64_t) const { return true; }
+  __device__ __forceinline__ void emit(int64_t o, int64_t, int64_t, bool, int64_t key) const {
+    out[o] = key;
+  }
+};
+
 // Sorted de-duplicated union of two strictly increasing position lists
 // (merge_sorted_idx / concat_sort_idx, primitives.cpp:125-139 — both give the
 // same list). Ties take A first, so a B step equal to the last A key is a

@@ -725,16 +725,112 @@ DMask mask_and(const CtxPtr& ctx, const DMask& m1, const DMask& m2) {  // mask_o
   return and_index_index(ctx, m1, m2);
 }
 
-// OR for the encoding pairs the path produces when recombining distributed
-// parts (combine_disjoint_masks → masks::or_mask, mask_ops.cpp:211-237).
-// The full OR/NOT algebra is the next §8(f) row.
-DMask mask_or(const CtxPtr& ctx, const DMask& m1, const DMask& m2) {
+namespace {
+
+DMask or_rle_rle(const CtxPtr& ctx, const DMask& a, const DMask& b) {  // mask_ops.cpp:66-69
+  // range_union (primitives.cpp:102-123): merge starts and ends separately
+  DArr S = merge_keys(ctx, a.s, b.s);
+  DArr E = merge_keys(ctx, a.e, b.e);
+  DMask m = make_rle_mask(DArr{}, DArr{}, a.total);
+  if (S.n) union_from_merged(ctx, S, E, m.s, m.e);
+  return m;
+}
+
+DMask or_rle_plain(const CtxPtr& ctx, const DMask& rle, const DMask& plain) {  // :93-96
+  if (rle_mask_sparse(ctx, rle))
+    return or_plain_index(ctx, plain, make_index_mask(rle_mask_positions(ctx, rle.s, rle.e), rle.total));
+  return make_plain_mask(bytes_or(ctx, rle_mask_bits(ctx, rle.s, rle.e, rle.total), plain.bits));
+}
+
+// points of idx not covered by rle; keeps composite parts disjoint (:98-111)
+DMask subtract_runs(const CtxPtr& ctx, const DMask& idx, const DMask& rle) {
+  return make_index_mask(points_not_in_runs(ctx, idx.p, rle.s, rle.e), idx.total);
+}
+
+DMask composite_of(DMask runs, DMask pts) {
+  DMask c;
+  c.enc = RQ_MASK_COMPOSITE;
+  c.total = runs.total;
+  c.s = runs.s;
+  c.e = runs.e;
+  c.p = pts.p;
+  return c;
+}
+
+void mask_parts(const DMask& m, DMask& runs, DMask& pts) {  // as_parts (:120-133)
+  if (m.enc == RQ_MASK_RLE) {
+    runs = m;
+    pts = make_index_mask(DArr{}, m.total);
+  } else if (m.enc == RQ_MASK_INDEX) {
+    runs = make_rle_mask(DArr{}, DArr{}, m.total);
+    pts = m;
+  } else if (m.enc == RQ_MASK_COMPOSITE) {
+    runs = rle_mask_part(m);
+    pts = index_mask_part(m);
+  } else {
+    fail("as_parts: plain mask has no positional parts");
+  }
+}
+
+DMask or_composite(const CtxPtr& ctx, const DMask& a, const DMask& b) {  // :160-165
+  DMask ra, pa, rb, pb;
+  mask_parts(a, ra, pa);
+  mask_parts(b, rb, pb);
+  DMask runs = or_rle_rle(ctx, ra, rb);
+  DMask pts = subtract_runs(ctx, or_index_index(ctx, pa, pb), runs);
+  return composite_of(runs, pts);
+}
+
+DMask or_composite_plain(const CtxPtr& ctx, const DMask& c, const DMask& plain) {  // :177-180
+  DMask with_runs = or_rle_plain(ctx, rle_mask_part(c), plain);
+  return or_plain_index(ctx, with_runs, index_mask_part(c));
+}
+
+}  // namespace
+
+DMask mask_or(const CtxPtr& ctx, const DMask& m1, const DMask& m2) {  // mask_ops.cpp:211-237
   require(m1.total == m2.total, "or_mask: total_size mismatch");
   const int e1 = m1.enc, e2 = m2.enc;
-  if (e1 == RQ_MASK_INDEX && e2 == RQ_MASK_INDEX) return or_index_index(ctx, m1, m2);
+  if (e1 == RQ_MASK_COMPOSITE || e2 == RQ_MASK_COMPOSITE) {
+    if (e1 == RQ_MASK_PLAIN) return or_composite_plain(ctx, m2, m1);
+    if (e2 == RQ_MASK_PLAIN) return or_composite_plain(ctx, m1, m2);
+    return or_composite(ctx, m1, m2);
+  }
+  if (e1 == RQ_MASK_RLE && e2 == RQ_MASK_RLE) return or_rle_rle(ctx, m1, m2);
+  if (e1 == RQ_MASK_RLE && e2 == RQ_MASK_PLAIN) return or_rle_plain(ctx, m1, m2);
+  if (e1 == RQ_MASK_PLAIN && e2 == RQ_MASK_RLE) return or_rle_plain(ctx, m2, m1);
+  if (e1 == RQ_MASK_RLE && e2 == RQ_MASK_INDEX) return composite_of(m1, subtract_runs(ctx, m2, m1));
+  if (e1 == RQ_MASK_INDEX && e2 == RQ_MASK_RLE) return composite_of(m2, subtract_runs(ctx, m1, m2));
+  if (e1 == RQ_MASK_PLAIN && e2 == RQ_MASK_PLAIN)
+    return make_plain_mask(bytes_or(ctx, m1.bits, m2.bits));
   if (e1 == RQ_MASK_PLAIN && e2 == RQ_MASK_INDEX) return or_plain_index(ctx, m1, m2);
   if (e1 == RQ_MASK_INDEX && e2 == RQ_MASK_PLAIN) return or_plain_index(ctx, m2, m1);
-  fail("or_mask: encoding pair not supported on the device path yet", RQ_INVALID);
+  return or_index_index(ctx, m1, m2);
+}
+
+DMask mask_not(const CtxPtr& ctx, const DMask& m) {  // mask_ops.cpp:239-265
+  switch (m.enc) {
+    case RQ_MASK_PLAIN:
+      return make_plain_mask(bytes_not(ctx, m.bits));
+    case RQ_MASK_RLE: {
+      DMask r = make_rle_mask(DArr{}, DArr{}, m.total);
+      complement_runs(ctx, m.s, m.e, m.total, r.s, r.e);
+      return r;
+    }
+    case RQ_MASK_INDEX: {
+      DMask r = make_rle_mask(DArr{}, DArr{}, m.total);
+      complement_runs(ctx, m.p, m.p, m.total, r.s, r.e);
+      return r;
+    }
+    default: {
+      // ~(runs | points) = ~runs & ~points; both complements are RLE
+      DArr rs, re, ps, pe;
+      complement_runs(ctx, m.s, m.e, m.total, rs, re);
+      complement_runs(ctx, m.p, m.p, m.total, ps, pe);
+      Intersection r = range_intersect(ctx, rs, re, ps, pe, false, false);
+      return make_rle_mask(r.s, r.e, m.total);
+    }
+  }
 }
 
 DCol normalize_basic(const CtxPtr& ctx, const DCol& c) {  // align.cpp:102-115

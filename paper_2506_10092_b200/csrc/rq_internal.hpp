@@ -77,6 +77,22 @@ struct Ctx {
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
 
+  // per-kernel CUDA-event timing (rq_ctx_set_profiling / rq_ctx_profile_report)
+  bool profiling = false;
+  struct Pending {
+    std::string tag;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  struct KStat {
+    double ms = 0;
+    int64_t count = 0;
+  };
+  std::vector<std::pair<std::string, KStat>> kstats;
+  cudaEvent_t get_event();
+  void collect_profile();
+
   ~Ctx();
   void* alloc(size_t bytes);
   void free(void* p);
@@ -90,6 +106,27 @@ struct Ctx {
 };
 
 using CtxPtr = std::shared_ptr<Ctx>;
+
+// Brackets the kernel launches issued in its scope with CUDA events on the
+// context stream when profiling is enabled (no-op otherwise).
+struct KTimer {
+  Ctx* c;
+  const char* tag;
+  cudaEvent_t a = nullptr;
+  KTimer(const CtxPtr& ctx, const char* t) : c(ctx.get()), tag(t) {
+    if (c->profiling) {
+      a = c->get_event();
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~KTimer() {
+    if (a) {
+      cudaEvent_t b = c->get_event();
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({tag, a, b});
+    }
+  }
+};
 
 // ---- buffers and arrays ----------------------------------------------------------
 
@@ -232,7 +269,18 @@ void merge_disjoint(const CtxPtr& ctx, const DArr& kA, const DArr* eA, const DAr
                     DArr* v_out);
 // sorted de-duplicated union of two position lists
 DArr union_points(const CtxPtr& ctx, const DArr& p1, const DArr& p2);
+// points of p not inside any run (subtract_runs)
+DArr points_not_in_runs(const CtxPtr& ctx, const DArr& p, const DArr& s, const DArr& e);
+// merge of two sorted lists keeping duplicates
+DArr merge_keys(const CtxPtr& ctx, const DArr& a, const DArr& b);
+// complement_rle / complement_index (primitives.cpp:141-167)
+void complement_runs(const CtxPtr& ctx, const DArr& s, const DArr& e, int64_t total, DArr& s_out,
+                     DArr& e_out);
+// range_union tail over merged starts / ends (primitives.cpp:102-123)
+void union_from_merged(const CtxPtr& ctx, const DArr& S, const DArr& E, DArr& s_out, DArr& e_out);
 // byte-mask helpers
+DArr bytes_or(const CtxPtr& ctx, const DArr& a, const DArr& b);
+DArr bytes_not(const CtxPtr& ctx, const DArr& a);
 DArr bytes_and(const CtxPtr& ctx, const DArr& a, const DArr& b);
 DArr bytes_copy01(const CtxPtr& ctx, const DArr& a);
 void set_bits(const CtxPtr& ctx, DArr& bits, const DArr& p);
@@ -306,6 +354,7 @@ DMask compare_scalar(const CtxPtr& ctx, const DCol& a, Scalar k, int op, bool re
 DCol filter(const CtxPtr& ctx, const DCol& a, const DMask& m);
 DMask mask_and(const CtxPtr& ctx, const DMask& a, const DMask& b);
 DMask mask_or(const CtxPtr& ctx, const DMask& a, const DMask& b);
+DMask mask_not(const CtxPtr& ctx, const DMask& a);
 DCol normalize_basic(const CtxPtr& ctx, const DCol& c);
 int64_t mask_true_count(const CtxPtr& ctx, const DMask& m);
 bool col_gapless(const CtxPtr& ctx, const DCol& c);

@@ -430,6 +430,26 @@ class masks:
         check(_L.rq_mask_and(ctx.handle, da.handle, db.handle, C.byref(o)))
         return _out(DeviceMask(o, ctx), host)
 
+    @staticmethod
+    def or_mask(a, b):
+        """masks::or_mask (mask_ops.cpp:211-237)."""
+        host = _is_host(a, b)
+        ctx = _ctx_of(a, b)
+        da, db = upload(a, ctx), upload(b, ctx)
+        o = _new()
+        check(_L.rq_mask_or(ctx.handle, da.handle, db.handle, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
+    @staticmethod
+    def not_mask(a):
+        """masks::not_mask (mask_ops.cpp:239-265)."""
+        host = _is_host(a)
+        ctx = _ctx_of(a)
+        da = upload(a, ctx)
+        o = _new()
+        check(_L.rq_mask_not(ctx.handle, da.handle, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
 
 def _agg_result(dt, i, f):
     return float(f.value) if dt.value == H.F64 else int(i.value)

@@ -196,6 +196,18 @@ def test_mask_and_all_pairs(rq, ref, m1, m2):
         assert_mask(rq.masks.and_mask(a, b), ref.and_mask(a, b), f"inst{inst}")
 
 
+@pytest.mark.parametrize("m1", range(4))
+@pytest.mark.parametrize("m2", range(4))
+def test_mask_or_not_all_pairs(rq, ref, m1, m2):
+    rng = np.random.default_rng(90 + 4 * m1 + m2)
+    for inst in range(8):
+        n = int(rng.integers(1, 3000))
+        a = G.random_mask(rng, MENCS[m1], n)
+        b = G.random_mask(rng, MENCS[m2], n)
+        assert_mask(rq.masks.or_mask(a, b), ref.or_mask(a, b), f"or inst{inst}")
+        assert_mask(rq.masks.not_mask(a), ref.not_mask(a), f"not inst{inst}")
+
+
 @pytest.mark.parametrize("enc", range(5), ids=lambda e: ENC_NAMES[e])
 def test_aggregate_all_every_fn(rq, ref, enc):
     rng = np.random.default_rng(600 + enc)
