@@ -113,12 +113,15 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+_PINNED = []  # keeps pinned host tensors alive
+
+
 def pinned_copy(a: np.ndarray) -> np.ndarray:
     import torch
-    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    t = torch.empty(max(1, a.nbytes), dtype=torch.uint8, pin_memory=True)
+    _PINNED.append(t)
     out = t.numpy().view(a.dtype)[: a.shape[0]]
     out[:] = a
-    out._pin_owner = t  # noqa: keep the pinned tensor alive
     return out
 
 
