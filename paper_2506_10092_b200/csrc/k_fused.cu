@@ -7,15 +7,27 @@
 // materialising the mask, two filtered columns and the product. With A RLE
 // and B Index, every surviving slot is a point p of B with C(p) passing and
 // A covering p, so the whole chain is
-//   Σ_{p ∈ B, pred(C(p)), p ∈ cover(A)} op(A(p), B(p))
-// and one merge-path walk over (B points, A run ends) computes it. C's runs
-// overlapping a tile's position range are staged in shared memory (range
-// located by a warp-cooperative search in the partition pass), so C is read
-// once too; a narrow-plain C is decoded inline at each point. Integer sums
-// wrap exactly as the chain's int64 arithmetic; f64 within tolerance.
+//   Σ_{p ∈ B, pred(C(p)), p ∈ cover(A)} op(A(p), B(p)).
+//
+// Points-driven single pass: B's points are cut into fixed tiles
+// (BLOCK×ITEMS points); a partition pass locates, per tile boundary, the
+// first A run and first C run that can contain the boundary point (one
+// warp-cooperative 32-ary search each). Each CTA stages its tile's A-run-end
+// window and C window (ends + predicate flag, evaluated once per run) in
+// shared memory with coalesced loads; every lane then takes one point per
+// round (striped → coalesced point/value loads) and resolves it with a
+// branchless binary search in shared memory — uniform trip counts, no
+// divergence, no global-latency chains. Windows larger than the staging
+// capacity fall back to a global binary search inside the window. Every byte
+// of A's run ends, B's points and C's runs comes from HBM once; A's values
+// are gathered only for covered points. (A merge-path walk over all run ends
+// measured issue-bound here: most steps were run ends with no output.)
+// Integer sums wrap exactly like the chain's int64 arithmetic; f64 within
+// tolerance.
+#include <cstdlib>
 #include <limits>
 
-#include "merge_walk.cuh"
+#include "device_common.cuh"
 #include "rq_internal.hpp"
 
 namespace rqb {
@@ -44,132 +56,310 @@ struct CSpec {
   int k_float;
   int64_t ki;
   double kf;
+  int opmask;  // bit c set: comparison holds for outcome class c (<, ==, >)
 };
 
-template <class T>
-__device__ __forceinline__ bool c_pass(const CSpec& c, T x) {
-  const T k = c.k_float ? static_cast<T>(c.kf) : static_cast<T>(c.ki);
-  return cmp_t<T>(x, k, c.cmp);
+inline int cmp_opmask(int cmp) {
+  switch (cmp) {
+    case RQ_LT: return 0b001;
+    case RQ_LE: return 0b011;
+    case RQ_EQ: return 0b010;
+    case RQ_NE: return 0b101;
+    case RQ_GE: return 0b110;
+    default: return 0b100;  // GT
+  }
 }
 
-__device__ __forceinline__ bool c_value_pass(const CSpec& c, int64_t idx) {
+struct XSpec {  // the RLE data column
+  const int64_t* s;
+  const int64_t* e;
+  const void* v;
+  int dt;
+  int64_t n;
+  int gapless;
+};
+
+__device__ __forceinline__ int64_t ld_i64_hot(const void* p, int dt, int64_t i) {
+  return dt == RQ_I64 ? ldg64(static_cast<const int64_t*>(p), i) : ld_i64(p, dt, i);
+}
+__device__ __forceinline__ double ld_f64_hot(const void* p, int dt, int64_t i) {
+  return dt == RQ_F64 ? __ldg(static_cast<const double*>(p) + i) : ld_f64(p, dt, i);
+}
+template <class T>
+__device__ __forceinline__ T ld_hot(const void* p, int dt, int64_t i);
+template <>
+__device__ __forceinline__ int64_t ld_hot<int64_t>(const void* p, int dt, int64_t i) {
+  return ld_i64_hot(p, dt, i);
+}
+template <>
+__device__ __forceinline__ double ld_hot<double>(const void* p, int dt, int64_t i) {
+  return ld_f64_hot(p, dt, i);
+}
+
+// Branch-free predicate: outcome class (0: x<k, 1: x==k, 2: x>k) selects a
+// bit of the comparison's 3-bit truth mask (cmp_opmask on the host).
+__device__ __forceinline__ bool c_run_pass(const CSpec& c, int64_t idx) {
+  int cls;
   if (c.k_float || dt_is_float_dev(c.dt)) {
     const double x = ld_f64(c.v, c.dt, idx);
     const double k = c.k_float ? c.kf : static_cast<double>(c.ki);
-    return cmp_t<double>(x, k, c.cmp);
+    if (x != x || k != k) return c.cmp == RQ_NE;  // NaN: only != holds
+    cls = x < k ? 0 : (x == k ? 1 : 2);
+  } else {
+    const int64_t x = ld_i64_hot(c.v, c.dt, idx);
+    cls = x < c.ki ? 0 : (x == c.ki ? 1 : 2);
   }
-  return cmp_t<int64_t>(ld_i64(c.v, c.dt, idx), c.ki, c.cmp);
+  return (c.opmask >> cls) & 1;
 }
 
 __device__ __forceinline__ bool c_plain_pass(const CSpec& c, int64_t row) {
   int64_t x = wrap_to(c.logical, ld_i64(c.v, c.dt, row));
   if (c.has_center)
     x = wrap_to(c.logical, static_cast<int64_t>(static_cast<uint64_t>(x) + static_cast<uint64_t>(c.center)));
-  return cmp_t<int64_t>(x, c.ki, c.cmp);
+  const int cls = x < c.ki ? 0 : (x == c.ki ? 1 : 2);
+  return (c.opmask >> cls) & 1;
 }
 
-// partition: merge split of (points P, run ends E) at each tile boundary,
-// plus the first C run whose end >= the tile's first point.
-__global__ void k_fused_partition(const int64_t* __restrict__ P, int64_t np,
-                                  const int64_t* __restrict__ E, int64_t ne, int64_t tile,
-                                  int64_t nparts, const int64_t* __restrict__ ce, int64_t nc,
-                                  int64_t* __restrict__ part, int64_t* __restrict__ cpart) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (w >= nparts) return;
-  int64_t diag = w * tile;
-  if (diag > np + ne) diag = np + ne;
-  const int64_t i = warp_merge_path(P, np, E, ne, diag);
-  int64_t c = nc;
-  if (ce != nullptr && i < np) c = warp_lower_bound(ce, nc, __ldg(reinterpret_cast<const long long*>(P) + i));
-  if ((threadIdx.x & 31) == 0) {
-    part[w] = i;
-    if (cpart) cpart[w] = c;
+// first index in [lo, hi) with e[idx] >= key (hi if none)
+__device__ __forceinline__ int64_t lb_window(const int64_t* __restrict__ e, int64_t lo, int64_t hi,
+                                             int64_t key) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ldg64(e, mid) < key) lo = mid + 1;
+    else hi = mid;
   }
+  return lo;
 }
 
-template <int BLOCK, int ITEMS, int CCAP, class T, bool X_GAPLESS, int CK>
+// Advances cursor r (e[r] >= previous point) to the first run with e >= key:
+// a few linear steps, then a binary search for long jumps.
+__device__ __forceinline__ int64_t advance(const int64_t* __restrict__ e, int64_t r, int64_t hi,
+                                           int64_t key) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (r >= hi || ldg64(e, r) >= key) return r;
+    ++r;
+  }
+  return lb_window(e, r, hi, key);
+}
+
+// tile boundary t: first A run and first C run with end >= P[t * tile]
+__global__ void k_points_partition(const int64_t* __restrict__ P, int64_t np, int64_t tile,
+                                   int64_t nparts, const int64_t* __restrict__ xe, int64_t nx,
+                                   const int64_t* __restrict__ ce, int64_t nc,
+                                   int64_t* __restrict__ apart, int64_t* __restrict__ cpart) {
+  // two warps per boundary: even warps search A's ends, odd warps C's ends
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t w = gw >> 1;
+  const bool is_c = gw & 1;
+  if (w >= nparts || (is_c && !ce)) return;  // warp-uniform
+  const int64_t q = w * tile;
+  int64_t r = is_c ? nc : nx;
+  if (q < np) r = is_c ? warp_lower_bound(ce, nc, ldg64(P, q)) : warp_lower_bound(xe, nx, ldg64(P, q));
+  if ((threadIdx.x & 31) == 0) (is_c ? cpart : apart)[w] = r;
+}
+
+template <class T, int OP>
+__device__ __forceinline__ T apply_op(T x, T y, int* err) {
+  return arith_t<T>(x, y, OP, err);
+}
+
+// Branchless lower_bound over a shared-memory window of 32-bit offsets,
+// fully unrolled over the power-of-two capacity CAP (log2(CAP) steps of
+// add / compare / load / select; identical trip count in every lane).
+// Entries at index >= len hold INT32_MAX, so no bounds test is needed.
+template <int CAP>
+__device__ __forceinline__ int smem_rank32(const int32_t* w, int32_t key) {
+  int pos = 0;  // number of entries < key found so far
+#pragma unroll
+  for (int step = CAP / 2; step > 0; step >>= 1) pos = (w[pos + step - 1] < key) ? pos + step : pos;
+  return pos + (w[pos] < key ? 1 : 0);
+}
+
+template <int BLOCK, int ITEMS, int ACAP, int CCAP, class T, int OP, int CK>
 __global__ void __launch_bounds__(BLOCK)
-    k_filtered_points_reduce(MergeArgs m, const int64_t* __restrict__ xs, const void* __restrict__ xv,
-                             int xdt, const void* __restrict__ yv, int ydt, CSpec c,
-                             const int64_t* __restrict__ cpart, int op, int swap,
+    k_points_filtered_reduce(const int64_t* __restrict__ P, const void* __restrict__ yv, int ydt,
+                             int64_t np, XSpec x, CSpec c, const int64_t* __restrict__ apart,
+                             const int64_t* __restrict__ cpart, int swap,
                              AggPart* __restrict__ parts, int* __restrict__ err) {
-  using Tile = MergeTile<BLOCK, ITEMS>;
-  __shared__ int64_t sk[Tile::TILE];
-  __shared__ int64_t c_e[CK == C_PLAIN ? 1 : CCAP];
-  __shared__ int64_t c_s[CK == C_RLE_GAPPED ? CCAP : 1];  // start, or INT64_MAX if failing
-  __shared__ uint8_t c_ok[CK == C_PLAIN ? 1 : CCAP];
-  Tile t;
+  constexpr int TILE = BLOCK * ITEMS;
+  static_assert((ACAP & (ACAP - 1)) == 0 && (CCAP & (CCAP - 1)) == 0, "power-of-two windows");
+  static_assert(BLOCK >= 128, "four partition warps");
+  __shared__ int32_t wa[ACAP];
+  __shared__ int32_t wc[CK == C_PLAIN ? 1 : CCAP];
+  __shared__ uint8_t wok[CK == C_PLAIN ? 1 : CCAP];
   const int tile = blockIdx.x;
-  int64_t c0 = 0, cn = 0;
+  const int64_t tbase = static_cast<int64_t>(tile) * TILE;
+  const int64_t tnext = tbase + TILE;
+  // positions inside the tile are stored as 32-bit offsets from its first
+  // point; valid when the tile spans < 2^31 - 1 rows (checked per tile)
+  const int64_t p0 = ldg64(P, tbase);
+  const int64_t tlast = (tnext < np ? tnext : np) - 1;
+  const bool narrow = ldg64(P, tlast) - p0 < INT32_MAX - 1;
+  // tile windows (from the partition pass): runs that may contain this
+  // tile's points
+  const int64_t a_lo = apart[tile];
+  int64_t a_hi = apart[tile + 1] + 1;
+  if (a_hi > x.n) a_hi = x.n;
+  const int64_t alen = a_hi > a_lo ? a_hi - a_lo : 0;
+  const bool a_staged = narrow && alen < ACAP;
+  // search length: the power of two above the window (uniform per CTA)
+  int la = 1;
+  while (la <= alen) la <<= 1;
+  int64_t c_lo = 0, clen = 0;
   bool c_staged = false;
+  int lc = 1;
   if (CK != C_PLAIN) {
-    c0 = cpart[tile];
-    int64_t c1 = cpart[tile + 1];
-    if (c1 >= c.n) c1 = c.n - 1;
-    cn = c1 - c0 + 1;
-    if (c0 >= c.n) cn = 0;
-    c_staged = cn <= CCAP;
-    if (c_staged) {
-      for (int64_t q = threadIdx.x; q < cn; q += BLOCK) {
-        c_e[q] = ldg64(c.e, c0 + q);
-        if (CK == C_RLE_GAPPED) c_s[q] = ldg64(c.s, c0 + q);
-        c_ok[q] = c_value_pass(c, c0 + q) ? 1 : 0;
+    c_lo = cpart[tile];
+    int64_t c_hi = cpart[tile + 1] + 1;
+    if (c_hi > c.n) c_hi = c.n;
+    clen = c_hi > c_lo ? c_hi - c_lo : 0;
+    c_staged = narrow && clen < CCAP;
+    while (lc <= clen) lc <<= 1;
+  }
+  // coalesced staging of the run windows as 32-bit offsets from p0 (C's
+  // predicate evaluated once per run); [len, L) padded with INT32_MAX. All
+  // loads of a thread are issued before any store.
+  static_assert(ACAP % BLOCK == 0 && CCAP % BLOCK == 0, "window capacity multiple of BLOCK");
+  constexpr int AU = ACAP / BLOCK, CU = CCAP / BLOCK;
+  const int64_t pad = p0 + INT32_MAX;
+  if (a_staged) {
+    int64_t t[AU];
+#pragma unroll
+    for (int u = 0; u < AU; ++u) {
+      const int q = u * BLOCK + threadIdx.x;
+      t[u] = q < alen ? ldg64(x.e, a_lo + q) : pad;
+    }
+#pragma unroll
+    for (int u = 0; u < AU; ++u) {
+      const int q = u * BLOCK + threadIdx.x;
+      if (q < la) wa[q] = static_cast<int32_t>(min(t[u] - p0, static_cast<int64_t>(INT32_MAX)));
+    }
+  }
+  if (CK != C_PLAIN && c_staged) {
+    int64_t te[CU];
+    bool tok[CU];
+#pragma unroll
+    for (int u = 0; u < CU; ++u) {
+      const int q = u * BLOCK + threadIdx.x;
+      te[u] = q < clen ? ldg64(c.e, c_lo + q) : pad;
+      tok[u] = q < clen && c_run_pass(c, c_lo + q);
+    }
+#pragma unroll
+    for (int u = 0; u < CU; ++u) {
+      const int q = u * BLOCK + threadIdx.x;
+      if (q < lc) {
+        wc[q] = static_cast<int32_t>(min(te[u] - p0, static_cast<int64_t>(INT32_MAX)));
+        wok[q] = tok[u] ? 1 : 0;
       }
     }
   }
-  t.load(m, tile, sk);  // includes __syncthreads()
+  __syncthreads();
 
   uint64_t isum = 0;
   double fsum = 0.0;
   int64_t cnt = 0;
   int lerr = 0;
-  int64_t ccur = -1;  // local C cursor (staged index or global index)
-  t.walk(sk, [&](int64_t i, int64_t j, bool takeP, int64_t p) {
-    if (!takeP) return;  // run-end step: nothing to emit
-    // A (RLE, "x") covers p?
-    if (j >= m.nb) return;
-    if (!X_GAPLESS && ldg64(xs, j) > p) return;
-    // predicate on C at p
+  // all ITEMS points of this lane first (independent coalesced loads) ...
+  int64_t pts[ITEMS];
+  int32_t key[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t q = tbase + k * BLOCK + threadIdx.x;  // striped: coalesced point loads
+    pts[k] = q < np ? ldg64(P, q) : INT64_MAX;
+    key[k] = static_cast<int32_t>(pts[k] - p0);  // used only when narrow
+  }
+  // ... then the shared-memory searches of every point advance in lockstep
+  // (2·ITEMS independent dependency chains per lane instead of serial ones)
+  int ra[ITEMS], rc[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) ra[k] = rc[k] = 0;
+  // search over [0, L) with L the window's power of two (trip count log2 L,
+  // uniform per CTA); both searches advance in the same step loop
+  const bool do_c = CK != C_PLAIN && c_staged;
+#pragma unroll
+  for (int step = (ACAP > CCAP ? ACAP : CCAP) / 2; step > 0; step >>= 1) {
+    if (a_staged && step < la) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) ra[k] = (wa[ra[k] + step - 1] < key[k]) ? ra[k] + step : ra[k];
+    }
+    if (do_c && step < lc) {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) rc[k] = (wc[rc[k] + step - 1] < key[k]) ? rc[k] + step : rc[k];
+    }
+  }
+  if (a_staged) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) ra[k] += wa[ra[k]] < key[k] ? 1 : 0;
+  }
+  if (do_c) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) rc[k] += wc[rc[k]] < key[k] ? 1 : 0;
+  }
+  // qualify every point (A covers it, C's run passes) ...
+  int64_t arun[ITEMS];
+  bool take[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t q = tbase + k * BLOCK + threadIdx.x;
+    const int64_t p = pts[k];
+    take[k] = false;
+    arun[k] = a_lo;
+    if (q >= np) continue;
+    const int64_t ar = a_staged ? a_lo + ra[k] : lb_window(x.e, a_lo, a_hi, p);
+    if (ar >= a_hi) continue;
+    if (!x.gapless && ldg64(x.s, ar) > p) continue;
     bool pass;
     if (CK == C_PLAIN) {
       pass = p < c.n && c_plain_pass(c, p);
     } else if (c_staged) {
-      if (ccur < 0) {  // first point of this thread: binary search the staged ends
-        int64_t lo = 0, hi = cn;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (c_e[mid] < p) lo = mid + 1;
-          else hi = mid;
-        }
-        ccur = lo;
-      }
-      while (ccur < cn && c_e[ccur] < p) ++ccur;
-      pass = ccur < cn && c_ok[ccur] && (CK == C_RLE_GAPLESS || c_s[ccur] <= p);
+      const int cr = rc[k];
+      pass = cr < clen && wok[cr] && (CK == C_RLE_GAPLESS || ldg64(c.s, c_lo + cr) <= p);
     } else {
-      if (ccur < 0) ccur = lower_bound_g(c.e, c.n, p);
-      while (ccur < c.n && ldg64(c.e, ccur) < p) ++ccur;
-      pass = ccur < c.n && (CK == C_RLE_GAPLESS || ldg64(c.s, ccur) <= p) && c_value_pass(c, ccur);
+      const int64_t cr = lb_window(c.e, c_lo, c_lo + clen, p);
+      pass = cr < c_lo + clen && (CK == C_RLE_GAPLESS || ldg64(c.s, cr) <= p) && c_run_pass(c, cr);
     }
-    if (!pass) return;
-    const T xa = ld_as<T>(xv, xdt, j);
-    const T yb = ld_as<T>(yv, ydt, i);
-    const T r = swap ? arith_t<T>(yb, xa, op, &lerr) : arith_t<T>(xa, yb, op, &lerr);
+    take[k] = pass;
+    arun[k] = ar;
+  }
+  // ... then gather both operands for all points at once (independent loads)
+  T xa[ITEMS], yb[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t q = tbase + k * BLOCK + threadIdx.x;
+    xa[k] = take[k] ? ld_hot<T>(x.v, x.dt, arun[k]) : T(0);
+    yb[k] = take[k] ? ld_hot<T>(yv, ydt, q) : T(0);
+  }
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    if (!take[k]) continue;
+    const T r = swap ? apply_op<T, OP>(yb[k], xa[k], &lerr) : apply_op<T, OP>(xa[k], yb[k], &lerr);
     isum += static_cast<uint64_t>(static_cast<int64_t>(r));
     fsum += static_cast<double>(r);
     ++cnt;
-  });
+  }
   if (lerr) atomicExch(err, 1);
-  // block reduction -> one partial per tile
-  __shared__ uint64_t ru[BLOCK / 32 + 1];
-  __shared__ double rf[BLOCK / 32 + 1];
-  const uint64_t bi = block_sum<BLOCK>(isum, ru);
-  const double bf = block_sum<BLOCK>(fsum, rf);
-  const uint64_t bc = block_sum<BLOCK>(static_cast<uint64_t>(cnt), ru);
+  // one block reduction of the three accumulators
+  __shared__ uint64_t ru[BLOCK / 32];
+  __shared__ double rf[BLOCK / 32];
+  __shared__ uint64_t rn[BLOCK / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  isum = warp_sum(isum);
+  fsum = warp_sum(fsum);
+  const uint64_t ucnt = warp_sum(static_cast<uint64_t>(cnt));
+  if (lane == 0) {
+    ru[wid] = isum;
+    rf[wid] = fsum;
+    rn[wid] = ucnt;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     AggPart pp{};
-    pp.isum = bi;
-    pp.fsum = bf;
-    pp.cnt = static_cast<long long>(bc);
+    for (int w = 0; w < BLOCK / 32; ++w) {
+      pp.isum += ru[w];
+      pp.fsum += rf[w];
+      pp.cnt += static_cast<long long>(rn[w]);
+    }
     parts[tile] = pp;
   }
 }
@@ -181,10 +371,27 @@ __global__ void __launch_bounds__(BLOCK)
   __shared__ double rf[BLOCK / 32 + 1];
   uint64_t isum = 0, cnt = 0;
   double fsum = 0.0;
-  for (int64_t q = threadIdx.x; q < n; q += BLOCK) {
-    isum += parts[q].isum;
-    fsum += parts[q].fsum;
-    cnt += static_cast<uint64_t>(parts[q].cnt);
+  // fixed-order strided fold; 8 partials per thread per batch so the loads
+  // of a batch are in flight together
+  constexpr int U = 8;
+  for (int64_t q0 = 0; q0 < n; q0 += static_cast<int64_t>(BLOCK) * U) {
+    unsigned long long bi[U];
+    double bf[U];
+    long long bc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + static_cast<int64_t>(u) * BLOCK + threadIdx.x;
+      const bool ok = q < n;
+      bi[u] = ok ? parts[q].isum : 0ull;
+      bf[u] = ok ? parts[q].fsum : 0.0;
+      bc[u] = ok ? parts[q].cnt : 0ll;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      isum += bi[u];
+      fsum += bf[u];
+      cnt += static_cast<uint64_t>(bc[u]);
+    }
   }
   isum = block_sum<BLOCK>(isum, ru);
   fsum = block_sum<BLOCK>(fsum, rf);
@@ -205,23 +412,57 @@ AggOut filtered_aggregate_binop_chain(const CtxPtr& ctx, const DCol& c, Scalar k
 
 namespace {
 
-constexpr int FB = 256, FI = 8, FCAP = 1024;
+constexpr int FB = 256, FI = 4, FACAP = 2048, FCCAP = 1024;
 
-template <class T, bool XG, int CK>
-void launch_fused(const CtxPtr& ctx, unsigned g, const dev::MergeArgs& m, const DCol& x, const DCol& y,
-                  const dev::CSpec& cs, const int64_t* cpart, int op, int swap, dev::AggPart* parts,
-                  int* err) {
-  dev::k_filtered_points_reduce<FB, FI, FCAP, T, XG, CK><<<g, FB, 0, ctx->stream>>>(
-      m, x.s.pos(), x.v.raw(), x.v.dt, y.v.raw(), y.v.dt, cs, cpart, op, swap, parts, err);
+struct FusedLaunch {
+  unsigned grid;
+  const DCol* y;
+  dev::XSpec xs;
+  dev::CSpec cs;
+  const int64_t* apart;
+  const int64_t* cpart;
+  int swap;
+  dev::AggPart* parts;
+  int* err;
+};
+
+// points per thread (tuning knob; RQ_FUSED_ITEMS=8 selects the 2048-point tile)
+int fused_items() {
+  static const int v = [] {
+    const char* s = std::getenv("RQ_FUSED_ITEMS");
+    return (s && std::atoi(s) == 8) ? 8 : FI;
+  }();
+  return v;
 }
 
-template <class T, bool XG>
-void launch_ck(int ck, const CtxPtr& ctx, unsigned g, const dev::MergeArgs& m, const DCol& x, const DCol& y,
-               const dev::CSpec& cs, const int64_t* cpart, int op, int swap, dev::AggPart* parts, int* err) {
+template <class T, int OP, int CK>
+void launch3(const CtxPtr& ctx, const FusedLaunch& f) {
+  if (fused_items() == 8)
+    dev::k_points_filtered_reduce<FB, 8, 2 * FACAP, FCCAP, T, OP, CK><<<f.grid, FB, 0, ctx->stream>>>(
+        f.y->p.pos(), f.y->v.raw(), f.y->v.dt, f.y->p.n, f.xs, f.cs, f.apart, f.cpart, f.swap, f.parts,
+        f.err);
+  else
+    dev::k_points_filtered_reduce<FB, FI, FACAP, FCCAP, T, OP, CK><<<f.grid, FB, 0, ctx->stream>>>(
+        f.y->p.pos(), f.y->v.raw(), f.y->v.dt, f.y->p.n, f.xs, f.cs, f.apart, f.cpart, f.swap, f.parts,
+        f.err);
+}
+
+template <class T, int OP>
+void launch2(int ck, const CtxPtr& ctx, const FusedLaunch& f) {
   switch (ck) {
-    case dev::C_RLE_GAPLESS: launch_fused<T, XG, dev::C_RLE_GAPLESS>(ctx, g, m, x, y, cs, cpart, op, swap, parts, err); break;
-    case dev::C_RLE_GAPPED: launch_fused<T, XG, dev::C_RLE_GAPPED>(ctx, g, m, x, y, cs, cpart, op, swap, parts, err); break;
-    default: launch_fused<T, XG, dev::C_PLAIN>(ctx, g, m, x, y, cs, cpart, op, swap, parts, err); break;
+    case dev::C_RLE_GAPLESS: launch3<T, OP, dev::C_RLE_GAPLESS>(ctx, f); break;
+    case dev::C_RLE_GAPPED: launch3<T, OP, dev::C_RLE_GAPPED>(ctx, f); break;
+    default: launch3<T, OP, dev::C_PLAIN>(ctx, f); break;
+  }
+}
+
+template <class T>
+void launch1(int op, int ck, const CtxPtr& ctx, const FusedLaunch& f) {
+  switch (op) {
+    case RQ_ADD: launch2<T, RQ_ADD>(ck, ctx, f); break;
+    case RQ_SUB: launch2<T, RQ_SUB>(ck, ctx, f); break;
+    case RQ_MUL: launch2<T, RQ_MUL>(ck, ctx, f); break;
+    default: launch2<T, RQ_DIV>(ck, ctx, f); break;
   }
 }
 
@@ -241,9 +482,7 @@ AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int 
 
   const DCol& x = a.enc == RQ_ENC_RLE ? a : b;  // runs
   const DCol& y = a.enc == RQ_ENC_RLE ? b : a;  // points
-  const int swap = a.enc == RQ_ENC_RLE ? 0 : 1;
   const bool flt = dt_float(x.v.dt) || dt_float(y.v.dt);
-  const bool xg = col_gapless(ctx, x);
   int ck = dev::C_PLAIN;
   if (c.enc == RQ_ENC_RLE) ck = col_gapless(ctx, c) ? dev::C_RLE_GAPLESS : dev::C_RLE_GAPPED;
 
@@ -260,48 +499,43 @@ AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int 
   cs.k_float = k.is_float ? 1 : 0;
   cs.ki = k.i;
   cs.kf = k.f;
+  cs.opmask = dev::cmp_opmask(cmp);
+  dev::XSpec xs{x.s.pos(), x.e.pos(), x.v.raw(), x.v.dt, x.e.n, col_gapless(ctx, x) ? 1 : 0};
 
-  const int64_t np = y.p.n, ne = x.e.n;
+  const int64_t np = y.p.n;
   dev::AggPart res{};
-  if (np > 0 && ne > 0 && cs.n > 0) {
-    constexpr int64_t TILE = FB * FI;
-    const int64_t ntiles = (np + ne + TILE - 1) / TILE;
-    DArr part = alloc_arr(ctx, RQ_I64, ntiles + 1);
+  if (np > 0 && xs.n > 0 && cs.n > 0) {
+    const int64_t TILE = static_cast<int64_t>(FB) * fused_items();
+    const int64_t ntiles = (np + TILE - 1) / TILE;
+    DArr apart = alloc_arr(ctx, RQ_I64, ntiles + 1);
     DArr cpart = alloc_arr(ctx, RQ_I64, ntiles + 1);
     DArr parts = alloc_arr(ctx, RQ_I64, ntiles * (sizeof(dev::AggPart) / 8));
-    DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8);
-    DArr err = alloc_arr(ctx, RQ_I32, 2);
-    RQ_CUDA_CHECK(cudaMemsetAsync(err.raw_mut(), 0, 8, ctx->stream));
+    DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8 + 1);
+    int* err = reinterpret_cast<int*>(out.as<int64_t>() + sizeof(dev::AggPart) / 8);
+    RQ_CUDA_CHECK(cudaMemsetAsync(err, 0, 8, ctx->stream));
     {
       KTimer timer(ctx, "filtered_points_reduce");
       const int64_t nparts = ntiles + 1;
-      dev::k_fused_partition<<<static_cast<unsigned>((nparts * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-          y.p.pos(), np, x.e.pos(), ne, TILE, nparts, ck == dev::C_PLAIN ? nullptr : c.e.pos(), cs.n,
-          part.as<int64_t>(), ck == dev::C_PLAIN ? nullptr : cpart.as<int64_t>());
+      dev::k_points_partition<<<static_cast<unsigned>((nparts * 64 + 255) / 256), 256, 0, ctx->stream>>>(
+          y.p.pos(), np, TILE, nparts, x.e.pos(), xs.n, ck == dev::C_PLAIN ? nullptr : c.e.pos(), cs.n,
+          apart.as<int64_t>(), ck == dev::C_PLAIN ? nullptr : cpart.as<int64_t>());
       ctx->count_launch();
       RQ_CUDA_CHECK(cudaGetLastError());
-      dev::MergeArgs m{y.p.pos(), np, x.e.pos(), ne, part.as<int64_t>()};
-      const unsigned g = static_cast<unsigned>(ntiles);
-      auto* P = parts.as<dev::AggPart>();
-      if (flt) {
-        if (xg) launch_ck<double, true>(ck, ctx, g, m, x, y, cs, cpart.pos(), op, swap, P, err.as<int>());
-        else launch_ck<double, false>(ck, ctx, g, m, x, y, cs, cpart.pos(), op, swap, P, err.as<int>());
-      } else {
-        if (xg) launch_ck<int64_t, true>(ck, ctx, g, m, x, y, cs, cpart.pos(), op, swap, P, err.as<int>());
-        else launch_ck<int64_t, false>(ck, ctx, g, m, x, y, cs, cpart.pos(), op, swap, P, err.as<int>());
-      }
+      FusedLaunch f{static_cast<unsigned>(ntiles), &y, xs, cs, apart.pos(), cpart.pos(),
+                    a.enc == RQ_ENC_RLE ? 0 : 1, parts.as<dev::AggPart>(), err};
+      if (flt) launch1<double>(op, ck, ctx, f);
+      else launch1<int64_t>(op, ck, ctx, f);
       ctx->count_launch();
       RQ_CUDA_CHECK(cudaGetLastError());
-      dev::k_sum_parts<256><<<1, 256, 0, ctx->stream>>>(P, ntiles, out.as<dev::AggPart>());
+      dev::k_sum_parts<1024><<<1, 1024, 0, ctx->stream>>>(parts.as<dev::AggPart>(), ntiles,
+                                                        out.as<dev::AggPart>());
       ctx->count_launch();
       RQ_CUDA_CHECK(cudaGetLastError());
     }
-    RQ_CUDA_CHECK(cudaMemcpyAsync(ctx->pinned, out.raw(), sizeof(dev::AggPart), cudaMemcpyDeviceToHost, ctx->stream));
-    RQ_CUDA_CHECK(cudaMemcpyAsync(ctx->pinned + 16, err.raw(), 8, cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->sync();
-    res = *reinterpret_cast<const dev::AggPart*>(ctx->pinned);
-    if (!flt && op == RQ_DIV && static_cast<int32_t>(ctx->pinned[16] & 0xffffffff))
-      fail("integer division by zero");
+    const int64_t* h = ctx->readback(out.raw(), sizeof(dev::AggPart) + 8);
+    res = *reinterpret_cast<const dev::AggPart*>(h);
+    const int32_t e = static_cast<int32_t>(h[sizeof(dev::AggPart) / 8] & 0xffffffff);
+    if (!flt && op == RQ_DIV && e) fail("integer division by zero");
   }
   AggOut o;
   if (fn == RQ_COUNT) {
