@@ -275,6 +275,14 @@ int rq_group_aggregate(rq_ctx_t ctx, const rq_col_t* keys, int32_t n_keys, const
                        const int32_t* fns, int32_t n_data, int64_t* n_groups, rq_arr_t* out_keys,
                        rq_arr_t* out_vals);
 
+/* The query runner's GroupAgg (runner.cpp:302-336): group_aggregate over
+ * normalize_basic(keys) / normalize_basic(data). Same outputs as calling
+ * rq_normalize_basic on every input first, but composite inputs are folded
+ * part by part instead of being expanded to rows. */
+int rq_group_aggregate_normalized(rq_ctx_t ctx, const rq_col_t* keys, int32_t n_keys,
+                                  const rq_col_t* data, const int32_t* fns, int32_t n_data,
+                                  int64_t* n_groups, rq_arr_t* out_keys, rq_arr_t* out_vals);
+
 /* ---------------------------------------------------------------------- */
 /* fused entry points (no reference counterpart: one kernel for an operator
  * chain whose intermediate the reference materialises)                     */

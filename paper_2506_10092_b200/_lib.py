@@ -74,6 +74,7 @@ PROTOTYPES = {
     "rq_mask_not": (C.c_int, [vp, vp, P(vp)]),
     "rq_aggregate_all": (C.c_int, [vp, vp, i32, P(i32), P(i64), P(C.c_double)]),
     "rq_group_aggregate": (C.c_int, [vp, P(vp), i32, P(vp), P(i32), i32, P(i64), P(vp), P(vp)]),
+    "rq_group_aggregate_normalized": (C.c_int, [vp, P(vp), i32, P(vp), P(i32), i32, P(i64), P(vp), P(vp)]),
     "rq_aggregate_binop": (C.c_int, [vp, vp, vp, i32, i32, P(i32), P(i64), P(C.c_double)]),
     "rq_filtered_aggregate_binop": (C.c_int, [vp, vp, Scalar, i32, vp, vp, i32, i32, P(i32), P(i64),
                                               P(C.c_double)]),

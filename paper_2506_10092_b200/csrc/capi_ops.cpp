@@ -243,9 +243,9 @@ int rq_aggregate_all(rq_ctx_t c, rq_col_t data, int32_t fn, int32_t* out_dtype, 
   });
 }
 
-int rq_group_aggregate(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys, const rq_col_t* data,
-                       const int32_t* fns, int32_t n_data, int64_t* n_groups, rq_arr_t* out_keys,
-                       rq_arr_t* out_vals) {
+static int group_aggregate_api(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys, const rq_col_t* data,
+                               const int32_t* fns, int32_t n_data, int64_t* n_groups, rq_arr_t* out_keys,
+                               rq_arr_t* out_vals, bool normalize) {
   return api_guard([&] {
     auto ctx = ctx_of(c);
     require(n_keys > 0, "group: empty key list");
@@ -256,11 +256,23 @@ int rq_group_aggregate(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys, const r
       d.push_back(&col_of(data[i]));
       f.push_back(fns[i]);
     }
-    GroupAggOut r = group_aggregate(ctx, k, d, f);
+    GroupAggOut r = group_aggregate(ctx, k, d, f, normalize);
     if (n_groups) *n_groups = r.n_groups;
     for (int i = 0; i < n_keys; ++i) out_keys[i] = wrap_arr(r.keys[static_cast<size_t>(i)]);
     for (int i = 0; i < n_data; ++i) out_vals[i] = wrap_arr(r.vals[static_cast<size_t>(i)]);
   });
+}
+
+int rq_group_aggregate(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys, const rq_col_t* data,
+                       const int32_t* fns, int32_t n_data, int64_t* n_groups, rq_arr_t* out_keys,
+                       rq_arr_t* out_vals) {
+  return group_aggregate_api(c, keys, n_keys, data, fns, n_data, n_groups, out_keys, out_vals, false);
+}
+
+int rq_group_aggregate_normalized(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys, const rq_col_t* data,
+                                  const int32_t* fns, int32_t n_data, int64_t* n_groups,
+                                  rq_arr_t* out_keys, rq_arr_t* out_vals) {
+  return group_aggregate_api(c, keys, n_keys, data, fns, n_data, n_groups, out_keys, out_vals, true);
 }
 
 int rq_aggregate_binop(rq_ctx_t c, rq_col_t a, rq_col_t b, int32_t op, int32_t fn,

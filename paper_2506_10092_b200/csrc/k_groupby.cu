@@ -317,13 +317,29 @@ MultiAligned align_many(const CtxPtr& ctx, const std::vector<const DCol*>& cols)
 }
 
 GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
-                            const std::vector<const DCol*>& data, const std::vector<int>& fns) {
+                            const std::vector<const DCol*>& data, const std::vector<int>& fns,
+                            bool normalize) {
   require(!keys.empty(), "group: empty key list");
   require(data.size() == fns.size(), "group_aggregate: data/function count mismatch");
   require(keys.size() <= 8, "group: at most 8 key columns");
   for (int fn : fns) require(fn >= RQ_SUM && fn <= RQ_VAR, "aggregate: unknown function");
   std::vector<const DCol*> all(keys.begin(), keys.end());
   all.insert(all.end(), data.begin(), data.end());
+  if (!normalize)
+    for (auto* c : all)
+      if (c->enc == RQ_ENC_RLE_INDEX) fail("decompose: rle+index has two positional parts; distribute first");
+  {
+    GroupAggOut fused;
+    if (group_aggregate_fused(ctx, keys, data, fns, fused)) return fused;
+  }
+  std::vector<DCol> normalized;
+  if (normalize) {
+    normalized.reserve(all.size());
+    for (auto*& c : all) {
+      normalized.push_back(normalize_basic(ctx, *c));
+      c = &normalized.back();
+    }
+  }
   MultiAligned ma = align_many(ctx, all);
   const size_t nk = keys.size();
   const int64_t slots = ma.values[0].n;

@@ -364,7 +364,14 @@ struct GroupAggOut {
   std::vector<DArr> keys;
   std::vector<DArr> vals;
 };
+// normalize=false: agg::group_aggregate semantics (RLE+Index inputs are an
+// error, groupby.cpp:144-162 → decompose). normalize=true: the query
+// runner's GroupAgg (normalize_basic on every input first, runner.cpp:306-336).
 GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
-                            const std::vector<const DCol*>& data, const std::vector<int>& fns);
+                            const std::vector<const DCol*>& data, const std::vector<int>& fns,
+                            bool normalize = false);
+bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
+                           const std::vector<const DCol*>& data, const std::vector<int>& fns,
+                           GroupAggOut& out);
 
 }  // namespace rqb

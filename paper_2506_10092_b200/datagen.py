@@ -171,3 +171,41 @@ def c2_tables(n: int = 1_000_000_000, seed: int = 42, c_variant: str = "rle"):
 
 
 C2_K = 20  # C < 20 passes ~31% of rows
+
+
+def rle_plus_index(n: int, L: int, point_frac: float, seed: int, lo: int = -1000,
+                   hi: int = 1000) -> H.RlePlusIndexColumn:
+    """RLE+Index covering every row: segments of length U[1, 2L-1]; a
+    segment is expanded to single-row points with probability point_frac
+    (so ~point_frac of the rows are points), else it is one run (the
+    heuristic's 'rle+index' shape, ingest.cpp:217-271)."""
+    rng = np.random.default_rng(seed)
+    e = run_ends(n, L, rng)
+    s = np.concatenate([[0], e[:-1] + 1])
+    is_pt = rng.random(len(e)) < point_frac
+    rs, re_ = s[~is_pt], e[~is_pt]
+    rv = rng.integers(lo, hi + 1, len(rs)).astype(np.int64)
+    ps, pe = s[is_pt], e[is_pt]
+    lens = pe - ps + 1
+    if len(lens):
+        p = np.repeat(ps - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens) + np.arange(lens.sum())
+    else:
+        p = np.empty(0, np.int64)
+    pv = rng.integers(lo, hi + 1, len(p)).astype(np.int64)
+    return H.RlePlusIndexColumn(H.RleColumn(rv, rs, re_, n), H.IndexColumn(pv, p.astype(np.int64), n))
+
+
+def c3_tables(n: int, seed: int = 42):
+    """C3: K codes 0..99 RLE L=4096, X RLE i64 L=128,
+    Y RLE+Index (90% of rows in runs L=256, 10% points), Z plain-centered i16
+    U[-20000, 20000] (logical i64), W plain f64 U[0, 100)."""
+    k = gapless_rle(n, 4096, seed, 0, 99)
+    x = gapless_rle(n, 128, seed + 1)
+    y = rle_plus_index(n, 256, 0.1, seed + 2)
+    rng = np.random.default_rng(seed + 3)
+    z = H.PlainColumn(rng.integers(-20000, 20001, n).astype(np.int16), H.I64, 0)
+    w = H.PlainColumn(rng.uniform(0.0, 100.0, n))
+    return k, x, y, z, w
+
+
+C3_FNS = ["sum", "count", "avg", "sum", "sum"]  # SUM(X), COUNT(*), AVG(Z), SUM(Y), SUM(W)

@@ -469,9 +469,12 @@ class agg:
         return _agg_result(dt, i, f)
 
     @staticmethod
-    def group_aggregate(keys: Sequence, data: Sequence, fns: Sequence):
-        """agg::group_aggregate (groupby.cpp:144-162) -> (keys list, values list, n_groups)."""
+    def group_aggregate(keys: Sequence, data: Sequence, fns: Sequence, normalize: bool = False):
+        """agg::group_aggregate (groupby.cpp:144-162) -> (keys list, values list, n_groups).
+        normalize=True: the query runner's GroupAgg (normalize_basic on every
+        input first, runner.cpp:306-336), composites folded without expansion."""
         fns = [H.AGG_NAMES.get(f, f) for f in fns]
+        fn_c = _L.rq_group_aggregate_normalized if normalize else _L.rq_group_aggregate
         host = _is_host(*keys, *data)
         ctx = _ctx_of(*keys, *data)
         dk = [upload(k, ctx) for k in keys]
@@ -482,7 +485,7 @@ class agg:
         ok = (C.c_void_p * max(1, len(dk)))()
         ov = (C.c_void_p * max(1, len(dd)))()
         ng = C.c_int64()
-        check(_L.rq_group_aggregate(ctx.handle, karr, len(dk), darr, farr, len(dd), C.byref(ng), ok, ov))
+        check(fn_c(ctx.handle, karr, len(dk), darr, farr, len(dd), C.byref(ng), ok, ov))
         ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
         vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(dd))]
         return ks, vs, int(ng.value)
