@@ -5,16 +5,18 @@ logical rows/s per query and % of HBM roofline on compressed bytes).
 Default workload = BASELINE config[1] (C2): filtered SUM(A*B) WHERE C < k
 over 1B logical rows per GPU — A RLE int64 (L=64, 15.6M runs), B Index int64
 (1% density, 10M points), C dictionary codes (cardinality 64) RLE L=256.
-A step is one execution of the query through the C ABI
-(rq_filtered_aggregate_binop → the fused single-pass kernel) on
-device-resident compressed columns; `e2e` repeats it through the same call
-with the compressed columns uploaded from pinned host memory every step and
-the result read back. Inputs (0.47 GB/GPU) exceed L2 (126 MB), so no flush is
-needed between steps.
+A step is one execution of the query through the C ABI on device-resident
+compressed columns (`value`); `e2e` repeats it through the same call with
+the compressed columns uploaded from pinned host memory every step and the
+result read back. Inputs exceed L2 (126 MB), so no flush is needed.
 
-Multi-GPU (torchrun): one process per GPU, each rank owns a 1B-row range
-shard of an N-billion-row table (weak scaling); the per-rank partial SUM is
-merged with one NCCL all_reduce per step.
+Other workloads (--workload): c1 = SUM(A+B) over two misaligned RLE int64
+columns (fused rq_aggregate_binop), c3 = GROUP BY dict key SUM/COUNT/AVG over
+RLE / RLE+Index / bit-width-reduced i16 / f64 columns (fused group-by).
+
+Multi-GPU (torchrun): one process per GPU, each rank owns a row-range shard
+of the same size (weak scaling); the per-rank partial aggregate is merged
+with one NCCL all_reduce per step.
 
 --impl reference runs the UNMODIFIED reference library (oracle/_ref, the
 reference compiled from its sources) on the same workload on the host's
@@ -128,34 +130,42 @@ def pinned_copy(a: np.ndarray) -> np.ndarray:
 def pin_column(col):
     from paper_2506_10092_b200 import host as H
     if isinstance(col, H.RleColumn):
-        return H.RleColumn(pinned_copy(col.v), pinned_copy(col.s), pinned_copy(col.e), col.total_size)
+        # gapless columns cross PCIe without their (implied) starts
+        s = None if col.is_gapless() else pinned_copy(col.s)
+        return H.RleColumn(pinned_copy(col.v), s, pinned_copy(col.e), col.total_size)
     if isinstance(col, H.IndexColumn):
         return H.IndexColumn(pinned_copy(col.v), pinned_copy(col.p), col.total_size)
     if isinstance(col, H.PlainColumn):
         return H.PlainColumn(pinned_copy(col.values), col.logical, col.center)
+    if isinstance(col, H.RlePlusIndexColumn):
+        return H.RlePlusIndexColumn(pin_column(col.runs), pin_column(col.points))
     raise TypeError(type(col))
 
 
 def col_bytes(col):
     from paper_2506_10092_b200 import host as H
     if isinstance(col, H.RleColumn):
-        return col.v.nbytes + col.s.nbytes + col.e.nbytes
+        return col.v.nbytes + (col.s.nbytes if col.s is not None else 0) + col.e.nbytes
     if isinstance(col, H.IndexColumn):
         return col.v.nbytes + col.p.nbytes
+    if isinstance(col, H.RlePlusIndexColumn):
+        return col_bytes(col.runs) + col_bytes(col.points)
     return col.values.nbytes
 
 
-def alg_bytes_c2(a, b, c):
-    """ALG_BYTES: gapless RLE R·(w_v+8) (v + e), Index
-    P·(w_v+8), a plain column read only at B's points P·w_storage."""
+def alg_bytes(col, gapless=True, only_points=None):
+    """ALG_BYTES per SURVEY.md §8d: gapless RLE R·(w_v+8) (v + e; s implied),
+    gapped RLE R·(w_v+16), Index P·(w_v+8), Plain n·w_storage (or P·w when
+    read only at P positions), composites = sum of parts."""
     from paper_2506_10092_b200 import host as H
-    ab = a.v.shape[0] * (a.v.itemsize + 8)
-    bb = b.p.shape[0] * (b.v.itemsize + 8)
-    if isinstance(c, H.RleColumn):
-        cb = c.v.shape[0] * (c.v.itemsize + 8)
-    else:
-        cb = b.p.shape[0] * c.values.itemsize
-    return ab + bb + cb
+    if isinstance(col, H.RleColumn):
+        return col.v.shape[0] * (col.v.itemsize + (8 if gapless else 16))
+    if isinstance(col, H.IndexColumn):
+        return col.p.shape[0] * (col.v.itemsize + 8)
+    if isinstance(col, H.RlePlusIndexColumn):
+        return alg_bytes(col.runs, gapless=False) + alg_bytes(col.points)
+    n = only_points if only_points is not None else col.values.shape[0]
+    return n * col.values.itemsize
 
 
 def ncu_traffic(tag):
@@ -173,56 +183,182 @@ def ncu_traffic(tag):
 
 
 # ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+
+class C2:
+    name = "c2"
+    tag = "filtered_points_reduce"
+    dtype = "int64"
+
+    def __init__(self, args):
+        self.args = args
+        self.k = 20
+
+    def describe(self):
+        cdesc = "RLE L=256" if self.args.variant == "rle" else "plain-centered i8 L=4"
+        return (f"C2: filtered SUM(A*B) WHERE C<{self.k}; A RLE i64 L=64, B Index i64 1%, "
+                f"C dict codes (card 64) {cdesc}")
+
+    def gen(self, rows, seed):
+        from paper_2506_10092_b200 import datagen as G
+        a, b, c = G.c2_tables(rows, seed=seed, c_variant=self.args.variant)
+        self.host = {"a": a, "b": b, "c": c}
+        return self.host
+
+    def alg_bytes(self, h):
+        from paper_2506_10092_b200 import host as H
+        c = h["c"]
+        cb = alg_bytes(c) if isinstance(c, H.RleColumn) else alg_bytes(c, only_points=h["b"].p.shape[0])
+        return alg_bytes(h["a"]) + alg_bytes(h["b"]) + cb
+
+    def query(self, rq, d, path):
+        if path == "fused":
+            return rq.agg.filtered_aggregate_binop(d["c"], self.k, "<", d["a"], d["b"], "*", "sum")
+        m = rq.compute.compare_scalar(d["c"], self.k, "<")
+        return rq.agg.aggregate_all(rq.compute.arith(rq.compute.filter(d["a"], m), rq.compute.filter(d["b"], m), "*"),
+                                    "sum")
+
+    def oracle(self, h):
+        from oracle import refpy
+        return refpy.Orq().filtered_sum(h["c"], self.k, "<", h["a"], h["b"], "*")
+
+    def ref_run(self, ref, shards, threads):
+        return ref.chain_filtered_sum(shards["c"], shards["a"], shards["b"], threads, self.k, "<", "*")
+
+
+class C1:
+    name = "c1"
+    tag = "pair_reduce"
+    dtype = "int64"
+
+    def __init__(self, args):
+        self.args = args
+
+    def describe(self):
+        return "C1: SUM(A+B) over two misaligned RLE i64 columns, L=64/96"
+
+    def gen(self, rows, seed):
+        from paper_2506_10092_b200 import datagen as G
+        a, b = G.c1_tables(rows, 64, 96, seed)
+        self.host = {"a": a, "b": b}
+        return self.host
+
+    def alg_bytes(self, h):
+        return alg_bytes(h["a"]) + alg_bytes(h["b"])
+
+    def query(self, rq, d, path):
+        if path == "fused":
+            return rq.agg.aggregate_binop(d["a"], d["b"], "+", "sum")
+        return rq.agg.aggregate_all(rq.compute.arith(d["a"], d["b"], "+"), "sum")
+
+    def oracle(self, h):
+        from oracle import refpy
+        return refpy.Orq().sum_rle_binop(h["a"], h["b"], "+")
+
+    def ref_run(self, ref, shards, threads):
+        return ref.chain_sum_binop(shards["a"], shards["b"], threads, "+")
+
+
+class C3:
+    name = "c3"
+    tag = "group_fused"
+    dtype = "int64/f64"
+
+    def __init__(self, args):
+        self.args = args
+
+    def describe(self):
+        return ("C3: GROUP BY K (codes 0..99, RLE L=4096) -> SUM(X RLE L=128), COUNT(*), AVG(Z plain-centered i16), "
+                "SUM(Y RLE+Index 90% runs L=256 / 10% points), SUM(W plain f64)")
+
+    def gen(self, rows, seed):
+        from paper_2506_10092_b200 import datagen as G
+        k, x, y, z, w = G.c3_tables(rows, seed)
+        self.host = {"k": k, "x": x, "y": y, "z": z, "w": w}
+        return self.host
+
+    def alg_bytes(self, h):
+        return sum(alg_bytes(h[n]) for n in ("k", "x", "y", "z", "w"))
+
+    def query(self, rq, d, path):
+        from paper_2506_10092_b200 import datagen as G
+        ks, vs, ng = rq.agg.group_aggregate([d["k"]], [d["x"], d["k"], d["z"], d["y"], d["w"]], G.C3_FNS,
+                                            normalize=True)
+        return int(vs[0].download().astype(np.int64).sum())  # checksum: Σ_g SUM(X)
+
+    def oracle(self, h):
+        # checksum of the SUM(X) column = Σ over X's runs of v·len (int64 wrap)
+        lens = h["x"].e - h["x"].s + 1
+        return int((h["x"].v.astype(np.int64) * lens).sum())
+
+    def ref_run(self, ref, shards, threads):
+        from paper_2506_10092_b200 import datagen as G
+        t0 = time.perf_counter()
+        tot = 0
+        for i in range(len(shards["k"])):
+            kk = ref.normalize_basic(shards["k"][i])
+            cols = [ref.normalize_basic(shards[n][i]) for n in ("x", "k", "z", "y", "w")]
+            ks, vs, ng = ref.group_aggregate([kk], cols, G.C3_FNS)
+            tot += int(vs[0].astype(np.int64).sum())
+        return tot, time.perf_counter() - t0
+
+
+WORKLOADS = {"c1": C1, "c2": C2, "c3": C3}
+
+
+def shard_map(host, nshards):
+    from paper_2506_10092_b200.runq import shard_host_column
+    out = {}
+    for k, col in host.items():
+        n = col.total_size
+        cuts = [n * i // nshards for i in range(nshards + 1)]
+        out[k] = [shard_host_column(col, lo, hi) for lo, hi in zip(cuts[:-1], cuts[1:])]
+    return out
+
+
+def config_dict(args, w, rows):
+    return {"workload": w.describe(), "rows_per_gpu": rows, "query_path": args.path,
+            "l2_policy": "inputs larger than L2 (126 MB) - no flush needed"}
+
+
+# ---------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------
 
 
-def shard_list(col, nshards):
-    from paper_2506_10092_b200.runq import shard_host_column
-    n = col.total_size
-    cuts = [n * i // nshards for i in range(nshards + 1)]
-    return [shard_host_column(col, lo, hi) for lo, hi in zip(cuts[:-1], cuts[1:])]
-
-
-def run_reference(args, rank, world):
+def run_reference(args, w, rank, world):
     if rank != 0:
         return
     from oracle import refpy
-    from paper_2506_10092_b200 import datagen as G
     ref = refpy.Ref()
     threads = os.cpu_count() or 1
-    rows = args.rows
-    a, b, c = G.c2_tables(rows, seed=42, c_variant=args.variant)
-    nshards = threads
-    cs, as_, bs = shard_list(c, nshards), shard_list(a, nshards), shard_list(b, nshards)
+    rows = args.rows if w.name != "c3" else min(args.rows, 20_000_000)
+    host = w.gen(rows, 42)
+    nshards = threads if w.name != "c3" else 1
+    shards = shard_map(host, nshards)
     for _ in range(args.warmup):
-        ref.chain_filtered_sum(cs, as_, bs, threads, G.C2_K, "<", "*")
+        w.ref_run(ref, shards, threads)
     times = []
+    val = None
     for _ in range(args.steps):
-        val, sec = ref.chain_filtered_sum(cs, as_, bs, threads, G.C2_K, "<", "*")
+        val, sec = w.ref_run(ref, shards, threads)
         times.append(sec)
     ms = 1000.0 * statistics.median(times)
     value = rows / (ms / 1000.0)
+    cores = threads if nshards > 1 else 1
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic",
-        "config": config_dict(args, rows),
-        "result": val,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full {rows:.0f}-row table as {nshards} row-range shards on {threads} threads "
-                                   "(reference operator chain compare_scalar→filter×2→arith→aggregate_all per shard)"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": w.dtype,
+        "data": "synthetic", "config": config_dict(args, w, rows), "result": val,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{rows}-row table as {nshards} row-range shard(s) on {cores} thread(s); "
+                                   "the reference operator chain per shard (oracle/_ref)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-def config_dict(args, rows):
-    cdesc = "RLE L=256" if args.variant == "rle" else "plain-centered i8 L=4"
-    return {"workload": f"C2: filtered SUM(A*B) WHERE C<20; A RLE i64 L=64, B Index i64 1%, C dict codes "
-                        f"(card 64) {cdesc}", "rows_per_gpu": rows, "query_path": args.path,
-            "l2_policy": "inputs larger than L2 (126 MB) — no flush needed"}
 
 
 # ---------------------------------------------------------------------------
@@ -236,12 +372,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--rows", type=int, default=1_000_000_000)
     ap.add_argument("--variant", default="rle", choices=["rle", "narrow"])
     ap.add_argument("--path", default="fused", choices=["fused", "chain"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.workload](args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -250,59 +389,48 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo",
-                                device_id=torch.device("cuda", local) if args.impl == "ours" else None)
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, w, rank, world)
         if dist is not None:
             dist.destroy_process_group()
         return
 
     import torch
-    from paper_2506_10092_b200 import datagen as G
     from paper_2506_10092_b200 import runq
 
     rows = args.rows
     t0 = time.time()
-    a, b, c = G.c2_tables(rows, seed=42 + rank, c_variant=args.variant)
-    log(f"[rank {rank}] generated {rows} rows in {time.time() - t0:.1f}s: A runs={len(a.s)} "
-        f"B points={len(b.p)} C={'runs=%d' % len(c.s) if hasattr(c, 's') else 'rows=%d' % c.total_size}")
+    host = w.gen(rows, 42 + rank)
+    log(f"[rank {rank}] generated {w.name} with {rows} rows in {time.time() - t0:.1f}s")
 
     ctx = runq.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
-    da, db, dc = runq.upload(a, ctx), runq.upload(b, ctx), runq.upload(c, ctx)
-    k = G.C2_K
-
-    def query(xc, xa, xb):
-        if args.path == "fused":
-            return runq.agg.filtered_aggregate_binop(xc, k, "<", xa, xb, "*", "sum")
-        m = runq.compute.compare_scalar(xc, k, "<")
-        return runq.agg.aggregate_all(
-            runq.compute.arith(runq.compute.filter(xa, m), runq.compute.filter(xb, m), "*"), "sum")
-
+    dev = {k: runq.upload(v, ctx) for k, v in host.items()}
     red = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
 
-    def step(xc, xa, xb):
-        v = query(xc, xa, xb)
+    def step(d, path=None):
+        v = w.query(runq, d, path or args.path)
         if dist is not None:  # partial-aggregate merge over NCCL (int64 SUM wraps like the reference)
-            red.fill_(v)
+            red.fill_(int(v))
             dist.all_reduce(red)
             v = int(red.item())
         return v
 
     # correctness gate: fused == device chain == C oracle (rank 0, N=1)
-    v_fused = runq.agg.filtered_aggregate_binop(dc, k, "<", da, db, "*", "sum")
-    m = runq.compute.compare_scalar(dc, k, "<")
-    v_chain = runq.agg.aggregate_all(runq.compute.arith(runq.compute.filter(da, m), runq.compute.filter(db, m), "*"), "sum")
-    del m
-    assert v_fused == v_chain, (v_fused, v_chain)
+    v_fused = w.query(runq, dev, "fused")
+    if w.name != "c3":
+        v_chain = w.query(runq, dev, "chain")
+        assert v_fused == v_chain, (v_fused, v_chain)
     oracle_ok = None
     if rank == 0 and world == 1:
-        from oracle import refpy
         t1 = time.time()
-        want = refpy.Orq().filtered_sum(c, k, "<", a, b, "*")
+        want = w.oracle(host)
         oracle_ok = want == v_fused
         log(f"oracle check {'OK' if oracle_ok else 'MISMATCH'} ({time.time() - t1:.1f}s): {v_fused} vs {want}")
         assert oracle_ok
@@ -319,9 +447,9 @@ def main():
         barrier()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
+        buf = (runq.C.c_char * 65536)()
         if profile:
             runq._L.rq_ctx_set_profiling(ctx.handle, 1)
-            buf = (runq.C.c_char * 65536)()
             runq._L.rq_ctx_profile_report(ctx.handle, 1, buf, 65536)  # reset
         l0 = ctx.launches
         sampler = ClockSampler(local)
@@ -335,7 +463,6 @@ def main():
         launches = ctx.launches - l0
         report = None
         if profile:
-            buf = (runq.C.c_char * 65536)()
             runq._L.rq_ctx_profile_report(ctx.handle, 1, buf, 65536)
             runq._L.rq_ctx_set_profiling(ctx.handle, 0)
             report = json.loads(buf.value.decode())
@@ -347,54 +474,49 @@ def main():
         return ms, launches, report, sampler.summary()
 
     # device-resident throughput (value) with live per-kernel event timing
-    ms, launches, report, clocks = timed(lambda: step(dc, da, db), args.steps, profile=True)
+    ms, launches, report, clocks = timed(lambda: step(dev), args.steps, profile=True)
     value = world * rows / (ms / 1000.0)
 
-    # chain path for reference (same inputs, same result)
     chain_ms = None
-    if args.path == "fused":
-        saved = args.path
-        args.path = "chain"
-        chain_ms, _, _, _ = timed(lambda: step(dc, da, db), max(3, args.steps // 2))
-        args.path = saved
+    if args.path == "fused" and w.name != "c3":
+        chain_ms, _, _, _ = timed(lambda: step(dev, "chain"), max(3, args.steps // 2))
 
     # e2e: upload compressed columns from pinned host memory + query + readback
-    pa, pb, pc = pin_column(a), pin_column(b), pin_column(c)
-    h2d = col_bytes(pa) + col_bytes(pb) + col_bytes(pc)
+    e2e = None
+    if not args.no_e2e:
+        pinned = {k: pin_column(v) for k, v in host.items()}
+        h2d = sum(col_bytes(v) for v in pinned.values())
 
-    def e2e_step():
-        xa, xb, xc = runq.upload(pa, ctx), runq.upload(pb, ctx), runq.upload(pc, ctx)
-        return step(xc, xa, xb)
+        def e2e_step():
+            d = {k: runq.upload(v, ctx) for k, v in pinned.items()}
+            return step(d)
 
-    e2e_ms, _, _, _ = timed(e2e_step, args.steps)
-    e2e_value = world * rows / (e2e_ms / 1000.0)
+        e2e_ms, _, _, _ = timed(e2e_step, args.steps)
+        e2e = {"value": world * rows / (e2e_ms / 1000.0), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8}
 
-    # roofline of the dominant kernel (live CUDA-event timing from the library)
+    # roofline of the dominant tagged region (live CUDA-event timing)
     hbm, peak_kind = peaks()
-    dom = max(report.items(), key=lambda kv: kv[1]["ms"]) if report else (None, None)
     roof = None
-    if dom[0]:
-        tag, st = dom
+    if report and w.tag in report:
+        st = report[w.tag]
         avg_ms = st["ms"] / st["count"]
-        ab = alg_bytes_c2(a, b, c) if tag == "filtered_points_reduce" else None
-        achieved = ab / (avg_ms / 1000.0) / 1e9 if ab else None
-        roof = {"bound": "hbm", "kernel": tag, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm if achieved else None, "traffic": ncu_traffic(tag),
-                "alg_bytes_per_launch": ab, "avg_launch_ms": avg_ms, "launches": st["count"],
-                "peak_source": peak_kind, "share_of_step": st["ms"] / (ms * args.steps)}
+        ab = w.alg_bytes(host)
+        achieved = ab / (avg_ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": w.tag, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": ncu_traffic(w.tag), "alg_bytes_per_launch": ab,
+                "avg_launch_ms": avg_ms, "launches": st["count"], "peak_source": peak_kind,
+                "share_of_step": st["ms"] / (ms * args.steps)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import refpy
         ref = refpy.Ref()
-        sample_rows = min(rows, 200_000_000)
-        from paper_2506_10092_b200.runq import shard_host_column
-        sa = shard_host_column(a, 0, sample_rows)
-        sb = shard_host_column(b, 0, sample_rows)
-        sc = shard_host_column(c, 0, sample_rows)
+        sample_rows = min(rows, 200_000_000 if w.name != "c3" else 5_000_000)
+        sample = shard_map({k: runq.shard_host_column(v, 0, sample_rows) for k, v in host.items()}, 1)
         secs = []
         for _ in range(3):
-            _, s = ref.chain_filtered_sum([sc], [sa], [sb], 1, k, "<", "*")
+            _, s = w.ref_run(ref, sample, 1)
             secs.append(s)
         sec = statistics.median(secs)
         cpu = {"value": sample_rows / sec, "unit": UNIT, "cores": 1, "kind": "reference",
@@ -405,10 +527,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": config_dict(args, rows),
-            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 8},
+            "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
+            "config": config_dict(args, w, rows), "e2e": e2e,
             "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "chain_ms_per_step": chain_ms, "result": v_fused, "oracle_match": oracle_ok,
             "kernel_times_ms": report,

@@ -94,6 +94,9 @@ typedef struct rq_scalar {
  *   RLE_INDEX   : runs as RLE (dtype/n/v/s/e); points in dtype2, n2, v2, p2
  * For download, call rq_col_describe first (fills everything but the
  * pointers), allocate, then rq_col_download copies into the pointers.
+ * Upload of a gapless RLE column (runs tile [0, total_size), as ingest
+ * produces them) may pass s = NULL: starts are implied (s_0 = 0,
+ * s_i = e_{i-1} + 1) and derived on the device, so only v and e cross PCIe.
  */
 typedef struct rq_host_column {
   int32_t encoding;

@@ -347,8 +347,13 @@ int rq_col_upload(rq_ctx_t c, const rq_host_column* h, rq_col_t* out) {
         break;
       case RQ_ENC_RLE:
         col.v = upload_arr(ctx, h->dtype, h->v, h->n);
-        col.s = up_pos(ctx, h->s, h->n);
         col.e = up_pos(ctx, h->e, h->n);
+        if (h->s == nullptr && h->n > 0) {  // gapless: starts implied by the ends
+          col.s = starts_from_ends(ctx, col.e);
+          col.gapless = 1;
+        } else {
+          col.s = up_pos(ctx, h->s, h->n);
+        }
         col.logical = h->dtype;
         break;
       case RQ_ENC_INDEX:

@@ -401,6 +401,7 @@ AggHost pair_reduce(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, boo
   const int64_t na = a.e.n, nb = b.e.n;
   const int64_t ntiles = (na + nb + TILE - 1) / TILE;
   DArr part = alloc_arr(ctx, RQ_I64, ntiles + 2);
+  auto timer = std::make_unique<KTimer>(ctx, "pair_reduce");
   {
     const int64_t nparts = ntiles + 1;
     const int blocks = static_cast<int>((nparts * 32 + 255) / 256);
@@ -424,6 +425,7 @@ AggHost pair_reduce(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, boo
   }
   ctx->count_launch();
   RQ_CUDA_CHECK(cudaGetLastError());
+  timer.reset();
   AggHost h = combine(ctx, parts, ntiles);
   if (!flt && op == RQ_DIV) {
     const int64_t* e = ctx->readback(err.raw(), 8);

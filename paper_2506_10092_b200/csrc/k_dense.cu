@@ -205,6 +205,13 @@ __global__ void k_normalize_bits(const uint8_t* __restrict__ a, int64_t n, uint8
     out[i] = a[i] ? 1 : 0;
 }
 
+// gapless run starts from ends: s_0 = 0, s_i = e_{i-1} + 1
+__global__ void k_starts(const int64_t* __restrict__ e, int64_t n, int64_t* __restrict__ s) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s[i] = i == 0 ? 0 : ldg64(e, i - 1) + 1;
+}
+
 __global__ void k_iota(int64_t* __restrict__ out, int64_t n) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -432,6 +439,14 @@ DArr zeros_bytes(const CtxPtr& ctx, int64_t n) {
   DArr out = alloc_arr(ctx, RQ_I8, n);
   if (n) RQ_CUDA_CHECK(cudaMemsetAsync(out.raw_mut(), 0, static_cast<size_t>(n), ctx->stream));
   return out;
+}
+
+DArr starts_from_ends(const CtxPtr& ctx, const DArr& e) {
+  DArr s = alloc_arr(ctx, RQ_I64, e.n);
+  if (e.n == 0) return s;
+  dev::k_starts<<<grid_for(ctx, e.n), 256, 0, ctx->stream>>>(e.pos(), e.n, s.as<int64_t>());
+  check_launch(ctx);
+  return s;
 }
 
 DArr iota(const CtxPtr& ctx, int64_t n) {

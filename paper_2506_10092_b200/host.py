@@ -97,11 +97,20 @@ class RleColumn:
 
     def __post_init__(self):
         self.v = _vals(self.v)
-        self.s = _pos(self.s)
+        # s may be None for a gapless column (runs tile [0, total_size)); the
+        # C ABI then derives the starts on the device (runq_b200.h)
+        self.s = _pos(self.s) if self.s is not None else None
         self.e = _pos(self.e)
         self.total_size = int(self.total_size)
 
     encoding = ENC_RLE
+
+    def is_gapless(self) -> bool:
+        if self.s is None:
+            return True
+        if len(self.e) == 0:
+            return self.total_size == 0
+        return bool(self.s[0] == 0 and self.e[-1] == self.total_size - 1 and np.array_equal(self.s[1:], self.e[:-1] + 1))
 
     def run_count(self) -> int:
         return int(self.s.shape[0])
@@ -258,9 +267,9 @@ def column_image(col: Column):
         keep.append(col.values)
     elif isinstance(col, RleColumn):
         h.dtype = h.logical = dtype_code(col.v)
-        h.n = col.s.shape[0]
+        h.n = col.e.shape[0]
         h.v, h.s, h.e = _ptr(col.v), _ptr(col.s), _ptr(col.e)
-        keep += [col.v, col.s, col.e]
+        keep += [col.v, col.e] + ([col.s] if col.s is not None else [])
     elif isinstance(col, IndexColumn):
         h.dtype = h.logical = dtype_code(col.v)
         h.n = col.p.shape[0]

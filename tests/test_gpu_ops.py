@@ -255,3 +255,18 @@ def test_group_aggregate_composite_keys(rq, ref):
         assert ng == wng
         for g, w in zip(ks + vs, wk + wv):
             assert_array(g, w)
+
+
+def test_gapless_upload_without_starts(rq, ref):
+    """A gapless RLE column may cross the C ABI without s (starts implied);
+    every operator result is identical to uploading s."""
+    from paper_2506_10092_b200 import datagen as G2
+    a = G2.gapless_rle(50_000, 16, 1)
+    b = G2.gapless_rle(50_000, 24, 2)
+    a_nos = H.RleColumn(a.v, None, a.e, a.total_size)
+    assert a.is_gapless() and a_nos.is_gapless()
+    da = rq.upload(a_nos)
+    got = da.download()
+    assert np.array_equal(got.s, a.s) and np.array_equal(got.e, a.e)
+    assert_column(rq.compute.arith(da, rq.upload(b), "*").download(), ref.arith(a, b, "*"))
+    assert rq.agg.aggregate_binop(da, rq.upload(b), "+", "sum") == ref.aggregate_all(ref.arith(a, b, "+"), "sum")
