@@ -199,6 +199,144 @@ __global__ void __launch_bounds__(BLOCK)
   block_store_acc<BLOCK>(acc, parts + blockIdx.x);
 }
 
+// K2 fast path for two GAPLESS run lists (every merged end closes one
+// fragment of length key − previous key): keys and values of the tile's two
+// segments are staged in shared memory (values converted to T once, plus the
+// run just past each segment, which can be the other list's cursor); each
+// step reloads only the consumed side. KIND: 0 = Σ r·len as int64 (SUM int),
+// 1 = Σ r·len as f64 + Σ len (SUM float / AVG), 2 = Σ len (COUNT).
+template <int BLOCK, int ITEMS, class T, int OP, int KIND>
+__global__ void __launch_bounds__(BLOCK)
+    k_pair_reduce_gapless(MergeArgs m, const void* __restrict__ v1, int dt1, const void* __restrict__ v2,
+                          int dt2, AggPart* __restrict__ parts, int* __restrict__ err) {
+  constexpr int TILE = BLOCK * ITEMS;
+  __shared__ int64_t sk[TILE];
+  __shared__ T sv[TILE + 2];
+  const int tile = blockIdx.x;
+  const int64_t d0 = static_cast<int64_t>(tile) * TILE;
+  const int64_t d1 = min(d0 + TILE, m.na + m.nb);
+  const int64_t i0 = m.part[tile], i1 = m.part[tile + 1];
+  const int64_t j0 = d0 - i0, j1 = d1 - i1;
+  const int a = static_cast<int>(i1 - i0), b = static_cast<int>(j1 - j0);
+  // keys: A ends [0, a), B ends [a, a + b); values: A [0, a], B [a + 1, a + b + 1]
+  // (all loads of a thread issued before the stores; typed fast path when
+  // both value arrays already hold T)
+  {
+    const int64_t* pa = m.A + i0;
+    const int64_t* pb = m.B + j0 - a;
+    constexpr int DT = sizeof(T) == 8 && T(0.5) != T(0) ? RQ_F64 : RQ_I64;
+    const bool typed = dt1 == DT && dt2 == DT;
+    const T* tv1 = static_cast<const T*>(v1) + i0;
+    const T* tv2 = static_cast<const T*>(v2) + j0 - (a + 1);
+    int64_t tk[ITEMS];
+    T tvv[ITEMS + 1];
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const int k = u * BLOCK + threadIdx.x;
+      tk[u] = k < a + b ? __ldg(reinterpret_cast<const long long*>(k < a ? pa : pb) + k) : 0;
+    }
+    // valid value slots: A k in [0, a_lim], B k in [a + 1, b_lim] (tile-uniform)
+    const int a_lim = static_cast<int>(min(static_cast<int64_t>(a), m.na - 1 - i0));
+    const int b_lim = static_cast<int>(min(static_cast<int64_t>(a + b + 1), a + m.nb - j0));
+    if (typed) {
+#pragma unroll
+      for (int u = 0; u <= ITEMS; ++u) {
+        const int k = u * BLOCK + threadIdx.x;
+        const bool in_a = k <= a;
+        const bool ok = in_a ? k <= a_lim : k <= b_lim;
+        tvv[u] = ok ? (in_a ? tv1 : tv2)[k] : T(0);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u <= ITEMS; ++u) {
+        const int k = u * BLOCK + threadIdx.x;
+        const bool in_a = k <= a;
+        const bool ok = in_a ? k <= a_lim : k <= b_lim;
+        tvv[u] = !ok ? T(0) : in_a ? ld_as<T>(v1, dt1, i0 + k) : ld_as<T>(v2, dt2, j0 + (k - a - 1));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const int k = u * BLOCK + threadIdx.x;
+      if (k < a + b) sk[k] = tk[u];
+    }
+#pragma unroll
+    for (int u = 0; u <= ITEMS; ++u) {
+      const int k = u * BLOCK + threadIdx.x;
+      if (k < a + b + 2) sv[k] = tvv[u];
+    }
+  }
+  __syncthreads();
+  int diag = threadIdx.x * ITEMS;
+  if (diag > a + b) diag = a + b;
+  int x = smem_merge_path(sk, a, b, diag);
+  int y = diag - x;
+  // previous merged key (-1 before the first run of the column)
+  int64_t prev;
+  {
+    int64_t pa = -1, pb = -1;
+    if (x > 0) pa = sk[x - 1];
+    else if (i0 > 0) pa = ldg64(m.A, i0 - 1);
+    if (y > 0) pb = sk[a + y - 1];
+    else if (j0 > 0) pb = ldg64(m.B, j0 - 1);
+    prev = pa > pb ? pa : pb;
+  }
+  int64_t ka = x < a ? sk[x] : KEY_MAX;
+  int64_t kb = y < b ? sk[a + y] : KEY_MAX;
+  T va = sv[x], vb = sv[a + 1 + y];
+  uint64_t isum = 0;
+  double fsum = 0.0;
+  int64_t cnt = 0;
+  int lerr = 0;
+  const int steps = min(ITEMS, a + b - diag);
+  for (int it = 0; it < steps; ++it) {
+    const bool takeA = ka <= kb;
+    const int64_t key = takeA ? ka : kb;
+    const int64_t len = key - prev;  // 0 on a shared end (tie)
+    prev = key;
+    if (KIND == 0) {
+      if (len > 0) {  // a tie closes no fragment (and must not divide)
+        const T r = arith_t<T>(va, vb, OP, &lerr);
+        isum += static_cast<uint64_t>(static_cast<int64_t>(r)) * static_cast<uint64_t>(len);
+      }
+    } else if (KIND == 1) {
+      if (len > 0) {
+        const T r = arith_t<T>(va, vb, OP, &lerr);
+        fsum += static_cast<double>(r) * static_cast<double>(len);
+      }
+      cnt += len;
+    } else {
+      cnt += len;
+    }
+    if (takeA) {
+      ++x;
+      ka = x < a ? sk[x] : KEY_MAX;
+      va = sv[x];
+    } else {
+      ++y;
+      kb = y < b ? sk[a + y] : KEY_MAX;
+      vb = sv[a + 1 + y];
+    }
+  }
+  if (lerr) atomicExch(err, 1);
+  __shared__ uint64_t ru[BLOCK / 32 + 1];
+  __shared__ double rf[BLOCK / 32 + 1];
+  isum = block_sum<BLOCK>(isum, ru);
+  fsum = block_sum<BLOCK>(fsum, rf);
+  const uint64_t c = block_sum<BLOCK>(static_cast<uint64_t>(cnt), ru);
+  if (threadIdx.x == 0) {
+    AggPart p{};
+    p.isum = isum;
+    p.fsum = fsum;
+    p.cnt = static_cast<long long>(c);
+    p.imin = INT64_MAX;
+    p.imax = INT64_MIN;
+    p.fmin = INFINITY;
+    p.fmax = -INFINITY;
+    parts[tile] = p;
+  }
+}
+
 }  // namespace dev
 
 namespace {
@@ -395,8 +533,39 @@ namespace {
 
 constexpr int PB = 256, PI = 8;
 
+template <class T, int OP>
+void launch_gapless_t(const CtxPtr& ctx, unsigned g, const dev::MergeArgs& m, const DCol& a, const DCol& b,
+                      int kind, dev::AggPart* P, int* err) {
+  switch (kind) {
+    case 0: dev::k_pair_reduce_gapless<PB, PI, T, OP, 0><<<g, PB, 0, ctx->stream>>>(m, a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, P, err); break;
+    case 1: dev::k_pair_reduce_gapless<PB, PI, T, OP, 1><<<g, PB, 0, ctx->stream>>>(m, a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, P, err); break;
+    default: dev::k_pair_reduce_gapless<PB, PI, T, OP, 2><<<g, PB, 0, ctx->stream>>>(m, a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, P, err); break;
+  }
+}
+
+void launch_gapless(const CtxPtr& ctx, unsigned g, const dev::MergeArgs& m, const DCol& a, const DCol& b,
+                    int op, int kind, bool flt, dev::AggPart* P, int* err) {
+  if (flt) {
+    switch (op) {
+      case RQ_ADD: launch_gapless_t<double, RQ_ADD>(ctx, g, m, a, b, kind, P, err); break;
+      case RQ_SUB: launch_gapless_t<double, RQ_SUB>(ctx, g, m, a, b, kind, P, err); break;
+      case RQ_MUL: launch_gapless_t<double, RQ_MUL>(ctx, g, m, a, b, kind, P, err); break;
+      default: launch_gapless_t<double, RQ_DIV>(ctx, g, m, a, b, kind, P, err); break;
+    }
+  } else {
+    switch (op) {
+      case RQ_ADD: launch_gapless_t<int64_t, RQ_ADD>(ctx, g, m, a, b, kind, P, err); break;
+      case RQ_SUB: launch_gapless_t<int64_t, RQ_SUB>(ctx, g, m, a, b, kind, P, err); break;
+      case RQ_MUL: launch_gapless_t<int64_t, RQ_MUL>(ctx, g, m, a, b, kind, P, err); break;
+      default: launch_gapless_t<int64_t, RQ_DIV>(ctx, g, m, a, b, kind, P, err); break;
+    }
+  }
+}
+
+// fast_kind: gapless fast-path accumulator (0 SUM int, 1 SUM f64/AVG, 2
+// COUNT) or -1 for the general walk (VAR/STD passes, gapped inputs).
 AggHost pair_reduce(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bool gapless,
-                    bool flt, bool pass2, double mean) {
+                    bool flt, bool pass2, double mean, int fast_kind = -1) {
   constexpr int TILE = PB * PI;
   const int64_t na = a.e.n, nb = b.e.n;
   const int64_t ntiles = (na + nb + TILE - 1) / TILE;
@@ -416,7 +585,9 @@ AggHost pair_reduce(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, boo
   dev::MergeArgs m{a.e.pos(), na, b.e.pos(), nb, part.as<int64_t>()};
   auto* P = parts.as<dev::AggPart>();
   const unsigned g = static_cast<unsigned>(ntiles);
-  if (gapless) {
+  if (gapless && fast_kind >= 0) {
+    launch_gapless(ctx, g, m, a, b, op, fast_kind, flt, P, err.as<int>());
+  } else if (gapless) {
     if (flt) dev::k_pair_reduce<PB, PI, true, double><<<g, PB, 0, ctx->stream>>>(m, a.s.pos(), b.s.pos(), a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, op, pass2, mean, P, err.as<int>());
     else dev::k_pair_reduce<PB, PI, true, int64_t><<<g, PB, 0, ctx->stream>>>(m, a.s.pos(), b.s.pos(), a.v.raw(), a.v.dt, b.v.raw(), b.v.dt, op, pass2, mean, P, err.as<int>());
   } else {
@@ -448,7 +619,11 @@ AggOut aggregate_binop(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, 
       return finish(fn, flt, h, nullptr);
     }
     const bool gapless = col_gapless(ctx, a) && col_gapless(ctx, b);
-    AggHost h = pair_reduce(ctx, a, b, op, gapless, flt, false, 0.0);
+    int fast_kind = -1;
+    if (fn == RQ_SUM) fast_kind = flt ? 1 : 0;
+    else if (fn == RQ_AVG) fast_kind = 1;
+    else if (fn == RQ_COUNT) fast_kind = 2;
+    AggHost h = pair_reduce(ctx, a, b, op, gapless, flt, false, 0.0, fast_kind);
     if ((fn == RQ_VAR || fn == RQ_STD) && h.cnt > 0) {
       AggHost sq = pair_reduce(ctx, a, b, op, gapless, flt, true, h.fsum / static_cast<double>(h.cnt));
       return finish(fn, flt, h, &sq);

@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(BLOCK)
   const int64_t alen = a_hi > a_lo ? a_hi - a_lo : 0;
   const bool a_staged = narrow && alen < ACAP;
   // search length: the power of two above the window (uniform per CTA)
-  int la = 1;
-  while (la <= alen) la <<= 1;
+  // smallest power of two > alen (alen < 2^31 whenever the window is staged)
+  const int la = alen > 0 ? (1 << (32 - __clz(static_cast<int>(min(alen, static_cast<int64_t>(INT32_MAX / 2)))))) : 1;
   int64_t c_lo = 0, clen = 0;
   bool c_staged = false;
   int lc = 1;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(BLOCK)
     if (c_hi > c.n) c_hi = c.n;
     clen = c_hi > c_lo ? c_hi - c_lo : 0;
     c_staged = narrow && clen < CCAP;
-    while (lc <= clen) lc <<= 1;
+    lc = clen > 0 ? (1 << (32 - __clz(static_cast<int>(min(clen, static_cast<int64_t>(INT32_MAX / 2)))))) : 1;
   }
   // coalesced staging of the run windows as 32-bit offsets from p0 (C's
   // predicate evaluated once per run); [len, L) padded with INT32_MAX. All

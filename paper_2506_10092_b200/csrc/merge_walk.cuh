@@ -61,8 +61,20 @@ struct MergeTile {
     const int64_t j1 = d1 - i1;
     a = static_cast<int>(i1 - i0);
     b = static_cast<int>(j1 - j0);
-    for (int k = threadIdx.x; k < a; k += BLOCK) sk[k] = ldg64(m.A, i0 + k);
-    for (int k = threadIdx.x; k < b; k += BLOCK) sk[a + k] = ldg64(m.B, j0 + k);
+    // a + b <= TILE: ITEMS unrolled, independent coalesced loads per thread
+    const int64_t* pa = m.A + i0;
+    const int64_t* pb = m.B + j0 - a;
+    int64_t t[ITEMS];
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const int k = u * BLOCK + threadIdx.x;
+      t[u] = k < a + b ? __ldg(reinterpret_cast<const long long*>(k < a ? pa : pb) + k) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const int k = u * BLOCK + threadIdx.x;
+      if (k < a + b) sk[k] = t[u];
+    }
     __syncthreads();
     int diag = threadIdx.x * ITEMS;
     if (diag > a + b) diag = a + b;

@@ -27,11 +27,14 @@ def main(path):
     src = subprocess.run(['ncu', '-i', path, '--page', 'source', '--csv', '--print-source', 'sass'],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
-    hdr = rows[1]
-    data = rows[2:]
-    i_src, i_s, i_ie = hdr.index('Source'), hdr.index('Warp Stall Sampling (All Samples)'), hdr.index('Instructions Executed')
     c, cs = Counter(), Counter()
-    for r in data:
+    i_src = i_s = i_ie = None
+    for r in rows:
+        if r and r[0] == 'Address':  # header of a kernel section
+            i_src, i_s, i_ie = r.index('Source'), r.index('Warp Stall Sampling (All Samples)'), r.index('Instructions Executed')
+            continue
+        if i_src is None or len(r) <= max(i_src, i_s, i_ie) or not r[0].startswith('0x'):
+            continue
         toks = r[i_src].split()
         if not toks:
             continue
