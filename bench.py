@@ -305,7 +305,95 @@ class C3:
         return tot, time.perf_counter() - t0
 
 
-WORKLOADS = {"c1": C1, "c2": C2, "c3": C3}
+class Q6:
+    """C4: TPC-H-style Q6 over synthetic lineitem (SF = rows / 6M) sorted by
+    (quantity, discount, shipdate) — device operator chain, same plan as the
+    reference runner."""
+    name = "q6"
+    tag = None  # whole query (operator chain)
+    dtype = "f64"
+    ref_rows = 60_000_000  # reference arm sample (SF10)
+
+    def __init__(self, args):
+        self.args = args
+
+    def describe(self):
+        return (f"C4 Q6: SUM(price*disc) WHERE shipdate in [1994-01-01,1995-01-01) AND disc BETWEEN 5 AND 7 AND "
+                f"qty < 24; lineitem SF{self.args.rows / 6e6:g} sorted (qty, disc, shipdate), RLE keys + f64 price")
+
+    def gen(self, rows, seed):
+        from paper_2506_10092_b200 import queries as Q
+        self.host = Q.lineitem_q6(rows, seed)
+        return self.host
+
+    def alg_bytes(self, h):
+        from paper_2506_10092_b200 import queries as Q
+        sd, d, q = h["l_shipdate"], h["l_discount"], h["l_quantity"]
+        # price is read only at the selected rows (SURVEY §8d): estimate them from the runs
+        n = h["l_extendedprice"].values.shape[0]
+        sel = self._selected(h)
+        return alg_bytes(sd) + alg_bytes(d) + alg_bytes(q) + sel * 8
+
+    def _selected(self, h):
+        from paper_2506_10092_b200 import queries as Q
+        sd, d, q = h["l_shipdate"], h["l_discount"], h["l_quantity"]
+        # runs of shipdate inside a passing (qty, disc) block and date range
+        qi = np.searchsorted(q.e, sd.s)
+        di = np.searchsorted(d.e, sd.s)
+        ok = (q.v[qi] < 24) & (d.v[di] >= 5) & (d.v[di] <= 7) & (sd.v >= Q.Q6_LO) & (sd.v < Q.Q6_HI)
+        return int((sd.e - sd.s + 1)[ok].sum())
+
+    def query(self, rq, d, path):
+        from paper_2506_10092_b200 import queries as Q
+        return Q.q6(rq, d)
+
+    def oracle(self, h):
+        return None
+
+    def ref_run(self, ref, shards, threads):
+        from oracle.refpy import RefAPI
+        from paper_2506_10092_b200 import queries as Q
+        api = RefAPI(ref)
+        t0 = time.perf_counter()
+        tot = sum(Q.q6(api, {k: v[i] for k, v in shards.items()}) for i in range(len(shards["l_shipdate"])))
+        return tot, time.perf_counter() - t0
+
+
+class Q1(Q6):
+    name = "q1"
+    dtype = "int64/f64"
+    ref_rows = 2_000_000
+
+    def describe(self):
+        return (f"C4 Q1: GROUP BY returnflag, linestatus: 4 SUMs, 3 AVGs, COUNT WHERE shipdate <= 1998-09-02; "
+                f"lineitem SF{self.args.rows / 6e6:g} sorted (rf, ls, shipdate, qty); disc/tax i8 plain, price f64")
+
+    def gen(self, rows, seed):
+        from paper_2506_10092_b200 import queries as Q
+        self.host = Q.lineitem_q1(rows, seed)
+        return self.host
+
+    def alg_bytes(self, h):
+        return sum(alg_bytes(c, gapless=True) for c in h.values())
+
+    def query(self, rq, d, path):
+        from paper_2506_10092_b200 import queries as Q
+        ks, vs, ng = Q.q1(rq, d)
+        return int(vs[7].download().sum()) if hasattr(vs[7], "download") else int(vs[7].sum())  # Σ COUNT
+
+    def ref_run(self, ref, shards, threads):
+        from oracle.refpy import RefAPI
+        from paper_2506_10092_b200 import queries as Q
+        api = RefAPI(ref)
+        t0 = time.perf_counter()
+        tot = 0
+        for i in range(len(shards["l_shipdate"])):
+            ks, vs, ng = Q.q1(api, {k: v[i] for k, v in shards.items()})
+            tot += int(vs[7].sum())
+        return tot, time.perf_counter() - t0
+
+
+WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "q6": Q6, "q1": Q1}
 
 
 def shard_map(host, nshards):
@@ -334,9 +422,9 @@ def run_reference(args, w, rank, world):
     from oracle import refpy
     ref = refpy.Ref()
     threads = os.cpu_count() or 1
-    rows = args.rows if w.name != "c3" else min(args.rows, 20_000_000)
+    rows = min(args.rows, getattr(w, "ref_rows", args.rows)) if w.name != "c3" else min(args.rows, 20_000_000)
     host = w.gen(rows, 42)
-    nshards = threads if w.name != "c3" else 1
+    nshards = threads if w.name in ("c1", "c2") else 1
     shards = shard_map(host, nshards)
     for _ in range(args.warmup):
         w.ref_run(ref, shards, threads)
@@ -373,13 +461,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--rows", type=int, default=1_000_000_000)
+    ap.add_argument("--rows", type=int, default=None,
+                    help="logical rows per GPU (default 1B; SF100 = 600M for q6/q1)")
     ap.add_argument("--variant", default="rle", choices=["rle", "narrow"])
     ap.add_argument("--path", default="fused", choices=["fused", "chain"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.rows is None:
+        args.rows = 600_000_000 if args.workload in ("q6", "q1") else 1_000_000_000
     w = WORKLOADS[args.workload](args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -424,11 +515,11 @@ def main():
 
     # correctness gate: fused == device chain == C oracle (rank 0, N=1)
     v_fused = w.query(runq, dev, "fused")
-    if w.name != "c3":
+    if w.name in ("c1", "c2"):
         v_chain = w.query(runq, dev, "chain")
         assert v_fused == v_chain, (v_fused, v_chain)
     oracle_ok = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and w.oracle(host) is not None:
         t1 = time.time()
         want = w.oracle(host)
         oracle_ok = want == v_fused
@@ -478,7 +569,7 @@ def main():
     value = world * rows / (ms / 1000.0)
 
     chain_ms = None
-    if args.path == "fused" and w.name != "c3":
+    if args.path == "fused" and w.name in ("c1", "c2"):
         chain_ms, _, _, _ = timed(lambda: step(dev, "chain"), max(3, args.steps // 2))
 
     # e2e: upload compressed columns from pinned host memory + query + readback
@@ -507,12 +598,18 @@ def main():
                 "frac": achieved / hbm, "traffic": ncu_traffic(w.tag), "alg_bytes_per_launch": ab,
                 "avg_launch_ms": avg_ms, "launches": st["count"], "peak_source": peak_kind,
                 "share_of_step": st["ms"] / (ms * args.steps)}
+    elif w.tag is None:  # operator-chain workloads: whole step against the query's bytes
+        ab = w.alg_bytes(host)
+        achieved = ab / (ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "kernel": "query (operator chain)", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "alg_bytes_per_launch": ab,
+                "avg_launch_ms": ms, "launches": args.steps, "peak_source": peak_kind, "share_of_step": 1.0}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import refpy
         ref = refpy.Ref()
-        sample_rows = min(rows, 200_000_000 if w.name != "c3" else 5_000_000)
+        sample_rows = min(rows, {"c3": 5_000_000, "q6": 60_000_000, "q1": 2_000_000}.get(w.name, 200_000_000))
         sample = shard_map({k: runq.shard_host_column(v, 0, sample_rows) for k, v in host.items()}, 1)
         secs = []
         for _ in range(3):

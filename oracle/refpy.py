@@ -299,6 +299,40 @@ class Ref:
         return val, float(sec.value)
 
 
+class RefAPI:
+    """The reference library behind the same namespaces as
+    paper_2506_10092_b200.runq (compute / masks / agg), so one plan function
+    (paper_2506_10092_b200.queries) drives both sides."""
+
+    def __init__(self, ref: Ref = None):
+        r = ref or Ref()
+
+        class _C:
+            filter = staticmethod(r.filter)
+            arith = staticmethod(r.arith)
+            compare = staticmethod(r.compare)
+            arith_scalar = staticmethod(r.arith_scalar)
+            compare_scalar = staticmethod(r.compare_scalar)
+            normalize_basic = staticmethod(r.normalize_basic)
+
+        class _M:
+            and_mask = staticmethod(r.and_mask)
+            or_mask = staticmethod(r.or_mask)
+            not_mask = staticmethod(r.not_mask)
+
+        class _A:
+            aggregate_all = staticmethod(r.aggregate_all)
+
+            @staticmethod
+            def group_aggregate(keys, data, fns, normalize=False):
+                if normalize:  # runner.cpp:306-323
+                    keys = [r.normalize_basic(k) for k in keys]
+                    data = [r.normalize_basic(d) for d in data]
+                return r.group_aggregate(keys, data, fns)
+
+        self.compute, self.masks, self.agg = _C, _M, _A
+
+
 class Orq:
     """The plain-C restatement (runq_oracle.c)."""
 

@@ -168,23 +168,25 @@ __device__ __forceinline__ T plain_value(const PlainSrc& s, int64_t row) {
 }
 
 // COUNT / presence: Σ key run lengths per slot
-__global__ void k_gk_count(const int64_t* __restrict__ ke, const void* __restrict__ kv, int kdt,
-                           int64_t nk, GTable t) {
+__global__ void k_gk_count(const int64_t* __restrict__ ks, const int64_t* __restrict__ ke,
+                           const void* __restrict__ kv, int kdt, int64_t nk, GTable t) {
   __shared__ unsigned long long smem[kSmemSlots];
   unsigned long long* tab = g_table_begin<G_SUM_I>(smem, t);
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nk;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t len = ldg64(ke, i) - (i == 0 ? -1 : ldg64(ke, i - 1));
+    const int64_t len = ldg64(ke, i) - ldg64(ks, i) + 1;
     atomicAdd(tab + (ld_i64(kv, kdt, i) - t.kmin), static_cast<unsigned long long>(len));
   }
   g_table_end<G_SUM_I>(smem, t);
 }
 
-// RLE data: merge walk over (key ends A, data ends B); key runs gapless.
+// RLE data: merge walk over (key ends A, data ends B). Key runs may have
+// gaps only where the data has no rows (uniform coverage, checked on host).
 template <int BLOCK, int ITEMS, int KIND>
 __global__ void __launch_bounds__(BLOCK)
-    k_gk_rle(MergeArgs m, const void* __restrict__ kv, int kdt, const int64_t* __restrict__ ds,
-             const void* __restrict__ dv, int ddt, GTable t, const double* __restrict__ mean) {
+    k_gk_rle(MergeArgs m, const int64_t* __restrict__ kst, const void* __restrict__ kv, int kdt,
+             const int64_t* __restrict__ ds, const void* __restrict__ dv, int ddt, GTable t,
+             const double* __restrict__ mean) {
   using T = typename GTraits<KIND>::T;
   using Tile = MergeTile<BLOCK, ITEMS>;
   __shared__ int64_t sk[Tile::TILE];
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(BLOCK)
   tl.walk(sk, [&](int64_t i, int64_t j, bool takeA, int64_t key) {
     if (i >= m.na || j >= m.nb) return;
     // key run i starts after key run i-1's end; data run j starts at ds[j]
-    const int64_t ks = i == 0 ? 0 : ldg64(m.A, i - 1) + 1;
+    const int64_t ks = ldg64(kst, i);
     const int64_t lo = max(ks, ldg64(ds, j));
     const int64_t len = key - lo + 1;
     if (len <= 0) return;
@@ -221,7 +223,8 @@ __global__ void __launch_bounds__(BLOCK)
 // windows inside one run take the fast path (pure register accumulation).
 template <int KIND, bool POINTS>
 __global__ void __launch_bounds__(256)
-    k_gk_items(const int64_t* __restrict__ ke, const void* __restrict__ kv, int kdt, int64_t nk,
+    k_gk_items(const int64_t* __restrict__ kst, const int64_t* __restrict__ ke, const void* __restrict__ kv,
+               int kdt, int64_t nk,
                PlainSrc ps, const int64_t* __restrict__ pp, const void* __restrict__ pv, int pdt,
                int64_t n, int64_t seg, GTable t, const double* __restrict__ mean,
                const PlainSrc* corr) {
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(256)
         continue;
       }
       // slow path: walk the key runs overlapping the window (warp-uniform)
-      int64_t kstart = kr == 0 ? 0 : ldg64(ke, kr - 1) + 1;
+      int64_t kstart = kr < nk ? ldg64(kst, kr) : INT64_MAX;
       while (true) {
 #pragma unroll
         for (int u = 0; u < PER; ++u)
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(256)
         if (lane == 0 && slot >= 0) g_atomic<KIND>(tab, slot, r);
         acc = g_zero<KIND>();
         ++kr;
-        kstart = kend + 1;
+        kstart = kr < nk ? ldg64(kst, kr) : INT64_MAX;
         kend = kr < nk ? ldg64(ke, kr) : INT64_MAX;
         slot = kr < nk ? ld_i64(kv, kdt, kr) - t.kmin : -1;
         if (KIND == G_SQ) mu = slot >= 0 ? mean[slot] : 0.0;
@@ -430,7 +433,7 @@ std::pair<int64_t, int64_t> minmax(const CtxPtr& ctx, const DArr& v) {
 }
 
 struct GroupKey {
-  DArr e;     // gapless key run ends
+  DArr s, e;  // key runs (aligned over all key columns); gaps allowed
   DArr slot;  // slot id per run (i64)
   int64_t G = 0;
   std::vector<int64_t> kmin, stride, range;
@@ -450,7 +453,7 @@ void run_rle(const CtxPtr& ctx, const GroupKey& K, const DArr& ds, const DArr& d
   launched(ctx);
   dev::MergeArgs m{K.e.pos(), na, de.pos(), nb, part.as<int64_t>()};
   dev::k_gk_rle<B, IT, KIND><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
-      m, K.slot.raw(), K.slot.dt, ds.pos(), dv.raw(), dv.dt, t, mean);
+      m, K.s.pos(), K.slot.raw(), K.slot.dt, ds.pos(), dv.raw(), dv.dt, t, mean);
   launched(ctx);
 }
 
@@ -475,7 +478,7 @@ void run_items(const CtxPtr& ctx, const GroupKey& K, const dev::PlainSrc& ps, co
     dcorr = corr_buf.as<dev::PlainSrc>();
   }
   dev::k_gk_items<KIND, POINTS><<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
-      K.e.pos(), K.slot.raw(), K.slot.dt, K.e.n, ps, p ? p->pos() : nullptr, v ? v->raw() : nullptr,
+      K.s.pos(), K.e.pos(), K.slot.raw(), K.slot.dt, K.e.n, ps, p ? p->pos() : nullptr, v ? v->raw() : nullptr,
       v ? v->dt : RQ_I64, n, seg, t, mean, dcorr);
   launched(ctx);
 }
@@ -546,9 +549,10 @@ DArr table_for(const CtxPtr& ctx, const GroupKey& K, const DCol& d, const double
 // aligned by range_intersect into one gapless run list of composite slots.
 bool build_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKey& K) {
   for (auto* k : keys)
-    if (k->enc != RQ_ENC_RLE || dt_float(k->v.dt) || !col_gapless(ctx, *k)) return false;
+    if (k->enc != RQ_ENC_RLE || dt_float(k->v.dt)) return false;
   const DArr& e = keys[0]->e;
   std::vector<DArr> vals{keys[0]->v};
+  K.s = keys[0]->s;
   K.e = e;
   auto mm = minmax(ctx, vals[0]);
   const int64_t range = mm.second - mm.first + 1;
@@ -574,8 +578,8 @@ bool build_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKey
 
 bool build_multi_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKey& K) {
   for (auto* k : keys)
-    if (k->enc != RQ_ENC_RLE || dt_float(k->v.dt) || !col_gapless(ctx, *k)) return false;
-  // fold-align the key runs (all gapless, so the aligned runs stay gapless)
+    if (k->enc != RQ_ENC_RLE || dt_float(k->v.dt)) return false;
+  // fold-align the key runs (range_intersect; coverage = ∩ of the keys)
   DArr s = keys[0]->s, e = keys[0]->e;
   std::vector<DArr> vals{keys[0]->v};
   for (size_t c = 1; c < keys.size(); ++c) {
@@ -612,6 +616,7 @@ bool build_multi_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, Gr
   DArr slot = alloc_arr(ctx, RQ_I64, e.n);
   dev::k_gk_compose<<<grid_cap(ctx, e.n), 256, 0, ctx->stream>>>(kc, e.n, slot.as<int64_t>());
   launched(ctx);
+  K.s = s;
   K.e = e;
   K.slot = slot;
   K.G = G;
@@ -632,17 +637,44 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
   if (keys.empty() || keys.size() > 8) return false;
   const int64_t total = keys[0]->total;
   for (auto* k : keys)
-    if (k->total != total || !full_cover(ctx, *k)) return false;
+    if (k->total != total || k->enc != RQ_ENC_RLE) return false;
   for (auto* d : data)
-    if (d->total != total || !full_cover(ctx, *d)) return false;
+    if (d->total != total) return false;
   GroupKey K;
   if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
+  // Per-aggregate alignment is exact when every input covers exactly the
+  // rows the (aligned) key runs cover: full tables, or columns all filtered
+  // by the same mask (query runner Filter → GroupAgg).
+  const int64_t kcov = covered_rows(ctx, K.s, K.e);
+  if (kcov == total) {
+    for (auto* d : data)
+      if (!full_cover(ctx, *d)) return false;
+  } else {
+    const void* checked_p = nullptr;  // Index columns sharing one position buffer: check once
+    for (auto* d : data) {
+      if (d->enc == RQ_ENC_INDEX) {
+        if (d->p.n != kcov) return false;
+        if (d->p.raw() != checked_p) {
+          PointsInRuns r = points_in_runs(ctx, d->p, K.s, K.e, false, false);
+          if (r.p_out.n != d->p.n) return false;
+          checked_p = d->p.raw();
+        }
+      } else if (d->enc == RQ_ENC_RLE) {
+        if (covered_rows(ctx, d->s, d->e) != kcov) return false;
+        Intersection r = range_intersect(ctx, K.s, K.e, d->s, d->e, false, false);
+        if (covered_rows(ctx, r.s, r.e) != kcov) return false;
+      } else {
+        return false;  // plain / composite data with filtered keys: general path
+      }
+    }
+  }
   KTimer timer(ctx, "group_fused");
   // counts / presence from the key runs
   DArr cnt = new_table(ctx, K.G, 0);
   {
     dev::GTable t{reinterpret_cast<unsigned long long*>(cnt.raw_mut()), K.G, 0};
-    dev::k_gk_count<<<grid_cap(ctx, K.e.n), 256, 0, ctx->stream>>>(K.e.pos(), K.slot.raw(), K.slot.dt, K.e.n, t);
+    dev::k_gk_count<<<grid_cap(ctx, K.e.n), 256, 0, ctx->stream>>>(K.s.pos(), K.e.pos(), K.slot.raw(),
+                                                                    K.slot.dt, K.e.n, t);
     launched(ctx);
   }
   DArr flags = alloc_arr(ctx, RQ_I8, K.G);

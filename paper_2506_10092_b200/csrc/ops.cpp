@@ -345,6 +345,12 @@ bool rle_mask_sparse(const CtxPtr& ctx, const DMask& m) {  // mask_ops.cpp:13-17
   return static_cast<double>(covered_rows(ctx, m.s, m.e)) < kSparseFraction * static_cast<double>(m.total);
 }
 
+// Index columns sharing one position buffer (e.g. plain columns filtered
+// with the same mask) have identical coverage by construction.
+bool same_points(const DCol& a, const DCol& b) {
+  return a.enc == RQ_ENC_INDEX && b.enc == RQ_ENC_INDEX && a.p.buf && a.p.buf == b.p.buf && a.p.n == b.p.n;
+}
+
 DMask make_index_mask(DArr p, int64_t total) {
   DMask m;
   m.enc = RQ_MASK_INDEX;
@@ -494,6 +500,12 @@ DCol arith(const CtxPtr& ctx, const DCol& a, const DCol& b, int op) {  // align.
     return combine_disjoint(ctx, arith(ctx, rle_part(a), b, op), arith(ctx, index_part(a), b, op));
   if (b.enc == RQ_ENC_RLE_INDEX)
     return combine_disjoint(ctx, arith(ctx, a, rle_part(b), op), arith(ctx, a, index_part(b), op));
+  if (same_points(a, b)) {
+    // identical position list (one shared buffer): idx_in_idx would return
+    // p itself with identity take indices, so align reduces to elementwise
+    require(a.total == b.total, "align: total_size mismatch");
+    return column_from_shape(POINT, {}, {}, a.p, arith_values(ctx, a.v, b.v, op), a.total);
+  }
   Aligned ap = align(ctx, a, b);
   DArr vals = arith_values(ctx, ap.v1, ap.v2, op);
   return column_from_shape(ap.kind, ap.s, ap.e, ap.p, vals, ap.total);
@@ -673,7 +685,9 @@ DCol filter_plain(const CtxPtr& ctx, const DCol& c, const DMask& m) {  // align.
     return out;
   };
   switch (m.enc) {
-    case RQ_MASK_RLE: return take_pos(rle_mask_positions(ctx, m.s, m.e));
+    case RQ_MASK_RLE:
+      if (!m.positions) m.positions = std::make_shared<DArr>(rle_mask_positions(ctx, m.s, m.e));
+      return take_pos(*m.positions);
     case RQ_MASK_INDEX: return take_pos(m.p);
     case RQ_MASK_PLAIN: return take_pos(plain_mask_to_index(ctx, m.bits));
     default:

@@ -193,6 +193,9 @@ struct DMask {
   DArr s, e;    // RLE / COMPOSITE runs
   DArr p;       // INDEX / COMPOSITE points
   mutable int64_t true_count = -1;
+  // RLE / composite-run masks: positions of the covered rows, expanded once
+  // and shared by every plain column filtered with this mask
+  mutable std::shared_ptr<DArr> positions;
 };
 
 }  // namespace rqb

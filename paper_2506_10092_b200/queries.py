@@ -1,0 +1,157 @@
+"""TPC-H-style Q6 / Q1 over a synthetic lineitem (BASELINE config C4).
+
+The reference has no TPC-H generator or Q1 plan;
+its query runner evaluates a plan as: predicate masks (compare_scalar per
+literal, and_mask per conjunction, runner.cpp:114-193) → Filter applies the
+mask to EVERY scanned column (runner.cpp:243-252) → GroupAgg evaluates each
+aggregate expression with binary/scalar ops, normalizes keys and inputs and
+calls aggregate_all (no keys) or group_aggregate (runner.cpp:302-336).
+``q6`` / ``q1`` restate those plans against an operator API object ``api``
+with the reference's namespaces (``api.compute``, ``api.masks``,
+``api.agg``): the device path passes ``paper_2506_10092_b200.runq``; tests and
+the bench's reference arm pass an adapter over the reference library, so both
+sides run the same operator sequence.
+
+Synthetic lineitem: returnflag {A,N,R} → codes 0..2,
+linestatus {F,O} → 0..1, shipdate days since 1970 in [8036, 10561], quantity
+1..50, discount 0..10 and tax 0..8 in hundredths (ints; the paper keeps
+decimals as floats, here hundredths keep the sums exact), extendedprice f64.
+Tables are sorted per query as in the paper's Table 7:
+Q1 by (returnflag, linestatus, shipdate, quantity), Q6 by (quantity,
+discount, shipdate); low-cardinality sort keys are RLE, discount/tax narrow
+plain (i8), price plain f64 — what choose_encoding picks (ingest.cpp:217-271).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import host as H
+from .datagen import run_ends
+
+ROWS_PER_SF = 6_000_000
+SHIP_LO, SHIP_HI = 8036, 10561      # 1992-01-02 .. 1998-12-01
+Q6_LO, Q6_HI = 8766, 9131           # [1994-01-01, 1995-01-01)
+Q1_CUTOFF = 10471                   # 1998-09-02
+
+
+def _rle_from_sorted(vals: np.ndarray, total: int) -> H.RleColumn:
+    """RLE of a sorted-by-key value array (plain_to_rle, primitives.cpp:223-250)."""
+    n = len(vals)
+    if n == 0:
+        return H.RleColumn(np.empty(0, vals.dtype), [], [], total)
+    brk = np.nonzero(vals[1:] != vals[:-1])[0]
+    s = np.concatenate([[0], brk + 1]).astype(np.int64)
+    e = np.concatenate([brk, [n - 1]]).astype(np.int64)
+    return H.RleColumn(vals[s], s, e, total)
+
+
+def _rle_from_counts(values: np.ndarray, counts: np.ndarray, total: int) -> H.RleColumn:
+    """RLE of consecutive groups (value, count), empty groups dropped and equal
+    neighbours merged (plain_to_rle of the sorted column, primitives.cpp:223-250)."""
+    keep = counts > 0
+    values, counts = values[keep], counts[keep]
+    if len(values):
+        brk = np.concatenate([[True], values[1:] != values[:-1]])
+        grp = np.cumsum(brk) - 1
+        counts = np.bincount(grp, weights=counts).astype(np.int64)
+        values = values[brk]
+    e = np.cumsum(counts) - 1
+    s = e - counts + 1
+    return H.RleColumn(values.astype(np.int64), s.astype(np.int64), e.astype(np.int64), total)
+
+
+def lineitem_q6(n: int, seed: int = 42):
+    """Lineitem sorted by (quantity, discount, shipdate); the sorted key
+    columns are generated directly as runs (multinomial group sizes)."""
+    rng = np.random.default_rng(seed)
+    days = np.arange(SHIP_LO, SHIP_HI + 1, dtype=np.int64)
+    qc = rng.multinomial(n, np.full(50, 1 / 50))
+    dvals, dcounts, svals, scounts = [], [], [], []
+    for q in range(50):
+        dc = rng.multinomial(qc[q], np.full(11, 1 / 11))
+        dvals.append(np.arange(11))
+        dcounts.append(dc)
+        for d in range(11):
+            sc = rng.multinomial(dc[d], np.full(len(days), 1 / len(days)))
+            svals.append(days)
+            scounts.append(sc)
+    price = rng.uniform(900.0, 105000.0, n)
+    return {
+        "l_quantity": _rle_from_counts(np.arange(1, 51), qc, n),
+        "l_discount": _rle_from_counts(np.concatenate(dvals), np.concatenate(dcounts), n),
+        "l_shipdate": _rle_from_counts(np.concatenate(svals), np.concatenate(scounts), n),
+        "l_extendedprice": H.PlainColumn(price),
+    }
+
+
+def lineitem_q1(n: int, seed: int = 43):
+    """Lineitem sorted by (returnflag, linestatus, shipdate, quantity):
+    linestatus 'O' (1) iff shipdate > 1995-06-17, returnflag 'N' (1) for open
+    lines else 'A' (0) / 'R' (2)."""
+    rng = np.random.default_rng(seed)
+    days = np.arange(SHIP_LO, SHIP_HI + 1, dtype=np.int64)
+    dc = rng.multinomial(n, np.full(len(days), 1 / len(days)))
+    open_ = days > 9298
+    a_cnt = np.where(open_, 0, rng.binomial(dc, 0.5))
+    groups = []  # (rf, ls, day, count) in sort order
+    for rf in (0, 1, 2):
+        for ls in (0, 1):
+            if rf == 1:
+                cnt = np.where(open_ if ls == 1 else np.zeros_like(open_), dc, 0)
+            else:
+                cnt = np.where(open_ | (ls == 1), 0, a_cnt if rf == 0 else dc - a_cnt)
+            groups.append((rf, ls, cnt))
+    rfv, rfc, lsv, lsc, shv, shc, qv, qc = [], [], [], [], [], [], [], []
+    for rf, ls, cnt in groups:
+        tot = int(cnt.sum())
+        rfv.append([rf]); rfc.append([tot]); lsv.append([ls]); lsc.append([tot])
+        shv.append(days); shc.append(cnt)
+        for c in cnt[cnt > 0]:
+            qv.append(np.arange(1, 51))
+            qc.append(rng.multinomial(c, np.full(50, 1 / 50)))
+    disc = rng.integers(0, 11, n).astype(np.int8)
+    tax = rng.integers(0, 9, n).astype(np.int8)
+    price = rng.uniform(900.0, 105000.0, n)
+    cat = lambda xs: np.concatenate([np.asarray(x) for x in xs])
+    return {
+        "l_returnflag": _rle_from_counts(cat(rfv), cat(rfc), n),
+        "l_linestatus": _rle_from_counts(cat(lsv), cat(lsc), n),
+        "l_shipdate": _rle_from_counts(cat(shv), cat(shc), n),
+        "l_quantity": _rle_from_counts(cat(qv), cat(qc), n),
+        "l_discount": H.PlainColumn(disc, H.I64),
+        "l_tax": H.PlainColumn(tax, H.I64),
+        "l_extendedprice": H.PlainColumn(price),
+    }
+
+
+def q6(api, t) -> float:
+    """SELECT SUM(l_extendedprice * l_discount) WHERE l_shipdate >= 1994-01-01
+    AND l_shipdate < 1995-01-01 AND l_discount BETWEEN 5 AND 7 AND
+    l_quantity < 24 — the acceptance Q6 plan shape (acceptance.cpp:399-415)."""
+    C, M, A = api.compute, api.masks, api.agg
+    m = M.and_mask(
+        M.and_mask(C.compare_scalar(t["l_shipdate"], Q6_LO, ">="), C.compare_scalar(t["l_shipdate"], Q6_HI, "<")),
+        M.and_mask(M.and_mask(C.compare_scalar(t["l_discount"], 5, ">="), C.compare_scalar(t["l_discount"], 7, "<=")),
+                   C.compare_scalar(t["l_quantity"], 24, "<")))
+    price = C.filter(t["l_extendedprice"], m)
+    disc = C.filter(t["l_discount"], m)
+    return A.aggregate_all(C.arith(price, disc, "*"), "sum")
+
+
+Q1_FNS = ["sum", "sum", "sum", "sum", "avg", "avg", "avg", "count"]
+
+
+def q1(api, t):
+    """SELECT rf, ls, SUM(qty), SUM(price), SUM(price*(100-disc)),
+    SUM(price*(100-disc)*(100+tax)), AVG(qty), AVG(price), AVG(disc), COUNT(*)
+    WHERE shipdate <= 1998-09-02 GROUP BY rf, ls (discount/tax in hundredths).
+    Returns (keys, values, n_groups) as the group_aggregate call does."""
+    C, A = api.compute, api.agg
+    m = C.compare_scalar(t["l_shipdate"], Q1_CUTOFF, "<=")
+    f = {k: C.filter(v, m) for k, v in t.items()}  # Filter applies to every scanned column
+    disc_price = C.arith(f["l_extendedprice"], C.arith_scalar(f["l_discount"], 100, "-", True), "*")
+    charge = C.arith(disc_price, C.arith_scalar(f["l_tax"], 100, "+"), "*")
+    keys = [f["l_returnflag"], f["l_linestatus"]]
+    data = [f["l_quantity"], f["l_extendedprice"], disc_price, charge, f["l_quantity"], f["l_extendedprice"],
+            f["l_discount"], f["l_quantity"]]
+    return A.group_aggregate(keys, data, Q1_FNS, normalize=True)
