@@ -139,6 +139,8 @@ def pin_column(col):
         return H.PlainColumn(pinned_copy(col.values), col.logical, col.center)
     if isinstance(col, H.RlePlusIndexColumn):
         return H.RlePlusIndexColumn(pin_column(col.runs), pin_column(col.points))
+    if isinstance(col, H.PlainPlusIndexColumn):
+        return H.PlainPlusIndexColumn(pin_column(col.base), pin_column(col.outliers))
     raise TypeError(type(col))
 
 
@@ -150,6 +152,8 @@ def col_bytes(col):
         return col.v.nbytes + col.p.nbytes
     if isinstance(col, H.RlePlusIndexColumn):
         return col_bytes(col.runs) + col_bytes(col.points)
+    if isinstance(col, H.PlainPlusIndexColumn):
+        return col_bytes(col.base) + col_bytes(col.outliers)
     return col.values.nbytes
 
 
@@ -393,7 +397,53 @@ class Q1(Q6):
         return tot, time.perf_counter() - t0
 
 
-WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "q6": Q6, "q1": Q1}
+class C5(Q6):
+    """C5: production-shaped 15-column table (7 RLE code columns incl. the
+    avg-34.41 heavy one, 4 Plain+Index i16+1% outliers, 4 narrow plain);
+    WHERE r2 IN (3,17,42) AND r3 < 50 GROUP BY r4: SUM(pi0), SUM(p1), COUNT.
+    6B rows over 8 GPUs = 750M rows per GPU (weak scaling per rank)."""
+    name = "c5"
+    dtype = "int64"
+    ref_rows = 20_000_000
+    columns = ["r2", "r3", "r4", "pi0", "p1"]
+
+    def describe(self):
+        return ("C5: production-shaped 15 cols (7 RLE i32 codes, 4 Plain+Index i16+1% i64, 4 narrow plain); "
+                "WHERE r2 IN (3,17,42) AND r3 < 50 GROUP BY r4 -> SUM(pi0), SUM(p1), COUNT(*)")
+
+    def gen(self, rows, seed):
+        from paper_2506_10092_b200 import queries as Q
+        self.host = Q.production_table(rows, seed)
+        return self.host
+
+    def alg_bytes(self, h):
+        # predicate / key runs + the two measures read only at the selected rows
+        sel = getattr(self, "_sel", 0)
+        runs = sum(alg_bytes(h[k]) for k in ("r2", "r3", "r4"))
+        pi0 = h["pi0"]
+        out_frac = len(pi0.outliers.p) / max(1, pi0.base.values.shape[0])
+        return runs + sel * (2 + 2) + int(sel * out_frac) * 16
+
+    def query(self, rq, d, path):
+        from paper_2506_10092_b200 import queries as Q
+        ks, vs, ng = Q.c5_query(rq, d)
+        cnt = vs[2].download() if hasattr(vs[2], "download") else vs[2]
+        self._sel = int(cnt.sum())
+        return self._sel
+
+    def ref_run(self, ref, shards, threads):
+        from oracle.refpy import RefAPI
+        from paper_2506_10092_b200 import queries as Q
+        api = RefAPI(ref)
+        t0 = time.perf_counter()
+        tot = 0
+        for i in range(len(shards["r4"])):
+            ks, vs, ng = Q.c5_query(api, {k: v[i] for k, v in shards.items()})
+            tot += int(vs[2].sum())
+        return tot, time.perf_counter() - t0
+
+
+WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "q6": Q6, "q1": Q1, "c5": C5}
 
 
 def shard_map(host, nshards):
@@ -470,7 +520,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.rows is None:
-        args.rows = 600_000_000 if args.workload in ("q6", "q1") else 1_000_000_000
+        args.rows = {"q6": 600_000_000, "q1": 600_000_000, "c5": 750_000_000}.get(args.workload, 1_000_000_000)
     w = WORKLOADS[args.workload](args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -575,7 +625,9 @@ def main():
     # e2e: upload compressed columns from pinned host memory + query + readback
     e2e = None
     if not args.no_e2e:
-        pinned = {k: pin_column(v) for k, v in host.items()}
+        # only the columns the query reads cross PCIe
+        used = getattr(w, "columns", None) or list(host)
+        pinned = {k: pin_column(host[k]) for k in used}
         h2d = sum(col_bytes(v) for v in pinned.values())
 
         def e2e_step():
@@ -609,7 +661,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import refpy
         ref = refpy.Ref()
-        sample_rows = min(rows, {"c3": 5_000_000, "q6": 60_000_000, "q1": 2_000_000}.get(w.name, 200_000_000))
+        sample_rows = min(rows, {"c3": 5_000_000, "q6": 60_000_000, "q1": 2_000_000,
+                                 "c5": 20_000_000}.get(w.name, 200_000_000))
         sample = shard_map({k: runq.shard_host_column(v, 0, sample_rows) for k, v in host.items()}, 1)
         secs = []
         for _ in range(3):

@@ -441,6 +441,15 @@ DArr zeros_bytes(const CtxPtr& ctx, int64_t n) {
   return out;
 }
 
+// dst[idx[i]] = src[i] (same dtype)
+void scatter_values(const CtxPtr& ctx, DArr& dst, const DArr& idx, const DArr& src) {
+  require(dst.dt == src.dt, "scatter: dtype mismatch");
+  if (idx.n == 0) return;
+  dev::k_scatter_values<<<grid_for(ctx, idx.n), 256, 0, ctx->stream>>>(src.raw(), src.dt, idx.pos(), idx.n,
+                                                                      dst.dt, dst.raw_mut());
+  check_launch(ctx);
+}
+
 DArr starts_from_ends(const CtxPtr& ctx, const DArr& e) {
   DArr s = alloc_arr(ctx, RQ_I64, e.n);
   if (e.n == 0) return s;

@@ -706,12 +706,44 @@ DCol filter(const CtxPtr& ctx, const DCol& a, const DMask& m) {  // align.cpp:75
     case RQ_ENC_RLE: return filter_rle(ctx, a, m);
     case RQ_ENC_INDEX: return filter_index(ctx, a, m);
     case RQ_ENC_PLAIN_INDEX: {
-      DCol dec;
-      dec.enc = RQ_ENC_PLAIN;
-      dec.v = decode_plain_index(ctx, a);
-      dec.logical = dec.v.dt;
-      dec.total = dec.v.n;
-      return filter_plain(ctx, dec, m);
+      // Reference: filter_plain(PlainColumn(decode_values(a)), m) — decodes
+      // every row first. Same result with the decode restricted to the
+      // selected rows: gather the narrow base at the selected positions,
+      // decode, then overlay the outliers that fall on selected positions.
+      if (m.enc == RQ_MASK_COMPOSITE) {
+        DCol dec;
+        dec.enc = RQ_ENC_PLAIN;
+        dec.v = decode_plain_index(ctx, a);
+        dec.logical = dec.v.dt;
+        dec.total = dec.v.n;
+        return filter_plain(ctx, dec, m);
+      }
+      DArr pos;
+      if (m.enc == RQ_MASK_RLE) {
+        if (!m.positions) m.positions = std::make_shared<DArr>(rle_mask_positions(ctx, m.s, m.e));
+        pos = *m.positions;
+      } else if (m.enc == RQ_MASK_INDEX) {
+        pos = m.p;
+      } else {
+        pos = plain_mask_to_index(ctx, m.bits);
+      }
+      DCol base = a;
+      base.enc = RQ_ENC_PLAIN;
+      base.v = gather(ctx, a.v, pos);
+      DArr vals = cast_values(ctx, decode_plain(ctx, base), a.v2.dt);
+      if (vals.buf == base.v.buf) vals = copy_prefix(ctx, vals, vals.n);
+      PointsIntersect hit = points_intersect(ctx, a.p2, pos, true, true);
+      if (hit.p_out.n > 0) {
+        DArr ov = gather(ctx, a.v2, hit.idx1);
+        scatter_values(ctx, vals, hit.idx2, ov);
+      }
+      DCol out;
+      out.enc = RQ_ENC_INDEX;
+      out.total = a.total;
+      out.v = vals;
+      out.logical = vals.dt;
+      out.p = pos;
+      return out;
     }
     case RQ_ENC_RLE_INDEX:
       return combine_disjoint(ctx, filter(ctx, rle_part(a), m), filter(ctx, index_part(a), m));

@@ -304,6 +304,7 @@ DArr plain_cmp_scalar(const CtxPtr& ctx, const DCol& c, Scalar k, int op, bool r
 void scatter_flags(const CtxPtr& ctx, DArr& bits, const DArr& p, const DArr& flags);
 DArr iota(const CtxPtr& ctx, int64_t n);
 DArr starts_from_ends(const CtxPtr& ctx, const DArr& e);  // gapless RLE starts
+void scatter_values(const CtxPtr& ctx, DArr& dst, const DArr& idx, const DArr& src);
 
 // compaction (k_select.cu)
 // keep (s,e) of runs whose flag is set

@@ -141,6 +141,72 @@ def q6(api, t) -> float:
 Q1_FNS = ["sum", "sum", "sum", "sum", "avg", "avg", "avg", "count"]
 
 
+# ---------------------------------------------------------------------------
+# C5: production-shaped wide table
+# ---------------------------------------------------------------------------
+
+def _code_runs(n: int, avg: float, card: int, rng, dtype=np.int32) -> H.RleColumn:
+    from .datagen import run_ends
+    if avg >= n:
+        return H.RleColumn(np.array([7], dtype), [0], [n - 1], n)
+    e = run_ends(n, max(1, int(round(avg))), rng)
+    s = np.concatenate([[0], e[:-1] + 1])
+    return H.RleColumn(rng.integers(0, card, len(e)).astype(dtype), s, e, n)
+
+
+def _plain_index(n: int, rng, frac: float = 0.01) -> H.PlainPlusIndexColumn:
+    """i16 base (centre 0) + ~1% wide i64 outliers shadowing it (ingest.cpp
+    plain_to_plain_index shape: base holds 0 at outlier rows)."""
+    base = rng.integers(-30000, 30001, n).astype(np.int16)
+    p = np.nonzero(rng.random(n) < frac)[0].astype(np.int64)
+    base[p] = 0
+    ov = rng.integers(-1_000_000_000, 1_000_000_001, len(p)).astype(np.int64)
+    return H.PlainPlusIndexColumn(H.PlainColumn(base, H.I64, 0), H.IndexColumn(ov, p, n))
+
+
+def production_table(n: int, seed: int = 5):
+    """15 columns: 7 RLE i32 dictionary-code columns (one single run, one with
+    average run 34.41 — the paper's heaviest RLE column, others 1e3..3e5),
+    4 Plain+Index (i16 + 1% i64 outliers), 4 bit-width-reduced plain
+    (i8 / i16 / i32 / i16 with centres)."""
+    rng = np.random.default_rng(seed)
+    t = {
+        "r0": _code_runs(n, n, 1, rng),
+        "r1": _code_runs(n, 34.41, 1000, rng),
+        "r2": _code_runs(n, 1e3, 100, rng),
+        "r3": _code_runs(n, 5e3, 100, rng),
+        "r4": _code_runs(n, 2e4, 50, rng),
+        "r5": _code_runs(n, 1e5, 20, rng),
+        "r6": _code_runs(n, 3e5, 10, rng),
+    }
+    for i in range(4):
+        t[f"pi{i}"] = _plain_index(n, rng)
+    t["p0"] = H.PlainColumn(rng.integers(-100, 101, n).astype(np.int8), H.I64, 1000)
+    t["p1"] = H.PlainColumn(rng.integers(-20000, 20001, n).astype(np.int16), H.I64, 50_000)
+    t["p2"] = H.PlainColumn(rng.integers(-(1 << 30), 1 << 30, n).astype(np.int32), H.I64, 0)
+    t["p3"] = H.PlainColumn(rng.integers(-300, 301, n).astype(np.int16), H.I64, None)
+    return t
+
+
+C5_IN = (3, 17, 42)
+C5_LT = 50
+C5_FNS = ["sum", "sum", "count"]
+
+
+def c5_query(api, t):
+    """SELECT r4, SUM(pi0), SUM(p1), COUNT(*) WHERE r2 IN (3, 17, 42) AND
+    r3 < 50 GROUP BY r4 — the production queries' semi-joins replaced by
+    dictionary-code predicates (IN-list = OR of equalities)."""
+    C, M, A = api.compute, api.masks, api.agg
+    m_in = None
+    for code in C5_IN:
+        e = C.compare_scalar(t["r2"], code, "==")
+        m_in = e if m_in is None else M.or_mask(m_in, e)
+    m = M.and_mask(m_in, C.compare_scalar(t["r3"], C5_LT, "<"))
+    f = {k: C.filter(t[k], m) for k in ("r4", "pi0", "p1")}
+    return A.group_aggregate([f["r4"]], [f["pi0"], f["p1"], f["pi0"]], C5_FNS, normalize=True)
+
+
 def q1(api, t):
     """SELECT rf, ls, SUM(qty), SUM(price), SUM(price*(100-disc)),
     SUM(price*(100-disc)*(100+tax)), AVG(qty), AVG(price), AVG(disc), COUNT(*)
