@@ -221,7 +221,47 @@ __global__ void __launch_bounds__(BLOCK)
 // per iteration lane l takes items [base + 8l, base + 8l + 8). A warp-uniform
 // cursor over the (gapless) key runs tracks the run at the window start;
 // windows inside one run take the fast path (pure register accumulation).
-template <int KIND, bool POINTS>
+// eight consecutive storage values with one or more vector loads
+template <class S>
+__device__ __forceinline__ void load8(const S* __restrict__ p, S (&out)[8]) {
+  constexpr int B = 8 * sizeof(S);
+  if constexpr (B >= 16) {
+    union {
+      uint4 v[B / 16];
+      S s[8];
+    } u;
+#pragma unroll
+    for (int k = 0; k < B / 16; ++k) u.v[k] = __ldg(reinterpret_cast<const uint4*>(p) + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out[k] = u.s[k];
+  } else {
+    union {
+      uint2 v;
+      S s[8];
+    } u;
+    u.v = __ldg(reinterpret_cast<const uint2*>(p));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out[k] = u.s[k];
+  }
+}
+
+// bit-width-reduced decode of one storage value (column.cpp:283-297)
+template <class T, class S>
+__device__ __forceinline__ T plain_decode(const PlainSrc& s, S raw) {
+  if constexpr (std::is_floating_point<S>::value) {
+    return static_cast<T>(raw);
+  } else {
+    int64_t x = static_cast<int64_t>(raw);
+    if (s.logical != RQ_I64) x = wrap_to(s.logical, x);
+    if (s.has_center) {
+      x = static_cast<int64_t>(static_cast<uint64_t>(x) + static_cast<uint64_t>(s.center));
+      if (s.logical != RQ_I64) x = wrap_to(s.logical, x);
+    }
+    return static_cast<T>(x);
+  }
+}
+
+template <int KIND, bool POINTS, class S = int64_t>
 __global__ void __launch_bounds__(256)
     k_gk_items(const int64_t* __restrict__ kst, const int64_t* __restrict__ ke, const void* __restrict__ kv,
                int kdt, int64_t nk,
@@ -248,18 +288,29 @@ __global__ void __launch_bounds__(256)
       const int64_t i0 = b + lane * PER;
       int64_t pos[PER];
       T val[PER];
+      if (!POINTS && i0 + PER <= s1 && (reinterpret_cast<uintptr_t>(ps.v) & 15) == 0) {
+        // 8 rows of narrow storage per lane in one 64/128-bit load set, decoded in registers
+        S raw[PER];
+        load8<S>(static_cast<const S*>(ps.v) + i0, raw);
 #pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int64_t q = i0 + u;
-        const bool ok = q < s1;
-        if (POINTS) {
-          pos[u] = ok ? ldg64(pp, q) : INT64_MAX;
-          T x = ok ? ld_as<T>(pv, pdt, q) : T(0);
-          if (corr && ok) x -= plain_value<T>(*corr, pos[u]);  // plain+index outlier correction
-          val[u] = x;
-        } else {
-          pos[u] = ok ? q : INT64_MAX;
-          val[u] = ok ? plain_value<T>(ps, q) : T(0);
+        for (int u = 0; u < PER; ++u) {
+          pos[u] = i0 + u;
+          val[u] = plain_decode<T, S>(ps, raw[u]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int64_t q = i0 + u;
+          const bool ok = q < s1;
+          if (POINTS) {
+            pos[u] = ok ? ldg64(pp, q) : INT64_MAX;
+            T x = ok ? ld_as<T>(pv, pdt, q) : T(0);
+            if (corr && ok) x -= plain_value<T>(*corr, pos[u]);  // plain+index outlier correction
+            val[u] = x;
+          } else {
+            pos[u] = ok ? q : INT64_MAX;
+            val[u] = ok ? plain_value<T>(ps, q) : T(0);
+          }
         }
       }
       // last valid position of the window (warp-wide)
@@ -477,9 +528,24 @@ void run_items(const CtxPtr& ctx, const GroupKey& K, const dev::PlainSrc& ps, co
                                   ctx->stream));
     dcorr = corr_buf.as<dev::PlainSrc>();
   }
-  dev::k_gk_items<KIND, POINTS><<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
-      K.s.pos(), K.e.pos(), K.slot.raw(), K.slot.dt, K.e.n, ps, p ? p->pos() : nullptr, v ? v->raw() : nullptr,
-      v ? v->dt : RQ_I64, n, seg, t, mean, dcorr);
+  auto go = [&](auto tag) {
+    using S = decltype(tag);
+    dev::k_gk_items<KIND, POINTS, S><<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
+        K.s.pos(), K.e.pos(), K.slot.raw(), K.slot.dt, K.e.n, ps, p ? p->pos() : nullptr,
+        v ? v->raw() : nullptr, v ? v->dt : RQ_I64, n, seg, t, mean, dcorr);
+  };
+  if (POINTS) {
+    go(int64_t{});
+  } else {
+    switch (ps.dt) {
+      case RQ_I8: go(int8_t{}); break;
+      case RQ_I16: go(int16_t{}); break;
+      case RQ_I32: go(int32_t{}); break;
+      case RQ_F32: go(float{}); break;
+      case RQ_F64: go(double{}); break;
+      default: go(int64_t{}); break;
+    }
+  }
   launched(ctx);
 }
 
