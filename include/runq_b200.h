@@ -220,6 +220,12 @@ int rq_plain_mask_to_rle(rq_ctx_t ctx, rq_mask_t plain, rq_mask_t* out);
 int rq_plain_mask_to_index(rq_ctx_t ctx, rq_mask_t plain, rq_mask_t* out);
 /* enc::compact_rle (primitives.cpp:370-379). */
 int rq_compact_rle(rq_ctx_t ctx, rq_col_t rle, rq_col_t* out);
+/* enc::plain_to_rle (primitives.cpp:223-250): runs start where the STORED
+ * value changes; run values are decoded (logical dtype, +center). */
+int rq_plain_to_rle(rq_ctx_t ctx, rq_col_t plain, rq_col_t* out);
+/* enc::plain_to_rle_index (primitives.cpp:252-279): runs of length >= min_run
+ * stay runs, shorter runs become points. min_run < 2 -> RQ_INVALID. */
+int rq_plain_to_rle_index(rq_ctx_t ctx, rq_col_t plain, int64_t min_run, rq_col_t* out);
 
 /* kernels::bucketize (kernels.cpp:10-19): searchsorted of x in boundaries. */
 int rq_bucketize(rq_ctx_t ctx, rq_arr_t x, rq_arr_t boundaries, int32_t right, rq_arr_t* out);

@@ -320,6 +320,12 @@ int ref_plain_mask_to_index(const rq_host_mask* m, rq_host_mask* out) {
 int ref_compact_rle(const rq_host_column* a, rq_host_column* out) {
   return guarded([&] { from_column(enc::compact_rle(to_column(a).rle()), out); });
 }
+int ref_plain_to_rle(const rq_host_column* a, rq_host_column* out) {
+  return guarded([&] { from_column(enc::plain_to_rle(to_column(a).plain()), out); });
+}
+int ref_plain_to_rle_index(const rq_host_column* a, int64_t min_run, rq_host_column* out) {
+  return guarded([&] { from_column(enc::plain_to_rle_index(to_column(a).plain(), min_run), out); });
+}
 
 int ref_decode_values(const rq_host_column* a, ref_host_array* out) {
   return guarded([&] {

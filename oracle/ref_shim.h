@@ -50,6 +50,8 @@ int ref_bucketize(const int64_t* x, int64_t nx, const int64_t* b, int64_t nb, in
 int ref_plain_mask_to_rle(const rq_host_mask* m, rq_host_mask* out);
 int ref_plain_mask_to_index(const rq_host_mask* m, rq_host_mask* out);
 int ref_compact_rle(const rq_host_column* a, rq_host_column* out);
+int ref_plain_to_rle(const rq_host_column* a, rq_host_column* out);
+int ref_plain_to_rle_index(const rq_host_column* a, int64_t min_run, rq_host_column* out);
 
 int ref_decode_values(const rq_host_column* a, ref_host_array* out);
 int ref_normalize_basic(const rq_host_column* a, rq_host_column* out);

@@ -139,6 +139,18 @@ class Ref:
         self._check(self.lib.ref_compact_rle(C.byref(img), C.byref(out)))
         return self._col(out)
 
+    def plain_to_rle(self, c):
+        img, keep = H.column_image(c)
+        out = H.HostColumn()
+        self._check(self.lib.ref_plain_to_rle(C.byref(img), C.byref(out)))
+        return self._col(out)
+
+    def plain_to_rle_index(self, c, min_run):
+        img, keep = H.column_image(c)
+        out = H.HostColumn()
+        self._check(self.lib.ref_plain_to_rle_index(C.byref(img), C.c_int64(min_run), C.byref(out)))
+        return self._col(out)
+
     # --- column model ---
     def roundtrip(self, c):
         img, keep = H.column_image(c)
@@ -344,7 +356,8 @@ class Orq:
         for name in ("orq_range_intersect", "orq_idx_in_rle", "orq_rle_contain_idx", "orq_idx_in_idx",
                      "orq_plain_mask_to_rle", "orq_plain_mask_to_index", "orq_compact_rle",
                      "orq_rle_compare_scalar_i64", "orq_sum_rle_binop_i64",
-                     "orq_filtered_sum_rle_idx_rle", "orq_filtered_sum_plain_idx_rle"):
+                     "orq_filtered_sum_rle_idx_rle", "orq_filtered_sum_plain_idx_rle",
+                     "orq_plain_to_rle_int"):
             getattr(L, name).restype = C.c_int64
         L.orq_sum_f64.restype = C.c_double
 
@@ -410,6 +423,14 @@ class Orq:
         so, eo = np.empty(len(s), np.int64), np.empty(len(s), np.int64)
         tot = self.lib.orq_compact_rle(self._ptr(s), self._ptr(e), C.c_int64(len(s)), self._ptr(so), self._ptr(eo))
         return so, eo, int(tot)
+
+    def plain_to_rle_int(self, values):
+        """-> (s, e) of the runs of an integer storage array."""
+        v = np.ascontiguousarray(values)
+        s, e = np.empty(len(v), np.int64), np.empty(len(v), np.int64)
+        k = self.lib.orq_plain_to_rle_int(C.c_int(H.dtype_code(v)), self._ptr(v), C.c_int64(len(v)),
+                                          self._ptr(s), self._ptr(e))
+        return s[:k], e[:k]
 
     def decode_plain_int(self, values, logical, center):
         v = np.ascontiguousarray(values)

@@ -175,6 +175,18 @@ static int64_t wrap_to(int dtype, int64_t x) {
 
 /* column.cpp:283-297: cast storage to the logical type, then
  * x = T(x + center) at the logical width. */
+int64_t orq_plain_to_rle_int(int dtype, const void* values, int64_t n, int64_t* s, int64_t* e) {
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (i == 0 || load_int(dtype, values, i) != load_int(dtype, values, i - 1)) {
+      if (k > 0) e[k - 1] = i - 1;
+      s[k++] = i;
+    }
+  }
+  if (k > 0) e[k - 1] = n - 1;
+  return k;
+}
+
 void orq_decode_plain_int(int dtype, const void* values, int64_t n, int logical,
                           int has_center, int64_t center, int64_t* out) {
   for (int64_t i = 0; i < n; ++i) {

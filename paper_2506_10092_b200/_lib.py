@@ -60,6 +60,8 @@ PROTOTYPES = {
     "rq_plain_mask_to_rle": (C.c_int, [vp, vp, P(vp)]),
     "rq_plain_mask_to_index": (C.c_int, [vp, vp, P(vp)]),
     "rq_compact_rle": (C.c_int, [vp, vp, P(vp)]),
+    "rq_plain_to_rle": (C.c_int, [vp, vp, P(vp)]),
+    "rq_plain_to_rle_index": (C.c_int, [vp, vp, C.c_int64, P(vp)]),
     "rq_bucketize": (C.c_int, [vp, vp, vp, i32, P(vp)]),
     "rq_decode_values": (C.c_int, [vp, vp, P(vp)]),
     "rq_normalize_basic": (C.c_int, [vp, vp, P(vp)]),

@@ -153,6 +153,14 @@ int rq_decode_values(rq_ctx_t c, rq_col_t col, rq_arr_t* out) {
   });
 }
 
+int rq_plain_to_rle(rq_ctx_t c, rq_col_t plain, rq_col_t* out) {
+  return api_guard([&] { *out = wrap_col(plain_to_rle(ctx_of(c), col_of(plain))); });
+}
+
+int rq_plain_to_rle_index(rq_ctx_t c, rq_col_t plain, int64_t min_run, rq_col_t* out) {
+  return api_guard([&] { *out = wrap_col(plain_to_rle_index(ctx_of(c), col_of(plain), min_run)); });
+}
+
 int rq_normalize_basic(rq_ctx_t c, rq_col_t col, rq_col_t* out) {
   return api_guard([&] {
     auto ctx = ctx_of(c);

@@ -303,6 +303,9 @@ DArr plain_cmp_scalar(const CtxPtr& ctx, const DCol& c, Scalar k, int op, bool r
 // set bits[p[i]] = flags[i] (P+I outlier overlay)
 void scatter_flags(const CtxPtr& ctx, DArr& bits, const DArr& p, const DArr& flags);
 DArr iota(const CtxPtr& ctx, int64_t n);
+// encoders (k_encode.cu): enc::plain_to_rle / plain_to_rle_index
+DCol plain_to_rle(const CtxPtr& ctx, const DCol& c);
+DCol plain_to_rle_index(const CtxPtr& ctx, const DCol& c, int64_t min_run);
 DArr starts_from_ends(const CtxPtr& ctx, const DArr& e);  // gapless RLE starts
 void scatter_values(const CtxPtr& ctx, DArr& dst, const DArr& idx, const DArr& src);
 

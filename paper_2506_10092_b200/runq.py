@@ -289,6 +289,26 @@ class enc:
         check(_L.rq_compact_rle(ctx.handle, dc.handle, C.byref(o)))
         return _out(DeviceColumn(o, ctx), host)
 
+    @staticmethod
+    def plain_to_rle(c):
+        """enc::plain_to_rle (primitives.cpp:223-250)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        o = _new()
+        check(_L.rq_plain_to_rle(ctx.handle, dc.handle, C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
+    def plain_to_rle_index(c, min_run: int):
+        """enc::plain_to_rle_index (primitives.cpp:252-279)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        o = _new()
+        check(_L.rq_plain_to_rle_index(ctx.handle, dc.handle, int(min_run), C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
 
 class kernels:
     @staticmethod

@@ -174,6 +174,48 @@ def main():
     add("compact_rle", "compact_rle", {"a": enc_col(gap)}, {"col": enc_col(ref.compact_rle(gap))},
         "proj/tests/test_primitives.cpp:283-298")
 
+    # --- encoders (enc::plain_to_rle / plain_to_rle_index) ----------------------------
+    p7 = H.PlainColumn(np.array([0, 0, 0, 0, 1, 1, 1], np.int64))
+    r = ref.plain_to_rle(p7)
+    assert r.s.tolist() == [0, 4] and r.e.tolist() == [3, 6] and r.v.tolist() == [0, 1]
+    add("plain_to_rle_paper", "plain_to_rle", {"a": enc_col(p7)}, {"col": enc_col(r)},
+        "proj/tests/test_primitives.cpp:219-226")
+    alt = H.PlainColumn(np.arange(64, dtype=np.int64) % 2)
+    r = ref.plain_to_rle(alt)
+    assert len(r.s) == 64
+    add("plain_to_rle_alternating", "plain_to_rle", {"a": enc_col(alt)}, {"col": enc_col(r)},
+        "proj/tests/test_primitives.cpp:231-234")
+    # narrow storage, centred: run values decoded to the logical type
+    nc = H.PlainColumn(np.array([-3, -3, 5, 5, 5, 0, -3], np.int8), H.I64, 1000)
+    add("plain_to_rle_narrow_centered", "plain_to_rle", {"a": enc_col(nc)}, {"col": enc_col(ref.plain_to_rle(nc))},
+        "primitives.cpp:235-245")
+    # storage values that decode equal (wrap at int8) still start separate runs
+    wr = H.PlainColumn(np.array([1, 1, 257, 257, 1], np.int64), H.I8)
+    r = ref.plain_to_rle(wr)
+    assert len(r.s) == 3 and r.v.tolist() == [1, 1, 1]
+    add("plain_to_rle_wrap_boundaries", "plain_to_rle", {"a": enc_col(wr)}, {"col": enc_col(r)},
+        "kernels.cpp:235-244 (boundaries on storage)")
+    p7b = H.PlainColumn(np.array([0, 0, 0, 0, 1, 2, 3], np.int64))
+    r = ref.plain_to_rle_index(p7b, 2)
+    assert r.runs.s.tolist() == [0] and r.points.p.tolist() == [4, 5, 6]
+    add("plain_to_rle_index_paper", "plain_to_rle_index", {"a": enc_col(p7b), "min_run": 2}, {"col": enc_col(r)},
+        "proj/tests/test_primitives.cpp:237-245")
+    for name, vals, line in (("constant", np.zeros(10, np.int64), "247-250"),
+                             ("scattered", np.array([1, 2, 3, 4], np.int64), "252-255")):
+        c = H.PlainColumn(vals)
+        add(f"plain_to_rle_index_{name}", "plain_to_rle_index", {"a": enc_col(c), "min_run": 2},
+            {"col": enc_col(ref.plain_to_rle_index(c, 2))}, f"proj/tests/test_primitives.cpp:{line}")
+    erng = np.random.default_rng(10092)
+    for it in range(6):
+        n = int(erng.integers(50, 600))
+        vals = np.repeat(erng.integers(-4, 5, n), erng.integers(1, 6, n))[:n].astype(np.int16)
+        c = H.PlainColumn(vals, H.I32, int(erng.integers(-50, 50)) if it % 2 else None)
+        add(f"plain_to_rle_rand{it}", "plain_to_rle", {"a": enc_col(c)}, {"col": enc_col(ref.plain_to_rle(c))},
+            "seeded")
+        mr = 2 + it % 3
+        add(f"plain_to_rle_index_rand{it}", "plain_to_rle_index", {"a": enc_col(c), "min_run": mr},
+            {"col": enc_col(ref.plain_to_rle_index(c, mr))}, "seeded")
+
     # --- seeded random primitive instances ----------------------------------------
     rng = np.random.default_rng(2506_10092)
     for it in range(12):

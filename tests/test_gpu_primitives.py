@@ -59,6 +59,40 @@ def test_compact_rle_golden(rq, case):
     assert_column(rq.enc.compact_rle(col(case["inputs"]["a"])), col(case["expected"]["col"]))
 
 
+@pytest.mark.parametrize("case", by_fn("plain_to_rle"), ids=lambda c: c["name"])
+def test_plain_to_rle_golden(rq, case):
+    assert_column(rq.enc.plain_to_rle(col(case["inputs"]["a"])), col(case["expected"]["col"]))
+
+
+@pytest.mark.parametrize("case", by_fn("plain_to_rle_index"), ids=lambda c: c["name"])
+def test_plain_to_rle_index_golden(rq, case):
+    i = case["inputs"]
+    assert_column(rq.enc.plain_to_rle_index(col(i["a"]), i["min_run"]), col(case["expected"]["col"]))
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 1000, 3_000_000])
+@pytest.mark.parametrize("storage", ["i8", "i16", "i32", "i64", "f32", "f64"])
+def test_plain_to_rle_random_vs_reference(rq, ref, n, storage):
+    rng = np.random.default_rng(n + len(storage))
+    runs = np.repeat(rng.integers(-3, 4, n), rng.integers(1, 9, n))[:n]
+    vals = runs.astype(np.dtype(storage.replace("i", "int").replace("f", "float")))
+    if storage.startswith("f") and n > 10:
+        vals[::97] = np.nan            # NaN != NaN: every NaN starts a run
+        vals[5::89] = -0.0             # -0.0 == 0.0: no boundary
+    if storage.startswith("i") and storage != "i64":
+        c = H.PlainColumn(vals, H.I64, int(rng.integers(-1000, 1000)))
+    else:
+        c = H.PlainColumn(vals)
+    assert_column(rq.enc.plain_to_rle(c), ref.plain_to_rle(c))
+    for mr in (2, 5):
+        assert_column(rq.enc.plain_to_rle_index(c, mr), ref.plain_to_rle_index(c, mr))
+
+
+def test_plain_to_rle_index_rejects_min_run(rq):
+    with pytest.raises(Exception):
+        rq.enc.plain_to_rle_index(H.PlainColumn(np.zeros(4, np.int64)), 1)
+
+
 @pytest.mark.parametrize("n", [0, 1, 7, 300, 5000, 200_000])
 def test_range_intersect_random_vs_reference(rq, ref, n):
     rng = np.random.default_rng(n + 1)

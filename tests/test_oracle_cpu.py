@@ -73,6 +73,26 @@ def test_orq_compact_golden(orq, case):
     assert tot == want.total_size
 
 
+@pytest.mark.parametrize("case", by_fn("plain_to_rle", "plain_to_rle_index"), ids=lambda c: c["name"])
+def test_orq_plain_to_rle_golden(orq, case):
+    a = col(case["inputs"]["a"])
+    want = col(case["expected"]["col"])
+    s, e = orq.plain_to_rle_int(a.values)
+    vals = orq.decode_plain_int(a.values[s], a.logical, a.center)
+    if case["fn"] == "plain_to_rle":
+        assert_array(s, want.s, "s")
+        assert_array(e, want.e, "e")
+        assert vals.tolist() == want.v.tolist()
+        return
+    mr = case["inputs"]["min_run"]
+    long_ = (e - s + 1) >= mr
+    assert_array(s[long_], want.runs.s, "s")
+    assert_array(e[long_], want.runs.e, "e")
+    assert vals[long_].tolist() == want.runs.v.tolist()
+    pts = np.concatenate([np.arange(a, b + 1) for a, b in zip(s[~long_], e[~long_])] or [i64([])])
+    assert_array(pts.astype(np.int64), want.points.p, "p")
+
+
 @pytest.mark.parametrize("case", by_fn("sum_binop"), ids=lambda c: c["name"])
 def test_orq_c1_sum_golden(orq, case):
     i = case["inputs"]
