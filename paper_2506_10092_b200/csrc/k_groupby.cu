@@ -346,19 +346,17 @@ GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& k
   const DArr* ws = ma.shape.kind == 1 ? &ma.shape.s : nullptr;
   const DArr* we = ma.shape.kind == 1 ? &ma.shape.e : nullptr;
 
-  // dense slot ids over the joint key range
+  // dense slot ids over the joint key range when it is small (dictionary
+  // codes, dates, flags); otherwise sort-based ids (K11, k_sort.cu)
   dev::KeySpec ks{};
   ks.nk = static_cast<int>(nk);
-  std::vector<int64_t> mn(nk), range(nk);
+  std::vector<int64_t> mn(nk, 0), range(nk, 1);
   int64_t G = 1;
-  for (size_t c = 0; c < nk; ++c) {
+  bool dense = true;
+  for (size_t c = 0; c < nk; ++c)
+    if (dt_float(ma.values[c].dt)) dense = false;
+  for (size_t c = 0; c < nk && dense && slots > 0; ++c) {
     const DArr& kv = ma.values[c];
-    require(!dt_float(kv.dt), "group: floating-point keys not supported on the device path yet");
-    if (slots == 0) {
-      mn[c] = 0;
-      range[c] = 1;
-      continue;
-    }
     DArr mm = alloc_arr(ctx, RQ_I64, 2);
     const int64_t init[2] = {INT64_MAX, INT64_MIN};
     RQ_CUDA_CHECK(cudaMemcpyAsync(mm.raw_mut(), init, 16, cudaMemcpyHostToDevice, ctx->stream));
@@ -367,28 +365,38 @@ GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& k
     launched(ctx);
     const int64_t* h = ctx->readback(mm.raw(), 16);
     mn[c] = h[0];
-    range[c] = h[1] - h[0] + 1;
-    require(range[c] > 0 && range[c] <= kDenseSlotLimit,
-            "group: key range too large for the dense-slot path");
+    const uint64_t r = static_cast<uint64_t>(h[1]) - static_cast<uint64_t>(h[0]) + 1;
+    if (r == 0 || r > static_cast<uint64_t>(kDenseSlotLimit / G)) {
+      dense = false;
+      break;
+    }
+    range[c] = static_cast<int64_t>(r);
     G *= range[c];
-    require(G <= kDenseSlotLimit, "group: joint key range too large for the dense-slot path");
   }
-  int64_t stride = 1;
-  std::vector<int64_t> strides(nk);
-  for (size_t c = nk; c-- > 0;) {
-    strides[c] = stride;
-    stride *= range[c];
-  }
-  for (size_t c = 0; c < nk; ++c) {
-    ks.v[c] = ma.values[c].raw();
-    ks.dt[c] = ma.values[c].dt;
-    ks.mn[c] = mn[c];
-    ks.stride[c] = strides[c];
-  }
-  DArr gid = alloc_arr(ctx, RQ_I64, slots);
-  if (slots) {
-    dev::k_group_slots<<<grid_for(ctx, slots), 256, 0, ctx->stream>>>(ks, slots, gid.as<int64_t>());
-    launched(ctx);
+  DArr gid;
+  SortedGroups sg;
+  std::vector<int64_t> strides(nk, 1);
+  if (dense) {
+    int64_t stride = 1;
+    for (size_t c = nk; c-- > 0;) {
+      strides[c] = stride;
+      stride *= range[c];
+    }
+    for (size_t c = 0; c < nk; ++c) {
+      ks.v[c] = ma.values[c].raw();
+      ks.dt[c] = ma.values[c].dt;
+      ks.mn[c] = mn[c];
+      ks.stride[c] = strides[c];
+    }
+    gid = alloc_arr(ctx, RQ_I64, slots);
+    if (slots) {
+      dev::k_group_slots<<<grid_for(ctx, slots), 256, 0, ctx->stream>>>(ks, slots, gid.as<int64_t>());
+      launched(ctx);
+    }
+  } else {
+    sg = group_ids_sorted(ctx, std::vector<DArr>(ma.values.begin(), ma.values.begin() + nk));
+    gid = sg.inverse;
+    G = sg.n_groups > 0 ? sg.n_groups : 1;
   }
 
   auto table = [&](unsigned long long init) {
@@ -427,6 +435,10 @@ GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& k
   out.n_groups = ng;
   for (size_t c = 0; c < nk; ++c) {
     const int32_t kdt = ma.values[c].dt;
+    if (!dense) {  // the group's key = its first row in stable sorted order
+      out.keys.push_back(gather(ctx, ma.values[c], gather(ctx, sg.first_rows, present)));
+      continue;
+    }
     DArr k = alloc_arr(ctx, kdt, ng);
     if (ng) {
       dev::k_slot_keys<<<grid_for(ctx, ng), 256, 0, ctx->stream>>>(present.pos(), ng, mn[c], strides[c],

@@ -303,6 +303,15 @@ DArr plain_cmp_scalar(const CtxPtr& ctx, const DCol& c, Scalar k, int op, bool r
 // set bits[p[i]] = flags[i] (P+I outlier overlay)
 void scatter_flags(const CtxPtr& ctx, DArr& bits, const DArr& p, const DArr& flags);
 DArr iota(const CtxPtr& ctx, int64_t n);
+// sort-based grouping (k_sort.cu): unique_with_inverse over aligned key values
+struct SortedGroups {
+  DArr inverse;     // group id per slot, ascending lexicographic key order
+  DArr first_rows;  // first slot of each group in stable sorted order
+  int64_t n_groups = 0;
+};
+SortedGroups group_ids_sorted(const CtxPtr& ctx, const std::vector<DArr>& keyvals);
+void radix_sort_pairs(const CtxPtr& ctx, DArr& keys, DArr& vals, int bits, uint64_t sub);
+void scan_exclusive_i64(const CtxPtr& ctx, const DArr& in, DArr& out);
 // encoders (k_encode.cu): enc::plain_to_rle / plain_to_rle_index
 DCol plain_to_rle(const CtxPtr& ctx, const DCol& c);
 DCol plain_to_rle_index(const CtxPtr& ctx, const DCol& c, int64_t min_run);

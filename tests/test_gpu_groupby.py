@@ -126,3 +126,70 @@ def test_c3_shape_20m_rows(rq):
             assert np.allclose(got, want, rtol=1e-9, atol=1e-9), fn
         else:
             assert np.array_equal(got, want), fn
+
+
+# ---- K11: sort-based grouping (float keys, wide integer key ranges) --------------------
+
+def _check_vs_ref(rq, ref, keys, data, fns):
+    ks, vs, ng = rq.agg.group_aggregate(keys, data, fns)
+    wk, wv, wng = ref.group_aggregate(keys, data, fns)
+    assert ng == wng
+    for g, w in zip(ks, wk):
+        assert_array(g, w, "keys")
+    for g, w, fn in zip(vs, wv, fns):
+        assert_array(g, w, fn)
+
+
+@pytest.mark.parametrize("kdt", [np.float64, np.float32])
+def test_float_keys_vs_reference(rq, ref, kdt):
+    rng = np.random.default_rng(31)
+    for inst in range(4):
+        n = int(rng.integers(200, 20000))
+        k = G.gapless_rle(n, int(rng.integers(2, 30)), inst, -40, 40)
+        k = H.RleColumn((k.v.astype(np.float64) * 0.25).astype(kdt), k.s, k.e, n)
+        k.v[k.v == 0] = -0.0 if inst % 2 else 0.0      # −0.0 and +0.0 share a group
+        d = G.gapless_rle(n, 5, inst + 9)
+        _check_vs_ref(rq, ref, [k], [d, d, d, d], ["sum", "count", "min", "avg"])
+        pk = H.PlainColumn(rng.choice(np.array([-1.5, -0.0, 0.0, 2.25, 1e30], kdt), n))
+        pd = H.PlainColumn(rng.uniform(-5, 5, n))
+        _check_vs_ref(rq, ref, [pk], [pd, pd, pd], ["sum", "max", "var"])
+
+
+def test_wide_int_keys_vs_reference(rq, ref):
+    rng = np.random.default_rng(32)
+    for inst in range(4):
+        n = int(rng.integers(500, 30000))
+        # keys spread over the full int64 range: no dense slot table
+        vals = rng.integers(-(1 << 62), 1 << 62, 64) * 2 + 1
+        k = H.PlainColumn(rng.choice(vals, n))
+        d = G.gapless_rle(n, 3, inst + 50)
+        _check_vs_ref(rq, ref, [k], [d, d, d], ["sum", "count", "std"])
+
+
+def test_composite_wide_keys_lsd_over_columns(rq, ref):
+    # two full-range int64 key columns + a float column: > 64 significant bits
+    rng = np.random.default_rng(33)
+    n = 12000
+    a = H.PlainColumn(rng.choice(rng.integers(-(1 << 62), 1 << 62, 5), n))
+    b = H.PlainColumn(rng.choice(rng.integers(-(1 << 62), 1 << 62, 7), n))
+    c = H.PlainColumn(rng.choice(np.array([0.5, -2.0, 3.0]), n))
+    d = H.PlainColumn(rng.integers(-100, 100, n))
+    _check_vs_ref(rq, ref, [a, b, c], [d, d], ["sum", "avg"])
+    _check_vs_ref(rq, ref, [c, a], [d], ["max"])
+
+
+def test_sort_grouping_10m_slots_vs_numpy(rq):
+    # 10M plain rows, 1M distinct wide keys: radix passes over many tiles
+    rng = np.random.default_rng(34)
+    n = 10_000_000
+    uniq = np.unique(rng.integers(-(1 << 40), 1 << 40, 1_000_000))
+    kv = uniq[rng.integers(0, len(uniq), n)]
+    dv = rng.integers(-1000, 1000, n)
+    ks, vs, ng = rq.agg.group_aggregate([H.PlainColumn(kv)], [H.PlainColumn(dv)] * 2, ["sum", "count"])
+    want_keys, inv = np.unique(kv, return_inverse=True)
+    assert ng == len(want_keys)
+    assert np.array_equal(ks[0], want_keys)
+    want_sum = np.zeros(ng, np.int64)
+    np.add.at(want_sum, inv, dv)
+    assert np.array_equal(vs[0], want_sum)
+    assert np.array_equal(vs[1], np.bincount(inv, minlength=ng))
