@@ -226,6 +226,51 @@ int rq_plain_to_rle(rq_ctx_t ctx, rq_col_t plain, rq_col_t* out);
 /* enc::plain_to_rle_index (primitives.cpp:252-279): runs of length >= min_run
  * stay runs, shorter runs become points. min_run < 2 -> RQ_INVALID. */
 int rq_plain_to_rle_index(rq_ctx_t ctx, rq_col_t plain, int64_t min_run, rq_col_t* out);
+/* enc::plain_to_plain_index (primitives.cpp:293-347): trimmed mid-range centre,
+ * narrowest base type, values outside it become int64 outliers.
+ * trim_fraction outside [0, 0.5) -> RQ_INVALID. */
+int rq_plain_to_plain_index(rq_ctx_t ctx, rq_col_t plain, double trim_fraction, rq_col_t* out);
+
+/* ---------------------------------------------------------------------- */
+/* ingest: encoding selection and table sort (runq::io, ingest.hpp:29-66)  */
+/* ---------------------------------------------------------------------- */
+
+/* runq::io::Scheme (ingest.hpp:29). */
+enum { RQ_SCHEME_PLAIN = 0, RQ_SCHEME_PLAIN_CENTERED = 1, RQ_SCHEME_RLE = 2, RQ_SCHEME_RLE_INDEX = 3,
+       RQ_SCHEME_PLAIN_INDEX = 4 };
+
+/* runq::io::HeuristicConfig (ingest.hpp:41-48); rq_heuristic_default fills
+ * the reference defaults (1e6 rows, ratio 20, trim 0.05, min_run 2, 0.5). */
+typedef struct rq_heuristic {
+  int64_t row_threshold;
+  double ratio_threshold;
+  double trim;
+  int64_t min_run;
+  double unit_run_share;
+} rq_heuristic;
+
+/* runq::io::EncodingChoice (ingest.hpp:33-39). */
+typedef struct rq_encoding_choice {
+  int32_t scheme;
+  int32_t width;      /* storage dtype of the (narrowed) plain base */
+  int64_t min_run;
+  double trim_fraction;
+  int32_t has_center;
+  int32_t _pad;
+  int64_t center;
+} rq_encoding_choice;
+
+void rq_heuristic_default(rq_heuristic* cfg);
+/* io::choose_encoding (ingest.cpp:217-271): run profile, trimmed split and
+ * centred width all computed on the device; cfg NULL = defaults. */
+int rq_choose_encoding(rq_ctx_t ctx, rq_col_t plain, const rq_heuristic* cfg, rq_encoding_choice* out);
+/* io::encode (ingest.cpp:273-290). */
+int rq_encode(rq_ctx_t ctx, rq_col_t plain, const rq_encoding_choice* choice, rq_col_t* out);
+/* io::sort_table (ingest.cpp:292-344): stable lexicographic sort of every
+ * column by the key columns cols[by[0..nby)]; inputs must be plain, outputs
+ * are decoded plain columns (logical dtype). out holds ncols handles. */
+int rq_sort_table(rq_ctx_t ctx, const rq_col_t* cols, int32_t ncols, const int32_t* by, int32_t nby,
+                  rq_col_t* out);
 
 /* kernels::bucketize (kernels.cpp:10-19): searchsorted of x in boundaries. */
 int rq_bucketize(rq_ctx_t ctx, rq_arr_t x, rq_arr_t boundaries, int32_t right, rq_arr_t* out);

@@ -15,6 +15,8 @@
 #include "runq/align.hpp"
 #include "runq/column.hpp"
 #include "runq/groupby.hpp"
+#include "runq/ingest.hpp"
+#include "runq/table.hpp"
 #include "runq/kernels.hpp"
 #include "runq/mask_ops.hpp"
 #include "runq/primitives.hpp"
@@ -325,6 +327,61 @@ int ref_plain_to_rle(const rq_host_column* a, rq_host_column* out) {
 }
 int ref_plain_to_rle_index(const rq_host_column* a, int64_t min_run, rq_host_column* out) {
   return guarded([&] { from_column(enc::plain_to_rle_index(to_column(a).plain(), min_run), out); });
+}
+int ref_plain_to_plain_index(const rq_host_column* a, double trim, rq_host_column* out) {
+  return guarded([&] { from_column(enc::plain_to_plain_index(to_column(a).plain(), trim), out); });
+}
+
+int ref_choose_encoding(const rq_host_column* a, const rq_heuristic* cfg, rq_encoding_choice* out) {
+  return guarded([&] {
+    io::HeuristicConfig h;
+    if (cfg) {
+      h.row_threshold = cfg->row_threshold;
+      h.ratio_threshold = cfg->ratio_threshold;
+      h.trim = cfg->trim;
+      h.min_run = cfg->min_run;
+      h.unit_run_share = cfg->unit_run_share;
+    }
+    io::EncodingChoice ch = io::choose_encoding(to_column(a).plain(), h);
+    out->scheme = static_cast<int32_t>(ch.scheme);
+    out->width = static_cast<int32_t>(ch.width);
+    out->min_run = ch.min_run;
+    out->trim_fraction = ch.trim_fraction;
+    out->has_center = ch.center.has_value() ? 1 : 0;
+    out->_pad = 0;
+    out->center = ch.center.value_or(0);
+  });
+}
+
+int ref_encode(const rq_host_column* a, const rq_encoding_choice* c, rq_host_column* out) {
+  return guarded([&] {
+    io::EncodingChoice ch;
+    ch.scheme = static_cast<io::Scheme>(c->scheme);
+    ch.width = static_cast<DType>(c->width);
+    ch.min_run = c->min_run;
+    ch.trim_fraction = c->trim_fraction;
+    if (c->has_center) ch.center = c->center;
+    from_column(io::encode(to_column(a).plain(), ch), out);
+  });
+}
+
+int ref_sort_table(const rq_host_column* cols, int32_t ncols, const int32_t* by, int32_t nby,
+                   rq_host_column* out) {
+  return guarded([&] {
+    Table t;
+    t.name = "t";
+    for (int32_t i = 0; i < ncols; ++i) {
+      TableColumn tc;
+      tc.name = "c" + std::to_string(i);
+      tc.column = std::make_shared<Column>(to_column(&cols[i]));
+      t.columns.push_back(tc);
+    }
+    t.rows = ncols > 0 ? t.columns[0].column->total_size() : 0;
+    std::vector<std::string> keys;
+    for (int32_t i = 0; i < nby; ++i) keys.push_back("c" + std::to_string(by[i]));
+    Table s = io::sort_table(t, keys);
+    for (int32_t i = 0; i < ncols; ++i) from_column(*s.columns[static_cast<size_t>(i)].column, &out[i]);
+  });
 }
 
 int ref_decode_values(const rq_host_column* a, ref_host_array* out) {

@@ -52,6 +52,12 @@ int ref_plain_mask_to_index(const rq_host_mask* m, rq_host_mask* out);
 int ref_compact_rle(const rq_host_column* a, rq_host_column* out);
 int ref_plain_to_rle(const rq_host_column* a, rq_host_column* out);
 int ref_plain_to_rle_index(const rq_host_column* a, int64_t min_run, rq_host_column* out);
+int ref_plain_to_plain_index(const rq_host_column* a, double trim, rq_host_column* out);
+/* runq::io (ingest.hpp:56-62): encoding selection, encode, table sort */
+int ref_choose_encoding(const rq_host_column* a, const rq_heuristic* cfg, rq_encoding_choice* out);
+int ref_encode(const rq_host_column* a, const rq_encoding_choice* ch, rq_host_column* out);
+int ref_sort_table(const rq_host_column* cols, int32_t ncols, const int32_t* by, int32_t nby,
+                   rq_host_column* out);
 
 int ref_decode_values(const rq_host_column* a, ref_host_array* out);
 int ref_normalize_basic(const rq_host_column* a, rq_host_column* out);

@@ -151,6 +151,34 @@ class Ref:
         self._check(self.lib.ref_plain_to_rle_index(C.byref(img), C.c_int64(min_run), C.byref(out)))
         return self._col(out)
 
+    def plain_to_plain_index(self, c, trim):
+        img, keep = H.column_image(c)
+        out = H.HostColumn()
+        self._check(self.lib.ref_plain_to_plain_index(C.byref(img), C.c_double(trim), C.byref(out)))
+        return self._col(out)
+
+    # --- io (ingest.hpp:56-62) ---
+    def choose_encoding(self, c, cfg=None):
+        img, keep = H.column_image(c)
+        out = H.EncodingChoice()
+        self._check(self.lib.ref_choose_encoding(C.byref(img), C.byref(cfg) if cfg is not None else None,
+                                                 C.byref(out)))
+        return out
+
+    def encode(self, c, choice):
+        img, keep = H.column_image(c)
+        out = H.HostColumn()
+        self._check(self.lib.ref_encode(C.byref(img), C.byref(choice), C.byref(out)))
+        return self._col(out)
+
+    def sort_table(self, cols, by):
+        imgs = [H.column_image(c) for c in cols]
+        arr = (H.HostColumn * len(cols))(*[i for i, _ in imgs])
+        outs = (H.HostColumn * len(cols))()
+        bys = (C.c_int32 * len(by))(*by)
+        self._check(self.lib.ref_sort_table(arr, C.c_int32(len(cols)), bys, C.c_int32(len(by)), outs))
+        return [self._col(o) for o in outs]
+
     # --- column model ---
     def roundtrip(self, c):
         img, keep = H.column_image(c)

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .host import HostColumn, HostMask, Scalar
+from .host import EncodingChoice, Heuristic, HostColumn, HostMask, Scalar
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librunq_b200.so")
 
@@ -62,6 +62,11 @@ PROTOTYPES = {
     "rq_compact_rle": (C.c_int, [vp, vp, P(vp)]),
     "rq_plain_to_rle": (C.c_int, [vp, vp, P(vp)]),
     "rq_plain_to_rle_index": (C.c_int, [vp, vp, C.c_int64, P(vp)]),
+    "rq_plain_to_plain_index": (C.c_int, [vp, vp, C.c_double, P(vp)]),
+    "rq_heuristic_default": (None, [P(Heuristic)]),
+    "rq_choose_encoding": (C.c_int, [vp, vp, P(Heuristic), P(EncodingChoice)]),
+    "rq_encode": (C.c_int, [vp, vp, P(EncodingChoice), P(vp)]),
+    "rq_sort_table": (C.c_int, [vp, P(vp), i32, P(i32), i32, P(vp)]),
     "rq_bucketize": (C.c_int, [vp, vp, vp, i32, P(vp)]),
     "rq_decode_values": (C.c_int, [vp, vp, P(vp)]),
     "rq_normalize_basic": (C.c_int, [vp, vp, P(vp)]),

@@ -161,6 +161,68 @@ int rq_plain_to_rle_index(rq_ctx_t c, rq_col_t plain, int64_t min_run, rq_col_t*
   return api_guard([&] { *out = wrap_col(plain_to_rle_index(ctx_of(c), col_of(plain), min_run)); });
 }
 
+int rq_plain_to_plain_index(rq_ctx_t c, rq_col_t plain, double trim, rq_col_t* out) {
+  return api_guard([&] { *out = wrap_col(plain_to_plain_index(ctx_of(c), col_of(plain), trim)); });
+}
+
+void rq_heuristic_default(rq_heuristic* cfg) {
+  if (!cfg) return;
+  const HeuristicD d;
+  cfg->row_threshold = d.row_threshold;
+  cfg->ratio_threshold = d.ratio_threshold;
+  cfg->trim = d.trim;
+  cfg->min_run = d.min_run;
+  cfg->unit_run_share = d.unit_run_share;
+}
+
+int rq_choose_encoding(rq_ctx_t c, rq_col_t plain, const rq_heuristic* cfg, rq_encoding_choice* out) {
+  return api_guard([&] {
+    require(out != nullptr, "choose_encoding: null output");
+    HeuristicD h;
+    if (cfg) {
+      h.row_threshold = cfg->row_threshold;
+      h.ratio_threshold = cfg->ratio_threshold;
+      h.trim = cfg->trim;
+      h.min_run = cfg->min_run;
+      h.unit_run_share = cfg->unit_run_share;
+    }
+    const EncodingChoiceD ch = choose_encoding(ctx_of(c), col_of(plain), h);
+    out->scheme = ch.scheme;
+    out->width = ch.width;
+    out->min_run = ch.min_run;
+    out->trim_fraction = ch.trim;
+    out->has_center = ch.has_center ? 1 : 0;
+    out->_pad = 0;
+    out->center = ch.center;
+  });
+}
+
+int rq_encode(rq_ctx_t c, rq_col_t plain, const rq_encoding_choice* choice, rq_col_t* out) {
+  return api_guard([&] {
+    require(choice != nullptr, "encode: null choice");
+    EncodingChoiceD ch;
+    ch.scheme = choice->scheme;
+    ch.width = choice->width;
+    ch.min_run = choice->min_run;
+    ch.trim = choice->trim_fraction;
+    ch.has_center = choice->has_center != 0;
+    ch.center = choice->center;
+    *out = wrap_col(encode_column(ctx_of(c), col_of(plain), ch));
+  });
+}
+
+int rq_sort_table(rq_ctx_t c, const rq_col_t* cols, int32_t ncols, const int32_t* by, int32_t nby,
+                  rq_col_t* out) {
+  return api_guard([&] {
+    require(ncols > 0 && cols && out, "sort_table: no columns");
+    require(nby > 0 && by, "sort_table: no sort columns");
+    std::vector<const DCol*> in;
+    for (int32_t i = 0; i < ncols; ++i) in.push_back(&col_of(cols[i]));
+    std::vector<DCol> res = sort_table(ctx_of(c), in, std::vector<int>(by, by + nby));
+    for (int32_t i = 0; i < ncols; ++i) out[i] = wrap_col(std::move(res[i]));
+  });
+}
+
 int rq_normalize_basic(rq_ctx_t c, rq_col_t col, rq_col_t* out) {
   return api_guard([&] {
     auto ctx = ctx_of(c);

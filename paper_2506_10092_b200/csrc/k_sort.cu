@@ -278,47 +278,51 @@ void radix_sort_pairs(const CtxPtr& ctx, DArr& keys, DArr& vals, int bits, uint6
   }
 }
 
-SortedGroups group_ids_sorted(const CtxPtr& ctx, const std::vector<DArr>& keyvals) {
-  const int nk = static_cast<int>(keyvals.size());
-  require(nk >= 1 && nk <= 8, "group: 1..8 key columns");
-  const int64_t n = keyvals[0].n;
-  SortedGroups g;
-  g.inverse = alloc_arr(ctx, RQ_I64, n);
-  if (n == 0) {
-    g.first_rows = alloc_arr(ctx, RQ_I64, 0);
-    return g;
-  }
+namespace {
+
+struct SortPlan {
   dev::PackSpec ps{};
-  ps.nk = nk;
-  std::vector<uint64_t> mn(nk);
-  std::vector<int> bits(nk);
+  std::vector<uint64_t> mn;
+  std::vector<int> bits;
+};
+
+// stable lexicographic permutation of rows by the key columns
+DArr sort_perm_impl(const CtxPtr& ctx, const std::vector<DArr>& keyvals, SortPlan& sp) {
+  const int nk = static_cast<int>(keyvals.size());
+  require(nk >= 1 && nk <= 8, "sort: 1..8 key columns");
+  const int64_t n = keyvals[0].n;
+  for (const auto& k : keyvals) require(k.n == n, "sort: key column length mismatch");
+  sp.ps.nk = nk;
+  sp.mn.assign(nk, 0);
+  sp.bits.assign(nk, 0);
+  DArr perm = iota(ctx, n);
+  if (n <= 1) return perm;
   int total_bits = 0;
   for (int c = 0; c < nk; ++c) {
     uint64_t lo, hi;
     key_minmax(ctx, keyvals[c], lo, hi);
-    mn[c] = lo;
-    bits[c] = sig_bits(hi - lo);
-    total_bits += bits[c];
-    ps.v[c] = keyvals[c].raw();
-    ps.dt[c] = keyvals[c].dt;
-    ps.mn[c] = lo;
+    sp.mn[c] = lo;
+    sp.bits[c] = sig_bits(hi - lo);
+    total_bits += sp.bits[c];
+    sp.ps.v[c] = keyvals[c].raw();
+    sp.ps.dt[c] = keyvals[c].dt;
+    sp.ps.mn[c] = lo;
   }
-  DArr perm = iota(ctx, n);
   if (total_bits <= 64) {
     // one packed word, most significant field = first key column
     int at = 0;
     for (int c = nk; c-- > 0;) {
-      ps.shift[c] = at;
-      at += bits[c];
+      sp.ps.shift[c] = at;
+      at += sp.bits[c];
     }
     DArr packed = alloc_arr(ctx, RQ_I64, n);
-    dev::k_pack_keys<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ps, n, packed.as<uint64_t>());
+    dev::k_pack_keys<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(sp.ps, n, packed.as<uint64_t>());
     launched(ctx);
     radix_sort_pairs(ctx, packed, perm, total_bits, 0);
   } else {
     // LSD over columns: stable sort by the last column first
     for (int c = nk; c-- > 0;) {
-      if (bits[c] == 0) continue;
+      if (sp.bits[c] == 0) continue;
       DArr img = alloc_arr(ctx, RQ_I64, n);
       DArr mm = alloc_arr(ctx, RQ_I64, 2);
       const uint64_t init[2] = {~0ull, 0};
@@ -327,9 +331,30 @@ SortedGroups group_ids_sorted(const CtxPtr& ctx, const std::vector<DArr>& keyval
           keyvals[c].raw(), keyvals[c].dt, perm.pos(), n, img.as<uint64_t>(),
           reinterpret_cast<unsigned long long*>(mm.raw_mut()));
       launched(ctx);
-      radix_sort_pairs(ctx, img, perm, bits[c], mn[c]);
+      radix_sort_pairs(ctx, img, perm, sp.bits[c], sp.mn[c]);
     }
   }
+  return perm;
+}
+
+}  // namespace
+
+DArr sort_permutation(const CtxPtr& ctx, const std::vector<DArr>& keyvals) {
+  SortPlan sp;
+  return sort_perm_impl(ctx, keyvals, sp);
+}
+
+SortedGroups group_ids_sorted(const CtxPtr& ctx, const std::vector<DArr>& keyvals) {
+  const int64_t n = keyvals.empty() ? 0 : keyvals[0].n;
+  SortedGroups g;
+  g.inverse = alloc_arr(ctx, RQ_I64, n);
+  if (n == 0) {
+    g.first_rows = alloc_arr(ctx, RQ_I64, 0);
+    return g;
+  }
+  SortPlan sp;
+  DArr perm = sort_perm_impl(ctx, keyvals, sp);
+  const dev::PackSpec& ps = sp.ps;
   DArr flags = alloc_arr(ctx, RQ_I64, n), fbytes = alloc_arr(ctx, RQ_I8, n);
   dev::k_group_bounds<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ps, perm.pos(), n, flags.as<int64_t>(),
                                                                  fbytes.as<uint8_t>());

@@ -310,11 +310,33 @@ struct SortedGroups {
   int64_t n_groups = 0;
 };
 SortedGroups group_ids_sorted(const CtxPtr& ctx, const std::vector<DArr>& keyvals);
+// stable lexicographic row permutation (sort_table's comparator, ingest.cpp:318-333)
+DArr sort_permutation(const CtxPtr& ctx, const std::vector<DArr>& keyvals);
 void radix_sort_pairs(const CtxPtr& ctx, DArr& keys, DArr& vals, int bits, uint64_t sub);
 void scan_exclusive_i64(const CtxPtr& ctx, const DArr& in, DArr& out);
 // encoders (k_encode.cu): enc::plain_to_rle / plain_to_rle_index
 DCol plain_to_rle(const CtxPtr& ctx, const DCol& c);
 DCol plain_to_rle_index(const CtxPtr& ctx, const DCol& c, int64_t min_run);
+DCol plain_to_plain_index(const CtxPtr& ctx, const DCol& c, double trim);
+struct HeuristicD {  // io::HeuristicConfig (ingest.hpp:41-48)
+  int64_t row_threshold = 1000000;
+  double ratio_threshold = 20.0;
+  double trim = 0.05;
+  int64_t min_run = 2;
+  double unit_run_share = 0.5;
+};
+struct EncodingChoiceD {  // io::EncodingChoice (ingest.hpp:33-39)
+  int32_t scheme = RQ_SCHEME_PLAIN;
+  int32_t width = RQ_I64;
+  int64_t min_run = 2;
+  double trim = 0.05;
+  bool has_center = false;
+  int64_t center = 0;
+};
+EncodingChoiceD choose_encoding(const CtxPtr& ctx, const DCol& c, const HeuristicD& cfg);
+DCol encode_column(const CtxPtr& ctx, const DCol& c, const EncodingChoiceD& ch);
+std::vector<DCol> sort_table(const CtxPtr& ctx, const std::vector<const DCol*>& cols,
+                             const std::vector<int>& by);
 DArr starts_from_ends(const CtxPtr& ctx, const DArr& e);  // gapless RLE starts
 void scatter_values(const CtxPtr& ctx, DArr& dst, const DArr& idx, const DArr& src);
 

@@ -238,6 +238,32 @@ class Scalar(C.Structure):
     _fields_ = [("is_float", C.c_int32), ("_pad", C.c_int32), ("i", C.c_int64), ("f", C.c_double)]
 
 
+# runq::io::Scheme (ingest.hpp:29)
+SCHEME_PLAIN, SCHEME_PLAIN_CENTERED, SCHEME_RLE, SCHEME_RLE_INDEX, SCHEME_PLAIN_INDEX = range(5)
+SCHEME_NAMES = {"plain": 0, "plain-centered": 1, "rle": 2, "rle+index": 3, "plain+index": 4}
+
+
+class Heuristic(C.Structure):
+    """runq::io::HeuristicConfig (ingest.hpp:41-48), reference defaults."""
+    _fields_ = [("row_threshold", C.c_int64), ("ratio_threshold", C.c_double), ("trim", C.c_double),
+                ("min_run", C.c_int64), ("unit_run_share", C.c_double)]
+
+    def __init__(self, row_threshold=1_000_000, ratio_threshold=20.0, trim=0.05, min_run=2,
+                 unit_run_share=0.5):
+        super().__init__(row_threshold, ratio_threshold, trim, min_run, unit_run_share)
+
+
+class EncodingChoice(C.Structure):
+    """runq::io::EncodingChoice (ingest.hpp:33-39)."""
+    _fields_ = [("scheme", C.c_int32), ("width", C.c_int32), ("min_run", C.c_int64),
+                ("trim_fraction", C.c_double), ("has_center", C.c_int32), ("_pad", C.c_int32),
+                ("center", C.c_int64)]
+
+    def as_tuple(self):
+        return (self.scheme, self.width, self.min_run, self.trim_fraction,
+                self.center if self.has_center else None)
+
+
 def make_scalar(k) -> Scalar:
     """runq::compute::Scalar = variant<int64_t, double> (align.hpp:76)."""
     if isinstance(k, (float, np.floating)):

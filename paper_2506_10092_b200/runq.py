@@ -310,6 +310,67 @@ class enc:
         return _out(DeviceColumn(o, ctx), host)
 
 
+    @staticmethod
+    def plain_to_plain_index(c, trim_fraction: float):
+        """enc::plain_to_plain_index (primitives.cpp:293-347)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        o = _new()
+        check(_L.rq_plain_to_plain_index(ctx.handle, dc.handle, float(trim_fraction), C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+
+class io:
+    """runq::io encoding selection and table sort (ingest.hpp:29-66), on the device."""
+    Heuristic = H.Heuristic
+    EncodingChoice = H.EncodingChoice
+
+    @staticmethod
+    def choose_encoding(c, cfg: "H.Heuristic" = None) -> "H.EncodingChoice":
+        """io::choose_encoding (ingest.cpp:217-271)."""
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        out = H.EncodingChoice()
+        check(_L.rq_choose_encoding(ctx.handle, dc.handle, C.byref(cfg) if cfg is not None else None,
+                                    C.byref(out)))
+        return out
+
+    @staticmethod
+    def encode(c, choice: "H.EncodingChoice"):
+        """io::encode (ingest.cpp:273-290)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        o = _new()
+        check(_L.rq_encode(ctx.handle, dc.handle, C.byref(choice), C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
+    def sort_table(cols, by):
+        """io::sort_table (ingest.cpp:292-344): cols is a list of plain
+        columns (or a dict name -> column), by the key column indices (or names)."""
+        names = None
+        if isinstance(cols, dict):
+            names = list(cols)
+            by = [names.index(b) if isinstance(b, str) else b for b in by]
+            cols = [cols[k] for k in names]
+        host = _is_host(*cols)
+        ctx = _ctx_of(*cols)
+        dcs = [upload(c, ctx) for c in cols]
+        handles = (C.c_void_p * len(dcs))(*[d.handle for d in dcs])
+        bys = (C.c_int32 * len(by))(*by)
+        outs = (C.c_void_p * len(dcs))()
+        check(_L.rq_sort_table(ctx.handle, handles, len(dcs), bys, len(by), outs))
+        res = [_out(DeviceColumn(C.c_void_p(h), ctx), host) for h in outs]
+        return dict(zip(names, res)) if names is not None else res
+
+    @staticmethod
+    def encode_table(cols: dict, cfg: "H.Heuristic" = None) -> dict:
+        """io::encode_table (ingest.cpp:346-357): choose + encode per column."""
+        return {k: io.encode(c, io.choose_encoding(c, cfg)) for k, c in cols.items()}
+
+
 class kernels:
     @staticmethod
     def bucketize(x, boundaries, right: bool):

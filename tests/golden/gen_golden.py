@@ -216,6 +216,54 @@ def main():
         add(f"plain_to_rle_index_rand{it}", "plain_to_rle_index", {"a": enc_col(c), "min_run": mr},
             {"col": enc_col(ref.plain_to_rle_index(c, mr))}, "seeded")
 
+    # --- plain_to_plain_index / choose_encoding / encode / sort_table ----------------
+    big = 10_000_000_000
+    for name, vals, trim, line in (
+            ("wide_outliers", [1, 2, 3, big, big], 0.4, "259-270"),
+            ("no_outliers", [5, 6, 7, 8], 0.05, "272-275"),
+            ("constant", [9, 9, 9], 0.05, "277-280")):
+        c = H.PlainColumn(np.array(vals, np.int64))
+        r = ref.plain_to_plain_index(c, trim)
+        add(f"plain_to_plain_index_{name}", "plain_to_plain_index", {"a": enc_col(c), "trim": trim},
+            {"col": enc_col(r)}, f"proj/tests/test_primitives.cpp:{line}")
+    assert ref.plain_to_plain_index(H.PlainColumn(np.array([9, 9, 9], np.int64)), 0.05).base.values.dtype == np.int8
+    for it in range(6):
+        n = int(erng.integers(100, 2000))
+        vals = erng.integers(-30_000, 30_000, n)
+        vals[erng.random(n) < 0.02] = erng.integers(1_000_000, 2_000_000_000)
+        c = H.PlainColumn(vals.astype(np.int32), H.I64, 7 if it % 2 else None)
+        trim = float(erng.choice([0.0, 0.01, 0.05, 0.2]))
+        add(f"plain_to_plain_index_rand{it}", "plain_to_plain_index", {"a": enc_col(c), "trim": trim},
+            {"col": enc_col(ref.plain_to_plain_index(c, trim))}, "seeded")
+    # encoding cascade on small columns (row_threshold lowered so every branch fires)
+    cfg = H.Heuristic(row_threshold=64)
+    n = 4000
+    cascade = {
+        "rle": np.repeat(np.arange(4), n // 4),
+        "rle_index": np.concatenate([np.repeat(np.arange(2), n // 4), 100 + np.arange(n // 2) % 2]),
+        "plain_index": np.where(erng.random(n) < 0.01, 1_500_000_000, erng.integers(-30_000, 30_000, n)),
+        "plain_centered": erng.integers(1_000_000, 1_000_100, n),
+        "plain": erng.integers(-(1 << 40), 1 << 40, n),
+        "float": erng.uniform(0, 1, n),
+    }
+    for name, vals in cascade.items():
+        c = H.PlainColumn(vals)
+        ch = ref.choose_encoding(c, cfg)
+        add(f"choose_encoding_{name}", "choose_encoding", {"a": enc_col(c), "row_threshold": 64},
+            {"choice": list(ch.as_tuple()), "col": enc_col(ref.encode(c, ch))}, "ingest.cpp:217-290")
+    assert ref.choose_encoding(H.PlainColumn(np.zeros(100, np.int64))).scheme == H.SCHEME_PLAIN  # test_ingest.cpp:88-92
+    k = np.arange(3000) % 3
+    cols = [H.PlainColumn(k), H.PlainColumn(np.arange(3000, dtype=np.int32)),
+            H.PlainColumn(erng.uniform(-1, 1, 3000))]
+    out = ref.sort_table(cols, [0])
+    assert len(ref.plain_to_rle(out[0]).s) == 3  # test_ingest.cpp:150-168
+    add("sort_table_mod3", "sort_table", {"cols": [enc_col(c) for c in cols], "by": [0]},
+        {"cols": [enc_col(c) for c in out]}, "proj/tests/test_ingest.cpp:150-168")
+    cols = [H.PlainColumn(erng.integers(0, 4, 500).astype(np.int8), H.I64, 10),
+            H.PlainColumn(erng.choice([-0.0, 0.0, 1.5, -2.0], 500)), H.PlainColumn(np.arange(500))]
+    add("sort_table_two_keys", "sort_table", {"cols": [enc_col(c) for c in cols], "by": [1, 0]},
+        {"cols": [enc_col(c) for c in ref.sort_table(cols, [1, 0])]}, "ingest.cpp:292-344")
+
     # --- seeded random primitive instances ----------------------------------------
     rng = np.random.default_rng(2506_10092)
     for it in range(12):

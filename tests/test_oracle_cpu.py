@@ -144,3 +144,25 @@ def test_orq_streaming_c1_c2_vs_reference(ref, orq):
             m = ref.compare_scalar(c2, G.C2_K, "<")
             want = ref.aggregate_all(ref.arith(ref.filter(a2, m), ref.filter(b2, m), "*"), "sum")
             assert orq.filtered_sum(c2, G.C2_K, "<", a2, b2, "*") == want
+
+
+@pytest.mark.parametrize("case", by_fn("plain_to_plain_index", "choose_encoding", "sort_table",
+                                       "plain_to_rle", "plain_to_rle_index"), ids=lambda c: c["name"])
+def test_ref_ingest_golden(ref, case):
+    """The reference library reproduces its own committed ingest fixtures."""
+    from helpers import assert_column
+    i, x = case["inputs"], case["expected"]
+    fn = case["fn"]
+    if fn == "sort_table":
+        for g, w in zip(ref.sort_table([col(c) for c in i["cols"]], i["by"]), x["cols"]):
+            assert_column(g, col(w))
+    elif fn == "choose_encoding":
+        ch = ref.choose_encoding(col(i["a"]), H.Heuristic(row_threshold=i["row_threshold"]))
+        assert list(ch.as_tuple()) == x["choice"]
+        assert_column(ref.encode(col(i["a"]), ch), col(x["col"]))
+    elif fn == "plain_to_plain_index":
+        assert_column(ref.plain_to_plain_index(col(i["a"]), i["trim"]), col(x["col"]))
+    elif fn == "plain_to_rle":
+        assert_column(ref.plain_to_rle(col(i["a"])), col(x["col"]))
+    else:
+        assert_column(ref.plain_to_rle_index(col(i["a"]), i["min_run"]), col(x["col"]))
