@@ -64,6 +64,7 @@ Ctx::~Ctx() {
   for (auto e : event_pool) cudaEventDestroy(e);
   if (tile_status) cudaFree(tile_status);
   if (scratch) cudaFree(scratch);
+  if (tickets) cudaFree(tickets);
   if (pinned) cudaFreeHost(pinned);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -148,6 +149,7 @@ DArr alloc_arr(const CtxPtr& ctx, int32_t dt, int64_t n) {
     b->ctx = ctx;
     b->bytes = static_cast<size_t>(n) * dt_width(dt);
     b->ptr = ctx->alloc(b->bytes);
+    b->cap = (b->bytes + 255) & ~size_t(255);
     a.buf = std::move(b);
   }
   return a;
@@ -229,6 +231,8 @@ int rq_ctx_create(int device, rq_ctx_t* out) {
     RQ_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
     ctx->sm_count = prop.multiProcessorCount;
     RQ_CUDA_CHECK(cudaMallocHost(&ctx->pinned, 4096));
+    RQ_CUDA_CHECK(cudaMalloc(&ctx->tickets, 256));
+    RQ_CUDA_CHECK(cudaMemsetAsync(ctx->tickets, 0, 256, ctx->stream));
     // keep freed blocks cached in the stream-ordered pool (no trim between ops)
     cudaMemPool_t pool;
     RQ_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -298,6 +302,7 @@ int rq_arr_wrap_device(rq_ctx_t c, int32_t dtype, void* dev, int64_t n, rq_arr_t
       b->ctx = ctx;
       b->ptr = dev;
       b->bytes = static_cast<size_t>(n) * dt_width(dtype);
+      b->cap = b->bytes;
       b->owned = false;
       a.buf = std::move(b);
     }

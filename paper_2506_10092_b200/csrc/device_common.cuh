@@ -19,6 +19,9 @@ constexpr int64_t KEY_MAX = INT64_MAX;
 // ---- dtype-tagged loads (runq::Array::to_i64 / to_f64, array.cpp:44-61) ---------
 
 __device__ __forceinline__ bool dt_is_float_dev(int dt) { return dt == RQ_F32 || dt == RQ_F64; }
+__device__ __forceinline__ int dt_width_dev(int dt) {
+  return dt == RQ_I8 ? 1 : dt == RQ_I16 ? 2 : (dt == RQ_I32 || dt == RQ_F32) ? 4 : 8;
+}
 
 __device__ __forceinline__ int64_t ld_i64(const void* p, int dt, int64_t i) {
   switch (dt) {
@@ -346,6 +349,62 @@ __device__ __forceinline__ int64_t lower_bound_g(const int64_t* __restrict__ a, 
 
 __device__ __forceinline__ int64_t ldg64(const int64_t* p, int64_t i) {
   return __ldg(reinterpret_cast<const long long*>(p) + i);
+}
+
+// ---- TMA 1-D bulk copies (cp.async.bulk → UBLKCP) completing on an mbarrier ----
+// Source and destination 16-B aligned, size a multiple of 16 B. A CTA launched
+// without a cluster is its own cluster, so the shared::cluster destination
+// form addresses this CTA's shared memory.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// orders this thread's generic-proxy shared-memory accesses before later
+// async-proxy (bulk copy) writes to the same bytes
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Branch-free lower_bound over a shared-memory array of n >= 1 sorted int64
+// (first index with a[i] >= key, n if none). The trip count depends on n
+// only, so every lane of a CTA runs the same steps; no padding is needed.
+__device__ __forceinline__ int smem_lower_bound(const int64_t* a, int n, int64_t key) {
+  int base = 0;
+  while (n > 1) {
+    const int half = n >> 1;
+    base = a[base + half] < key ? base + half : base;
+    n -= half;
+  }
+  return base + (a[base] < key ? 1 : 0);
 }
 
 }  // namespace dev

@@ -428,6 +428,392 @@ __global__ void __launch_bounds__(BLOCK)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent TMA variant (the production path when every buffer is 16-B
+// aligned). Each CTA owns a CONTIGUOUS range of point tiles, so the first
+// A/C run a tile can touch is the run of the previous tile's last point:
+// one warp-level search per CTA replaces the per-tile partition pass, and
+// the tile windows are chained forward. Per tile, one elected thread issues
+// 1-D bulk copies (cp.async.bulk, completing on an mbarrier) of the tile's
+// points and B values, A's run-end window and C's run-end + value window, in
+// the stored int64 / storage-width form (no register staging, no
+// conversion); lanes then resolve ITEMS consecutive points each with one
+// branch-free shared-memory lower_bound and short forward scans. The window
+// length is predicted from the previous tile's span (×1.25 + 32, at most
+// AW / CW runs); a point past a window's last staged run falls back to a
+// global search, so the prediction affects only speed. The per-CTA partials
+// are folded by the last CTA to finish (ticket counter that wraps back to 0),
+// in a fixed order.
+// ---------------------------------------------------------------------------
+
+template <class T>
+__device__ __forceinline__ T lds_as(const unsigned char* base, int dt, int i);
+template <>
+__device__ __forceinline__ int64_t lds_as<int64_t>(const unsigned char* b, int dt, int i) {
+  switch (dt) {
+    case RQ_I8: return reinterpret_cast<const int8_t*>(b)[i];
+    case RQ_I16: return reinterpret_cast<const int16_t*>(b)[i];
+    case RQ_I32: return reinterpret_cast<const int32_t*>(b)[i];
+    case RQ_I64: return reinterpret_cast<const int64_t*>(b)[i];
+    case RQ_F32: return static_cast<int64_t>(reinterpret_cast<const float*>(b)[i]);
+    default: return static_cast<int64_t>(reinterpret_cast<const double*>(b)[i]);
+  }
+}
+template <>
+__device__ __forceinline__ double lds_as<double>(const unsigned char* b, int dt, int i) {
+  switch (dt) {
+    case RQ_I8: return reinterpret_cast<const int8_t*>(b)[i];
+    case RQ_I16: return reinterpret_cast<const int16_t*>(b)[i];
+    case RQ_I32: return reinterpret_cast<const int32_t*>(b)[i];
+    case RQ_I64: return static_cast<double>(reinterpret_cast<const int64_t*>(b)[i]);
+    case RQ_F32: return reinterpret_cast<const float*>(b)[i];
+    default: return reinterpret_cast<const double*>(b)[i];
+  }
+}
+
+// c_run_pass on a value staged in shared memory
+__device__ __forceinline__ bool c_smem_pass(const CSpec& c, const unsigned char* sv, int idx) {
+  if (c.dt == RQ_I64 && !c.k_float) {  // dictionary codes as int64 (the common case)
+    const int64_t x = reinterpret_cast<const int64_t*>(sv)[idx];
+    return (c.opmask >> (x < c.ki ? 0 : (x == c.ki ? 1 : 2))) & 1;
+  }
+  int cls;
+  if (c.k_float || dt_is_float_dev(c.dt)) {
+    const double x = lds_as<double>(sv, c.dt, idx);
+    const double k = c.k_float ? c.kf : static_cast<double>(c.ki);
+    if (x != x || k != k) return c.cmp == RQ_NE;
+    cls = x < k ? 0 : (x == k ? 1 : 2);
+  } else {
+    const int64_t x = lds_as<int64_t>(sv, c.dt, idx);
+    cls = x < c.ki ? 0 : (x == c.ki ? 1 : 2);
+  }
+  return (c.opmask >> cls) & 1;
+}
+
+struct TmaWin {
+  int64_t lo16;  // first staged run (multiple of 16)
+  int n;         // staged runs
+};
+
+__device__ __forceinline__ TmaWin tma_window(int64_t lo, int est, int cap, int64_t total) {
+  TmaWin w;
+  w.lo16 = lo & ~int64_t(15);
+  int64_t n = static_cast<int64_t>(est) + (lo - w.lo16);
+  if (n > cap) n = cap;
+  if (n > total - w.lo16) n = total - w.lo16;
+  w.n = n > 0 ? static_cast<int>(n) : 0;
+  return w;
+}
+__device__ __forceinline__ uint32_t ceil16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// lower_bound over a shared-memory window padded with INT64_MAX up to the
+// power of two L (uniform per CTA; L <= CAP): log2(L) steps of
+// load / compare / select / add, no bounds tests
+template <int CAP>
+__device__ __forceinline__ int smem_lb_pow2(const int64_t* a, int L, int64_t key) {
+  int pos = 0;
+#pragma unroll
+  for (int step = CAP / 2; step > 0; step >>= 1)
+    if (step < L) pos = a[pos + step - 1] < key ? pos + step : pos;
+  return pos + (a[pos] < key ? 1 : 0);
+}
+__device__ __forceinline__ int pow2_above(int n) {  // smallest power of two > n (n >= 0)
+  return n > 0 ? 1 << (32 - __clz(n)) : 1;
+}
+
+// one pipeline stage: A's run-end window, C's run-end window and C's values
+template <int AW, int CW>
+struct C2Stage {
+  // staged runs n < W (W a power of two), padded with INT64_MAX up to the
+  // power of two above n (<= W); + 16 for the bulk copy's round-up
+  static constexpr int A_CAP = AW + 16;  // >= max(ceil16(AW - 1), AW + 8)
+  static constexpr int C_CAP = CW + 16;
+  static constexpr size_t A_OFF = 0;
+  static constexpr size_t C_OFF = A_OFF + A_CAP * 8;
+  static constexpr size_t CV_OFF = C_OFF + C_CAP * 8;
+  static constexpr size_t BYTES = CV_OFF + C_CAP * 8;
+};
+
+template <int BLOCK, int ITEMS>
+__device__ __forceinline__ void load_keys(const int64_t* __restrict__ P, int64_t np, int64_t q0,
+                                          int64_t (&k)[ITEMS]) {
+  static_assert(ITEMS % 2 == 0, "pairs of points per 128-bit load");
+  if (q0 + ITEMS <= np) {
+#pragma unroll
+    for (int j = 0; j < ITEMS; j += 2) {
+      const longlong2 v = __ldg(reinterpret_cast<const longlong2*>(P + q0 + j));
+      k[j] = v.x;
+      k[j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) k[j] = q0 + j < np ? ldg64(P, q0 + j) : INT64_MAX;
+  }
+}
+
+template <int BLOCK, int ITEMS, int AW, int CW, class T, int OP, int CK, bool SAME>
+__global__ void __launch_bounds__(BLOCK, 4)
+    k_points_filtered_reduce_tma(const int64_t* __restrict__ P, const void* __restrict__ yv, int ydt,
+                                 int64_t np, XSpec x, CSpec c, int64_t ntiles, int swap,
+                                 AggPart* __restrict__ parts, unsigned* __restrict__ ticket,
+                                 AggPart* __restrict__ out, int* __restrict__ err) {
+  constexpr int NCW = BLOCK / 32 - 1;  // consumer warps; warp 0 produces
+  constexpr int TILE = NCW * 32 * ITEMS;
+  constexpr bool HAS_C = CK != C_PLAIN;
+  using S = C2Stage<AW, CW>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[2], empty[2];
+  __shared__ int64_t s_lo[2][2];  // [stage][A, C] first staged run
+  __shared__ int s_n[2][2];       // [stage][A, C] staged runs
+
+  const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * ntiles / gridDim.x;
+  const int64_t t_end = static_cast<int64_t>(blockIdx.x + 1) * ntiles / gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wc = HAS_C ? dt_width_dev(c.dt) : 1;
+  auto sA = [&](int st) { return reinterpret_cast<int64_t*>(smem + st * S::BYTES + S::A_OFF); };
+  auto sC = [&](int st) { return reinterpret_cast<int64_t*>(smem + st * S::BYTES + S::C_OFF); };
+  auto sCv = [&](int st) { return smem + st * S::BYTES + S::CV_OFF; };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 32);  // every producer lane arrives (releasing its own stores)
+    mbar_init(&full[1], 32);
+    mbar_init(&empty[0], NCW);
+    mbar_init(&empty[1], NCW);
+  }
+  __syncthreads();
+
+  uint64_t isum = 0;
+  double fsum = 0.0;
+  int64_t cnt = 0;
+  int lerr = 0;
+  if (wid == 0) {
+    // ---- producer warp: window chain + staging -------------------------------
+    // Tile t's windows start at the runs of its first point, ranked in tile
+    // t-1's (landed, padded) windows — a global warp search only when the
+    // point lies past them. Full 16-run chunks are bulk-copied; the tail
+    // chunk at a column's end and the INT64_MAX pad up to the power-of-two
+    // capacity (+8 for the fixed-width forward steps) are written by the
+    // lanes, outside the copied range, before the arrive that publishes them.
+    int64_t a_cur = 0, c_cur = 0, a_lo16 = 0, c_lo16 = 0;
+    int a_est = AW, c_est = CW, a_n = 0, c_n = 0;
+    int64_t pf = t_begin < t_end ? ldg64(P, t_begin * TILE) : 0;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int st = static_cast<int>((t - t_begin) & 1);
+      const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
+      const int64_t p_first = pf;
+      if (t + 1 < t_end) pf = ldg64(P, (t + 1) * TILE);
+      if (t == t_begin) {
+        a_cur = warp_lower_bound(x.e, x.n, p_first);
+        if (HAS_C) c_cur = warp_lower_bound(c.e, c.n, p_first);
+      } else {
+        mbar_wait(&full[st ^ 1], ((t - 1 - t_begin) >> 1) & 1);  // tile t-1 landed
+        const int ra = smem_lb_pow2<AW>(sA(st ^ 1), AW, p_first);
+        int64_t an = a_lo16 + ra;
+        if (ra >= a_n && an < x.n) an += warp_lower_bound(x.e + an, x.n - an, p_first);
+        const int64_t ua = an - a_cur;  // runs spanned by tile t-1
+        a_est = static_cast<int>(min(static_cast<int64_t>(AW), ua + (ua >> 2) + 32));
+        a_cur = an;
+        if (HAS_C) {
+          const int rc = smem_lb_pow2<CW>(sC(st ^ 1), CW, p_first);
+          int64_t cn = c_lo16 + rc;
+          if (rc >= c_n && cn < c.n) cn += warp_lower_bound(c.e + cn, c.n - cn, p_first);
+          const int64_t uc = cn - c_cur;
+          c_est = static_cast<int>(min(static_cast<int64_t>(CW), uc + (uc >> 2) + 32));
+          c_cur = cn;
+        }
+      }
+      if (t - t_begin >= 2) mbar_wait(&empty[st], (use - 1) & 1);  // consumers done with tile t-2
+      // staged counts: whole 16-run chunks (< W), clipped at the column end
+      auto stage_n = [](int64_t lo, int est, int W, int64_t total, int64_t& lo16) {
+        lo16 = lo & ~int64_t(15);
+        int64_t n = static_cast<int64_t>(est) + (lo - lo16);
+        if (n > W - 16) n = W - 16;
+        n = (n + 15) & ~int64_t(15);
+        if (n > total - lo16) n = total - lo16;
+        return n > 0 ? static_cast<int>(n) : 0;
+      };
+      a_n = stage_n(a_cur, a_est, AW, x.n, a_lo16);
+      c_n = HAS_C ? stage_n(c_cur, c_est, CW, c.n, c_lo16) : 0;
+      int64_t* wA = sA(st);
+      int64_t* wC = sC(st);
+      unsigned char* wCv = sCv(st);
+      const int a_bulk = a_n & ~15, c_bulk = c_n & ~15;
+      for (int i = a_bulk + lane; i < a_n; i += 32) wA[i] = ldg64(x.e, a_lo16 + i);
+      for (int i = a_n + lane; i < AW + 8; i += 32) wA[i] = INT64_MAX;
+      if (HAS_C) {
+        for (int i = c_bulk + lane; i < c_n; i += 32) {
+          wC[i] = ldg64(c.e, c_lo16 + i);
+          const unsigned char* src = static_cast<const unsigned char*>(c.v) + (c_lo16 + i) * wc;
+          for (int j = 0; j < wc; ++j) wCv[i * wc + j] = src[j];
+        }
+        for (int i = c_n + lane; i < CW + 8; i += 32) wC[i] = INT64_MAX;
+      }
+      if (lane != 0) mbar_arrive(&full[st]);
+      if (lane == 0) {
+        s_lo[st][0] = a_lo16;
+        s_n[st][0] = a_n;
+        s_lo[st][1] = c_lo16;
+        s_n[st][1] = c_n;
+        const uint32_t ba = static_cast<uint32_t>(a_bulk) * 8u;
+        const uint32_t bc = static_cast<uint32_t>(c_bulk) * 8u;
+        const uint32_t bcv = static_cast<uint32_t>(c_bulk) * static_cast<uint32_t>(wc);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[st], ba + (HAS_C ? bc + bcv : 0u));
+        if (ba) bulk_g2s(wA, x.e + a_lo16, ba, &full[st]);
+        if (HAS_C && bc) {
+          bulk_g2s(wC, c.e + c_lo16, bc, &full[st]);
+          bulk_g2s(wCv, static_cast<const unsigned char*>(c.v) + c_lo16 * wc, bcv, &full[st]);
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---- consumer warps: ITEMS consecutive points per lane ---------------------
+    const int i0 = ((wid - 1) * 32 + lane) * ITEMS;
+    int64_t cur[ITEMS], nxt[ITEMS];
+    if (t_begin < t_end) load_keys<BLOCK, ITEMS>(P, np, t_begin * TILE + i0, cur);
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int st = static_cast<int>((t - t_begin) & 1);
+      const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
+      const int64_t tbase = t * TILE;
+      const int npt = static_cast<int>(np - tbase < TILE ? np - tbase : TILE);
+      if (t + 1 < t_end) load_keys<BLOCK, ITEMS>(P, np, tbase + TILE + i0, nxt);
+      mbar_wait(&full[st], use & 1u);
+      const int64_t a16 = s_lo[st][0], c16 = s_lo[st][1];
+      const int na = s_n[st][0], nc = s_n[st][1];
+      const int64_t* wA = sA(st);
+      const int64_t* wC = sC(st);
+
+      int ra[ITEMS], rc[ITEMS];
+      {  // both windows searched in one unrolled loop: two independent chains
+        int pa = 0, pc = 0;
+#pragma unroll
+        for (int step = AW / 2; step > 0; step >>= 1) {
+          pa = wA[pa + step - 1] < cur[0] ? pa + step : pa;
+          if (HAS_C && step < CW) pc = wC[pc + step - 1] < cur[0] ? pc + step : pc;
+        }
+        ra[0] = pa + (wA[pa] < cur[0] ? 1 : 0);
+        if (HAS_C) rc[0] = pc + (wC[pc] < cur[0] ? 1 : 0);
+      }
+      // forward from the previous point: a branch-free search over the next 8
+      // (A) / 4 (C) runs covers the usual gap between neighbouring points; the
+      // loop runs only for longer gaps (rare, so warps seldom diverge). The pad
+      // entries stop every scan.
+#pragma unroll
+      for (int k = 1; k < ITEMS; ++k) {
+        int r = ra[k - 1];
+        r = wA[r + 3] < cur[k] ? r + 4 : r;
+        r = wA[r + 1] < cur[k] ? r + 2 : r;
+        r = wA[r] < cur[k] ? r + 1 : r;
+        while (wA[r] < cur[k]) ++r;
+        ra[k] = r;
+        if (HAS_C) {
+          int q = rc[k - 1];
+          q = wC[q + 1] < cur[k] ? q + 2 : q;
+          q = wC[q] < cur[k] ? q + 1 : q;
+          while (wC[q] < cur[k]) ++q;
+          rc[k] = q;
+        }
+      }
+      int64_t arun[ITEMS];
+      bool take[ITEMS];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int64_t p = cur[k];
+        int64_t ar = a16 + ra[k];
+        if (ra[k] >= na && ar < x.n) ar = lb_window(x.e, ar, x.n, p);  // past the window
+        arun[k] = ar;
+        bool pass = i0 + k < npt && ar < x.n && (x.gapless || ldg64(x.s, ar) <= p);
+        if (CK == C_PLAIN) {
+          pass = pass && p < c.n && c_plain_pass(c, p);
+        } else {
+          int64_t cr = c16 + rc[k];
+          if (rc[k] >= nc) {
+            if (cr < c.n) cr = lb_window(c.e, cr, c.n, p);
+            pass = pass && cr < c.n && (CK == C_RLE_GAPLESS || ldg64(c.s, cr) <= p) && c_run_pass(c, cr);
+          } else {
+            pass = pass && (CK == C_RLE_GAPLESS || ldg64(c.s, cr) <= p) && c_smem_pass(c, sCv(st), rc[k]);
+          }
+        }
+        take[k] = pass;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);  // stage reads done (the gathers below are global)
+      T xa[ITEMS], yb[ITEMS];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int64_t q = tbase + i0 + k;
+        if (SAME) {
+          xa[k] = take[k] ? ld_same<T>(x.v, arun[k]) : T(0);
+          yb[k] = take[k] ? ld_same<T>(yv, q) : T(0);
+        } else {
+          xa[k] = take[k] ? ld_hot<T>(x.v, x.dt, arun[k]) : T(0);
+          yb[k] = take[k] ? ld_hot<T>(yv, ydt, q) : T(0);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        if (!take[k]) continue;
+        const T r = swap ? apply_op<T, OP>(yb[k], xa[k], &lerr) : apply_op<T, OP>(xa[k], yb[k], &lerr);
+        isum += static_cast<uint64_t>(static_cast<int64_t>(r));
+        fsum += static_cast<double>(r);
+        ++cnt;
+      }
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) cur[k] = nxt[k];
+    }
+  }
+  if (lerr) atomicOr(err, 1);
+
+  __shared__ uint64_t ru[BLOCK / 32 + 1];
+  __shared__ double rf[BLOCK / 32 + 1];
+  __shared__ uint64_t rn[BLOCK / 32 + 1];
+  __shared__ bool last;
+  isum = warp_sum(isum);
+  fsum = warp_sum(fsum);
+  uint64_t ucnt = warp_sum(static_cast<uint64_t>(cnt));
+  if (lane == 0) {
+    ru[wid] = isum;
+    rf[wid] = fsum;
+    rn[wid] = ucnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    AggPart pp{};
+    for (int w = 0; w < BLOCK / 32; ++w) {
+      pp.isum += ru[w];
+      pp.fsum += rf[w];
+      pp.cnt += static_cast<long long>(rn[w]);
+    }
+    parts[blockIdx.x] = pp;
+    __threadfence();
+    last = atomicInc(ticket, gridDim.x - 1) == gridDim.x - 1;  // wraps to 0 for the next launch
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the last CTA folds every partial in a fixed order
+  isum = 0;
+  fsum = 0.0;
+  ucnt = 0;
+  for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += BLOCK) {
+    isum += __ldcg(&parts[i].isum);
+    fsum += __ldcg(&parts[i].fsum);
+    ucnt += static_cast<uint64_t>(__ldcg(&parts[i].cnt));
+  }
+  isum = block_sum<BLOCK>(isum, ru);
+  fsum = block_sum<BLOCK>(fsum, rf);
+  ucnt = block_sum<BLOCK>(ucnt, rn);
+  if (threadIdx.x == 0) {
+    AggPart pp{};
+    pp.isum = isum;
+    pp.fsum = fsum;
+    pp.cnt = static_cast<long long>(ucnt);
+    pp.imin = atomicExch(err, 0);  // error flag travels with the result; reset for the next launch
+    *out = pp;
+  }
+}
+
 }  // namespace dev
 
 AggOut filtered_aggregate_binop_chain(const CtxPtr& ctx, const DCol& c, Scalar k, int cmp,
@@ -482,6 +868,80 @@ void launch1(int op, int ck, const CtxPtr& ctx, const FusedLaunch& f) {
   }
 }
 
+// ---- persistent TMA path ----
+constexpr int TB = 256, TI = 4, TAW = 2048, TCW = 512;
+using TmaSmem = dev::C2Stage<TAW, TCW>;
+constexpr size_t TMA_SMEM = 2 * TmaSmem::BYTES;
+
+struct TmaLaunch {
+  const DCol* y;
+  dev::XSpec xs;
+  dev::CSpec cs;
+  int64_t ntiles;
+  int swap;
+  dev::AggPart* parts;
+  unsigned* ticket;
+  dev::AggPart* out;
+  int* err;
+};
+
+// CTAs resident per SM for an instantiation (queried once; sets the
+// dynamic shared-memory limit on first use)
+template <class K>
+int tma_occupancy(K kernel) {
+  RQ_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(TMA_SMEM)));
+  int occ = 0;
+  RQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, TB, TMA_SMEM));
+  return occ > 0 ? occ : 1;
+}
+
+template <class T, int OP, int CK>
+int64_t launch_tma3(const CtxPtr& ctx, const TmaLaunch& f, bool dry) {
+  const int32_t tdt = std::is_same<T, double>::value ? RQ_F64 : RQ_I64;
+  const bool same = f.xs.dt == tdt && f.y->v.dt == tdt;
+  auto k_same = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, T, OP, CK, true>;
+  auto k_gen = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, T, OP, CK, false>;
+  static int occ_same = 0, occ_gen = 0;  // per instantiation
+  int& occ = same ? occ_same : occ_gen;
+  if (!occ) occ = tma_occupancy(same ? k_same : k_gen);
+  int64_t grid = static_cast<int64_t>(ctx->sm_count) * occ;
+  if (grid > f.ntiles) grid = f.ntiles;
+  if (dry) return grid;
+  (same ? k_same : k_gen)<<<static_cast<unsigned>(grid), TB, TMA_SMEM, ctx->stream>>>(
+      f.y->p.pos(), f.y->v.raw(), f.y->v.dt, f.y->p.n, f.xs, f.cs, f.ntiles, f.swap, f.parts, f.ticket,
+      f.out, f.err);
+  return grid;
+}
+
+template <class T, int OP>
+int64_t launch_tma2(int ck, const CtxPtr& ctx, const TmaLaunch& f, bool dry) {
+  switch (ck) {
+    case dev::C_RLE_GAPLESS: return launch_tma3<T, OP, dev::C_RLE_GAPLESS>(ctx, f, dry);
+    case dev::C_RLE_GAPPED: return launch_tma3<T, OP, dev::C_RLE_GAPPED>(ctx, f, dry);
+    default: return launch_tma3<T, OP, dev::C_PLAIN>(ctx, f, dry);
+  }
+}
+
+template <class T>
+int64_t launch_tma1(int op, int ck, const CtxPtr& ctx, const TmaLaunch& f, bool dry) {
+  switch (op) {
+    case RQ_ADD: return launch_tma2<T, RQ_ADD>(ck, ctx, f, dry);
+    case RQ_SUB: return launch_tma2<T, RQ_SUB>(ck, ctx, f, dry);
+    case RQ_MUL: return launch_tma2<T, RQ_MUL>(ck, ctx, f, dry);
+    default: return launch_tma2<T, RQ_DIV>(ck, ctx, f, dry);
+  }
+}
+
+// bulk copies need 16-B aligned bases and room to round a copy up to 16
+// elements inside the allocation
+bool tma_ok(const DArr& a) {
+  if (!a.buf || !a.buf->ptr) return a.n == 0;
+  const size_t w = static_cast<size_t>(dt_width(a.dt));
+  return (reinterpret_cast<uintptr_t>(a.buf->ptr) & 15) == 0 &&
+         a.buf->cap >= static_cast<size_t>((a.n + 15) & ~int64_t(15)) * w;
+}
+
 }  // namespace
 
 AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int cmp, const DCol& a,
@@ -520,7 +980,29 @@ AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int 
 
   const int64_t np = y.p.n;
   dev::AggPart res{};
-  if (np > 0 && xs.n > 0 && cs.n > 0) {
+  const bool use_tma = tma_ok(y.p) && tma_ok(y.v) && tma_ok(x.e) &&
+                       (ck == dev::C_PLAIN || (tma_ok(c.e) && tma_ok(c.v)));
+  if (np > 0 && xs.n > 0 && cs.n > 0 && use_tma) {
+    constexpr int64_t TILE = static_cast<int64_t>(TB - 32) * TI;  // warp 0 produces
+    const int64_t ntiles = (np + TILE - 1) / TILE;
+    TmaLaunch f{&y, xs, cs, ntiles, a.enc == RQ_ENC_RLE ? 0 : 1, nullptr, ctx->tickets, nullptr, nullptr};
+    const int64_t grid = flt ? launch_tma1<double>(op, ck, ctx, f, true) : launch_tma1<int64_t>(op, ck, ctx, f, true);
+    DArr parts = alloc_arr(ctx, RQ_I64, grid * static_cast<int64_t>(sizeof(dev::AggPart) / 8));
+    DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8);
+    f.parts = parts.as<dev::AggPart>();
+    f.out = out.as<dev::AggPart>();
+    f.err = reinterpret_cast<int*>(ctx->tickets + 1);  // zero between launches (the kernel resets it)
+    {
+      KTimer timer(ctx, "filtered_points_reduce");
+      if (flt) launch_tma1<double>(op, ck, ctx, f, false);
+      else launch_tma1<int64_t>(op, ck, ctx, f, false);
+      ctx->count_launch();
+      RQ_CUDA_CHECK(cudaGetLastError());
+    }
+    const int64_t* h = ctx->readback(out.raw(), sizeof(dev::AggPart));
+    res = *reinterpret_cast<const dev::AggPart*>(h);
+    if (!flt && op == RQ_DIV && res.imin) fail("integer division by zero");
+  } else if (np > 0 && xs.n > 0 && cs.n > 0) {
     constexpr int64_t TILE = static_cast<int64_t>(FB) * FI;
     const int64_t ntiles = (np + TILE - 1) / TILE;
     DArr apart = alloc_arr(ctx, RQ_I64, ntiles + 1);

@@ -73,6 +73,9 @@ struct Ctx {
   unsigned long long* tile_status = nullptr;
   int64_t tile_status_cap = 0;
   uint32_t epoch = 0;
+  // last-CTA-done ticket counters (zeroed once; every kernel using one
+  // leaves it at 0 again via atomicInc wrap-around)
+  unsigned* tickets = nullptr;
   // small device scratch for counters / reduction partials
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -134,6 +137,7 @@ struct Buffer {
   CtxPtr ctx;  // keeps the stream alive for the stream-ordered free
   void* ptr = nullptr;
   size_t bytes = 0;
+  size_t cap = 0;  // readable bytes from ptr (allocation rounded up to 256 B)
   bool owned = true;
   ~Buffer();
 };
