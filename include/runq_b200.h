@@ -354,6 +354,36 @@ int rq_filtered_aggregate_binop(rq_ctx_t ctx, rq_col_t c, rq_scalar k, int32_t c
                                 rq_col_t a, rq_col_t b, int32_t op, int32_t fn,
                                 int32_t* out_dtype, int64_t* out_i64, double* out_f64);
 
+/* One aggregate expression of the query runner's GroupAgg
+ * (runner.cpp:302-336 over the plan's arith / arith_scalar nodes,
+ * align.cpp:495-508, :571-596): a left-deep chain
+ * ((t0 ops[0] t1) ops[1] t2) of up to 3 terms; a term is `col` (op = -1) or
+ * `col op k` (`k op col` when reversed). n_terms = 0 is COUNT(*). */
+typedef struct rq_term {
+  rq_col_t col;
+  int32_t op;       /* RQ_ADD..RQ_DIV, or -1 for the bare column */
+  int32_t reversed; /* scalar on the left */
+  rq_scalar k;
+} rq_term;
+typedef struct rq_expr {
+  int32_t n_terms;
+  int32_t ops[2];
+  rq_term terms[3];
+} rq_expr;
+
+/* The runner's Filter → expressions → GroupAgg sequence (runner.cpp:243-336):
+ * every operand filtered by `mask` (NULL: no WHERE), each expression
+ * evaluated, then group_aggregate(normalize_basic(...)) over `keys`
+ * (n_keys = 0: aggregate_all per expression, returned as one group). fns[i]
+ * is the aggregate of exprs[i]. Same outputs as rq_group_aggregate_normalized.
+ * Runs as one pass over the compressed columns (K12) when the shape allows
+ * (RLE mask, RLE integer keys, plain / RLE / Plain+Index operands,
+ * SUM / AVG / COUNT); otherwise through the operator chain. *fused (may be
+ * NULL) reports which. */
+int rq_group_aggregate_exprs(rq_ctx_t ctx, rq_mask_t mask, const rq_col_t* keys, int32_t n_keys,
+                             const rq_expr* exprs, const int32_t* fns, int32_t n_exprs, int64_t* n_groups,
+                             rq_arr_t* out_keys, rq_arr_t* out_vals, int32_t* fused);
+
 /* ---------------------------------------------------------------------- */
 /* row-range sharding (multi-GPU; no reference counterpart)                 */
 /* ---------------------------------------------------------------------- */

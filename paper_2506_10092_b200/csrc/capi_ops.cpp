@@ -363,6 +363,43 @@ int rq_filtered_aggregate_binop(rq_ctx_t c, rq_col_t pred, rq_scalar k, int32_t 
   });
 }
 
+int rq_group_aggregate_exprs(rq_ctx_t c, rq_mask_t mask, const rq_col_t* keys, int32_t n_keys,
+                             const rq_expr* exprs, const int32_t* fns, int32_t n_exprs, int64_t* n_groups,
+                             rq_arr_t* out_keys, rq_arr_t* out_vals, int32_t* fused) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require(n_exprs > 0 && exprs != nullptr && fns != nullptr, "group_aggregate_exprs: no expressions");
+    std::vector<const DCol*> k;
+    for (int i = 0; i < n_keys; ++i) k.push_back(&col_of(keys[i]));
+    std::vector<XExpr> xs(static_cast<size_t>(n_exprs));
+    std::vector<int> f;
+    for (int i = 0; i < n_exprs; ++i) {
+      const rq_expr& e = exprs[i];
+      require(e.n_terms >= 0 && e.n_terms <= 3, "group_aggregate_exprs: 0..3 terms per expression");
+      for (int t = 0; t < e.n_terms; ++t) {
+        XTerm tm;
+        tm.col = &col_of(e.terms[t].col);
+        tm.sop = e.terms[t].op;
+        tm.rev = e.terms[t].reversed != 0;
+        tm.k = scal(e.terms[t].k);
+        require(tm.sop == -1 || (tm.sop >= RQ_ADD && tm.sop <= RQ_DIV), "arith: arithmetic operator required");
+        xs[static_cast<size_t>(i)].terms.push_back(tm);
+        if (t > 0) {
+          require(e.ops[t - 1] >= RQ_ADD && e.ops[t - 1] <= RQ_DIV, "arith: arithmetic operator required");
+          xs[static_cast<size_t>(i)].ops.push_back(e.ops[t - 1]);
+        }
+      }
+      f.push_back(fns[i]);
+    }
+    bool was_fused = false;
+    GroupAggOut r = group_aggregate_exprs(ctx, mask ? &mask_of(mask) : nullptr, k, xs, f, &was_fused);
+    if (fused) *fused = was_fused ? 1 : 0;
+    if (n_groups) *n_groups = r.n_groups;
+    for (int i = 0; i < n_keys; ++i) out_keys[i] = wrap_arr(r.keys[static_cast<size_t>(i)]);
+    for (int i = 0; i < n_exprs; ++i) out_vals[i] = wrap_arr(r.vals[static_cast<size_t>(i)]);
+  });
+}
+
 // ---- host-side row-range sharding -------------------------------------------------
 
 namespace {

@@ -1,0 +1,409 @@
+// jit_xg.cpp — run-time specialisation of the K12 row kernel.
+//
+// The interpreted row kernel (k_groupfused.cu, k_xg_rows) pays for its
+// generality on every row: operand selection, type promotion and operator
+// dispatch are data the kernel reads. Query engines on GPUs compile the
+// expression instead. This file emits CUDA source for ONE plan shape —
+// operand storage types, decode (logical width, centre present), term and
+// chain operators, promotion, accumulator types — with the rows of a lane
+// unrolled, compiles it with NVRTC for sm_100a (loaded with dlopen; no
+// link-time dependency), loads the cubin with the runtime's library API and
+// caches the kernel by its source text. Literal values and centres are kernel
+// arguments, so plans that differ only in constants share one kernel.
+// Semantics are the interpreted kernel's (and so the reference's): int64
+// wrapping arithmetic, any float → f64, int ÷0 raises, AVG sums in f64.
+// If NVRTC is unavailable the caller runs the interpreted kernel.
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "rq_internal.hpp"
+#include "xg_plan.hpp"
+
+namespace rqb {
+
+namespace {
+
+constexpr int ROWS = 8;  // rows per lane per window (one 8-byte load of an i8 column)
+
+struct Nvrtc {
+  bool ok = false;
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  Nvrtc() {
+    const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                           "/usr/local/cuda/lib64/libnvrtc.so"};
+    void* h = nullptr;
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_LOCAL))) break;
+    if (!h) return;
+    create = reinterpret_cast<decltype(create)>(dlsym(h, "nvrtcCreateProgram"));
+    compile = reinterpret_cast<decltype(compile)>(dlsym(h, "nvrtcCompileProgram"));
+    log_size = reinterpret_cast<decltype(log_size)>(dlsym(h, "nvrtcGetProgramLogSize"));
+    log = reinterpret_cast<decltype(log)>(dlsym(h, "nvrtcGetProgramLog"));
+    cubin_size = reinterpret_cast<decltype(cubin_size)>(dlsym(h, "nvrtcGetCUBINSize"));
+    cubin = reinterpret_cast<decltype(cubin)>(dlsym(h, "nvrtcGetCUBIN"));
+    destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "nvrtcDestroyProgram"));
+    ok = create && compile && log_size && log && cubin_size && cubin && destroy;
+  }
+};
+
+Nvrtc& nvrtc() {
+  static Nvrtc n;
+  return n;
+}
+
+// Fixed part of every generated kernel: segment walk over covered rows
+// (same schedule as k_xg_rows), warp reductions, table flush.
+const char* kPrelude = R"(
+typedef long long i64;
+typedef unsigned long long u64;
+struct XgSegs { const i64* s; const i64* e; const i64* off; const i64* slot; const u64* cst; i64 n; i64 ncov; };
+struct XgCol { const void* v; i64 center; };
+struct XgK { i64 i[24]; double f[24]; };
+__device__ __forceinline__ i64 ldg64(const i64* p, i64 i) { return __ldg(p + i); }
+__device__ __forceinline__ i64 warp_lb(const i64* a, i64 n, i64 key) {
+  const int lane = threadIdx.x & 31;
+  i64 lo = 0, hi = n;
+  while (hi - lo > 32) {
+    const i64 step = (hi - lo + 31) / 32;
+    i64 x = lo + (i64)(lane + 1) * step - 1;
+    if (x > hi - 1) x = hi - 1;
+    const bool pred = __ldg(a + x) < key;
+    const int c = __popc(__ballot_sync(0xffffffffu, pred));
+    const i64 nlo = c == 0 ? lo : __shfl_sync(0xffffffffu, x, c - 1) + 1;
+    const i64 nhi = c == 32 ? hi : __shfl_sync(0xffffffffu, x, c);
+    lo = nlo;
+    hi = nhi;
+  }
+  const i64 x = lo + lane;
+  const bool pred = x < hi && __ldg(a + x) < key;
+  return lo + __popc(__ballot_sync(0xffffffffu, pred));
+}
+__device__ __forceinline__ i64 idiv(i64 x, i64 y, int* err) {
+  if (y == 0) { *err = 1; return 0; }
+  if (x == (i64)0x8000000000000000ull && y == -1) return x;
+  return x / y;
+}
+__device__ __forceinline__ i64 wadd(i64 a, i64 b) { return (i64)((u64)a + (u64)b); }
+__device__ __forceinline__ i64 wsub(i64 a, i64 b) { return (i64)((u64)a - (u64)b); }
+__device__ __forceinline__ i64 wmul(i64 a, i64 b) { return (i64)((u64)a * (u64)b); }
+__device__ __forceinline__ double wsum_d(double x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ u64 wsum_u(u64 x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+)";
+
+std::string ty(int f) { return f ? "double" : "i64"; }
+
+std::string binop(const std::string& a, int fa, const std::string& b, int fb, int op) {
+  if (fa || fb) {
+    const char* o = op == RQ_ADD ? "+" : op == RQ_SUB ? "-" : op == RQ_MUL ? "*" : "/";
+    return "((double)(" + a + ") " + o + " (double)(" + b + "))";
+  }
+  switch (op) {
+    case RQ_ADD: return "wadd(" + a + ", " + b + ")";
+    case RQ_SUB: return "wsub(" + a + ", " + b + ")";
+    case RQ_MUL: return "wmul(" + a + ", " + b + ")";
+    default: return "idiv(" + a + ", " + b + ", &lerr)";
+  }
+}
+
+std::string wrap(int logical, const std::string& x) {
+  switch (logical) {
+    case RQ_I8: return "(i64)(signed char)(" + x + ")";
+    case RQ_I16: return "(i64)(short)(" + x + ")";
+    case RQ_I32: return "(i64)(int)(" + x + ")";
+    default: return x;
+  }
+}
+
+// loads + decode of column c for the lane's ROWS rows into x<c>_<u>
+void gen_load(std::ostringstream& o, int c, const dev::PlainSrc& s) {
+  const std::string p = "c" + std::to_string(c);
+  auto raw = [&](int u) -> std::string {
+    switch (s.dt) {
+      case RQ_I8: return "(i64)(signed char)(w" + std::to_string(c) + (u < 4 ? ".x" : ".y") + " >> " +
+                         std::to_string(8 * (u % 4)) + ")";
+      case RQ_I16: {
+        const char* f[] = {".x", ".y", ".z", ".w"};
+        return "(i64)(short)(w" + std::to_string(c) + f[u / 2] + " >> " + std::to_string(16 * (u % 2)) + ")";
+      }
+      case RQ_I32: return "(i64)w" + std::to_string(c) + "_" + std::to_string(u / 4) + "." + "xyzw"[u % 4];
+      case RQ_F32: return "(double)w" + std::to_string(c) + "_" + std::to_string(u / 4) + "." + "xyzw"[u % 4];
+      default: return std::string("w") + std::to_string(c) + "_" + std::to_string(u / 2) + (u % 2 ? ".y" : ".x");
+    }
+  };
+  switch (s.dt) {
+    case RQ_I8:
+      o << "    const uint2 w" << c << " = __ldg((const uint2*)((const signed char*)" << p << ".v + row));\n";
+      break;
+    case RQ_I16:
+      o << "    const uint4 w" << c << " = __ldg((const uint4*)((const short*)" << p << ".v + row));\n";
+      break;
+    case RQ_I32:
+      for (int q = 0; q < 2; ++q)
+        o << "    const int4 w" << c << "_" << q << " = __ldg((const int4*)((const int*)" << p << ".v + row) + " << q
+          << ");\n";
+      break;
+    case RQ_F32:
+      for (int q = 0; q < 2; ++q)
+        o << "    const float4 w" << c << "_" << q << " = __ldg((const float4*)((const float*)" << p << ".v + row) + "
+          << q << ");\n";
+      break;
+    case RQ_F64:
+      for (int q = 0; q < 4; ++q)
+        o << "    const double2 w" << c << "_" << q << " = __ldg((const double2*)((const double*)" << p
+          << ".v + row) + " << q << ");\n";
+      break;
+    default:
+      for (int q = 0; q < 4; ++q)
+        o << "    const longlong2 w" << c << "_" << q << " = __ldg((const longlong2*)((const i64*)" << p
+          << ".v + row) + " << q << ");\n";
+  }
+  const bool fstore = s.dt == RQ_F32 || s.dt == RQ_F64;
+  for (int u = 0; u < ROWS; ++u) {
+    std::string v = raw(u);
+    if (!fstore) {
+      if (s.logical != RQ_I64 && s.logical != RQ_F32 && s.logical != RQ_F64) v = wrap(s.logical, v);
+      if (s.has_center) {
+        v = "wadd(" + v + ", " + p + ".center)";
+        if (s.logical != RQ_I64 && s.logical != RQ_F32 && s.logical != RQ_F64) v = wrap(s.logical, v);
+      }
+      if (s.flt) v = "(double)(" + v + ")";
+    }
+    o << "    const " << ty(s.flt) << " x" << c << "_" << u << " = " << v << ";\n";
+  }
+}
+
+// the source of a plan's kernel; literal slots are appended to ki / kf
+std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf) {
+  std::ostringstream o;
+  o << kPrelude;
+  o << "extern \"C\" __global__ void __launch_bounds__(256) xg_kernel(const XgSegs S, const i64 chunk, u64* gtab, "
+       "const i64 G, int* err, const XgCol c0, const XgCol c1, const XgCol c2, const XgCol c3, const XgK K) {\n";
+  o << "  constexpr int NE = " << P.ne << ";\n";
+  o << "  __shared__ u64 stab[4096];\n";
+  o << "  const i64 cells = G * NE;\n  const bool in_smem = cells <= 4096;\n";
+  o << "  if (in_smem) { for (i64 i = threadIdx.x; i < cells; i += 256) stab[i] = 0ull; __syncthreads(); }\n";
+  o << "  u64* tab = in_smem ? stab : gtab;\n";
+  o << "  const int lane = threadIdx.x & 31;\n";
+  o << "  const i64 warp = ((i64)blockIdx.x * 256 + threadIdx.x) >> 5;\n";
+  o << "  const i64 nwarps = ((i64)gridDim.x * 256) >> 5;\n  int lerr = 0;\n";
+  for (int e = 0; e < P.ne; ++e)
+    if (P.e[e].rows) o << "  " << (P.e[e].acc_f ? "double" : "u64") << " a" << e << " = 0;\n";
+  o << "  for (i64 c0_ = warp * chunk; c0_ < S.ncov; c0_ += nwarps * chunk) {\n"
+       "    const i64 c1_ = min(c0_ + chunk, S.ncov);\n"
+       "    i64 k = warp_lb(S.off, S.n, c0_ + 1) - 1;\n"
+       "    i64 c = c0_;\n"
+       "    while (c < c1_) {\n"
+       "      const i64 off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k);\n"
+       "      const i64 slot = ldg64(S.slot, k);\n";
+  for (int j = 0; j < P.ncst; ++j) {
+    if (P.cst_f[j])
+      o << "      const double k" << j << " = __longlong_as_double((long long)__ldg(S.cst + " << j << " * S.n + k));\n";
+    else
+      o << "      const i64 k" << j << " = (i64)__ldg(S.cst + " << j << " * S.n + k);\n";
+  }
+  o << "      const i64 r0 = s + (c - off);\n"
+       "      const i64 r1 = min(e, s + (c1_ - off) - 1);\n"
+       "      for (i64 b = r0 & ~(i64)" << (ROWS - 1) << "; b <= r1; b += " << 32 * ROWS << ") {\n"
+       "        const i64 row = b + lane * " << ROWS << ";\n"
+       "        if (row > r1) continue;\n";
+  // loads
+  std::ostringstream ld;
+  for (int c = 0; c < P.nc; ++c) gen_load(ld, c, P.col[c]);
+  o << ld.str();
+  // expression values per row, then the accumulation (guarded form for partial windows)
+  auto lit = [&](const dev::XgTerm& t) -> std::string {
+    if (t.kflt) {
+      kf.push_back(t.kf);
+      return "K.f[" + std::to_string(kf.size() - 1) + "]";
+    }
+    ki.push_back(t.ki);
+    return "K.i[" + std::to_string(ki.size() - 1) + "]";
+  };
+  std::vector<std::vector<std::string>> lits(static_cast<size_t>(P.ne));
+  for (int e = 0; e < P.ne; ++e) {
+    const dev::XgExpr& X = P.e[e];
+    if (!X.rows) continue;
+    for (int t = 0; t < X.nt; ++t) lits[static_cast<size_t>(e)].push_back(X.t[t].sop >= 0 ? lit(X.t[t]) : "");
+  }
+  for (int e = 0; e < P.ne; ++e) {
+    const dev::XgExpr& X = P.e[e];
+    if (!X.rows) continue;
+    for (int u = 0; u < ROWS; ++u) {
+      std::string v;
+      int vf = 0;
+      for (int t = 0; t < X.nt; ++t) {
+        const dev::XgTerm& T = X.t[t];
+        std::string x = T.src < dev::XG_COLS ? "x" + std::to_string(T.src) + "_" + std::to_string(u)
+                                             : "k" + std::to_string(T.src - dev::XG_COLS);
+        int xf = T.flt;
+        if (T.sop >= 0) {
+          const std::string& k = lits[static_cast<size_t>(e)][static_cast<size_t>(t)];
+          x = T.rev ? binop(k, T.kflt, x, xf, T.sop) : binop(x, xf, k, T.kflt, T.sop);
+          xf = xf || T.kflt;
+        }
+        if (t == 0) {
+          v = x;
+          vf = xf;
+        } else {
+          v = binop(v, vf, x, xf, X.op[t - 1]);
+          vf = vf || xf;
+        }
+      }
+      o << "        const " << ty(vf) << " v" << e << "_" << u << " = " << v << ";\n";
+    }
+  }
+  o << "        if (row >= r0 && row + " << ROWS - 1 << " <= r1) {\n";
+  for (int e = 0; e < P.ne; ++e) {
+    const dev::XgExpr& X = P.e[e];
+    if (!X.rows) continue;
+    for (int u = 0; u < ROWS; ++u)
+      o << "          a" << e << " += " << (X.acc_f ? "(double)" : "(u64)") << "v" << e << "_" << u << ";\n";
+  }
+  o << "        } else {\n";
+  for (int e = 0; e < P.ne; ++e) {
+    const dev::XgExpr& X = P.e[e];
+    if (!X.rows) continue;
+    for (int u = 0; u < ROWS; ++u)
+      o << "          if (row + " << u << " >= r0 && row + " << u << " <= r1) a" << e << " += "
+        << (X.acc_f ? "(double)" : "(u64)") << "v" << e << "_" << u << ";\n";
+  }
+  o << "        }\n      }\n";
+  o << "      c = min(c1_, off + (e - s + 1));\n"
+       "      const i64 next_slot = (c < c1_ && k + 1 < S.n) ? ldg64(S.slot, k + 1) : -1;\n"
+       "      if (next_slot != slot) {\n";
+  for (int e = 0; e < P.ne; ++e) {
+    const dev::XgExpr& X = P.e[e];
+    if (!X.rows) continue;
+    if (X.acc_f)
+      o << "        { const double t = wsum_d(a" << e << "); if (lane == 0 && t != 0.0) atomicAdd((double*)tab + slot * NE + "
+        << e << ", t); a" << e << " = 0.0; }\n";
+    else
+      o << "        { const u64 t = wsum_u(a" << e << "); if (lane == 0 && t != 0ull) atomicAdd(tab + slot * NE + " << e
+        << ", t); a" << e << " = 0ull; }\n";
+  }
+  o << "      }\n      ++k;\n    }\n  }\n";
+  o << "  if (lerr) atomicOr(err, 1);\n";
+  o << "  if (in_smem) {\n    __syncthreads();\n    for (i64 i = threadIdx.x; i < cells; i += 256) {\n"
+       "      const u64 v = stab[i];\n      if (!v) continue;\n      switch ((int)(i % NE)) {\n";
+  for (int e = 0; e < P.ne; ++e) {
+    if (!P.e[e].rows) continue;
+    if (P.e[e].acc_f)
+      o << "        case " << e << ": atomicAdd((double*)gtab + i, __longlong_as_double((long long)v)); break;\n";
+    else
+      o << "        case " << e << ": atomicAdd(gtab + i, v); break;\n";
+  }
+  o << "        default: break;\n      }\n    }\n  }\n}\n";
+  return o.str();
+}
+
+struct Cache {
+  std::mutex mu;
+  std::unordered_map<std::string, cudaKernel_t> kernels;
+  std::unordered_map<std::string, bool> failed;
+};
+Cache& cache() {
+  static Cache c;
+  return c;
+}
+
+cudaKernel_t compile(const std::string& src) {
+  Nvrtc& N = nvrtc();
+  if (!N.ok) return nullptr;
+  Cache& C = cache();
+  std::lock_guard<std::mutex> g(C.mu);
+  auto it = C.kernels.find(src);
+  if (it != C.kernels.end()) return it->second;
+  if (C.failed.count(src)) return nullptr;
+  nvrtcProgram prog;
+  if (N.create(&prog, src.c_str(), "xg_kernel.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    C.failed[src] = true;
+    return nullptr;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--fmad=false"};
+  const nvrtcResult r = N.compile(prog, 4, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    N.log_size(prog, &n);
+    std::string log(n, '\0');
+    N.log(prog, &log[0]);
+    std::fprintf(stderr, "runq_b200: K12 kernel compilation failed (interpreted kernel used):\n%s\n", log.c_str());
+    N.destroy(&prog);
+    C.failed[src] = true;
+    return nullptr;
+  }
+  size_t n = 0;
+  N.cubin_size(prog, &n);
+  std::vector<char> bin(n);
+  N.cubin(prog, bin.data());
+  N.destroy(&prog);
+  cudaLibrary_t lib;
+  if (cudaLibraryLoadData(&lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
+    cudaGetLastError();
+    C.failed[src] = true;
+    return nullptr;
+  }
+  cudaKernel_t k;
+  if (cudaLibraryGetKernel(&k, lib, "xg_kernel") != cudaSuccess) {
+    cudaGetLastError();
+    C.failed[src] = true;
+    return nullptr;
+  }
+  C.kernels[src] = k;
+  return k;
+}
+
+struct XgColArg {
+  const void* v;
+  int64_t center;
+};
+struct XgKArg {
+  int64_t i[24];
+  double f[24];
+};
+
+}  // namespace
+
+bool xg_jit_available() { return nvrtc().ok; }
+
+// Launches the generated kernel for plan P; false if it cannot be built
+// (NVRTC missing, too many literals, compile failure).
+bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S, int64_t chunk,
+                   unsigned long long* tab, int64_t G, int* err, unsigned blocks) {
+  std::vector<int64_t> ki;
+  std::vector<double> kf;
+  const std::string src = gen_source(P, ki, kf);
+  if (ki.size() > 24 || kf.size() > 24) return false;
+  cudaKernel_t k = compile(src);
+  if (!k) return false;
+  XgColArg cols[4] = {};
+  for (int c = 0; c < P.nc && c < 4; ++c) cols[c] = {P.col[c].v, P.col[c].center};
+  XgKArg K{};
+  for (size_t i = 0; i < ki.size(); ++i) K.i[i] = ki[i];
+  for (size_t i = 0; i < kf.size(); ++i) K.f[i] = kf[i];
+  dev::XgSegs s = S;
+  int64_t ch = chunk, g = G;
+  void* args[] = {&s, &ch, &tab, &g, &err, &cols[0], &cols[1], &cols[2], &cols[3], &K};
+  RQ_CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(blocks), dim3(256), args, 0, ctx->stream));
+  return true;
+}
+
+}  // namespace rqb

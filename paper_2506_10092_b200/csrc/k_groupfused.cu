@@ -20,10 +20,12 @@
 // slot). Tables are per-CTA shared memory when they fit, global otherwise;
 // integer sums wrap like the reference's int64 accumulators.
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 
 #include "merge_walk.cuh"
 #include "rq_internal.hpp"
+#include "xg_plan.hpp"
 
 namespace rqb {
 namespace dev {
@@ -152,11 +154,6 @@ __device__ __forceinline__ void g_table_end(unsigned long long* smem, const GTab
 
 // value sources --------------------------------------------------------------
 
-struct PlainSrc {  // bit-width-reduced plain column (decode inline)
-  const void* v;
-  int dt, logical, has_center, flt;
-  int64_t center;
-};
 
 template <class T>
 __device__ __forceinline__ T plain_value(const PlainSrc& s, int64_t row) {
@@ -803,6 +800,708 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
     out.vals.push_back(res);
   }
   return true;
+}
+
+
+
+// ===========================================================================
+// K12 — filtered group-aggregate over expression aggregates.
+//
+// The query runner evaluates Filter → arith / arith_scalar → GroupAgg
+// (runner.cpp:243-336): every scanned column is filtered by the predicate
+// mask (a plain column becomes an IndexColumn of survivors, align.cpp:733-751),
+// each aggregate expression is materialised by binary / scalar operators
+// (align.cpp:495-508, :571-596) and group_aggregate aligns keys and data
+// (groupby.cpp:144-162). Here the rows that survive are described by a
+// SEGMENT table — the key runs ∩ the mask's runs ∩ the runs of every RLE
+// operand (the joint alignment of align_many, computed on the small run
+// lists) — each segment carrying its group slot and its RLE operands'
+// values. One row kernel then streams the plain operand columns once
+// (128-bit / narrow vector loads, bit-width-reduced decode in registers),
+// evaluates every expression per row with the reference's promotion rules
+// (any float → f64, else wrapping int64; int ÷0 raises) and accumulates
+// per-lane partials that are flushed per segment into a (slot × expression)
+// table. Covered rows are split evenly over warps (a prefix over segment
+// lengths), so only selected rows are read. Plain+Index operands (SUM/AVG of
+// the bare column) add a per-outlier correction; COUNT and expressions over
+// RLE operands only are evaluated once per segment (value × length, the
+// reference's run weights, groupby.cpp:67-135).
+// ===========================================================================
+
+namespace dev {
+
+__device__ __forceinline__ double xg_f(uint64_t b, int f) {
+  return f ? __longlong_as_double(static_cast<long long>(b)) : static_cast<double>(static_cast<int64_t>(b));
+}
+// binary op with the reference's promotion (align.cpp:290-305)
+__device__ __forceinline__ uint64_t xg_op(uint64_t a, int fa, uint64_t b, int fb, int op, int* err) {
+  if (fa || fb) return static_cast<uint64_t>(__double_as_longlong(arith_f64(xg_f(a, fa), xg_f(b, fb), op, nullptr)));
+  return static_cast<uint64_t>(arith_i64(static_cast<int64_t>(a), static_cast<int64_t>(b), op, err));
+}
+__device__ __forceinline__ uint64_t xg_term(const XgTerm& t, uint64_t x, int* err) {
+  if (t.sop < 0) return x;
+  const uint64_t k = t.kflt ? static_cast<uint64_t>(__double_as_longlong(t.kf)) : static_cast<uint64_t>(t.ki);
+  return t.rev ? xg_op(k, t.kflt, x, t.flt, t.sop, err) : xg_op(x, t.flt, k, t.kflt, t.sop, err);
+}
+
+// decode of one storage value to the logical value bits (column.cpp:283-297)
+template <class S>
+__device__ __forceinline__ uint64_t xg_decode(const PlainSrc& s, S raw) {
+  if constexpr (std::is_same<S, double>::value) {
+    return static_cast<uint64_t>(__double_as_longlong(raw));
+  } else if constexpr (std::is_same<S, float>::value) {
+    return static_cast<uint64_t>(__double_as_longlong(static_cast<double>(raw)));
+  } else {
+    int64_t x = static_cast<int64_t>(raw);
+    if (s.logical != RQ_I64) x = wrap_to(s.logical, x);
+    if (s.has_center) {
+      x = static_cast<int64_t>(static_cast<uint64_t>(x) + static_cast<uint64_t>(s.center));
+      if (s.logical != RQ_I64) x = wrap_to(s.logical, x);
+    }
+    if (s.flt) return static_cast<uint64_t>(__double_as_longlong(static_cast<double>(x)));
+    return static_cast<uint64_t>(x);
+  }
+}
+
+// four consecutive rows (row0 % 4 == 0) of a plain column, decoded
+__device__ __forceinline__ void xg_load4(const PlainSrc& s, int64_t row0, uint64_t (&o)[4]) {
+  switch (s.dt) {
+    case RQ_I8: {
+      const uint32_t w = __ldg(reinterpret_cast<const unsigned int*>(static_cast<const int8_t*>(s.v) + row0));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = xg_decode<int8_t>(s, static_cast<int8_t>((w >> (8 * u)) & 0xff));
+      break;
+    }
+    case RQ_I16: {
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(static_cast<const int16_t*>(s.v) + row0));
+      o[0] = xg_decode<int16_t>(s, static_cast<int16_t>(w.x & 0xffff));
+      o[1] = xg_decode<int16_t>(s, static_cast<int16_t>(w.x >> 16));
+      o[2] = xg_decode<int16_t>(s, static_cast<int16_t>(w.y & 0xffff));
+      o[3] = xg_decode<int16_t>(s, static_cast<int16_t>(w.y >> 16));
+      break;
+    }
+    case RQ_I32: {
+      const int4 w = __ldg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(s.v) + row0));
+      o[0] = xg_decode<int32_t>(s, w.x);
+      o[1] = xg_decode<int32_t>(s, w.y);
+      o[2] = xg_decode<int32_t>(s, w.z);
+      o[3] = xg_decode<int32_t>(s, w.w);
+      break;
+    }
+    case RQ_F32: {
+      const float4 w = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(s.v) + row0));
+      o[0] = xg_decode<float>(s, w.x);
+      o[1] = xg_decode<float>(s, w.y);
+      o[2] = xg_decode<float>(s, w.z);
+      o[3] = xg_decode<float>(s, w.w);
+      break;
+    }
+    case RQ_F64: {
+      const double2* p = reinterpret_cast<const double2*>(static_cast<const double*>(s.v) + row0);
+      const double2 a = __ldg(p), b = __ldg(p + 1);
+      o[0] = xg_decode<double>(s, a.x);
+      o[1] = xg_decode<double>(s, a.y);
+      o[2] = xg_decode<double>(s, b.x);
+      o[3] = xg_decode<double>(s, b.y);
+      break;
+    }
+    default: {
+      const longlong2* p = reinterpret_cast<const longlong2*>(static_cast<const int64_t*>(s.v) + row0);
+      const longlong2 a = __ldg(p), b = __ldg(p + 1);
+      o[0] = xg_decode<int64_t>(s, a.x);
+      o[1] = xg_decode<int64_t>(s, a.y);
+      o[2] = xg_decode<int64_t>(s, b.x);
+      o[3] = xg_decode<int64_t>(s, b.y);
+    }
+  }
+}
+
+
+__device__ __forceinline__ void xg_flush(const XgPlan& P, unsigned long long* tab, int64_t slot,
+                                         uint64_t (&acc)[XG_EXPRS]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int e = 0; e < XG_EXPRS; ++e) {
+    if (e >= P.ne || !P.e[e].rows) continue;
+    if (P.e[e].acc_f) {
+      double v = __longlong_as_double(static_cast<long long>(acc[e]));
+      v = warp_sum(v);
+      if (lane == 0 && v != 0.0) atomicAdd(reinterpret_cast<double*>(tab) + slot * P.ne + e, v);
+    } else {
+      unsigned long long v = warp_sum(static_cast<unsigned long long>(acc[e]));
+      if (lane == 0 && v != 0ull) atomicAdd(tab + slot * P.ne + e, v);
+    }
+    acc[e] = 0;
+  }
+}
+
+// v[u] = v[u] op x[u] for the lane's 4 rows; the type / operator dispatch
+// is uniform and hoisted out of the row loop
+__device__ __forceinline__ void xg_op4(uint64_t (&v)[4], int vf, const uint64_t (&x)[4], int xf, int op, int* err) {
+  if (vf || xf) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = xg_f(v[u], vf);
+      b[u] = xg_f(x[u], xf);
+    }
+    switch (op) {
+      case RQ_ADD:
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = a[u] + b[u];
+        break;
+      case RQ_SUB:
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = a[u] - b[u];
+        break;
+      case RQ_MUL:
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = a[u] * b[u];
+        break;
+      default:
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = a[u] / b[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = static_cast<uint64_t>(__double_as_longlong(a[u]));
+  } else {
+    switch (op) {
+      case RQ_ADD:
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = v[u] + x[u];
+        break;
+      case RQ_SUB:
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = v[u] - x[u];
+        break;
+      case RQ_MUL:
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = v[u] * x[u];
+        break;
+      default:
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = static_cast<uint64_t>(arith_i64(static_cast<int64_t>(v[u]), static_cast<int64_t>(x[u]), RQ_DIV, err));
+    }
+  }
+}
+
+// Row kernel: warp w takes covered rows [w·chunk, (w+1)·chunk) (segment
+// order), lanes take 4 consecutive rows each per 128-row window. Every
+// operand column is decoded once per window into the lane's slice of a
+// shared-memory tile (so a term's source is an address, not a register
+// select); expressions are then evaluated term by term over the 4 rows with
+// the operator / type dispatch hoisted out of the row loop.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    k_xg_rows(const __grid_constant__ XgPlan P, const __grid_constant__ XgSegs S, int64_t chunk, unsigned long long* __restrict__ gtab, int64_t G,
+              int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned long long xsm[];
+  const int64_t cells = G * P.ne;
+  const bool in_smem = cells <= kSmemSlots;
+  unsigned long long* stab = xsm;                                   // kSmemSlots
+  uint64_t* ctile = reinterpret_cast<uint64_t*>(xsm + kSmemSlots);  // [XG_COLS][BLOCK * 4]
+  uint64_t* kcs = ctile + XG_COLS * BLOCK * 4;                      // [BLOCK / 32][XG_CONSTS]
+  if (in_smem) {
+    for (int64_t i = threadIdx.x; i < cells; i += BLOCK) stab[i] = 0ull;
+    __syncthreads();
+  }
+  unsigned long long* tab = in_smem ? stab : gtab;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * BLOCK + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * BLOCK) >> 5;
+  uint64_t* my = ctile + threadIdx.x * 4;  // this lane's 4 rows of column c at my[c * BLOCK * 4]
+  uint64_t* wk = kcs + wid * XG_CONSTS;
+  int lerr = 0;
+  uint64_t acc[XG_EXPRS];
+#pragma unroll
+  for (int e = 0; e < XG_EXPRS; ++e) acc[e] = 0;
+  for (int64_t c0 = warp * chunk; c0 < S.ncov; c0 += nwarps * chunk) {
+    const int64_t c1 = min(c0 + chunk, S.ncov);
+    int64_t k = warp_lower_bound(S.off, S.n, c0 + 1) - 1;  // segment holding covered row c0
+    int64_t c = c0;
+    while (c < c1) {
+      const int64_t off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k);
+      const int64_t slot = ldg64(S.slot, k);
+      if (lane < P.ncst) wk[lane] = __ldg(S.cst + lane * S.n + k);
+      __syncwarp();
+      const int64_t r0 = s + (c - off);
+      const int64_t r1 = min(e, s + (c1 - off) - 1);
+      for (int64_t b = r0 & ~int64_t(3); b <= r1; b += 128) {
+        const int64_t row = b + lane * 4;
+        if (row > r1) continue;  // lane past the piece (no cross-lane traffic below)
+        for (int ci = 0; ci < P.nc; ++ci) {
+          uint64_t t[4];
+          xg_load4(P.col[ci], row, t);
+          uint64_t* d = my + ci * BLOCK * 4;
+          reinterpret_cast<ulonglong2*>(d)[0] = make_ulonglong2(t[0], t[1]);
+          reinterpret_cast<ulonglong2*>(d)[1] = make_ulonglong2(t[2], t[3]);
+        }
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ok[u] = row + u >= r0 && row + u <= r1;
+#pragma unroll
+        for (int ei = 0; ei < XG_EXPRS; ++ei) {
+          if (ei >= P.ne || !P.e[ei].rows) continue;
+          uint64_t v[4];
+          int vf = 0;
+          for (int ti = 0; ti < P.e[ei].nt; ++ti) {
+            const XgTerm& T = P.e[ei].t[ti];
+            uint64_t x[4];
+            if (T.src < XG_COLS) {
+              const ulonglong2* q = reinterpret_cast<const ulonglong2*>(my + T.src * BLOCK * 4);
+              const ulonglong2 p0 = q[0], p1 = q[1];
+              x[0] = p0.x;
+              x[1] = p0.y;
+              x[2] = p1.x;
+              x[3] = p1.y;
+            } else {
+              const uint64_t kv = wk[T.src - XG_COLS];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) x[u] = kv;
+            }
+            int xf = T.flt;
+            if (T.sop >= 0) {  // scalar op: x op k, or k op x
+              const uint64_t kb = T.kflt ? static_cast<uint64_t>(__double_as_longlong(T.kf)) : static_cast<uint64_t>(T.ki);
+              uint64_t kk[4] = {kb, kb, kb, kb};
+              if (T.rev) {
+                xg_op4(kk, T.kflt, x, xf, T.sop, &lerr);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = kk[u];
+              } else {
+                xg_op4(x, xf, kk, T.kflt, T.sop, &lerr);
+              }
+              xf = xf || T.kflt;
+            }
+            if (ti == 0) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) v[u] = x[u];
+              vf = xf;
+            } else {
+              xg_op4(v, vf, x, xf, P.e[ei].op[ti - 1], &lerr);
+              vf = vf || xf;
+            }
+          }
+          if (P.e[ei].acc_f) {
+            double a = __longlong_as_double(static_cast<long long>(acc[ei]));
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (ok[u]) a += xg_f(v[u], vf);
+            acc[ei] = static_cast<uint64_t>(__double_as_longlong(a));
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (ok[u]) acc[ei] += v[u];
+          }
+        }
+      }
+      c = min(c1, off + (e - s + 1));
+      // flush at segment ends where the slot changes, and at the chunk end
+      const int64_t next_slot = (c < c1 && k + 1 < S.n) ? ldg64(S.slot, k + 1) : -1;
+      if (next_slot != slot) xg_flush(P, tab, slot, acc);
+      __syncwarp();
+      ++k;
+    }
+  }
+  if (lerr) atomicOr(err, 1);
+  if (in_smem) {
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < cells; i += BLOCK) {
+      const unsigned long long v = stab[i];
+      if (!v) continue;
+      const int ei = static_cast<int>(i % P.ne);
+      if (P.e[ei].acc_f) atomicAdd(reinterpret_cast<double*>(gtab) + i, __longlong_as_double(static_cast<long long>(v)));
+      else atomicAdd(gtab + i, v);
+    }
+  }
+}
+
+template <int BLOCK>
+constexpr size_t xg_rows_smem() {
+  return (static_cast<size_t>(kSmemSlots) + XG_COLS * BLOCK * 4 + (BLOCK / 32) * XG_CONSTS) * 8;
+}
+
+// Per segment: COUNT (Σ lengths) and expressions over RLE operands only
+// (value × length, the reference's run weights).
+__global__ void k_xg_segs(const __grid_constant__ XgPlan P, const __grid_constant__ XgSegs S, unsigned long long* __restrict__ tab,
+                          unsigned long long* __restrict__ cnt, int* __restrict__ err) {
+  int lerr = 0;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < S.n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t len = ldg64(S.e, k) - ldg64(S.s, k) + 1;
+    const int64_t slot = ldg64(S.slot, k);
+    atomicAdd(cnt + slot, static_cast<unsigned long long>(len));
+    for (int ei = 0; ei < P.ne; ++ei) {
+      const XgExpr& X = P.e[ei];
+      if (X.rows || X.nt == 0) continue;
+      uint64_t v = 0;
+      int vf = 0;
+      for (int ti = 0; ti < X.nt; ++ti) {
+        const XgTerm& T = X.t[ti];
+        const uint64_t y = xg_term(T, __ldg(S.cst + (T.src - XG_COLS) * S.n + k), &lerr);
+        const int yf = T.flt || (T.sop >= 0 && T.kflt);
+        if (ti == 0) {
+          v = y;
+          vf = yf;
+        } else {
+          v = xg_op(v, vf, y, yf, X.op[ti - 1], &lerr);
+          vf = vf || yf;
+        }
+      }
+      if (X.acc_f) atomicAdd(reinterpret_cast<double*>(tab) + slot * P.ne + ei, xg_f(v, vf) * static_cast<double>(len));
+      else atomicAdd(tab + slot * P.ne + ei, static_cast<unsigned long long>(static_cast<uint64_t>(v) * static_cast<uint64_t>(len)));
+    }
+  }
+  if (lerr) atomicOr(err, 1);
+}
+
+// Plain+Index operand: outlier rows inside segments replace the base's
+// decoded value (column.cpp:299-309).
+__global__ void k_xg_outliers(PlainSrc base, const int64_t* __restrict__ p, const void* __restrict__ v2, int v2dt,
+                              const int64_t* __restrict__ idx_of, const int64_t* __restrict__ run_of, int64_t n,
+                              const int64_t* __restrict__ seg_slot, int ne, int ei, int acc_f,
+                              unsigned long long* __restrict__ tab) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pos = ldg64(p, i);
+    const int64_t slot = ldg64(seg_slot, ldg64(run_of, i));
+    const int64_t q = ldg64(idx_of, i);
+    if (acc_f) {
+      const double d = ld_f64(v2, v2dt, q) - plain_value<double>(base, pos);
+      atomicAdd(reinterpret_cast<double*>(tab) + slot * ne + ei, d);
+    } else {
+      const uint64_t d = static_cast<uint64_t>(ld_i64(v2, v2dt, q)) - static_cast<uint64_t>(plain_value<int64_t>(base, pos));
+      atomicAdd(tab + slot * ne + ei, static_cast<unsigned long long>(d));
+    }
+  }
+}
+
+__global__ void k_xg_finish(const int64_t* __restrict__ slots, int64_t ng, int ne, int ei, int fn, int acc_f,
+                            const unsigned long long* __restrict__ tab, const unsigned long long* __restrict__ cnt,
+                            void* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < ng;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = ldg64(slots, i);
+    const unsigned long long c = cnt[g];
+    if (fn == RQ_COUNT) {
+      static_cast<long long*>(out)[i] = static_cast<long long>(c);
+    } else if (fn == RQ_AVG) {
+      static_cast<double*>(out)[i] = c ? __longlong_as_double(static_cast<long long>(tab[g * ne + ei])) / static_cast<double>(c)
+                                       : __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      static_cast<unsigned long long*>(out)[i] = tab[g * ne + ei];
+    }
+    (void)acc_f;
+  }
+}
+
+__global__ void k_xg_lengths(const int64_t* __restrict__ s, const int64_t* __restrict__ e, int64_t n,
+                             int64_t* __restrict__ len) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    len[i] = ldg64(e, i) - ldg64(s, i) + 1;
+}
+
+}  // namespace dev
+
+namespace {
+
+// 16-B aligned base and room for the 8-row vector groups past the last row
+// (the generated kernel reads 8 rows per lane, the interpreted one 4)
+bool xg_vec_ok(const DArr& a) {
+  if (!a.buf || !a.buf->ptr) return a.n == 0;
+  const size_t w = static_cast<size_t>(dt_width(a.dt));
+  return (reinterpret_cast<uintptr_t>(a.buf->ptr) & 15) == 0 &&
+         a.buf->cap >= static_cast<size_t>((a.n + 7) & ~int64_t(7)) * w;
+}
+
+DArr xg_const_bits(const CtxPtr& ctx, const DArr& v) {
+  return cast_values(ctx, v, dt_float(v.dt) ? RQ_F64 : RQ_I64);
+}
+
+bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
+              const std::vector<XExpr>& exprs, const std::vector<int>& fns, GroupAggOut& out) {
+  if (exprs.size() > static_cast<size_t>(dev::XG_EXPRS) || keys.size() > 8) return false;
+  const int64_t total = !keys.empty() ? keys[0]->total
+                        : mask        ? mask->total
+                                      : (exprs.empty() || exprs[0].terms.empty() ? -1 : exprs[0].terms[0].col->total);
+  if (total < 0) return false;
+  if (mask && (mask->enc != RQ_MASK_RLE || mask->total != total)) return false;
+  for (int f : fns)
+    if (f != RQ_SUM && f != RQ_AVG && f != RQ_COUNT) return false;
+  for (auto* k : keys)
+    if (k->enc != RQ_ENC_RLE || dt_float(k->v.dt) || k->total != total) return false;
+
+  dev::XgPlan P{};
+  std::vector<const DCol*> plain_cols, rle_cols;
+  std::vector<std::pair<int, const DCol*>> pi_exprs;  // (expr, Plain+Index column)
+  auto col_slot = [](std::vector<const DCol*>& v, const DCol* c, int cap) -> int {
+    for (size_t i = 0; i < v.size(); ++i)  // the same column (possibly through another handle)
+      if (v[i] == c || (v[i]->enc == c->enc && v[i]->v.raw() == c->v.raw() && v[i]->e.raw() == c->e.raw()))
+        return static_cast<int>(i);
+    if (static_cast<int>(v.size()) >= cap) return -1;
+    v.push_back(c);
+    return static_cast<int>(v.size()) - 1;
+  };
+  P.ne = static_cast<int>(exprs.size());
+  for (size_t i = 0; i < exprs.size(); ++i) {
+    const XExpr& x = exprs[i];
+    dev::XgExpr& X = P.e[i];
+    X.nt = static_cast<int>(x.terms.size());
+    if (X.nt > 3 || static_cast<int>(x.ops.size()) != std::max(0, X.nt - 1)) return false;
+    if (X.nt == 0 && fns[i] != RQ_COUNT) return false;
+    int vf = 0;
+    for (int t = 0; t < X.nt; ++t) {
+      const XTerm& tm = x.terms[static_cast<size_t>(t)];
+      const DCol& c = *tm.col;
+      if (c.total != total) return false;
+      dev::XgTerm& T = X.t[t];
+      T.sop = tm.sop;
+      T.rev = tm.rev ? 1 : 0;
+      T.kflt = tm.k.is_float ? 1 : 0;
+      T.ki = tm.k.i;
+      T.kf = tm.k.f;
+      if (tm.sop >= 0 && (tm.sop < RQ_ADD || tm.sop > RQ_DIV)) return false;
+      if (c.enc == RQ_ENC_PLAIN || c.enc == RQ_ENC_PLAIN_INDEX) {
+        if (c.enc == RQ_ENC_PLAIN_INDEX) {  // bare column SUM / AVG only
+          if (X.nt != 1 || tm.sop >= 0) return false;
+          pi_exprs.push_back({static_cast<int>(i), &c});
+        }
+        if (!xg_vec_ok(c.v)) return false;
+        const int ci = col_slot(plain_cols, &c, dev::XG_COLS);
+        if (ci < 0) return false;
+        T.src = ci;
+        T.flt = (dt_float(c.v.dt) || dt_float(c.logical)) ? 1 : 0;
+        X.rows = 1;
+      } else if (c.enc == RQ_ENC_RLE) {
+        const int ri = col_slot(rle_cols, &c, dev::XG_CONSTS);
+        if (ri < 0) return false;
+        T.src = dev::XG_COLS + ri;
+        T.flt = dt_float(c.v.dt) ? 1 : 0;
+      } else {
+        return false;  // Index / RLE+Index operands: operator chain
+      }
+      const int yf = T.flt || (T.sop >= 0 && T.kflt);
+      if (t > 0) {
+        X.op[t - 1] = x.ops[static_cast<size_t>(t - 1)];
+        if (X.op[t - 1] < RQ_ADD || X.op[t - 1] > RQ_DIV) return false;
+      }
+      vf = vf || yf;
+    }
+    X.res_f = vf;
+    X.acc_f = (vf || fns[i] == RQ_AVG) ? 1 : 0;
+  }
+  // plain columns referenced by a Plain+Index expression are read as their base
+  P.nc = static_cast<int>(plain_cols.size());
+  for (size_t c = 0; c < plain_cols.size(); ++c) P.col[c] = plain_src(*plain_cols[c]);
+  P.ncst = static_cast<int>(rle_cols.size());
+  for (size_t j = 0; j < rle_cols.size(); ++j) P.cst_f[j] = dt_float(rle_cols[j]->v.dt) ? 1 : 0;
+
+  // ---- segment table: keys ∩ mask ∩ RLE operands (align_many's joint shape) ----
+  GroupKey K;
+  if (!keys.empty()) {
+    if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
+  } else {
+    const int64_t zs = 0, ze = total - 1, zslot = 0;
+    if (total == 0) return false;
+    K.s = upload_arr(ctx, RQ_I64, &zs, 1);
+    K.e = upload_arr(ctx, RQ_I64, &ze, 1);
+    K.slot = upload_arr(ctx, RQ_I64, &zslot, 1);
+    K.G = 1;
+  }
+  KTimer timer(ctx, "group_exprs");
+  DArr s = K.s, e = K.e, slot = K.slot;
+  std::vector<DArr> cst;
+  if (mask) {
+    Intersection r = range_intersect(ctx, s, e, mask->s, mask->e, true, false);
+    slot = gather(ctx, slot, r.idx1);
+    s = r.s;
+    e = r.e;
+  }
+  for (const DCol* rc : rle_cols) {
+    Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
+    slot = gather(ctx, slot, r.idx1);
+    for (auto& c : cst) c = gather(ctx, c, r.idx1);
+    cst.push_back(xg_const_bits(ctx, gather(ctx, rc->v, r.idx2)));
+    s = r.s;
+    e = r.e;
+  }
+  const int64_t nseg = s.n;
+  DArr cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * static_cast<int64_t>(cst.size())));
+  for (size_t j = 0; j < cst.size(); ++j)
+    if (nseg)
+      RQ_CUDA_CHECK(cudaMemcpyAsync(cst_all.as<int64_t>() + j * nseg, cst[j].raw(), nseg * 8,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  DArr off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
+  int64_t ncov = 0;
+  if (nseg) {
+    DArr len = alloc_arr(ctx, RQ_I64, nseg);
+    dev::k_xg_lengths<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
+    launched(ctx);
+    scan_exclusive_i64(ctx, len, off);
+    ncov = covered_rows(ctx, s, e);
+  }
+  const int64_t G = K.G;
+  const int64_t cells = G * P.ne;
+  if (cells > (int64_t{1} << 26)) return false;
+  DArr tab = new_table(ctx, std::max<int64_t>(1, cells), 0);
+  DArr cnt = new_table(ctx, G, 0);
+  int* err = reinterpret_cast<int*>(ctx->tickets + 2);  // zero between launches (reset after the check)
+  dev::XgSegs S{s.pos(), e.pos(), off.pos(), slot.pos(), reinterpret_cast<const uint64_t*>(cst_all.raw()), nseg,
+                ncov};
+  auto* tabp = reinterpret_cast<unsigned long long*>(tab.raw_mut());
+  auto* cntp = reinterpret_cast<unsigned long long*>(cnt.raw_mut());
+  if (nseg) {
+    dev::k_xg_segs<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(P, S, tabp, cntp, err);
+    launched(ctx);
+  }
+  bool any_rows = false;
+  for (int i = 0; i < P.ne; ++i) any_rows = any_rows || P.e[i].rows;
+  if (any_rows && ncov > 0) {
+    constexpr int B = 256;
+    const int64_t warps = static_cast<int64_t>(ctx->sm_count) * 8 * (B / 32);
+    int64_t chunk = (ncov + warps - 1) / warps;
+    chunk = std::max<int64_t>(512, (chunk + 127) / 128 * 128);
+    const int64_t blocks = std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
+                                             (ncov / chunk + (B / 32)) / (B / 32) + 1);
+    constexpr size_t smem = dev::xg_rows_smem<B>();
+    static bool attr = false;
+    if (!attr) {
+      RQ_CUDA_CHECK(cudaFuncSetAttribute(dev::k_xg_rows<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+      attr = true;
+    }
+    const char* nojit = std::getenv("RQ_NO_JIT");
+    if ((nojit && nojit[0] == '1') ||
+        !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks)))
+      dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
+    launched(ctx);
+  }
+  for (auto& pe : pi_exprs) {  // Plain+Index: outliers inside segments
+    const DCol& c = *pe.second;
+    if (c.p2.n == 0 || nseg == 0) continue;
+    PointsInRuns r = points_in_runs(ctx, c.p2, s, e, true, true);
+    if (r.p_out.n == 0) continue;
+    const dev::XgExpr& X = P.e[pe.first];
+    dev::k_xg_outliers<<<grid_cap(ctx, r.p_out.n), 256, 0, ctx->stream>>>(
+        P.col[X.t[0].src], r.p_out.pos(), c.v2.raw(), c.v2.dt, r.idx_of.pos(), r.run_of.pos(), r.p_out.n,
+        slot.pos(), P.ne, pe.first, X.acc_f, tabp);
+    launched(ctx);
+  }
+  {
+    const int64_t* h = ctx->readback(err, 8);
+    const bool div0 = (h[0] & 0xffffffff) != 0;
+    if (div0) {
+      RQ_CUDA_CHECK(cudaMemsetAsync(err, 0, 4, ctx->stream));
+      fail("integer division by zero");
+    }
+  }
+  // ---- outputs: present slots ascending (= ascending keys) ----
+  DArr present;
+  if (keys.empty()) {
+    const int64_t z = 0;
+    present = upload_arr(ctx, RQ_I64, &z, 1);
+  } else {
+    DArr flags = alloc_arr(ctx, RQ_I8, G);
+    dev::k_gk_flags<<<grid_cap(ctx, G), 256, 0, ctx->stream>>>(reinterpret_cast<const unsigned long long*>(cnt.raw()),
+                                                                G, flags.as<uint8_t>());
+    launched(ctx);
+    select_points(ctx, flags, iota(ctx, G), present, nullptr);
+  }
+  const int64_t ng = present.n;
+  out.n_groups = ng;
+  for (size_t c = 0; c < keys.size(); ++c) {
+    DArr kout = alloc_arr(ctx, K.kdt[c], ng);
+    if (ng) {
+      dev::k_gk_keys<<<grid_cap(ctx, ng), 256, 0, ctx->stream>>>(present.pos(), ng, K.kmin[c], K.stride[c],
+                                                                 K.range[c], K.kdt[c], kout.raw_mut());
+      launched(ctx);
+    }
+    out.keys.push_back(kout);
+  }
+  for (int i = 0; i < P.ne; ++i) {
+    const int fn = fns[static_cast<size_t>(i)];
+    const int32_t odt = fn == RQ_COUNT ? RQ_I64 : (fn == RQ_AVG || P.e[i].res_f) ? RQ_F64 : RQ_I64;
+    DArr res = alloc_arr(ctx, odt, ng);
+    if (ng) {
+      dev::k_xg_finish<<<grid_cap(ctx, ng), 256, 0, ctx->stream>>>(present.pos(), ng, P.ne, i, fn, P.e[i].acc_f,
+                                                                    reinterpret_cast<const unsigned long long*>(tab.raw()),
+                                                                    reinterpret_cast<const unsigned long long*>(cnt.raw()),
+                                                                    res.raw_mut());
+      launched(ctx);
+    }
+    out.vals.push_back(res);
+  }
+  return true;
+}
+
+// The runner's chain (runner.cpp:243-336) on the operator API: Filter every
+// operand column, evaluate the expressions with arith / arith_scalar, then
+// group_aggregate(normalize) — or aggregate_all per expression with no keys.
+GroupAggOut xg_chain(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
+                     const std::vector<XExpr>& exprs, const std::vector<int>& fns) {
+  std::vector<std::pair<const DCol*, DCol>> filtered;
+  size_t nref = keys.size();
+  for (auto& x : exprs) nref += x.terms.size();
+  filtered.reserve(nref);  // references into it stay valid
+  auto F = [&](const DCol* c) -> const DCol& {
+    if (!mask) return *c;
+    for (auto& f : filtered)
+      if (f.first == c) return f.second;
+    filtered.push_back({c, filter(ctx, *c, *mask)});
+    return filtered.back().second;
+  };
+  std::vector<DCol> keep;  // stable storage for expression results
+  keep.reserve(exprs.size() + 1);
+  std::vector<const DCol*> kf;
+  for (auto* k : keys) kf.push_back(&F(k));
+  std::vector<const DCol*> data;
+  for (size_t i = 0; i < exprs.size(); ++i) {
+    const XExpr& x = exprs[i];
+    if (x.terms.empty()) {  // COUNT(*): any column with the query's coverage
+      require(!kf.empty() || !exprs.empty(), "count: no column");
+      const DCol* any = !kf.empty() ? kf[0] : nullptr;
+      for (size_t j = 0; !any && j < exprs.size(); ++j)
+        if (!exprs[j].terms.empty()) any = &F(exprs[j].terms[0].col);
+      require(any != nullptr, "count(*) needs a key or an operand column");
+      data.push_back(any);
+      continue;
+    }
+    auto term = [&](const XTerm& t) -> DCol {
+      const DCol& c = F(t.col);
+      return t.sop >= 0 ? arith_scalar(ctx, c, t.k, t.sop, t.rev) : c;
+    };
+    DCol v = term(x.terms[0]);
+    for (size_t t = 1; t < x.terms.size(); ++t) v = arith(ctx, v, term(x.terms[t]), x.ops[t - 1]);
+    keep.push_back(v);
+    data.push_back(&keep.back());
+  }
+  if (!keys.empty()) return group_aggregate(ctx, kf, data, fns, true);
+  GroupAggOut out;
+  out.n_groups = 1;
+  for (size_t i = 0; i < data.size(); ++i) {
+    AggOut a = aggregate_column(ctx, normalize_basic(ctx, *data[i]), fns[i]);
+    DArr r = a.dtype == RQ_F64 ? upload_arr(ctx, RQ_F64, &a.f, 1) : upload_arr(ctx, RQ_I64, &a.i, 1);
+    out.vals.push_back(r);
+  }
+  return out;
+}
+
+}  // namespace
+
+GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
+                                  const std::vector<XExpr>& exprs, const std::vector<int>& fns, bool* fused) {
+  require(exprs.size() == fns.size(), "group_aggregate_exprs: one function per expression");
+  for (auto& x : exprs) {
+    require(x.terms.size() <= 3 && x.ops.size() + 1 == std::max<size_t>(1, x.terms.size()),
+            "group_aggregate_exprs: expressions are left-deep chains of at most 3 terms");
+    for (auto& t : x.terms) require(t.col != nullptr, "group_aggregate_exprs: null operand");
+  }
+  GroupAggOut out;
+  const bool ok = xg_fused(ctx, mask, keys, exprs, fns, out);
+  if (fused) *fused = ok;
+  if (ok) return out;
+  return xg_chain(ctx, mask, keys, exprs, fns);
 }
 
 }  // namespace rqb

@@ -413,6 +413,32 @@ struct GroupAggOut {
 GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
                             const std::vector<const DCol*>& data, const std::vector<int>& fns,
                             bool normalize = false);
+// Filter → expression → GroupAgg (runner.cpp:243-336) as one pass (K12):
+// each expression is a left-deep chain ((t0 op0 t1) op1 t2) of terms
+// `col` or `col sop k` / `k sop col` (reversed); no terms = COUNT(*).
+// mask may be null; keys may be empty (one global group). Falls back to the
+// operator chain for shapes the fused kernels do not take (*fused = false).
+struct XTerm {
+  const DCol* col = nullptr;
+  int sop = -1;
+  bool rev = false;
+  Scalar k;
+};
+struct XExpr {
+  std::vector<XTerm> terms;
+  std::vector<int> ops;
+};
+namespace dev {
+struct XgPlan;
+struct XgSegs;
+}  // namespace dev
+// jit_xg.cpp: run-time specialised K12 row kernel (NVRTC)
+bool xg_jit_available();
+bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S, int64_t chunk,
+                   unsigned long long* tab, int64_t G, int* err, unsigned blocks);
+GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
+                                  const std::vector<XExpr>& exprs, const std::vector<int>& fns,
+                                  bool* fused = nullptr);
 bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
                            const std::vector<const DCol*>& data, const std::vector<int>& fns,
                            GroupAggOut& out);

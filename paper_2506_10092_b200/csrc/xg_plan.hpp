@@ -1,0 +1,57 @@
+// xg_plan.hpp — the K12 expression group-aggregate plan (host-built, passed
+// by value to the interpreted row kernel and to the generated one).
+#pragma once
+
+#include <stdint.h>
+
+#include <string>
+
+namespace rqb {
+namespace dev {
+
+struct PlainSrc {  // bit-width-reduced plain column (decode inline)
+  const void* v;
+  int dt, logical, has_center, flt;
+  int64_t center;
+};
+
+constexpr int XG_COLS = 4, XG_CONSTS = 4, XG_EXPRS = 8;
+
+struct XgTerm {
+  int src;   // < XG_COLS: plain column; >= XG_COLS: segment constant src - XG_COLS
+  int flt;   // source value is f64
+  int sop;   // scalar op (RQ_ADD..RQ_DIV) or -1
+  int rev;   // scalar on the left (k op x)
+  int kflt;  // scalar is f64
+  int64_t ki;
+  double kf;
+};
+struct XgExpr {
+  int nt;     // 1..3 terms
+  int op[2];  // chain ops, left-deep: ((t0 op0 t1) op1 t2)
+  XgTerm t[3];
+  int acc_f;  // accumulate in f64 (float result, or AVG)
+  int res_f;  // expression result is f64
+  int rows;   // evaluated per row (references a plain column)
+};
+struct XgPlan {
+  int nc;
+  PlainSrc col[XG_COLS];
+  int ncst;
+  int cst_f[XG_CONSTS];
+  int ne;
+  XgExpr e[XG_EXPRS];
+};
+
+struct XgSegs {
+  const int64_t* s;
+  const int64_t* e;
+  const int64_t* off;   // exclusive prefix of segment lengths (covered rows)
+  const int64_t* slot;
+  const uint64_t* cst;  // [XG_CONSTS][nseg] RLE operand values (i64 / f64 bits)
+  int64_t n;
+  int64_t ncov;
+};
+
+}  // namespace dev
+}  // namespace rqb

@@ -238,6 +238,16 @@ class Scalar(C.Structure):
     _fields_ = [("is_float", C.c_int32), ("_pad", C.c_int32), ("i", C.c_int64), ("f", C.c_double)]
 
 
+class Term(C.Structure):
+    """rq_term: `col` (op = -1) or `col op k` / `k op col` (reversed)."""
+    _fields_ = [("col", C.c_void_p), ("op", C.c_int32), ("reversed", C.c_int32), ("k", Scalar)]
+
+
+class Expr(C.Structure):
+    """rq_expr: left-deep chain ((t0 ops[0] t1) ops[1] t2); n_terms 0 = COUNT(*)."""
+    _fields_ = [("n_terms", C.c_int32), ("ops", C.c_int32 * 2), ("terms", Term * 3)]
+
+
 # runq::io::Scheme (ingest.hpp:29)
 SCHEME_PLAIN, SCHEME_PLAIN_CENTERED, SCHEME_RLE, SCHEME_RLE_INDEX, SCHEME_PLAIN_INDEX = range(5)
 SCHEME_NAMES = {"plain": 0, "plain-centered": 1, "rle": 2, "rle+index": 3, "plain+index": 4}

@@ -221,3 +221,54 @@ def q1(api, t):
     data = [f["l_quantity"], f["l_extendedprice"], disc_price, charge, f["l_quantity"], f["l_extendedprice"],
             f["l_discount"], f["l_quantity"]]
     return A.group_aggregate(keys, data, Q1_FNS, normalize=True)
+
+
+# ---------------------------------------------------------------------------
+# Fused forms: the same plans through agg.group_aggregate_exprs (K12 — one
+# pass over the compressed columns instead of materialised filter / arith
+# outputs). `rq` is paper_2506_10092_b200.runq; the masks are built with the
+# same compare_scalar / and_mask / or_mask calls as the chain plans above.
+# ---------------------------------------------------------------------------
+
+
+def q6_mask(api, t):
+    C, M = api.compute, api.masks
+    return M.and_mask(
+        M.and_mask(C.compare_scalar(t["l_shipdate"], Q6_LO, ">="), C.compare_scalar(t["l_shipdate"], Q6_HI, "<")),
+        M.and_mask(M.and_mask(C.compare_scalar(t["l_discount"], 5, ">="), C.compare_scalar(t["l_discount"], 7, "<=")),
+                   C.compare_scalar(t["l_quantity"], 24, "<")))
+
+
+def q6_fused(rq, t):
+    X = rq.X
+    _, vs, _, fused = rq.agg.group_aggregate_exprs(
+        q6_mask(rq, t), [], [X.col(t["l_extendedprice"]).arith(X.col(t["l_discount"]), "*")], ["sum"])
+    v = vs[0]
+    return (float(v.download()[0]) if hasattr(v, "download") else float(v[0])), fused
+
+
+def q1_fused(rq, t):
+    X = rq.X
+    m = rq.compute.compare_scalar(t["l_shipdate"], Q1_CUTOFF, "<=")
+    price, disc, tax, qty = (t[k] for k in ("l_extendedprice", "l_discount", "l_tax", "l_quantity"))
+    disc_price = X.col(price).arith(X.col(disc).scalar(100, "-", True), "*")
+    charge = disc_price.arith(X.col(tax).scalar(100, "+"), "*")
+    exprs = [X.col(qty), X.col(price), disc_price, charge, X.col(qty), X.col(price), X.col(disc), X.count()]
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(m, [t["l_returnflag"], t["l_linestatus"]], exprs, Q1_FNS)
+    return (ks, vs, ng), fused
+
+
+def c5_mask(api, t):
+    C, M = api.compute, api.masks
+    m_in = None
+    for code in C5_IN:
+        e = C.compare_scalar(t["r2"], code, "==")
+        m_in = e if m_in is None else M.or_mask(m_in, e)
+    return M.and_mask(m_in, C.compare_scalar(t["r3"], C5_LT, "<"))
+
+
+def c5_fused(rq, t):
+    X = rq.X
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(c5_mask(rq, t), [t["r4"]],
+                                                     [X.col(t["pi0"]), X.col(t["p1"]), X.count()], C5_FNS)
+    return (ks, vs, ng), fused

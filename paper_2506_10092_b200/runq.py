@@ -532,6 +532,37 @@ class masks:
         return _out(DeviceMask(o, ctx), host)
 
 
+class X:
+    """Aggregate expressions for agg.group_aggregate_exprs — the runner's
+    arith / arith_scalar plan nodes (align.cpp:495-508, :571-596) as a
+    left-deep chain of at most 3 terms:
+        X.col(c)                    a column
+        X.col(c).scalar(k, op)      c op k   (reversed=True: k op c)
+        x.arith(y, op)              x op y   (y a single term)
+        X.count()                   COUNT(*)
+    """
+
+    def __init__(self, terms, ops):
+        self.terms, self.ops = terms, ops
+
+    @staticmethod
+    def col(c):
+        return X([[c, -1, False, 0]], [])
+
+    @staticmethod
+    def count():
+        return X([], [])
+
+    def scalar(self, k, op, reversed=False):
+        assert len(self.terms) == 1 and self.terms[0][1] == -1, "scalar op applies to a bare column term"
+        c = self.terms[0][0]
+        return X([[c, H.BINOP_NAMES.get(op, op), bool(reversed), k]], [])
+
+    def arith(self, other, op):
+        assert len(other.terms) == 1, "right operand must be a single term (left-deep chains)"
+        return X(self.terms + other.terms, self.ops + [H.BINOP_NAMES.get(op, op)])
+
+
 def _agg_result(dt, i, f):
     return float(f.value) if dt.value == H.F64 else int(i.value)
 
@@ -570,6 +601,48 @@ class agg:
         ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
         vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(dd))]
         return ks, vs, int(ng.value)
+
+    @staticmethod
+    def group_aggregate_exprs(mask, keys: Sequence, exprs: Sequence, fns: Sequence):
+        """The runner's Filter → expressions → GroupAgg (runner.cpp:243-336)
+        in one call: operands filtered by `mask` (None: no WHERE), each X
+        expression evaluated, group_aggregate(normalize) over `keys` (empty:
+        one global group). Returns (keys list, values list, n_groups, fused)."""
+        fns = [H.AGG_NAMES.get(f, f) for f in fns]
+        cols = [t[0] for x in exprs for t in x.terms]
+        host = _is_host(*keys, *cols, *([mask] if mask is not None else []))
+        ctx = _ctx_of(*keys, *cols, *([mask] if mask is not None else []))
+        dm = upload(mask, ctx) if mask is not None else None
+        dk = [upload(k, ctx) for k in keys]
+        arr = (H.Expr * len(exprs))()
+        keep = [dm, dk]
+        uploaded = {}  # one device column per distinct operand object
+
+        def up(c):
+            if id(c) not in uploaded:
+                uploaded[id(c)] = (c, upload(c, ctx))
+            return uploaded[id(c)][1]
+        for i, x in enumerate(exprs):
+            arr[i].n_terms = len(x.terms)
+            for j, op in enumerate(x.ops):
+                arr[i].ops[j] = op
+            for j, (c, op, rev, k) in enumerate(x.terms):
+                dc = up(c)
+                keep.append(dc)
+                arr[i].terms[j].col = dc.handle.value
+                arr[i].terms[j].op = op
+                arr[i].terms[j].reversed = int(rev)
+                arr[i].terms[j].k = H.make_scalar(k)
+        karr = (C.c_void_p * max(1, len(dk)))(*[k.handle.value for k in dk])
+        farr = (C.c_int32 * len(fns))(*fns)
+        ok = (C.c_void_p * max(1, len(dk)))()
+        ov = (C.c_void_p * len(exprs))()
+        ng, fused = C.c_int64(), C.c_int32()
+        check(_L.rq_group_aggregate_exprs(ctx.handle, dm.handle if dm is not None else None, karr, len(dk), arr,
+                                          farr, len(exprs), C.byref(ng), ok, ov, C.byref(fused)))
+        ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
+        vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(exprs))]
+        return ks, vs, int(ng.value), bool(fused.value)
 
     @staticmethod
     def aggregate_binop(a, b, op, fn):
