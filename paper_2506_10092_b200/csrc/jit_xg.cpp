@@ -17,6 +17,7 @@
 #include <nvrtc.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -195,7 +196,9 @@ void gen_load(std::ostringstream& o, int c, const dev::PlainSrc& s) {
 std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf) {
   std::ostringstream o;
   o << kPrelude;
-  o << "extern \"C\" __global__ void __launch_bounds__(256) xg_kernel(const XgSegs S, const i64 chunk, u64* gtab, "
+  const char* mb = std::getenv("RQ_JIT_MINB");  // tuning knob: min resident CTAs per SM
+  const int minb = mb ? std::atoi(mb) : 3;
+  o << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") xg_kernel(const XgSegs S, const i64 chunk, u64* gtab, "
        "const i64 G, int* err, const XgCol c0, const XgCol c1, const XgCol c2, const XgCol c3, const XgK K) {\n";
   o << "  constexpr int NE = " << P.ne << ";\n";
   o << "  __shared__ u64 stab[4096];\n";

@@ -1371,6 +1371,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
                                          static_cast<int>(smem)));
       attr = true;
     }
+    KTimer rows_timer(ctx, "xg_rows");
     const char* nojit = std::getenv("RQ_NO_JIT");
     if ((nojit && nojit[0] == '1') ||
         !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks)))
