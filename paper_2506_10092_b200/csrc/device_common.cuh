@@ -394,6 +394,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// lower_bound over a shared-memory window padded with INT64_MAX up to the
+// power of two L (uniform per CTA; L <= CAP): log2(L) steps of
+// load / compare / select / add, no bounds tests
+template <int CAP>
+__device__ __forceinline__ int smem_lb_pow2(const int64_t* a, int L, int64_t key) {
+  int pos = 0;
+#pragma unroll
+  for (int step = CAP / 2; step > 0; step >>= 1)
+    if (step < L) pos = a[pos + step - 1] < key ? pos + step : pos;
+  return pos + (a[pos] < key ? 1 : 0);
+}
+__device__ __forceinline__ int pow2_above(int n) {  // smallest power of two > n (n >= 0)
+  return n > 0 ? 1 << (32 - __clz(n)) : 1;
+}
+
 // Branch-free lower_bound over a shared-memory array of n >= 1 sorted int64
 // (first index with a[i] >= key, n if none). The trip count depends on n
 // only, so every lane of a CTA runs the same steps; no padding is needed.

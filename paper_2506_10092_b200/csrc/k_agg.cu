@@ -10,6 +10,8 @@
 // the whole compute::arith → agg::aggregate_all chain (align.cpp:495-508,
 // groupby.cpp:164-172) in one pass over the compressed bytes.
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <limits>
 
 #include "merge_walk.cuh"
@@ -337,6 +339,335 @@ __global__ void __launch_bounds__(BLOCK)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2 persistent TMA form (gapless RLE × gapless RLE, 8-byte values).
+// The list with more runs drives: tile t = its runs [t·TA, (t+1)·TA) (the
+// row range (r_lo, r_hi]); the other list's window = its runs whose ends
+// fall after r_lo, chained from tile to tile by the producer warp (rank of
+// r_hi + 1 in the landed window, a warp search only past it) and staged with
+// 1-D bulk copies into two mbarrier stages, as in the C2 kernel. Every
+// fragment of the union of boundaries ends at a driver end or at an other-
+// list end; consumers take the driver ends (ITEMS per lane: one shared-
+// memory lower_bound, forward steps) and then the other list's ends inside
+// the tile (ties belong to the driver), each closing
+//   (va op vb) · (end − max(prev driver end, prev other end)).
+// Per-CTA partials are folded by the last CTA (ticket counter).
+// ---------------------------------------------------------------------------
+
+template <int TA, int BW>
+struct PairStage {
+  static constexpr int AE = TA + 2 + 16;  // ends: 2 previous + tile (+ rounding)
+  static constexpr int AV = TA + 16;
+  static constexpr int BE = BW + 16;      // window padded to the power of two BW (+8 forward steps)
+  static constexpr size_t AE_OFF = 0;
+  static constexpr size_t AV_OFF = AE_OFF + AE * 8;
+  static constexpr size_t BE_OFF = AV_OFF + AV * 8;
+  static constexpr size_t BV_OFF = BE_OFF + BE * 8;
+  static constexpr size_t BYTES = BV_OFF + BE * 8;
+};
+
+template <int BLOCK, int IA, int BW, class T, int OP, int KIND>
+__global__ void __launch_bounds__(BLOCK, 4)
+    k_pair_reduce_tma(const int64_t* __restrict__ Ae, const T* __restrict__ Av, int64_t na,
+                      const int64_t* __restrict__ Be, const T* __restrict__ Bv, int64_t nb, int swap,
+                      int64_t ntiles, AggPart* __restrict__ parts, unsigned* __restrict__ ticket,
+                      AggPart* __restrict__ out, int* __restrict__ err) {
+  constexpr int NCW = BLOCK / 32 - 1;
+  constexpr int NL = NCW * 32;  // consumer lanes
+  constexpr int TA = NL * IA;
+  using S = PairStage<TA, BW>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[2], empty[2];
+  __shared__ int64_t s_lo[2];
+  __shared__ int s_nb[2], s_jf[2];
+
+  const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * ntiles / gridDim.x;
+  const int64_t t_end = static_cast<int64_t>(blockIdx.x + 1) * ntiles / gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto sAe = [&](int st) { return reinterpret_cast<int64_t*>(smem + st * S::BYTES + S::AE_OFF); };
+  auto sAv = [&](int st) { return reinterpret_cast<T*>(smem + st * S::BYTES + S::AV_OFF); };
+  auto sBe = [&](int st) { return reinterpret_cast<int64_t*>(smem + st * S::BYTES + S::BE_OFF); };
+  auto sBv = [&](int st) { return reinterpret_cast<T*>(smem + st * S::BYTES + S::BV_OFF); };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 32);
+    mbar_init(&full[1], 32);
+    mbar_init(&empty[0], NCW);
+    mbar_init(&empty[1], NCW);
+  }
+  __syncthreads();
+
+  uint64_t isum = 0;
+  double fsum = 0.0;
+  int64_t cnt = 0;
+  int lerr = 0;
+  if (wid == 0) {
+    // ---- producer ----
+    int64_t jb = 0, b_lo = 0;
+    int b_est = BW, b_n = 0;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int st = static_cast<int>((t - t_begin) & 1);
+      const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
+      const int64_t a0 = t * TA;
+      const int na_t = static_cast<int>(min(static_cast<int64_t>(TA), na - a0));
+      if (t == t_begin) {
+        const int64_t r_lo = a0 > 0 ? ldg64(Ae, a0 - 1) : -1;
+        jb = warp_lower_bound(Be, nb, r_lo + 1);
+      } else {
+        mbar_wait(&full[st ^ 1], ((t - 1 - t_begin) >> 1) & 1);  // tile t-1 landed
+        const int pst = st ^ 1;
+        const int pna = static_cast<int>(min(static_cast<int64_t>(TA), na - (a0 - TA)));
+        const int64_t r_prev_hi = sAe(pst)[2 + pna - 1];
+        const int rb = smem_lb_pow2<BW>(sBe(pst), BW, r_prev_hi + 1);
+        int64_t jn = b_lo + rb;
+        if (rb >= b_n && jn < nb) jn += warp_lower_bound(Be + jn, nb - jn, r_prev_hi + 1);
+        const int64_t used = jn - jb;
+        b_est = static_cast<int>(min(static_cast<int64_t>(BW), used + (used >> 2) + 32));
+        jb = jn;
+      }
+      if (t - t_begin >= 2) mbar_wait(&empty[st], (use - 1) & 1);
+      // other-list window [b_lo, b_lo + b_n): even start, < BW - 8 entries, clipped at nb
+      b_lo = jb & ~int64_t(1);
+      int64_t n = static_cast<int64_t>(b_est) + (jb - b_lo);
+      if (n > BW - 16) n = BW - 16;
+      n = (n + 1) & ~int64_t(1);  // whole 16-byte chunks: the tail path runs only at the column end
+      if (n > nb - b_lo) n = nb - b_lo;
+      b_n = n > 0 ? static_cast<int>(n) : 0;
+      int64_t* wAe = sAe(st);
+      T* wAv = sAv(st);
+      int64_t* wBe = sBe(st);
+      T* wBv = sBv(st);
+      // driver: ends from a0 - 2 (two previous ends; -1 before the column) and values from a0
+      const bool first = a0 == 0;
+      const int ae_n = na_t + (first ? 0 : 2);
+      const int ae_bulk = ae_n & ~1, av_bulk = na_t & ~1, b_bulk = b_n & ~1;
+      int64_t* ae_dst = first ? wAe + 2 : wAe;
+      const int64_t* ae_src = first ? Ae : Ae + (a0 - 2);
+      if (first && lane < 2) wAe[lane] = -1;
+      if (lane == 0 && ae_bulk < ae_n) ae_dst[ae_bulk] = ldg64(ae_src, ae_bulk);
+      if (lane == 1 && av_bulk < na_t) wAv[av_bulk] = Av[a0 + av_bulk];
+      if (lane == 2 && b_bulk < b_n) {
+        wBe[b_bulk] = ldg64(Be, b_lo + b_bulk);
+        wBv[b_bulk] = Bv[b_lo + b_bulk];
+      }
+      for (int i = b_n + lane; i < BW + 8; i += 32) wBe[i] = INT64_MAX;
+      if (lane != 0) mbar_arrive(&full[st]);
+      if (lane == 0) {
+        s_lo[st] = b_lo;
+        s_nb[st] = b_n;
+        s_jf[st] = static_cast<int>(jb - b_lo);
+        const uint32_t bytes = static_cast<uint32_t>(ae_bulk + av_bulk + 2 * b_bulk) * 8u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[st], bytes);
+        if (ae_bulk) bulk_g2s(ae_dst, ae_src, ae_bulk * 8u, &full[st]);
+        if (av_bulk) bulk_g2s(wAv, Av + a0, av_bulk * 8u, &full[st]);
+        if (b_bulk) {
+          bulk_g2s(wBe, Be + b_lo, b_bulk * 8u, &full[st]);
+          bulk_g2s(wBv, Bv + b_lo, b_bulk * 8u, &full[st]);
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---- consumers ----
+    const int cl = (wid - 1) * 32 + lane;  // consumer lane
+    auto fold = [&](T va, T vb, int64_t len) {
+      if (len <= 0) return;
+      if (KIND == 2) {
+        cnt += len;
+        return;
+      }
+      const T r = swap ? arith_t<T>(vb, va, OP, &lerr) : arith_t<T>(va, vb, OP, &lerr);
+      if (KIND == 0) {
+        isum += static_cast<uint64_t>(static_cast<int64_t>(r)) * static_cast<uint64_t>(len);
+      } else {
+        fsum += static_cast<double>(r) * static_cast<double>(len);
+        cnt += len;
+      }
+    };
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int st = static_cast<int>((t - t_begin) & 1);
+      const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
+      const int64_t a0 = t * TA;
+      const int na_t = static_cast<int>(min(static_cast<int64_t>(TA), na - a0));
+      mbar_wait(&full[st], use & 1u);
+      const int64_t b_lo = s_lo[st];
+      const int b_n = s_nb[st];
+      const int64_t* wAe = sAe(st) + 2;  // wAe[-1] = previous driver end
+      const T* wAv = sAv(st);
+      const int64_t* wBe = sBe(st);
+      const T* wBv = sBv(st);
+      const int64_t r_lo = wAe[-1], r_hi = wAe[na_t - 1];
+      // other-list window entries: [jf, jl) end inside (r_lo, r_hi); entry jl
+      // is the run covering r_hi (uniform searches)
+      const int jf = s_jf[st];  // = jb - window start (the producer's search)
+      const int jl = smem_lb_pow2<BW>(wBe, BW, r_hi);
+      if (jl < b_n) {
+        // fast path: merge path over the tile's driver ends and the window's
+        // ends, ITEMS-free even split of the merged sequence over the lanes;
+        // ties take the driver end first (the other end then closes 0 rows)
+        const int nbi = jl - jf;
+        const int tot = na_t + nbi;
+        const int per = (tot + NL - 1) / NL;
+        const int d = min(cl * per, tot), dend = min(d + per, tot);
+        if (d < dend) {
+          const int64_t* wB = wBe + jf;
+          const T* vB = wBv + jf;
+          int lo = d > nbi ? d - nbi : 0, hi = d < na_t ? d : na_t;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (wAe[mid] <= wB[d - mid - 1]) lo = mid + 1;
+            else hi = mid;
+          }
+          int x = lo, y = d - lo;
+          const int64_t pa0 = wAe[x - 1];
+          const int64_t pb0 = jf + y > 0 ? wB[y - 1] : INT64_MIN;
+          int64_t prev = pa0 > pb0 ? pa0 : pb0;
+          int64_t ka = x < na_t ? wAe[x] : INT64_MAX;
+          int64_t kb = y < nbi ? wB[y] : INT64_MAX;
+          for (int it = d; it < dend; ++it) {
+            const bool takeA = ka <= kb;
+            const int64_t key = takeA ? ka : kb;
+            fold(wAv[x], vB[y], key - prev);  // x / y: the runs covering key
+            prev = key;
+            if (takeA) {
+              ++x;
+              ka = x < na_t ? wAe[x] : INT64_MAX;
+            } else {
+              ++y;
+              kb = y < nbi ? wB[y] : INT64_MAX;
+            }
+          }
+        }
+      } else {
+        // slow path (the covering run is past the staged window): driver
+        // ends ranked in the window with global fall-backs, then the other
+        // list's ends inside the tile
+        // (a) fragments ending at driver ends
+        const int i0 = cl * IA;
+        if (i0 < na_t) {
+          int j = smem_lb_pow2<BW>(wBe, BW, wAe[i0]);
+  #pragma unroll
+          for (int k = 0; k < IA; ++k) {
+            const int i = i0 + k;
+            if (i >= na_t) break;
+            const int64_t e = wAe[i];
+            if (k > 0) {
+              j = wBe[j + 1] < e ? j + 2 : j;
+              j = wBe[j] < e ? j + 1 : j;
+              while (wBe[j] < e) ++j;
+            }
+            int64_t gj = b_lo + j, pb;
+            T vb;
+            if (j < b_n) {
+              vb = wBv[j];
+              pb = j > 0 ? wBe[j - 1] : INT64_MIN;
+            } else {  // past the staged window
+              gj += lower_bound_g(Be + gj, nb - gj, e);
+              vb = gj < nb ? Bv[gj] : T(0);
+              pb = gj > 0 ? ldg64(Be, gj - 1) : INT64_MIN;
+            }
+            const int64_t pa = wAe[i - 1];
+            fold(wAv[i], vb, e - (pa > pb ? pa : pb));
+          }
+        }
+        // (b) fragments ending at other-list ends strictly inside (r_lo, r_hi)
+        // that are not driver ends; ends past the staged window come from
+        // global memory (rare)
+        const int jf = smem_lb_pow2<BW>(wBe, BW, r_lo + 1);  // first window end > r_lo (uniform)
+        const int64_t last_in = wBe[b_n > 0 ? b_n - 1 : 0];
+        const bool spill = b_n == 0 || (last_in < r_hi && b_lo + b_n < nb);
+        const int64_t jcount = (b_n > jf ? b_n - jf : 0);
+        const int per = static_cast<int>((jcount + NL - 1) / NL);
+        int i = 0;
+        bool have_i = false;
+        for (int k = 0; k < per; ++k) {
+          const int j = jf + cl * per + k;
+          if (j >= b_n) break;
+          const int64_t e = wBe[j];
+          if (e >= r_hi) break;
+          if (!have_i) {
+            i = smem_lower_bound(wAe, na_t, e);
+            have_i = true;
+          } else {
+            while (wAe[i] < e) ++i;
+          }
+          if (wAe[i] == e) continue;  // tie: closed by the driver end
+          const int64_t pa = wAe[i - 1];
+          const int64_t pb = j > 0 ? wBe[j - 1] : INT64_MIN;
+          fold(wAv[i], wBv[j], e - (pa > pb ? pa : pb));
+        }
+        if (spill) {  // other-list ends past the window: strided over consumer lanes
+          for (int64_t gj = b_lo + b_n + cl; gj < nb; gj += NL) {
+            const int64_t e = ldg64(Be, gj);
+            if (e >= r_hi) break;
+            if (e <= r_lo) continue;
+            const int ii = smem_lower_bound(wAe, na_t, e);
+            if (wAe[ii] == e) continue;
+            const int64_t pa = wAe[ii - 1];
+            const int64_t pb = ldg64(Be, gj - 1);
+            fold(wAv[ii], Bv[gj], e - (pa > pb ? pa : pb));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  if (lerr) atomicOr(err, 1);
+
+  __shared__ uint64_t ru[BLOCK / 32 + 1];
+  __shared__ double rf[BLOCK / 32 + 1];
+  __shared__ uint64_t rn[BLOCK / 32 + 1];
+  __shared__ bool last;
+  isum = warp_sum(isum);
+  fsum = warp_sum(fsum);
+  uint64_t ucnt = warp_sum(static_cast<uint64_t>(cnt));
+  if (lane == 0) {
+    ru[wid] = isum;
+    rf[wid] = fsum;
+    rn[wid] = ucnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    AggPart pp{};
+    for (int w = 0; w < BLOCK / 32; ++w) {
+      pp.isum += ru[w];
+      pp.fsum += rf[w];
+      pp.cnt += static_cast<long long>(rn[w]);
+    }
+    parts[blockIdx.x] = pp;
+    __threadfence();
+    last = atomicInc(ticket, gridDim.x - 1) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  isum = 0;
+  fsum = 0.0;
+  ucnt = 0;
+  for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += BLOCK) {
+    isum += __ldcg(&parts[i].isum);
+    fsum += __ldcg(&parts[i].fsum);
+    ucnt += static_cast<uint64_t>(__ldcg(&parts[i].cnt));
+  }
+  isum = block_sum<BLOCK>(isum, ru);
+  fsum = block_sum<BLOCK>(fsum, rf);
+  ucnt = block_sum<BLOCK>(ucnt, rn);
+  if (threadIdx.x == 0) {
+    AggPart pp{};
+    pp.isum = isum;
+    pp.fsum = fsum;
+    pp.cnt = static_cast<long long>(ucnt);
+    pp.imin = INT64_MAX;
+    pp.imax = INT64_MIN;
+    pp.fmin = INFINITY;
+    pp.fmax = -INFINITY;
+    pp.pad = __longlong_as_double(static_cast<long long>(atomicExch(err, 0)));
+    *out = pp;
+  }
+}
+
 }  // namespace dev
 
 namespace {
@@ -562,10 +893,94 @@ void launch_gapless(const CtxPtr& ctx, unsigned g, const dev::MergeArgs& m, cons
   }
 }
 
+// ---- persistent TMA form (K2) ----
+constexpr int TPB = 256, TPI = 3, TPW = 1024;
+constexpr int TP_TA = (TPB - 32) * TPI;
+using TPStage = dev::PairStage<TP_TA, TPW>;
+constexpr size_t TP_SMEM = 2 * TPStage::BYTES;
+
+template <class T, int OP, int KIND>
+void launch_pair_tma3(const CtxPtr& ctx, const DCol& A, const DCol& B, int swap, dev::AggPart* parts,
+                      dev::AggPart* out, int64_t ntiles, int64_t& grid_out, bool dry) {
+  auto k = dev::k_pair_reduce_tma<TPB, TPI, TPW, T, OP, KIND>;
+  static int occ = 0;
+  if (!occ) {
+    RQ_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TP_SMEM)));
+    RQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, TPB, TP_SMEM));
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = static_cast<int64_t>(ctx->sm_count) * occ;
+  if (grid > ntiles) grid = ntiles;
+  grid_out = grid;
+  if (dry) return;
+  k<<<static_cast<unsigned>(grid), TPB, TP_SMEM, ctx->stream>>>(
+      A.e.pos(), static_cast<const T*>(A.v.raw()), A.e.n, B.e.pos(), static_cast<const T*>(B.v.raw()), B.e.n, swap,
+      ntiles, parts, ctx->tickets, out, reinterpret_cast<int*>(ctx->tickets + 3));
+}
+
+template <class T, int OP>
+void launch_pair_tma2(int kind, const CtxPtr& ctx, const DCol& A, const DCol& B, int swap, dev::AggPart* parts,
+                      dev::AggPart* out, int64_t ntiles, int64_t& grid, bool dry) {
+  switch (kind) {
+    case 0: launch_pair_tma3<T, OP, 0>(ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+    case 1: launch_pair_tma3<T, OP, 1>(ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+    default: launch_pair_tma3<T, OP, 2>(ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+  }
+}
+
+template <class T>
+void launch_pair_tma1(int op, int kind, const CtxPtr& ctx, const DCol& A, const DCol& B, int swap,
+                      dev::AggPart* parts, dev::AggPart* out, int64_t ntiles, int64_t& grid, bool dry) {
+  switch (op) {
+    case RQ_ADD: launch_pair_tma2<T, RQ_ADD>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+    case RQ_SUB: launch_pair_tma2<T, RQ_SUB>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+    case RQ_MUL: launch_pair_tma2<T, RQ_MUL>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+    default: launch_pair_tma2<T, RQ_DIV>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+  }
+}
+
+// gapless RLE × gapless RLE with 8-byte values of the arithmetic type, every
+// array bulk-copyable: the persistent kernel (one launch). false otherwise.
+bool pair_reduce_tma(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bool flt, int kind, AggHost& h) {
+  const int32_t tdt = flt ? RQ_F64 : RQ_I64;
+  if (a.v.dt != tdt || b.v.dt != tdt) return false;
+  if (!tma_ok(a.e) || !tma_ok(a.v) || !tma_ok(b.e) || !tma_ok(b.v)) return false;
+  const bool a_drives = a.e.n >= b.e.n;  // the list with more runs drives
+  const DCol& A = a_drives ? a : b;
+  const DCol& B = a_drives ? b : a;
+  const int swap = a_drives ? 0 : 1;
+  const int64_t ntiles = (A.e.n + TP_TA - 1) / TP_TA;
+  int64_t grid = 0;
+  if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, nullptr, nullptr, ntiles, grid, true);
+  else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, nullptr, nullptr, ntiles, grid, true);
+  DArr parts = alloc_arr(ctx, RQ_I64, grid * static_cast<int64_t>(sizeof(dev::AggPart) / 8));
+  DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8);
+  {
+    KTimer timer(ctx, "pair_reduce");
+    if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ntiles, grid, false);
+    else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ntiles, grid, false);
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  const auto* p = reinterpret_cast<const dev::AggPart*>(ctx->readback(out.raw(), sizeof(dev::AggPart)));
+  h.isum = p->isum;
+  h.fsum = p->fsum;
+  h.cnt = p->cnt;
+  long long e;
+  std::memcpy(&e, &p->pad, 8);
+  if (!flt && op == RQ_DIV && e) fail("integer division by zero");
+  return true;
+}
+
 // fast_kind: gapless fast-path accumulator (0 SUM int, 1 SUM f64/AVG, 2
 // COUNT) or -1 for the general walk (VAR/STD passes, gapped inputs).
 AggHost pair_reduce(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bool gapless,
                     bool flt, bool pass2, double mean, int fast_kind = -1) {
+  if (gapless && fast_kind >= 0 && !pass2) {
+    AggHost h;
+    const char* off = std::getenv("RQ_NO_TMA");
+    if (!(off && off[0] == '1') && pair_reduce_tma(ctx, a, b, op, flt, fast_kind, h)) return h;
+  }
   constexpr int TILE = PB * PI;
   const int64_t na = a.e.n, nb = b.e.n;
   const int64_t ntiles = (na + nb + TILE - 1) / TILE;

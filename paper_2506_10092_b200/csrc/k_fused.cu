@@ -506,21 +506,6 @@ __device__ __forceinline__ TmaWin tma_window(int64_t lo, int est, int cap, int64
 }
 __device__ __forceinline__ uint32_t ceil16(uint32_t x) { return (x + 15u) & ~15u; }
 
-// lower_bound over a shared-memory window padded with INT64_MAX up to the
-// power of two L (uniform per CTA; L <= CAP): log2(L) steps of
-// load / compare / select / add, no bounds tests
-template <int CAP>
-__device__ __forceinline__ int smem_lb_pow2(const int64_t* a, int L, int64_t key) {
-  int pos = 0;
-#pragma unroll
-  for (int step = CAP / 2; step > 0; step >>= 1)
-    if (step < L) pos = a[pos + step - 1] < key ? pos + step : pos;
-  return pos + (a[pos] < key ? 1 : 0);
-}
-__device__ __forceinline__ int pow2_above(int n) {  // smallest power of two > n (n >= 0)
-  return n > 0 ? 1 << (32 - __clz(n)) : 1;
-}
-
 // one pipeline stage: A's run-end window, C's run-end window and C's values
 template <int AW, int CW>
 struct C2Stage {
@@ -933,14 +918,6 @@ int64_t launch_tma1(int op, int ck, const CtxPtr& ctx, const TmaLaunch& f, bool 
   }
 }
 
-// bulk copies need 16-B aligned bases and room to round a copy up to 16
-// elements inside the allocation
-bool tma_ok(const DArr& a) {
-  if (!a.buf || !a.buf->ptr) return a.n == 0;
-  const size_t w = static_cast<size_t>(dt_width(a.dt));
-  return (reinterpret_cast<uintptr_t>(a.buf->ptr) & 15) == 0 &&
-         a.buf->cap >= static_cast<size_t>((a.n + 15) & ~int64_t(15)) * w;
-}
 
 }  // namespace
 

@@ -158,6 +158,15 @@ struct DArr {
 };
 
 DArr alloc_arr(const CtxPtr& ctx, int32_t dt, int64_t n);
+// bulk copies need 16-B aligned bases and room to round a copy up to 16
+// elements inside the allocation
+inline bool tma_ok(const DArr& a) {
+  if (!a.buf || !a.buf->ptr) return a.n == 0;
+  const size_t w = static_cast<size_t>(dt_width(a.dt));
+  return (reinterpret_cast<uintptr_t>(a.buf->ptr) & 15) == 0 &&
+         a.buf->cap >= static_cast<size_t>((a.n + 15) & ~int64_t(15)) * w;
+}
+
 DArr upload_arr(const CtxPtr& ctx, int32_t dt, const void* host, int64_t n);
 void download_arr(const CtxPtr& ctx, const DArr& a, void* host);
 // Device-side copy of the first n elements into a new array.
