@@ -692,6 +692,12 @@ bool build_multi_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, Gr
 
 }  // namespace
 
+namespace {
+bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
+              const std::vector<XExpr>& exprs, const std::vector<int>& fns, GroupAggOut& out,
+              const GroupKey* preK = nullptr);
+}  // namespace
+
 // Returns false when the inputs are not in the fused shape (caller then runs
 // the general aligned path).
 bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
@@ -732,6 +738,30 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
     }
   }
   KTimer timer(ctx, "group_fused");
+  // Plain / Plain+Index SUM and AVG over fully covered keys: one K12 row pass
+  // streams all of them together (decode baked into the generated kernel)
+  std::vector<size_t> x_idx;
+  GroupAggOut x_out;
+  bool x_ok = false;
+  if (kcov == total) {
+    std::vector<XExpr> xe;
+    std::vector<int> xf;
+    for (size_t i = 0; i < data.size(); ++i) {
+      const DCol& d = *data[i];
+      if ((d.enc == RQ_ENC_PLAIN || d.enc == RQ_ENC_PLAIN_INDEX) && (fns[i] == RQ_SUM || fns[i] == RQ_AVG) &&
+          xe.size() < 4) {
+        XExpr x;
+        XTerm t;
+        t.col = &d;
+        x.terms.push_back(t);
+        xe.push_back(x);
+        xf.push_back(fns[i]);
+        x_idx.push_back(i);
+      }
+    }
+    if (!xe.empty()) x_ok = xg_fused(ctx, nullptr, keys, xe, xf, x_out, &K);
+    if (!x_ok) x_idx.clear();
+  }
   // counts / presence from the key runs
   DArr cnt = new_table(ctx, K.G, 0);
   {
@@ -758,6 +788,13 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
     out.keys.push_back(kout);
   }
   for (size_t i = 0; i < data.size(); ++i) {
+    bool taken = false;
+    for (size_t j = 0; j < x_idx.size(); ++j)
+      if (x_idx[j] == i && x_out.n_groups == ng) {
+        out.vals.push_back(x_out.vals[j]);
+        taken = true;
+      }
+    if (taken) continue;
     const DCol& d = *data[i];
     const int fn = fns[i];
     const bool flt = dt_float(d.value_type());
@@ -1220,7 +1257,8 @@ DArr xg_const_bits(const CtxPtr& ctx, const DArr& v) {
 }
 
 bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
-              const std::vector<XExpr>& exprs, const std::vector<int>& fns, GroupAggOut& out) {
+              const std::vector<XExpr>& exprs, const std::vector<int>& fns, GroupAggOut& out,
+              const GroupKey* preK) {
   if (exprs.size() > static_cast<size_t>(dev::XG_EXPRS) || keys.size() > 8) return false;
   const int64_t total = !keys.empty() ? keys[0]->total
                         : mask        ? mask->total
@@ -1299,7 +1337,9 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
 
   // ---- segment table: keys ∩ mask ∩ RLE operands (align_many's joint shape) ----
   GroupKey K;
-  if (!keys.empty()) {
+  if (preK) {
+    K = *preK;
+  } else if (!keys.empty()) {
     if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
   } else {
     const int64_t zs = 0, ze = total - 1, zslot = 0;
