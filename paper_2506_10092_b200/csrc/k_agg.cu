@@ -358,7 +358,7 @@ template <int TA, int BW>
 struct PairStage {
   static constexpr int AE = TA + 2 + 16;  // ends: 2 previous + tile (+ rounding)
   static constexpr int AV = TA + 16;
-  static constexpr int BE = BW + 16;      // window padded to the power of two BW (+8 forward steps)
+  static constexpr int BE = BW + 16;      // window padded to BW (+8 for the forward steps)
   static constexpr size_t AE_OFF = 0;
   static constexpr size_t AV_OFF = AE_OFF + AE * 8;
   static constexpr size_t BE_OFF = AV_OFF + AV * 8;
@@ -367,10 +367,10 @@ struct PairStage {
 };
 
 template <int BLOCK, int IA, int BW, class T, int OP, int KIND>
-__global__ void __launch_bounds__(BLOCK, 4)
+__global__ void __launch_bounds__(BLOCK, 8)
     k_pair_reduce_tma(const int64_t* __restrict__ Ae, const T* __restrict__ Av, int64_t na,
                       const int64_t* __restrict__ Be, const T* __restrict__ Bv, int64_t nb, int swap,
-                      int64_t ntiles, AggPart* __restrict__ parts, unsigned* __restrict__ ticket,
+                      int ta, int64_t ntiles, AggPart* __restrict__ parts, unsigned* __restrict__ ticket,
                       AggPart* __restrict__ out, int* __restrict__ err) {
   constexpr int NCW = BLOCK / 32 - 1;
   constexpr int NL = NCW * 32;  // consumer lanes
@@ -405,20 +405,21 @@ __global__ void __launch_bounds__(BLOCK, 4)
     // ---- producer ----
     int64_t jb = 0, b_lo = 0;
     int b_est = BW, b_n = 0;
+    int hw0 = BW + 8, hw1 = BW + 8;  // per stage: entries [hw, BW + 8) still hold the pad
     for (int64_t t = t_begin; t < t_end; ++t) {
       const int st = static_cast<int>((t - t_begin) & 1);
       const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
-      const int64_t a0 = t * TA;
-      const int na_t = static_cast<int>(min(static_cast<int64_t>(TA), na - a0));
+      const int64_t a0 = t * ta;
+      const int na_t = static_cast<int>(min(static_cast<int64_t>(ta), na - a0));
       if (t == t_begin) {
         const int64_t r_lo = a0 > 0 ? ldg64(Ae, a0 - 1) : -1;
         jb = warp_lower_bound(Be, nb, r_lo + 1);
       } else {
         mbar_wait(&full[st ^ 1], ((t - 1 - t_begin) >> 1) & 1);  // tile t-1 landed
         const int pst = st ^ 1;
-        const int pna = static_cast<int>(min(static_cast<int64_t>(TA), na - (a0 - TA)));
+        const int pna = static_cast<int>(min(static_cast<int64_t>(ta), na - (a0 - ta)));
         const int64_t r_prev_hi = sAe(pst)[2 + pna - 1];
-        const int rb = smem_lb_pow2<BW>(sBe(pst), BW, r_prev_hi + 1);
+        const int rb = smem_lower_bound(sBe(pst), BW, r_prev_hi + 1);
         int64_t jn = b_lo + rb;
         if (rb >= b_n && jn < nb) jn += warp_lower_bound(Be + jn, nb - jn, r_prev_hi + 1);
         const int64_t used = jn - jb;
@@ -450,7 +451,11 @@ __global__ void __launch_bounds__(BLOCK, 4)
         wBe[b_bulk] = ldg64(Be, b_lo + b_bulk);
         wBv[b_bulk] = Bv[b_lo + b_bulk];
       }
-      for (int i = b_n + lane; i < BW + 8; i += 32) wBe[i] = INT64_MAX;
+      {  // re-pad only what earlier copies into this stage overwrote
+        int& hw = st == 0 ? hw0 : hw1;
+        for (int i = b_n + lane; i < hw; i += 32) wBe[i] = INT64_MAX;
+        hw = b_n;
+      }
       if (lane != 0) mbar_arrive(&full[st]);
       if (lane == 0) {
         s_lo[st] = b_lo;
@@ -488,8 +493,8 @@ __global__ void __launch_bounds__(BLOCK, 4)
     for (int64_t t = t_begin; t < t_end; ++t) {
       const int st = static_cast<int>((t - t_begin) & 1);
       const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
-      const int64_t a0 = t * TA;
-      const int na_t = static_cast<int>(min(static_cast<int64_t>(TA), na - a0));
+      const int64_t a0 = t * ta;
+      const int na_t = static_cast<int>(min(static_cast<int64_t>(ta), na - a0));
       mbar_wait(&full[st], use & 1u);
       const int64_t b_lo = s_lo[st];
       const int b_n = s_nb[st];
@@ -501,7 +506,7 @@ __global__ void __launch_bounds__(BLOCK, 4)
       // other-list window entries: [jf, jl) end inside (r_lo, r_hi); entry jl
       // is the run covering r_hi (uniform searches)
       const int jf = s_jf[st];  // = jb - window start (the producer's search)
-      const int jl = smem_lb_pow2<BW>(wBe, BW, r_hi);
+      const int jl = smem_lower_bound(wBe, BW, r_hi);
       if (jl < b_n) {
         // fast path: merge path over the tile's driver ends and the window's
         // ends, ITEMS-free even split of the merged sequence over the lanes;
@@ -523,20 +528,31 @@ __global__ void __launch_bounds__(BLOCK, 4)
           const int64_t pa0 = wAe[x - 1];
           const int64_t pb0 = jf + y > 0 ? wB[y - 1] : INT64_MIN;
           int64_t prev = pa0 > pb0 ? pa0 : pb0;
+          // branch-free steps (no divergence between lanes taking A or B):
+          // both cursors' keys and values are reloaded every step; reads at
+          // x = na_t / y = nbi stay inside the stage (slack entries / run jl)
           int64_t ka = x < na_t ? wAe[x] : INT64_MAX;
           int64_t kb = y < nbi ? wB[y] : INT64_MAX;
+          T va = wAv[x], vb = vB[y];
           for (int it = d; it < dend; ++it) {
             const bool takeA = ka <= kb;
             const int64_t key = takeA ? ka : kb;
-            fold(wAv[x], vB[y], key - prev);  // x / y: the runs covering key
-            prev = key;
-            if (takeA) {
-              ++x;
-              ka = x < na_t ? wAe[x] : INT64_MAX;
+            const int64_t len = key - prev;  // 0 on a tie: no fragment
+            if (KIND == 2) {
+              cnt += len;
+            } else if (KIND == 0 && OP != RQ_DIV) {
+              const T r = swap ? arith_t<T>(vb, va, OP, &lerr) : arith_t<T>(va, vb, OP, &lerr);
+              isum += static_cast<uint64_t>(static_cast<int64_t>(r)) * static_cast<uint64_t>(len);
             } else {
-              ++y;
-              kb = y < nbi ? wB[y] : INT64_MAX;
+              fold(va, vb, len);
             }
+            prev = key;
+            x += takeA ? 1 : 0;
+            y += takeA ? 0 : 1;
+            ka = x < na_t ? wAe[x] : INT64_MAX;
+            kb = y < nbi ? wB[y] : INT64_MAX;
+            va = wAv[x];
+            vb = vB[y];
           }
         }
       } else {
@@ -546,7 +562,7 @@ __global__ void __launch_bounds__(BLOCK, 4)
         // (a) fragments ending at driver ends
         const int i0 = cl * IA;
         if (i0 < na_t) {
-          int j = smem_lb_pow2<BW>(wBe, BW, wAe[i0]);
+          int j = smem_lower_bound(wBe, BW, wAe[i0]);
   #pragma unroll
           for (int k = 0; k < IA; ++k) {
             const int i = i0 + k;
@@ -574,7 +590,7 @@ __global__ void __launch_bounds__(BLOCK, 4)
         // (b) fragments ending at other-list ends strictly inside (r_lo, r_hi)
         // that are not driver ends; ends past the staged window come from
         // global memory (rare)
-        const int jf = smem_lb_pow2<BW>(wBe, BW, r_lo + 1);  // first window end > r_lo (uniform)
+        const int jf = smem_lower_bound(wBe, BW, r_lo + 1);  // first window end > r_lo (uniform)
         const int64_t last_in = wBe[b_n > 0 ? b_n - 1 : 0];
         const bool spill = b_n == 0 || (last_in < r_hi && b_lo + b_n < nb);
         const int64_t jcount = (b_n > jf ? b_n - jf : 0);
@@ -894,14 +910,14 @@ void launch_gapless(const CtxPtr& ctx, unsigned g, const dev::MergeArgs& m, cons
 }
 
 // ---- persistent TMA form (K2) ----
-constexpr int TPB = 256, TPI = 3, TPW = 1024;
+constexpr int TPB = 128, TPI = 10, TPW = 768;
 constexpr int TP_TA = (TPB - 32) * TPI;
 using TPStage = dev::PairStage<TP_TA, TPW>;
 constexpr size_t TP_SMEM = 2 * TPStage::BYTES;
 
 template <class T, int OP, int KIND>
 void launch_pair_tma3(const CtxPtr& ctx, const DCol& A, const DCol& B, int swap, dev::AggPart* parts,
-                      dev::AggPart* out, int64_t ntiles, int64_t& grid_out, bool dry) {
+                      dev::AggPart* out, int ta, int64_t ntiles, int64_t& grid_out, bool dry) {
   auto k = dev::k_pair_reduce_tma<TPB, TPI, TPW, T, OP, KIND>;
   static int occ = 0;
   if (!occ) {
@@ -915,27 +931,27 @@ void launch_pair_tma3(const CtxPtr& ctx, const DCol& A, const DCol& B, int swap,
   if (dry) return;
   k<<<static_cast<unsigned>(grid), TPB, TP_SMEM, ctx->stream>>>(
       A.e.pos(), static_cast<const T*>(A.v.raw()), A.e.n, B.e.pos(), static_cast<const T*>(B.v.raw()), B.e.n, swap,
-      ntiles, parts, ctx->tickets, out, reinterpret_cast<int*>(ctx->tickets + 3));
+      ta, ntiles, parts, ctx->tickets, out, reinterpret_cast<int*>(ctx->tickets + 3));
 }
 
 template <class T, int OP>
 void launch_pair_tma2(int kind, const CtxPtr& ctx, const DCol& A, const DCol& B, int swap, dev::AggPart* parts,
-                      dev::AggPart* out, int64_t ntiles, int64_t& grid, bool dry) {
+                      dev::AggPart* out, int ta, int64_t ntiles, int64_t& grid, bool dry) {
   switch (kind) {
-    case 0: launch_pair_tma3<T, OP, 0>(ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
-    case 1: launch_pair_tma3<T, OP, 1>(ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
-    default: launch_pair_tma3<T, OP, 2>(ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+    case 0: launch_pair_tma3<T, OP, 0>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    case 1: launch_pair_tma3<T, OP, 1>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    default: launch_pair_tma3<T, OP, 2>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
   }
 }
 
 template <class T>
 void launch_pair_tma1(int op, int kind, const CtxPtr& ctx, const DCol& A, const DCol& B, int swap,
-                      dev::AggPart* parts, dev::AggPart* out, int64_t ntiles, int64_t& grid, bool dry) {
+                      dev::AggPart* parts, dev::AggPart* out, int ta, int64_t ntiles, int64_t& grid, bool dry) {
   switch (op) {
-    case RQ_ADD: launch_pair_tma2<T, RQ_ADD>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
-    case RQ_SUB: launch_pair_tma2<T, RQ_SUB>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
-    case RQ_MUL: launch_pair_tma2<T, RQ_MUL>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
-    default: launch_pair_tma2<T, RQ_DIV>(kind, ctx, A, B, swap, parts, out, ntiles, grid, dry); break;
+    case RQ_ADD: launch_pair_tma2<T, RQ_ADD>(kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    case RQ_SUB: launch_pair_tma2<T, RQ_SUB>(kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    case RQ_MUL: launch_pair_tma2<T, RQ_MUL>(kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    default: launch_pair_tma2<T, RQ_DIV>(kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
   }
 }
 
@@ -949,16 +965,22 @@ bool pair_reduce_tma(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bo
   const DCol& A = a_drives ? a : b;
   const DCol& B = a_drives ? b : a;
   const int swap = a_drives ? 0 : 1;
-  const int64_t ntiles = (A.e.n + TP_TA - 1) / TP_TA;
+  // driver runs per tile: the full capacity unless the other list is dense
+  // enough that its window would overflow (expected window ≈ ta · nb / na)
+  int ta = TP_TA;
+  const double ratio = static_cast<double>(B.e.n) / static_cast<double>(A.e.n);
+  const int fit = static_cast<int>((TPW - 16 - 64) / std::max(ratio, 1e-9) * 0.9);
+  if (fit < ta) ta = std::max(64, fit & ~1);
+  const int64_t ntiles = (A.e.n + ta - 1) / ta;
   int64_t grid = 0;
-  if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, nullptr, nullptr, ntiles, grid, true);
-  else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, nullptr, nullptr, ntiles, grid, true);
+  if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, nullptr, nullptr, ta, ntiles, grid, true);
+  else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, nullptr, nullptr, ta, ntiles, grid, true);
   DArr parts = alloc_arr(ctx, RQ_I64, grid * static_cast<int64_t>(sizeof(dev::AggPart) / 8));
   DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8);
   {
     KTimer timer(ctx, "pair_reduce");
-    if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ntiles, grid, false);
-    else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ntiles, grid, false);
+    if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ta, ntiles, grid, false);
+    else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ta, ntiles, grid, false);
     ctx->count_launch();
     RQ_CUDA_CHECK(cudaGetLastError());
   }

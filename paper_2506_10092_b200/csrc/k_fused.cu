@@ -536,7 +536,7 @@ __device__ __forceinline__ void load_keys(const int64_t* __restrict__ P, int64_t
   }
 }
 
-template <int BLOCK, int ITEMS, int AW, int CW, class T, int OP, int CK, bool SAME>
+template <int BLOCK, int ITEMS, int AW, int CW, int NS, class T, int OP, int CK, bool SAME>
 __global__ void __launch_bounds__(BLOCK, 4)
     k_points_filtered_reduce_tma(const int64_t* __restrict__ P, const void* __restrict__ yv, int ydt,
                                  int64_t np, XSpec x, CSpec c, int64_t ntiles, int swap,
@@ -547,9 +547,9 @@ __global__ void __launch_bounds__(BLOCK, 4)
   constexpr bool HAS_C = CK != C_PLAIN;
   using S = C2Stage<AW, CW>;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[2], empty[2];
-  __shared__ int64_t s_lo[2][2];  // [stage][A, C] first staged run
-  __shared__ int s_n[2][2];       // [stage][A, C] staged runs
+  __shared__ uint64_t full[NS], empty[NS];
+  __shared__ int64_t s_lo[NS][2];  // [stage][A, C] first staged run
+  __shared__ int s_n[NS][2];       // [stage][A, C] staged runs
 
   const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * ntiles / gridDim.x;
   const int64_t t_end = static_cast<int64_t>(blockIdx.x + 1) * ntiles / gridDim.x;
@@ -560,10 +560,10 @@ __global__ void __launch_bounds__(BLOCK, 4)
   auto sCv = [&](int st) { return smem + st * S::BYTES + S::CV_OFF; };
 
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 32);  // every producer lane arrives (releasing its own stores)
-    mbar_init(&full[1], 32);
-    mbar_init(&empty[0], NCW);
-    mbar_init(&empty[1], NCW);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 32);  // every producer lane arrives (releasing its own stores)
+      mbar_init(&empty[i], NCW);
+    }
   }
   __syncthreads();
 
@@ -580,26 +580,32 @@ __global__ void __launch_bounds__(BLOCK, 4)
     // capacity (+8 for the fixed-width forward steps) are written by the
     // lanes, outside the copied range, before the arrive that publishes them.
     int64_t a_cur = 0, c_cur = 0, a_lo16 = 0, c_lo16 = 0;
+    // per stage: entries [hw, W + 8) still hold the pad (only what earlier
+    // copies into a stage overwrote is re-padded)
+    int hwA[NS], hwC[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) hwA[i] = AW + 8, hwC[i] = CW + 8;
     int a_est = AW, c_est = CW, a_n = 0, c_n = 0;
     int64_t pf = t_begin < t_end ? ldg64(P, t_begin * TILE) : 0;
     for (int64_t t = t_begin; t < t_end; ++t) {
-      const int st = static_cast<int>((t - t_begin) & 1);
-      const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
+      const int st = static_cast<int>((t - t_begin) % NS);
+      const uint32_t use = static_cast<uint32_t>((t - t_begin) / NS);
+      const int pst = static_cast<int>((t - 1 - t_begin + NS) % NS);  // tile t-1's stage
       const int64_t p_first = pf;
       if (t + 1 < t_end) pf = ldg64(P, (t + 1) * TILE);
       if (t == t_begin) {
         a_cur = warp_lower_bound(x.e, x.n, p_first);
         if (HAS_C) c_cur = warp_lower_bound(c.e, c.n, p_first);
       } else {
-        mbar_wait(&full[st ^ 1], ((t - 1 - t_begin) >> 1) & 1);  // tile t-1 landed
-        const int ra = smem_lb_pow2<AW>(sA(st ^ 1), AW, p_first);
+        mbar_wait(&full[pst], ((t - 1 - t_begin) / NS) & 1);  // tile t-1 landed
+        const int ra = smem_lb_pow2<AW>(sA(pst), AW, p_first);
         int64_t an = a_lo16 + ra;
         if (ra >= a_n && an < x.n) an += warp_lower_bound(x.e + an, x.n - an, p_first);
         const int64_t ua = an - a_cur;  // runs spanned by tile t-1
         a_est = static_cast<int>(min(static_cast<int64_t>(AW), ua + (ua >> 2) + 32));
         a_cur = an;
         if (HAS_C) {
-          const int rc = smem_lb_pow2<CW>(sC(st ^ 1), CW, p_first);
+          const int rc = smem_lb_pow2<CW>(sC(pst), CW, p_first);
           int64_t cn = c_lo16 + rc;
           if (rc >= c_n && cn < c.n) cn += warp_lower_bound(c.e + cn, c.n - cn, p_first);
           const int64_t uc = cn - c_cur;
@@ -607,7 +613,7 @@ __global__ void __launch_bounds__(BLOCK, 4)
           c_cur = cn;
         }
       }
-      if (t - t_begin >= 2) mbar_wait(&empty[st], (use - 1) & 1);  // consumers done with tile t-2
+      if (t - t_begin >= NS) mbar_wait(&empty[st], (use - 1) & 1);  // consumers done with tile t-NS
       // staged counts: whole 16-run chunks (< W), clipped at the column end
       auto stage_n = [](int64_t lo, int est, int W, int64_t total, int64_t& lo16) {
         lo16 = lo & ~int64_t(15);
@@ -624,15 +630,22 @@ __global__ void __launch_bounds__(BLOCK, 4)
       unsigned char* wCv = sCv(st);
       const int a_bulk = a_n & ~15, c_bulk = c_n & ~15;
       for (int i = a_bulk + lane; i < a_n; i += 32) wA[i] = ldg64(x.e, a_lo16 + i);
-      for (int i = a_n + lane; i < AW + 8; i += 32) wA[i] = INT64_MAX;
+      int hwa = hwA[0], hwc = hwC[0];
+#pragma unroll
+      for (int i = 1; i < NS; ++i)
+        if (st == i) hwa = hwA[i], hwc = hwC[i];
+      for (int i = a_n + lane; i < hwa; i += 32) wA[i] = INT64_MAX;
       if (HAS_C) {
         for (int i = c_bulk + lane; i < c_n; i += 32) {
           wC[i] = ldg64(c.e, c_lo16 + i);
           const unsigned char* src = static_cast<const unsigned char*>(c.v) + (c_lo16 + i) * wc;
           for (int j = 0; j < wc; ++j) wCv[i * wc + j] = src[j];
         }
-        for (int i = c_n + lane; i < CW + 8; i += 32) wC[i] = INT64_MAX;
+        for (int i = c_n + lane; i < hwc; i += 32) wC[i] = INT64_MAX;
       }
+#pragma unroll
+      for (int i = 0; i < NS; ++i)
+        if (st == i) hwA[i] = a_n, hwC[i] = c_n;
       if (lane != 0) mbar_arrive(&full[st]);
       if (lane == 0) {
         s_lo[st][0] = a_lo16;
@@ -658,8 +671,8 @@ __global__ void __launch_bounds__(BLOCK, 4)
     int64_t cur[ITEMS], nxt[ITEMS];
     if (t_begin < t_end) load_keys<BLOCK, ITEMS>(P, np, t_begin * TILE + i0, cur);
     for (int64_t t = t_begin; t < t_end; ++t) {
-      const int st = static_cast<int>((t - t_begin) & 1);
-      const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
+      const int st = static_cast<int>((t - t_begin) % NS);
+      const uint32_t use = static_cast<uint32_t>((t - t_begin) / NS);
       const int64_t tbase = t * TILE;
       const int npt = static_cast<int>(np - tbase < TILE ? np - tbase : TILE);
       if (t + 1 < t_end) load_keys<BLOCK, ITEMS>(P, np, tbase + TILE + i0, nxt);
@@ -854,9 +867,9 @@ void launch1(int op, int ck, const CtxPtr& ctx, const FusedLaunch& f) {
 }
 
 // ---- persistent TMA path ----
-constexpr int TB = 256, TI = 4, TAW = 2048, TCW = 512;
+constexpr int TB = 256, TI = 4, TAW = 2048, TCW = 512, TNS = 2;  // 3 stages measured slower (3 CTAs/SM)
 using TmaSmem = dev::C2Stage<TAW, TCW>;
-constexpr size_t TMA_SMEM = 2 * TmaSmem::BYTES;
+constexpr size_t TMA_SMEM = TNS * TmaSmem::BYTES;
 
 struct TmaLaunch {
   const DCol* y;
@@ -885,8 +898,8 @@ template <class T, int OP, int CK>
 int64_t launch_tma3(const CtxPtr& ctx, const TmaLaunch& f, bool dry) {
   const int32_t tdt = std::is_same<T, double>::value ? RQ_F64 : RQ_I64;
   const bool same = f.xs.dt == tdt && f.y->v.dt == tdt;
-  auto k_same = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, T, OP, CK, true>;
-  auto k_gen = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, T, OP, CK, false>;
+  auto k_same = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, true>;
+  auto k_gen = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, false>;
   static int occ_same = 0, occ_gen = 0;  // per instantiation
   int& occ = same ? occ_same : occ_gen;
   if (!occ) occ = tma_occupancy(same ? k_same : k_gen);
