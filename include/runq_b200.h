@@ -384,6 +384,27 @@ int rq_group_aggregate_exprs(rq_ctx_t ctx, rq_mask_t mask, const rq_col_t* keys,
                              const rq_expr* exprs, const int32_t* fns, int32_t n_exprs, int64_t* n_groups,
                              rq_arr_t* out_keys, rq_arr_t* out_vals, int32_t* fused);
 
+/* One WHERE conjunct of the runner's predicate tree (runner.cpp:114-193):
+ * `col op k` (compare_scalar, align.cpp:598-652) or, with n_in > 0,
+ * `col IN (in_list[0..n_in))` = OR of equalities (mask_ops.cpp:211-237). */
+typedef struct rq_pred {
+  rq_col_t col;
+  int32_t op;   /* RQ_LT..RQ_GT (ignored when n_in > 0) */
+  int32_t n_in;
+  rq_scalar k;
+  const rq_scalar* in_list;
+} rq_pred;
+
+/* rq_group_aggregate_exprs with the WHERE clause given as conjuncts instead
+ * of a materialised mask (`mask` may still be given: it is AND-ed in). With
+ * RLE predicate columns the predicates are evaluated once per segment of the
+ * joint run alignment (no mask is built); otherwise the mask is built with
+ * compare_scalar / mask_or / mask_and exactly as the runner does. */
+int rq_group_aggregate_where(rq_ctx_t ctx, const rq_pred* where, int32_t n_where, rq_mask_t mask,
+                             const rq_col_t* keys, int32_t n_keys, const rq_expr* exprs, const int32_t* fns,
+                             int32_t n_exprs, int64_t* n_groups, rq_arr_t* out_keys, rq_arr_t* out_vals,
+                             int32_t* fused);
+
 /* ---------------------------------------------------------------------- */
 /* row-range sharding (multi-GPU; no reference counterpart)                 */
 /* ---------------------------------------------------------------------- */

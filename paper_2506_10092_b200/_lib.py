@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .host import EncodingChoice, Expr, Heuristic, HostColumn, HostMask, Scalar
+from .host import EncodingChoice, Expr, Heuristic, HostColumn, HostMask, Pred, Scalar
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librunq_b200.so")
 
@@ -87,6 +87,8 @@ PROTOTYPES = {
                                               P(C.c_double)]),
     "rq_group_aggregate_exprs": (C.c_int, [vp, vp, P(vp), i32, P(Expr), P(i32), i32, P(i64), P(vp), P(vp),
                                            P(i32)]),
+    "rq_group_aggregate_where": (C.c_int, [vp, P(Pred), i32, vp, P(vp), i32, P(Expr), P(i32), i32, P(i64), P(vp),
+                                           P(vp), P(i32)]),
     "rq_shard_host_column": (C.c_int, [P(HostColumn), i64, i64, P(HostColumn)]),
     "rq_host_column_free": (None, [P(HostColumn)]),
 }

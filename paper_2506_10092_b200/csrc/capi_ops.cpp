@@ -363,9 +363,10 @@ int rq_filtered_aggregate_binop(rq_ctx_t c, rq_col_t pred, rq_scalar k, int32_t 
   });
 }
 
-int rq_group_aggregate_exprs(rq_ctx_t c, rq_mask_t mask, const rq_col_t* keys, int32_t n_keys,
-                             const rq_expr* exprs, const int32_t* fns, int32_t n_exprs, int64_t* n_groups,
-                             rq_arr_t* out_keys, rq_arr_t* out_vals, int32_t* fused) {
+static int group_aggregate_exprs_api(rq_ctx_t c, const rq_pred* where, int32_t n_where, rq_mask_t mask,
+                                     const rq_col_t* keys, int32_t n_keys, const rq_expr* exprs,
+                                     const int32_t* fns, int32_t n_exprs, int64_t* n_groups, rq_arr_t* out_keys,
+                                     rq_arr_t* out_vals, int32_t* fused) {
   return api_guard([&] {
     auto ctx = ctx_of(c);
     require(n_exprs > 0 && exprs != nullptr && fns != nullptr, "group_aggregate_exprs: no expressions");
@@ -391,13 +392,40 @@ int rq_group_aggregate_exprs(rq_ctx_t c, rq_mask_t mask, const rq_col_t* keys, i
       }
       f.push_back(fns[i]);
     }
+    std::vector<XPred> preds;
+    for (int i = 0; i < n_where; ++i) {
+      XPred q;
+      q.col = &col_of(where[i].col);
+      q.op = where[i].op;
+      q.k = scal(where[i].k);
+      require(where[i].n_in >= 0, "where: negative IN-list length");
+      if (where[i].n_in == 0) require(q.op >= RQ_LT && q.op <= RQ_GT, "compare_scalar: comparison operator required");
+      for (int j = 0; j < where[i].n_in; ++j) q.in.push_back(scal(where[i].in_list[j]));
+      preds.push_back(q);
+    }
     bool was_fused = false;
-    GroupAggOut r = group_aggregate_exprs(ctx, mask ? &mask_of(mask) : nullptr, k, xs, f, &was_fused);
+    GroupAggOut r = group_aggregate_exprs(ctx, mask ? &mask_of(mask) : nullptr, k, xs, f, &was_fused,
+                                          preds.empty() ? nullptr : &preds);
     if (fused) *fused = was_fused ? 1 : 0;
     if (n_groups) *n_groups = r.n_groups;
     for (int i = 0; i < n_keys; ++i) out_keys[i] = wrap_arr(r.keys[static_cast<size_t>(i)]);
     for (int i = 0; i < n_exprs; ++i) out_vals[i] = wrap_arr(r.vals[static_cast<size_t>(i)]);
   });
+}
+
+int rq_group_aggregate_exprs(rq_ctx_t c, rq_mask_t mask, const rq_col_t* keys, int32_t n_keys,
+                             const rq_expr* exprs, const int32_t* fns, int32_t n_exprs, int64_t* n_groups,
+                             rq_arr_t* out_keys, rq_arr_t* out_vals, int32_t* fused) {
+  return group_aggregate_exprs_api(c, nullptr, 0, mask, keys, n_keys, exprs, fns, n_exprs, n_groups, out_keys,
+                                   out_vals, fused);
+}
+
+int rq_group_aggregate_where(rq_ctx_t c, const rq_pred* where, int32_t n_where, rq_mask_t mask,
+                             const rq_col_t* keys, int32_t n_keys, const rq_expr* exprs, const int32_t* fns,
+                             int32_t n_exprs, int64_t* n_groups, rq_arr_t* out_keys, rq_arr_t* out_vals,
+                             int32_t* fused) {
+  return group_aggregate_exprs_api(c, where, n_where, mask, keys, n_keys, exprs, fns, n_exprs, n_groups, out_keys,
+                                   out_vals, fused);
 }
 
 // ---- host-side row-range sharding -------------------------------------------------

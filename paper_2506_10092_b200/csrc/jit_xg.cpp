@@ -389,13 +389,76 @@ bool xg_jit_available() { return nvrtc().ok; }
 
 // Launches the generated kernel for plan P; false if it cannot be built
 // (NVRTC missing, too many literals, compile failure).
+// Compact structural signature of a plan (what the generated source depends
+// on): the source is built only on a cache miss.
+std::string plan_signature(const dev::XgPlan& P, int minb) {
+  std::string sig;
+  auto put = [&](int64_t v) { sig += std::to_string(v); sig += ','; };
+  put(minb);
+  put(P.nc);
+  for (int c = 0; c < P.nc; ++c) {
+    put(P.col[c].dt);
+    put(P.col[c].logical);
+    put(P.col[c].has_center);
+    put(P.col[c].flt);
+  }
+  put(P.ncst);
+  for (int j = 0; j < P.ncst; ++j) put(P.cst_f[j]);
+  put(P.ne);
+  for (int e = 0; e < P.ne; ++e) {
+    const dev::XgExpr& X = P.e[e];
+    put(X.nt);
+    put(X.rows);
+    put(X.acc_f);
+    put(X.op[0]);
+    put(X.op[1]);
+    for (int t = 0; t < X.nt; ++t) {
+      put(X.t[t].src);
+      put(X.t[t].flt);
+      put(X.t[t].sop);
+      put(X.t[t].rev);
+      put(X.t[t].kflt);
+    }
+  }
+  return sig;
+}
+
+// literal slots in the order gen_source numbers them
+void plan_literals(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf) {
+  for (int e = 0; e < P.ne; ++e) {
+    const dev::XgExpr& X = P.e[e];
+    if (!X.rows) continue;
+    for (int t = 0; t < X.nt; ++t) {
+      if (X.t[t].sop < 0) continue;
+      if (X.t[t].kflt) kf.push_back(X.t[t].kf);
+      else ki.push_back(X.t[t].ki);
+    }
+  }
+}
+
 bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S, int64_t chunk,
                    unsigned long long* tab, int64_t G, int* err, unsigned blocks) {
   std::vector<int64_t> ki;
   std::vector<double> kf;
-  const std::string src = gen_source(P, ki, kf);
+  plan_literals(P, ki, kf);
   if (ki.size() > 24 || kf.size() > 24) return false;
-  cudaKernel_t k = compile(src);
+  const char* mb = std::getenv("RQ_JIT_MINB");
+  const std::string sig = plan_signature(P, mb ? std::atoi(mb) : 3);
+  cudaKernel_t k = nullptr;
+  {
+    static std::mutex mu;
+    static std::unordered_map<std::string, cudaKernel_t> by_sig;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = by_sig.find(sig);
+    if (it != by_sig.end()) {
+      k = it->second;
+    } else {
+      std::vector<int64_t> ki2;
+      std::vector<double> kf2;
+      k = compile(gen_source(P, ki2, kf2));
+      by_sig[sig] = k;  // nullptr too: a failed compilation is not retried
+    }
+  }
   if (!k) return false;
   XgColArg cols[4] = {};
   for (int c = 0; c < P.nc && c < 4; ++c) cols[c] = {P.col[c].v, P.col[c].center};

@@ -695,7 +695,7 @@ bool build_multi_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, Gr
 namespace {
 bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
               const std::vector<XExpr>& exprs, const std::vector<int>& fns, GroupAggOut& out,
-              const GroupKey* preK = nullptr);
+              const GroupKey* preK = nullptr, const std::vector<XPred>* preds = nullptr);
 }  // namespace
 
 // Returns false when the inputs are not in the fused shape (caller then runs
@@ -1241,7 +1241,63 @@ __global__ void k_xg_lengths(const int64_t* __restrict__ s, const int64_t* __res
 
 }  // namespace dev
 
+namespace dev {
+__global__ void k_xg_fill1(int64_t* __restrict__ out, int64_t v) { *out = v; }
+
+// WHERE pushdown: one conjunct per entry, `col op k` or `col IN (list)`,
+// evaluated once per segment on the segment's value of the predicate column
+// (compare_scalar semantics, align.cpp:551-567: f64 if either side is float)
+constexpr int XG_PREDS = 8, XG_IN = 16;
+struct XgPred {
+  int src;  // index of the predicate column's per-segment value array
+  int flt;  // column values are f64
+  int op;   // RQ_LT..RQ_GT, or -1 for IN
+  int n_in;
+  int kflt[XG_IN];
+  int64_t ki[XG_IN];
+  double kf[XG_IN];
+};
+struct XgPreds {
+  int n;
+  const uint64_t* val[XG_PREDS];
+  XgPred p[XG_PREDS];
+};
+__device__ __forceinline__ bool xg_cmp1(uint64_t v, int vf, int64_t ki, double kf, int kflt, int op) {
+  if (vf || kflt) {
+    const double x = vf ? __longlong_as_double(static_cast<long long>(v)) : static_cast<double>(static_cast<int64_t>(v));
+    const double k = kflt ? kf : static_cast<double>(ki);
+    return cmp_t<double>(x, k, op);
+  }
+  return cmp_t<int64_t>(static_cast<int64_t>(v), ki, op);
+}
+__global__ void k_xg_where(const __grid_constant__ XgPreds W, int64_t n, uint8_t* __restrict__ flags) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    bool pass = true;
+    for (int i = 0; i < W.n && pass; ++i) {
+      const XgPred& P = W.p[i];
+      const uint64_t v = __ldg(reinterpret_cast<const unsigned long long*>(W.val[P.src]) + k);
+      if (P.op >= 0) {
+        pass = xg_cmp1(v, P.flt, P.ki[0], P.kf[0], P.kflt[0], P.op);
+      } else {
+        bool any = false;
+        for (int j = 0; j < P.n_in && !any; ++j) any = xg_cmp1(v, P.flt, P.ki[j], P.kf[j], P.kflt[j], RQ_EQ);
+        pass = any;
+      }
+    }
+    flags[k] = pass ? 1 : 0;
+  }
+}
+}  // namespace dev
+
 namespace {
+
+DArr xg_fill(const CtxPtr& ctx, int64_t v) {  // one-element device array
+  DArr a = alloc_arr(ctx, RQ_I64, 1);
+  dev::k_xg_fill1<<<1, 1, 0, ctx->stream>>>(a.as<int64_t>(), v);
+  launched(ctx);
+  return a;
+}
 
 // 16-B aligned base and room for the 8-row vector groups past the last row
 // (the generated kernel reads 8 rows per lane, the interpreted one 4)
@@ -1258,13 +1314,20 @@ DArr xg_const_bits(const CtxPtr& ctx, const DArr& v) {
 
 bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
               const std::vector<XExpr>& exprs, const std::vector<int>& fns, GroupAggOut& out,
-              const GroupKey* preK) {
+              const GroupKey* preK, const std::vector<XPred>* preds) {
   if (exprs.size() > static_cast<size_t>(dev::XG_EXPRS) || keys.size() > 8) return false;
   const int64_t total = !keys.empty() ? keys[0]->total
                         : mask        ? mask->total
                                       : (exprs.empty() || exprs[0].terms.empty() ? -1 : exprs[0].terms[0].col->total);
   if (total < 0) return false;
-  if (mask && (mask->enc != RQ_MASK_RLE || mask->total != total)) return false;
+  if (mask && (mask->total != total || mask->enc == RQ_MASK_COMPOSITE)) return false;
+  const size_t npred = preds ? preds->size() : 0;
+  if (npred > static_cast<size_t>(dev::XG_PREDS)) return false;
+  for (size_t i = 0; i < npred; ++i) {
+    const XPred& q = (*preds)[i];
+    if (q.col->enc != RQ_ENC_RLE || q.col->total != total || q.in.size() > static_cast<size_t>(dev::XG_IN)) return false;
+    if (q.in.empty() && (q.op < RQ_LT || q.op > RQ_GT)) return false;
+  }
   for (int f : fns)
     if (f != RQ_SUM && f != RQ_AVG && f != RQ_COUNT) return false;
   for (auto* k : keys)
@@ -1342,21 +1405,71 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   } else if (!keys.empty()) {
     if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
   } else {
-    const int64_t zs = 0, ze = total - 1, zslot = 0;
     if (total == 0) return false;
-    K.s = upload_arr(ctx, RQ_I64, &zs, 1);
-    K.e = upload_arr(ctx, RQ_I64, &ze, 1);
-    K.slot = upload_arr(ctx, RQ_I64, &zslot, 1);
+    K.s = xg_fill(ctx, 0);  // one run [0, total) in slot 0 (device fills: no host staging)
+    K.e = xg_fill(ctx, total - 1);
+    K.slot = xg_fill(ctx, 0);
     K.G = 1;
   }
   KTimer timer(ctx, "group_exprs");
   DArr s = K.s, e = K.e, slot = K.slot;
   std::vector<DArr> cst;
   if (mask) {
-    Intersection r = range_intersect(ctx, s, e, mask->s, mask->e, true, false);
+    // the mask's true rows as runs: RLE as is, a plain byte mask through
+    // plain_mask_to_rle (primitives.cpp:349-360), index points as 1-row runs
+    DArr ms = mask->s, me = mask->e;
+    if (mask->enc == RQ_MASK_PLAIN) plain_mask_to_rle(ctx, mask->bits, ms, me);
+    else if (mask->enc == RQ_MASK_INDEX) ms = me = mask->p;
+    Intersection r = range_intersect(ctx, s, e, ms, me, true, false);
     slot = gather(ctx, slot, r.idx1);
     s = r.s;
     e = r.e;
+  }
+  if (npred) {  // WHERE pushdown: segment ∩ each predicate column's runs, then keep the passing segments
+    std::vector<const DCol*> pcols;
+    std::vector<DArr> pv;
+    dev::XgPreds W{};
+    W.n = static_cast<int>(npred);
+    for (size_t i = 0; i < npred; ++i) {
+      const XPred& q = (*preds)[i];
+      int src = -1;
+      for (size_t j = 0; j < pcols.size(); ++j)
+        if (pcols[j] == q.col || (pcols[j]->v.raw() == q.col->v.raw() && pcols[j]->e.raw() == q.col->e.raw()))
+          src = static_cast<int>(j);
+      if (src < 0) {
+        Intersection r = range_intersect(ctx, s, e, q.col->s, q.col->e, true, true);
+        slot = gather(ctx, slot, r.idx1);
+        for (auto& v : pv) v = gather(ctx, v, r.idx1);
+        pv.push_back(xg_const_bits(ctx, gather(ctx, q.col->v, r.idx2)));
+        pcols.push_back(q.col);
+        s = r.s;
+        e = r.e;
+        src = static_cast<int>(pv.size()) - 1;
+      }
+      dev::XgPred& P = W.p[i];
+      P.src = src;
+      P.flt = dt_float(q.col->v.dt) ? 1 : 0;
+      P.op = q.in.empty() ? q.op : -1;
+      const std::vector<Scalar> one{q.k};
+      const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
+      P.n_in = static_cast<int>(ks.size());
+      for (size_t j = 0; j < ks.size(); ++j) {
+        P.kflt[j] = ks[j].is_float ? 1 : 0;
+        P.ki[j] = ks[j].i;
+        P.kf[j] = ks[j].f;
+      }
+    }
+    for (size_t j = 0; j < pv.size(); ++j) W.val[j] = reinterpret_cast<const uint64_t*>(pv[j].raw());
+    if (s.n) {
+      DArr flags = alloc_arr(ctx, RQ_I8, s.n);
+      dev::k_xg_where<<<grid_cap(ctx, s.n), 256, 0, ctx->stream>>>(W, s.n, flags.as<uint8_t>());
+      launched(ctx);
+      DArr keep;
+      select_points(ctx, flags, iota(ctx, s.n), keep, nullptr);
+      s = gather(ctx, s, keep);
+      e = gather(ctx, e, keep);
+      slot = gather(ctx, slot, keep);
+    }
   }
   for (const DCol* rc : rle_cols) {
     Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
@@ -1429,7 +1542,11 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
         slot.pos(), P.ne, pe.first, X.acc_f, tabp);
     launched(ctx);
   }
-  {
+  bool int_div = false;  // only integer division can raise (align.cpp:297-299)
+  for (int i = 0; i < P.ne; ++i)
+    for (int t = 0; t < P.e[i].nt; ++t)
+      int_div = int_div || P.e[i].t[t].sop == RQ_DIV || (t > 0 && P.e[i].op[t - 1] == RQ_DIV);
+  if (int_div) {
     const int64_t* h = ctx->readback(err, 8);
     const bool div0 = (h[0] & 0xffffffff) != 0;
     if (div0) {
@@ -1440,8 +1557,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   // ---- outputs: present slots ascending (= ascending keys) ----
   DArr present;
   if (keys.empty()) {
-    const int64_t z = 0;
-    present = upload_arr(ctx, RQ_I64, &z, 1);
+    present = xg_fill(ctx, 0);
   } else {
     DArr flags = alloc_arr(ctx, RQ_I8, G);
     dev::k_gk_flags<<<grid_cap(ctx, G), 256, 0, ctx->stream>>>(reinterpret_cast<const unsigned long long*>(cnt.raw()),
@@ -1531,7 +1647,8 @@ GroupAggOut xg_chain(const CtxPtr& ctx, const DMask* mask, const std::vector<con
 }  // namespace
 
 GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
-                                  const std::vector<XExpr>& exprs, const std::vector<int>& fns, bool* fused) {
+                                  const std::vector<XExpr>& exprs, const std::vector<int>& fns, bool* fused,
+                                  const std::vector<XPred>* preds) {
   require(exprs.size() == fns.size(), "group_aggregate_exprs: one function per expression");
   for (auto& x : exprs) {
     require(x.terms.size() <= 3 && x.ops.size() + 1 == std::max<size_t>(1, x.terms.size()),
@@ -1539,10 +1656,35 @@ GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const st
     for (auto& t : x.terms) require(t.col != nullptr, "group_aggregate_exprs: null operand");
   }
   GroupAggOut out;
-  const bool ok = xg_fused(ctx, mask, keys, exprs, fns, out);
-  if (fused) *fused = ok;
-  if (ok) return out;
-  return xg_chain(ctx, mask, keys, exprs, fns);
+  const bool has_preds = preds && !preds->empty();
+  bool ok = xg_fused(ctx, mask, keys, exprs, fns, out, nullptr, has_preds ? preds : nullptr);
+  if (ok) {
+    if (fused) *fused = true;
+    return out;
+  }
+  // the WHERE list as the runner builds it: compare_scalar per conjunct
+  // (IN = OR of equalities), and_mask across conjuncts and with `mask`
+  std::unique_ptr<DMask> built;
+  if (has_preds) {
+    for (const XPred& q : *preds) {
+      DMask m;
+      if (q.in.empty()) {
+        m = compare_scalar(ctx, *q.col, q.k, q.op, false);
+      } else {
+        m = compare_scalar(ctx, *q.col, q.in[0], RQ_EQ, false);
+        for (size_t j = 1; j < q.in.size(); ++j) m = mask_or(ctx, m, compare_scalar(ctx, *q.col, q.in[j], RQ_EQ, false));
+      }
+      built.reset(new DMask(built ? mask_and(ctx, *built, m) : m));
+    }
+    if (mask) built.reset(new DMask(mask_and(ctx, *built, *mask)));
+    ok = xg_fused(ctx, built.get(), keys, exprs, fns, out);
+    if (ok) {
+      if (fused) *fused = true;
+      return out;
+    }
+  }
+  if (fused) *fused = false;
+  return xg_chain(ctx, built ? built.get() : mask, keys, exprs, fns);
 }
 
 }  // namespace rqb

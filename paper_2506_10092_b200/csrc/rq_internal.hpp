@@ -445,9 +445,17 @@ struct XgSegs;
 bool xg_jit_available();
 bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S, int64_t chunk,
                    unsigned long long* tab, int64_t G, int* err, unsigned blocks);
+// WHERE conjunct for the pushdown form: `col op k`, or `col IN (in)` when
+// `in` is non-empty (the runner's OR of equalities)
+struct XPred {
+  const DCol* col = nullptr;
+  int op = RQ_EQ;
+  Scalar k;
+  std::vector<Scalar> in;
+};
 GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
                                   const std::vector<XExpr>& exprs, const std::vector<int>& fns,
-                                  bool* fused = nullptr);
+                                  bool* fused = nullptr, const std::vector<XPred>* preds = nullptr);
 bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
                            const std::vector<const DCol*>& data, const std::vector<int>& fns,
                            GroupAggOut& out);

@@ -243,6 +243,12 @@ class Term(C.Structure):
     _fields_ = [("col", C.c_void_p), ("op", C.c_int32), ("reversed", C.c_int32), ("k", Scalar)]
 
 
+class Pred(C.Structure):
+    """rq_pred: `col op k`, or `col IN (in_list)` when n_in > 0."""
+    _fields_ = [("col", C.c_void_p), ("op", C.c_int32), ("n_in", C.c_int32), ("k", Scalar),
+                ("in_list", C.POINTER(Scalar))]
+
+
 class Expr(C.Structure):
     """rq_expr: left-deep chain ((t0 ops[0] t1) ops[1] t2); n_terms 0 = COUNT(*)."""
     _fields_ = [("n_terms", C.c_int32), ("ops", C.c_int32 * 2), ("terms", Term * 3)]

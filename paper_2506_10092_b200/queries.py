@@ -239,22 +239,29 @@ def q6_mask(api, t):
                    C.compare_scalar(t["l_quantity"], 24, "<")))
 
 
+Q6_WHERE = [("l_shipdate", ">=", Q6_LO), ("l_shipdate", "<", Q6_HI), ("l_discount", ">=", 5),
+            ("l_discount", "<=", 7), ("l_quantity", "<", 24)]
+
+
 def q6_fused(rq, t):
+    """WHERE pushed into the fused call (conjuncts on RLE columns are
+    evaluated per run segment; no mask is materialised)."""
     X = rq.X
     _, vs, _, fused = rq.agg.group_aggregate_exprs(
-        q6_mask(rq, t), [], [X.col(t["l_extendedprice"]).arith(X.col(t["l_discount"]), "*")], ["sum"])
+        None, [], [X.col(t["l_extendedprice"]).arith(X.col(t["l_discount"]), "*")], ["sum"],
+        where=[(t[c], op, k) for c, op, k in Q6_WHERE])
     v = vs[0]
     return (float(v.download()[0]) if hasattr(v, "download") else float(v[0])), fused
 
 
 def q1_fused(rq, t):
     X = rq.X
-    m = rq.compute.compare_scalar(t["l_shipdate"], Q1_CUTOFF, "<=")
     price, disc, tax, qty = (t[k] for k in ("l_extendedprice", "l_discount", "l_tax", "l_quantity"))
     disc_price = X.col(price).arith(X.col(disc).scalar(100, "-", True), "*")
     charge = disc_price.arith(X.col(tax).scalar(100, "+"), "*")
     exprs = [X.col(qty), X.col(price), disc_price, charge, X.col(qty), X.col(price), X.col(disc), X.count()]
-    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(m, [t["l_returnflag"], t["l_linestatus"]], exprs, Q1_FNS)
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [t["l_returnflag"], t["l_linestatus"]], exprs, Q1_FNS,
+                                                     where=[(t["l_shipdate"], "<=", Q1_CUTOFF)])
     return (ks, vs, ng), fused
 
 
@@ -269,6 +276,7 @@ def c5_mask(api, t):
 
 def c5_fused(rq, t):
     X = rq.X
-    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(c5_mask(rq, t), [t["r4"]],
-                                                     [X.col(t["pi0"]), X.col(t["p1"]), X.count()], C5_FNS)
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [t["r4"]],
+                                                     [X.col(t["pi0"]), X.col(t["p1"]), X.count()], C5_FNS,
+                                                     where=[(t["r2"], "in", C5_IN), (t["r3"], "<", C5_LT)])
     return (ks, vs, ng), fused

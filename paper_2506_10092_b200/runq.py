@@ -603,13 +603,14 @@ class agg:
         return ks, vs, int(ng.value)
 
     @staticmethod
-    def group_aggregate_exprs(mask, keys: Sequence, exprs: Sequence, fns: Sequence):
+    def group_aggregate_exprs(mask, keys: Sequence, exprs: Sequence, fns: Sequence, where: Sequence = ()):
         """The runner's Filter → expressions → GroupAgg (runner.cpp:243-336)
-        in one call: operands filtered by `mask` (None: no WHERE), each X
+        in one call: operands filtered by `mask` (None: no WHERE) and by the
+        conjuncts `where` — (col, op, k) or (col, "in", [k...]) — each X
         expression evaluated, group_aggregate(normalize) over `keys` (empty:
         one global group). Returns (keys list, values list, n_groups, fused)."""
         fns = [H.AGG_NAMES.get(f, f) for f in fns]
-        cols = [t[0] for x in exprs for t in x.terms]
+        cols = [t[0] for x in exprs for t in x.terms] + [w[0] for w in where]
         host = _is_host(*keys, *cols, *([mask] if mask is not None else []))
         ctx = _ctx_of(*keys, *cols, *([mask] if mask is not None else []))
         dm = upload(mask, ctx) if mask is not None else None
@@ -638,8 +639,21 @@ class agg:
         ok = (C.c_void_p * max(1, len(dk)))()
         ov = (C.c_void_p * len(exprs))()
         ng, fused = C.c_int64(), C.c_int32()
-        check(_L.rq_group_aggregate_exprs(ctx.handle, dm.handle if dm is not None else None, karr, len(dk), arr,
-                                          farr, len(exprs), C.byref(ng), ok, ov, C.byref(fused)))
+        warr = (H.Pred * max(1, len(where)))()
+        for i, w in enumerate(where):
+            col, op, k = w
+            warr[i].col = up(col).handle.value
+            if isinstance(op, str) and op.lower() == "in":
+                lst = (H.Scalar * len(k))(*[H.make_scalar(x) for x in k])
+                keep.append(lst)
+                warr[i].op, warr[i].n_in, warr[i].in_list = 0, len(k), lst
+                warr[i].k = H.make_scalar(0)
+            else:
+                warr[i].op, warr[i].n_in = H.BINOP_NAMES.get(op, op), 0
+                warr[i].k = H.make_scalar(k)
+        keep.extend(uploaded.values())
+        check(_L.rq_group_aggregate_where(ctx.handle, warr, len(where), dm.handle if dm is not None else None, karr,
+                                          len(dk), arr, farr, len(exprs), C.byref(ng), ok, ov, C.byref(fused)))
         ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
         vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(exprs))]
         return ks, vs, int(ng.value), bool(fused.value)

@@ -151,3 +151,78 @@ def test_unfusable_shapes_fall_back_to_chain(rq, ref):
         assert_array(g, w)
     _, vs, _, fused = rq.agg.group_aggregate_exprs(None, [k], [X.col(idx)], ["sum"])
     assert not fused
+
+
+def _ref_where_mask(ref, where):
+    m = None
+    for col, op, k in where:
+        if op == "in":
+            c = None
+            for x in k:
+                e = ref.compare_scalar(col, x, "==")
+                c = e if c is None else ref.or_mask(c, e)
+        else:
+            c = ref.compare_scalar(col, k, op)
+        m = c if m is None else ref.and_mask(m, c)
+    return m
+
+
+@pytest.mark.parametrize("inst", range(6))
+def test_where_pushdown_vs_reference(rq, ref, inst, row_kernel):
+    """WHERE conjuncts evaluated per run segment (no mask) == the runner's
+    compare_scalar / or_mask / and_mask mask followed by the chain."""
+    rng = np.random.default_rng(900 + inst)
+    X = rq.X
+    n = int(rng.integers(5_000, 500_000))
+    k1 = _rle(rng, n, int(rng.integers(100, 20_000)), 0, 5)
+    p1 = _rle(rng, n, 80, 0, 30, gaps=bool(inst % 2))
+    p2 = _rle(rng, n, 900, -5, 5)
+    pf = H.PlainColumn(rng.uniform(0, 10, n))
+    p8 = H.PlainColumn(rng.integers(-100, 101, n).astype(np.int8), H.I64, 3)
+    where = [(p1, "in", [1, 7, 12, 29]), (p2, ">=", -2), (p2, "<", 4.5)]
+    if inst >= 3:
+        where = where[1:] + [(p1, "!=", 3)]
+    exprs = [X.col(pf).arith(X.col(p8), "*"), X.col(p8), X.count(), X.col(p2).scalar(2, "*")]
+    fns = ["sum", "avg", "count", "sum"]
+    keys = [k1] if inst % 3 else []
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, keys, exprs, fns, where=where)
+    assert fused
+    hm = _ref_where_mask(ref, where)
+    if keys:
+        wk, wv, wng = _chain(ref, hm, keys, exprs, fns)
+        assert ng == wng
+        for g, w in zip(ks + vs, wk + wv):
+            assert_array(g, w)
+    else:
+        for i, (x, fn) in enumerate(zip(exprs, fns)):
+            if not x.terms:
+                want = ref.aggregate_all(ref.filter(p2, hm), "count")
+            else:
+                def term(tm):
+                    c, op, rev, kk = tm
+                    return ref.arith_scalar(ref.filter(c, hm), kk, op, rev) if op != -1 else ref.filter(c, hm)
+                v = term(x.terms[0])
+                for tm, op in zip(x.terms[1:], x.ops):
+                    v = ref.arith(v, term(tm), op)
+                want = ref.aggregate_all(v, fn)
+            got = vs[i][0]
+            assert_scalar(float(got) if isinstance(want, float) else int(got), want, f"expr {i}")
+
+
+def test_where_on_plain_column_falls_back_to_mask(rq, ref):
+    """A conjunct on a plain column cannot be evaluated per run segment: the
+    call builds the runner's mask and still fuses the aggregation."""
+    rng = np.random.default_rng(77)
+    X = rq.X
+    n = 200_000
+    k = _rle(rng, n, 500, 0, 4)
+    p = H.PlainColumn(rng.integers(0, 100, n).astype(np.int16), H.I64, None)
+    r = _rle(rng, n, 60, 0, 9)
+    where = [(p, "<", 40), (r, ">", 2)]
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [k], [X.col(p), X.count()], ["sum", "count"],
+                                                     where=where)
+    assert fused
+    wk, wv, wng = _chain(ref, _ref_where_mask(ref, where), [k], [X.col(p), X.count()], ["sum", "count"])
+    assert ng == wng
+    for g, w in zip(ks + vs, wk + wv):
+        assert_array(g, w)
