@@ -411,6 +411,30 @@ __global__ void __launch_bounds__(BLOCK, 8)
       const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
       const int64_t a0 = t * ta;
       const int na_t = static_cast<int>(min(static_cast<int64_t>(ta), na - a0));
+      if (t - t_begin >= 2) mbar_wait(&empty[st], (use - 1) & 1);
+      int64_t* wAe = sAe(st);
+      T* wAv = sAv(st);
+      int64_t* wBe = sBe(st);
+      T* wBv = sBv(st);
+      // (1) the driver part does not depend on the window chain: issue it
+      // first, as soon as the stage is free (ends from a0 - 2: two previous
+      // ends, -1 before the column; values from a0). Its bytes are expected
+      // on the stage barrier without arriving; the lanes arrive in (2).
+      const bool first = a0 == 0;
+      const int ae_n = na_t + (first ? 0 : 2);
+      const int ae_bulk = ae_n & ~1, av_bulk = na_t & ~1;
+      int64_t* ae_dst = first ? wAe + 2 : wAe;
+      const int64_t* ae_src = first ? Ae : Ae + (a0 - 2);
+      if (first && lane < 2) wAe[lane] = -1;
+      if (lane == 0 && ae_bulk < ae_n) ae_dst[ae_bulk] = ldg64(ae_src, ae_bulk);
+      if (lane == 1 && av_bulk < na_t) wAv[av_bulk] = Av[a0 + av_bulk];
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&full[st], static_cast<uint32_t>(ae_bulk + av_bulk) * 8u);
+        if (ae_bulk) bulk_g2s(ae_dst, ae_src, ae_bulk * 8u, &full[st]);
+        if (av_bulk) bulk_g2s(wAv, Av + a0, av_bulk * 8u, &full[st]);
+      }
+      // (2) the other list's window: chained from tile t-1's landed window
       if (t == t_begin) {
         const int64_t r_lo = a0 > 0 ? ldg64(Ae, a0 - 1) : -1;
         jb = warp_lower_bound(Be, nb, r_lo + 1);
@@ -426,27 +450,14 @@ __global__ void __launch_bounds__(BLOCK, 8)
         b_est = static_cast<int>(min(static_cast<int64_t>(BW), used + (used >> 2) + 32));
         jb = jn;
       }
-      if (t - t_begin >= 2) mbar_wait(&empty[st], (use - 1) & 1);
-      // other-list window [b_lo, b_lo + b_n): even start, < BW - 8 entries, clipped at nb
+      // window [b_lo, b_lo + b_n): even start, < BW - 8 entries, clipped at nb
       b_lo = jb & ~int64_t(1);
       int64_t n = static_cast<int64_t>(b_est) + (jb - b_lo);
       if (n > BW - 16) n = BW - 16;
       n = (n + 1) & ~int64_t(1);  // whole 16-byte chunks: the tail path runs only at the column end
       if (n > nb - b_lo) n = nb - b_lo;
       b_n = n > 0 ? static_cast<int>(n) : 0;
-      int64_t* wAe = sAe(st);
-      T* wAv = sAv(st);
-      int64_t* wBe = sBe(st);
-      T* wBv = sBv(st);
-      // driver: ends from a0 - 2 (two previous ends; -1 before the column) and values from a0
-      const bool first = a0 == 0;
-      const int ae_n = na_t + (first ? 0 : 2);
-      const int ae_bulk = ae_n & ~1, av_bulk = na_t & ~1, b_bulk = b_n & ~1;
-      int64_t* ae_dst = first ? wAe + 2 : wAe;
-      const int64_t* ae_src = first ? Ae : Ae + (a0 - 2);
-      if (first && lane < 2) wAe[lane] = -1;
-      if (lane == 0 && ae_bulk < ae_n) ae_dst[ae_bulk] = ldg64(ae_src, ae_bulk);
-      if (lane == 1 && av_bulk < na_t) wAv[av_bulk] = Av[a0 + av_bulk];
+      const int b_bulk = b_n & ~1;
       if (lane == 2 && b_bulk < b_n) {
         wBe[b_bulk] = ldg64(Be, b_lo + b_bulk);
         wBv[b_bulk] = Bv[b_lo + b_bulk];
@@ -461,11 +472,8 @@ __global__ void __launch_bounds__(BLOCK, 8)
         s_lo[st] = b_lo;
         s_nb[st] = b_n;
         s_jf[st] = static_cast<int>(jb - b_lo);
-        const uint32_t bytes = static_cast<uint32_t>(ae_bulk + av_bulk + 2 * b_bulk) * 8u;
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&full[st], bytes);
-        if (ae_bulk) bulk_g2s(ae_dst, ae_src, ae_bulk * 8u, &full[st]);
-        if (av_bulk) bulk_g2s(wAv, Av + a0, av_bulk * 8u, &full[st]);
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(2 * b_bulk) * 8u);
         if (b_bulk) {
           bulk_g2s(wBe, Be + b_lo, b_bulk * 8u, &full[st]);
           bulk_g2s(wBv, Bv + b_lo, b_bulk * 8u, &full[st]);
