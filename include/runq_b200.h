@@ -314,6 +314,16 @@ int rq_mask_or(rq_ctx_t ctx, rq_mask_t a, rq_mask_t b, rq_mask_t* out);
 int rq_mask_not(rq_ctx_t ctx, rq_mask_t a, rq_mask_t* out);
 
 /* ---------------------------------------------------------------------- */
+/* joins: runq::joins (join.hpp:58-59)                                      */
+/* ---------------------------------------------------------------------- */
+
+/* joins::semi_join_mask (join.cpp:368-406): probe-side mask of the entries
+ * (runs / points / rows) whose key occurs on the build side; keys compared
+ * as f64 (−0 == +0) if either side is float, else int64. RLE probe → RLE
+ * mask of the hit runs; Plain probe → Plain mask; otherwise Index mask. */
+int rq_semi_join_mask(rq_ctx_t ctx, rq_col_t probe, rq_col_t build, rq_mask_t* out);
+
+/* ---------------------------------------------------------------------- */
 /* aggregation: runq::agg (groupby.hpp:22-50)                               */
 /* ---------------------------------------------------------------------- */
 

@@ -15,6 +15,7 @@
 #include "runq/align.hpp"
 #include "runq/column.hpp"
 #include "runq/groupby.hpp"
+#include "runq/join.hpp"
 #include "runq/ingest.hpp"
 #include "runq/table.hpp"
 #include "runq/kernels.hpp"
@@ -444,6 +445,9 @@ int ref_or_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out)
 }
 int ref_not_mask(const rq_host_mask* a, rq_host_mask* out) {
   return guarded([&] { from_mask(masks::not_mask(to_mask(a)), out); });
+}
+int ref_semi_join_mask(const rq_host_column* probe, const rq_host_column* build, rq_host_mask* out) {
+  return guarded([&] { from_mask(joins::semi_join_mask(to_column(probe), to_column(build)), out); });
 }
 int ref_mask_true_count(const rq_host_mask* a, int64_t* out) {
   return guarded([&] { *out = to_mask(a).true_count(); });

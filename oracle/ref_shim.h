@@ -71,6 +71,7 @@ int ref_arith_scalar(const rq_host_column* a, rq_scalar k, int32_t op, int32_t r
 int ref_compare_scalar(const rq_host_column* a, rq_scalar k, int32_t op, int32_t reversed,
                        rq_host_mask* out);
 int ref_filter(const rq_host_column* a, const rq_host_mask* m, rq_host_column* out);
+int ref_semi_join_mask(const rq_host_column* probe, const rq_host_column* build, rq_host_mask* out);
 int ref_and_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out);
 int ref_or_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out);
 int ref_not_mask(const rq_host_mask* a, rq_host_mask* out);

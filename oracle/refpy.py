@@ -257,6 +257,14 @@ class Ref:
         self._check(self.lib.ref_filter(C.byref(ia), C.byref(im), C.byref(out)))
         return self._col(out)
 
+    def semi_join_mask(self, probe, build):
+        """joins::semi_join_mask (join.cpp:368-406)."""
+        ip, kp = H.column_image(probe)
+        ib, kb = H.column_image(build)
+        out = H.HostMask()
+        self._check(self.lib.ref_semi_join_mask(C.byref(ip), C.byref(ib), C.byref(out)))
+        return self._mask(out)
+
     def and_mask(self, a, b):
         ia, ka = H.mask_image(a)
         ib, kb = H.mask_image(b)

@@ -89,6 +89,7 @@ PROTOTYPES = {
                                            P(i32)]),
     "rq_group_aggregate_where": (C.c_int, [vp, P(Pred), i32, vp, P(vp), i32, P(Expr), P(i32), i32, P(i64), P(vp),
                                            P(vp), P(i32)]),
+    "rq_semi_join_mask": (C.c_int, [vp, vp, vp, P(vp)]),
     "rq_shard_host_column": (C.c_int, [P(HostColumn), i64, i64, P(HostColumn)]),
     "rq_host_column_free": (None, [P(HostColumn)]),
 }

@@ -284,6 +284,14 @@ int rq_filter(rq_ctx_t c, rq_col_t a, rq_mask_t m, rq_col_t* out) {
   });
 }
 
+int rq_semi_join_mask(rq_ctx_t c, rq_col_t probe, rq_col_t build, rq_mask_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require(out != nullptr, "null out");
+    *out = wrap_mask(semi_join_mask(ctx, col_of(probe), col_of(build)));
+  });
+}
+
 int rq_mask_and(rq_ctx_t c, rq_mask_t a, rq_mask_t b, rq_mask_t* out) {
   return api_guard([&] {
     auto ctx = ctx_of(c);

@@ -408,6 +408,8 @@ DMask mask_and(const CtxPtr& ctx, const DMask& a, const DMask& b);
 DMask mask_or(const CtxPtr& ctx, const DMask& a, const DMask& b);
 DMask mask_not(const CtxPtr& ctx, const DMask& a);
 DCol normalize_basic(const CtxPtr& ctx, const DCol& c);
+// joins::semi_join_mask (join.cpp:368-406), k_join.cu
+DMask semi_join_mask(const CtxPtr& ctx, const DCol& probe, const DCol& build);
 int64_t mask_true_count(const CtxPtr& ctx, const DMask& m);
 bool col_gapless(const CtxPtr& ctx, const DCol& c);
 

@@ -563,6 +563,18 @@ class X:
         return X(self.terms + other.terms, self.ops + [H.BINOP_NAMES.get(op, op)])
 
 
+class joins:
+    @staticmethod
+    def semi_join_mask(probe, build):
+        """joins::semi_join_mask (join.cpp:368-406): probe rows whose key occurs in build."""
+        host = _is_host(probe, build)
+        ctx = _ctx_of(probe, build)
+        dp, db = upload(probe, ctx), upload(build, ctx)
+        o = _new()
+        check(_L.rq_semi_join_mask(ctx.handle, dp.handle, db.handle, C.byref(o)))
+        return _out(DeviceMask(o, ctx), host)
+
+
 def _agg_result(dt, i, f):
     return float(f.value) if dt.value == H.F64 else int(i.value)
 
