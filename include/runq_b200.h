@@ -323,6 +323,28 @@ int rq_mask_not(rq_ctx_t ctx, rq_mask_t a, rq_mask_t* out);
  * mask of the hit runs; Plain probe → Plain mask; otherwise Index mask. */
 int rq_semi_join_mask(rq_ctx_t ctx, rq_col_t probe, rq_col_t build, rq_mask_t* out);
 
+/* joins::JoinIndex (join.hpp:7-31): `rows` (UnsortedIndexJoin) when is_rle
+ * = 0, else the reference ranges (v = source run, s, e) of UnsortedRleJoin. */
+typedef struct rq_join_side {
+  int32_t is_rle;
+  int32_t _pad;
+  rq_arr_t rows;
+  rq_arr_t v, s, e;
+} rq_join_side;
+
+/* joins::get_join_index (join.cpp:183-238): equi-join index of two columns in
+ * the reference's pairing order (probe-major, matches in build-entry order;
+ * the side with fewer entries builds, ties: the left side probes). Runs join
+ * as single entries; each side's index is RLE-shaped iff its column is RLE.
+ * Output arrays are new handles owned by the caller. */
+int rq_get_join_index(rq_ctx_t ctx, rq_col_t left, rq_col_t right, rq_join_side* left_out,
+                      rq_join_side* right_out, int64_t* cardinality);
+
+/* joins::apply_join_index (join.cpp:245-366): the column's values in the
+ * join index's row order (Plain for row references; RLE / Index ranges keep
+ * their encoding). References outside the covered rows raise RQ_INVALID. */
+int rq_apply_join_index(rq_ctx_t ctx, rq_col_t col, const rq_join_side* j, rq_col_t* out);
+
 /* ---------------------------------------------------------------------- */
 /* aggregation: runq::agg (groupby.hpp:22-50)                               */
 /* ---------------------------------------------------------------------- */

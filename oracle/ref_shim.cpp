@@ -446,6 +446,45 @@ int ref_or_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out)
 int ref_not_mask(const rq_host_mask* a, rq_host_mask* out) {
   return guarded([&] { from_mask(masks::not_mask(to_mask(a)), out); });
 }
+namespace {
+void side_out(const joins::JoinIndex& j, ref_join_side* o) {
+  o->is_rle = j.is_rle() ? 1 : 0;
+  auto dupv = [](const PosVec& v) {
+    return static_cast<int64_t*>(dup_bytes(v.data(), v.size() * sizeof(int64_t)));
+  };
+  if (j.is_rle()) {
+    o->n = static_cast<int64_t>(j.rle().s.size());
+    o->rows = nullptr;
+    o->v = dupv(j.rle().v);
+    o->s = dupv(j.rle().s);
+    o->e = dupv(j.rle().e);
+  } else {
+    o->n = static_cast<int64_t>(j.index().rows.size());
+    o->rows = dupv(j.index().rows);
+    o->v = o->s = o->e = nullptr;
+  }
+}
+joins::JoinIndex side_in(const ref_join_side* j) {
+  auto vec = [&](const int64_t* p) { return PosVec(p, p + j->n); };
+  if (j->is_rle) return joins::JoinIndex(joins::UnsortedRleJoin{vec(j->v), vec(j->s), vec(j->e)});
+  return joins::JoinIndex(joins::UnsortedIndexJoin{vec(j->rows)});
+}
+}  // namespace
+
+int ref_get_join_index(const rq_host_column* left, const rq_host_column* right, ref_join_side* lo,
+                       ref_join_side* ro, int64_t* cardinality) {
+  return guarded([&] {
+    joins::JoinResult r = joins::get_join_index(to_column(left), to_column(right));
+    side_out(r.left, lo);
+    side_out(r.right, ro);
+    *cardinality = r.cardinality;
+  });
+}
+int ref_apply_join_index(const rq_host_column* col, const ref_join_side* j, rq_host_column* out) {
+  return guarded([&] { from_column(joins::apply_join_index(to_column(col), side_in(j)), out); });
+}
+void ref_free(void* p) { std::free(p); }
+
 int ref_semi_join_mask(const rq_host_column* probe, const rq_host_column* build, rq_host_mask* out) {
   return guarded([&] { from_mask(joins::semi_join_mask(to_column(probe), to_column(build)), out); });
 }

@@ -71,6 +71,16 @@ int ref_arith_scalar(const rq_host_column* a, rq_scalar k, int32_t op, int32_t r
 int ref_compare_scalar(const rq_host_column* a, rq_scalar k, int32_t op, int32_t reversed,
                        rq_host_mask* out);
 int ref_filter(const rq_host_column* a, const rq_host_mask* m, rq_host_column* out);
+typedef struct ref_join_side {
+  int32_t is_rle;
+  int64_t n;
+  int64_t* rows;
+  int64_t *v, *s, *e;
+} ref_join_side;
+int ref_get_join_index(const rq_host_column* left, const rq_host_column* right, ref_join_side* lo,
+                       ref_join_side* ro, int64_t* cardinality);
+int ref_apply_join_index(const rq_host_column* col, const ref_join_side* j, rq_host_column* out);
+void ref_free(void* p);
 int ref_semi_join_mask(const rq_host_column* probe, const rq_host_column* build, rq_host_mask* out);
 int ref_and_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out);
 int ref_or_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out);

@@ -52,6 +52,11 @@ def _take(ptr, n, dt):
     return np.frombuffer(bytes(buf), dtype=dt).copy()
 
 
+class RefJoinSide(C.Structure):
+    _fields_ = [("is_rle", C.c_int32), ("n", C.c_int64), ("rows", C.POINTER(C.c_int64)), ("v", C.POINTER(C.c_int64)),
+                ("s", C.POINTER(C.c_int64)), ("e", C.POINTER(C.c_int64))]
+
+
 class Ref:
     """The reference operator API (runq::compute / enc / masks / agg)."""
 
@@ -255,6 +260,40 @@ class Ref:
         im, km = H.mask_image(m)
         out = H.HostColumn()
         self._check(self.lib.ref_filter(C.byref(ia), C.byref(im), C.byref(out)))
+        return self._col(out)
+
+    def get_join_index(self, left, right):
+        """joins::get_join_index (join.cpp:183-238) -> (left side, right side, cardinality);
+        a side is ("rows", rows) or ("rle", v, s, e)."""
+        il, kl = H.column_image(left)
+        ir, kr = H.column_image(right)
+        lo, ro, card = RefJoinSide(), RefJoinSide(), C.c_int64()
+        self._check(self.lib.ref_get_join_index(C.byref(il), C.byref(ir), C.byref(lo), C.byref(ro), C.byref(card)))
+        return self._side(lo), self._side(ro), int(card.value)
+
+    def _side(self, s):
+        def take(p):
+            a = np.ctypeslib.as_array(p, shape=(s.n,)).copy() if s.n else np.zeros(0, np.int64)
+            self.lib.ref_free(C.cast(p, C.c_void_p))
+            return a
+        if s.is_rle:
+            return ("rle", take(s.v), take(s.s), take(s.e))
+        return ("rows", take(s.rows))
+
+    def apply_join_index(self, col, side):
+        """joins::apply_join_index (join.cpp:363-366)."""
+        ic, kc = H.column_image(col)
+        keep = [np.ascontiguousarray(x, dtype=np.int64) for x in side[1:]]
+        j = RefJoinSide()
+        j.is_rle = 1 if side[0] == "rle" else 0
+        j.n = len(keep[0])
+        P = C.POINTER(C.c_int64)
+        if j.is_rle:
+            j.v, j.s, j.e = (k.ctypes.data_as(P) for k in keep)
+        else:
+            j.rows = keep[0].ctypes.data_as(P)
+        out = H.HostColumn()
+        self._check(self.lib.ref_apply_join_index(C.byref(ic), C.byref(j), C.byref(out)))
         return self._col(out)
 
     def semi_join_mask(self, probe, build):

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .host import EncodingChoice, Expr, Heuristic, HostColumn, HostMask, Pred, Scalar
+from .host import EncodingChoice, Expr, Heuristic, HostColumn, HostMask, JoinSide, Pred, Scalar
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librunq_b200.so")
 
@@ -90,6 +90,8 @@ PROTOTYPES = {
     "rq_group_aggregate_where": (C.c_int, [vp, P(Pred), i32, vp, P(vp), i32, P(Expr), P(i32), i32, P(i64), P(vp),
                                            P(vp), P(i32)]),
     "rq_semi_join_mask": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_get_join_index": (C.c_int, [vp, vp, vp, P(JoinSide), P(JoinSide), P(i64)]),
+    "rq_apply_join_index": (C.c_int, [vp, vp, P(JoinSide), P(vp)]),
     "rq_shard_host_column": (C.c_int, [P(HostColumn), i64, i64, P(HostColumn)]),
     "rq_host_column_free": (None, [P(HostColumn)]),
 }

@@ -292,6 +292,49 @@ int rq_semi_join_mask(rq_ctx_t c, rq_col_t probe, rq_col_t build, rq_mask_t* out
   });
 }
 
+namespace {
+void side_to_abi(const JoinSideD& j, rq_join_side* o) {
+  o->is_rle = j.is_rle ? 1 : 0;
+  o->_pad = 0;
+  o->rows = j.is_rle ? nullptr : wrap_arr(j.rows);
+  o->v = j.is_rle ? wrap_arr(j.v) : nullptr;
+  o->s = j.is_rle ? wrap_arr(j.s) : nullptr;
+  o->e = j.is_rle ? wrap_arr(j.e) : nullptr;
+}
+}  // namespace
+
+int rq_get_join_index(rq_ctx_t c, rq_col_t left, rq_col_t right, rq_join_side* left_out, rq_join_side* right_out,
+                      int64_t* cardinality) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require(left_out && right_out, "null out");
+    JoinResultD r = get_join_index(ctx, col_of(left), col_of(right));
+    side_to_abi(r.left, left_out);
+    side_to_abi(r.right, right_out);
+    if (cardinality) *cardinality = r.cardinality;
+  });
+}
+
+int rq_apply_join_index(rq_ctx_t c, rq_col_t col, const rq_join_side* j, rq_col_t* out) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require(j != nullptr && out != nullptr, "null argument");
+    JoinSideD s;
+    s.is_rle = j->is_rle != 0;
+    if (s.is_rle) {
+      require(j->v && j->s && j->e, "apply_join_index: ranges required");
+      s.v = arr_of(j->v);
+      s.s = arr_of(j->s);
+      s.e = arr_of(j->e);
+      require(s.s.n == s.e.n && s.v.n == s.s.n, "apply_join_index: range arrays differ in length");
+    } else {
+      require(j->rows != nullptr, "apply_join_index: rows required");
+      s.rows = arr_of(j->rows);
+    }
+    *out = wrap_col(apply_join_index(ctx, col_of(col), s));
+  });
+}
+
 int rq_mask_and(rq_ctx_t c, rq_mask_t a, rq_mask_t b, rq_mask_t* out) {
   return api_guard([&] {
     auto ctx = ctx_of(c);

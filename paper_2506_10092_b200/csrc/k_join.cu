@@ -17,6 +17,8 @@
 // sequence; the hit flags are compacted by the existing ordered selects
 // (select_runs / select_points), so entry order — and so the mask — is the
 // reference's. Work is O(build + probe) entries: runs are never expanded.
+#include <algorithm>
+
 #include "device_common.cuh"
 #include "rq_internal.hpp"
 
@@ -69,6 +71,218 @@ __global__ void k_hash_probe(const uint64_t* __restrict__ keys, int64_t n, const
       h = (h + 1) & mask;
     }
     hit[i] = found;
+  }
+}
+
+// ---- get_join_index (join.cpp:183-238) ----
+// build keys sorted (stable radix on the 64-bit key pattern) so the matches
+// of a probe entry are one equal range, in build-entry order — the order of
+// the reference's insertion-ordered hash chains.
+__device__ __forceinline__ int64_t u64_lower(const uint64_t* a, int64_t n, uint64_t k) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(reinterpret_cast<const unsigned long long*>(a) + mid) < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t u64_upper(const uint64_t* a, int64_t n, uint64_t k) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(reinterpret_cast<const unsigned long long*>(a) + mid) <= k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_join_ranges(const uint64_t* __restrict__ pk, int64_t np, const uint64_t* __restrict__ bsorted,
+                              int64_t nb, int64_t* __restrict__ lo, int64_t* __restrict__ cnt) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < np;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = pk[i];
+    const int64_t l = u64_lower(bsorted, nb, k);
+    lo[i] = l;
+    cnt[i] = u64_upper(bsorted, nb, k) - l;
+  }
+}
+
+struct JSide {  // one side's entries
+  int is_rle;
+  const int64_t* s;
+  const int64_t* e;
+  const int64_t* rows;  // null: plain rows (entry index = row)
+};
+__device__ __forceinline__ int64_t jlen(const JSide& x, int64_t i) {
+  return x.is_rle ? ldg64(x.e, i) - ldg64(x.s, i) + 1 : 1;
+}
+__device__ __forceinline__ int64_t jrow(const JSide& x, int64_t i) { return x.rows ? ldg64(x.rows, i) : i; }
+
+// per probe entry: its matches (p, b) in order, with each side's entry counts
+__global__ void k_join_matches(const int64_t* __restrict__ lo, const int64_t* __restrict__ moff, int64_t np,
+                               const int64_t* __restrict__ bidx, JSide P, JSide B, int64_t* __restrict__ mp,
+                               int64_t* __restrict__ mb, int64_t* __restrict__ cp, int64_t* __restrict__ cb,
+                               unsigned long long* __restrict__ card) {
+  unsigned long long c = 0;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < np;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t o = moff[p], m = moff[p + 1] - o, l = lo[p];
+    const int64_t lp = jlen(P, p);
+    for (int64_t k = 0; k < m; ++k) {
+      const int64_t b = ldg64(bidx, l + k);
+      const int64_t lb = jlen(B, b);
+      mp[o + k] = p;
+      mb[o + k] = b;
+      c += static_cast<unsigned long long>(lp * lb);
+      if (!P.is_rle && !B.is_rle) {
+        cp[o + k] = 1;
+        cb[o + k] = 1;
+      } else if (!P.is_rle) {  // one probe row repeated by the run length, one build range
+        cp[o + k] = lb;
+        cb[o + k] = 1;
+      } else if (!B.is_rle) {  // one probe range, the build row repeated
+        cp[o + k] = 1;
+        cb[o + k] = lp;
+      } else {  // build rows outer: lb probe ranges, lb·lp single-row build ranges
+        cp[o + k] = lb;
+        cb[o + k] = lb * lp;
+      }
+    }
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(card, c);
+}
+
+// writes one side's join index entries for every match
+__global__ void k_join_emit(const int64_t* __restrict__ mp, const int64_t* __restrict__ mb, int64_t nm,
+                            const int64_t* __restrict__ off, JSide P, JSide B, int probe_side,
+                            int64_t* __restrict__ rows, int64_t* __restrict__ v, int64_t* __restrict__ s,
+                            int64_t* __restrict__ e) {
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < nm;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t p = mp[j], b = mb[j];
+    const int64_t at = off[j];
+    const int64_t lp = jlen(P, p), lb = jlen(B, b);
+    if (probe_side) {
+      if (!P.is_rle) {
+        const int64_t r = jrow(P, p), n = B.is_rle ? lb : 1;
+        for (int64_t k = 0; k < n; ++k) rows[at + k] = r;
+      } else {
+        const int64_t n = B.is_rle ? lb : 1, ps = ldg64(P.s, p), pe = ldg64(P.e, p);
+        for (int64_t k = 0; k < n; ++k) {
+          v[at + k] = p;
+          s[at + k] = ps;
+          e[at + k] = pe;
+        }
+      }
+    } else {
+      if (!B.is_rle) {
+        const int64_t r = jrow(B, b), n = P.is_rle ? lp : 1;
+        for (int64_t k = 0; k < n; ++k) rows[at + k] = r;
+      } else if (!P.is_rle) {
+        v[at] = b;
+        s[at] = ldg64(B.s, b);
+        e[at] = ldg64(B.e, b);
+      } else {
+        const int64_t bs = ldg64(B.s, b);
+        for (int64_t k = 0; k < lb * lp; ++k) {
+          const int64_t row = bs + k / lp;
+          v[at + k] = b;
+          s[at + k] = row;
+          e[at + k] = row;
+        }
+      }
+    }
+  }
+}
+
+// ---- apply_join_index (join.cpp:245-362) ----
+__global__ void k_xg_lengths_join(const int64_t* __restrict__ s, const int64_t* __restrict__ e, int64_t n,
+                                  int64_t* __restrict__ len) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    len[i] = ldg64(e, i) - ldg64(s, i) + 1;
+}
+// index join into an RLE column: the run holding each referenced row
+__global__ void k_join_run_of(const int64_t* __restrict__ rows, const int64_t* __restrict__ bin, int64_t n,
+                              const int64_t* __restrict__ e, const int64_t* __restrict__ p, int64_t* __restrict__ at,
+                              int* __restrict__ err) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = bin[i] - 1, r = rows[i];
+    const bool ok = b >= 0 && (e ? r <= ldg64(e, b) : ldg64(p, b) == r);
+    if (!ok) atomicOr(err, 1);
+    at[i] = ok ? b : 0;
+  }
+}
+
+// RLE join into an RLE column: fragment counts per reference range, with
+// the coverage checks of apply_rle_join (start inside a run, no gap inside)
+__global__ void k_join_frag_count(const int64_t* __restrict__ qs, const int64_t* __restrict__ qe, int64_t nq,
+                                  const int64_t* __restrict__ cs, const int64_t* __restrict__ ce, int64_t nr,
+                                  const int64_t* __restrict__ gaps, int64_t* __restrict__ r0, int64_t* __restrict__ cnt,
+                                  int* __restrict__ err) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nq;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = qs[k], e = qe[k];
+    const int64_t a = upper_bound_g(cs, nr, s) - 1;  // run with start <= s
+    const int64_t b = upper_bound_g(cs, nr, e) - 1;
+    bool ok = a >= 0 && s <= ldg64(ce, a) && ldg64(ce, b) >= e && ldg64(gaps, b) == ldg64(gaps, a);
+    if (!ok) atomicOr(err, 1);
+    r0[k] = ok ? a : 0;
+    cnt[k] = ok ? b - a + 1 : 0;
+  }
+}
+__global__ void k_join_frag_emit(const int64_t* __restrict__ qs, const int64_t* __restrict__ qe, int64_t nq,
+                                 const int64_t* __restrict__ at_rows, const int64_t* __restrict__ r0,
+                                 const int64_t* __restrict__ foff, const int64_t* __restrict__ cs,
+                                 const int64_t* __restrict__ ce, int64_t* __restrict__ os, int64_t* __restrict__ oe,
+                                 int64_t* __restrict__ src) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nq;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = qs[k], e = qe[k], o = foff[k], n = foff[k + 1] - o;
+    int64_t at = at_rows[k], pos = s;
+    for (int64_t f = 0; f < n; ++f) {
+      const int64_t r = r0[k] + f;
+      const int64_t fe = min(e, ldg64(ce, r));
+      os[o + f] = at;
+      oe[o + f] = at + (fe - pos);
+      src[o + f] = r;
+      at += fe - pos + 1;
+      pos = fe + 1;
+    }
+    (void)cs;
+  }
+}
+// gap flags of a run list: gaps[r] = number of runs r' <= r starting after e[r'-1] + 1
+__global__ void k_gap_flags(const int64_t* __restrict__ s, const int64_t* __restrict__ e, int64_t n,
+                            int64_t* __restrict__ flag) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    flag[i] = (i > 0 && ldg64(s, i) > ldg64(e, i - 1) + 1) ? 1 : 0;
+}
+// RLE join into an Index column: points inside each reference range
+__global__ void k_join_pts_count(const int64_t* __restrict__ qs, const int64_t* __restrict__ qe, int64_t nq,
+                                 const int64_t* __restrict__ p, int64_t np, int64_t* __restrict__ lo,
+                                 int64_t* __restrict__ cnt) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nq;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = lower_bound_g(p, np, qs[k]);
+    lo[k] = a;
+    cnt[k] = upper_bound_g(p, np, qe[k]) - a;
+  }
+}
+__global__ void k_join_pts_emit(const int64_t* __restrict__ qs, int64_t nq, const int64_t* __restrict__ at_rows,
+                                const int64_t* __restrict__ lo, const int64_t* __restrict__ poff,
+                                const int64_t* __restrict__ p, int64_t* __restrict__ op, int64_t* __restrict__ take) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nq;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t o = poff[k], n = poff[k + 1] - o, a = lo[k], s = qs[k], at = at_rows[k];
+    for (int64_t f = 0; f < n; ++f) {
+      op[o + f] = at + (ldg64(p, a + f) - s);
+      take[o + f] = a + f;
+    }
   }
 }
 
@@ -183,6 +397,217 @@ DMask semi_join_mask(const CtxPtr& ctx, const DCol& probe, const DCol& build) {
   m.total = total;
   m.p = p;
   return m;
+}
+
+
+// joins::get_join_index (join.cpp:183-238)
+JoinResultD get_join_index(const CtxPtr& ctx, const DCol& left, const DCol& right) {
+  Entries le = entries_of(ctx, left);
+  Entries re = entries_of(ctx, right);
+  const bool build_right = re.values.n <= le.values.n;  // ties: the left side probes
+  Entries& be = build_right ? re : le;
+  Entries& pe = build_right ? le : re;
+  const bool as_float = dt_float(le.values.dt) || dt_float(re.values.dt);
+  KTimer timer(ctx, "join_index");
+  DArr pk = join_keys(ctx, pe.values, as_float);
+  DArr bk = join_keys(ctx, be.values, as_float);
+  DArr bidx = iota(ctx, bk.n);
+  if (bk.n > 1) radix_sort_pairs(ctx, bk, bidx, 64, 0);  // stable: equal keys keep build order
+  const int64_t np = pk.n;
+  DArr lo = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, np));
+  DArr cnt = alloc_arr(ctx, RQ_I64, np + 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(cnt.raw_mut(), 0, (np + 1) * 8, ctx->stream));
+  if (np) {
+    dev::k_join_ranges<<<grid_of(ctx, np), 256, 0, ctx->stream>>>(pk.as<uint64_t>(), np, bk.as<uint64_t>(), bk.n,
+                                                                   lo.as<int64_t>(), cnt.as<int64_t>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  DArr moff;
+  scan_exclusive_i64(ctx, cnt, moff);  // np + 1 entries: moff[np] = matches
+  const int64_t nm = np ? ctx->readback(moff.as<int64_t>() + np, 8)[0] : 0;
+  dev::JSide P{pe.is_rle ? 1 : 0, pe.s.pos(), pe.e.pos(), pe.plain_rows ? nullptr : pe.rows.pos()};
+  dev::JSide B{be.is_rle ? 1 : 0, be.s.pos(), be.e.pos(), be.plain_rows ? nullptr : be.rows.pos()};
+  DArr mp = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nm)), mb = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nm));
+  DArr cp = alloc_arr(ctx, RQ_I64, nm + 1), cb = alloc_arr(ctx, RQ_I64, nm + 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(cp.raw_mut(), 0, (nm + 1) * 8, ctx->stream));
+  RQ_CUDA_CHECK(cudaMemsetAsync(cb.raw_mut(), 0, (nm + 1) * 8, ctx->stream));
+  DArr card = alloc_arr(ctx, RQ_I64, 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(card.raw_mut(), 0, 8, ctx->stream));
+  if (np) {
+    dev::k_join_matches<<<grid_of(ctx, np), 256, 0, ctx->stream>>>(
+        lo.pos(), moff.pos(), np, bidx.pos(), P, B, mp.as<int64_t>(), mb.as<int64_t>(), cp.as<int64_t>(),
+        cb.as<int64_t>(), card.as<unsigned long long>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  JoinResultD out;
+  out.cardinality = ctx->readback(card.raw(), 8)[0];
+  auto emit = [&](int probe_side, const DArr& c, bool is_rle) {
+    DArr off;
+    scan_exclusive_i64(ctx, c, off);
+    const int64_t n = ctx->readback(off.as<int64_t>() + nm, 8)[0];
+    JoinSideD js;
+    js.is_rle = is_rle;
+    if (is_rle) {
+      js.v = alloc_arr(ctx, RQ_I64, n);
+      js.s = alloc_arr(ctx, RQ_I64, n);
+      js.e = alloc_arr(ctx, RQ_I64, n);
+    } else {
+      js.rows = alloc_arr(ctx, RQ_I64, n);
+    }
+    if (nm) {
+      dev::k_join_emit<<<grid_of(ctx, nm), 256, 0, ctx->stream>>>(
+          mp.pos(), mb.pos(), nm, off.pos(), P, B, probe_side, is_rle ? nullptr : js.rows.as<int64_t>(),
+          is_rle ? js.v.as<int64_t>() : nullptr, is_rle ? js.s.as<int64_t>() : nullptr,
+          is_rle ? js.e.as<int64_t>() : nullptr);
+      ctx->count_launch();
+      RQ_CUDA_CHECK(cudaGetLastError());
+    }
+    return js;
+  };
+  JoinSideD po = emit(1, cp, pe.is_rle);
+  JoinSideD bo = emit(0, cb, be.is_rle);
+  out.left = build_right ? po : bo;
+  out.right = build_right ? bo : po;
+  return out;
+}
+
+
+namespace {
+
+DCol plain_of(DArr values) {
+  DCol c;
+  c.enc = RQ_ENC_PLAIN;
+  c.total = values.n;
+  c.logical = values.dt;
+  c.v = std::move(values);
+  return c;
+}
+
+int64_t readback_i64(const CtxPtr& ctx, const DArr& a, int64_t i) { return ctx->readback(a.as<int64_t>() + i, 8)[0]; }
+
+void check_err(const CtxPtr& ctx, const DArr& err, const char* msg) {
+  if (ctx->readback(err.raw(), 8)[0] & 0xffffffff) fail(msg);
+}
+
+DArr decoded(const CtxPtr& ctx, const DCol& c) {  // decode_full of a plain-shaped column
+  return c.enc == RQ_ENC_PLAIN ? decode_plain(ctx, c) : decode_plain_index(ctx, c);
+}
+
+DArr starts_of(const CtxPtr& ctx, const DCol& c) {
+  return c.s.n || c.e.n == 0 ? c.s : starts_from_ends(ctx, c.e);
+}
+
+}  // namespace
+
+// joins::apply_join_index (join.cpp:245-366)
+DCol apply_join_index(const CtxPtr& ctx, const DCol& col, const JoinSideD& j) {
+  if (col.enc == RQ_ENC_RLE_INDEX) return apply_join_index(ctx, normalize_basic(ctx, col), j);
+  KTimer timer(ctx, "apply_join");
+  DArr err = alloc_arr(ctx, RQ_I64, 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(err.raw_mut(), 0, 8, ctx->stream));
+  if (!j.is_rle) {  // apply_index_join (join.cpp:247-282): a plain column of the referenced rows
+    const DArr& rows = j.rows;
+    if (col.enc == RQ_ENC_PLAIN || col.enc == RQ_ENC_PLAIN_INDEX) return plain_of(gather(ctx, decoded(ctx, col), rows));
+    const bool rle = col.enc == RQ_ENC_RLE;
+    DArr keys = rle ? starts_of(ctx, col) : col.p;
+    DArr bin = bucketize(ctx, rows, keys, true);
+    DArr at = alloc_arr(ctx, RQ_I64, rows.n);
+    if (rows.n) {
+      dev::k_join_run_of<<<grid_of(ctx, rows.n), 256, 0, ctx->stream>>>(
+          rows.pos(), bin.pos(), rows.n, rle ? col.e.pos() : nullptr, rle ? nullptr : col.p.pos(), at.as<int64_t>(),
+          reinterpret_cast<int*>(err.raw_mut()));
+      ctx->count_launch();
+      RQ_CUDA_CHECK(cudaGetLastError());
+      check_err(ctx, err, "apply_join_index: reference outside covered rows");
+    }
+    return plain_of(gather(ctx, col.v, at));
+  }
+  // apply_rle_join (join.cpp:284-362)
+  const int64_t nq = j.s.n;
+  DArr lens_off;  // exclusive offsets of the reference ranges in output row space
+  int64_t out_rows = 0;
+  DArr len = alloc_arr(ctx, RQ_I64, nq + 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(len.raw_mut(), 0, (nq + 1) * 8, ctx->stream));
+  if (nq) {
+    dev::k_xg_lengths_join<<<grid_of(ctx, nq), 256, 0, ctx->stream>>>(j.s.pos(), j.e.pos(), nq, len.as<int64_t>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  scan_exclusive_i64(ctx, len, lens_off);
+  out_rows = nq ? readback_i64(ctx, lens_off, nq) : 0;
+  if (col.enc == RQ_ENC_PLAIN || col.enc == RQ_ENC_PLAIN_INDEX) {
+    DArr flat;
+    expand_runs(ctx, j.s, j.e, &flat, nullptr);
+    return plain_of(gather(ctx, decoded(ctx, col), flat));
+  }
+  if (col.enc == RQ_ENC_RLE) {
+    DArr cs = starts_of(ctx, col);
+    const int64_t nr = col.e.n;
+    DArr gflag = alloc_arr(ctx, RQ_I64, nr + 1), gaps;
+    RQ_CUDA_CHECK(cudaMemsetAsync(gflag.raw_mut(), 0, (nr + 1) * 8, ctx->stream));
+    if (nr) {
+      dev::k_gap_flags<<<grid_of(ctx, nr), 256, 0, ctx->stream>>>(cs.pos(), col.e.pos(), nr, gflag.as<int64_t>());
+      ctx->count_launch();
+    }
+    scan_exclusive_i64(ctx, gflag, gaps);
+    // gaps[r + 1] - gaps[a + 1] counts the gaps between runs a and r: shift by one
+    DArr r0 = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nq)), cnt = alloc_arr(ctx, RQ_I64, nq + 1);
+    RQ_CUDA_CHECK(cudaMemsetAsync(cnt.raw_mut(), 0, (nq + 1) * 8, ctx->stream));
+    if (nq) {
+      dev::k_join_frag_count<<<grid_of(ctx, nq), 256, 0, ctx->stream>>>(
+          j.s.pos(), j.e.pos(), nq, cs.pos(), col.e.pos(), nr, gaps.pos() + 1, r0.as<int64_t>(), cnt.as<int64_t>(),
+          reinterpret_cast<int*>(err.raw_mut()));
+      ctx->count_launch();
+      RQ_CUDA_CHECK(cudaGetLastError());
+      check_err(ctx, err, "apply_join_index: range outside covered rows or across a coverage gap");
+    }
+    DArr foff;
+    scan_exclusive_i64(ctx, cnt, foff);
+    const int64_t nf = nq ? readback_i64(ctx, foff, nq) : 0;
+    DArr os = alloc_arr(ctx, RQ_I64, nf), oe = alloc_arr(ctx, RQ_I64, nf), src = alloc_arr(ctx, RQ_I64, nf);
+    if (nf) {
+      dev::k_join_frag_emit<<<grid_of(ctx, nq), 256, 0, ctx->stream>>>(
+          j.s.pos(), j.e.pos(), nq, lens_off.pos(), r0.pos(), foff.pos(), cs.pos(), col.e.pos(), os.as<int64_t>(),
+          oe.as<int64_t>(), src.as<int64_t>());
+      ctx->count_launch();
+      RQ_CUDA_CHECK(cudaGetLastError());
+    }
+    DCol out;
+    out.enc = RQ_ENC_RLE;
+    out.total = out_rows;
+    out.v = gather(ctx, col.v, src);
+    out.s = os;
+    out.e = oe;
+    return out;
+  }
+  // Index column: points inside each range, at their offset in output row space
+  DArr lo = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nq)), cnt = alloc_arr(ctx, RQ_I64, nq + 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(cnt.raw_mut(), 0, (nq + 1) * 8, ctx->stream));
+  if (nq) {
+    dev::k_join_pts_count<<<grid_of(ctx, nq), 256, 0, ctx->stream>>>(j.s.pos(), j.e.pos(), nq, col.p.pos(), col.p.n,
+                                                                      lo.as<int64_t>(), cnt.as<int64_t>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  DArr poff;
+  scan_exclusive_i64(ctx, cnt, poff);
+  const int64_t npts = nq ? readback_i64(ctx, poff, nq) : 0;
+  DArr op = alloc_arr(ctx, RQ_I64, npts), take = alloc_arr(ctx, RQ_I64, npts);
+  if (npts) {
+    dev::k_join_pts_emit<<<grid_of(ctx, nq), 256, 0, ctx->stream>>>(j.s.pos(), nq, lens_off.pos(), lo.pos(),
+                                                                     poff.pos(), col.p.pos(), op.as<int64_t>(),
+                                                                     take.as<int64_t>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  DCol out;
+  out.enc = RQ_ENC_INDEX;
+  out.total = out_rows;
+  out.v = gather(ctx, col.v, take);
+  out.p = op;
+  return out;
 }
 
 }  // namespace rqb

@@ -408,8 +408,19 @@ DMask mask_and(const CtxPtr& ctx, const DMask& a, const DMask& b);
 DMask mask_or(const CtxPtr& ctx, const DMask& a, const DMask& b);
 DMask mask_not(const CtxPtr& ctx, const DMask& a);
 DCol normalize_basic(const CtxPtr& ctx, const DCol& c);
-// joins::semi_join_mask (join.cpp:368-406), k_join.cu
+// joins (join.hpp:7-59), k_join.cu
 DMask semi_join_mask(const CtxPtr& ctx, const DCol& probe, const DCol& build);
+struct JoinSideD {  // joins::JoinIndex: rows (UnsortedIndexJoin) or (v, s, e) ranges (UnsortedRleJoin)
+  bool is_rle = false;
+  DArr rows;
+  DArr v, s, e;
+};
+struct JoinResultD {
+  JoinSideD left, right;
+  int64_t cardinality = 0;
+};
+JoinResultD get_join_index(const CtxPtr& ctx, const DCol& left, const DCol& right);
+DCol apply_join_index(const CtxPtr& ctx, const DCol& col, const JoinSideD& j);
 int64_t mask_true_count(const CtxPtr& ctx, const DMask& m);
 bool col_gapless(const CtxPtr& ctx, const DCol& c);
 

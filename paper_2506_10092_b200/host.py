@@ -243,6 +243,12 @@ class Term(C.Structure):
     _fields_ = [("col", C.c_void_p), ("op", C.c_int32), ("reversed", C.c_int32), ("k", Scalar)]
 
 
+class JoinSide(C.Structure):
+    """rq_join_side: `rows` (is_rle = 0) or the ranges (v, s, e)."""
+    _fields_ = [("is_rle", C.c_int32), ("_pad", C.c_int32), ("rows", C.c_void_p), ("v", C.c_void_p),
+                ("s", C.c_void_p), ("e", C.c_void_p)]
+
+
 class Pred(C.Structure):
     """rq_pred: `col op k`, or `col IN (in_list)` when n_in > 0."""
     _fields_ = [("col", C.c_void_p), ("op", C.c_int32), ("n_in", C.c_int32), ("k", Scalar),

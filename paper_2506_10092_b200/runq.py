@@ -565,6 +565,38 @@ class X:
 
 class joins:
     @staticmethod
+    def get_join_index(left, right):
+        """joins::get_join_index (join.cpp:183-238) -> (left side, right side,
+        cardinality); a side is ("rows", rows) or ("rle", v, s, e) (numpy)."""
+        ctx = _ctx_of(left, right)
+        dl, dr = upload(left, ctx), upload(right, ctx)
+        lo, ro, card = H.JoinSide(), H.JoinSide(), C.c_int64()
+        check(_L.rq_get_join_index(ctx.handle, dl.handle, dr.handle, C.byref(lo), C.byref(ro), C.byref(card)))
+
+        def side(j):
+            if j.is_rle:
+                return ("rle",) + tuple(DeviceArray(C.c_void_p(p), ctx).download() for p in (j.v, j.s, j.e))
+            return ("rows", DeviceArray(C.c_void_p(j.rows), ctx).download())
+        return side(lo), side(ro), int(card.value)
+
+    @staticmethod
+    def apply_join_index(col, side):
+        """joins::apply_join_index (join.cpp:363-366) of a side ("rows", rows) / ("rle", v, s, e)."""
+        host = _is_host(col)
+        ctx = _ctx_of(col)
+        dc = upload(col, ctx)
+        arrs = [upload(np.ascontiguousarray(a, dtype=np.int64), ctx) for a in side[1:]]
+        j = H.JoinSide()
+        j.is_rle = 1 if side[0] == "rle" else 0
+        if j.is_rle:
+            j.v, j.s, j.e = (a.handle.value for a in arrs)
+        else:
+            j.rows = arrs[0].handle.value
+        o = _new()
+        check(_L.rq_apply_join_index(ctx.handle, dc.handle, C.byref(j), C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
     def semi_join_mask(probe, build):
         """joins::semi_join_mask (join.cpp:368-406): probe rows whose key occurs in build."""
         host = _is_host(probe, build)

@@ -58,3 +58,56 @@ def test_semi_join_large_rle_probe(rq, ref):
     build = H.PlainColumn(np.random.default_rng(6).integers(0, 1_000_000, 50_000).astype(np.int64))
     got = rq.joins.semi_join_mask(rq.upload(probe), rq.upload(build)).download()
     assert_mask(got, ref.semi_join_mask(probe, build))
+
+
+def _assert_side(got, want, what):
+    assert got[0] == want[0], f"{what}: side shape {got[0]} != {want[0]}"
+    for g, w in zip(got[1:], want[1:]):
+        assert np.array_equal(np.asarray(g, np.int64), np.asarray(w, np.int64)), f"{what}: {g} != {w}"
+
+
+@pytest.mark.parametrize("re_", range(5))
+@pytest.mark.parametrize("le", range(5))
+def test_join_index_all_pairs(rq, ref, le, re_):
+    """get_join_index in the reference's pairing order (acceptance.cpp:300-320
+    combos), then apply_join_index of both sides onto columns of every
+    encoding of those tables."""
+    from helpers import assert_column
+    rng = np.random.default_rng(3000 + 10 * le + re_)
+    for it in range(3):
+        nl, nr = int(rng.integers(1, 400)), int(rng.integers(1, 400))
+        left = G.random_column(rng, ENCS[le], nl, False, True, 6)
+        right = G.random_column(rng, ENCS[re_], nr, False, True, 6)
+        gl, gr, gc = rq.joins.get_join_index(left, right)
+        wl, wr, wc = ref.get_join_index(left, right)
+        assert gc == wc, f"cardinality {gc} != {wc}"
+        _assert_side(gl, wl, f"left iter {it}")
+        _assert_side(gr, wr, f"right iter {it}")
+        # apply each side to the table's columns (full-coverage encodings)
+        for e2 in (H.ENC_PLAIN, H.ENC_RLE, H.ENC_INDEX, H.ENC_PLAIN_INDEX, H.ENC_RLE_INDEX):
+            lc = G.random_column(rng, e2, nl, bool(it % 2), False, 20)
+            rc = G.random_column(rng, e2, nr, bool(it % 2), False, 20)
+            assert_column(rq.joins.apply_join_index(lc, wl), ref.apply_join_index(lc, wl), f"apply left enc {e2}")
+            assert_column(rq.joins.apply_join_index(rc, wr), ref.apply_join_index(rc, wr), f"apply right enc {e2}")
+
+
+def test_join_float_keys_and_many_to_many(rq, ref):
+    left = H.RleColumn(np.array([1.0, -0.0, 2.5, 1.0]), np.array([0, 3, 5, 9], np.int64),
+                       np.array([2, 4, 8, 11], np.int64), 12)
+    right = H.RleColumn(np.array([0, 1, 1], np.int64), np.array([0, 2, 4], np.int64), np.array([1, 3, 6], np.int64), 7)
+    gl, gr, gc = rq.joins.get_join_index(left, right)
+    wl, wr, wc = ref.get_join_index(left, right)
+    assert gc == wc
+    _assert_side(gl, wl, "left")
+    _assert_side(gr, wr, "right")
+
+
+def test_apply_join_index_out_of_coverage_raises(rq):
+    """test_join.cpp:189-193: a row reference outside the covered rows raises."""
+    from paper_2506_10092_b200._lib import RqError
+    gapped = H.RleColumn(np.array([1], np.int64), np.array([2], np.int64), np.array([4], np.int64), 10)
+    with pytest.raises(RqError):
+        rq.joins.apply_join_index(gapped, ("rows", np.array([0], np.int64)))
+    with pytest.raises(RqError):
+        rq.joins.apply_join_index(gapped, ("rle", np.array([0], np.int64), np.array([1], np.int64),
+                                           np.array([3], np.int64)))
