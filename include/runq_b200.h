@@ -323,6 +323,12 @@ int rq_mask_not(rq_ctx_t ctx, rq_mask_t a, rq_mask_t* out);
  * mask of the hit runs; Plain probe → Plain mask; otherwise Index mask. */
 int rq_semi_join_mask(rq_ctx_t ctx, rq_col_t probe, rq_col_t build, rq_mask_t* out);
 
+/* joins::hash_build_probe (join.cpp:167-181): the matching (build, probe)
+ * position pairs of two value arrays, probe-major, each probe's matches in
+ * build-entry order. */
+int rq_hash_build_probe(rq_ctx_t ctx, rq_arr_t build_values, rq_arr_t probe_values, rq_arr_t* build_pos,
+                        rq_arr_t* probe_pos);
+
 /* joins::JoinIndex (join.hpp:7-31): `rows` (UnsortedIndexJoin) when is_rle
  * = 0, else the reference ranges (v = source run, s, e) of UnsortedRleJoin. */
 typedef struct rq_join_side {

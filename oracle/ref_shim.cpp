@@ -484,6 +484,15 @@ int ref_apply_join_index(const rq_host_column* col, const ref_join_side* j, rq_h
   return guarded([&] { from_column(joins::apply_join_index(to_column(col), side_in(j)), out); });
 }
 void ref_free(void* p) { std::free(p); }
+int ref_hash_build_probe(const void* bv, int32_t bdt, int64_t nb, const void* pv, int32_t pdt, int64_t np,
+                         int64_t** bpos, int64_t** ppos, int64_t* n) {
+  return guarded([&] {
+    joins::ProbeHits h = joins::hash_build_probe(make_array(bdt, nb, bv), make_array(pdt, np, pv));
+    *n = static_cast<int64_t>(h.build_pos.size());
+    *bpos = static_cast<int64_t*>(dup_bytes(h.build_pos.data(), h.build_pos.size() * 8));
+    *ppos = static_cast<int64_t*>(dup_bytes(h.probe_pos.data(), h.probe_pos.size() * 8));
+  });
+}
 
 int ref_semi_join_mask(const rq_host_column* probe, const rq_host_column* build, rq_host_mask* out) {
   return guarded([&] { from_mask(joins::semi_join_mask(to_column(probe), to_column(build)), out); });

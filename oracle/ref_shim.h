@@ -81,6 +81,8 @@ int ref_get_join_index(const rq_host_column* left, const rq_host_column* right, 
                        ref_join_side* ro, int64_t* cardinality);
 int ref_apply_join_index(const rq_host_column* col, const ref_join_side* j, rq_host_column* out);
 void ref_free(void* p);
+int ref_hash_build_probe(const void* bv, int32_t bdt, int64_t nb, const void* pv, int32_t pdt, int64_t np,
+                         int64_t** bpos, int64_t** ppos, int64_t* n);
 int ref_semi_join_mask(const rq_host_column* probe, const rq_host_column* build, rq_host_mask* out);
 int ref_and_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out);
 int ref_or_mask(const rq_host_mask* a, const rq_host_mask* b, rq_host_mask* out);

@@ -262,6 +262,21 @@ class Ref:
         self._check(self.lib.ref_filter(C.byref(ia), C.byref(im), C.byref(out)))
         return self._col(out)
 
+    def hash_build_probe(self, build_values, probe_values):
+        """joins::hash_build_probe (join.cpp:167-181) -> (build_pos, probe_pos)."""
+        b = np.ascontiguousarray(build_values)
+        p = np.ascontiguousarray(probe_values)
+        bp, pp, n = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.c_int64()
+        self._check(self.lib.ref_hash_build_probe(
+            b.ctypes.data if b.size else None, H.dtype_code(b), b.shape[0],
+            p.ctypes.data if p.size else None, H.dtype_code(p), p.shape[0], C.byref(bp), C.byref(pp), C.byref(n)))
+        out = []
+        for ptr in (bp, pp):
+            a = np.ctypeslib.as_array(ptr, shape=(n.value,)).copy() if n.value else np.zeros(0, np.int64)
+            self.lib.ref_free(C.cast(ptr, C.c_void_p))
+            out.append(a)
+        return out[0], out[1]
+
     def get_join_index(self, left, right):
         """joins::get_join_index (join.cpp:183-238) -> (left side, right side, cardinality);
         a side is ("rows", rows) or ("rle", v, s, e)."""

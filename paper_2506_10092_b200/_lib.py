@@ -90,6 +90,7 @@ PROTOTYPES = {
     "rq_group_aggregate_where": (C.c_int, [vp, P(Pred), i32, vp, P(vp), i32, P(Expr), P(i32), i32, P(i64), P(vp),
                                            P(vp), P(i32)]),
     "rq_semi_join_mask": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_hash_build_probe": (C.c_int, [vp, vp, vp, P(vp), P(vp)]),
     "rq_get_join_index": (C.c_int, [vp, vp, vp, P(JoinSide), P(JoinSide), P(i64)]),
     "rq_apply_join_index": (C.c_int, [vp, vp, P(JoinSide), P(vp)]),
     "rq_shard_host_column": (C.c_int, [P(HostColumn), i64, i64, P(HostColumn)]),

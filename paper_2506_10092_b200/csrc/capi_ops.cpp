@@ -303,6 +303,18 @@ void side_to_abi(const JoinSideD& j, rq_join_side* o) {
 }
 }  // namespace
 
+int rq_hash_build_probe(rq_ctx_t c, rq_arr_t build_values, rq_arr_t probe_values, rq_arr_t* build_pos,
+                        rq_arr_t* probe_pos) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require(build_pos && probe_pos, "null out");
+    DArr b, p;
+    hash_build_probe(ctx, arr_of(build_values), arr_of(probe_values), b, p);
+    *build_pos = wrap_arr(b);
+    *probe_pos = wrap_arr(p);
+  });
+}
+
 int rq_get_join_index(rq_ctx_t c, rq_col_t left, rq_col_t right, rq_join_side* left_out, rq_join_side* right_out,
                       int64_t* cardinality) {
   return api_guard([&] {

@@ -610,4 +610,41 @@ DCol apply_join_index(const CtxPtr& ctx, const DCol& col, const JoinSideD& j) {
   return out;
 }
 
+
+// joins::hash_build_probe (join.cpp:167-181): matching (build, probe)
+// positions of two value arrays, probe-major, build matches in entry order
+void hash_build_probe(const CtxPtr& ctx, const DArr& build_values, const DArr& probe_values, DArr& build_pos,
+                      DArr& probe_pos) {
+  const bool as_float = dt_float(build_values.dt) || dt_float(probe_values.dt);
+  KTimer timer(ctx, "hash_build_probe");
+  DArr pk = join_keys(ctx, probe_values, as_float);
+  DArr bk = join_keys(ctx, build_values, as_float);
+  DArr bidx = iota(ctx, bk.n);
+  if (bk.n > 1) radix_sort_pairs(ctx, bk, bidx, 64, 0);
+  const int64_t np = pk.n;
+  DArr lo = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, np));
+  DArr cnt = alloc_arr(ctx, RQ_I64, np + 1);
+  RQ_CUDA_CHECK(cudaMemsetAsync(cnt.raw_mut(), 0, (np + 1) * 8, ctx->stream));
+  if (np) {
+    dev::k_join_ranges<<<grid_of(ctx, np), 256, 0, ctx->stream>>>(pk.as<uint64_t>(), np, bk.as<uint64_t>(), bk.n,
+                                                                   lo.as<int64_t>(), cnt.as<int64_t>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+  DArr moff;
+  scan_exclusive_i64(ctx, cnt, moff);
+  const int64_t nm = np ? ctx->readback(moff.as<int64_t>() + np, 8)[0] : 0;
+  build_pos = alloc_arr(ctx, RQ_I64, nm);
+  probe_pos = alloc_arr(ctx, RQ_I64, nm);
+  if (nm) {
+    const dev::JSide plain{0, nullptr, nullptr, nullptr};
+    DArr cp = alloc_arr(ctx, RQ_I64, nm + 1), cb = alloc_arr(ctx, RQ_I64, nm + 1), card = alloc_arr(ctx, RQ_I64, 1);
+    dev::k_join_matches<<<grid_of(ctx, np), 256, 0, ctx->stream>>>(
+        lo.pos(), moff.pos(), np, bidx.pos(), plain, plain, probe_pos.as<int64_t>(), build_pos.as<int64_t>(),
+        cp.as<int64_t>(), cb.as<int64_t>(), card.as<unsigned long long>());
+    ctx->count_launch();
+    RQ_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
 }  // namespace rqb

@@ -420,6 +420,8 @@ struct JoinResultD {
   int64_t cardinality = 0;
 };
 JoinResultD get_join_index(const CtxPtr& ctx, const DCol& left, const DCol& right);
+void hash_build_probe(const CtxPtr& ctx, const DArr& build_values, const DArr& probe_values, DArr& build_pos,
+                      DArr& probe_pos);
 DCol apply_join_index(const CtxPtr& ctx, const DCol& col, const JoinSideD& j);
 int64_t mask_true_count(const CtxPtr& ctx, const DMask& m);
 bool col_gapless(const CtxPtr& ctx, const DCol& c);

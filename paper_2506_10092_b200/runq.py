@@ -565,6 +565,15 @@ class X:
 
 class joins:
     @staticmethod
+    def hash_build_probe(build_values, probe_values):
+        """joins::hash_build_probe (join.cpp:167-181) -> (build_pos, probe_pos) numpy arrays."""
+        ctx = _ctx_of(build_values, probe_values)
+        db, dp = upload(np.asarray(build_values), ctx), upload(np.asarray(probe_values), ctx)
+        ob, op = C.c_void_p(), C.c_void_p()
+        check(_L.rq_hash_build_probe(ctx.handle, db.handle, dp.handle, C.byref(ob), C.byref(op)))
+        return DeviceArray(ob, ctx).download(), DeviceArray(op, ctx).download()
+
+    @staticmethod
     def get_join_index(left, right):
         """joins::get_join_index (join.cpp:183-238) -> (left side, right side,
         cardinality); a side is ("rows", rows) or ("rle", v, s, e) (numpy)."""

@@ -111,3 +111,15 @@ def test_apply_join_index_out_of_coverage_raises(rq):
     with pytest.raises(RqError):
         rq.joins.apply_join_index(gapped, ("rle", np.array([0], np.int64), np.array([1], np.int64),
                                            np.array([3], np.int64)))
+
+
+def test_hash_build_probe_vs_reference(rq, ref):
+    rng = np.random.default_rng(71)
+    for it in range(6):
+        b = rng.integers(0, 40, int(rng.integers(0, 3000)))
+        p = rng.integers(0, 40, int(rng.integers(0, 3000)))
+        if it % 2:
+            b = b.astype(np.float64)
+        gb, gp = rq.joins.hash_build_probe(b, p)
+        wb, wp = ref.hash_build_probe(b, p)
+        assert np.array_equal(gb, wb) and np.array_equal(gp, wp), f"iter {it}"
