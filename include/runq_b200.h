@@ -444,6 +444,32 @@ int rq_group_aggregate_where(rq_ctx_t ctx, const rq_pred* where, int32_t n_where
                              int32_t* fused);
 
 /* ---------------------------------------------------------------------- */
+/* query runner: runq::query (plan.hpp:13-80, runner.hpp:14-95)             */
+/* ---------------------------------------------------------------------- */
+
+typedef struct rq_catalog_s* rq_catalog_t; /* runq::query::Catalog (runner.hpp:14-28) */
+typedef struct rq_result_s* rq_result_t;   /* runq::query::ResultTable (runner.hpp:42-48) */
+
+int rq_catalog_create(rq_catalog_t* out);
+int rq_catalog_destroy(rq_catalog_t cat);
+/* Adds a column (TableColumn, table.hpp:14-19) to `table` (created on first
+ * use). dict: the dictionary's strings in code order (dictionary.hpp:16-43),
+ * or dict_n = 0 for non-string columns; columns naming the same dict_name
+ * share one dictionary (no recoding across them in joins). is_date: the
+ * column holds days since 1970-01-01 and takes 'YYYY-MM-DD' literals. */
+int rq_catalog_add_column(rq_catalog_t cat, const char* table, const char* column, rq_col_t col,
+                          const char* const* dict, int64_t dict_n, const char* dict_name, int32_t is_date);
+/* runq::query::run in Compressed mode (runner.cpp:86-373): parses the JSON
+ * plan (plan.cpp:13-105) and executes it on the device, materialising the
+ * result rows. */
+int rq_run_plan(rq_ctx_t ctx, rq_catalog_t cat, const char* plan_json, rq_result_t* out);
+/* fused_nodes: GroupAgg nodes that ran as one fused call */
+int rq_result_info(rq_result_t r, int32_t* n_cols, int64_t* rows, int32_t* fused_nodes);
+/* name stays valid until rq_result_free; values is a new array handle */
+int rq_result_column(rq_result_t r, int32_t i, const char** name, rq_arr_t* values);
+int rq_result_free(rq_result_t r);
+
+/* ---------------------------------------------------------------------- */
 /* row-range sharding (multi-GPU; no reference counterpart)                 */
 /* ---------------------------------------------------------------------- */
 

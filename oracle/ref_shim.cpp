@@ -6,6 +6,7 @@
 #include "ref_shim.h"
 
 #include <chrono>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -16,6 +17,7 @@
 #include "runq/column.hpp"
 #include "runq/groupby.hpp"
 #include "runq/join.hpp"
+#include "runq/runner.hpp"
 #include "runq/ingest.hpp"
 #include "runq/table.hpp"
 #include "runq/kernels.hpp"
@@ -484,6 +486,75 @@ int ref_apply_join_index(const rq_host_column* col, const ref_join_side* j, rq_h
   return guarded([&] { from_column(joins::apply_join_index(to_column(col), side_in(j)), out); });
 }
 void ref_free(void* p) { std::free(p); }
+
+// ---- query runner (runner.cpp:457-520) over a catalog built from column images ----
+struct RefCatalog {
+  query::Catalog cat;
+  std::map<std::string, DictionaryPtr> dicts;
+};
+struct RefResult {
+  query::ResultTable t;
+};
+int ref_catalog_create(void** out) {
+  return guarded([&] { *out = new RefCatalog{}; });
+}
+void ref_catalog_free(void* c) { delete static_cast<RefCatalog*>(c); }
+int ref_catalog_add_column(void* cp, const char* table, const char* column, const rq_host_column* col,
+                           const char* const* dict, int64_t dict_n, const char* dict_name, int32_t is_date) {
+  return guarded([&] {
+    auto* c = static_cast<RefCatalog*>(cp);
+    Table* t = nullptr;
+    for (auto& x : c->cat.tables)
+      if (x.name == table) t = &x;
+    if (!t) {
+      c->cat.tables.push_back(Table{});
+      t = &c->cat.tables.back();
+      t->name = table;
+    }
+    Column colv = to_column(col);
+    t->rows = colv.total_size();
+    DictionaryPtr dp;
+    if (dict_n > 0 || dict_name) {
+      const std::string key = dict_name ? dict_name : std::string(table) + "." + column;
+      auto it = c->dicts.find(key);
+      if (it != c->dicts.end() && dict_n == 0) {
+        dp = it->second;
+      } else {
+        auto nd = std::make_shared<Dictionary>();
+        for (int64_t i = 0; i < dict_n; ++i) nd->intern(dict[i]);
+        dp = nd;
+        c->dicts[key] = dp;
+      }
+    }
+    t->columns.push_back(TableColumn{column, std::make_shared<const Column>(std::move(colv)), dp, is_date != 0});
+  });
+}
+int ref_run_plan(void* cp, const char* json, void** out) {
+  return guarded([&] {
+    auto* c = static_cast<RefCatalog*>(cp);
+    query::PlanPtr plan = query::parse_plan_json(json);
+    query::RunReport r = query::run(c->cat, *plan, query::RunMode::Compressed);
+    *out = new RefResult{std::move(r.result)};
+  });
+}
+int ref_result_info(void* rp, int32_t* ncols, int64_t* rows) {
+  return guarded([&] {
+    auto* r = static_cast<RefResult*>(rp);
+    *ncols = static_cast<int32_t>(r->t.columns.size());
+    *rows = r->t.rows;
+  });
+}
+int ref_result_column(void* rp, int32_t i, const char** name, int32_t* dtype, const void** data, int64_t* n) {
+  return guarded([&] {
+    auto* r = static_cast<RefResult*>(rp);
+    const Array& a = r->t.columns[static_cast<size_t>(i)];
+    *name = r->t.names[static_cast<size_t>(i)].c_str();
+    *dtype = static_cast<int32_t>(a.dtype());
+    *data = a.data();
+    *n = a.size();
+  });
+}
+void ref_result_free(void* r) { delete static_cast<RefResult*>(r); }
 int ref_hash_build_probe(const void* bv, int32_t bdt, int64_t nb, const void* pv, int32_t pdt, int64_t np,
                          int64_t** bpos, int64_t** ppos, int64_t* n) {
   return guarded([&] {

@@ -81,6 +81,14 @@ int ref_get_join_index(const rq_host_column* left, const rq_host_column* right, 
                        ref_join_side* ro, int64_t* cardinality);
 int ref_apply_join_index(const rq_host_column* col, const ref_join_side* j, rq_host_column* out);
 void ref_free(void* p);
+int ref_catalog_create(void** out);
+void ref_catalog_free(void* c);
+int ref_catalog_add_column(void* c, const char* table, const char* column, const rq_host_column* col,
+                           const char* const* dict, int64_t dict_n, const char* dict_name, int32_t is_date);
+int ref_run_plan(void* c, const char* json, void** out);
+int ref_result_info(void* r, int32_t* ncols, int64_t* rows);
+int ref_result_column(void* r, int32_t i, const char** name, int32_t* dtype, const void** data, int64_t* n);
+void ref_result_free(void* r);
 int ref_hash_build_probe(const void* bv, int32_t bdt, int64_t nb, const void* pv, int32_t pdt, int64_t np,
                          int64_t** bpos, int64_t** ppos, int64_t* n);
 int ref_semi_join_mask(const rq_host_column* probe, const rq_host_column* build, rq_host_mask* out);

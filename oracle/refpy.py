@@ -57,6 +57,49 @@ class RefJoinSide(C.Structure):
                 ("s", C.POINTER(C.c_int64)), ("e", C.POINTER(C.c_int64))]
 
 
+class RefCatalog:
+    """runq::query::Catalog of the reference built from column images, and
+    runq::query::run in Compressed mode over it (runner.cpp:457-520)."""
+
+    def __init__(self, ref):
+        self.ref = ref
+        self.h = C.c_void_p()
+        ref._check(ref.lib.ref_catalog_create(C.byref(self.h)))
+        self._keep = []
+
+    def add_column(self, table, name, col, dict=None, dict_name=None, is_date=False):
+        img, keep = H.column_image(col)
+        self._keep.append((img, keep))
+        strs = [s.encode() for s in (dict or [])]
+        arr = (C.c_char_p * max(1, len(strs)))(*strs)
+        self.ref._check(self.ref.lib.ref_catalog_add_column(
+            self.h, table.encode(), name.encode(), C.byref(img), arr, len(strs),
+            dict_name.encode() if dict_name else None, int(is_date)))
+
+    def run_plan(self, plan_json: str):
+        lib = self.ref.lib
+        r = C.c_void_p()
+        self.ref._check(lib.ref_run_plan(self.h, plan_json.encode(), C.byref(r)))
+        try:
+            nc, rows = C.c_int32(), C.c_int64()
+            self.ref._check(lib.ref_result_info(r, C.byref(nc), C.byref(rows)))
+            out = {}
+            for i in range(nc.value):
+                name, dt, data, n = C.c_char_p(), C.c_int32(), C.c_void_p(), C.c_int64()
+                self.ref._check(lib.ref_result_column(r, i, C.byref(name), C.byref(dt), C.byref(data), C.byref(n)))
+                npdt = H.DTYPES[dt.value]
+                buf = (C.c_char * (n.value * np.dtype(npdt).itemsize)).from_address(data.value) if n.value else b""
+                out[name.value.decode()] = np.frombuffer(bytes(buf), dtype=npdt).copy()
+            return out
+        finally:
+            lib.ref_result_free(r)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_catalog_free(self.h)
+            self.h = None
+
+
 class Ref:
     """The reference operator API (runq::compute / enc / masks / agg)."""
 

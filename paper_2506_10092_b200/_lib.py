@@ -93,6 +93,13 @@ PROTOTYPES = {
     "rq_hash_build_probe": (C.c_int, [vp, vp, vp, P(vp), P(vp)]),
     "rq_get_join_index": (C.c_int, [vp, vp, vp, P(JoinSide), P(JoinSide), P(i64)]),
     "rq_apply_join_index": (C.c_int, [vp, vp, P(JoinSide), P(vp)]),
+    "rq_catalog_create": (C.c_int, [P(vp)]),
+    "rq_catalog_destroy": (C.c_int, [vp]),
+    "rq_catalog_add_column": (C.c_int, [vp, C.c_char_p, C.c_char_p, vp, P(C.c_char_p), i64, C.c_char_p, i32]),
+    "rq_run_plan": (C.c_int, [vp, vp, C.c_char_p, P(vp)]),
+    "rq_result_info": (C.c_int, [vp, P(i32), P(i64), P(i32)]),
+    "rq_result_column": (C.c_int, [vp, i32, P(C.c_char_p), P(vp)]),
+    "rq_result_free": (C.c_int, [vp]),
     "rq_shard_host_column": (C.c_int, [P(HostColumn), i64, i64, P(HostColumn)]),
     "rq_host_column_free": (None, [P(HostColumn)]),
 }

@@ -563,6 +563,46 @@ class X:
         return X(self.terms + other.terms, self.ops + [H.BINOP_NAMES.get(op, op)])
 
 
+class Catalog:
+    """runq::query::Catalog (runner.hpp:14-28) of device-resident columns;
+    run_plan executes a reference JSON plan on the device (runner.cpp:86-373)."""
+
+    def __init__(self, ctx: Context = None):
+        self.ctx = _ctx(ctx)
+        self.h = C.c_void_p()
+        check(_L.rq_catalog_create(C.byref(self.h)))
+        self._cols = []
+
+    def add_column(self, table, name, col, dict=None, dict_name=None, is_date=False):
+        dc = upload(col, self.ctx)
+        self._cols.append(dc)
+        strs = [s.encode() for s in (dict or [])]
+        arr = (C.c_char_p * max(1, len(strs)))(*strs)
+        check(_L.rq_catalog_add_column(self.h, table.encode(), name.encode(), dc.handle, arr, len(strs),
+                                       dict_name.encode() if dict_name else None, int(is_date)))
+
+    def run_plan(self, plan_json: str):
+        """-> (dict column name -> numpy values, rows, fused GroupAgg nodes)."""
+        r = C.c_void_p()
+        check(_L.rq_run_plan(self.ctx.handle, self.h, plan_json.encode(), C.byref(r)))
+        try:
+            nc, rows, fused = C.c_int32(), C.c_int64(), C.c_int32()
+            check(_L.rq_result_info(r, C.byref(nc), C.byref(rows), C.byref(fused)))
+            out = {}
+            for i in range(nc.value):
+                name, arr = C.c_char_p(), C.c_void_p()
+                check(_L.rq_result_column(r, i, C.byref(name), C.byref(arr)))
+                out[name.value.decode()] = DeviceArray(arr, self.ctx).download()
+            return out, int(rows.value), int(fused.value)
+        finally:
+            _L.rq_result_free(r)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _L.rq_catalog_destroy(self.h)
+            self.h = None
+
+
 class joins:
     @staticmethod
     def hash_build_probe(build_values, probe_values):
