@@ -230,7 +230,9 @@ int rq_ctx_create(int device, rq_ctx_t* out) {
     cudaDeviceProp prop;
     RQ_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
     ctx->sm_count = prop.multiProcessorCount;
-    RQ_CUDA_CHECK(cudaMallocHost(&ctx->pinned, 4096));
+    RQ_CUDA_CHECK(cudaHostAlloc(&ctx->pinned, 8192, cudaHostAllocMapped));
+    ctx->result_host = reinterpret_cast<char*>(ctx->pinned) + 4096;
+    RQ_CUDA_CHECK(cudaHostGetDevicePointer(&ctx->result_dev, ctx->result_host, 0));
     RQ_CUDA_CHECK(cudaMalloc(&ctx->tickets, 256));
     RQ_CUDA_CHECK(cudaMemsetAsync(ctx->tickets, 0, 256, ctx->stream));
     // keep freed blocks cached in the stream-ordered pool (no trim between ops)

@@ -983,16 +983,18 @@ bool pair_reduce_tma(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bo
   int64_t grid = 0;
   if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, nullptr, nullptr, ta, ntiles, grid, true);
   else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, nullptr, nullptr, ta, ntiles, grid, true);
-  DArr parts = alloc_arr(ctx, RQ_I64, grid * static_cast<int64_t>(sizeof(dev::AggPart) / 8));
-  DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8);
+  // partials in the context's scratch; the folded result lands in mapped pinned host memory
+  auto* parts = static_cast<dev::AggPart*>(ctx->get_scratch(static_cast<size_t>(grid) * sizeof(dev::AggPart)));
+  auto* out = static_cast<dev::AggPart*>(ctx->result_dev);
   {
     KTimer timer(ctx, "pair_reduce");
-    if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ta, ntiles, grid, false);
-    else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, parts.as<dev::AggPart>(), out.as<dev::AggPart>(), ta, ntiles, grid, false);
+    if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, false);
+    else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, false);
     ctx->count_launch();
     RQ_CUDA_CHECK(cudaGetLastError());
   }
-  const auto* p = reinterpret_cast<const dev::AggPart*>(ctx->readback(out.raw(), sizeof(dev::AggPart)));
+  ctx->sync();
+  const auto* p = static_cast<const dev::AggPart*>(ctx->result_host);
   h.isum = p->isum;
   h.fsum = p->fsum;
   h.cnt = p->cnt;

@@ -25,6 +25,7 @@
 // Integer sums wrap exactly like the chain's int64 arithmetic; f64 within
 // tolerance.
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 #include <type_traits>
 
@@ -977,10 +978,10 @@ AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int 
     const int64_t ntiles = (np + TILE - 1) / TILE;
     TmaLaunch f{&y, xs, cs, ntiles, a.enc == RQ_ENC_RLE ? 0 : 1, nullptr, ctx->tickets, nullptr, nullptr};
     const int64_t grid = flt ? launch_tma1<double>(op, ck, ctx, f, true) : launch_tma1<int64_t>(op, ck, ctx, f, true);
-    DArr parts = alloc_arr(ctx, RQ_I64, grid * static_cast<int64_t>(sizeof(dev::AggPart) / 8));
-    DArr out = alloc_arr(ctx, RQ_I64, sizeof(dev::AggPart) / 8);
-    f.parts = parts.as<dev::AggPart>();
-    f.out = out.as<dev::AggPart>();
+    // per-CTA partials in the context's scratch; the last CTA writes the
+    // folded result straight into mapped pinned host memory
+    f.parts = static_cast<dev::AggPart*>(ctx->get_scratch(static_cast<size_t>(grid) * sizeof(dev::AggPart)));
+    f.out = static_cast<dev::AggPart*>(ctx->result_dev);
     f.err = reinterpret_cast<int*>(ctx->tickets + 1);  // zero between launches (the kernel resets it)
     {
       KTimer timer(ctx, "filtered_points_reduce");
@@ -989,8 +990,8 @@ AggOut filtered_aggregate_binop(const CtxPtr& ctx, const DCol& c, Scalar k, int 
       ctx->count_launch();
       RQ_CUDA_CHECK(cudaGetLastError());
     }
-    const int64_t* h = ctx->readback(out.raw(), sizeof(dev::AggPart));
-    res = *reinterpret_cast<const dev::AggPart*>(h);
+    ctx->sync();
+    std::memcpy(&res, ctx->result_host, sizeof(res));
     if (!flt && op == RQ_DIV && res.imin) fail("integer division by zero");
   } else if (np > 0 && xs.n > 0 && cs.n > 0) {
     constexpr int64_t TILE = static_cast<int64_t>(FB) * FI;

@@ -69,6 +69,10 @@ struct Ctx {
   int sm_count = 148;
   int64_t launches = 0;
   int64_t* pinned = nullptr;  // host-pinned readback slots
+  // host-pinned slot kernels write their final result into directly
+  // (device-visible alias of pinned + 2048 B): no copy launch per query
+  void* result_host = nullptr;
+  void* result_dev = nullptr;
   // decoupled look-back tile status (epoch-tagged, see device_common.cuh)
   unsigned long long* tile_status = nullptr;
   int64_t tile_status_cap = 0;
