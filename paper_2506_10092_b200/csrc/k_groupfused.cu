@@ -19,7 +19,9 @@
 // COUNT and group presence come from the key runs alone (Σ run lengths per
 // slot). Tables are per-CTA shared memory when they fit, global otherwise;
 // integer sums wrap like the reference's int64 accumulators.
+#include <algorithm>
 #include <cmath>
+#include <memory>
 #include <cstdlib>
 #include <limits>
 
@@ -1160,14 +1162,34 @@ constexpr size_t xg_rows_smem() {
 
 // Per segment: COUNT (Σ lengths) and expressions over RLE operands only
 // (value × length, the reference's run weights).
+// Warp-aggregated add: lanes holding the same cell combine first (segments
+// come in position order, so neighbouring segments mostly share a slot) and
+// one lane per distinct cell issues the atomic.
+__device__ __forceinline__ void xg_add_u64(unsigned long long* base, int64_t cell, uint64_t v) {
+  const unsigned same = __match_any_sync(__activemask(), static_cast<unsigned long long>(cell));
+  uint64_t sum = 0;
+  for (unsigned m = same; m; m &= m - 1) sum += __shfl_sync(same, v, __ffs(m) - 1);
+  if ((threadIdx.x & 31) == __ffs(same) - 1 && sum) atomicAdd(base + cell, static_cast<unsigned long long>(sum));
+}
+__device__ __forceinline__ void xg_add_f64(double* base, int64_t cell, double v) {
+  const unsigned same = __match_any_sync(__activemask(), static_cast<unsigned long long>(cell));
+  double sum = 0.0;
+  for (unsigned m = same; m; m &= m - 1) sum += __shfl_sync(same, v, __ffs(m) - 1);
+  if ((threadIdx.x & 31) == __ffs(same) - 1 && sum != 0.0) atomicAdd(base + cell, sum);
+}
+
 __global__ void k_xg_segs(const __grid_constant__ XgPlan P, const __grid_constant__ XgSegs S, unsigned long long* __restrict__ tab,
                           unsigned long long* __restrict__ cnt, int* __restrict__ err) {
   int lerr = 0;
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < S.n;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t len = ldg64(S.e, k) - ldg64(S.s, k) + 1;
-    const int64_t slot = ldg64(S.slot, k);
-    atomicAdd(cnt + slot, static_cast<unsigned long long>(len));
+  // every lane of a warp runs the same number of iterations (warp-collective adds)
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t base = first; base < S.n; base += stride) {
+    const int64_t k = base + (threadIdx.x & 31);
+    const bool ok = k < S.n;
+    const int64_t len = ok ? ldg64(S.e, k) - ldg64(S.s, k) + 1 : 0;
+    const int64_t slot = ok ? ldg64(S.slot, k) : 0;
+    xg_add_u64(cnt, slot, static_cast<uint64_t>(len));
     for (int ei = 0; ei < P.ne; ++ei) {
       const XgExpr& X = P.e[ei];
       if (X.rows || X.nt == 0) continue;
@@ -1175,18 +1197,19 @@ __global__ void k_xg_segs(const __grid_constant__ XgPlan P, const __grid_constan
       int vf = 0;
       for (int ti = 0; ti < X.nt; ++ti) {
         const XgTerm& T = X.t[ti];
-        const uint64_t y = xg_term(T, __ldg(S.cst + (T.src - XG_COLS) * S.n + k), &lerr);
+        const uint64_t y = ok ? xg_term(T, __ldg(S.cst + (T.src - XG_COLS) * S.n + k), &lerr) : 0;
         const int yf = T.flt || (T.sop >= 0 && T.kflt);
         if (ti == 0) {
           v = y;
           vf = yf;
         } else {
-          v = xg_op(v, vf, y, yf, X.op[ti - 1], &lerr);
+          v = ok ? xg_op(v, vf, y, yf, X.op[ti - 1], &lerr) : 0;
           vf = vf || yf;
         }
       }
-      if (X.acc_f) atomicAdd(reinterpret_cast<double*>(tab) + slot * P.ne + ei, xg_f(v, vf) * static_cast<double>(len));
-      else atomicAdd(tab + slot * P.ne + ei, static_cast<unsigned long long>(static_cast<uint64_t>(v) * static_cast<uint64_t>(len)));
+      const int64_t cell = slot * P.ne + ei;
+      if (X.acc_f) xg_add_f64(reinterpret_cast<double*>(tab), cell, ok ? xg_f(v, vf) * static_cast<double>(len) : 0.0);
+      else xg_add_u64(tab, cell, static_cast<uint64_t>(v) * static_cast<uint64_t>(len));
     }
   }
   if (lerr) atomicOr(err, 1);
@@ -1198,17 +1221,20 @@ __global__ void k_xg_outliers(PlainSrc base, const int64_t* __restrict__ p, cons
                               const int64_t* __restrict__ idx_of, const int64_t* __restrict__ run_of, int64_t n,
                               const int64_t* __restrict__ seg_slot, int ne, int ei, int acc_f,
                               unsigned long long* __restrict__ tab) {
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t pos = ldg64(p, i);
-    const int64_t slot = ldg64(seg_slot, ldg64(run_of, i));
-    const int64_t q = ldg64(idx_of, i);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t b = first; b < n; b += stride) {  // warp-uniform trip count (warp-collective adds)
+    const int64_t i = b + (threadIdx.x & 31);
+    const bool ok = i < n;
+    const int64_t pos = ok ? ldg64(p, i) : 0;
+    const int64_t slot = ok ? ldg64(seg_slot, ldg64(run_of, i)) : 0;
+    const int64_t q = ok ? ldg64(idx_of, i) : 0;
     if (acc_f) {
-      const double d = ld_f64(v2, v2dt, q) - plain_value<double>(base, pos);
-      atomicAdd(reinterpret_cast<double*>(tab) + slot * ne + ei, d);
+      const double d = ok ? ld_f64(v2, v2dt, q) - plain_value<double>(base, pos) : 0.0;
+      xg_add_f64(reinterpret_cast<double*>(tab), slot * ne + ei, d);
     } else {
-      const uint64_t d = static_cast<uint64_t>(ld_i64(v2, v2dt, q)) - static_cast<uint64_t>(plain_value<int64_t>(base, pos));
-      atomicAdd(tab + slot * ne + ei, static_cast<unsigned long long>(d));
+      const uint64_t d = ok ? static_cast<uint64_t>(ld_i64(v2, v2dt, q)) - static_cast<uint64_t>(plain_value<int64_t>(base, pos)) : 0;
+      xg_add_u64(tab, slot * ne + ei, d);
     }
   }
 }
@@ -1399,6 +1425,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   for (size_t j = 0; j < rle_cols.size(); ++j) P.cst_f[j] = dt_float(rle_cols[j]->v.dt) ? 1 : 0;
 
   // ---- segment table: keys ∩ mask ∩ RLE operands (align_many's joint shape) ----
+  auto stage = std::make_unique<KTimer>(ctx, "xg_keys");  // per-stage profile tags (no-ops unless profiling)
   GroupKey K;
   if (preK) {
     K = *preK;
@@ -1411,7 +1438,9 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     K.slot = xg_fill(ctx, 0);
     K.G = 1;
   }
+  stage.reset();
   KTimer timer(ctx, "group_exprs");
+  stage = std::make_unique<KTimer>(ctx, "xg_where");
   DArr s = K.s, e = K.e, slot = K.slot;
   std::vector<DArr> cst;
   if (mask) {
@@ -1425,11 +1454,14 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     s = r.s;
     e = r.e;
   }
-  if (npred) {  // WHERE pushdown: segment ∩ each predicate column's runs, then keep the passing segments
-    std::vector<const DCol*> pcols;
-    std::vector<DArr> pv;
-    dev::XgPreds W{};
-    W.n = static_cast<int>(npred);
+  if (npred) {
+    // WHERE pushdown: the segments are intersected with each distinct
+    // predicate column's runs (fewest runs first) and the passing segments
+    // kept; before a column with many runs the segments are pruned by the
+    // conjuncts already evaluable, so the large intersection runs on the
+    // selected segments only.
+    std::vector<const DCol*> pcols;  // distinct predicate columns
+    std::vector<int> pcol_of(npred);
     for (size_t i = 0; i < npred; ++i) {
       const XPred& q = (*preds)[i];
       int src = -1;
@@ -1437,30 +1469,38 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
         if (pcols[j] == q.col || (pcols[j]->v.raw() == q.col->v.raw() && pcols[j]->e.raw() == q.col->e.raw()))
           src = static_cast<int>(j);
       if (src < 0) {
-        Intersection r = range_intersect(ctx, s, e, q.col->s, q.col->e, true, true);
-        slot = gather(ctx, slot, r.idx1);
-        for (auto& v : pv) v = gather(ctx, v, r.idx1);
-        pv.push_back(xg_const_bits(ctx, gather(ctx, q.col->v, r.idx2)));
         pcols.push_back(q.col);
-        s = r.s;
-        e = r.e;
-        src = static_cast<int>(pv.size()) - 1;
+        src = static_cast<int>(pcols.size()) - 1;
       }
-      dev::XgPred& P = W.p[i];
-      P.src = src;
-      P.flt = dt_float(q.col->v.dt) ? 1 : 0;
-      P.op = q.in.empty() ? q.op : -1;
-      const std::vector<Scalar> one{q.k};
-      const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
-      P.n_in = static_cast<int>(ks.size());
-      for (size_t j = 0; j < ks.size(); ++j) {
-        P.kflt[j] = ks[j].is_float ? 1 : 0;
-        P.ki[j] = ks[j].i;
-        P.kf[j] = ks[j].f;
-      }
+      pcol_of[i] = src;
     }
-    for (size_t j = 0; j < pv.size(); ++j) W.val[j] = reinterpret_cast<const uint64_t*>(pv[j].raw());
-    if (s.n) {
+    std::vector<int> order(pcols.size());
+    for (size_t j = 0; j < order.size(); ++j) order[j] = static_cast<int>(j);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return pcols[x]->e.n < pcols[y]->e.n; });
+    std::vector<int> slot_of(pcols.size(), -1);  // predicate column -> its value array in pv
+    std::vector<DArr> pv;
+    // keep the segments passing every conjunct whose column is already joined in
+    auto prune = [&]() {
+      dev::XgPreds W{};
+      for (size_t i = 0; i < npred; ++i) {
+        const int src = slot_of[pcol_of[i]];
+        if (src < 0) continue;
+        const XPred& q = (*preds)[i];
+        dev::XgPred& P = W.p[W.n++];
+        P.src = src;
+        P.flt = dt_float(q.col->v.dt) ? 1 : 0;
+        P.op = q.in.empty() ? q.op : -1;
+        const std::vector<Scalar> one{q.k};
+        const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
+        P.n_in = static_cast<int>(ks.size());
+        for (size_t j = 0; j < ks.size(); ++j) {
+          P.kflt[j] = ks[j].is_float ? 1 : 0;
+          P.ki[j] = ks[j].i;
+          P.kf[j] = ks[j].f;
+        }
+      }
+      for (size_t j = 0; j < pv.size(); ++j) W.val[j] = reinterpret_cast<const uint64_t*>(pv[j].raw());
+      if (!s.n || !W.n) return;
       DArr flags = alloc_arr(ctx, RQ_I8, s.n);
       dev::k_xg_where<<<grid_cap(ctx, s.n), 256, 0, ctx->stream>>>(W, s.n, flags.as<uint8_t>());
       launched(ctx);
@@ -1469,8 +1509,22 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       s = gather(ctx, s, keep);
       e = gather(ctx, e, keep);
       slot = gather(ctx, slot, keep);
+      for (auto& v : pv) v = gather(ctx, v, keep);
+    };
+    for (size_t oi = 0; oi < order.size(); ++oi) {
+      const DCol* col = pcols[order[oi]];
+      if (oi > 0 && col->e.n >= 65536 && s.n > 0 && col->e.n >= 16 * s.n) prune();
+      Intersection r = range_intersect(ctx, s, e, col->s, col->e, true, true);
+      slot = gather(ctx, slot, r.idx1);
+      for (auto& v : pv) v = gather(ctx, v, r.idx1);
+      pv.push_back(xg_const_bits(ctx, gather(ctx, col->v, r.idx2)));
+      slot_of[order[oi]] = static_cast<int>(pv.size()) - 1;
+      s = r.s;
+      e = r.e;
     }
+    prune();
   }
+  stage = std::make_unique<KTimer>(ctx, "xg_operands");
   for (const DCol* rc : rle_cols) {
     Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
     slot = gather(ctx, slot, r.idx1);
@@ -1479,6 +1533,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     s = r.s;
     e = r.e;
   }
+  stage = std::make_unique<KTimer>(ctx, "xg_prep");
   const int64_t nseg = s.n;
   DArr cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * static_cast<int64_t>(cst.size())));
   for (size_t j = 0; j < cst.size(); ++j)
@@ -1510,6 +1565,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   }
   bool any_rows = false;
   for (int i = 0; i < P.ne; ++i) any_rows = any_rows || P.e[i].rows;
+  stage.reset();
   if (any_rows && ncov > 0) {
     constexpr int B = 256;
     const int64_t warps = static_cast<int64_t>(ctx->sm_count) * 8 * (B / 32);
@@ -1555,6 +1611,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     }
   }
   // ---- outputs: present slots ascending (= ascending keys) ----
+  stage = std::make_unique<KTimer>(ctx, "xg_out");
   DArr present;
   if (keys.empty()) {
     present = xg_fill(ctx, 0);
