@@ -1270,6 +1270,25 @@ __global__ void k_xg_lengths(const int64_t* __restrict__ s, const int64_t* __res
 namespace dev {
 __global__ void k_xg_fill1(int64_t* __restrict__ out, int64_t v) { *out = v; }
 
+constexpr int XG_GATHER = 8;
+struct XgGather {
+  int n;
+  const void* src[XG_GATHER];
+  int dt[XG_GATHER];
+  int to_f[XG_GATHER];
+  void* dst[XG_GATHER];
+};
+__global__ void k_xg_gather(const __grid_constant__ XgGather G, const int64_t* __restrict__ idx, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = ldg64(idx, i);
+    for (int a = 0; a < G.n; ++a) {
+      if (G.to_f[a]) static_cast<double*>(G.dst[a])[i] = ld_f64(G.src[a], G.dt[a], j);
+      else static_cast<int64_t*>(G.dst[a])[i] = ld_i64(G.src[a], G.dt[a], j);
+    }
+  }
+}
+
 // WHERE pushdown: one conjunct per entry, `col op k` or `col IN (list)`,
 // evaluated once per segment on the segment's value of the predicate column
 // (compare_scalar semantics, align.cpp:551-567: f64 if either side is float)
@@ -1336,6 +1355,31 @@ bool xg_vec_ok(const DArr& a) {
 
 DArr xg_const_bits(const CtxPtr& ctx, const DArr& v) {
   return cast_values(ctx, v, dt_float(v.dt) ? RQ_F64 : RQ_I64);
+}
+
+// Several gathers through one index array in one launch; each source may
+// be of any dtype and lands as i64 / f64 (segment-table columns). Replaces
+// the arrays in place (one launch instead of one per array).
+void gather_many(const CtxPtr& ctx, const std::vector<DArr*>& arrs, const DArr& idx) {
+  for (size_t a0 = 0; a0 < arrs.size(); a0 += dev::XG_GATHER) {
+    dev::XgGather G{};
+    std::vector<DArr> outs;
+    for (size_t a = a0; a < arrs.size() && a < a0 + dev::XG_GATHER; ++a) {
+      const DArr& src = *arrs[a];
+      const int32_t odt = dt_float(src.dt) ? RQ_F64 : RQ_I64;
+      outs.push_back(alloc_arr(ctx, odt, idx.n));
+      G.src[G.n] = src.raw();
+      G.dt[G.n] = src.dt;
+      G.to_f[G.n] = odt == RQ_F64 ? 1 : 0;
+      G.dst[G.n] = outs.back().raw_mut();
+      ++G.n;
+    }
+    if (idx.n) {
+      dev::k_xg_gather<<<grid_cap(ctx, idx.n), 256, 0, ctx->stream>>>(G, idx.pos(), idx.n);
+      launched(ctx);
+    }
+    for (size_t a = a0; a < arrs.size() && a < a0 + dev::XG_GATHER; ++a) *arrs[a] = outs[a - a0];
+  }
 }
 
 bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
@@ -1506,18 +1550,20 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       launched(ctx);
       DArr keep;
       select_points(ctx, flags, iota(ctx, s.n), keep, nullptr);
-      s = gather(ctx, s, keep);
-      e = gather(ctx, e, keep);
-      slot = gather(ctx, slot, keep);
-      for (auto& v : pv) v = gather(ctx, v, keep);
+      std::vector<DArr*> g{&s, &e, &slot};
+      for (auto& v : pv) g.push_back(&v);
+      gather_many(ctx, g, keep);
     };
     for (size_t oi = 0; oi < order.size(); ++oi) {
       const DCol* col = pcols[order[oi]];
       if (oi > 0 && col->e.n >= 65536 && s.n > 0 && col->e.n >= 16 * s.n) prune();
       Intersection r = range_intersect(ctx, s, e, col->s, col->e, true, true);
-      slot = gather(ctx, slot, r.idx1);
-      for (auto& v : pv) v = gather(ctx, v, r.idx1);
-      pv.push_back(xg_const_bits(ctx, gather(ctx, col->v, r.idx2)));
+      std::vector<DArr*> g{&slot};
+      for (auto& v : pv) g.push_back(&v);
+      gather_many(ctx, g, r.idx1);
+      DArr nv = col->v;
+      gather_many(ctx, {&nv}, r.idx2);
+      pv.push_back(nv);
       slot_of[order[oi]] = static_cast<int>(pv.size()) - 1;
       s = r.s;
       e = r.e;
@@ -1527,9 +1573,12 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   stage = std::make_unique<KTimer>(ctx, "xg_operands");
   for (const DCol* rc : rle_cols) {
     Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
-    slot = gather(ctx, slot, r.idx1);
-    for (auto& c : cst) c = gather(ctx, c, r.idx1);
-    cst.push_back(xg_const_bits(ctx, gather(ctx, rc->v, r.idx2)));
+    std::vector<DArr*> g{&slot};
+    for (auto& c : cst) g.push_back(&c);
+    gather_many(ctx, g, r.idx1);
+    DArr nv = rc->v;
+    gather_many(ctx, {&nv}, r.idx2);
+    cst.push_back(nv);
     s = r.s;
     e = r.e;
   }
