@@ -403,7 +403,7 @@ class Q1(Q6):
             assert fused, "q1: fused path not taken"
         else:
             ks, vs, ng = Q.q1(rq, d)
-        h = [v.download() if hasattr(v, "download") else v for v in vs]
+        h = rq.download_all(vs)
         return (int(h[7].sum()), int(h[0].sum()), float(h[3].sum()))  # Σ COUNT, Σ SUM(qty), Σ SUM(charge)
 
     def ref_run(self, ref, shards, threads):
@@ -459,7 +459,7 @@ class C5(Q6):
             assert fused, "c5: fused path not taken"
         else:
             ks, vs, ng = Q.c5_query(rq, d)
-        h = [v.download() if hasattr(v, "download") else v for v in vs]
+        h = rq.download_all(vs)
         self._sel = int(h[2].sum())
         return (self._sel, int(h[0].sum()), int(h[1].sum()))
 

@@ -169,6 +169,8 @@ int rq_arr_wrap_device(rq_ctx_t ctx, int32_t dtype, void* dev, int64_t n, rq_arr
 int rq_arr_info(rq_arr_t a, int32_t* dtype, int64_t* n);
 void* rq_arr_device_ptr(rq_arr_t a);
 int rq_arr_download(rq_ctx_t ctx, rq_arr_t a, void* host);
+/* downloads n arrays (hosts[i] sized like arrs[i]) with one synchronisation */
+int rq_arr_download_many(rq_ctx_t ctx, int32_t n, const rq_arr_t* arrs, void* const* hosts);
 int rq_arr_free(rq_arr_t a);
 
 /* ---------------------------------------------------------------------- */

@@ -36,6 +36,7 @@ PROTOTYPES = {
     "rq_arr_info": (C.c_int, [vp, P(i32), P(i64)]),
     "rq_arr_device_ptr": (vp, [vp]),
     "rq_arr_download": (C.c_int, [vp, vp, vp]),
+    "rq_arr_download_many": (C.c_int, [vp, i32, P(vp), P(vp)]),
     "rq_arr_free": (C.c_int, [vp]),
     "rq_col_upload": (C.c_int, [vp, P(HostColumn), P(vp)]),
     "rq_col_describe": (C.c_int, [vp, P(HostColumn)]),

@@ -330,6 +330,14 @@ int rq_arr_download(rq_ctx_t c, rq_arr_t a, void* host) {
   });
 }
 
+int rq_arr_download_many(rq_ctx_t c, int32_t n, const rq_arr_t* arrs, void* const* hosts) {
+  return api_guard([&] {
+    auto ctx = get_ctx(c);
+    for (int32_t i = 0; i < n; ++i) download_arr(ctx, get_arr(arrs[i]), hosts[i]);
+    ctx->sync();  // one synchronisation for the whole result set
+  });
+}
+
 int rq_arr_free(rq_arr_t a) {
   return api_guard([&] { delete a; });
 }

@@ -472,6 +472,18 @@ bool full_cover(const CtxPtr& ctx, const DCol& c) {
   }
 }
 
+std::pair<int64_t, int64_t> minmax(const CtxPtr& ctx, const DArr& v);
+// a key column's value range, cached on the column
+std::pair<int64_t, int64_t> col_minmax(const CtxPtr& ctx, const DCol& c) {
+  if (!c.has_minmax) {
+    auto mm = minmax(ctx, c.v);
+    c.vmin = mm.first;
+    c.vmax = mm.second;
+    c.has_minmax = true;
+  }
+  return {c.vmin, c.vmax};
+}
+
 std::pair<int64_t, int64_t> minmax(const CtxPtr& ctx, const DArr& v) {
   DArr mm = alloc_arr(ctx, RQ_I64, 2);
   const int64_t init[2] = {INT64_MAX, INT64_MIN};
@@ -619,7 +631,7 @@ bool build_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKey
   std::vector<DArr> vals{keys[0]->v};
   K.s = keys[0]->s;
   K.e = e;
-  auto mm = minmax(ctx, vals[0]);
+  auto mm = col_minmax(ctx, *keys[0]);
   const int64_t range = mm.second - mm.first + 1;
   if (vals[0].n == 0 || range <= 0 || range > kFusedSlotLimit) return false;
   K.G = range;
@@ -660,7 +672,9 @@ bool build_multi_key(const CtxPtr& ctx, const std::vector<const DCol*>& keys, Gr
   std::vector<int64_t> mn(keys.size()), range(keys.size()), stride(keys.size());
   for (size_t c = 0; c < keys.size(); ++c) {
     if (vals[c].n == 0) return false;
-    auto mm = minmax(ctx, vals[c]);
+    // the column's range (cached) bounds the aligned values: slots of absent
+    // combinations stay empty and are dropped by the count > 0 test
+    auto mm = col_minmax(ctx, *keys[c]);
     mn[c] = mm.first;
     range[c] = mm.second - mm.first + 1;
     if (range[c] <= 0 || range[c] > kFusedSlotLimit) return false;
@@ -1258,6 +1272,32 @@ __global__ void k_xg_finish(const int64_t* __restrict__ slots, int64_t ng, int n
   }
 }
 
+struct XgFinish {
+  int ne;
+  int fn[XG_EXPRS];
+  void* out[XG_EXPRS];
+};
+__global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_t* __restrict__ slots, int64_t ng,
+                                const unsigned long long* __restrict__ tab, const unsigned long long* __restrict__ cnt) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < ng;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = ldg64(slots, i);
+    const unsigned long long c = cnt[g];
+    for (int ei = 0; ei < F.ne; ++ei) {
+      const int fn = F.fn[ei];
+      if (fn == RQ_COUNT) {
+        static_cast<long long*>(F.out[ei])[i] = static_cast<long long>(c);
+      } else if (fn == RQ_AVG) {
+        static_cast<double*>(F.out[ei])[i] =
+            c ? __longlong_as_double(static_cast<long long>(tab[g * F.ne + ei])) / static_cast<double>(c)
+              : __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        static_cast<unsigned long long*>(F.out[ei])[i] = tab[g * F.ne + ei];
+      }
+    }
+  }
+}
+
 __global__ void k_xg_lengths(const int64_t* __restrict__ s, const int64_t* __restrict__ e, int64_t n,
                              int64_t* __restrict__ len) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -1682,18 +1722,21 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     }
     out.keys.push_back(kout);
   }
+  dev::XgFinish F{};  // every expression's output in one launch
+  F.ne = P.ne;
   for (int i = 0; i < P.ne; ++i) {
     const int fn = fns[static_cast<size_t>(i)];
     const int32_t odt = fn == RQ_COUNT ? RQ_I64 : (fn == RQ_AVG || P.e[i].res_f) ? RQ_F64 : RQ_I64;
     DArr res = alloc_arr(ctx, odt, ng);
-    if (ng) {
-      dev::k_xg_finish<<<grid_cap(ctx, ng), 256, 0, ctx->stream>>>(present.pos(), ng, P.ne, i, fn, P.e[i].acc_f,
-                                                                    reinterpret_cast<const unsigned long long*>(tab.raw()),
-                                                                    reinterpret_cast<const unsigned long long*>(cnt.raw()),
-                                                                    res.raw_mut());
-      launched(ctx);
-    }
+    F.fn[i] = fn;
+    F.out[i] = res.raw_mut();
     out.vals.push_back(res);
+  }
+  if (ng) {
+    dev::k_xg_finish_all<<<grid_cap(ctx, ng), 256, 0, ctx->stream>>>(
+        F, present.pos(), ng, reinterpret_cast<const unsigned long long*>(tab.raw()),
+        reinterpret_cast<const unsigned long long*>(cnt.raw()));
+    launched(ctx);
   }
   return true;
 }

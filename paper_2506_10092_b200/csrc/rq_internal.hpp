@@ -192,6 +192,10 @@ struct DCol {
   DArr v2, p2;
   // RLE facts computed on demand: 1 if runs tile [0,total) with no gaps
   mutable int gapless = -1;
+  // min / max of v (integer columns; computed on first use by the group-by
+  // key builder — columns are immutable, so the facts stay valid)
+  mutable bool has_minmax = false;
+  mutable int64_t vmin = 0, vmax = 0;
 
   int32_t value_type() const {  // column.cpp:88-97
     switch (enc) {

@@ -199,6 +199,23 @@ def _out(dev, host_mode: bool):
     return dev.download() if host_mode else dev
 
 
+def download_all(arrays):
+    """Host copies of several device arrays (results of one query) with one
+    synchronisation; host objects pass through unchanged."""
+    dev = [a for a in arrays if isinstance(a, DeviceArray)]
+    if not dev:
+        return list(arrays)
+    outs = {}
+    for a in dev:
+        dt, n = a.info
+        outs[id(a)] = np.empty(n, dtype=H.DTYPES[dt])
+    ctx = dev[0].ctx
+    handles = (C.c_void_p * len(dev))(*[a.handle.value for a in dev])
+    ptrs = (C.c_void_p * len(dev))(*[outs[id(a)].ctypes.data if outs[id(a)].size else None for a in dev])
+    check(_L.rq_arr_download_many(ctx.handle, len(dev), handles, ptrs))
+    return [outs[id(a)] if isinstance(a, DeviceArray) else a for a in arrays]
+
+
 def _ctx_of(*xs) -> Context:
     for x in xs:
         if isinstance(x, (DeviceColumn, DeviceMask, DeviceArray)):
