@@ -172,16 +172,17 @@ def alg_bytes(col, gapless=True, only_points=None):
     return n * col.values.itemsize
 
 
-def ncu_traffic(tag):
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    capture summary (profiles/ncu_traffic.json), or None."""
+def ncu_traffic(workload, tag):
+    """dram bytes per launch of the dominant kernel (tag) or of the whole
+    query step (tag "query") of one workload, from the committed ncu captures
+    (profiles/ncu_traffic.json, keyed "<workload>:<tag>"), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(tag, {}).get("dram_bytes_per_launch")
+        return d.get(f"{workload}:{tag}", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -710,7 +711,7 @@ def main():
         ab = w.alg_bytes(host)
         achieved = ab / (avg_ms / 1000.0) / 1e9
         roof = {"bound": "hbm", "kernel": w.tag, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": ncu_traffic(w.tag), "alg_bytes_per_launch": ab,
+                "frac": achieved / hbm, "traffic": ncu_traffic(w.name, w.tag), "alg_bytes_per_launch": ab,
                 "avg_launch_ms": avg_ms, "launches": st["count"], "peak_source": peak_kind,
                 "share_of_step": st["ms"] / (ms * args.steps)}
         if w.tag == "xg_rows":  # also the whole query (segment table + masks + row kernel) against its bytes
@@ -719,11 +720,12 @@ def main():
             w.tag = "xg_rows"
             roof["query_alg_bytes"] = qb
             roof["query_achieved_gbs"] = qb / (ms / 1000.0) / 1e9
+            roof["query_traffic"] = ncu_traffic(w.name, "query")
     elif w.tag is None:  # operator-chain workloads: whole step against the query's bytes
         ab = w.alg_bytes(host)
         achieved = ab / (ms / 1000.0) / 1e9
         roof = {"bound": "hbm", "kernel": "query (operator chain)", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "alg_bytes_per_launch": ab,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(w.name, "query"), "alg_bytes_per_launch": ab,
                 "avg_launch_ms": ms, "launches": args.steps, "peak_source": peak_kind, "share_of_step": 1.0}
 
     cpu = None

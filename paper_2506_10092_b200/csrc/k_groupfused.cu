@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(256)
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   constexpr int PER = 8, WIN = 32 * PER;
+  const bool vec_pts = POINTS && (reinterpret_cast<uintptr_t>(pp) & 15) == 0 && (reinterpret_cast<uintptr_t>(pv) & 15) == 0;
   for (int64_t s0 = warp * seg; s0 < n; s0 += nwarps * seg) {
     const int64_t s1 = min(s0 + seg, n);
     // key run containing the segment's first position
@@ -295,6 +296,24 @@ __global__ void __launch_bounds__(256)
         for (int u = 0; u < PER; ++u) {
           pos[u] = i0 + u;
           val[u] = plain_decode<T, S>(ps, raw[u]);
+        }
+      } else if (POINTS && i0 + PER <= s1 && vec_pts) {
+        // 8 consecutive points per lane: 4 x 16-B loads of positions (and of
+        // 8-byte values), instead of 8 strided scalar loads each
+        load8<int64_t>(pp + i0, pos);
+        if (pdt == RQ_I64 || pdt == RQ_F64) {
+          int64_t raw[PER];
+          load8<int64_t>(static_cast<const int64_t*>(pv) + i0, raw);
+#pragma unroll
+          for (int u = 0; u < PER; ++u)
+            val[u] = pdt == RQ_I64 ? static_cast<T>(raw[u]) : static_cast<T>(__longlong_as_double(raw[u]));
+        } else {
+#pragma unroll
+          for (int u = 0; u < PER; ++u) val[u] = ld_as<T>(pv, pdt, i0 + u);
+        }
+        if (corr) {
+#pragma unroll
+          for (int u = 0; u < PER; ++u) val[u] -= plain_value<T>(*corr, pos[u]);
         }
       } else {
 #pragma unroll
@@ -505,15 +524,15 @@ struct GroupKey {
 template <int KIND>
 void run_rle(const CtxPtr& ctx, const GroupKey& K, const DArr& ds, const DArr& de, const DArr& dv,
              dev::GTable t, const double* mean) {
+  const int64_t nk = K.e.n, n = de.n;
+  if (nk == 0 || n == 0) return;
   constexpr int B = 256, IT = 8, TILE = B * IT;
-  const int64_t na = K.e.n, nb = de.n;
-  if (na == 0 || nb == 0) return;
-  const int64_t ntiles = (na + nb + TILE - 1) / TILE;
+  const int64_t ntiles = (nk + n + TILE - 1) / TILE;
   DArr part = alloc_arr(ctx, RQ_I64, ntiles + 1);
   dev::k_merge_partition<<<static_cast<unsigned>(((ntiles + 1) * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-      K.e.pos(), na, de.pos(), nb, TILE, ntiles + 1, part.as<int64_t>());
+      K.e.pos(), nk, de.pos(), n, TILE, ntiles + 1, part.as<int64_t>());
   launched(ctx);
-  dev::MergeArgs m{K.e.pos(), na, de.pos(), nb, part.as<int64_t>()};
+  dev::MergeArgs m{K.e.pos(), nk, de.pos(), n, part.as<int64_t>()};
   dev::k_gk_rle<B, IT, KIND><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
       m, K.s.pos(), K.slot.raw(), K.slot.dt, ds.pos(), dv.raw(), dv.dt, t, mean);
   launched(ctx);
@@ -545,7 +564,7 @@ void run_items(const CtxPtr& ctx, const GroupKey& K, const dev::PlainSrc& ps, co
         K.s.pos(), K.e.pos(), K.slot.raw(), K.slot.dt, K.e.n, ps, p ? p->pos() : nullptr,
         v ? v->raw() : nullptr, v ? v->dt : RQ_I64, n, seg, t, mean, dcorr);
   };
-  if (POINTS) {
+  if constexpr (POINTS) {
     go(int64_t{});
   } else {
     switch (ps.dt) {
