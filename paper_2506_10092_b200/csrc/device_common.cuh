@@ -438,5 +438,20 @@ __device__ __forceinline__ int smem_lower_bound(const int64_t* a, int n, int64_t
   return base + (a[base] < key ? 1 : 0);
 }
 
+// Warp-cooperative lower_bound over n <= 1024 sorted shared-memory int64
+// (all 32 lanes, same key; entries past the valid ones padded with
+// INT64_MAX): 32 evenly spaced probes and a ballot pick the block, a second
+// ballot over the block's <= 32 entries gives the rank. Two dependent
+// shared-memory rounds instead of log2(n).
+__device__ __forceinline__ int warp_smem_lower_bound(const int64_t* a, int n, int64_t key) {
+  const int lane = threadIdx.x & 31;
+  const int step = (n + 31) >> 5;
+  const int probe = min((lane + 1) * step, n) - 1;
+  const int c = __popc(__ballot_sync(FULL, a[probe] < key));
+  const int base = c * step;
+  const int i = base + lane;
+  return base + __popc(__ballot_sync(FULL, lane < step && i < n && a[i] < key));
+}
+
 }  // namespace dev
 }  // namespace rqb

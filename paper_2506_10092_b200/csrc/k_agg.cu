@@ -367,7 +367,7 @@ struct PairStage {
 };
 
 template <int BLOCK, int IA, int BW, class T, int OP, int KIND>
-__global__ void __launch_bounds__(BLOCK, 8)
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     k_pair_reduce_tma(const int64_t* __restrict__ Ae, const T* __restrict__ Av, int64_t na,
                       const int64_t* __restrict__ Be, const T* __restrict__ Bv, int64_t nb, int swap,
                       int ta, int64_t ntiles, AggPart* __restrict__ parts, unsigned* __restrict__ ticket,
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(BLOCK, 8)
         const int pst = st ^ 1;
         const int pna = static_cast<int>(min(static_cast<int64_t>(ta), na - (a0 - ta)));
         const int64_t r_prev_hi = sAe(pst)[2 + pna - 1];
-        const int rb = smem_lower_bound(sBe(pst), BW, r_prev_hi + 1);
+        const int rb = warp_smem_lower_bound(sBe(pst), BW, r_prev_hi + 1);
         int64_t jn = b_lo + rb;
         if (rb >= b_n && jn < nb) jn += warp_lower_bound(Be + jn, nb - jn, r_prev_hi + 1);
         const int64_t used = jn - jb;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(BLOCK, 8)
       // other-list window entries: [jf, jl) end inside (r_lo, r_hi); entry jl
       // is the run covering r_hi (uniform searches)
       const int jf = s_jf[st];  // = jb - window start (the producer's search)
-      const int jl = smem_lower_bound(wBe, BW, r_hi);
+      const int jl = warp_smem_lower_bound(wBe, BW, r_hi);
       if (jl < b_n) {
         // fast path: merge path over the tile's driver ends and the window's
         // ends, ITEMS-free even split of the merged sequence over the lanes;
@@ -918,26 +918,33 @@ void launch_gapless(const CtxPtr& ctx, unsigned g, const dev::MergeArgs& m, cons
 }
 
 // ---- persistent TMA form (K2) ----
-constexpr int TPB = 128, TPI = 10, TPW = 768;
-constexpr int TP_TA = (TPB - 32) * TPI;
-using TPStage = dev::PairStage<TP_TA, TPW>;
-constexpr size_t TP_SMEM = 2 * TPStage::BYTES;
+// CTA shape: BLOCK threads (one producer warp), IA driver runs per consumer
+// lane, BW-entry window of the other list. TpCfg<128, 10, 768> measured
+// best on C1 (sweep of 5..14 runs per lane, 128..256 threads, 384..1024
+// window entries: every other shape 3-15% slower).
+template <int B_, int I_, int W_>
+struct TpCfg {
+  static constexpr int BLOCK = B_, IA = I_, BW = W_;
+  static constexpr int TA = (B_ - 32) * I_;
+  static constexpr size_t SMEM = 2 * dev::PairStage<TA, W_>::BYTES;
+};
+using TpBase = TpCfg<128, 10, 768>;
 
-template <class T, int OP, int KIND>
+template <class C, class T, int OP, int KIND>
 void launch_pair_tma3(const CtxPtr& ctx, const DCol& A, const DCol& B, int swap, dev::AggPart* parts,
                       dev::AggPart* out, int ta, int64_t ntiles, int64_t& grid_out, bool dry) {
-  auto k = dev::k_pair_reduce_tma<TPB, TPI, TPW, T, OP, KIND>;
+  auto k = dev::k_pair_reduce_tma<C::BLOCK, C::IA, C::BW, T, OP, KIND>;
   static int occ = 0;
   if (!occ) {
-    RQ_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TP_SMEM)));
-    RQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, TPB, TP_SMEM));
+    RQ_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    RQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::BLOCK, C::SMEM));
     if (occ < 1) occ = 1;
   }
   int64_t grid = static_cast<int64_t>(ctx->sm_count) * occ;
   if (grid > ntiles) grid = ntiles;
   grid_out = grid;
   if (dry) return;
-  k<<<static_cast<unsigned>(grid), TPB, TP_SMEM, ctx->stream>>>(
+  k<<<static_cast<unsigned>(grid), C::BLOCK, C::SMEM, ctx->stream>>>(
       A.e.pos(), static_cast<const T*>(A.v.raw()), A.e.n, B.e.pos(), static_cast<const T*>(B.v.raw()), B.e.n, swap,
       ta, ntiles, parts, ctx->tickets, out, reinterpret_cast<int*>(ctx->tickets + 3));
 }
@@ -946,9 +953,9 @@ template <class T, int OP>
 void launch_pair_tma2(int kind, const CtxPtr& ctx, const DCol& A, const DCol& B, int swap, dev::AggPart* parts,
                       dev::AggPart* out, int ta, int64_t ntiles, int64_t& grid, bool dry) {
   switch (kind) {
-    case 0: launch_pair_tma3<T, OP, 0>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
-    case 1: launch_pair_tma3<T, OP, 1>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
-    default: launch_pair_tma3<T, OP, 2>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    case 0: launch_pair_tma3<TpBase, T, OP, 0>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    case 1: launch_pair_tma3<TpBase, T, OP, 1>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
+    default: launch_pair_tma3<TpBase, T, OP, 2>(ctx, A, B, swap, parts, out, ta, ntiles, grid, dry); break;
   }
 }
 
@@ -963,6 +970,17 @@ void launch_pair_tma1(int op, int kind, const CtxPtr& ctx, const DCol& A, const 
   }
 }
 
+// driver runs per tile: the full capacity unless the other list is dense
+// enough that its window would overflow (expected window ≈ ta · nb / na)
+template <class C>
+int tile_runs(const DCol& A, const DCol& B) {
+  int ta = C::TA;
+  const double ratio = static_cast<double>(B.e.n) / static_cast<double>(A.e.n);
+  const int fit = static_cast<int>((C::BW - 16 - 64) / std::max(ratio, 1e-9) * 0.9);
+  if (fit < ta) ta = std::max(64, fit & ~1);
+  return ta;
+}
+
 // gapless RLE × gapless RLE with 8-byte values of the arithmetic type, every
 // array bulk-copyable: the persistent kernel (one launch). false otherwise.
 bool pair_reduce_tma(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bool flt, int kind, AggHost& h) {
@@ -973,23 +991,20 @@ bool pair_reduce_tma(const CtxPtr& ctx, const DCol& a, const DCol& b, int op, bo
   const DCol& A = a_drives ? a : b;
   const DCol& B = a_drives ? b : a;
   const int swap = a_drives ? 0 : 1;
-  // driver runs per tile: the full capacity unless the other list is dense
-  // enough that its window would overflow (expected window ≈ ta · nb / na)
-  int ta = TP_TA;
-  const double ratio = static_cast<double>(B.e.n) / static_cast<double>(A.e.n);
-  const int fit = static_cast<int>((TPW - 16 - 64) / std::max(ratio, 1e-9) * 0.9);
-  if (fit < ta) ta = std::max(64, fit & ~1);
-  const int64_t ntiles = (A.e.n + ta - 1) / ta;
+  auto launch = [&](dev::AggPart* parts, dev::AggPart* out, int64_t& grid, bool dry) {
+    const int ta = tile_runs<TpBase>(A, B);
+    const int64_t ntiles = (A.e.n + ta - 1) / ta;
+    if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, dry);
+    else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, dry);
+  };
   int64_t grid = 0;
-  if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, nullptr, nullptr, ta, ntiles, grid, true);
-  else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, nullptr, nullptr, ta, ntiles, grid, true);
+  launch(nullptr, nullptr, grid, true);
   // partials in the context's scratch; the folded result lands in mapped pinned host memory
   auto* parts = static_cast<dev::AggPart*>(ctx->get_scratch(static_cast<size_t>(grid) * sizeof(dev::AggPart)));
   auto* out = static_cast<dev::AggPart*>(ctx->result_dev);
   {
     KTimer timer(ctx, "pair_reduce");
-    if (flt) launch_pair_tma1<double>(op, kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, false);
-    else launch_pair_tma1<int64_t>(op, kind, ctx, A, B, swap, parts, out, ta, ntiles, grid, false);
+    launch(parts, out, grid, false);
     ctx->count_launch();
     RQ_CUDA_CHECK(cudaGetLastError());
   }
