@@ -11,7 +11,7 @@ import os
 
 from .host import EncodingChoice, Expr, Heuristic, HostColumn, HostMask, JoinSide, Pred, Scalar
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librunq_b200.so")
+LIB_PATH = os.environ.get("RQ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "librunq_b200.so")
 
 _lib = None
 
