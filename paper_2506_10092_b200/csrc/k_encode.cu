@@ -174,7 +174,7 @@ DCol plain_to_rle(const CtxPtr& ctx, const DCol& c) {
   }
   launched(ctx);
   DArr starts;
-  select_points(ctx, flags, iota(ctx, n), starts, nullptr);
+  flagged_indices(ctx, flags, n, starts);
   const int64_t k = starts.n;
   out.s = starts;
   out.e = alloc_arr(ctx, RQ_I64, k);
@@ -351,7 +351,7 @@ DCol plain_to_plain_index(const CtxPtr& ctx, const DCol& c, double trim) {
   });
   launched(ctx);
   DArr op;
-  select_points(ctx, flags, iota(ctx, n), op, nullptr);
+  flagged_indices(ctx, flags, n, op);
   out.v = base;
   out.logical = c.logical;
   out.has_center = true;

@@ -810,7 +810,7 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
       reinterpret_cast<const unsigned long long*>(cnt.raw()), K.G, flags.as<uint8_t>());
   launched(ctx);
   DArr present;
-  select_points(ctx, flags, iota(ctx, K.G), present, nullptr);
+  flagged_indices(ctx, flags, K.G, present);
   const int64_t ng = present.n;
   out.n_groups = ng;
   for (size_t c = 0; c < keys.size(); ++c) {
@@ -1318,30 +1318,36 @@ __global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_
 }
 
 __global__ void k_xg_lengths(const int64_t* __restrict__ s, const int64_t* __restrict__ e, int64_t n,
-                             int64_t* __restrict__ len) {
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+                             int64_t* __restrict__ len) {  // len[n] = 0
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    len[i] = ldg64(e, i) - ldg64(s, i) + 1;
+    len[i] = i < n ? ldg64(e, i) - ldg64(s, i) + 1 : 0;
 }
 
 }  // namespace dev
 
 namespace dev {
 __global__ void k_xg_fill1(int64_t* __restrict__ out, int64_t v) { *out = v; }
+__global__ void k_xg_fill3(int64_t* a, int64_t va, int64_t* b, int64_t vb, int64_t* c, int64_t vc) {
+  *a = va;
+  *b = vb;
+  *c = vc;
+}
 
 constexpr int XG_GATHER = 8;
 struct XgGather {
   int n;
   const void* src[XG_GATHER];
+  const int64_t* idx[XG_GATHER];  // each array's own index (all of length n)
   int dt[XG_GATHER];
   int to_f[XG_GATHER];
   void* dst[XG_GATHER];
 };
-__global__ void k_xg_gather(const __grid_constant__ XgGather G, const int64_t* __restrict__ idx, int64_t n) {
+__global__ void k_xg_gather(const __grid_constant__ XgGather G, int64_t n) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = ldg64(idx, i);
     for (int a = 0; a < G.n; ++a) {
+      const int64_t j = ldg64(G.idx[a], i);
       if (G.to_f[a]) static_cast<double*>(G.dst[a])[i] = ld_f64(G.src[a], G.dt[a], j);
       else static_cast<int64_t*>(G.dst[a])[i] = ld_i64(G.src[a], G.dt[a], j);
     }
@@ -1416,29 +1422,38 @@ DArr xg_const_bits(const CtxPtr& ctx, const DArr& v) {
   return cast_values(ctx, v, dt_float(v.dt) ? RQ_F64 : RQ_I64);
 }
 
-// Several gathers through one index array in one launch; each source may
-// be of any dtype and lands as i64 / f64 (segment-table columns). Replaces
-// the arrays in place (one launch instead of one per array).
-void gather_many(const CtxPtr& ctx, const std::vector<DArr*>& arrs, const DArr& idx) {
-  for (size_t a0 = 0; a0 < arrs.size(); a0 += dev::XG_GATHER) {
+// Several gathers in one launch, each array through its own index array (all
+// of one length); each source may be of any dtype and lands as i64 / f64
+// (segment-table columns). Replaces the arrays in place.
+void gather_multi(const CtxPtr& ctx, const std::vector<std::pair<DArr*, const DArr*>>& items) {
+  for (size_t a0 = 0; a0 < items.size(); a0 += dev::XG_GATHER) {
     dev::XgGather G{};
     std::vector<DArr> outs;
-    for (size_t a = a0; a < arrs.size() && a < a0 + dev::XG_GATHER; ++a) {
-      const DArr& src = *arrs[a];
+    const int64_t n = items[a0].second->n;
+    for (size_t a = a0; a < items.size() && a < a0 + dev::XG_GATHER; ++a) {
+      const DArr& src = *items[a].first;
+      require(items[a].second->n == n, "gather_multi: index length mismatch");
       const int32_t odt = dt_float(src.dt) ? RQ_F64 : RQ_I64;
-      outs.push_back(alloc_arr(ctx, odt, idx.n));
+      outs.push_back(alloc_arr(ctx, odt, n));
       G.src[G.n] = src.raw();
+      G.idx[G.n] = items[a].second->pos();
       G.dt[G.n] = src.dt;
       G.to_f[G.n] = odt == RQ_F64 ? 1 : 0;
       G.dst[G.n] = outs.back().raw_mut();
       ++G.n;
     }
-    if (idx.n) {
-      dev::k_xg_gather<<<grid_cap(ctx, idx.n), 256, 0, ctx->stream>>>(G, idx.pos(), idx.n);
+    if (n) {
+      dev::k_xg_gather<<<grid_cap(ctx, n), 256, 0, ctx->stream>>>(G, n);
       launched(ctx);
     }
-    for (size_t a = a0; a < arrs.size() && a < a0 + dev::XG_GATHER; ++a) *arrs[a] = outs[a - a0];
+    for (size_t a = a0; a < items.size() && a < a0 + dev::XG_GATHER; ++a) *items[a].first = outs[a - a0];
   }
+}
+
+void gather_many(const CtxPtr& ctx, const std::vector<DArr*>& arrs, const DArr& idx) {
+  std::vector<std::pair<DArr*, const DArr*>> items;
+  for (DArr* a : arrs) items.push_back({a, &idx});
+  gather_multi(ctx, items);
 }
 
 bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
@@ -1536,9 +1551,13 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
   } else {
     if (total == 0) return false;
-    K.s = xg_fill(ctx, 0);  // one run [0, total) in slot 0 (device fills: no host staging)
-    K.e = xg_fill(ctx, total - 1);
-    K.slot = xg_fill(ctx, 0);
+    // one run [0, total) in slot 0 (one device fill: no host staging)
+    K.s = alloc_arr(ctx, RQ_I64, 1);
+    K.e = alloc_arr(ctx, RQ_I64, 1);
+    K.slot = alloc_arr(ctx, RQ_I64, 1);
+    dev::k_xg_fill3<<<1, 1, 0, ctx->stream>>>(K.s.as<int64_t>(), 0, K.e.as<int64_t>(), total - 1,
+                                              K.slot.as<int64_t>(), 0);
+    launched(ctx);
     K.G = 1;
   }
   stage.reset();
@@ -1608,7 +1627,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       dev::k_xg_where<<<grid_cap(ctx, s.n), 256, 0, ctx->stream>>>(W, s.n, flags.as<uint8_t>());
       launched(ctx);
       DArr keep;
-      select_points(ctx, flags, iota(ctx, s.n), keep, nullptr);
+      flagged_indices(ctx, flags, s.n, keep);
       std::vector<DArr*> g{&s, &e, &slot};
       for (auto& v : pv) g.push_back(&v);
       gather_many(ctx, g, keep);
@@ -1617,11 +1636,11 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       const DCol* col = pcols[order[oi]];
       if (oi > 0 && col->e.n >= 65536 && s.n > 0 && col->e.n >= 16 * s.n) prune();
       Intersection r = range_intersect(ctx, s, e, col->s, col->e, true, true);
-      std::vector<DArr*> g{&slot};
-      for (auto& v : pv) g.push_back(&v);
-      gather_many(ctx, g, r.idx1);
-      DArr nv = col->v;
-      gather_many(ctx, {&nv}, r.idx2);
+      DArr nv = col->v;  // segment tables through idx1, the column's values through idx2: one launch
+      std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
+      for (auto& v : pv) g.push_back({&v, &r.idx1});
+      g.push_back({&nv, &r.idx2});
+      gather_multi(ctx, g);
       pv.push_back(nv);
       slot_of[order[oi]] = static_cast<int>(pv.size()) - 1;
       s = r.s;
@@ -1632,11 +1651,11 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   stage = std::make_unique<KTimer>(ctx, "xg_operands");
   for (const DCol* rc : rle_cols) {
     Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
-    std::vector<DArr*> g{&slot};
-    for (auto& c : cst) g.push_back(&c);
-    gather_many(ctx, g, r.idx1);
     DArr nv = rc->v;
-    gather_many(ctx, {&nv}, r.idx2);
+    std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
+    for (auto& c : cst) g.push_back({&c, &r.idx1});
+    g.push_back({&nv, &r.idx2});
+    gather_multi(ctx, g);
     cst.push_back(nv);
     s = r.s;
     e = r.e;
@@ -1651,11 +1670,12 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   DArr off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
   int64_t ncov = 0;
   if (nseg) {
-    DArr len = alloc_arr(ctx, RQ_I64, nseg);
-    dev::k_xg_lengths<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
+    // lengths plus a trailing 0: the exclusive scan's last entry is the covered-row total
+    DArr len = alloc_arr(ctx, RQ_I64, nseg + 1);
+    dev::k_xg_lengths<<<grid_cap(ctx, nseg + 1), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
     launched(ctx);
     scan_exclusive_i64(ctx, len, off);
-    ncov = covered_rows(ctx, s, e);
+    ncov = *ctx->readback(off.as<int64_t>() + nseg, 8);
   }
   const int64_t G = K.G;
   const int64_t cells = G * P.ne;
@@ -1728,7 +1748,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     dev::k_gk_flags<<<grid_cap(ctx, G), 256, 0, ctx->stream>>>(reinterpret_cast<const unsigned long long*>(cnt.raw()),
                                                                 G, flags.as<uint8_t>());
     launched(ctx);
-    select_points(ctx, flags, iota(ctx, G), present, nullptr);
+    flagged_indices(ctx, flags, G, present);
   }
   const int64_t ng = present.n;
   out.n_groups = ng;

@@ -74,7 +74,7 @@ struct PointsByFlags {
   int64_t *p_out, *idx_out;
   __device__ __forceinline__ bool flag(int64_t i) const { return flags[i] != 0; }
   __device__ __forceinline__ void emit(int64_t o, int64_t i) const {
-    p_out[o] = ldg64(p, i);
+    p_out[o] = p ? ldg64(p, i) : i;  // no p: the flagged indices themselves
     if (idx_out) idx_out[o] = i;
   }
 };
@@ -370,6 +370,13 @@ void select_points(const CtxPtr& ctx, const DArr& flags, const DArr& p, DArr& p_
   const int64_t n = run_select(ctx, p.n, pol);
   set_len(p_out, n);
   if (idx_out) set_len(*idx_out, n);
+}
+
+// indices of the set flags (select_points over iota without materialising it)
+void flagged_indices(const CtxPtr& ctx, const DArr& flags, int64_t n, DArr& out) {
+  out = alloc_arr(ctx, RQ_I64, n);
+  dev::PointsByFlags pol{flags.as<uint8_t>(), nullptr, out.as<int64_t>(), nullptr};
+  set_len(out, run_select(ctx, n, pol));
 }
 
 void rle_cmp_scalar_select(const CtxPtr& ctx, const DArr& v, const DArr& s, const DArr& e,

@@ -368,6 +368,7 @@ void select_runs(const CtxPtr& ctx, const DArr& flags, const DArr& s, const DArr
 // keep p of points whose flag is set (optionally also their index)
 void select_points(const CtxPtr& ctx, const DArr& flags, const DArr& p, DArr& p_out,
                    DArr* idx_out);
+void flagged_indices(const CtxPtr& ctx, const DArr& flags, int64_t n, DArr& out);
 // RLE-column compare_scalar fused: flags computed inline from v
 void rle_cmp_scalar_select(const CtxPtr& ctx, const DArr& v, const DArr& s, const DArr& e,
                            Scalar k, int op, bool reversed, DArr& s_out, DArr& e_out);

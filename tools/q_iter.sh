@@ -2,7 +2,7 @@
 # K12 iteration: expression parity tests, q1/q6/c5 bench lines, ncu of the row kernel (q1)
 set -u
 TAG=${1:-x}
-timeout 900 python -m pytest tests/test_gpu_exprs.py tests/test_gpu_queries.py tests/test_c5.py -x -q > gpurun_out/t_$TAG.log 2>&1; tail -2 gpurun_out/t_$TAG.log
+timeout 900 python -m pytest tests/test_gpu_exprs.py tests/test_gpu_queries.py tests/test_c5.py tests/test_gpu_groupby.py tests/test_gpu_plans.py tests/test_gpu_encode.py -x -q > gpurun_out/t_$TAG.log 2>&1; tail -2 gpurun_out/t_$TAG.log
 for w in q1 q6 c5; do
   timeout 600 python bench.py --workload $w --no-cpu-baseline > gpurun_out/b_${TAG}_$w.json 2> gpurun_out/b_${TAG}_$w.log
   python -c "
