@@ -1,3 +1,4 @@
+#include <chrono>
 // ctx.cu — context, stream-ordered allocation, device arrays, column/mask
 // upload/download and the handle half of the C ABI (include/runq_b200.h).
 #include <cstring>
@@ -57,6 +58,8 @@ void Ctx::collect_profile() {
 Ctx::~Ctx() {
   cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  for (auto& kv : block_cache)
+    for (void* p : kv.second) cudaFree(p);
   for (auto& p : pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -69,12 +72,44 @@ Ctx::~Ctx() {
   if (stream) cudaStreamDestroy(stream);
 }
 
-void* Ctx::alloc(size_t bytes) {
+// Size classes of the context's block cache: powers of two up to 4 KB, then
+// eight steps per power of two (<= 12.5% slack).
+static size_t size_class(size_t bytes) {
+  size_t r = bytes < 256 ? 256 : bytes;
+  if (r <= 4096) {
+    size_t p = 256;
+    while (p < r) p <<= 1;
+    return p;
+  }
+  size_t p = size_t(1) << (63 - __builtin_clzll(r));
+  const size_t step = p / 8;
+  return (r + step - 1) / step * step;
+}
+
+// Blocks up to 64 MB are recycled through per-class free lists (at most 1 GB
+// held): every use of a block is ordered on this context's one stream, so a
+// block freed by one operator is safe to hand to the next launch at once —
+// no cudaMallocAsync / cudaFreeAsync round trip per intermediate array.
+void* Ctx::alloc(size_t bytes, size_t* cap) {
   if (bytes == 0) return nullptr;
+  const size_t c = size_class(bytes);
+  if (cap) *cap = c;
+  if (c <= kCacheMaxBlock) {
+    auto it = block_cache.find(c);
+    if (it != block_cache.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      cached_bytes -= c;
+      return p;
+    }
+  }
   void* p = nullptr;
-  // round up so 128-bit vector loads of the tail stay inside the allocation
-  size_t rounded = (bytes + 255) & ~size_t(255);
-  cudaError_t err = cudaMallocAsync(&p, rounded, stream);
+  cudaError_t err = cudaMallocAsync(&p, c, stream);
+  if (err != cudaSuccess) {  // give the cached blocks back and retry once
+    cudaGetLastError();
+    release_cache();
+    err = cudaMallocAsync(&p, c, stream);
+  }
   if (err != cudaSuccess) {
     cudaGetLastError();
     throw RqError(RQ_RESOURCE, "device allocation of " + std::to_string(bytes) +
@@ -83,16 +118,50 @@ void* Ctx::alloc(size_t bytes) {
   return p;
 }
 
-void Ctx::free(void* p) {
-  if (p) cudaFreeAsync(p, stream);
+void Ctx::free(void* p, size_t cap) {
+  if (!p) return;
+  if (cap && cap <= kCacheMaxBlock && cached_bytes + cap <= kCacheMaxBytes) {
+    block_cache[cap].push_back(p);
+    cached_bytes += cap;
+    return;
+  }
+  cudaSetDevice(device);
+  cudaFreeAsync(p, stream);
 }
 
-void Ctx::sync() { RQ_CUDA_CHECK(cudaStreamSynchronize(stream)); }
+void Ctx::release_cache() {
+  for (auto& kv : block_cache)
+    for (void* p : kv.second) cudaFreeAsync(p, stream);
+  block_cache.clear();
+  cached_bytes = 0;
+  cudaStreamSynchronize(stream);
+}
+
+// Stream synchronisation; under profiling its host wall time is recorded as
+// the pseudo-tag "host_sync_wait" (time the host spent blocked on the GPU).
+void Ctx::wait_stream() {
+  if (!profiling) {
+    RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  for (auto& kv : kstats)
+    if (kv.first == "host_sync_wait") {
+      kv.second.ms += ms;
+      kv.second.count += 1;
+      return;
+    }
+  kstats.push_back({"host_sync_wait", KStat{ms, 1}});
+}
+
+void Ctx::sync() { wait_stream(); }
 
 const int64_t* Ctx::readback(const void* dev, size_t bytes) {
   if (bytes > 4096) fail("readback too large");
   RQ_CUDA_CHECK(cudaMemcpyAsync(pinned, dev, bytes, cudaMemcpyDeviceToHost, stream));
-  RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
+  wait_stream();
   return pinned;
 }
 
@@ -133,8 +202,7 @@ void* Ctx::get_scratch(size_t bytes) {
 
 Buffer::~Buffer() {
   if (owned && ptr && ctx) {
-    cudaSetDevice(ctx->device);
-    ctx->free(ptr);
+    ctx->free(ptr, cap);
   }
 }
 
@@ -148,8 +216,7 @@ DArr alloc_arr(const CtxPtr& ctx, int32_t dt, int64_t n) {
     auto b = std::make_shared<Buffer>();
     b->ctx = ctx;
     b->bytes = static_cast<size_t>(n) * dt_width(dt);
-    b->ptr = ctx->alloc(b->bytes);
-    b->cap = (b->bytes + 255) & ~size_t(255);
+    b->ptr = ctx->alloc(b->bytes, &b->cap);
     a.buf = std::move(b);
   }
   return a;

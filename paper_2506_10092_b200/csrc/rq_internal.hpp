@@ -16,6 +16,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/runq_b200.h"
@@ -98,11 +99,16 @@ struct Ctx {
   };
   std::vector<std::pair<std::string, KStat>> kstats;
   cudaEvent_t get_event();
+  void wait_stream();
   void collect_profile();
 
   ~Ctx();
-  void* alloc(size_t bytes);
-  void free(void* p);
+  void* alloc(size_t bytes, size_t* cap = nullptr);
+  void free(void* p, size_t cap = 0);
+  void release_cache();
+  static constexpr size_t kCacheMaxBlock = size_t(64) << 20, kCacheMaxBytes = size_t(1) << 30;
+  std::unordered_map<size_t, std::vector<void*>> block_cache;
+  size_t cached_bytes = 0;
   void sync();
   // Copies `bytes` from device to the pinned slots and waits (one sync).
   const int64_t* readback(const void* dev, size_t bytes);
