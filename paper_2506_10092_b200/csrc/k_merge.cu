@@ -113,13 +113,13 @@ int64_t merge_select(const CtxPtr& ctx, const int64_t* A, int64_t na, const int6
     KTimer timer(ctx, tag);
     part = merge_partition(ctx, A, na, B, nb, MTILE, ntiles);
     dev::MergeArgs m{A, na, B, nb, part.as<int64_t>()};
-    count = part.as<int64_t>() + ntiles + 1;
+    count = ctx->count_slot_dev();
     dev::k_merge_select<MB, MI, Policy>
         <<<static_cast<unsigned>(ntiles), MB, 0, ctx->stream>>>(m, pol, lb, count);
     ctx->count_launch();
     RQ_CUDA_CHECK(cudaGetLastError());
   }
-  return *ctx->readback(count, 8);
+  return ctx->read_count_slot();
 }
 
 // Shrink an over-allocated output array's logical length (buffer kept).
@@ -173,12 +173,11 @@ PointsInRuns points_in_runs(const CtxPtr& ctx, const DArr& p, const DArr& s, con
       dev::LookBack lb{ctx->tile_status, 0};
       lb.epoch = ctx->next_epoch(ntiles);
       lb.status = ctx->tile_status;
-      DArr cnt = alloc_arr(ctx, RQ_I64, 1);
       dev::k_points_in_runs_search<B, IT><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
-          p.pos(), p.n, s.pos(), e.pos(), s.n, lb, po, ro, io, cnt.as<int64_t>());
+          p.pos(), p.n, s.pos(), e.pos(), s.n, lb, po, ro, io, ctx->count_slot_dev());
       ctx->count_launch();
       RQ_CUDA_CHECK(cudaGetLastError());
-      n = *ctx->readback(cnt.raw(), 8);
+      n = ctx->read_count_slot();
     } else {
       dev::PointsInRunsPolicy pol{s.pos(), s.n, po, ro, io};
       n = merge_select(ctx, p.pos(), p.n, e.pos(), e.n, pol, "points_in_runs");

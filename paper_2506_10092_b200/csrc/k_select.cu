@@ -327,12 +327,11 @@ int64_t run_select(const CtxPtr& ctx, int64_t n, const Policy& pol) {
   const int64_t ntiles = (n + STILE - 1) / STILE;
   dev::LookBack lb{nullptr, ctx->next_epoch(ntiles)};
   lb.status = ctx->tile_status;
-  DArr cnt = alloc_arr(ctx, RQ_I64, 1);
   dev::k_select<SB, SI, Policy><<<static_cast<unsigned>(ntiles), SB, 0, ctx->stream>>>(
-      n, pol, lb, cnt.as<int64_t>());
+      n, pol, lb, ctx->count_slot_dev());
   ctx->count_launch();
   RQ_CUDA_CHECK(cudaGetLastError());
-  return *ctx->readback(cnt.raw(), 8);
+  return ctx->read_count_slot();
 }
 
 void set_len(DArr& a, int64_t n) {

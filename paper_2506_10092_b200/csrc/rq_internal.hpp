@@ -99,6 +99,13 @@ struct Ctx {
   };
   std::vector<std::pair<std::string, KStat>> kstats;
   cudaEvent_t get_event();
+  // A size a select kernel writes straight into mapped pinned memory (one
+  // slot, read right after the sync that follows the launch): no D2H copy.
+  int64_t* count_slot_dev() const { return reinterpret_cast<int64_t*>(static_cast<char*>(result_dev) + 2048); }
+  int64_t read_count_slot() {
+    wait_stream();
+    return *reinterpret_cast<volatile int64_t*>(static_cast<char*>(result_host) + 2048);
+  }
   void wait_stream();
   void collect_profile();
 
