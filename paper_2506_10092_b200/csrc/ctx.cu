@@ -146,14 +146,8 @@ void Ctx::wait_stream() {
   }
   const auto t0 = std::chrono::steady_clock::now();
   RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
-  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  for (auto& kv : kstats)
-    if (kv.first == "host_sync_wait") {
-      kv.second.ms += ms;
-      kv.second.count += 1;
-      return;
-    }
-  kstats.push_back({"host_sync_wait", KStat{ms, 1}});
+  add_host_stat("host_sync_wait",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
 }
 
 void Ctx::sync() { wait_stream(); }

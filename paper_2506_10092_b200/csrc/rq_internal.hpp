@@ -12,7 +12,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -106,6 +108,16 @@ struct Ctx {
     wait_stream();
     return *reinterpret_cast<volatile int64_t*>(static_cast<char*>(result_host) + 2048);
   }
+  bool host_profiling = std::getenv("RQ_HOST_PROFILE") != nullptr;
+  void add_host_stat(const std::string& tag, double ms) {
+    for (auto& kv : kstats)
+      if (kv.first == tag) {
+        kv.second.ms += ms;
+        kv.second.count += 1;
+        return;
+      }
+    kstats.push_back({tag, KStat{ms, 1}});
+  }
   void wait_stream();
   void collect_profile();
 
@@ -133,10 +145,12 @@ struct KTimer {
   Ctx* c;
   const char* tag;
   cudaEvent_t a = nullptr;
+  std::chrono::steady_clock::time_point h0;
   KTimer(const CtxPtr& ctx, const char* t) : c(ctx.get()), tag(t) {
     if (c->profiling) {
       a = c->get_event();
       cudaEventRecord(a, c->stream);
+      if (c->host_profiling) h0 = std::chrono::steady_clock::now();
     }
   }
   ~KTimer() {
@@ -144,6 +158,9 @@ struct KTimer {
       cudaEvent_t b = c->get_event();
       cudaEventRecord(b, c->stream);
       c->pending.push_back({tag, a, b});
+      if (c->host_profiling)  // host wall time of the region (RQ_HOST_PROFILE=1)
+        c->add_host_stat(std::string("host:") + tag,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
     }
   }
 };
