@@ -180,6 +180,15 @@ int rq_arr_free(rq_arr_t a);
 int rq_col_upload(rq_ctx_t ctx, const rq_host_column* h, rq_col_t* out);
 int rq_col_describe(rq_col_t c, rq_host_column* h);
 int rq_col_download(rq_ctx_t ctx, rq_col_t c, rq_host_column* h);
+
+/* Column images — the reference's dump_column format (column.cpp:513-563:
+ * one JSON header line, then the arrays back to back) as the shard on-disk /
+ * wire format. rq_col_dump_image returns a malloc'd image (free with
+ * rq_image_free); rq_col_load_image uploads an image's sections straight to
+ * the device. Errors: RQ_INVALID for a malformed or truncated image. */
+int rq_col_dump_image(rq_ctx_t ctx, rq_col_t c, void** image, int64_t* nbytes);
+int rq_col_load_image(rq_ctx_t ctx, const void* image, int64_t nbytes, rq_col_t* out);
+void rq_image_free(void* image);
 int rq_col_free(rq_col_t c);
 int rq_col_encoding(rq_col_t c);
 int64_t rq_col_total_size(rq_col_t c);

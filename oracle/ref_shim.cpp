@@ -3,6 +3,7 @@
 // in place by oracle/Makefile). Converts host column images to runq::Column,
 // calls the reference operator API, converts results back. Nothing here is
 // on the product path; see ref_shim.h.
+#include <sstream>
 #include "ref_shim.h"
 
 #include <chrono>
@@ -256,6 +257,18 @@ void ref_free_mask(rq_host_mask* m) {
 void ref_free_array(ref_host_array* a) {
   std::free(a->data);
   std::memset(a, 0, sizeof(*a));
+}
+
+// runq::dump_column (column.cpp:513-563): the column image as bytes
+int ref_dump_column(const rq_host_column* a, ref_host_array* out) {
+  return guarded([&] {
+    std::ostringstream os;
+    dump_column(to_column(a), os);
+    const std::string b = os.str();
+    out->dtype = 0;
+    out->n = static_cast<int64_t>(b.size());
+    out->data = dup_bytes(b.data(), b.size());
+  });
 }
 
 int ref_roundtrip(const rq_host_column* a, rq_host_column* out) {

@@ -31,6 +31,7 @@ void ref_free_mask(rq_host_mask* m);
 void ref_free_array(ref_host_array* a);
 
 /* round trip through runq::Column (validation of the image conversion) */
+int ref_dump_column(const rq_host_column* a, ref_host_array* out);
 int ref_roundtrip(const rq_host_column* a, rq_host_column* out);
 /* runq::validate (column.cpp:178-216): number of violations */
 int ref_validate(const rq_host_column* a);

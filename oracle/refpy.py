@@ -244,6 +244,16 @@ class Ref:
         self._check(self.lib.ref_decode_values(C.byref(img), C.byref(o)))
         return self._arr(o)
 
+    def dump_column(self, c) -> bytes:
+        """runq::dump_column (column.cpp:513-563): JSON header line + raw arrays."""
+        img, keep = H.column_image(c)
+        o = RefHostArray()
+        self._check(self.lib.ref_dump_column(C.byref(img), C.byref(o)))
+        try:
+            return C.string_at(o.data, o.n) if o.n else b""
+        finally:
+            self.lib.ref_free_array(C.byref(o))
+
     def normalize_basic(self, c):
         img, keep = H.column_image(c)
         out = H.HostColumn()

@@ -41,6 +41,9 @@ PROTOTYPES = {
     "rq_col_upload": (C.c_int, [vp, P(HostColumn), P(vp)]),
     "rq_col_describe": (C.c_int, [vp, P(HostColumn)]),
     "rq_col_download": (C.c_int, [vp, vp, P(HostColumn)]),
+    "rq_col_dump_image": (C.c_int, [vp, vp, P(vp), P(C.c_int64)]),
+    "rq_col_load_image": (C.c_int, [vp, vp, C.c_int64, P(vp)]),
+    "rq_image_free": (None, [vp]),
     "rq_col_free": (C.c_int, [vp]),
     "rq_col_encoding": (C.c_int, [vp]),
     "rq_col_total_size": (i64, [vp]),

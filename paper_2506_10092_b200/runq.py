@@ -191,6 +191,26 @@ def upload(x, ctx: Context = None):
     return DeviceColumn(h, ctx)
 
 
+def dump_image(col, ctx: Context = None) -> bytes:
+    """rq_col_dump_image: the column's dump_column image (column.cpp:513-563)."""
+    d = upload(col, ctx)
+    p, n = C.c_void_p(), C.c_int64()
+    check(_L.rq_col_dump_image(d.ctx.handle, d.handle, C.byref(p), C.byref(n)))
+    try:
+        return C.string_at(p, n.value)
+    finally:
+        _L.rq_image_free(p)
+
+
+def load_image(image: bytes, ctx: Context = None) -> DeviceColumn:
+    """rq_col_load_image: a dump_column image -> device column."""
+    ctx = _ctx(ctx)
+    h = C.c_void_p()
+    buf = C.create_string_buffer(bytes(image), len(image))
+    check(_L.rq_col_load_image(ctx.handle, buf, len(image), C.byref(h)))
+    return DeviceColumn(h, ctx)
+
+
 def _is_host(*xs) -> bool:
     return any(not isinstance(x, (DeviceColumn, DeviceMask, DeviceArray)) for x in xs)
 

@@ -166,3 +166,21 @@ def test_ref_ingest_golden(ref, case):
         assert_column(ref.plain_to_rle(col(i["a"])), col(x["col"]))
     else:
         assert_column(ref.plain_to_rle_index(col(i["a"]), i["min_run"]), col(x["col"]))
+
+
+def test_reference_dump_column_example(ref):
+    """test_column.cpp:115-129: header fields and body length = stats bytes;
+    the checker the GPU image tests compare against."""
+    import json
+
+    import numpy as np
+
+    from paper_2506_10092_b200 import host as H
+    c = H.RleColumn(v=np.array([5, 6], dtype=np.int32), s=np.array([0, 4]), e=np.array([1, 6]), total_size=8)
+    img = ref.dump_column(c)
+    nl = img.index(b"\n")
+    hdr = json.loads(img[:nl])
+    assert hdr == {"encoding": "rle", "total_size": 8, "value_type": "i32",
+                   "widths": {"value": 4, "position": 8}, "runs": 2}
+    assert len(img) - nl - 1 == 2 * (4 + 16)
+    assert np.frombuffer(img[nl + 1:nl + 9], np.int32).tolist() == [5, 6]
