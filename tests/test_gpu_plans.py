@@ -172,3 +172,138 @@ def test_plan_errors_match_reference(rq, ref):
         dcat.run_plan(json.dumps(bad))
     with pytest.raises(RqError):
         dcat.run_plan(json.dumps({"node": "scan", "table": "nope"}))
+
+
+# ---- random plans: predicate trees x keys x expression aggregates ------------------
+
+NUM_COLS = ["l_quantity", "l_extendedprice", "l_discount", "l_tax"]
+
+
+def _rand_cmp(rng):
+    c = str(rng.choice(NUM_COLS + ["l_shipdate", "l_returnflag", "l_linestatus", "l_shipmode"]))
+    o = str(rng.choice(["<", "<=", "==", "!=", ">=", ">"]))
+    if c == "l_shipdate":
+        v = lit(f"199{int(rng.integers(2, 9))}-0{int(rng.integers(1, 10))}-1{int(rng.integers(0, 10))}")
+    elif c == "l_returnflag":
+        v = lit(str(rng.choice(RF + ["Z"])))  # absent strings resolve to code -1
+    elif c == "l_linestatus":
+        v = lit(str(rng.choice(LS)))
+    elif c == "l_shipmode":
+        v = lit(str(rng.choice(MODES_L)))
+    elif c == "l_extendedprice":
+        v = lit(float(rng.uniform(900, 100000)))
+    else:
+        v = lit(int(rng.integers(0, 51)))
+    return op(o, v, col(c)) if rng.random() < 0.2 else op(o, col(c), v)
+
+
+def _rand_pred(rng, depth):
+    r = rng.random()
+    if depth == 0 or r < 0.4:
+        return _rand_cmp(rng)
+    if r < 0.55:
+        return {"op": "not", "arg": _rand_pred(rng, depth - 1)}
+    return op(str(rng.choice(["and", "or"])), _rand_pred(rng, depth - 1), _rand_pred(rng, depth - 1))
+
+
+def _rand_expr(rng, depth=2):
+    r = rng.random()
+    if depth == 0 or r < 0.35:
+        return col(str(rng.choice(NUM_COLS)))
+    if r < 0.6:
+        k = lit(int(rng.integers(1, 100))) if rng.random() < 0.6 else lit(float(rng.uniform(0.5, 3.0)))
+        o = str(rng.choice(["+", "-", "*"]))
+        return op(o, k, _rand_expr(rng, depth - 1)) if rng.random() < 0.3 else op(o, _rand_expr(rng, depth - 1), k)
+    if r < 0.7:
+        return op("/", _rand_expr(rng, depth - 1), lit(float(rng.uniform(0.5, 4.0))))
+    return op(str(rng.choice(["+", "-", "*"])), _rand_expr(rng, depth - 1), _rand_expr(rng, depth - 1))
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_random_plans_vs_reference(rq, ref, seed):
+    """Random filter trees (and / or / not over every column kind, reversed
+    literals, absent dictionary strings), random key sets and random
+    expression aggregates: the device runner (fused or chain, whichever the
+    plan takes) against the reference runner."""
+    from oracle.refpy import RefCatalog
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(2_000, 60_000))
+    t, orders, modes = _tables(n, 500 + seed)
+    keys = [k for k in ("l_returnflag", "l_linestatus", "l_shipmode") if rng.random() < 0.35]
+    aggs = [agg("count", "n")]
+    for i in range(int(rng.integers(1, 5))):
+        aggs.append(agg(str(rng.choice(["sum", "avg", "min", "max"])), f"a{i}", _rand_expr(rng)))
+    plan = {"node": "group_agg", "aggs": aggs,
+            "input": {"node": "filter", "pred": _rand_pred(rng, 3), "input": scan("lineitem")}}
+    if keys:
+        plan["keys"] = keys
+    dcat, rcat = rq.Catalog(), RefCatalog(ref)
+    _fill(dcat, t, orders, modes)
+    _fill(rcat, t, orders, modes)
+    text = json.dumps({"plan": plan})
+    got, rows, fused = dcat.run_plan(text)
+    want = rcat.run_plan(text)
+    assert list(got) == list(want), (list(got), list(want))
+    g, w = _canon(got), _canon(want)
+    for c in want:
+        a, b = g[c], w[c]
+        assert len(a) == len(b), f"{c}: {len(a)} rows != {len(b)} ({text})"
+        if np.issubdtype(b.dtype, np.floating) or np.issubdtype(a.dtype, np.floating):
+            a, b = a.astype(np.float64), b.astype(np.float64)
+            tol = 1e-9 * np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+            with np.errstate(invalid="ignore"):  # equal infinities (empty MIN / MAX sentinels) subtract to NaN
+                ok = (a == b) | (np.abs(a - b) <= tol) | (np.isnan(a) & np.isnan(b))
+            assert np.all(ok), f"{c}: {text}"
+        else:
+            assert np.array_equal(a.astype(np.int64), b.astype(np.int64)), f"{c}: {text}"
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_join_plans_vs_reference(rq, ref, seed):
+    """Random filtered inner / semi joins (lineitem ⋈ orders on the key,
+    lineitem ⋉ modes across differently ordered dictionaries) under random
+    keys and aggregates, against the reference runner."""
+    from oracle.refpy import RefCatalog
+    rng = np.random.default_rng(4000 + seed)
+    n = int(rng.integers(2_000, 40_000))
+    t, orders, modes = _tables(n, 700 + seed)
+    left = {"node": "filter", "pred": _rand_pred(rng, 2), "input": scan("lineitem")}
+    if rng.random() < 0.5:
+        j = {"node": "join", "on": {"left": "l_orderkey", "right": "o_orderkey"}, "left": left,
+             "right": scan("orders")}
+        keys = ["o_orderpriority"] if rng.random() < 0.6 else []
+        pool = NUM_COLS + ["o_totalprice"]
+    else:
+        j = {"node": "join", "kind": "semi", "on": {"left": "l_shipmode", "right": "m_mode"}, "left": left,
+             "right": {"node": "filter", "pred": op(">", col("m_weight"), lit(int(rng.integers(0, 6)))),
+                       "input": scan("modes")}}
+        keys = ["l_shipmode"] if rng.random() < 0.6 else []
+        pool = NUM_COLS
+    aggs = [agg("count", "n")]
+    for i in range(int(rng.integers(1, 4))):
+        e = col(str(rng.choice(pool)))
+        if rng.random() < 0.5:
+            e = op(str(rng.choice(["+", "*", "-"])), e, lit(int(rng.integers(1, 9))))
+        aggs.append(agg(str(rng.choice(["sum", "avg", "min", "max"])), f"a{i}", e))
+    plan = {"node": "group_agg", "aggs": aggs, "input": j}
+    if keys:
+        plan["keys"] = keys
+    dcat, rcat = rq.Catalog(), RefCatalog(ref)
+    _fill(dcat, t, orders, modes)
+    _fill(rcat, t, orders, modes)
+    text = json.dumps({"plan": plan})
+    got, rows, fused = dcat.run_plan(text)
+    want = rcat.run_plan(text)
+    assert list(got) == list(want), (list(got), list(want))
+    g, w = _canon(got), _canon(want)
+    for c in want:
+        a, b = g[c], w[c]
+        assert len(a) == len(b), f"{c}: {len(a)} rows != {len(b)} ({text})"
+        if np.issubdtype(b.dtype, np.floating) or np.issubdtype(a.dtype, np.floating):
+            a, b = a.astype(np.float64), b.astype(np.float64)
+            tol = 1e-9 * np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+            with np.errstate(invalid="ignore"):
+                ok = (a == b) | (np.abs(a - b) <= tol) | (np.isnan(a) & np.isnan(b))
+            assert np.all(ok), f"{c}: {text}"
+        else:
+            assert np.array_equal(a.astype(np.int64), b.astype(np.int64)), f"{c}: {text}"

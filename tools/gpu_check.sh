@@ -15,4 +15,5 @@ for w in $WL; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $OUT/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_c2.log 2>&1
+for w in c2 c1 c3 q6 q1 c5; do timeout 300 python tools/host_breakdown.py $w 10 2>/dev/null | head -1; done > $OUT/host_split.txt
 echo done
