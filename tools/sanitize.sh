@@ -20,6 +20,13 @@ bl = H.PlainColumn(np.random.default_rng(1).integers(0, 5000, 3000).astype(np.in
 m = runq.joins.semi_join_mask(p, bl)
 l, r, card = runq.joins.get_join_index(p, bl)
 print("join", card)
+k, x, y, z, w = G.c3_tables(2_000_000, 4)
+ks, vs, ng = runq.agg.group_aggregate([k], [x, k, z, y, w], G.C3_FNS, normalize=True)
+print("c3", ng)
+h5 = Q.production_table(400_000, 5)
+print("c5", Q.c5_fused(runq, h5)[0] if isinstance(Q.c5_fused(runq, h5), tuple) else Q.c5_fused(runq, h5))
+img = runq.dump_image(x)
+print("image", len(img), runq.load_image(img).download().total_size)
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool python /tmp/san_run.py > gpurun_out/san_$tool.log 2>&1
