@@ -192,6 +192,16 @@ void gen_load(std::ostringstream& o, int c, const dev::PlainSrc& s) {
   }
 }
 
+// windows ahead the row loop prefetches into L2 (RQ_JIT_PF, default 1; 0 = off;
+// Q1 row kernel 1.20 -> 1.12 ms at 1, 1.14 at 2, 1.17 at 4)
+int prefetch_distance() {
+  static const int pf = [] {
+    const char* e = std::getenv("RQ_JIT_PF");
+    return e ? std::atoi(e) : 1;
+  }();
+  return pf;
+}
+
 // the source of a plan's kernel; literal slots are appended to ki / kf
 std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf) {
   std::ostringstream o;
@@ -225,8 +235,23 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
   }
   o << "      const i64 r0 = s + (c - off);\n"
        "      const i64 r1 = min(e, s + (c1_ - off) - 1);\n"
-       "      for (i64 b = r0 & ~(i64)" << (ROWS - 1) << "; b <= r1; b += " << 32 * ROWS << ") {\n"
-       "        const i64 row = b + lane * " << ROWS << ";\n"
+       "      for (i64 b = r0 & ~(i64)" << (ROWS - 1) << "; b <= r1; b += " << 32 * ROWS << ") {\n";
+  // L2 prefetch of the window PF windows ahead, one 128-B line per lane and
+  // column: more bytes in flight per warp without holding them in registers
+  const int pf = prefetch_distance();
+  if (pf > 0 && P.nc > 0) {
+    o << "        { const i64 pb = b + " << pf * 32 * ROWS << ";\n"
+         "          if (pb <= r1) {\n"
+         "            const i64 pe = min(r1 + 1, pb + " << 32 * ROWS << ");\n";
+    for (int c = 0; c < P.nc; ++c) {
+      const int w = dt_width(P.col[c].dt);
+      o << "            { const i64 lo = (pb * " << w << ") & ~(i64)127, a = lo + (i64)lane * 128;\n"
+           "              if (a < pe * " << w << ") asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"((const char*)c" << c
+        << ".v + a)); }\n";
+    }
+    o << "          }\n        }\n";
+  }
+  o << "        const i64 row = b + lane * " << ROWS << ";\n"
        "        if (row > r1) continue;\n";
   // loads
   std::ostringstream ld;
@@ -395,6 +420,7 @@ std::string plan_signature(const dev::XgPlan& P, int minb) {
   std::string sig;
   auto put = [&](int64_t v) { sig += std::to_string(v); sig += ','; };
   put(minb);
+  put(prefetch_distance());
   put(P.nc);
   for (int c = 0; c < P.nc; ++c) {
     put(P.col[c].dt);
