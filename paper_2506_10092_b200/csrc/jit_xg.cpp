@@ -203,7 +203,7 @@ int prefetch_distance() {
 }
 
 // the source of a plan's kernel; literal slots are appended to ki / kf
-std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf) {
+std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf, int pf) {
   std::ostringstream o;
   o << kPrelude;
   const char* mb = std::getenv("RQ_JIT_MINB");  // tuning knob: min resident CTAs per SM
@@ -238,7 +238,6 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
        "      for (i64 b = r0 & ~(i64)" << (ROWS - 1) << "; b <= r1; b += " << 32 * ROWS << ") {\n";
   // L2 prefetch of the window PF windows ahead, one 128-B line per lane and
   // column: more bytes in flight per warp without holding them in registers
-  const int pf = prefetch_distance();
   if (pf > 0 && P.nc > 0) {
     o << "        { const i64 pb = b + " << pf * 32 * ROWS << ";\n"
          "          if (pb <= r1) {\n"
@@ -416,11 +415,11 @@ bool xg_jit_available() { return nvrtc().ok; }
 // (NVRTC missing, too many literals, compile failure).
 // Compact structural signature of a plan (what the generated source depends
 // on): the source is built only on a cache miss.
-std::string plan_signature(const dev::XgPlan& P, int minb) {
+std::string plan_signature(const dev::XgPlan& P, int minb, int pf) {
   std::string sig;
   auto put = [&](int64_t v) { sig += std::to_string(v); sig += ','; };
   put(minb);
-  put(prefetch_distance());
+  put(pf);
   put(P.nc);
   for (int c = 0; c < P.nc; ++c) {
     put(P.col[c].dt);
@@ -469,7 +468,10 @@ bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S
   plan_literals(P, ki, kf);
   if (ki.size() > 24 || kf.size() > 24) return false;
   const char* mb = std::getenv("RQ_JIT_MINB");
-  const std::string sig = plan_signature(P, mb ? std::atoi(mb) : 3);
+  // the L2 prefetch pays on long segments (Q1: 1.20 -> 1.12 ms, C3's row pass
+  // -4%) and costs on plans of many short selected segments (Q6: +20%)
+  const int pf = S.n > 0 && S.ncov / S.n >= 2048 ? prefetch_distance() : 0;
+  const std::string sig = plan_signature(P, mb ? std::atoi(mb) : 3, pf);
   cudaKernel_t k = nullptr;
   {
     static std::mutex mu;
@@ -481,7 +483,7 @@ bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S
     } else {
       std::vector<int64_t> ki2;
       std::vector<double> kf2;
-      k = compile(gen_source(P, ki2, kf2));
+      k = compile(gen_source(P, ki2, kf2, pf));
       by_sig[sig] = k;  // nullptr too: a failed compilation is not retried
     }
   }
