@@ -663,17 +663,6 @@ __global__ void __launch_bounds__(BLOCK, 4)
           bulk_g2s(wC, c.e + c_lo16, bc, &full[st]);
           bulk_g2s(wCv, static_cast<const unsigned char*>(c.v) + c_lo16 * wc, bcv, &full[st]);
         }
-        // the consumers gather A's values at the window's runs and B's values
-        // at the tile's points straight from global memory: stage both in L2
-        if (ba && (reinterpret_cast<uintptr_t>(x.v) & 15) == 0)
-          bulk_prefetch_l2(static_cast<const unsigned char*>(x.v) + a_lo16 * dt_width_dev(x.dt),
-                                 static_cast<uint32_t>(a_bulk) * static_cast<uint32_t>(dt_width_dev(x.dt)));
-        {
-          const int64_t tb = t * TILE;
-          const int64_t nbv = (min(static_cast<int64_t>(TILE), np - tb) * dt_width_dev(ydt)) & ~int64_t(15);
-          if (nbv > 0)
-            bulk_prefetch_l2(static_cast<const unsigned char*>(yv) + tb * dt_width_dev(ydt), static_cast<uint32_t>(nbv));
-        }
       }
       __syncwarp();
     }
