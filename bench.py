@@ -482,13 +482,10 @@ WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "q6": Q6, "q1": Q1, "c5": C5}
 
 
 def shard_map(host, nshards):
-    from paper_2506_10092_b200.runq import shard_host_column
-    out = {}
-    for k, col in host.items():
-        n = col.total_size
-        cuts = [n * i // nshards for i in range(nshards + 1)]
-        out[k] = [shard_host_column(col, lo, hi) for lo, hi in zip(cuts[:-1], cuts[1:])]
-    return out
+    # numpy slicer from the oracle side: the reference / cpu_baseline legs
+    # never load the product library
+    from oracle.refpy import shard_map as np_shard_map
+    return np_shard_map(host, nshards)
 
 
 def config_dict(args, w, rows):
@@ -521,6 +518,10 @@ def run_reference(args, w, rank, world):
     ms = 1000.0 * statistics.median(times)
     value = rows / (ms / 1000.0)
     cores = threads if nshards > 1 else 1
+    # this arm runs only the reference library: the product must not be mapped
+    with open("/proc/self/maps") as f:
+        product_loaded = "librunq_b200" in f.read()
+    assert not product_loaded, "reference arm loaded the product library"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -530,6 +531,7 @@ def run_reference(args, w, rank, world):
                          "sample": f"{rows}-row table as {nshards} row-range shard(s) on {cores} thread(s); "
                                    "the reference operator chain per shard (oracle/_ref)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_library_loaded": product_loaded,
     }
     print(json.dumps(line), flush=True)
 
@@ -736,7 +738,8 @@ def main():
         ref = refpy.Ref()
         sample_rows = min(rows, {"c3": 5_000_000, "q6": 60_000_000, "q1": 2_000_000,
                                  "c5": 20_000_000}.get(w.name, 200_000_000))
-        sample = shard_map({k: runq.shard_host_column(v, 0, sample_rows) for k, v in host.items()}, 1)
+        from oracle.refpy import shard_column
+        sample = shard_map({k: shard_column(v, 0, sample_rows) for k, v in host.items()}, 1)
         secs = []
         for _ in range(3):
             _, s = w.ref_run(ref, sample, 1)

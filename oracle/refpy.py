@@ -618,3 +618,54 @@ class Orq:
     def sum_f64(self, x) -> float:
         x = np.ascontiguousarray(np.asarray(x, np.float64))
         return float(self.lib.orq_sum_f64(self._ptr(x), C.c_int64(len(x))))
+
+
+# ---------------------------------------------------------------------------
+# row-range shard slicing for the reference arm (numpy only: the reference
+# and cpu_baseline legs never load the product library)
+# ---------------------------------------------------------------------------
+
+
+def _slice_points(v, p, lo, hi):
+    a, b = np.searchsorted(p, lo, "left"), np.searchsorted(p, hi, "left")
+    return v[a:b].copy(), (p[a:b] - lo).astype(np.int64)
+
+
+def _slice_runs(v, s, e, lo, hi):
+    # runs overlapping [lo, hi): first run whose end >= lo, last whose start < hi;
+    # runs crossing a cut are clipped (value duplicated), positions rebased
+    a, b = np.searchsorted(e, lo, "left"), np.searchsorted(s, hi, "left")
+    ss = np.maximum(s[a:b], lo) - lo
+    ee = np.minimum(e[a:b], hi - 1) - lo
+    return v[a:b].copy(), ss.astype(np.int64), ee.astype(np.int64)
+
+
+def shard_column(col, lo: int, hi: int):
+    """Rows [lo, hi) of a host column image as a standalone shard (same
+    result as the product's rq_shard_host_column; tests/test_oracle_cpu.py
+    checks the two agree)."""
+    if isinstance(col, H.PlainColumn):
+        return H.PlainColumn(col.values[lo:hi].copy(), col.logical, col.center)
+    if isinstance(col, H.PlainPlusIndexColumn):
+        v, p = _slice_points(col.outliers.v, col.outliers.p, lo, hi)
+        return H.PlainPlusIndexColumn(shard_column(col.base, lo, hi), H.IndexColumn(v, p, hi - lo))
+    if isinstance(col, H.RleColumn):
+        s = col.s if col.s is not None else np.concatenate([[0], col.e[:-1] + 1]).astype(np.int64)
+        v, ss, ee = _slice_runs(col.v, s, col.e, lo, hi)
+        return H.RleColumn(v, ss, ee, hi - lo)
+    if isinstance(col, H.IndexColumn):
+        v, p = _slice_points(col.v, col.p, lo, hi)
+        return H.IndexColumn(v, p, hi - lo)
+    if isinstance(col, H.RlePlusIndexColumn):
+        return H.RlePlusIndexColumn(shard_column(col.runs, lo, hi), shard_column(col.points, lo, hi))
+    raise TypeError(type(col))
+
+
+def shard_map(host: dict, nshards: int) -> dict:
+    """Every column cut into `nshards` equal row ranges."""
+    out = {}
+    for k, col in host.items():
+        n = col.total_size
+        cuts = [n * i // nshards for i in range(nshards + 1)]
+        out[k] = [shard_column(col, lo, hi) for lo, hi in zip(cuts[:-1], cuts[1:])]
+    return out

@@ -2,11 +2,30 @@
 // ctx.cu — context, stream-ordered allocation, device arrays, column/mask
 // upload/download and the handle half of the C ABI (include/runq_b200.h).
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "rq_internal.hpp"
 
 namespace rqb {
+
+int kernel_occupancy(int device, const void* fn, int block, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(fn, device, block, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024)
+    RQ_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  RQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem));
+  if (occ < 1) occ = 1;
+  cache.emplace(key, occ);
+  return occ;
+}
+
 
 namespace {
 thread_local std::string g_last_error;

@@ -112,7 +112,11 @@ __device__ __forceinline__ u64 wsum_u(u64 x) {
 
 std::string ty(int f) { return f ? "double" : "i64"; }
 
-std::string binop(const std::string& a, int fa, const std::string& b, int fb, int op) {
+// `ok`: the row-in-[r0, r1] test of the row being evaluated; integer division
+// divides the other rows of the window by 1 so a zero divisor there (a row the
+// WHERE dropped, a neighbouring segment, padding) cannot raise (the reference
+// divides only the filtered rows, align.cpp:290-305)
+std::string binop(const std::string& a, int fa, const std::string& b, int fb, int op, const std::string& ok) {
   if (fa || fb) {
     const char* o = op == RQ_ADD ? "+" : op == RQ_SUB ? "-" : op == RQ_MUL ? "*" : "/";
     return "((double)(" + a + ") " + o + " (double)(" + b + "))";
@@ -121,7 +125,7 @@ std::string binop(const std::string& a, int fa, const std::string& b, int fb, in
     case RQ_ADD: return "wadd(" + a + ", " + b + ")";
     case RQ_SUB: return "wsub(" + a + ", " + b + ")";
     case RQ_MUL: return "wmul(" + a + ", " + b + ")";
-    default: return "idiv(" + a + ", " + b + ", &lerr)";
+    default: return "idiv(" + a + ", (" + ok + ") ? (" + b + ") : (i64)1, &lerr)";
   }
 }
 
@@ -275,6 +279,7 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
     const dev::XgExpr& X = P.e[e];
     if (!X.rows) continue;
     for (int u = 0; u < ROWS; ++u) {
+      const std::string ok = "row + " + std::to_string(u) + " >= r0 && row + " + std::to_string(u) + " <= r1";
       std::string v;
       int vf = 0;
       for (int t = 0; t < X.nt; ++t) {
@@ -284,14 +289,14 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
         int xf = T.flt;
         if (T.sop >= 0) {
           const std::string& k = lits[static_cast<size_t>(e)][static_cast<size_t>(t)];
-          x = T.rev ? binop(k, T.kflt, x, xf, T.sop) : binop(x, xf, k, T.kflt, T.sop);
+          x = T.rev ? binop(k, T.kflt, x, xf, T.sop, ok) : binop(x, xf, k, T.kflt, T.sop, ok);
           xf = xf || T.kflt;
         }
         if (t == 0) {
           v = x;
           vf = xf;
         } else {
-          v = binop(v, vf, x, xf, X.op[t - 1]);
+          v = binop(v, vf, x, xf, X.op[t - 1], ok);
           vf = vf || xf;
         }
       }

@@ -934,12 +934,7 @@ template <class C, class T, int OP, int KIND>
 void launch_pair_tma3(const CtxPtr& ctx, const DCol& A, const DCol& B, int swap, dev::AggPart* parts,
                       dev::AggPart* out, int ta, int64_t ntiles, int64_t& grid_out, bool dry) {
   auto k = dev::k_pair_reduce_tma<C::BLOCK, C::IA, C::BW, T, OP, KIND>;
-  static int occ = 0;
-  if (!occ) {
-    RQ_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
-    RQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::BLOCK, C::SMEM));
-    if (occ < 1) occ = 1;
-  }
+  const int occ = kernel_occupancy(ctx, k, C::BLOCK, C::SMEM);
   int64_t grid = static_cast<int64_t>(ctx->sm_count) * occ;
   if (grid > ntiles) grid = ntiles;
   grid_out = grid;

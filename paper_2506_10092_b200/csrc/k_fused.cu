@@ -884,16 +884,6 @@ struct TmaLaunch {
   int* err;
 };
 
-// CTAs resident per SM for an instantiation (queried once; sets the
-// dynamic shared-memory limit on first use)
-template <class K>
-int tma_occupancy(K kernel) {
-  RQ_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(TMA_SMEM)));
-  int occ = 0;
-  RQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, TB, TMA_SMEM));
-  return occ > 0 ? occ : 1;
-}
 
 template <class T, int OP, int CK>
 int64_t launch_tma3(const CtxPtr& ctx, const TmaLaunch& f, bool dry) {
@@ -901,9 +891,7 @@ int64_t launch_tma3(const CtxPtr& ctx, const TmaLaunch& f, bool dry) {
   const bool same = f.xs.dt == tdt && f.y->v.dt == tdt;
   auto k_same = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, true>;
   auto k_gen = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, false>;
-  static int occ_same = 0, occ_gen = 0;  // per instantiation
-  int& occ = same ? occ_same : occ_gen;
-  if (!occ) occ = tma_occupancy(same ? k_same : k_gen);
+  const int occ = kernel_occupancy(ctx, same ? k_same : k_gen, TB, TMA_SMEM);
   int64_t grid = static_cast<int64_t>(ctx->sm_count) * occ;
   if (grid > f.ntiles) grid = f.ntiles;
   if (dry) return grid;

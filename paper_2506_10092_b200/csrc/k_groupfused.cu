@@ -1009,7 +1009,13 @@ __device__ __forceinline__ void xg_flush(const XgPlan& P, unsigned long long* ta
 
 // v[u] = v[u] op x[u] for the lane's 4 rows; the type / operator dispatch
 // is uniform and hoisted out of the row loop
-__device__ __forceinline__ void xg_op4(uint64_t (&v)[4], int vf, const uint64_t (&x)[4], int xf, int op, int* err) {
+// Integer division only divides the rows that count (ok[u]: inside the
+// segment's [r0, r1]); the window's other rows (dropped by the WHERE, a
+// neighbouring segment, padding past the last covered row) divide by 1, so a
+// zero there cannot raise — the reference divides only the filtered rows
+// (align.cpp:290-305 after filter, :755-771).
+__device__ __forceinline__ void xg_op4(uint64_t (&v)[4], int vf, const uint64_t (&x)[4], int xf, int op, int* err,
+                                       const bool (&ok)[4]) {
   if (vf || xf) {
     double a[4], b[4];
 #pragma unroll
@@ -1053,7 +1059,8 @@ __device__ __forceinline__ void xg_op4(uint64_t (&v)[4], int vf, const uint64_t 
       default:
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          v[u] = static_cast<uint64_t>(arith_i64(static_cast<int64_t>(v[u]), static_cast<int64_t>(x[u]), RQ_DIV, err));
+          v[u] = static_cast<uint64_t>(
+              arith_i64(static_cast<int64_t>(v[u]), ok[u] ? static_cast<int64_t>(x[u]) : int64_t(1), RQ_DIV, err));
     }
   }
 }
@@ -1137,11 +1144,11 @@ __global__ void __launch_bounds__(BLOCK)
               const uint64_t kb = T.kflt ? static_cast<uint64_t>(__double_as_longlong(T.kf)) : static_cast<uint64_t>(T.ki);
               uint64_t kk[4] = {kb, kb, kb, kb};
               if (T.rev) {
-                xg_op4(kk, T.kflt, x, xf, T.sop, &lerr);
+                xg_op4(kk, T.kflt, x, xf, T.sop, &lerr, ok);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) x[u] = kk[u];
               } else {
-                xg_op4(x, xf, kk, T.kflt, T.sop, &lerr);
+                xg_op4(x, xf, kk, T.kflt, T.sop, &lerr, ok);
               }
               xf = xf || T.kflt;
             }
@@ -1150,7 +1157,7 @@ __global__ void __launch_bounds__(BLOCK)
               for (int u = 0; u < 4; ++u) v[u] = x[u];
               vf = xf;
             } else {
-              xg_op4(v, vf, x, xf, P.e[ei].op[ti - 1], &lerr);
+              xg_op4(v, vf, x, xf, P.e[ei].op[ti - 1], &lerr, ok);
               vf = vf || xf;
             }
           }
@@ -1702,12 +1709,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     const int64_t blocks = std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
                                              (ncov / chunk + (B / 32)) / (B / 32) + 1);
     constexpr size_t smem = dev::xg_rows_smem<B>();
-    static bool attr = false;
-    if (!attr) {
-      RQ_CUDA_CHECK(cudaFuncSetAttribute(dev::k_xg_rows<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-      attr = true;
-    }
+    kernel_occupancy(ctx, dev::k_xg_rows<B>, B, smem);  // shared-memory opt-in on this device
     KTimer rows_timer(ctx, "xg_rows");
     const char* nojit = std::getenv("RQ_NO_JIT");
     if ((nojit && nojit[0] == '1') ||
@@ -1834,9 +1836,19 @@ GroupAggOut xg_chain(const CtxPtr& ctx, const DMask* mask, const std::vector<con
 
 }  // namespace
 
+bool col_full_coverage(const CtxPtr& ctx, const DCol& c) {
+  switch (c.enc) {
+    case RQ_ENC_PLAIN:
+    case RQ_ENC_PLAIN_INDEX: return true;
+    case RQ_ENC_RLE: return col_gapless(ctx, c);
+    case RQ_ENC_INDEX: return c.p.n == c.total;
+    default: return false;
+  }
+}
+
 GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
                                   const std::vector<XExpr>& exprs, const std::vector<int>& fns, bool* fused,
-                                  const std::vector<XPred>* preds) {
+                                  const std::vector<XPred>* preds, bool fused_only) {
   require(exprs.size() == fns.size(), "group_aggregate_exprs: one function per expression");
   for (auto& x : exprs) {
     require(x.terms.size() <= 3 && x.ops.size() + 1 == std::max<size_t>(1, x.terms.size()),
@@ -1845,7 +1857,15 @@ GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const st
   }
   GroupAggOut out;
   const bool has_preds = preds && !preds->empty();
-  bool ok = xg_fused(ctx, mask, keys, exprs, fns, out, nullptr, has_preds ? preds : nullptr);
+  // Without keys the runner aggregates each expression over its own coverage
+  // (aggregate_all per column, runner.cpp:325-333); the fused pass shares one
+  // segment table across expressions, which is the same thing only when the
+  // operands' coverages cannot differ.
+  bool fusable = true;
+  if (keys.empty() && exprs.size() > 1)
+    for (auto& x : exprs)
+      for (auto& t : x.terms) fusable = fusable && col_full_coverage(ctx, *t.col);
+  bool ok = fusable && xg_fused(ctx, mask, keys, exprs, fns, out, nullptr, has_preds ? preds : nullptr);
   if (ok) {
     if (fused) *fused = true;
     return out;
@@ -1865,13 +1885,16 @@ GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const st
       built.reset(new DMask(built ? mask_and(ctx, *built, m) : m));
     }
     if (mask) built.reset(new DMask(mask_and(ctx, *built, *mask)));
-    ok = xg_fused(ctx, built.get(), keys, exprs, fns, out);
+    ok = fusable && xg_fused(ctx, built.get(), keys, exprs, fns, out);
     if (ok) {
       if (fused) *fused = true;
       return out;
     }
   }
   if (fused) *fused = false;
+  // probe-only callers (the plan executor) run their own generic path next:
+  // do not run the chain here too
+  if (fused_only) return GroupAggOut{};
   return xg_chain(ctx, built ? built.get() : mask, keys, exprs, fns);
 }
 

@@ -693,13 +693,25 @@ bool Exec::try_fused_group(const Node& n, CSet& out) {
   }
   std::vector<const DCol*> keys;
   for (const auto& k : n.keys) keys.push_back(in.at(k).col.get());
+  // The fused pass intersects one segment table with the coverage of every
+  // operand of every expression (and the WHERE). The runner instead
+  // (runner.cpp:302-336) aligns keys with all data jointly — including, for
+  // count(*), the scan's FIRST column (in.cols.front()) — and without keys
+  // aggregates each expression over its own coverage. The two agree when the
+  // columns whose coverage differs are full-coverage; otherwise take the
+  // runner's generic path (the no-key case is checked inside
+  // group_aggregate_exprs, which the C ABI shares).
+  bool has_count_star = false;
+  for (auto& x : exprs) has_count_star |= x.terms.empty();
   if (keys.empty()) {  // count(*) without keys needs a column for the row count
-    for (auto& x : exprs)
-      if (x.terms.empty()) return false;
+    if (has_count_star) return false;
+  } else if (has_count_star) {
+    if (in.cols.empty() || !col_full_coverage(ctx, *in.cols.front().col)) return false;
   }
   bool was_fused = false;
-  GroupAggOut r = group_aggregate_exprs(ctx, nullptr, keys, exprs, fns, &was_fused, preds.empty() ? nullptr : &preds);
-  if (!was_fused) return false;  // same result either way; count it only when fused
+  GroupAggOut r = group_aggregate_exprs(ctx, nullptr, keys, exprs, fns, &was_fused, preds.empty() ? nullptr : &preds,
+                                        /*fused_only=*/true);
+  if (!was_fused) return false;  // the generic path runs next (same result); counted only when fused
   ++fused;
   out.rows = r.n_groups;
   for (size_t k = 0; k < n.keys.size(); ++k) {

@@ -139,6 +139,17 @@ struct Ctx {
 
 using CtxPtr = std::shared_ptr<Ctx>;
 
+// Resident CTAs per SM of `fn` at (block, smem) on `device`, setting the
+// dynamic shared-memory opt-in first when smem > 48 KB. The attribute applies
+// per device context, so it is set (and the occupancy cached) once per
+// (kernel, device, block, smem) — a process with contexts on several devices
+// opts in on each before its first launch there. Thread-safe.
+int kernel_occupancy(int device, const void* fn, int block, size_t smem);
+template <class K>
+int kernel_occupancy(const CtxPtr& ctx, K* fn, int block, size_t smem) {
+  return kernel_occupancy(ctx->device, reinterpret_cast<const void*>(fn), block, smem);
+}
+
 // Brackets the kernel launches issued in its scope with CUDA events on the
 // context stream when profiling is enabled (no-op otherwise).
 struct KTimer {
@@ -464,6 +475,8 @@ void hash_build_probe(const CtxPtr& ctx, const DArr& build_values, const DArr& p
 DCol apply_join_index(const CtxPtr& ctx, const DCol& col, const JoinSideD& j);
 int64_t mask_true_count(const CtxPtr& ctx, const DMask& m);
 bool col_gapless(const CtxPtr& ctx, const DCol& c);
+// every row of [0, total) covered (Plain / Plain+Index, gapless RLE, full Index)
+bool col_full_coverage(const CtxPtr& ctx, const DCol& c);
 
 struct GroupAggOut {
   int64_t n_groups = 0;
@@ -509,7 +522,8 @@ struct XPred {
 };
 GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
                                   const std::vector<XExpr>& exprs, const std::vector<int>& fns,
-                                  bool* fused = nullptr, const std::vector<XPred>* preds = nullptr);
+                                  bool* fused = nullptr, const std::vector<XPred>* preds = nullptr,
+                                  bool fused_only = false);
 bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
                            const std::vector<const DCol*>& data, const std::vector<int>& fns,
                            GroupAggOut& out);

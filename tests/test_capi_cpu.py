@@ -66,3 +66,24 @@ def test_shard_slicer_rebases_and_splits_runs():
             assert np.array_equal(p, wp) and np.array_equal(v, wv), (enc, lo, hi)
             total_rows += len(p)
         assert total_rows == len(H.column_rows(col)[0])
+
+
+def test_oracle_side_numpy_slicer_matches_product_slicer():
+    """bench.py's reference / cpu_baseline legs slice shards with the numpy
+    slicer in oracle/refpy.py (they must not load librunq_b200.so); it must
+    give exactly the product's rq_shard_host_column shards."""
+    from oracle.refpy import shard_column
+    from paper_2506_10092_b200.runq import shard_host_column
+    rng = np.random.default_rng(4)
+    for enc in (H.ENC_PLAIN, H.ENC_RLE, H.ENC_INDEX, H.ENC_PLAIN_INDEX, H.ENC_RLE_INDEX):
+        for rep in range(4):
+            col = G.random_column(rng, enc, 2000)
+            cuts = sorted({0, 2000, *rng.integers(0, 2001, 4).tolist()})
+            for lo, hi in zip(cuts[:-1], cuts[1:]):
+                a, b = shard_column(col, lo, hi), shard_host_column(col, lo, hi)
+                ia, ib = H.column_image(a)[0], H.column_image(b)[0]
+                assert type(a) is type(b) and a.total_size == b.total_size
+                pa, va = H.column_rows(a)
+                pb, vb = H.column_rows(b)
+                assert np.array_equal(pa, pb) and np.array_equal(va, vb), (enc, lo, hi)
+                assert ia.n == ib.n and ia.n2 == ib.n2, (enc, lo, hi)

@@ -226,3 +226,36 @@ def test_where_on_plain_column_falls_back_to_mask(rq, ref):
     assert ng == wng
     for g, w in zip(ks + vs, wk + wv):
         assert_array(g, w)
+
+
+@pytest.mark.parametrize("n", [1003, 77_777])
+def test_plain_divisor_zeros_only_on_dropped_rows(rq, ref, n, row_kernel):
+    """SUM(a / b) with a Plain i64 divisor that is 0 only on rows the WHERE
+    drops (and n % 8 != 0, so the last window has padding rows): the reference
+    filters first and divides only kept rows (align.cpp:290-305, :755-771), so
+    no error; a zero on a kept row still raises."""
+    rng = np.random.default_rng(n)
+    X = rq.X
+    k = _rle(rng, n, 97, 0, 3)
+    mcol = _rle(rng, n, 13, 0, 9)
+    keep = np.zeros(n, bool)
+    for s, e, v in zip(mcol.s, mcol.e, mcol.v):
+        keep[s:e + 1] = v < 5
+    bv = rng.integers(1, 50, n).astype(np.int64)
+    bv[~keep] = 0
+    a = H.PlainColumn(rng.integers(-1000, 1000, n).astype(np.int64))
+    b = H.PlainColumn(bv)
+    mask = rq.compute.compare_scalar(mcol, 5, "<")
+    hmask = ref.compare_scalar(mcol, 5, "<")
+    # a / b and the reversed scalar 1000 / b both divide by b = 0 on dropped rows
+    exprs = [X.col(a).arith(X.col(b), "/"), X.col(b).scalar(1000, "/", True), X.count()]
+    fns = ["sum", "sum", "count"]
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(mask, [k], exprs, fns)
+    assert fused
+    wk, wv, wng = _chain(ref, hmask, [k], exprs, fns)
+    assert ng == wng
+    for g, w in zip(ks + vs, wk + wv):
+        assert_array(g, w)
+    # no WHERE: the zeros are on counted rows now -> integer division by zero
+    with pytest.raises(RqError):
+        rq.agg.group_aggregate_exprs(None, [k], [X.col(a).arith(X.col(b), "/")], ["sum"])

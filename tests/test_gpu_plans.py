@@ -307,3 +307,60 @@ def test_random_join_plans_vs_reference(rq, ref, seed):
             assert np.all(ok), f"{c}: {text}"
         else:
             assert np.array_equal(a.astype(np.int64), b.astype(np.int64)), f"{c}: {text}"
+
+
+def _gapped_rle(rng, n, L, lo, hi):
+    e = np.cumsum(rng.integers(1, 2 * L, n // L + 2))
+    e = e[e < n - 1]
+    e = np.append(e, n - 1).astype(np.int64)
+    s = np.concatenate([[0], e[:-1] + 1]).astype(np.int64)
+    keep = rng.random(len(s)) > 0.35
+    return H.RleColumn(rng.integers(lo, hi + 1, int(keep.sum())).astype(np.int64), s[keep], e[keep], n)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_plan_coverage_rules_with_gapped_columns(rq, ref, seed):
+    """Catalog columns with gaps: the runner aligns keys with ALL data jointly
+    — for count(*) through the scan's first column — and aggregates each
+    expression over its own coverage when there are no keys
+    (runner.cpp:302-336). The fused pass must not be taken where its shared
+    segment table would differ (gapped first column, no-key
+    expressions over differently gapped columns)."""
+    from oracle.refpy import RefCatalog
+    rng = np.random.default_rng(seed)
+    n = 60_000
+    t = {"g1": _gapped_rle(rng, n, 300, 0, 50), "key": _gapped_rle(rng, n, 2000, 0, 4) if seed == 2 else
+         H.RleColumn(*_full_rle(rng, n, 2000, 0, 4), n),
+         "a": _gapped_rle(rng, n, 40, -20, 20), "b": _gapped_rle(rng, n, 70, 1, 9),
+         "p": H.PlainColumn(rng.integers(-100, 100, n).astype(np.int16), H.I64)}
+    plans = [
+        {"node": "group_agg", "keys": ["key"], "aggs": [agg("count", "n"), agg("sum", "s", col("p"))],
+         "input": scan("t")},
+        {"node": "group_agg", "aggs": [agg("sum", "sa", col("a")), agg("sum", "sb", col("b")),
+                                       agg("avg", "ap", col("p"))], "input": scan("t")},
+        {"node": "group_agg", "keys": ["key"], "aggs": [agg("count", "n"), agg("sum", "s", col("a"))],
+         "input": {"node": "filter", "pred": op("<", col("b"), lit(6)), "input": scan("t")}},
+    ]
+    dcat, rcat = rq.Catalog(), RefCatalog(ref)
+    for k, c in t.items():
+        dcat.add_column("t", k, c)
+        rcat.add_column("t", k, c)
+    for plan in plans:
+        text = json.dumps({"plan": plan})
+        got, rows, fused = dcat.run_plan(text)
+        want = rcat.run_plan(text)
+        g, w = _canon(got), _canon(want)
+        assert list(got) == list(want)
+        for c in want:
+            a, b = g[c].astype(np.float64), w[c].astype(np.float64)
+            assert len(a) == len(b), (plan, c)
+            tol = 1e-9 * np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+            assert np.all((np.abs(a - b) <= tol) | (np.isnan(a) & np.isnan(b))), (plan, c)
+
+
+def _full_rle(rng, n, L, lo, hi):
+    e = np.cumsum(rng.integers(1, 2 * L, n // L + 2))
+    e = e[e < n - 1]
+    e = np.append(e, n - 1).astype(np.int64)
+    s = np.concatenate([[0], e[:-1] + 1]).astype(np.int64)
+    return rng.integers(lo, hi + 1, len(s)).astype(np.int64), s, e
