@@ -164,6 +164,13 @@ int rq_ctx_profile_report(rq_ctx_t ctx, int32_t reset, char* buf, int64_t cap);
 /* ---------------------------------------------------------------------- */
 
 int rq_arr_upload(rq_ctx_t ctx, int32_t dtype, const void* host, int64_t n, rq_arr_t* out);
+/* Uninitialised device array of n elements, filled by rq_arr_write: a column
+ * larger than host RAM streams into HBM in row chunks (the reference builds
+ * columns in host memory only, array.hpp:16-99). */
+int rq_arr_alloc(rq_ctx_t ctx, int32_t dtype, int64_t n, rq_arr_t* out);
+/* Copies host[0, count) into elements [offset, offset + count) (stream-ordered;
+ * the host buffer must stay valid until the context synchronises). */
+int rq_arr_write(rq_ctx_t ctx, rq_arr_t a, int64_t offset, const void* host, int64_t count);
 /* Wraps caller-owned device memory without copying; caller keeps it alive. */
 int rq_arr_wrap_device(rq_ctx_t ctx, int32_t dtype, void* dev, int64_t n, rq_arr_t* out);
 int rq_arr_info(rq_arr_t a, int32_t* dtype, int64_t* n);
@@ -491,6 +498,60 @@ int rq_result_free(rq_result_t r);
  * with rq_host_column_free. */
 int rq_shard_host_column(const rq_host_column* in, int64_t lo, int64_t hi, rq_host_column* out);
 void rq_host_column_free(rq_host_column* h);
+
+/* Communicators. Every rank runs the single-GPU path on its
+ * row-range shard; the partial aggregates are combined with ONE collective
+ * on the context stream: a grouped ncclAllReduce of 8-byte partials for
+ * global aggregates, an ncclAllGather of fixed-capacity (key, partial)
+ * packets + a device regroup (keys ascending) for group tables. Integer
+ * SUM / COUNT combine by wrapping addition (bit-exact); f64 sums reassociate
+ * (1e-9 relative); AVG is recomputed from the merged SUM and COUNT;
+ * STD / VAR are rejected (RQ_INVALID: not exact under a merge). The result
+ * is identical on every rank. NCCL errors (incl. ncclCommGetAsyncError,
+ * polled after each merge) return RQ_NCCL. */
+typedef struct rq_comm_s* rq_comm_t;
+enum { RQ_COMM_NCCL = 0, RQ_COMM_HOST = 1 };
+/* host transport: gathers every rank's `bytes` from `send` into
+ * recv[rank * bytes ...] (same `bytes` on every rank); returns 0 on success */
+typedef int (*rq_host_allgather_fn)(const void* send, int64_t bytes, void* recv, void* user);
+
+/* ncclGetUniqueId into id[0..128) (rank 0 creates it, the launcher
+ * broadcasts it); NCCL is loaded on first use (libnccl.so.2). */
+int rq_comm_unique_id(void* id, int64_t cap);
+/* ncclCommInitRank on the context's device (one rank per GPU). */
+int rq_comm_init_nccl(rq_ctx_t ctx, const void* id, int32_t nranks, int32_t rank, rq_comm_t* out);
+/* Host transport (several ranks on one device, e.g. tests over gloo). */
+int rq_comm_init_host(rq_ctx_t ctx, int32_t nranks, int32_t rank, rq_host_allgather_fn fn, void* user,
+                      rq_comm_t* out);
+int rq_comm_info(rq_comm_t comm, int32_t* nranks, int32_t* rank, int32_t* transport);
+int rq_comm_destroy(rq_comm_t comm);
+
+/* Low level: merges per-rank partial tables (n_groups rows of n_keys key
+ * arrays + n_parts 8-byte partial arrays, part_fns in SUM/COUNT/MIN/MAX)
+ * into the global table: keys ascending, COUNT / SUM partials summed, MIN /
+ * MAX re-reduced. n_keys = 0: one row per rank, all-reduced. */
+int rq_merge_group_tables(rq_ctx_t ctx, rq_comm_t comm, const rq_arr_t* keys, int32_t n_keys,
+                          const rq_arr_t* parts, const int32_t* part_fns, int32_t n_parts, int64_t n_groups,
+                          int64_t* out_groups, rq_arr_t* out_keys, rq_arr_t* out_parts);
+
+/* The sharded forms of the entry points above: same arguments plus the
+ * communicator, called by every rank on its shard; outputs are the merged
+ * global result (on every rank). */
+int rq_aggregate_all_sharded(rq_ctx_t ctx, rq_comm_t comm, rq_col_t data, int32_t fn, int32_t* out_dtype,
+                             int64_t* out_i64, double* out_f64);
+int rq_aggregate_binop_sharded(rq_ctx_t ctx, rq_comm_t comm, rq_col_t a, rq_col_t b, int32_t op, int32_t fn,
+                               int32_t* out_dtype, int64_t* out_i64, double* out_f64);
+int rq_filtered_aggregate_binop_sharded(rq_ctx_t ctx, rq_comm_t comm, rq_col_t c, rq_scalar k, int32_t cmp,
+                                        rq_col_t a, rq_col_t b, int32_t op, int32_t fn, int32_t* out_dtype,
+                                        int64_t* out_i64, double* out_f64);
+/* normalized != 0: rq_group_aggregate_normalized semantics */
+int rq_group_aggregate_sharded(rq_ctx_t ctx, rq_comm_t comm, const rq_col_t* keys, int32_t n_keys,
+                               const rq_col_t* data, const int32_t* fns, int32_t n_data, int32_t normalized,
+                               int64_t* n_groups, rq_arr_t* out_keys, rq_arr_t* out_vals);
+int rq_group_aggregate_where_sharded(rq_ctx_t ctx, rq_comm_t comm, const rq_pred* where, int32_t n_where,
+                                     rq_mask_t mask, const rq_col_t* keys, int32_t n_keys, const rq_expr* exprs,
+                                     const int32_t* fns, int32_t n_exprs, int64_t* n_groups, rq_arr_t* out_keys,
+                                     rq_arr_t* out_vals, int32_t* fused);
 
 #ifdef __cplusplus
 }

@@ -305,3 +305,187 @@ double orq_sum_f64(const double* x, int64_t n) {
   }
   return sum + comp;
 }
+
+/* ---------------------------------------------------------------------------
+ * Streaming group-by restatement (see runq_oracle.h). Segments: disjoint
+ * ascending closed ranges, one group slot each.
+ * ------------------------------------------------------------------------- */
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <unistd.h>
+
+static void neumaier_add(double* sum, double* comp, double x) {
+  double t = *sum + x;
+  if (fabs(*sum) >= fabs(x)) *comp += (*sum - t) + x;
+  else *comp += (x - t) + *sum;
+  *sum = t;
+}
+
+/* groupby.cpp:82-89 with shape weights = fragment lengths (align.cpp:20-70). */
+void orq_seg_sum_runs_i64(const int64_t* ss, const int64_t* se, const int64_t* slot, int64_t nseg,
+                          const int64_t* v, const int64_t* s, const int64_t* e, int64_t nr,
+                          int64_t* out, int64_t* cnt) {
+  int64_t i = 0, j = 0;
+  while (i < nseg && j < nr) {
+    int64_t lo = ss[i] > s[j] ? ss[i] : s[j];
+    int64_t hi = se[i] < e[j] ? se[i] : e[j];
+    if (lo <= hi) {
+      int64_t len = hi - lo + 1;
+      out[slot[i]] = (int64_t)((uint64_t)out[slot[i]] + (uint64_t)v[j] * (uint64_t)len);
+      if (cnt) cnt[slot[i]] += len;
+    }
+    if (se[i] < e[j]) ++i;
+    else if (e[j] < se[i]) ++j;
+    else { ++i; ++j; }
+  }
+}
+
+/* Points of an Index / RLE+Index / Plain+Index part located in segments by a
+ * merge walk (idx_in_rle, primitives.cpp:48-61), weight 1 each. */
+void orq_seg_sum_points_i64(const int64_t* ss, const int64_t* se, const int64_t* slot,
+                            int64_t nseg, const int64_t* p, const int64_t* v, int64_t np,
+                            int64_t shadow, int64_t* out, int64_t* cnt) {
+  int64_t i = 0;
+  for (int64_t q = 0; q < np && i < nseg; ++q) {
+    while (i < nseg && se[i] < p[q]) ++i;
+    if (i < nseg && ss[i] <= p[q]) {
+      out[slot[i]] = (int64_t)((uint64_t)out[slot[i]] + (uint64_t)v[q] - (uint64_t)shadow);
+      if (cnt) cnt[slot[i]] += 1;
+    }
+  }
+}
+
+/* --- a tiny pthread parallel-for: thread t of T takes rows [lo, hi) ------- */
+
+typedef struct Fold {
+  const int64_t *ss, *se, *slot;
+  int64_t nseg, nslots, row0, n;
+  int dtype, logical, has_center;
+  int64_t center;
+  const void* values;
+  const double *x, *seg_scale;
+  int d1_dtype, d2_dtype;
+  const void *d1, *d2;
+  int64_t m1, a1, m2, a2;
+  void* part;          /* per-thread slot tables */
+  int T;
+} Fold;
+
+typedef struct Job {
+  Fold* f;
+  int t;
+  void (*fn)(Fold*, int);
+} Job;
+
+static void* job_main(void* p) {
+  Job* j = (Job*)p;
+  j->fn(j->f, j->t);
+  return NULL;
+}
+
+static int n_threads(int64_t n) {
+  long c = sysconf(_SC_NPROCESSORS_ONLN);
+  int T = c > 0 ? (int)c : 1;
+  if (T > 64) T = 64;
+  if (n < (int64_t)T * 65536) T = (int)(n / 65536) + 1;
+  return T;
+}
+
+static void par_run(Fold* f, void (*fn)(Fold*, int)) {
+  pthread_t th[64];
+  Job jobs[64];
+  for (int t = 0; t < f->T; ++t) {
+    jobs[t].f = f;
+    jobs[t].t = t;
+    jobs[t].fn = fn;
+    if (t > 0) pthread_create(&th[t], NULL, job_main, &jobs[t]);
+  }
+  fn(f, 0);
+  for (int t = 1; t < f->T; ++t) pthread_join(th[t], NULL);
+}
+
+static void rows_of(const Fold* f, int t, int64_t* lo, int64_t* hi) {
+  *lo = f->row0 + (int64_t)((__int128)f->n * t / f->T);
+  *hi = f->row0 + (int64_t)((__int128)f->n * (t + 1) / f->T);
+}
+
+/* decode_values(PlainColumn) column.cpp:283-297 per row, Σ per slot. */
+static void fold_int(Fold* f, int t) {
+  int64_t lo, hi;
+  rows_of(f, t, &lo, &hi);
+  uint64_t* acc = (uint64_t*)f->part + (size_t)t * (size_t)f->nslots;
+  for (int64_t i = lower_bound(f->se, f->nseg, lo); i < f->nseg && f->ss[i] < hi; ++i) {
+    int64_t a = f->ss[i] > lo ? f->ss[i] : lo, b = f->se[i] < hi - 1 ? f->se[i] : hi - 1;
+    uint64_t sum = 0;
+    for (int64_t r = a; r <= b; ++r) {
+      int64_t x = wrap_to(f->logical, load_int(f->dtype, f->values, r - f->row0));
+      if (f->has_center) x = wrap_to(f->logical, (int64_t)((uint64_t)x + (uint64_t)f->center));
+      sum += (uint64_t)x;
+    }
+    acc[f->slot[i]] += sum;
+  }
+}
+
+void orq_seg_sum_plain_int(const int64_t* ss, const int64_t* se, const int64_t* slot, int64_t nseg,
+                           int64_t nslots, int64_t row0, int64_t n, int dtype, const void* values,
+                           int logical, int has_center, int64_t center, int64_t* out) {
+  Fold f = {0};
+  f.ss = ss; f.se = se; f.slot = slot; f.nseg = nseg; f.nslots = nslots; f.row0 = row0; f.n = n;
+  f.dtype = dtype; f.values = values; f.logical = logical; f.has_center = has_center;
+  f.center = center; f.T = n_threads(n);
+  f.part = calloc((size_t)f.T * (size_t)nslots, sizeof(uint64_t));
+  par_run(&f, fold_int);
+  const uint64_t* part = (const uint64_t*)f.part;
+  for (int t = 0; t < f.T; ++t)
+    for (int64_t g = 0; g < nslots; ++g)
+      out[g] = (int64_t)((uint64_t)out[g] + part[(size_t)t * (size_t)nslots + (size_t)g]);
+  free(f.part);
+}
+
+static double factor(int dtype, const void* d, int64_t r, int64_t m, int64_t a) {
+  return (double)(int64_t)((uint64_t)m * (uint64_t)load_int(dtype, d, r) + (uint64_t)a);
+}
+
+/* arith(x, f1) then arith(·, f2) in f64 (align.cpp:290-334), SUM float
+ * (groupby.cpp:91-97) with weight 1 per row, Neumaier per thread. */
+static void fold_f64(Fold* f, int t) {
+  int64_t lo, hi;
+  rows_of(f, t, &lo, &hi);
+  double* ps = (double*)f->part + (size_t)t * (size_t)f->nslots * 2;
+  for (int64_t i = lower_bound(f->se, f->nseg, lo); i < f->nseg && f->ss[i] < hi; ++i) {
+    int64_t a = f->ss[i] > lo ? f->ss[i] : lo, b = f->se[i] < hi - 1 ? f->se[i] : hi - 1;
+    double s0 = ps[2 * f->slot[i]], c0 = ps[2 * f->slot[i] + 1];
+    for (int64_t r = a; r <= b; ++r) {
+      double y = f->x[r - f->row0];
+      if (f->d1) y = y * factor(f->d1_dtype, f->d1, r - f->row0, f->m1, f->a1);
+      else if (f->seg_scale) y = y * f->seg_scale[i];
+      if (f->d2) y = y * factor(f->d2_dtype, f->d2, r - f->row0, f->m2, f->a2);
+      neumaier_add(&s0, &c0, y);
+    }
+    ps[2 * f->slot[i]] = s0;
+    ps[2 * f->slot[i] + 1] = c0;
+  }
+}
+
+void orq_seg_sum_plain_f64(const int64_t* ss, const int64_t* se, const int64_t* slot, int64_t nseg,
+                           int64_t nslots, int64_t row0, int64_t n, const double* x,
+                           const double* seg_scale, int d1_dtype, const void* d1, int64_t m1,
+                           int64_t a1, int d2_dtype, const void* d2, int64_t m2, int64_t a2,
+                           double* sum, double* comp) {
+  Fold f = {0};
+  f.ss = ss; f.se = se; f.slot = slot; f.nseg = nseg; f.nslots = nslots; f.row0 = row0; f.n = n;
+  f.x = x; f.seg_scale = seg_scale; f.d1_dtype = d1_dtype; f.d1 = d1; f.m1 = m1; f.a1 = a1;
+  f.d2_dtype = d2_dtype; f.d2 = d2; f.m2 = m2; f.a2 = a2; f.T = n_threads(n);
+  f.part = calloc((size_t)f.T * (size_t)nslots * 2, sizeof(double));
+  par_run(&f, fold_f64);
+  const double* part = (const double*)f.part;
+  for (int t = 0; t < f.T; ++t)
+    for (int64_t g = 0; g < nslots; ++g) {
+      const double* ps = part + ((size_t)t * (size_t)nslots + (size_t)g) * 2;
+      neumaier_add(&sum[g], &comp[g], ps[0]);
+      neumaier_add(&sum[g], &comp[g], ps[1]);
+    }
+  free(f.part);
+}

@@ -33,6 +33,8 @@ PROTOTYPES = {
     "rq_ctx_profile_report": (C.c_int, [vp, i32, C.c_char_p, i64]),
     "rq_arr_upload": (C.c_int, [vp, i32, vp, i64, P(vp)]),
     "rq_arr_wrap_device": (C.c_int, [vp, i32, vp, i64, P(vp)]),
+    "rq_arr_alloc": (C.c_int, [vp, i32, i64, P(vp)]),
+    "rq_arr_write": (C.c_int, [vp, vp, i64, vp, i64]),
     "rq_arr_info": (C.c_int, [vp, P(i32), P(i64)]),
     "rq_arr_device_ptr": (vp, [vp]),
     "rq_arr_download": (C.c_int, [vp, vp, vp]),

@@ -396,6 +396,63 @@ static int group_aggregate_api(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys,
   });
 }
 
+int rq_group_aggregate_sharded(rq_ctx_t c, rq_comm_t comm, const rq_col_t* keys, int32_t n_keys,
+                               const rq_col_t* data, const int32_t* fns, int32_t n_data, int32_t normalized,
+                               int64_t* n_groups, rq_arr_t* out_keys, rq_arr_t* out_vals) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    require(n_keys > 0, "group: empty key list");
+    std::vector<const DCol*> k, d;
+    std::vector<int> f;
+    for (int i = 0; i < n_keys; ++i) k.push_back(&col_of(keys[i]));
+    for (int i = 0; i < n_data; ++i) {
+      d.push_back(&col_of(data[i]));
+      f.push_back(fns[i]);
+    }
+    GroupAggOut r = sharded(ctx, comm_of(comm), f, [&](const PartialPlan& p) {
+      std::vector<const DCol*> ld;
+      for (int i : p.src) ld.push_back(d[static_cast<size_t>(i)]);
+      return group_aggregate(ctx, k, ld, p.local_fns, normalized != 0);
+    });
+    if (n_groups) *n_groups = r.n_groups;
+    for (int i = 0; i < n_keys; ++i) out_keys[i] = wrap_arr(r.keys[static_cast<size_t>(i)]);
+    for (int i = 0; i < n_data; ++i) out_vals[i] = wrap_arr(r.vals[static_cast<size_t>(i)]);
+  });
+}
+
+int rq_aggregate_all_sharded(rq_ctx_t c, rq_comm_t comm, rq_col_t data, int32_t fn, int32_t* out_dtype,
+                             int64_t* out_i64, double* out_f64) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    const DCol& d = col_of(data);
+    put_agg(sharded_scalar(ctx, comm_of(comm), fn, [&](int f) { return aggregate_column(ctx, d, f); }), out_dtype,
+            out_i64, out_f64);
+  });
+}
+
+int rq_aggregate_binop_sharded(rq_ctx_t c, rq_comm_t comm, rq_col_t a, rq_col_t b, int32_t op, int32_t fn,
+                               int32_t* out_dtype, int64_t* out_i64, double* out_f64) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    const DCol &x = col_of(a), &y = col_of(b);
+    put_agg(sharded_scalar(ctx, comm_of(comm), fn, [&](int f) { return aggregate_binop(ctx, x, y, op, f); }),
+            out_dtype, out_i64, out_f64);
+  });
+}
+
+int rq_filtered_aggregate_binop_sharded(rq_ctx_t c, rq_comm_t comm, rq_col_t pred, rq_scalar k, int32_t cmp,
+                                        rq_col_t a, rq_col_t b, int32_t op, int32_t fn, int32_t* out_dtype,
+                                        int64_t* out_i64, double* out_f64) {
+  return api_guard([&] {
+    auto ctx = ctx_of(c);
+    const DCol &p = col_of(pred), &x = col_of(a), &y = col_of(b);
+    const Scalar ks = scal(k);
+    put_agg(sharded_scalar(ctx, comm_of(comm), fn,
+                           [&](int f) { return filtered_aggregate_binop(ctx, p, ks, cmp, x, y, op, f); }),
+            out_dtype, out_i64, out_f64);
+  });
+}
+
 int rq_group_aggregate(rq_ctx_t c, const rq_col_t* keys, int32_t n_keys, const rq_col_t* data,
                        const int32_t* fns, int32_t n_data, int64_t* n_groups, rq_arr_t* out_keys,
                        rq_arr_t* out_vals) {
@@ -429,7 +486,7 @@ int rq_filtered_aggregate_binop(rq_ctx_t c, rq_col_t pred, rq_scalar k, int32_t 
 static int group_aggregate_exprs_api(rq_ctx_t c, const rq_pred* where, int32_t n_where, rq_mask_t mask,
                                      const rq_col_t* keys, int32_t n_keys, const rq_expr* exprs,
                                      const int32_t* fns, int32_t n_exprs, int64_t* n_groups, rq_arr_t* out_keys,
-                                     rq_arr_t* out_vals, int32_t* fused) {
+                                     rq_arr_t* out_vals, int32_t* fused, rq_comm_t comm = nullptr) {
   return api_guard([&] {
     auto ctx = ctx_of(c);
     require(n_exprs > 0 && exprs != nullptr && fns != nullptr, "group_aggregate_exprs: no expressions");
@@ -467,8 +524,18 @@ static int group_aggregate_exprs_api(rq_ctx_t c, const rq_pred* where, int32_t n
       preds.push_back(q);
     }
     bool was_fused = false;
-    GroupAggOut r = group_aggregate_exprs(ctx, mask ? &mask_of(mask) : nullptr, k, xs, f, &was_fused,
-                                          preds.empty() ? nullptr : &preds);
+    const DMask* m = mask ? &mask_of(mask) : nullptr;
+    const std::vector<XPred>* pp = preds.empty() ? nullptr : &preds;
+    GroupAggOut r;
+    if (comm) {  // this rank's partials (AVG → SUM, COUNT of the same expression), merged
+      r = sharded(ctx, comm_of(comm), f, [&](const PartialPlan& p) {
+        std::vector<XExpr> lx;
+        for (int i : p.src) lx.push_back(xs[static_cast<size_t>(i)]);
+        return group_aggregate_exprs(ctx, m, k, lx, p.local_fns, &was_fused, pp);
+      });
+    } else {
+      r = group_aggregate_exprs(ctx, m, k, xs, f, &was_fused, pp);
+    }
     if (fused) *fused = was_fused ? 1 : 0;
     if (n_groups) *n_groups = r.n_groups;
     for (int i = 0; i < n_keys; ++i) out_keys[i] = wrap_arr(r.keys[static_cast<size_t>(i)]);
@@ -481,6 +548,15 @@ int rq_group_aggregate_exprs(rq_ctx_t c, rq_mask_t mask, const rq_col_t* keys, i
                              rq_arr_t* out_keys, rq_arr_t* out_vals, int32_t* fused) {
   return group_aggregate_exprs_api(c, nullptr, 0, mask, keys, n_keys, exprs, fns, n_exprs, n_groups, out_keys,
                                    out_vals, fused);
+}
+
+int rq_group_aggregate_where_sharded(rq_ctx_t c, rq_comm_t comm, const rq_pred* where, int32_t n_where,
+                                     rq_mask_t mask, const rq_col_t* keys, int32_t n_keys, const rq_expr* exprs,
+                                     const int32_t* fns, int32_t n_exprs, int64_t* n_groups, rq_arr_t* out_keys,
+                                     rq_arr_t* out_vals, int32_t* fused) {
+  if (!comm) return api_guard([] { fail("null communicator"); });
+  return group_aggregate_exprs_api(c, where, n_where, mask, keys, n_keys, exprs, fns, n_exprs, n_groups, out_keys,
+                                   out_vals, fused, comm);
 }
 
 int rq_group_aggregate_where(rq_ctx_t c, const rq_pred* where, int32_t n_where, rq_mask_t mask,

@@ -372,6 +372,29 @@ int rq_arr_upload(rq_ctx_t c, int32_t dtype, const void* host, int64_t n, rq_arr
   });
 }
 
+int rq_arr_alloc(rq_ctx_t c, int32_t dtype, int64_t n, rq_arr_t* out) {
+  return api_guard([&] {
+    auto ctx = get_ctx(c);
+    require(dt_valid(dtype), "invalid dtype");
+    require(n >= 0, "rq_arr_alloc: negative size");
+    *out = wrap_arr(alloc_arr(ctx, dtype, n));
+  });
+}
+
+int rq_arr_write(rq_ctx_t c, rq_arr_t a, int64_t offset, const void* host, int64_t count) {
+  return api_guard([&] {
+    auto ctx = get_ctx(c);
+    require(a != nullptr, "rq_arr_write: null array");
+    DArr& x = a->a;
+    require(offset >= 0 && count >= 0 && offset + count <= x.n, "rq_arr_write: range outside the array");
+    if (count == 0) return;
+    require(host != nullptr, "rq_arr_write: null host pointer");
+    size_t w = dt_width(x.dt);
+    RQ_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(x.raw_mut()) + static_cast<size_t>(offset) * w, host,
+                                  static_cast<size_t>(count) * w, cudaMemcpyHostToDevice, ctx->stream));
+  });
+}
+
 int rq_arr_wrap_device(rq_ctx_t c, int32_t dtype, void* dev, int64_t n, rq_arr_t* out) {
   return api_guard([&] {
     auto ctx = get_ctx(c);

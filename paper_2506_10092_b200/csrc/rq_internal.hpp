@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -527,5 +528,23 @@ GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const st
 bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& keys,
                            const std::vector<const DCol*>& data, const std::vector<int>& fns,
                            GroupAggOut& out);
+
+// ---- row-range sharded execution (comm.cu) ---------------------------------------
+
+struct Comm;
+Comm& comm_of(rq_comm_t c);
+// AVG → (SUM, COUNT) partials of the same input; local_fns / src per
+// partial, sum_of / cnt_of per original function (cnt_of = -1 unless AVG)
+struct PartialPlan {
+  std::vector<int> local_fns, src, sum_of, cnt_of;
+};
+PartialPlan partial_plan(const std::vector<int>& fns);
+GroupAggOut merge_group_tables(const CtxPtr& ctx, Comm& cm, const GroupAggOut& local,
+                               const std::vector<int>& part_fns);
+// local(plan) computes this rank's partial table; the result is the merged,
+// finalised table (identical on every rank)
+GroupAggOut sharded(const CtxPtr& ctx, Comm& cm, const std::vector<int>& fns,
+                    const std::function<GroupAggOut(const PartialPlan&)>& local);
+AggOut sharded_scalar(const CtxPtr& ctx, Comm& cm, int fn, const std::function<AggOut(int)>& local);
 
 }  // namespace rqb

@@ -195,16 +195,37 @@ def rle_plus_index(n: int, L: int, point_frac: float, seed: int, lo: int = -1000
     return H.RlePlusIndexColumn(H.RleColumn(rv, rs, re_, n), H.IndexColumn(pv, p.astype(np.int64), n))
 
 
-def c3_tables(n: int, seed: int = 42):
-    """C3: K codes 0..99 RLE L=4096, X RLE i64 L=128,
-    Y RLE+Index (90% of rows in runs L=256, 10% points), Z plain-centered i16
-    U[-20000, 20000] (logical i64), W plain f64 U[0, 100)."""
+C3_CHUNK = 1 << 28  # rows per generated chunk of C3's plain columns
+
+
+def c3_run_columns(n: int, seed: int = 42):
+    """C3's run-encoded columns: K codes 0..99 RLE L=4096, X RLE i64 L=128,
+    Y RLE+Index (90% of rows in runs L=256, 10% points)."""
     k = gapless_rle(n, 4096, seed, 0, 99)
     x = gapless_rle(n, 128, seed + 1)
     y = rle_plus_index(n, 256, 0.1, seed + 2)
-    rng = np.random.default_rng(seed + 3)
-    z = H.PlainColumn(rng.integers(-20000, 20001, n).astype(np.int16), H.I64, 0)
-    w = H.PlainColumn(rng.uniform(0.0, 100.0, n))
+    return k, x, y
+
+
+def c3_plain_chunk(n: int, seed: int, row0: int):
+    """Rows [row0, row0 + C3_CHUNK) ∩ [0, n) of C3's plain columns: Z
+    plain-centered i16 U[-20000, 20000] (logical i64) and W plain f64
+    U[0, 100). Each chunk has its own stream, so a 10B-row table can be
+    generated, uploaded and checked chunk by chunk."""
+    assert row0 % C3_CHUNK == 0
+    m = min(C3_CHUNK, n - row0)
+    rng = np.random.default_rng([seed + 3, row0 // C3_CHUNK])
+    z = rng.integers(-20000, 20001, m, dtype=np.int16)
+    w = rng.uniform(0.0, 100.0, m)
+    return z, w
+
+
+def c3_tables(n: int, seed: int = 42):
+    """C3: K, X, Y (c3_run_columns) + Z, W (c3_plain_chunk)."""
+    k, x, y = c3_run_columns(n, seed)
+    parts = [c3_plain_chunk(n, seed, r) for r in range(0, n, C3_CHUNK)]
+    z = H.PlainColumn(np.concatenate([p[0] for p in parts]) if parts else np.empty(0, np.int16), H.I64, 0)
+    w = H.PlainColumn(np.concatenate([p[1] for p in parts]) if parts else np.empty(0))
     return k, x, y, z, w
 
 

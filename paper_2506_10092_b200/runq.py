@@ -91,6 +91,14 @@ class DeviceArray:
     def device_ptr(self) -> int:
         return _L.rq_arr_device_ptr(self.handle) or 0
 
+    def write(self, offset: int, host: np.ndarray):
+        """rq_arr_write: host[...] → elements [offset, offset + len(host)).
+        Stream-ordered: `host` must stay alive until the context syncs."""
+        a = np.ascontiguousarray(host, dtype=H.DTYPES[self.dtype])
+        check(_L.rq_arr_write(self.ctx.handle, self.handle, offset, a.ctypes.data if a.size else None,
+                              a.shape[0]))
+        return a
+
     def download(self) -> np.ndarray:
         dt, n = self.info
         out = np.empty(n, dtype=H.DTYPES[dt])
@@ -189,6 +197,24 @@ def upload(x, ctx: Context = None):
     img, keep = H.column_image(x)
     check(_L.rq_col_upload(ctx.handle, C.byref(img), C.byref(h)))
     return DeviceColumn(h, ctx)
+
+
+def alloc_array(dtype: int, n: int, ctx: Context = None) -> DeviceArray:
+    """rq_arr_alloc: an uninitialised device array, filled by DeviceArray.write
+    (columns larger than host RAM stream into HBM in row chunks)."""
+    ctx = _ctx(ctx)
+    h = C.c_void_p()
+    check(_L.rq_arr_alloc(ctx.handle, dtype, n, C.byref(h)))
+    return DeviceArray(h, ctx)
+
+
+def make_plain(values: DeviceArray, logical: int = None, center=None) -> DeviceColumn:
+    """rq_col_make_plain: a PlainColumn over a device array (shared)."""
+    h = C.c_void_p()
+    logical = values.dtype if logical is None else logical
+    check(_L.rq_col_make_plain(values.ctx.handle, values.handle, logical, 0 if center is None else 1,
+                               int(center or 0), C.byref(h)))
+    return DeviceColumn(h, values.ctx)
 
 
 def dump_image(col, ctx: Context = None) -> bytes:
