@@ -14,9 +14,18 @@ Other workloads (--workload): c1 = SUM(A+B) over two misaligned RLE int64
 columns (fused rq_aggregate_binop), c3 = GROUP BY dict key SUM/COUNT/AVG over
 RLE / RLE+Index / bit-width-reduced i16 / f64 columns (fused group-by).
 
-Multi-GPU (torchrun): one process per GPU, each rank owns a row-range shard
-of the same size (weak scaling); the per-rank partial aggregate is merged
-with one NCCL all_reduce per step.
+Multi-GPU (torchrun): one process per GPU. The N-GPU table is ONE table of
+N × rows rows; each rank owns a row-range shard of it (cuts snapped to the run
+boundaries of the column with the most runs; run-encoded columns cut with
+rq_shard_host_column, plain columns generated for the rank's rows only), so
+per-GPU work is fixed as N grows (weak scaling). Every step runs the
+library's sharded entry point: the single-GPU kernels on the shard, then ONE
+collective inside the library (NCCL all-reduce of the partial aggregates, or
+an all-gather of the (key, partial) group tables + device regroup; AVG from
+the merged SUM / COUNT). torch.distributed (gloo) only bootstraps the NCCL
+unique id, barriers, and takes the max of the per-rank times. The gate
+checks the merged result on rank 0 against the oracle of the whole table
+(the merge of every rank's oracle over its own rows).
 
 --impl reference runs the UNMODIFIED reference library (oracle/_ref, the
 reference compiled from its sources) on the same workload on the host's
@@ -174,6 +183,22 @@ def alg_bytes(col, gapless=True, only_points=None):
     return n * col.values.itemsize
 
 
+def stats_bytes(col):
+    """The reference's own byte accounting, stats() (column.cpp:244-279):
+    RLE R·(w+16) (positions s and e per run), Index P·(w+8), Plain storage
+    bytes, composites summed — reported next to ALG_BYTES."""
+    from paper_2506_10092_b200 import host as H
+    if isinstance(col, H.RleColumn):
+        return col.v.shape[0] * (col.v.itemsize + 16)
+    if isinstance(col, H.IndexColumn):
+        return col.p.shape[0] * (col.v.itemsize + 8)
+    if isinstance(col, H.RlePlusIndexColumn):
+        return stats_bytes(col.runs) + stats_bytes(col.points)
+    if isinstance(col, H.PlainPlusIndexColumn):
+        return stats_bytes(col.base) + stats_bytes(col.outliers)
+    return col.values.nbytes
+
+
 def ncu_traffic(workload, tag):
     """dram bytes per launch of the dominant kernel (tag) or of the whole
     query step (tag "query") of one workload, from the committed ncu captures
@@ -192,80 +217,6 @@ def ncu_traffic(workload, tag):
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
-
-
-class C2:
-    name = "c2"
-    tag = "filtered_points_reduce"
-    dtype = "int64"
-
-    def __init__(self, args):
-        self.args = args
-        self.k = 20
-
-    def describe(self):
-        cdesc = "RLE L=256" if self.args.variant == "rle" else "plain-centered i8 L=4"
-        return (f"C2: filtered SUM(A*B) WHERE C<{self.k}; A RLE i64 L=64, B Index i64 1%, "
-                f"C dict codes (card 64) {cdesc}")
-
-    def gen(self, rows, seed):
-        from paper_2506_10092_b200 import datagen as G
-        a, b, c = G.c2_tables(rows, seed=seed, c_variant=self.args.variant)
-        self.host = {"a": a, "b": b, "c": c}
-        return self.host
-
-    def alg_bytes(self, h):
-        from paper_2506_10092_b200 import host as H
-        c = h["c"]
-        cb = alg_bytes(c) if isinstance(c, H.RleColumn) else alg_bytes(c, only_points=h["b"].p.shape[0])
-        return alg_bytes(h["a"]) + alg_bytes(h["b"]) + cb
-
-    def query(self, rq, d, path):
-        if path == "fused":
-            return rq.agg.filtered_aggregate_binop(d["c"], self.k, "<", d["a"], d["b"], "*", "sum")
-        m = rq.compute.compare_scalar(d["c"], self.k, "<")
-        return rq.agg.aggregate_all(rq.compute.arith(rq.compute.filter(d["a"], m), rq.compute.filter(d["b"], m), "*"),
-                                    "sum")
-
-    def oracle(self, h):
-        from oracle import refpy
-        return refpy.Orq().filtered_sum(h["c"], self.k, "<", h["a"], h["b"], "*")
-
-    def ref_run(self, ref, shards, threads):
-        return ref.chain_filtered_sum(shards["c"], shards["a"], shards["b"], threads, self.k, "<", "*")
-
-
-class C1:
-    name = "c1"
-    tag = "pair_reduce"
-    dtype = "int64"
-
-    def __init__(self, args):
-        self.args = args
-
-    def describe(self):
-        return "C1: SUM(A+B) over two misaligned RLE i64 columns, L=64/96"
-
-    def gen(self, rows, seed):
-        from paper_2506_10092_b200 import datagen as G
-        a, b = G.c1_tables(rows, 64, 96, seed)
-        self.host = {"a": a, "b": b}
-        return self.host
-
-    def alg_bytes(self, h):
-        return alg_bytes(h["a"]) + alg_bytes(h["b"])
-
-    def query(self, rq, d, path):
-        if path == "fused":
-            return rq.agg.aggregate_binop(d["a"], d["b"], "+", "sum")
-        return rq.agg.aggregate_all(rq.compute.arith(d["a"], d["b"], "+"), "sum")
-
-    def oracle(self, h):
-        from oracle import refpy
-        return refpy.Orq().sum_rle_binop(h["a"], h["b"], "+")
-
-    def ref_run(self, ref, shards, threads):
-        return ref.chain_sum_binop(shards["a"], shards["b"], threads, "+")
 
 
 def table_summary(t):
@@ -300,36 +251,143 @@ def tables_same(a, b):
     return True
 
 
-class C3:
+def f64_same(a, b):
+    return abs(a - b) <= 1e-9 * max(1.0, abs(a), abs(b))
+
+
+def scalar_partial(v):
+    from oracle import streaming as S
+    return S.Partial([], [np.array([v], np.int64)])
+
+
+class Workload:
+    """One BASELINE configuration. gen() returns this rank's shard of the
+    table (the whole table when part is None); query() runs it through the
+    library (sharded entry point when comm is given); oracle_partial() is the
+    checker over the shard's rows, oracle_finish() of the merged partials is
+    the whole table's expected result."""
+    tag = None
+    dtype = "int64"
+    same = staticmethod(lambda a, b: a == b)
+    summary = staticmethod(lambda v: v)
+    chunked = False
+    ref_rows = None
+
+    def __init__(self, args):
+        self.args = args
+
+    def upload(self, rq, ctx, host, check):
+        return {k: rq.upload(v, ctx) for k, v in host.items()}
+
+    def oracle_finish(self, merged):
+        return int(merged.parts[0][0])
+
+    def stats_bytes(self, h):
+        return sum(stats_bytes(c) for c in h.values())
+
+    def cpu_sample(self, rows):
+        return self.gen(rows, 42)
+
+
+class C2(Workload):
+    name = "c2"
+    tag = "filtered_points_reduce"
+    k = 20
+
+    def describe(self):
+        cdesc = "RLE L=256" if self.args.variant == "rle" else "plain-centered i8 L=4"
+        return (f"C2: filtered SUM(A*B) WHERE C<{self.k}; A RLE i64 L=64, B Index i64 1%, "
+                f"C dict codes (card 64) {cdesc}")
+
+    def gen(self, rows, seed, part=None, slicer=None):
+        from paper_2506_10092_b200 import datagen as G
+        from paper_2506_10092_b200 import sharding
+        a, b, c = G.c2_tables(rows, seed=seed, c_variant=self.args.variant)
+        t = {"a": a, "b": b, "c": c}
+        return t if part is None else sharding.shard_table(t, part[0], part[1], snap="a")
+
+    def alg_bytes(self, h):
+        from paper_2506_10092_b200 import host as H
+        c = h["c"]
+        cb = alg_bytes(c) if isinstance(c, H.RleColumn) else alg_bytes(c, only_points=h["b"].p.shape[0])
+        return alg_bytes(h["a"]) + alg_bytes(h["b"]) + cb
+
+    def query(self, rq, d, path, comm=None):
+        if path == "fused":
+            return rq.agg.filtered_aggregate_binop(d["c"], self.k, "<", d["a"], d["b"], "*", "sum", comm=comm)
+        m = rq.compute.compare_scalar(d["c"], self.k, "<")
+        return rq.agg.aggregate_all(rq.compute.arith(rq.compute.filter(d["a"], m), rq.compute.filter(d["b"], m), "*"),
+                                    "sum", comm=comm)
+
+    def oracle_partial(self, h):
+        from oracle import refpy
+        return scalar_partial(refpy.Orq().filtered_sum(h["c"], self.k, "<", h["a"], h["b"], "*"))
+
+    def ref_run(self, ref, shards, threads):
+        return ref.chain_filtered_sum(shards["c"], shards["a"], shards["b"], threads, self.k, "<", "*")
+
+
+class C1(Workload):
+    name = "c1"
+    tag = "pair_reduce"
+
+    def describe(self):
+        return "C1: SUM(A+B) over two misaligned RLE i64 columns, L=64/96"
+
+    def gen(self, rows, seed, part=None, slicer=None):
+        from paper_2506_10092_b200 import datagen as G
+        from paper_2506_10092_b200 import sharding
+        a, b = G.c1_tables(rows, 64, 96, seed)
+        t = {"a": a, "b": b}
+        return t if part is None else sharding.shard_table(t, part[0], part[1], snap="a")
+
+    def alg_bytes(self, h):
+        return alg_bytes(h["a"]) + alg_bytes(h["b"])
+
+    def query(self, rq, d, path, comm=None):
+        if path == "fused":
+            return rq.agg.aggregate_binop(d["a"], d["b"], "+", "sum", comm=comm)
+        return rq.agg.aggregate_all(rq.compute.arith(d["a"], d["b"], "+"), "sum", comm=comm)
+
+    def oracle_partial(self, h):
+        from oracle import refpy
+        return scalar_partial(refpy.Orq().sum_rle_binop(h["a"], h["b"], "+"))
+
+    def ref_run(self, ref, shards, threads):
+        return ref.chain_sum_binop(shards["a"], shards["b"], threads, "+")
+
+
+class C3(Workload):
     name = "c3"
     tag = "group_fused"
     dtype = "int64/f64"
     host_rows_max = 2_000_000_000  # above this Z / W stream into HBM chunk by chunk (never whole on the host)
     same = staticmethod(tables_same)
     summary = staticmethod(table_summary)
+    ref_rows = 20_000_000
 
     def __init__(self, args):
-        self.args = args
+        super().__init__(args)
         self.fold = None
 
     def describe(self):
         return ("C3: GROUP BY K (codes 0..99, RLE L=4096) -> SUM(X RLE L=128), COUNT(*), AVG(Z plain-centered i16), "
                 "SUM(Y RLE+Index 90% runs L=256 / 10% points), SUM(W plain f64)")
 
-    def gen(self, rows, seed):
+    def gen(self, rows, seed, part=None, slicer=None):
         from paper_2506_10092_b200 import datagen as G
-        self.rows, self.seed = rows, seed
-        self.chunked = rows > self.host_rows_max
-        if self.chunked:
-            k, x, y = G.c3_run_columns(rows, seed)
-            self.host = {"k": k, "x": x, "y": y}
-        else:
-            k, x, y, z, w = G.c3_tables(rows, seed)
-            self.host = {"k": k, "x": x, "y": y, "z": z, "w": w}
-        return self.host
+        from paper_2506_10092_b200 import host as H
+        k, x, y, lo, hi = G.c3_run_columns(rows, seed, part, slicer)
+        self.total, self.seed, self.lo, self.hi = rows, seed, lo, hi
+        self.chunked = hi - lo > self.host_rows_max
+        t = {"k": k, "x": x, "y": y}
+        if not self.chunked:
+            z, w = G.c3_plain_rows(rows, seed, lo, hi)
+            t["z"], t["w"] = H.PlainColumn(z, H.I64, 0), H.PlainColumn(w)
+        return t
 
     def upload(self, rq, ctx, host, check):
-        """Chunked tables: Z / W generated chunk by chunk, written into HBM
+        """Chunked shards: Z / W generated chunk by chunk, written into HBM
         (rq_arr_alloc + rq_arr_write) and, when `check`, folded into the
         streaming oracle as they pass."""
         dev = {k: rq.upload(v, ctx) for k, v in host.items()}
@@ -340,44 +398,48 @@ class C3:
         if check:
             from oracle import streaming as S
             self.fold = S.C3Fold(S.StreamingOracle(), host["k"], host["x"], host["y"])
-        za, wa = rq.alloc_array(H.I16, self.rows, ctx), rq.alloc_array(H.F64, self.rows, ctx)
+        n = self.hi - self.lo
+        za, wa = rq.alloc_array(H.I16, n, ctx), rq.alloc_array(H.F64, n, ctx)
         t0 = time.time()
-        for r0 in range(0, self.rows, G.C3_CHUNK):
-            z, w = G.c3_plain_chunk(self.rows, self.seed, r0)
-            keep = (za.write(r0, z), wa.write(r0, w))
+        r = self.lo
+        while r < self.hi:
+            r1 = min(self.hi, (r // G.GEN_CHUNK + 1) * G.GEN_CHUNK)
+            z, w = G.c3_plain_rows(self.total, self.seed, r, r1)
+            keep = (za.write(r - self.lo, z), wa.write(r - self.lo, w))
             if self.fold is not None:
-                self.fold.add_plain_chunk(r0, H.PlainColumn(z, H.I64, 0), w)
+                self.fold.add_plain_chunk(r - self.lo, H.PlainColumn(z, H.I64, 0), w)
             ctx.synchronize()
             del keep
-        log(f"streamed Z/W ({self.rows} rows) into HBM in {time.time() - t0:.1f}s")
+            r = r1
+        log(f"streamed Z/W ({n} rows) into HBM in {time.time() - t0:.1f}s")
         dev["z"], dev["w"] = rq.make_plain(za, H.I64, 0), rq.make_plain(wa)
         return dev
 
     def alg_bytes(self, h):
         b = sum(alg_bytes(h[n]) for n in ("k", "x", "y"))
-        return b + self.rows * (2 + 8)  # Z i16 + W f64 per row
+        return b + (self.hi - self.lo) * (2 + 8)  # Z i16 + W f64 per row
 
-    def query(self, rq, d, path):
+    def stats_bytes(self, h):
+        return sum(stats_bytes(h[n]) for n in ("k", "x", "y")) + (self.hi - self.lo) * (2 + 8)
+
+    def query(self, rq, d, path, comm=None):
         from paper_2506_10092_b200 import datagen as G
         ks, vs, ng = rq.agg.group_aggregate([d["k"]], [d["x"], d["k"], d["z"], d["y"], d["w"]], G.C3_FNS,
-                                            normalize=True)
+                                            normalize=True, comm=comm)
         h = rq.download_all(list(ks) + list(vs))
         return h[:1], h[1:]
 
-    def oracle(self, h):
-        """The full group table from the streaming oracle (oracle/streaming.py,
-        pinned against the reference library up to 100M rows)."""
-        if self.fold is not None:
-            return self.fold.result()
+    def oracle_partial(self, h):
+        """The streaming oracle (oracle/streaming.py, pinned against the
+        reference library up to 100M rows) over this shard's rows."""
         from oracle import streaming as S
-        return S.c3(h)
+        if self.fold is not None:
+            return self.fold.partial()
+        return S.c3_partial(h)
 
-    def cpu_sample(self, host, rows):
-        if not self.chunked:
-            return None
-        from paper_2506_10092_b200 import datagen as G
-        k, x, y, z, w = G.c3_tables(rows, self.seed)
-        return {"k": k, "x": x, "y": y, "z": z, "w": w}
+    def oracle_finish(self, merged):
+        from oracle import streaming as S
+        return S.c3_finish(merged)
 
     def ref_run(self, ref, shards, threads):
         from paper_2506_10092_b200 import datagen as G
@@ -391,31 +453,29 @@ class C3:
         return tot, time.perf_counter() - t0
 
 
-class Q6:
+class Q6(Workload):
     """C4: TPC-H-style Q6 over synthetic lineitem (SF = rows / 6M) sorted by
-    (quantity, discount, shipdate) — device operator chain, same plan as the
-    reference runner."""
+    (quantity, discount, shipdate)."""
     name = "q6"
-    tag = None  # whole query (operator chain)
     dtype = "f64"
     ref_rows = 60_000_000  # reference arm sample (SF10)
+    same = staticmethod(f64_same)
 
     def __init__(self, args):
-        self.args = args
+        super().__init__(args)
         # fused path: the K12 row kernel (the query's dominant kernel); chain: whole query
         self.tag = "xg_rows" if args.path == "fused" else None
 
     def describe(self):
         return (f"C4 Q6: SUM(price*disc) WHERE shipdate in [1994-01-01,1995-01-01) AND disc BETWEEN 5 AND 7 AND "
-                f"qty < 24; lineitem SF{self.args.rows / 6e6:g} sorted (qty, disc, shipdate), RLE keys + f64 price")
+                f"qty < 24; lineitem SF{self.args.rows / 6e6:g} per GPU sorted (qty, disc, shipdate), RLE keys + "
+                f"f64 price")
 
-    def gen(self, rows, seed):
+    def gen(self, rows, seed, part=None, slicer=None):
         from paper_2506_10092_b200 import queries as Q
-        self.host = Q.lineitem_q6(rows, seed)
-        return self.host
+        return Q.lineitem_q6(rows, seed, part, slicer)
 
     def alg_bytes(self, h):
-        from paper_2506_10092_b200 import queries as Q
         sd, d, q = h["l_shipdate"], h["l_discount"], h["l_quantity"]
         # price is read only at the selected rows (SURVEY §8d): estimate them from the runs
         sel = self._selected(h)
@@ -426,29 +486,28 @@ class Q6:
     def _selected(self, h):
         from paper_2506_10092_b200 import queries as Q
         sd, d, q = h["l_shipdate"], h["l_discount"], h["l_quantity"]
-        # runs of shipdate inside a passing (qty, disc) block and date range
-        qi = np.searchsorted(q.e, sd.s)
-        di = np.searchsorted(d.e, sd.s)
+        sds = sd.s if sd.s is not None else np.concatenate([[0], sd.e[:-1] + 1])
+        qi = np.searchsorted(q.e, sds)
+        di = np.searchsorted(d.e, sds)
         ok = (q.v[qi] < 24) & (d.v[di] >= 5) & (d.v[di] <= 7) & (sd.v >= Q.Q6_LO) & (sd.v < Q.Q6_HI)
-        return int((sd.e - sd.s + 1)[ok].sum())
+        return int((sd.e - sds + 1)[ok].sum())
 
-    def query(self, rq, d, path):
+    def query(self, rq, d, path, comm=None):
         from paper_2506_10092_b200 import queries as Q
         if path == "fused":
-            v, fused = Q.q6_fused(rq, d)
+            v, fused = Q.q6_fused(rq, d, comm)
             assert fused, "q6: fused path not taken"
             return v
         return Q.q6(rq, d)
 
-    def oracle(self, h):
-        """Streaming oracle (oracle/streaming.py) on the full table."""
+    def oracle_partial(self, h):
         from oracle import streaming as S
         from paper_2506_10092_b200 import queries as Q
-        return S.q6(h, Q.Q6_WHERE)
+        return S.q6_partial(h, Q.Q6_WHERE)
 
-    @staticmethod
-    def same(a, b):
-        return abs(a - b) <= 1e-9 * max(1.0, abs(a), abs(b))
+    def oracle_finish(self, merged):
+        from oracle import streaming as S
+        return S.q6_finish(merged)
 
     def ref_run(self, ref, shards, threads):
         from oracle.refpy import RefAPI
@@ -463,41 +522,45 @@ class Q1(Q6):
     name = "q1"
     dtype = "int64/f64"
     ref_rows = 2_000_000
+    same = staticmethod(tables_same)
+    summary = staticmethod(table_summary)
 
     def describe(self):
         return (f"C4 Q1: GROUP BY returnflag, linestatus: 4 SUMs, 3 AVGs, COUNT WHERE shipdate <= 1998-09-02; "
-                f"lineitem SF{self.args.rows / 6e6:g} sorted (rf, ls, shipdate, qty); disc/tax i8 plain, price f64")
+                f"lineitem SF{self.args.rows / 6e6:g} per GPU sorted (rf, ls, shipdate, qty); disc/tax i8 plain, "
+                f"price f64")
 
-    def gen(self, rows, seed):
+    def gen(self, rows, seed, part=None, slicer=None):
         from paper_2506_10092_b200 import queries as Q
-        self.host = Q.lineitem_q1(rows, seed)
-        return self.host
+        return Q.lineitem_q1(rows, seed + 1, part, slicer)
 
     def alg_bytes(self, h):
         if self.tag == "xg_rows":  # the row kernel streams price / disc / tax over the rows passing the filter
             from paper_2506_10092_b200 import queries as Q
             sd = h["l_shipdate"]
-            sel = int((sd.e - sd.s + 1)[sd.v <= Q.Q1_CUTOFF].sum())
+            sds = sd.s if sd.s is not None else np.concatenate([[0], sd.e[:-1] + 1])
+            sel = int((sd.e - sds + 1)[sd.v <= Q.Q1_CUTOFF].sum())
             return sel * (8 + 1 + 1)
         return sum(alg_bytes(c, gapless=True) for c in h.values())
 
-    def query(self, rq, d, path):
+    def query(self, rq, d, path, comm=None):
         from paper_2506_10092_b200 import queries as Q
         if path == "fused":
-            (ks, vs, ng), fused = Q.q1_fused(rq, d)
+            (ks, vs, ng), fused = Q.q1_fused(rq, d, comm)
             assert fused, "q1: fused path not taken"
         else:
             ks, vs, ng = Q.q1(rq, d)
         h = rq.download_all(list(ks) + list(vs))
         return h[:2], h[2:]
 
-    def oracle(self, h):
+    def oracle_partial(self, h):
         from oracle import streaming as S
         from paper_2506_10092_b200 import queries as Q
-        return S.q1(h, Q.Q1_CUTOFF)
+        return S.q1_partial(h, Q.Q1_CUTOFF)
 
-    same = staticmethod(tables_same)
-    summary = staticmethod(table_summary)
+    def oracle_finish(self, merged):
+        from oracle import streaming as S
+        return S.q1_finish(merged)
 
     def ref_run(self, ref, shards, threads):
         from oracle.refpy import RefAPI
@@ -515,7 +578,8 @@ class C5(Q6):
     """C5: production-shaped 15-column table (7 RLE code columns incl. the
     avg-34.41 heavy one, 4 Plain+Index i16+1% outliers, 4 narrow plain);
     WHERE r2 IN (3,17,42) AND r3 < 50 GROUP BY r4: SUM(pi0), SUM(p1), COUNT.
-    6B rows over 8 GPUs = 750M rows per GPU (weak scaling per rank)."""
+    750M rows per GPU: 6B rows over 8 GPUs (the table is too large
+    uncompressed for one GPU)."""
     name = "c5"
     dtype = "int64"
     same = staticmethod(tables_same)
@@ -525,12 +589,12 @@ class C5(Q6):
 
     def describe(self):
         return ("C5: production-shaped 15 cols (7 RLE i32 codes, 4 Plain+Index i16+1% i64, 4 narrow plain); "
-                "WHERE r2 IN (3,17,42) AND r3 < 50 GROUP BY r4 -> SUM(pi0), SUM(p1), COUNT(*)")
+                "WHERE r2 IN (3,17,42) AND r3 < 50 GROUP BY r4 -> SUM(pi0), SUM(p1), COUNT(*); the columns the "
+                "query reads are generated")
 
-    def gen(self, rows, seed):
+    def gen(self, rows, seed, part=None, slicer=None):
         from paper_2506_10092_b200 import queries as Q
-        self.host = Q.production_table(rows, seed)
-        return self.host
+        return Q.production_table(rows, seed - 37, part, slicer, columns=self.columns)
 
     def alg_bytes(self, h):
         # predicate / key runs + the two measures read only at the selected rows
@@ -542,21 +606,24 @@ class C5(Q6):
         out_frac = len(pi0.outliers.p) / max(1, pi0.base.values.shape[0])
         return runs + sel * (2 + 2) + int(sel * out_frac) * 16
 
-    def query(self, rq, d, path):
+    def query(self, rq, d, path, comm=None):
         from paper_2506_10092_b200 import queries as Q
         if path == "fused":
-            (ks, vs, ng), fused = Q.c5_fused(rq, d)
+            (ks, vs, ng), fused = Q.c5_fused(rq, d, comm)
             assert fused, "c5: fused path not taken"
         else:
             ks, vs, ng = Q.c5_query(rq, d)
         h = rq.download_all(list(ks) + list(vs))
-        self._sel = int(h[3].sum())
         return h[:1], h[1:]
 
-    def oracle(self, h):
+    def oracle_partial(self, h):
         from oracle import streaming as S
         from paper_2506_10092_b200 import queries as Q
-        return S.c5(h, Q.C5_IN, Q.C5_LT)
+        return S.c5_partial(h, Q.C5_IN, Q.C5_LT)
+
+    def oracle_finish(self, merged):
+        from oracle import streaming as S
+        return S.c5_finish(merged)
 
     def ref_run(self, ref, shards, threads):
         from oracle.refpy import RefAPI
@@ -588,8 +655,10 @@ def result_bytes(v):
     return 8
 
 
-def config_dict(args, w, rows):
-    return {"workload": w.describe(), "rows_per_gpu": rows, "query_path": args.path,
+def config_dict(args, w, rows, world=1):
+    return {"workload": w.describe(), "rows_per_gpu": rows, "total_rows": rows * world, "query_path": args.path,
+            "sharding": ("one table of rows_per_gpu x N rows, row-range shards (cuts snapped to runs), one "
+                         "in-library collective per step" if world > 1 else "single GPU"),
             "l2_policy": "inputs larger than L2 (126 MB) - no flush needed"}
 
 
@@ -604,7 +673,7 @@ def run_reference(args, w, rank, world):
     from oracle import refpy
     ref = refpy.Ref()
     threads = os.cpu_count() or 1
-    rows = min(args.rows, getattr(w, "ref_rows", args.rows)) if w.name != "c3" else min(args.rows, 20_000_000)
+    rows = min(args.rows, w.ref_rows or args.rows)
     host = w.gen(rows, 42)
     nshards = threads if w.name in ("c1", "c2") else 1
     shards = shard_map(host, nshards)
@@ -649,11 +718,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--rows", type=int, default=None,
-                    help="logical rows per GPU (default 1B; SF100 = 600M for q6/q1)")
+                    help="logical rows per GPU (default 1B; SF100 = 600M for q6/q1; 750M for c5)")
     ap.add_argument("--variant", default="rle", choices=["rle", "narrow"])
     ap.add_argument("--path", default="fused", choices=["fused", "chain"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="N>1 transport: the library's NCCL communicator (one rank per GPU), or its host "
+                         "transport over gloo (several ranks may share a GPU: tests of the N>1 logic)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.rows is None:
@@ -665,13 +737,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
     if world > 1:
-        import torch
+        # plumbing only (unique-id broadcast, barriers, max-over-ranks time,
+        # oracle partials); the data-path collective is the library's NCCL
         import torch.distributed as dist
-        if args.impl == "ours":
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group("gloo")
+        dist.init_process_group("gloo")
 
     if args.impl == "reference":
         run_reference(args, w, rank, world)
@@ -683,76 +752,59 @@ def main():
     from paper_2506_10092_b200 import runq
 
     rows = args.rows
+    total = rows * world
     t0 = time.time()
-    host = w.gen(rows, 42 + rank)
-    log(f"[rank {rank}] generated {w.name} with {rows} rows in {time.time() - t0:.1f}s")
+    part = (rank, world) if world > 1 else None
+    host = w.gen(total, 42, part, runq.shard_host_column)
+    log(f"[rank {rank}] generated {w.name}: shard of {total} rows in {time.time() - t0:.1f}s")
 
+    if args.comm == "host":  # ranks may share a device
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
     ctx = runq.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
-    check = rank == 0 and world == 1
-    if hasattr(w, "upload"):
-        dev = w.upload(runq, ctx, host, check)
-    else:
-        dev = {k: runq.upload(v, ctx) for k, v in host.items()}
-    pending = []  # in-flight partial merges (async NCCL all_reduce; completed by the closing barrier)
+    comm = None
+    if world > 1 and args.comm == "nccl":
+        uid = [runq.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = runq.Comm.nccl(ctx, uid[0], world, rank)
+    elif world > 1:
+        def allgather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+        comm = runq.Comm.host(ctx, world, rank, allgather)
+    check = True  # every rank folds its shard's oracle; rank 0 merges them
+    dev = w.upload(runq, ctx, host, check)
 
-    def step(d, path=None, merge_async=False):
-        v = w.query(runq, d, path or args.path)
-        if dist is not None and merge_async:
-            # the merge of step i overlaps step i+1's kernels: enqueue the
-            # all_reduce of this step's partials and keep the handles alive
-            parts = list(v) if isinstance(v, tuple) else [v]
-            ints = [x for x in parts if isinstance(x, int)]
-            flts = [x for x in parts if not isinstance(x, int)]
-            for vals, dt in ((ints, torch.int64), (flts, torch.float64)):
-                if vals:
-                    t = torch.tensor(vals, dtype=dt, device=f"cuda:{local}")
-                    pending.append((t, dist.all_reduce(t, async_op=True)))
-            return v
-        if dist is not None:
-            # partial-aggregate merge over NCCL: every component of the rank's
-            # result is a SUM / COUNT partial (int64 wraps like the reference,
-            # f64 sums reassociate within tolerance); one all_reduce per dtype
-            parts = list(v) if isinstance(v, tuple) else [v]
-            ints = [x for x in parts if isinstance(x, int)]
-            flts = [x for x in parts if not isinstance(x, int)]
-            out_i, out_f = [], []
-            if ints:
-                ti = torch.tensor(ints, dtype=torch.int64, device=f"cuda:{local}")
-                dist.all_reduce(ti)
-                out_i = ti.tolist()
-            if flts:
-                tf = torch.tensor(flts, dtype=torch.float64, device=f"cuda:{local}")
-                dist.all_reduce(tf)
-                out_f = tf.tolist()
-            merged = [out_i.pop(0) if isinstance(x, int) else out_f.pop(0) for x in parts]
-            v = tuple(merged) if isinstance(v, tuple) else merged[0]
-        return v
-
-    # correctness gate (rank 0, N=1): fused == device chain == oracle. The
-    # oracle is the C restatement (C1 / C2) or the streaming group-by oracle
-    # (C3 / Q1 / Q6 / C5, oracle/streaming.py) over the FULL table, pinned
-    # against the reference library up to 100M rows.
-    same = getattr(w, "same", lambda a, b: a == b)
-    v_fused = w.query(runq, dev, args.path)
-    if args.path == "fused":  # fused kernels == the device operator chain (itself checked vs the reference)
+    # correctness gate: fused == device chain (N=1) and merged result == the
+    # oracle of the whole table (rank 0). The oracle is the C restatement
+    # (C1 / C2) or the streaming group-by oracle (C3 / Q1 / Q6 / C5,
+    # oracle/streaming.py), pinned against the reference library up to 100M
+    # rows; for N>1 it is the merge of every rank's oracle over its own rows.
+    same = w.same
+    v_fused = w.query(runq, dev, args.path, comm)
+    if args.path == "fused" and world == 1:  # fused kernels == the device operator chain
         v_chain = w.query(runq, dev, "chain")
         assert same(v_fused, v_chain), (v_fused, v_chain)
-    oracle_ok = None
-    if check:
-        t1 = time.time()
-        want = w.oracle(host)
-        if want is not None:
-            oracle_ok = bool(same(v_fused, want))
-            log(f"oracle check {'OK' if oracle_ok else 'MISMATCH'} ({time.time() - t1:.1f}s)")
-            assert oracle_ok, (v_fused, want)
-    summarize = getattr(w, "summary", lambda v: v)
+    t1 = time.time()
+    mine = w.oracle_partial(host)
+    parts = [mine]
+    if dist is not None:
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+    from oracle import streaming as S
+    want = w.oracle_finish(S.merge(parts))
+    oracle_ok = bool(same(v_fused, want))
+    if rank == 0:
+        log(f"oracle check {'OK' if oracle_ok else 'MISMATCH'} ({time.time() - t1:.1f}s)")
+    assert oracle_ok, (v_fused, want)
 
     def barrier():
-        if dist is not None:
-            dist.barrier()
         ctx.synchronize()
         torch.cuda.synchronize(local)
+        if dist is not None:
+            dist.barrier()
 
     def timed(fn, steps, profile=False):
         for _ in range(args.warmup):
@@ -770,10 +822,6 @@ def main():
             ev0.record(stream)
             for _ in range(steps):
                 fn()
-            if pending:  # the timed region ends when the last merge has landed
-                with torch.cuda.stream(stream):
-                    for _, h in pending:
-                        h.wait()
             ev1.record(stream)
             ev1.synchronize()
         barrier()
@@ -784,41 +832,39 @@ def main():
             runq._L.rq_ctx_set_profiling(ctx.handle, 0)
             report = json.loads(buf.value.decode())
         ms = ev0.elapsed_time(ev1) / steps
-        if dist is not None:
-            t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        if dist is not None:  # max over ranks
+            t = torch.tensor([ms], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, launches, report, sampler.summary()
 
     # device-resident throughput (value) with live per-kernel event timing
-    ms, launches, report, clocks = timed(lambda: step(dev, merge_async=True), args.steps, profile=True)
-    pending.clear()
-    value = world * rows / (ms / 1000.0)
+    ms, launches, report, clocks = timed(lambda: w.query(runq, dev, args.path, comm), args.steps, profile=True)
+    value = total / (ms / 1000.0)
 
     chain_ms = None
-    if args.path == "fused":
-        chain_ms, _, _, _ = timed(lambda: step(dev, "chain"), max(3, args.steps // 2))
+    if args.path == "fused" and world == 1:
+        chain_ms, _, _, _ = timed(lambda: w.query(runq, dev, "chain"), max(3, args.steps // 2))
 
-    # e2e: upload compressed columns from pinned host memory + query + readback
+    # e2e: upload the shard's compressed columns from pinned host memory +
+    # query + readback of the merged result
     e2e = None
-    if getattr(w, "chunked", False):
+    if w.chunked:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                "note": "not measured: the chunked table is never whole in host memory"}
     elif not args.no_e2e:
-        # only the columns the query reads cross PCIe
-        used = getattr(w, "columns", None) or list(host)
-        pinned = {k: pin_column(host[k]) for k in used}
+        pinned = {k: pin_column(v) for k, v in host.items()}
         h2d = sum(col_bytes(v) for v in pinned.values())
 
         def e2e_step():
             d = {k: runq.upload(v, ctx) for k, v in pinned.items()}
-            return step(d)
+            return w.query(runq, d, args.path, comm)
 
         e2e_ms, _, _, _ = timed(e2e_step, args.steps)
-        e2e = {"value": world * rows / (e2e_ms / 1000.0), "unit": UNIT, "ms_per_step": e2e_ms,
+        e2e = {"value": total / (e2e_ms / 1000.0), "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": result_bytes(v_fused)}
 
-    # roofline of the dominant tagged region (live CUDA-event timing)
+    # roofline of the dominant tagged region (live CUDA-event timing, this rank)
     hbm, peak_kind = peaks()
     roof = None
     if report and w.tag in report:
@@ -828,8 +874,8 @@ def main():
         achieved = ab / (avg_ms / 1000.0) / 1e9
         roof = {"bound": "hbm", "kernel": w.tag, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": ncu_traffic(w.name, w.tag), "alg_bytes_per_launch": ab,
-                "avg_launch_ms": avg_ms, "launches": st["count"], "peak_source": peak_kind,
-                "share_of_step": st["ms"] / (ms * args.steps)}
+                "stats_bytes": w.stats_bytes(host), "avg_launch_ms": avg_ms, "launches": st["count"],
+                "peak_source": peak_kind, "share_of_step": st["ms"] / (ms * args.steps)}
         if w.tag == "xg_rows":  # also the whole query (segment table + masks + row kernel) against its bytes
             w.tag = None
             qb = w.alg_bytes(host)
@@ -841,8 +887,9 @@ def main():
         ab = w.alg_bytes(host)
         achieved = ab / (ms / 1000.0) / 1e9
         roof = {"bound": "hbm", "kernel": "query (operator chain)", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(w.name, "query"), "alg_bytes_per_launch": ab,
-                "avg_launch_ms": ms, "launches": args.steps, "peak_source": peak_kind, "share_of_step": 1.0}
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(w.name, "query"),
+                "alg_bytes_per_launch": ab, "stats_bytes": w.stats_bytes(host), "avg_launch_ms": ms,
+                "launches": args.steps, "peak_source": peak_kind, "share_of_step": 1.0}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -850,19 +897,14 @@ def main():
         ref = refpy.Ref()
         sample_rows = min(rows, {"c3": 5_000_000, "q6": 60_000_000, "q1": 2_000_000,
                                  "c5": 20_000_000}.get(w.name, 200_000_000))
-        from oracle.refpy import shard_column
-        full = getattr(w, "cpu_sample", lambda h, r: None)(host, sample_rows)
-        if full is not None:  # chunked table: a fresh table of the sample size, same generator
-            sample = shard_map(full, 1)
-        else:
-            sample = shard_map({k: shard_column(v, 0, sample_rows) for k, v in host.items()}, 1)
+        sample = shard_map(w.cpu_sample(sample_rows), 1)
         secs = []
         for _ in range(3):
             _, s = w.ref_run(ref, sample, 1)
             secs.append(s)
         sec = statistics.median(secs)
         cpu = {"value": sample_rows / sec, "unit": UNIT, "cores": 1, "kind": "reference",
-               "sample": f"first {sample_rows} rows of the same table, reference operator chain "
+               "sample": f"a {sample_rows}-row table of the same generator, reference operator chain "
                          f"(oracle/_ref) single-threaded, median of 3 ({sec:.2f}s)"}
 
     if rank == 0:
@@ -870,12 +912,17 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
-            "config": config_dict(args, w, rows), "e2e": e2e,
+            "config": config_dict(args, w, rows, world), "e2e": e2e,
             "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
-            "chain_ms_per_step": chain_ms, "result": summarize(v_fused), "oracle_match": oracle_ok,
+            "chain_ms_per_step": chain_ms, "result": w.summary(v_fused), "oracle_match": oracle_ok,
+            "collective": (None if world == 1 else
+                           "library NCCL (rq_comm_init_nccl): grouped all-reduce of partials / all-gather of "
+                           "group tables + device regroup, inside the timed step" if args.comm == "nccl" else
+                           "library host transport over gloo (test mode)"),
             "kernel_times_ms": report,
         }
         print(json.dumps(line), flush=True)
+    del comm
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

@@ -488,6 +488,84 @@ int rq_result_column(rq_result_t r, int32_t i, const char** name, rq_arr_t* valu
 int rq_result_free(rq_result_t r);
 
 /* ---------------------------------------------------------------------- */
+/* boundary completions: the rest of the reference operator surface the    */
+/* reference's own tests and the C++ drop-in adapter call                   */
+/* (paper_2506_10092_b200/adapter/). Shapes (compute::Shape, align.hpp:12-25)*/
+/* cross the ABI as (kind, n, s, e, p): kind 0 dense with n slots, 1 runs   */
+/* s/e (n runs), 2 points p (n points); unused handles are NULL.            */
+/* ---------------------------------------------------------------------- */
+
+/* compute::decompose (align.cpp:86-100); RLE+Index raises RQ_INVALID. */
+int rq_decompose(rq_ctx_t ctx, rq_col_t c, int32_t* kind, int64_t* n, rq_arr_t* s, rq_arr_t* e, rq_arr_t* p,
+                 rq_arr_t* values);
+/* compute::align_many (align.cpp:233-254): the left-fold alignment; values[ncols]. */
+int rq_align_many(rq_ctx_t ctx, const rq_col_t* cols, int32_t ncols, int32_t* kind, int64_t* n, rq_arr_t* s,
+                  rq_arr_t* e, rq_arr_t* p, rq_arr_t* values);
+/* compute::shape_weights (align.cpp:57-70): run lengths or ones. */
+int rq_shape_weights(rq_ctx_t ctx, int32_t kind, int64_t n, rq_arr_t s, rq_arr_t e, rq_arr_t p, rq_arr_t* out);
+/* agg::group (groupby.cpp:46-50) = align_many + unique_with_inverse: the
+ * aligned shape, inverse (group id per slot), keys_out[n_keys], n_groups. */
+int rq_group(rq_ctx_t ctx, const rq_col_t* keys, int32_t n_keys, int32_t* kind, int64_t* n, rq_arr_t* s,
+             rq_arr_t* e, rq_arr_t* p, rq_arr_t* inverse, rq_arr_t* keys_out, int64_t* n_groups);
+/* agg::group_on_arrays (groupby.cpp:33-44) over aligned key arrays (the shape stays with the caller). */
+int rq_group_on_arrays(rq_ctx_t ctx, const rq_arr_t* key_values, int32_t n_keys, rq_arr_t* inverse,
+                       rq_arr_t* keys_out, int64_t* n_groups);
+/* agg::aggregate_array (groupby.cpp:67-135): run-length-weighted SUM /
+ * COUNT / AVG / STD / VAR, MIN / MAX with empty-group sentinels; f64 sums
+ * fold each group in slot order (bit-identical to the reference). */
+int rq_aggregate_array(rq_ctx_t ctx, int32_t kind, int64_t n, rq_arr_t s, rq_arr_t e, rq_arr_t p, rq_arr_t values,
+                       rq_arr_t inverse, int64_t n_groups, int32_t fn, rq_arr_t* out);
+
+/* kernels::Reduce (kernels.hpp:44) */
+enum { RQ_REDUCE_SUM = 0, RQ_REDUCE_MIN = 1, RQ_REDUCE_MAX = 2, RQ_REDUCE_COUNT = 3 };
+/* kernels::scatter_reduce (kernels.cpp:97-125): values fold in input order
+ * per group; out-of-range group index raises RQ_INVALID. */
+int rq_scatter_reduce(rq_ctx_t ctx, rq_arr_t values, rq_arr_t index, int64_t n_groups, int32_t reduce,
+                      rq_arr_t* out);
+/* kernels::unique_with_inverse (kernels.cpp:127-187): keys ascending lexicographic. */
+int rq_unique_with_inverse(rq_ctx_t ctx, const rq_arr_t* cols, int32_t n, rq_arr_t* keys_out, rq_arr_t* inverse,
+                           int64_t* n_groups);
+/* kernels::cumsum / checked_sum (kernels.cpp:21-38): int64 overflow raises RQ_OVERFLOW. */
+int rq_cumsum(rq_ctx_t ctx, rq_arr_t x, int32_t exclusive, rq_arr_t* out);
+int rq_checked_sum(rq_ctx_t ctx, rq_arr_t x, int64_t* out);
+/* kernels::repeat_interleave / range_arange (kernels.cpp:40-60). */
+int rq_repeat_interleave(rq_ctx_t ctx, rq_arr_t values, rq_arr_t counts, rq_arr_t* out);
+int rq_range_arange(rq_ctx_t ctx, rq_arr_t start, rq_arr_t length, rq_arr_t* out);
+/* kernels::gather (kernels.cpp:195-219): out-of-range index raises RQ_INVALID. */
+int rq_gather(rq_ctx_t ctx, rq_arr_t values, rq_arr_t idx, rq_arr_t* out);
+/* kernels::sort_with_perm / adjacent_ne (kernels.cpp:221-245); adjacent_ne is RQ_I8 0/1. */
+int rq_sort_with_perm(rq_ctx_t ctx, rq_arr_t values, rq_arr_t* sorted, rq_arr_t* perm);
+int rq_adjacent_ne(rq_ctx_t ctx, rq_arr_t x, rq_arr_t* out);
+/* enc::range_union / merge_sorted_idx / concat_sort_idx / complement_rle /
+ * complement_index (primitives.cpp:102-167). */
+int rq_range_union(rq_ctx_t ctx, rq_arr_t s1, rq_arr_t e1, rq_arr_t s2, rq_arr_t e2, rq_arr_t* s, rq_arr_t* e);
+int rq_merge_sorted_idx(rq_ctx_t ctx, rq_arr_t p1, rq_arr_t p2, rq_arr_t* out);
+int rq_concat_sort_idx(rq_ctx_t ctx, rq_arr_t p1, rq_arr_t p2, rq_arr_t* out);
+int rq_complement_rle(rq_ctx_t ctx, rq_arr_t s, rq_arr_t e, int64_t total, rq_arr_t* s_out, rq_arr_t* e_out);
+int rq_complement_index(rq_ctx_t ctx, rq_arr_t p, int64_t total, rq_arr_t* s_out, rq_arr_t* e_out);
+/* enc::rle_to_index / rle_to_plain for columns and masks (primitives.cpp:172-220);
+ * an expansion above `budget` elements raises RQ_RESOURCE. */
+int rq_rle_to_index(rq_ctx_t ctx, rq_col_t c, int64_t budget, rq_col_t* out);
+int rq_rle_to_plain(rq_ctx_t ctx, rq_col_t c, double fill, int64_t budget, rq_col_t* out);
+int rq_mask_rle_to_index(rq_ctx_t ctx, rq_mask_t m, int64_t budget, rq_mask_t* out);
+int rq_mask_rle_to_plain(rq_ctx_t ctx, rq_mask_t m, int64_t budget, rq_mask_t* out);
+/* enc::compact_rle_index (primitives.cpp:381-420). */
+int rq_compact_rle_index(rq_ctx_t ctx, rq_col_t c, rq_col_t* out);
+/* decode_full (column.cpp:311-329; gaps raise RQ_INVALID) and to_rows (column.cpp:331-376). */
+int rq_decode_full(rq_ctx_t ctx, rq_col_t c, rq_arr_t* out);
+int rq_to_rows(rq_ctx_t ctx, rq_col_t c, rq_arr_t* positions, rq_arr_t* values);
+/* runq::ColumnStats / stats (column.hpp:162-173, column.cpp:244-279): the
+ * reference's byte accounting (positions at 8 B, RLE run = w + 16 B). */
+typedef struct rq_column_stats {
+  int64_t n_runs;
+  double avg_run_length;
+  int64_t encoded_bytes;
+  int64_t plain_bytes;
+  double compression_ratio;
+} rq_column_stats;
+int rq_col_stats(rq_ctx_t ctx, rq_col_t c, rq_column_stats* out);
+
+/* ---------------------------------------------------------------------- */
 /* row-range sharding (multi-GPU; no reference counterpart)                 */
 /* ---------------------------------------------------------------------- */
 

@@ -203,6 +203,70 @@ def _present(seg: Segments, cnt: np.ndarray, keys_out, vals_out):
 
 
 # ---------------------------------------------------------------------------
+# Partial tables: a configuration's oracle over ONE row range, in merge form
+# (every column a SUM — int64 wrapping or f64 (sum, comp) — or a COUNT), so
+# the oracle of a table cut into shards is merge(partials) → finish. The
+# whole-table oracle is finish(partial(table)).
+# ---------------------------------------------------------------------------
+
+
+class Partial:
+    def __init__(self, keys: List[np.ndarray], parts: list):
+        self.keys, self.parts = keys, parts  # parts: int64 arrays or (sum, comp) f64 pairs
+
+
+def merge(partials: Sequence[Partial]) -> Partial:
+    """Union of the shards' groups, keys ascending; int64 parts wrap, f64
+    parts add (Neumaier pairs kept)."""
+    nk = len(partials[0].keys)
+    if nk == 0:
+        keys, inv, ng = [], [np.zeros(1, np.int64) for _ in partials], 1
+    else:
+        allk = [np.concatenate([p.keys[i].astype(np.float64 if p.keys[i].dtype.kind == "f" else np.int64)
+                                for p in partials]) for i in range(nk)]
+        order = np.lexsort(tuple(reversed(allk)))
+        brk = np.zeros(len(order), bool)
+        if len(order):
+            brk[0] = True
+            for k in allk:
+                ks = k[order]
+                brk[1:] |= ks[1:] != ks[:-1]
+        gid = np.empty(len(order), np.int64)
+        gid[order] = np.cumsum(brk) - 1
+        ng = int(brk.sum())
+        keys = [k[order][brk].astype(partials[0].keys[i].dtype) for i, k in enumerate(allk)]
+        offs = np.cumsum([0] + [len(p.keys[0]) for p in partials])
+        inv = [gid[offs[r]:offs[r + 1]] for r in range(len(partials))]
+    parts = []
+    for j, p0 in enumerate(partials[0].parts):
+        if isinstance(p0, tuple):
+            s, c = np.zeros(ng), np.zeros(ng)
+            for r, p in enumerate(partials):
+                np.add.at(s, inv[r], p.parts[j][0])
+                np.add.at(c, inv[r], p.parts[j][1])
+            parts.append((s, c))
+        else:
+            acc = np.zeros(ng, np.uint64)
+            for r, p in enumerate(partials):
+                np.add.at(acc, inv[r], p.parts[j].astype(np.int64).view(np.uint64))
+            parts.append(acc.view(np.int64))
+    return Partial(keys, parts)
+
+
+def _val(x):
+    return f64_result(x) if isinstance(x, tuple) else x
+
+
+def _finish(p: Partial, spec):
+    """spec: per output column, ("v", j) = part j as is, ("avg", j, c) =
+    part j / part c; the count column of `cnt_at` drops empty groups."""
+    cols = []
+    for sp in spec:
+        cols.append(_val(p.parts[sp[1]]) if sp[0] == "v" else avg(_val(p.parts[sp[1]]), p.parts[sp[2]]))
+    return cols
+
+
+# ---------------------------------------------------------------------------
 # The configurations (each returns (keys, values) like group_aggregate)
 # ---------------------------------------------------------------------------
 
@@ -210,7 +274,8 @@ def _present(seg: Segments, cnt: np.ndarray, keys_out, vals_out):
 class C3Fold:
     """C3: GROUP BY K → SUM(X), COUNT(*), AVG(Z), SUM(Y), SUM(W) over gapless
     columns (every row is in the joint alignment). RLE / RLE+Index inputs
-    fold whole; the plain Z / W fold chunk by chunk via `add_plain_chunk`."""
+    fold whole; the plain Z / W fold chunk by chunk via `add_plain_chunk`
+    (row0 relative to the columns' first row)."""
 
     def __init__(self, so: StreamingOracle, k: H.RleColumn, x: H.RleColumn, y: H.RlePlusIndexColumn):
         self.so = so
@@ -226,19 +291,31 @@ class C3Fold:
         self.so.fold_plain_int(self.seg, z, row0, out=self.sz)
         self.so.fold_plain_f64(self.seg, w, row0, acc=self.sw)
 
+    def partial(self) -> Partial:
+        keys, parts = _present(self.seg, self.cnt, self.seg.keys, [self.sx, self.cnt, self.sz, self.sy])
+        keep = self.cnt > 0
+        return Partial(keys, parts + [(self.sw[0][keep], self.sw[1][keep])])
+
     def result(self):
-        vals = [self.sx, self.cnt, avg(self.sz, self.cnt), self.sy, f64_result(self.sw)]
-        return _present(self.seg, self.cnt, self.seg.keys, vals)
+        return c3_finish(self.partial())
 
 
-def c3(host: Dict[str, H.Column], so: StreamingOracle = None):
+def c3_finish(p: Partial):
+    return p.keys, _finish(p, [("v", 0), ("v", 1), ("avg", 2, 1), ("v", 3), ("v", 4)])
+
+
+def c3_partial(host: Dict[str, H.Column], so: StreamingOracle = None) -> Partial:
     so = so or StreamingOracle()
     f = C3Fold(so, host["k"], host["x"], host["y"])
     f.add_plain_chunk(0, host["z"], host["w"].values)
-    return f.result()
+    return f.partial()
 
 
-def q1(t: Dict[str, H.Column], cutoff: int, so: StreamingOracle = None):
+def c3(host: Dict[str, H.Column], so: StreamingOracle = None):
+    return c3_finish(c3_partial(host, so))
+
+
+def q1_partial(t: Dict[str, H.Column], cutoff: int, so: StreamingOracle = None) -> Partial:
     """Q1 (queries.q1): WHERE shipdate <= cutoff GROUP BY rf, ls → SUM(qty),
     SUM(price), SUM(price·(100−disc)), SUM(price·(100−disc)·(100+tax)),
     AVG(qty), AVG(price), AVG(disc), COUNT(*)."""
@@ -249,15 +326,26 @@ def q1(t: Dict[str, H.Column], cutoff: int, so: StreamingOracle = None):
     price = t["l_extendedprice"].values
     disc, tax = t["l_discount"], t["l_tax"]
     assert disc.center is None and tax.center is None
-    sp = f64_result(so.fold_plain_f64(seg, price))
-    sdp = f64_result(so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100)))
-    sch = f64_result(so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100), f2=(tax.values, 1, 100)))
+    sp = so.fold_plain_f64(seg, price)
+    sdp = so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100))
+    sch = so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100), f2=(tax.values, 1, 100))
     sd = so.fold_plain_int(seg, disc)
-    vals = [sq, sp, sdp, sch, avg(sq, cnt), avg(sp, cnt), avg(sd, cnt), cnt]
-    return _present(seg, cnt, seg.keys, vals)
+    keep = cnt > 0
+    keys, ints = _present(seg, cnt, seg.keys, [sq, sd, cnt])
+    f = [(a[0][keep], a[1][keep]) for a in (sp, sdp, sch)]
+    return Partial(keys, ints + f)  # sq, sd, cnt, sp, sdp, sch
 
 
-def q6(t: Dict[str, H.Column], where, so: StreamingOracle = None) -> float:
+def q1_finish(p: Partial):
+    return p.keys, _finish(p, [("v", 0), ("v", 3), ("v", 4), ("v", 5), ("avg", 0, 2), ("avg", 3, 2),
+                               ("avg", 1, 2), ("v", 2)])
+
+
+def q1(t: Dict[str, H.Column], cutoff: int, so: StreamingOracle = None):
+    return q1_finish(q1_partial(t, cutoff, so))
+
+
+def q6_partial(t: Dict[str, H.Column], where, so: StreamingOracle = None) -> Partial:
     """Q6: SUM(price·disc) under the five RLE conjuncts; disc is RLE in the
     Q6 sort order, so its value is constant over every segment (the
     segments include disc's runs)."""
@@ -267,10 +355,18 @@ def q6(t: Dict[str, H.Column], where, so: StreamingOracle = None) -> float:
     # seg.keys[0][slot] is the discount of each segment
     scale = seg.keys[0][seg.slot].astype(np.float64)
     one = Segments(seg.ss, seg.se, np.zeros(seg.n, np.int64), [], 1)
-    return float(f64_result(so.fold_plain_f64(one, t["l_extendedprice"].values, seg_scale=scale))[0])
+    return Partial([], [so.fold_plain_f64(one, t["l_extendedprice"].values, seg_scale=scale)])
 
 
-def c5(t: Dict[str, H.Column], in_list, lt: int, so: StreamingOracle = None):
+def q6_finish(p: Partial) -> float:
+    return float(_val(p.parts[0])[0])
+
+
+def q6(t: Dict[str, H.Column], where, so: StreamingOracle = None) -> float:
+    return q6_finish(q6_partial(t, where, so))
+
+
+def c5_partial(t: Dict[str, H.Column], in_list, lt: int, so: StreamingOracle = None) -> Partial:
     """C5: WHERE r2 IN (...) AND r3 < lt GROUP BY r4 → SUM(pi0), SUM(p1),
     COUNT(*); pi0 is Plain+Index (base folded as plain, outliers as points
     with the base's decode of 0 subtracted)."""
@@ -282,4 +378,13 @@ def c5(t: Dict[str, H.Column], in_list, lt: int, so: StreamingOracle = None):
     shadow = int(np.int64(0) + np.int64(pi0.base.center or 0))
     so.fold_points(seg, pi0.outliers.p, pi0.outliers.v, shadow, out=s0)
     s1 = so.fold_plain_int(seg, t["p1"])
-    return _present(seg, cnt, seg.keys, [s0, s1, cnt])
+    keys, parts = _present(seg, cnt, seg.keys, [s0, s1, cnt])
+    return Partial(keys, parts)
+
+
+def c5_finish(p: Partial):
+    return p.keys, _finish(p, [("v", 0), ("v", 1), ("v", 2)])
+
+
+def c5(t: Dict[str, H.Column], in_list, lt: int, so: StreamingOracle = None):
+    return c5_finish(c5_partial(t, in_list, lt, so))

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .host import EncodingChoice, Expr, Heuristic, HostColumn, HostMask, JoinSide, Pred, Scalar
+from .host import ColumnStats, EncodingChoice, Expr, Heuristic, HostColumn, HostMask, JoinSide, Pred, Scalar
 
 LIB_PATH = os.environ.get("RQ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "librunq_b200.so")
 
@@ -108,7 +108,51 @@ PROTOTYPES = {
     "rq_result_free": (C.c_int, [vp]),
     "rq_shard_host_column": (C.c_int, [P(HostColumn), i64, i64, P(HostColumn)]),
     "rq_host_column_free": (None, [P(HostColumn)]),
+    "rq_comm_unique_id": (C.c_int, [vp, i64]),
+    "rq_comm_init_nccl": (C.c_int, [vp, vp, i32, i32, P(vp)]),
+    "rq_comm_init_host": (C.c_int, [vp, i32, i32, vp, vp, P(vp)]),
+    "rq_comm_info": (C.c_int, [vp, P(i32), P(i32), P(i32)]),
+    "rq_comm_destroy": (C.c_int, [vp]),
+    "rq_merge_group_tables": (C.c_int, [vp, vp, P(vp), i32, P(vp), P(i32), i32, i64, P(i64), P(vp), P(vp)]),
+    "rq_aggregate_all_sharded": (C.c_int, [vp, vp, vp, i32, P(i32), P(i64), P(C.c_double)]),
+    "rq_aggregate_binop_sharded": (C.c_int, [vp, vp, vp, vp, i32, i32, P(i32), P(i64), P(C.c_double)]),
+    "rq_filtered_aggregate_binop_sharded": (C.c_int, [vp, vp, vp, Scalar, i32, vp, vp, i32, i32, P(i32), P(i64),
+                                                      P(C.c_double)]),
+    "rq_group_aggregate_sharded": (C.c_int, [vp, vp, P(vp), i32, P(vp), P(i32), i32, i32, P(i64), P(vp), P(vp)]),
+    "rq_group_aggregate_where_sharded": (C.c_int, [vp, vp, vp, i32, vp, P(vp), i32, vp, P(i32), i32, P(i64), P(vp),
+                                                   P(vp), P(i32)]),
+    "rq_decompose": (C.c_int, [vp, vp, P(i32), P(i64), P(vp), P(vp), P(vp), P(vp)]),
+    "rq_align_many": (C.c_int, [vp, P(vp), i32, P(i32), P(i64), P(vp), P(vp), P(vp), P(vp)]),
+    "rq_shape_weights": (C.c_int, [vp, i32, i64, vp, vp, vp, P(vp)]),
+    "rq_group": (C.c_int, [vp, P(vp), i32, P(i32), P(i64), P(vp), P(vp), P(vp), P(vp), P(vp), P(i64)]),
+    "rq_group_on_arrays": (C.c_int, [vp, P(vp), i32, P(vp), P(vp), P(i64)]),
+    "rq_aggregate_array": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, i64, i32, P(vp)]),
+    "rq_scatter_reduce": (C.c_int, [vp, vp, vp, i64, i32, P(vp)]),
+    "rq_unique_with_inverse": (C.c_int, [vp, P(vp), i32, P(vp), P(vp), P(i64)]),
+    "rq_cumsum": (C.c_int, [vp, vp, i32, P(vp)]),
+    "rq_checked_sum": (C.c_int, [vp, vp, P(i64)]),
+    "rq_repeat_interleave": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_range_arange": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_gather": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_sort_with_perm": (C.c_int, [vp, vp, P(vp), P(vp)]),
+    "rq_adjacent_ne": (C.c_int, [vp, vp, P(vp)]),
+    "rq_range_union": (C.c_int, [vp, vp, vp, vp, vp, P(vp), P(vp)]),
+    "rq_merge_sorted_idx": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_concat_sort_idx": (C.c_int, [vp, vp, vp, P(vp)]),
+    "rq_complement_rle": (C.c_int, [vp, vp, vp, i64, P(vp), P(vp)]),
+    "rq_complement_index": (C.c_int, [vp, vp, i64, P(vp), P(vp)]),
+    "rq_rle_to_index": (C.c_int, [vp, vp, i64, P(vp)]),
+    "rq_rle_to_plain": (C.c_int, [vp, vp, C.c_double, i64, P(vp)]),
+    "rq_mask_rle_to_index": (C.c_int, [vp, vp, i64, P(vp)]),
+    "rq_mask_rle_to_plain": (C.c_int, [vp, vp, i64, P(vp)]),
+    "rq_compact_rle_index": (C.c_int, [vp, vp, P(vp)]),
+    "rq_decode_full": (C.c_int, [vp, vp, P(vp)]),
+    "rq_to_rows": (C.c_int, [vp, vp, P(vp), P(vp)]),
+    "rq_col_stats": (C.c_int, [vp, vp, P(ColumnStats)]),
 }
+
+# host-transport all-gather callback (include/runq_b200.h rq_host_allgather_fn)
+HOST_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, vp, i64, vp, vp)
 
 
 class RqError(RuntimeError):

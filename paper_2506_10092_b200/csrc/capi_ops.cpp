@@ -409,11 +409,14 @@ int rq_group_aggregate_sharded(rq_ctx_t c, rq_comm_t comm, const rq_col_t* keys,
       d.push_back(&col_of(data[i]));
       f.push_back(fns[i]);
     }
-    GroupAggOut r = sharded(ctx, comm_of(comm), f, [&](const PartialPlan& p) {
-      std::vector<const DCol*> ld;
-      for (int i : p.src) ld.push_back(d[static_cast<size_t>(i)]);
-      return group_aggregate(ctx, k, ld, p.local_fns, normalized != 0);
-    });
+    GroupAggOut r = sharded(
+        ctx, comm_of(comm), f,
+        [&](const PartialPlan& p) {
+          std::vector<const DCol*> ld;
+          for (int i : p.src) ld.push_back(d[static_cast<size_t>(i)]);
+          return group_aggregate(ctx, k, ld, p.local_fns, normalized != 0);
+        },
+        [&](int a, int b) { return d[static_cast<size_t>(a)] == d[static_cast<size_t>(b)]; });
     if (n_groups) *n_groups = r.n_groups;
     for (int i = 0; i < n_keys; ++i) out_keys[i] = wrap_arr(r.keys[static_cast<size_t>(i)]);
     for (int i = 0; i < n_data; ++i) out_vals[i] = wrap_arr(r.vals[static_cast<size_t>(i)]);
@@ -528,11 +531,28 @@ static int group_aggregate_exprs_api(rq_ctx_t c, const rq_pred* where, int32_t n
     const std::vector<XPred>* pp = preds.empty() ? nullptr : &preds;
     GroupAggOut r;
     if (comm) {  // this rank's partials (AVG → SUM, COUNT of the same expression), merged
-      r = sharded(ctx, comm_of(comm), f, [&](const PartialPlan& p) {
-        std::vector<XExpr> lx;
-        for (int i : p.src) lx.push_back(xs[static_cast<size_t>(i)]);
-        return group_aggregate_exprs(ctx, m, k, lx, p.local_fns, &was_fused, pp);
-      });
+      auto same_expr = [&](int a, int b) {
+        const XExpr &x = xs[static_cast<size_t>(a)], &y = xs[static_cast<size_t>(b)];
+        if (x.terms.size() != y.terms.size() || x.ops != y.ops) return false;
+        for (size_t t = 0; t < x.terms.size(); ++t) {
+          const XTerm &u = x.terms[t], &v = y.terms[t];
+          if (u.col != v.col || u.sop != v.sop || u.rev != v.rev || u.k.is_float != v.k.is_float ||
+              u.k.i != v.k.i || std::memcmp(&u.k.f, &v.k.f, 8) != 0)
+            return false;
+        }
+        return true;
+      };
+      r = sharded(
+          ctx, comm_of(comm), f,
+          [&](const PartialPlan& p) {
+            // COUNT partials run as COUNT(*): every aggregate of the GroupAgg
+            // is aligned jointly (runner.cpp:306-336), so they count the same rows
+            std::vector<XExpr> lx;
+            for (size_t j = 0; j < p.src.size(); ++j)
+              lx.push_back(p.local_fns[j] == RQ_COUNT ? XExpr{} : xs[static_cast<size_t>(p.src[j])]);
+            return group_aggregate_exprs(ctx, m, k, lx, p.local_fns, &was_fused, pp);
+          },
+          same_expr);
     } else {
       r = group_aggregate_exprs(ctx, m, k, xs, f, &was_fused, pp);
     }

@@ -329,22 +329,24 @@ GroupAggOut merge_group_tables(const CtxPtr& ctx, Comm& cm, const GroupAggOut& l
 
 // The partial form of a list of aggregate functions: AVG → (SUM, COUNT) of
 // the same input; STD / VAR are not exact under a merge.
-PartialPlan partial_plan(const std::vector<int>& fns) {
+PartialPlan partial_plan(const std::vector<int>& fns, const std::function<bool(int, int)>& same_input) {
   PartialPlan p;
+  // one partial per distinct (function, input); COUNT partials are all the
+  // same — a GroupAgg aligns every input jointly (groupby.cpp:144-162), so
+  // every input has the same rows per group
+  auto find_or_add = [&](int fn, int src) {
+    for (size_t j = 0; j < p.local_fns.size(); ++j)
+      if (p.local_fns[j] == fn && (fn == RQ_COUNT || same_input(p.src[j], src))) return static_cast<int>(j);
+    p.local_fns.push_back(fn);
+    p.src.push_back(src);
+    return static_cast<int>(p.local_fns.size() - 1);
+  };
   for (size_t i = 0; i < fns.size(); ++i) {
     const int f = fns[i];
     require(f != RQ_STD && f != RQ_VAR, "sharded aggregation: STD / VAR do not merge exactly across shards");
     require(f >= RQ_SUM && f <= RQ_AVG, "aggregate: unknown function");
-    p.sum_of.push_back(static_cast<int>(p.local_fns.size()));
-    p.local_fns.push_back(f == RQ_AVG ? RQ_SUM : f);
-    p.src.push_back(static_cast<int>(i));
-    if (f == RQ_AVG) {
-      p.cnt_of.push_back(static_cast<int>(p.local_fns.size()));
-      p.local_fns.push_back(RQ_COUNT);
-      p.src.push_back(static_cast<int>(i));
-    } else {
-      p.cnt_of.push_back(-1);
-    }
+    p.sum_of.push_back(find_or_add(f == RQ_AVG ? RQ_SUM : f, static_cast<int>(i)));
+    p.cnt_of.push_back(f == RQ_AVG ? find_or_add(RQ_COUNT, static_cast<int>(i)) : -1);
   }
   return p;
 }
@@ -366,8 +368,9 @@ GroupAggOut finalize(const CtxPtr& ctx, GroupAggOut merged, const std::vector<in
 }
 
 GroupAggOut sharded(const CtxPtr& ctx, Comm& cm, const std::vector<int>& fns,
-                    const std::function<GroupAggOut(const PartialPlan&)>& local) {
-  PartialPlan p = partial_plan(fns);
+                    const std::function<GroupAggOut(const PartialPlan&)>& local,
+                    const std::function<bool(int, int)>& same_input) {
+  PartialPlan p = partial_plan(fns, same_input ? same_input : [](int a, int b) { return a == b; });
   GroupAggOut part = local(p);
   return finalize(ctx, merge_group_tables(ctx, cm, part, p.local_fns), fns, p);
 }

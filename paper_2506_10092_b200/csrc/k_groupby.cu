@@ -227,11 +227,7 @@ void launched(const CtxPtr& ctx) {
   RQ_CUDA_CHECK(cudaGetLastError());
 }
 
-struct Decomp {
-  int kind = 0;  // 0 dense, 1 run, 2 point
-  int64_t n = 0;
-  DArr s, e, p, values;
-};
+}  // namespace
 
 Decomp decompose_for_group(const CtxPtr& ctx, const DCol& c) {
   Decomp d;
@@ -281,16 +277,9 @@ DCol col_from_decomp(const Decomp& d, const DArr& v, int64_t total) {
   return c;
 }
 
-}  // namespace
-
 // Left-fold alignment of all columns (align_many, align.cpp:233-254): the
 // shape of column 0 is intersected with each next column; accumulated value
 // arrays are re-gathered through the new take indices.
-struct MultiAligned {
-  Decomp shape;
-  std::vector<DArr> values;
-};
-
 MultiAligned align_many(const CtxPtr& ctx, const std::vector<const DCol*>& cols) {
   require(!cols.empty(), "align_many: no columns");
   const int64_t total = cols[0]->total;

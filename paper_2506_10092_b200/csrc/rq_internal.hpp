@@ -529,22 +529,80 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
                            const std::vector<const DCol*>& data, const std::vector<int>& fns,
                            GroupAggOut& out);
 
+// compute::decompose (align.cpp:86-100): shape + values of a basic column
+// (kind 0 dense with n slots, 1 runs s/e, 2 points p); RLE+Index raises.
+struct Decomp {
+  int kind = 0;  // 0 dense, 1 run, 2 point
+  int64_t n = 0;
+  DArr s, e, p, values;
+};
+Decomp decompose_for_group(const CtxPtr& ctx, const DCol& c);
+DCol col_from_decomp(const Decomp& d, const DArr& v, int64_t total);
+// compute::align_many (align.cpp:233-254)
+struct MultiAligned {
+  Decomp shape;
+  std::vector<DArr> values;
+};
+MultiAligned align_many(const CtxPtr& ctx, const std::vector<const DCol*>& cols);
+
+// ---- the rest of the operator API surface (k_boundary.cu) ----------------------------
+
+// kernels::cumsum / checked_sum (kernels.cpp:21-38): exact int64 prefix sums;
+// the first element whose running sum leaves int64 raises RQ_OVERFLOW
+DArr checked_cumsum(const CtxPtr& ctx, const DArr& x, bool exclusive);
+int64_t checked_sum(const CtxPtr& ctx, const DArr& x);
+// kernels::repeat_interleave / range_arange (kernels.cpp:40-60)
+DArr repeat_interleave(const CtxPtr& ctx, const DArr& values, const DArr& counts);
+DArr range_arange(const CtxPtr& ctx, const DArr& start, const DArr& length);
+// kernels::scatter_reduce (kernels.cpp:97-125): op 0 sum, 1 min, 2 max, 3 count;
+// values fold in input order within each group (bit-exact f64 sums)
+DArr scatter_reduce(const CtxPtr& ctx, const DArr& values, const DArr& index, int64_t n_groups, int op);
+// kernels::unique_with_inverse (kernels.cpp:127-187)
+struct Unique {
+  std::vector<DArr> keys;
+  DArr inverse;
+  int64_t n_groups = 0;
+};
+Unique unique_with_inverse(const CtxPtr& ctx, const std::vector<DArr>& cols);
+// kernels::gather with the reference's bounds check (kernels.cpp:189-219)
+DArr gather_checked(const CtxPtr& ctx, const DArr& values, const DArr& idx);
+// kernels::sort_with_perm / adjacent_ne (kernels.cpp:221-245)
+void sort_with_perm(const CtxPtr& ctx, const DArr& values, DArr& sorted, DArr& perm);
+DArr adjacent_ne(const CtxPtr& ctx, const DArr& x);
+// compute::shape_weights (align.cpp:57-70)
+DArr shape_weights(const CtxPtr& ctx, const Decomp& shape);
+// agg::aggregate_array (groupby.cpp:67-135)
+DArr aggregate_array(const CtxPtr& ctx, const Decomp& shape, const DArr& values, const DArr& inverse,
+                     int64_t n_groups, int fn);
+// enc::rle_to_index / rle_to_plain / compact_rle_index (primitives.cpp:172-220, 381-420)
+DCol rle_to_index(const CtxPtr& ctx, const DCol& c, int64_t budget);
+DMask rle_mask_to_index(const CtxPtr& ctx, const DMask& m, int64_t budget);
+DCol rle_to_plain(const CtxPtr& ctx, const DCol& c, double fill, int64_t budget);
+DMask rle_mask_to_plain(const CtxPtr& ctx, const DMask& m, int64_t budget);
+DCol compact_rle_index(const CtxPtr& ctx, const DCol& c);
+// decode_full / to_rows (column.cpp:311-376)
+DArr decode_full(const CtxPtr& ctx, const DCol& c);
+void col_to_rows(const CtxPtr& ctx, const DCol& c, DArr& positions, DArr& values);
+
 // ---- row-range sharded execution (comm.cu) ---------------------------------------
 
 struct Comm;
 Comm& comm_of(rq_comm_t c);
-// AVG → (SUM, COUNT) partials of the same input; local_fns / src per
-// partial, sum_of / cnt_of per original function (cnt_of = -1 unless AVG)
+// AVG → (SUM, COUNT) partials; one partial per distinct (function, input)
+// (same_input(i, j): inputs i and j are the same column / expression);
+// local_fns / src per partial, sum_of / cnt_of per original function
+// (cnt_of = -1 unless AVG)
 struct PartialPlan {
   std::vector<int> local_fns, src, sum_of, cnt_of;
 };
-PartialPlan partial_plan(const std::vector<int>& fns);
+PartialPlan partial_plan(const std::vector<int>& fns, const std::function<bool(int, int)>& same_input);
 GroupAggOut merge_group_tables(const CtxPtr& ctx, Comm& cm, const GroupAggOut& local,
                                const std::vector<int>& part_fns);
 // local(plan) computes this rank's partial table; the result is the merged,
 // finalised table (identical on every rank)
 GroupAggOut sharded(const CtxPtr& ctx, Comm& cm, const std::vector<int>& fns,
-                    const std::function<GroupAggOut(const PartialPlan&)>& local);
+                    const std::function<GroupAggOut(const PartialPlan&)>& local,
+                    const std::function<bool(int, int)>& same_input = nullptr);
 AggOut sharded_scalar(const CtxPtr& ctx, Comm& cm, int fn, const std::function<AggOut(int)>& local);
 
 }  // namespace rqb

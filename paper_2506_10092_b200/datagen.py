@@ -179,9 +179,12 @@ def rle_plus_index(n: int, L: int, point_frac: float, seed: int, lo: int = -1000
     segment is expanded to single-row points with probability point_frac
     (so ~point_frac of the rows are points), else it is one run (the
     heuristic's 'rle+index' shape, ingest.cpp:217-271)."""
-    rng = np.random.default_rng(seed)
-    e = run_ends(n, L, rng)
-    s = np.concatenate([[0], e[:-1] + 1])
+    return _rle_plus_index_rng(np.random.default_rng(seed), n, L, point_frac, lo, hi)
+
+
+def _rle_plus_index_rng(rng, n, L, point_frac, lo=-1000, hi=1000) -> H.RlePlusIndexColumn:
+    e = run_ends(n, L, rng) if n > 0 else np.empty(0, np.int64)
+    s = np.concatenate([[0], e[:-1] + 1]).astype(np.int64) if n > 0 else np.empty(0, np.int64)
     is_pt = rng.random(len(e)) < point_frac
     rs, re_ = s[~is_pt], e[~is_pt]
     rv = rng.integers(lo, hi + 1, len(rs)).astype(np.int64)
@@ -195,38 +198,119 @@ def rle_plus_index(n: int, L: int, point_frac: float, seed: int, lo: int = -1000
     return H.RlePlusIndexColumn(H.RleColumn(rv, rs, re_, n), H.IndexColumn(pv, p.astype(np.int64), n))
 
 
-C3_CHUNK = 1 << 28  # rows per generated chunk of C3's plain columns
+# ---------------------------------------------------------------------------
+# Row-range generation: a table of n rows is a deterministic function of its
+# seed, and any row range [lo, hi) of it can be generated alone (one rank's
+# shard of a table larger than any host, or a 10B-row column streamed into
+# HBM chunk by chunk). Plain columns are positional: chunk c (rows
+# [c·GEN_CHUNK, ...)) comes from its own stream default_rng([seed, c]).
+# Run-encoded columns are either generated whole (few runs) and cut with a
+# slicer (rq_shard_host_column on the device side, the numpy slicer in
+# oracle/refpy on the checker side — the same function, tested equal), or
+# chunk-positional too (runs end at chunk boundaries).
+# ---------------------------------------------------------------------------
+
+GEN_CHUNK = 50_000_000
 
 
-def c3_run_columns(n: int, seed: int = 42):
-    """C3's run-encoded columns: K codes 0..99 RLE L=4096, X RLE i64 L=128,
-    Y RLE+Index (90% of rows in runs L=256, 10% points)."""
+def _chunks(n: int, lo: int, hi: int):
+    for c in range(lo // GEN_CHUNK, (hi - 1) // GEN_CHUNK + 1) if hi > lo else ():
+        r0 = c * GEN_CHUNK
+        yield c, r0, min(GEN_CHUNK, n - r0)
+
+
+def positional(n: int, seed: int, lo: int, hi: int, fn, dtype) -> np.ndarray:
+    """Rows [lo, hi) of a plain column whose chunk c is fn(default_rng([seed, c]), rows)."""
+    parts = []
+    for c, r0, m in _chunks(n, lo, hi):
+        a = fn(np.random.default_rng([seed, c]), m)
+        parts.append(a[max(lo, r0) - r0:min(hi, r0 + m) - r0])
+    return np.concatenate(parts).astype(dtype, copy=False) if parts else np.empty(0, dtype)
+
+
+def _shift(col, off: int, total: int):
+    if isinstance(col, H.RleColumn):
+        return H.RleColumn(col.v, col.s + off, col.e + off, total)
+    if isinstance(col, H.IndexColumn):
+        return H.IndexColumn(col.v, col.p + off, total)
+    if isinstance(col, H.RlePlusIndexColumn):
+        return H.RlePlusIndexColumn(_shift(col.runs, off, total), _shift(col.points, off, total))
+    if isinstance(col, H.PlainPlusIndexColumn):
+        return H.PlainPlusIndexColumn(col.base, _shift(col.outliers, off, total))
+    return col
+
+
+def _concat(cols, total: int):
+    c0 = cols[0]
+    if isinstance(c0, H.RleColumn):
+        return H.RleColumn(np.concatenate([c.v for c in cols]), np.concatenate([c.s for c in cols]),
+                           np.concatenate([c.e for c in cols]), total)
+    if isinstance(c0, H.IndexColumn):
+        return H.IndexColumn(np.concatenate([c.v for c in cols]), np.concatenate([c.p for c in cols]), total)
+    if isinstance(c0, H.RlePlusIndexColumn):
+        return H.RlePlusIndexColumn(_concat([c.runs for c in cols], total), _concat([c.points for c in cols], total))
+    if isinstance(c0, H.PlainPlusIndexColumn):
+        base = H.PlainColumn(np.concatenate([c.base.values for c in cols]), c0.base.logical, c0.base.center)
+        return H.PlainPlusIndexColumn(base, _concat([c.outliers for c in cols], total))
+    return H.PlainColumn(np.concatenate([c.values for c in cols]), c0.logical, c0.center)
+
+
+def positional_column(n: int, seed: int, lo: int, hi: int, fn, slicer=None):
+    """Rows [lo, hi) of a column whose chunk c is the column fn(rng_c, rows)
+    (runs / points end at chunk boundaries), positions rebased to lo."""
+    chunks = list(_chunks(n, lo, hi))
+    if not chunks:
+        return fn(np.random.default_rng([seed, 0]), 0)
+    span0 = chunks[0][1]
+    span = chunks[-1][1] + chunks[-1][2] - span0
+    col = _concat([_shift(fn(np.random.default_rng([seed, c]), m), r0 - span0, span) for c, r0, m in chunks], span)
+    if (lo, hi) == (span0, span0 + span):
+        return col
+    assert slicer is not None, "a range not on chunk boundaries needs a slicer"
+    return slicer(col, lo - span0, hi - span0)
+
+
+def part_range(total: int, part, snap=None):
+    """(lo, hi) of rank `part[0]` of `part[1]` (whole table when part is None),
+    cut points snapped to `snap`'s run boundaries (sharding.plan_cuts)."""
+    if part is None:
+        return 0, total
+    from .sharding import plan_cuts
+    cuts = plan_cuts(total, part[1], snap)
+    return cuts[part[0]], cuts[part[0] + 1]
+
+
+def cut(col, lo: int, hi: int, slicer):
+    if (lo, hi) == (0, col.total_size):
+        return col
+    return slicer(col, lo, hi)
+
+
+def c3_run_columns(n: int, seed: int = 42, part=None, slicer=None):
+    """C3's run-encoded columns over this part's rows: K codes 0..99 RLE
+    L=4096, X RLE i64 L=128 (whole, cut; the cut points snap to X's runs),
+    Y RLE+Index (90% of rows in runs L=256, 10% points; chunk-positional).
+    Returns (k, x, y, lo, hi)."""
     k = gapless_rle(n, 4096, seed, 0, 99)
     x = gapless_rle(n, 128, seed + 1)
-    y = rle_plus_index(n, 256, 0.1, seed + 2)
-    return k, x, y
+    lo, hi = part_range(n, part, x)
+    y = positional_column(n, seed + 2, lo, hi, lambda rng, m: _rle_plus_index_rng(rng, m, 256, 0.1), slicer)
+    return cut(k, lo, hi, slicer), cut(x, lo, hi, slicer), y, lo, hi
 
 
-def c3_plain_chunk(n: int, seed: int, row0: int):
-    """Rows [row0, row0 + C3_CHUNK) ∩ [0, n) of C3's plain columns: Z
-    plain-centered i16 U[-20000, 20000] (logical i64) and W plain f64
-    U[0, 100). Each chunk has its own stream, so a 10B-row table can be
-    generated, uploaded and checked chunk by chunk."""
-    assert row0 % C3_CHUNK == 0
-    m = min(C3_CHUNK, n - row0)
-    rng = np.random.default_rng([seed + 3, row0 // C3_CHUNK])
-    z = rng.integers(-20000, 20001, m, dtype=np.int16)
-    w = rng.uniform(0.0, 100.0, m)
+def c3_plain_rows(n: int, seed: int, lo: int, hi: int):
+    """Rows [lo, hi) of C3's plain columns: Z plain-centered i16
+    U[-20000, 20000] (logical i64) and W plain f64 U[0, 100)."""
+    z = positional(n, seed + 3, lo, hi, lambda r, m: r.integers(-20000, 20001, m, dtype=np.int16), np.int16)
+    w = positional(n, seed + 4, lo, hi, lambda r, m: r.uniform(0.0, 100.0, m), np.float64)
     return z, w
 
 
-def c3_tables(n: int, seed: int = 42):
-    """C3: K, X, Y (c3_run_columns) + Z, W (c3_plain_chunk)."""
-    k, x, y = c3_run_columns(n, seed)
-    parts = [c3_plain_chunk(n, seed, r) for r in range(0, n, C3_CHUNK)]
-    z = H.PlainColumn(np.concatenate([p[0] for p in parts]) if parts else np.empty(0, np.int16), H.I64, 0)
-    w = H.PlainColumn(np.concatenate([p[1] for p in parts]) if parts else np.empty(0))
-    return k, x, y, z, w
+def c3_tables(n: int, seed: int = 42, part=None, slicer=None):
+    """C3: K, X, Y, Z, W over this part's rows."""
+    k, x, y, lo, hi = c3_run_columns(n, seed, part, slicer)
+    z, w = c3_plain_rows(n, seed, lo, hi)
+    return k, x, y, H.PlainColumn(z, H.I64, 0), H.PlainColumn(w)
 
 
 C3_FNS = ["sum", "count", "avg", "sum", "sum"]  # SUM(X), COUNT(*), AVG(Z), SUM(Y), SUM(W)

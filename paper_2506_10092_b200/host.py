@@ -265,6 +265,12 @@ SCHEME_PLAIN, SCHEME_PLAIN_CENTERED, SCHEME_RLE, SCHEME_RLE_INDEX, SCHEME_PLAIN_
 SCHEME_NAMES = {"plain": 0, "plain-centered": 1, "rle": 2, "rle+index": 3, "plain+index": 4}
 
 
+class ColumnStats(C.Structure):
+    """rq_column_stats = runq::ColumnStats (column.hpp:162-168)."""
+    _fields_ = [("n_runs", C.c_int64), ("avg_run_length", C.c_double), ("encoded_bytes", C.c_int64),
+                ("plain_bytes", C.c_int64), ("compression_ratio", C.c_double)]
+
+
 class Heuristic(C.Structure):
     """runq::io::HeuristicConfig (ingest.hpp:41-48), reference defaults."""
     _fields_ = [("row_threshold", C.c_int64), ("ratio_threshold", C.c_double), ("trim", C.c_double),

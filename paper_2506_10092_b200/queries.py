@@ -26,7 +26,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import host as H
-from .datagen import run_ends
+from .datagen import cut, part_range, positional, positional_column, run_ends
 
 ROWS_PER_SF = 6_000_000
 SHIP_LO, SHIP_HI = 8036, 10561      # 1992-01-02 .. 1998-12-01
@@ -60,9 +60,11 @@ def _rle_from_counts(values: np.ndarray, counts: np.ndarray, total: int) -> H.Rl
     return H.RleColumn(values.astype(np.int64), s.astype(np.int64), e.astype(np.int64), total)
 
 
-def lineitem_q6(n: int, seed: int = 42):
+def lineitem_q6(n: int, seed: int = 42, part=None, slicer=None):
     """Lineitem sorted by (quantity, discount, shipdate); the sorted key
-    columns are generated directly as runs (multinomial group sizes)."""
+    columns are generated directly as runs (multinomial group sizes) over the
+    whole table and cut to this part's rows (snapped to shipdate's runs);
+    price is positional (datagen.positional)."""
     rng = np.random.default_rng(seed)
     days = np.arange(SHIP_LO, SHIP_HI + 1, dtype=np.int64)
     qc = rng.multinomial(n, np.full(50, 1 / 50))
@@ -75,19 +77,23 @@ def lineitem_q6(n: int, seed: int = 42):
             sc = rng.multinomial(dc[d], np.full(len(days), 1 / len(days)))
             svals.append(days)
             scounts.append(sc)
-    price = rng.uniform(900.0, 105000.0, n)
+    ship = _rle_from_counts(np.concatenate(svals), np.concatenate(scounts), n)
+    lo, hi = part_range(n, part, ship)
+    price = positional(n, seed + 1, lo, hi, lambda r, m: r.uniform(900.0, 105000.0, m), np.float64)
     return {
-        "l_quantity": _rle_from_counts(np.arange(1, 51), qc, n),
-        "l_discount": _rle_from_counts(np.concatenate(dvals), np.concatenate(dcounts), n),
-        "l_shipdate": _rle_from_counts(np.concatenate(svals), np.concatenate(scounts), n),
+        "l_quantity": cut(_rle_from_counts(np.arange(1, 51), qc, n), lo, hi, slicer),
+        "l_discount": cut(_rle_from_counts(np.concatenate(dvals), np.concatenate(dcounts), n), lo, hi, slicer),
+        "l_shipdate": cut(ship, lo, hi, slicer),
         "l_extendedprice": H.PlainColumn(price),
     }
 
 
-def lineitem_q1(n: int, seed: int = 43):
+def lineitem_q1(n: int, seed: int = 43, part=None, slicer=None):
     """Lineitem sorted by (returnflag, linestatus, shipdate, quantity):
     linestatus 'O' (1) iff shipdate > 1995-06-17, returnflag 'N' (1) for open
-    lines else 'A' (0) / 'R' (2)."""
+    lines else 'A' (0) / 'R' (2). Sorted key columns as runs (whole table, cut
+    to this part's rows, snapped to quantity's runs); discount / tax / price
+    positional."""
     rng = np.random.default_rng(seed)
     days = np.arange(SHIP_LO, SHIP_HI + 1, dtype=np.int64)
     dc = rng.multinomial(n, np.full(len(days), 1 / len(days)))
@@ -109,15 +115,17 @@ def lineitem_q1(n: int, seed: int = 43):
         for c in cnt[cnt > 0]:
             qv.append(np.arange(1, 51))
             qc.append(rng.multinomial(c, np.full(50, 1 / 50)))
-    disc = rng.integers(0, 11, n).astype(np.int8)
-    tax = rng.integers(0, 9, n).astype(np.int8)
-    price = rng.uniform(900.0, 105000.0, n)
     cat = lambda xs: np.concatenate([np.asarray(x) for x in xs])
+    qty = _rle_from_counts(cat(qv), cat(qc), n)
+    lo, hi = part_range(n, part, qty)
+    disc = positional(n, seed + 1, lo, hi, lambda r, m: r.integers(0, 11, m).astype(np.int8), np.int8)
+    tax = positional(n, seed + 2, lo, hi, lambda r, m: r.integers(0, 9, m).astype(np.int8), np.int8)
+    price = positional(n, seed + 3, lo, hi, lambda r, m: r.uniform(900.0, 105000.0, m), np.float64)
     return {
-        "l_returnflag": _rle_from_counts(cat(rfv), cat(rfc), n),
-        "l_linestatus": _rle_from_counts(cat(lsv), cat(lsc), n),
-        "l_shipdate": _rle_from_counts(cat(shv), cat(shc), n),
-        "l_quantity": _rle_from_counts(cat(qv), cat(qc), n),
+        "l_returnflag": cut(_rle_from_counts(cat(rfv), cat(rfc), n), lo, hi, slicer),
+        "l_linestatus": cut(_rle_from_counts(cat(lsv), cat(lsc), n), lo, hi, slicer),
+        "l_shipdate": cut(_rle_from_counts(cat(shv), cat(shc), n), lo, hi, slicer),
+        "l_quantity": cut(qty, lo, hi, slicer),
         "l_discount": H.PlainColumn(disc, H.I64),
         "l_tax": H.PlainColumn(tax, H.I64),
         "l_extendedprice": H.PlainColumn(price),
@@ -146,7 +154,6 @@ Q1_FNS = ["sum", "sum", "sum", "sum", "avg", "avg", "avg", "count"]
 # ---------------------------------------------------------------------------
 
 def _code_runs(n: int, avg: float, card: int, rng, dtype=np.int32) -> H.RleColumn:
-    from .datagen import run_ends
     if avg >= n:
         return H.RleColumn(np.array([7], dtype), [0], [n - 1], n)
     e = run_ends(n, max(1, int(round(avg))), rng)
@@ -154,7 +161,7 @@ def _code_runs(n: int, avg: float, card: int, rng, dtype=np.int32) -> H.RleColum
     return H.RleColumn(rng.integers(0, card, len(e)).astype(dtype), s, e, n)
 
 
-def _plain_index(n: int, rng, frac: float = 0.01) -> H.PlainPlusIndexColumn:
+def _plain_index(rng, n: int, frac: float = 0.01) -> H.PlainPlusIndexColumn:
     """i16 base (centre 0) + ~1% wide i64 outliers shadowing it (ingest.cpp
     plain_to_plain_index shape: base holds 0 at outlier rows)."""
     base = rng.integers(-30000, 30001, n).astype(np.int16)
@@ -164,27 +171,38 @@ def _plain_index(n: int, rng, frac: float = 0.01) -> H.PlainPlusIndexColumn:
     return H.PlainPlusIndexColumn(H.PlainColumn(base, H.I64, 0), H.IndexColumn(ov, p, n))
 
 
-def production_table(n: int, seed: int = 5):
+# C5 columns: RLE i32 dictionary codes (average run, cardinality), one single
+# run, one with average run 34.41 (the paper's heaviest RLE column)
+C5_RLE = {"r0": (None, 1), "r1": (34.41, 1000), "r2": (1e3, 100), "r3": (5e3, 100), "r4": (2e4, 50),
+          "r5": (1e5, 20), "r6": (3e5, 10)}
+# bit-width-reduced plain: (storage dtype, lo, hi, centre)
+C5_PLAIN = {"p0": (np.int8, -100, 100, 1000), "p1": (np.int16, -20000, 20000, 50_000),
+            "p2": (np.int32, -(1 << 30), (1 << 30) - 1, 0), "p3": (np.int16, -300, 300, None)}
+
+
+def production_table(n: int, seed: int = 5, part=None, slicer=None, columns=None):
     """15 columns: 7 RLE i32 dictionary-code columns (one single run, one with
     average run 34.41 — the paper's heaviest RLE column, others 1e3..3e5),
     4 Plain+Index (i16 + 1% i64 outliers), 4 bit-width-reduced plain
-    (i8 / i16 / i32 / i16 with centres)."""
-    rng = np.random.default_rng(seed)
-    t = {
-        "r0": _code_runs(n, n, 1, rng),
-        "r1": _code_runs(n, 34.41, 1000, rng),
-        "r2": _code_runs(n, 1e3, 100, rng),
-        "r3": _code_runs(n, 5e3, 100, rng),
-        "r4": _code_runs(n, 2e4, 50, rng),
-        "r5": _code_runs(n, 1e5, 20, rng),
-        "r6": _code_runs(n, 3e5, 10, rng),
-    }
+    (i8 / i16 / i32 / i16 with centres). Every column has its own stream
+    (RLE: whole table, cut to the part, cuts snapped to r2's runs; plain /
+    Plain+Index: positional); `columns` limits what is generated."""
+    names = columns or (list(C5_RLE) + [f"pi{i}" for i in range(4)] + list(C5_PLAIN))
+    t = {}
+    for i, c in enumerate(C5_RLE):
+        if c in names or c == "r2":
+            avg, card = C5_RLE[c]
+            t[c] = _code_runs(n, n if avg is None else avg, card, np.random.default_rng([seed, 100 + i]))
+    lo, hi = part_range(n, part, t["r2"])
+    t = {c: cut(v, lo, hi, slicer) for c, v in t.items() if c in names}
     for i in range(4):
-        t[f"pi{i}"] = _plain_index(n, rng)
-    t["p0"] = H.PlainColumn(rng.integers(-100, 101, n).astype(np.int8), H.I64, 1000)
-    t["p1"] = H.PlainColumn(rng.integers(-20000, 20001, n).astype(np.int16), H.I64, 50_000)
-    t["p2"] = H.PlainColumn(rng.integers(-(1 << 30), 1 << 30, n).astype(np.int32), H.I64, 0)
-    t["p3"] = H.PlainColumn(rng.integers(-300, 301, n).astype(np.int16), H.I64, None)
+        if f"pi{i}" in names:
+            t[f"pi{i}"] = positional_column(n, seed * 1000 + 10 + i, lo, hi, lambda r, m: _plain_index(r, m), slicer)
+    for j, (c, (dt, a, b, centre)) in enumerate(C5_PLAIN.items()):
+        if c in names:
+            v = positional(n, seed * 1000 + 20 + j, lo, hi, lambda r, m, a=a, b=b, dt=dt: r.integers(a, b + 1, m).astype(dt),
+                           dt)
+            t[c] = H.PlainColumn(v, H.I64, centre)
     return t
 
 
@@ -243,25 +261,27 @@ Q6_WHERE = [("l_shipdate", ">=", Q6_LO), ("l_shipdate", "<", Q6_HI), ("l_discoun
             ("l_discount", "<=", 7), ("l_quantity", "<", 24)]
 
 
-def q6_fused(rq, t):
+def q6_fused(rq, t, comm=None):
     """WHERE pushed into the fused call (conjuncts on RLE columns are
-    evaluated per run segment; no mask is materialised)."""
+    evaluated per run segment; no mask is materialised). `comm`: this rank's
+    shard, merged over the communicator."""
     X = rq.X
     _, vs, _, fused = rq.agg.group_aggregate_exprs(
         None, [], [X.col(t["l_extendedprice"]).arith(X.col(t["l_discount"]), "*")], ["sum"],
-        where=[(t[c], op, k) for c, op, k in Q6_WHERE])
+        where=[(t[c], op, k) for c, op, k in Q6_WHERE], **({"comm": comm} if comm is not None else {}))
     v = vs[0]
     return (float(v.download()[0]) if hasattr(v, "download") else float(v[0])), fused
 
 
-def q1_fused(rq, t):
+def q1_fused(rq, t, comm=None):
     X = rq.X
     price, disc, tax, qty = (t[k] for k in ("l_extendedprice", "l_discount", "l_tax", "l_quantity"))
     disc_price = X.col(price).arith(X.col(disc).scalar(100, "-", True), "*")
     charge = disc_price.arith(X.col(tax).scalar(100, "+"), "*")
     exprs = [X.col(qty), X.col(price), disc_price, charge, X.col(qty), X.col(price), X.col(disc), X.count()]
     ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [t["l_returnflag"], t["l_linestatus"]], exprs, Q1_FNS,
-                                                     where=[(t["l_shipdate"], "<=", Q1_CUTOFF)])
+                                                     where=[(t["l_shipdate"], "<=", Q1_CUTOFF)],
+                                                     **({"comm": comm} if comm is not None else {}))
     return (ks, vs, ng), fused
 
 
@@ -274,9 +294,10 @@ def c5_mask(api, t):
     return M.and_mask(m_in, C.compare_scalar(t["r3"], C5_LT, "<"))
 
 
-def c5_fused(rq, t):
+def c5_fused(rq, t, comm=None):
     X = rq.X
     ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [t["r4"]],
                                                      [X.col(t["pi0"]), X.col(t["p1"]), X.count()], C5_FNS,
-                                                     where=[(t["r2"], "in", C5_IN), (t["r3"], "<", C5_LT)])
+                                                     where=[(t["r2"], "in", C5_IN), (t["r3"], "<", C5_LT)],
+                                                     **({"comm": comm} if comm is not None else {}))
     return (ks, vs, ng), fused

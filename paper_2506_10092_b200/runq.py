@@ -18,7 +18,7 @@ from typing import List, Sequence, Tuple
 import numpy as np
 
 from . import host as H
-from ._lib import check, load
+from ._lib import RqDeviceError, RqError, RqOverflowError, RqResourceError, check, load  # noqa: F401
 
 _L = load()
 
@@ -273,6 +273,59 @@ def _new():
     return C.c_void_p()
 
 
+def _arr_in(x, ctx, dtype=None):
+    """numpy / list → device array (int64 unless the array has a dtype)."""
+    if isinstance(x, DeviceArray):
+        return x
+    a = np.asarray(x) if dtype is None else np.asarray(x, dtype)
+    if a.dtype == np.bool_:
+        a = a.astype(np.int8)
+    if dtype is None and a.dtype.kind in "iu" and a.dtype not in (np.int8, np.int16, np.int32, np.int64):
+        a = a.astype(np.int64)
+    return upload(np.ascontiguousarray(a), ctx)
+
+
+def _arr_call(fn, ins, n_out, *scalars, dtype=np.int64, ctx=None):
+    """Calls fn(ctx, *in_handles, *scalars, *out_ptrs) and returns the outputs
+    (host arrays when any input was host, else device arrays)."""
+    host = _is_host(*ins)
+    ctx = ctx or _ctx_of(*ins)
+    da = [_arr_in(x, ctx, dtype) for x in ins]
+    outs = [_new() for _ in range(n_out)]
+    check(fn(ctx.handle, *[a.handle for a in da], *scalars, *[C.byref(o) for o in outs]))
+    res = tuple(_out(DeviceArray(o, ctx), host) if o.value else None for o in outs)
+    return res[0] if n_out == 1 else res
+
+
+class Shape:
+    """compute::Shape (align.hpp:12-25): kind "dense" (n slots), "run" (s, e)
+    or "point" (p)."""
+
+    KINDS = ("dense", "run", "point")
+
+    def __init__(self, kind, n=0, s=None, e=None, p=None):
+        self.kind, self.n, self.s, self.e, self.p = kind, n, s, e, p
+
+    @classmethod
+    def _from(cls, kind, n, s, e, p, ctx, host):
+        k = cls.KINDS[kind.value]
+        get = lambda h: _out(DeviceArray(h, ctx), host) if h.value else None  # noqa: E731
+        return cls(k, int(n.value), get(s), get(e), get(p))
+
+    def _args(self, ctx):
+        h = lambda x: _arr_in(x, ctx).handle if x is not None else None  # noqa: E731
+        keep = [self.s, self.e, self.p]
+        return (C.c_int32(self.KINDS.index(self.kind)), C.c_int64(int(self.n if self.kind == "dense" else 0)),
+                h(keep[0]), h(keep[1]), h(keep[2]))
+
+    def __repr__(self):
+        return f"Shape({self.kind}, n={self.n})"
+
+
+def _shape_outs():
+    return C.c_int32(), C.c_int64(), _new(), _new(), _new()
+
+
 # ---------------------------------------------------------------------------
 # runq::enc (primitives.hpp:28-92) and runq::kernels (kernels.hpp:13-72)
 # ---------------------------------------------------------------------------
@@ -383,6 +436,79 @@ class enc:
         check(_L.rq_plain_to_plain_index(ctx.handle, dc.handle, float(trim_fraction), C.byref(o)))
         return _out(DeviceColumn(o, ctx), host)
 
+    @staticmethod
+    def range_union(s1, e1, s2, e2):
+        """enc::range_union (primitives.cpp:102-123) -> (s, e)."""
+        return _arr_call(_L.rq_range_union, (s1, e1, s2, e2), 2)
+
+    @staticmethod
+    def merge_sorted_idx(p1, p2):
+        """enc::merge_sorted_idx (primitives.cpp:125-131)."""
+        return _arr_call(_L.rq_merge_sorted_idx, (p1, p2), 1)
+
+    @staticmethod
+    def concat_sort_idx(p1, p2):
+        """enc::concat_sort_idx (primitives.cpp:133-139)."""
+        return _arr_call(_L.rq_concat_sort_idx, (p1, p2), 1)
+
+    @staticmethod
+    def complement_rle(s, e, total: int):
+        """enc::complement_rle (primitives.cpp:141-154) -> (s, e)."""
+        host = _is_host(s, e)
+        ctx = _ctx_of(s, e)
+        a, b = _arr_in(s, ctx, np.int64), _arr_in(e, ctx, np.int64)
+        so, eo = _new(), _new()
+        check(_L.rq_complement_rle(ctx.handle, a.handle, b.handle, C.c_int64(total), C.byref(so), C.byref(eo)))
+        return _out(DeviceArray(so, ctx), host), _out(DeviceArray(eo, ctx), host)
+
+    @staticmethod
+    def complement_index(p, total: int):
+        """enc::complement_index (primitives.cpp:156-167) -> (s, e)."""
+        host = _is_host(p)
+        ctx = _ctx_of(p)
+        a = _arr_in(p, ctx, np.int64)
+        so, eo = _new(), _new()
+        check(_L.rq_complement_index(ctx.handle, a.handle, C.c_int64(total), C.byref(so), C.byref(eo)))
+        return _out(DeviceArray(so, ctx), host), _out(DeviceArray(eo, ctx), host)
+
+    BUDGET = 1 << 33  # kDefaultElementBudget (primitives.hpp:12)
+
+    @staticmethod
+    def rle_to_index(c, budget: int = BUDGET):
+        """enc::rle_to_index (primitives.cpp:172-192) for an RLE column or mask."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        d = upload(c, ctx)
+        o = _new()
+        if isinstance(d, DeviceMask):
+            check(_L.rq_mask_rle_to_index(ctx.handle, d.handle, C.c_int64(budget), C.byref(o)))
+            return _out(DeviceMask(o, ctx), host)
+        check(_L.rq_rle_to_index(ctx.handle, d.handle, C.c_int64(budget), C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
+    def rle_to_plain(c, fill: float = 0.0, budget: int = BUDGET):
+        """enc::rle_to_plain (primitives.cpp:194-218) for an RLE column or mask."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        d = upload(c, ctx)
+        o = _new()
+        if isinstance(d, DeviceMask):
+            check(_L.rq_mask_rle_to_plain(ctx.handle, d.handle, C.c_int64(budget), C.byref(o)))
+            return _out(DeviceMask(o, ctx), host)
+        check(_L.rq_rle_to_plain(ctx.handle, d.handle, C.c_double(fill), C.c_int64(budget), C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
+    @staticmethod
+    def compact_rle_index(c):
+        """enc::compact_rle_index (primitives.cpp:381-420)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        d = upload(c, ctx)
+        o = _new()
+        check(_L.rq_compact_rle_index(ctx.handle, d.handle, C.byref(o)))
+        return _out(DeviceColumn(o, ctx), host)
+
 
 class io:
     """runq::io encoding selection and table sort (ingest.hpp:29-66), on the device."""
@@ -446,6 +572,93 @@ class kernels:
         check(_L.rq_bucketize(ctx.handle, a.handle, b.handle, 1 if right else 0, C.byref(o)))
         return _out(DeviceArray(o, ctx), host)
 
+    SUM, MIN, MAX, COUNT = range(4)  # kernels::Reduce (kernels.hpp:44)
+
+    @staticmethod
+    def cumsum(x, exclusive: bool):
+        """kernels::cumsum (kernels.cpp:21-31); int64 overflow raises RqOverflowError."""
+        return _arr_call(_L.rq_cumsum, (x,), 1, C.c_int32(1 if exclusive else 0))
+
+    @staticmethod
+    def checked_sum(x) -> int:
+        """kernels::checked_sum (kernels.cpp:33-38)."""
+        ctx = _ctx_of(x)
+        a = _arr_in(x, ctx, np.int64)
+        out = C.c_int64()
+        check(_L.rq_checked_sum(ctx.handle, a.handle, C.byref(out)))
+        return int(out.value)
+
+    @staticmethod
+    def repeat_interleave(values, counts):
+        """kernels::repeat_interleave (kernels.cpp:40-45)."""
+        host = _is_host(values, counts)
+        ctx = _ctx_of(values, counts)
+        v, c = _arr_in(values, ctx), _arr_in(counts, ctx, np.int64)
+        o = _new()
+        check(_L.rq_repeat_interleave(ctx.handle, v.handle, c.handle, C.byref(o)))
+        return _out(DeviceArray(o, ctx), host)
+
+    @staticmethod
+    def range_arange(start, length):
+        """kernels::range_arange (kernels.cpp:47-60)."""
+        return _arr_call(_L.rq_range_arange, (start, length), 1)
+
+    @staticmethod
+    def scatter_reduce(values, index, n_groups: int, op):
+        """kernels::scatter_reduce (kernels.cpp:97-125); op = kernels.SUM/MIN/MAX/COUNT
+        or its name."""
+        op = {"sum": 0, "min": 1, "max": 2, "count": 3}.get(op, op)
+        host = _is_host(values, index)
+        ctx = _ctx_of(values, index)
+        v, i = _arr_in(values, ctx), _arr_in(index, ctx, np.int64)
+        o = _new()
+        check(_L.rq_scatter_reduce(ctx.handle, v.handle, i.handle, C.c_int64(n_groups), C.c_int32(op), C.byref(o)))
+        return _out(DeviceArray(o, ctx), host)
+
+    @staticmethod
+    def unique_with_inverse(columns):
+        """kernels::unique_with_inverse (kernels.cpp:127-187) -> (keys, inverse, n_groups)."""
+        host = _is_host(*columns)
+        ctx = _ctx_of(*columns)
+        ds = [_arr_in(c, ctx) for c in columns]
+        arr = (C.c_void_p * max(1, len(ds)))(*[d.handle.value for d in ds])
+        ko = (C.c_void_p * max(1, len(ds)))()
+        inv, ng = _new(), C.c_int64()
+        check(_L.rq_unique_with_inverse(ctx.handle, arr, len(ds), ko, C.byref(inv), C.byref(ng)))
+        keys = [_out(DeviceArray(C.c_void_p(ko[i]), ctx), host) for i in range(len(ds))]
+        return keys, _out(DeviceArray(inv, ctx), host), int(ng.value)
+
+    @staticmethod
+    def gather(values, idx):
+        """kernels::gather (kernels.cpp:195-219); out-of-range raises RqError."""
+        host = _is_host(values, idx)
+        ctx = _ctx_of(values, idx)
+        v, i = _arr_in(values, ctx), _arr_in(idx, ctx, np.int64)
+        o = _new()
+        check(_L.rq_gather(ctx.handle, v.handle, i.handle, C.byref(o)))
+        return _out(DeviceArray(o, ctx), host)
+
+    @staticmethod
+    def sort_with_perm(values):
+        """kernels::sort_with_perm (kernels.cpp:221-233) -> (sorted, perm)."""
+        host = _is_host(values)
+        ctx = _ctx_of(values)
+        v = _arr_in(values, ctx)
+        so, pe = _new(), _new()
+        check(_L.rq_sort_with_perm(ctx.handle, v.handle, C.byref(so), C.byref(pe)))
+        return _out(DeviceArray(so, ctx), host), _out(DeviceArray(pe, ctx), host)
+
+    @staticmethod
+    def adjacent_ne(x):
+        """kernels::adjacent_ne (kernels.cpp:235-245) -> uint8 0/1."""
+        host = _is_host(x)
+        ctx = _ctx_of(x)
+        v = _arr_in(x, ctx)
+        o = _new()
+        check(_L.rq_adjacent_ne(ctx.handle, v.handle, C.byref(o)))
+        r = _out(DeviceArray(o, ctx), host)
+        return r.view(np.uint8) if host else r
+
 
 # ---------------------------------------------------------------------------
 # column model helpers
@@ -462,6 +675,40 @@ def decode_values(c):
     return _out(DeviceArray(o, ctx), host)
 
 
+def _host_arr(x):
+    return x.download() if isinstance(x, DeviceArray) else np.asarray(x)
+
+
+def decode_full(c):
+    """decode_full (column.cpp:311-329): values of a gap-free column (gaps raise RqError)."""
+    host = _is_host(c)
+    ctx = _ctx_of(c)
+    dc = upload(c, ctx)
+    o = _new()
+    check(_L.rq_decode_full(ctx.handle, dc.handle, C.byref(o)))
+    return _out(DeviceArray(o, ctx), host)
+
+
+def to_rows(c):
+    """to_rows (column.cpp:331-376) -> (positions, values) of the covered rows."""
+    host = _is_host(c)
+    ctx = _ctx_of(c)
+    dc = upload(c, ctx)
+    p, v = _new(), _new()
+    check(_L.rq_to_rows(ctx.handle, dc.handle, C.byref(p), C.byref(v)))
+    return _out(DeviceArray(p, ctx), host), _out(DeviceArray(v, ctx), host)
+
+
+def stats(c) -> dict:
+    """stats (column.cpp:244-279): the reference's byte accounting."""
+    ctx = _ctx_of(c)
+    dc = upload(c, ctx)
+    st = H.ColumnStats()
+    check(_L.rq_col_stats(ctx.handle, dc.handle, C.byref(st)))
+    return {"n_runs": st.n_runs, "avg_run_length": st.avg_run_length, "encoded_bytes": st.encoded_bytes,
+            "plain_bytes": st.plain_bytes, "compression_ratio": st.compression_ratio}
+
+
 # ---------------------------------------------------------------------------
 # runq::compute (align.hpp:59-95)
 # ---------------------------------------------------------------------------
@@ -469,6 +716,43 @@ def decode_values(c):
 
 class compute:
     DENSE, RUN, POINT = 0, 1, 2
+    Shape = Shape
+
+    @staticmethod
+    def decompose(c):
+        """compute::decompose (align.cpp:86-100) -> (Shape, values)."""
+        host = _is_host(c)
+        ctx = _ctx_of(c)
+        dc = upload(c, ctx)
+        k, n, ps, pe, pp = _shape_outs()
+        v = _new()
+        check(_L.rq_decompose(ctx.handle, dc.handle, C.byref(k), C.byref(n), C.byref(ps), C.byref(pe), C.byref(pp),
+                              C.byref(v)))
+        return Shape._from(k, n, ps, pe, pp, ctx, host), _out(DeviceArray(v, ctx), host)
+
+    @staticmethod
+    def align_many(cols):
+        """compute::align_many (align.cpp:233-254) -> (Shape, [values per column])."""
+        host = _is_host(*cols)
+        ctx = _ctx_of(*cols)
+        dcs = [upload(c, ctx) for c in cols]
+        arr = (C.c_void_p * len(dcs))(*[d.handle.value for d in dcs])
+        vals = (C.c_void_p * len(dcs))()
+        k, n, ps, pe, pp = _shape_outs()
+        check(_L.rq_align_many(ctx.handle, arr, len(dcs), C.byref(k), C.byref(n), C.byref(ps), C.byref(pe),
+                               C.byref(pp), vals))
+        return (Shape._from(k, n, ps, pe, pp, ctx, host),
+                [_out(DeviceArray(C.c_void_p(vals[i]), ctx), host) for i in range(len(dcs))])
+
+    @staticmethod
+    def shape_weights(sh: Shape):
+        """compute::shape_weights (align.cpp:57-70)."""
+        ins = [x for x in (sh.s, sh.e, sh.p) if x is not None]
+        host = _is_host(*ins) if ins else True
+        ctx = _ctx_of(*ins)
+        o = _new()
+        check(_L.rq_shape_weights(ctx.handle, *sh._args(ctx), C.byref(o)))
+        return _out(DeviceArray(o, ctx), host)
 
     @staticmethod
     def normalize_basic(c):
@@ -719,6 +1003,61 @@ class joins:
         return _out(DeviceMask(o, ctx), host)
 
 
+class Comm:
+    """rq_comm_t: the ranks of a row-range sharded table.
+
+    ``Comm.nccl(ctx, uid, nranks, rank)`` — one rank per GPU over NCCL (rank 0
+    makes ``uid = Comm.unique_id()`` and the launcher broadcasts it);
+    ``Comm.host(ctx, nranks, rank, allgather)`` — the host transport, where
+    ``allgather(bytes) -> list[bytes]`` (one entry per rank) moves the
+    packets, e.g. over torch.distributed gloo with several ranks on one GPU."""
+
+    def __init__(self, handle, ctx, keep=None):
+        self.handle, self.ctx, self._keep = handle, ctx, keep
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(_L.rq_comm_unique_id(buf, 128))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, ctx: Context, uid: bytes, nranks: int, rank: int) -> "Comm":
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        check(_L.rq_comm_init_nccl(ctx.handle, buf, nranks, rank, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def host(cls, ctx: Context, nranks: int, rank: int, allgather) -> "Comm":
+        from ._lib import HOST_ALLGATHER_FN
+
+        def cb(send, nbytes, recv, user):
+            try:
+                parts = allgather(C.string_at(send, nbytes) if nbytes else b"")
+                blob = b"".join(parts)
+                assert len(blob) == nbytes * nranks
+                if blob:
+                    C.memmove(recv, blob, len(blob))
+                return 0
+            except Exception:  # noqa: BLE001 — reported as RQ_NCCL by the library
+                return 1
+        fn = HOST_ALLGATHER_FN(cb)
+        h = C.c_void_p()
+        check(_L.rq_comm_init_host(ctx.handle, nranks, rank, fn, None, C.byref(h)))
+        return cls(h, ctx, keep=fn)
+
+    def info(self):
+        n, r, t = C.c_int32(), C.c_int32(), C.c_int32()
+        check(_L.rq_comm_info(self.handle, C.byref(n), C.byref(r), C.byref(t)))
+        return int(n.value), int(r.value), ("nccl", "host")[t.value]
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _L.rq_comm_destroy(self.handle)
+            self.handle = None
+
+
 def _agg_result(dt, i, f):
     return float(f.value) if dt.value == H.F64 else int(i.value)
 
@@ -726,18 +1065,86 @@ def _agg_result(dt, i, f):
 class agg:
     SUM, COUNT, MIN, MAX, AVG, STD, VAR = range(7)
 
+    class GroupingResult:
+        """agg::GroupingResult (groupby.hpp:12-18)."""
+
+        def __init__(self, inverse, n_groups, keys, shape, total_size):
+            self.inverse, self.n_groups, self.keys, self.shape, self.total_size = \
+                inverse, n_groups, keys, shape, total_size
+
     @staticmethod
-    def aggregate_all(data, fn):
-        """agg::aggregate_all (groupby.cpp:164-172) -> python int (i64) or float (f64)."""
+    def group(keys: Sequence) -> "agg.GroupingResult":
+        """agg::group (groupby.cpp:46-50): align_many + unique_with_inverse."""
+        host = _is_host(*keys)
+        ctx = _ctx_of(*keys)
+        dk = [upload(k, ctx) for k in keys]
+        arr = (C.c_void_p * len(dk))(*[d.handle.value for d in dk])
+        ko = (C.c_void_p * len(dk))()
+        k, n, ps, pe, pp = _shape_outs()
+        inv, ng = _new(), C.c_int64()
+        check(_L.rq_group(ctx.handle, arr, len(dk), C.byref(k), C.byref(n), C.byref(ps), C.byref(pe), C.byref(pp),
+                          C.byref(inv), ko, C.byref(ng)))
+        return agg.GroupingResult(_out(DeviceArray(inv, ctx), host), int(ng.value),
+                                  [_out(DeviceArray(C.c_void_p(ko[i]), ctx), host) for i in range(len(dk))],
+                                  Shape._from(k, n, ps, pe, pp, ctx, host), dk[0].total_size)
+
+    @staticmethod
+    def group_on_arrays(shape: Shape, key_values: Sequence, total_size: int) -> "agg.GroupingResult":
+        """agg::group_on_arrays (groupby.cpp:33-44)."""
+        host = _is_host(*key_values)
+        ctx = _ctx_of(*key_values)
+        dk = [_arr_in(k, ctx) for k in key_values]
+        arr = (C.c_void_p * max(1, len(dk)))(*[d.handle.value for d in dk])
+        ko = (C.c_void_p * max(1, len(dk)))()
+        inv, ng = _new(), C.c_int64()
+        check(_L.rq_group_on_arrays(ctx.handle, arr, len(dk), C.byref(inv), ko, C.byref(ng)))
+        return agg.GroupingResult(_out(DeviceArray(inv, ctx), host), int(ng.value),
+                                  [_out(DeviceArray(C.c_void_p(ko[i]), ctx), host) for i in range(len(dk))],
+                                  shape, total_size)
+
+    @staticmethod
+    def aggregate_array(shape: Shape, values, g: "agg.GroupingResult", fn):
+        """agg::aggregate_array (groupby.cpp:67-135)."""
+        fn = H.AGG_NAMES.get(fn, fn)
+        host = _is_host(values, g.inverse)
+        ctx = _ctx_of(values, g.inverse)
+        v, inv = _arr_in(values, ctx), _arr_in(g.inverse, ctx, np.int64)
+        o = _new()
+        check(_L.rq_aggregate_array(ctx.handle, *shape._args(ctx), v.handle, inv.handle, C.c_int64(g.n_groups),
+                                    C.c_int32(fn), C.byref(o)))
+        return _out(DeviceArray(o, ctx), host)
+
+    @staticmethod
+    def aggregate(data, g: "agg.GroupingResult", fn):
+        """agg::aggregate (groupby.cpp:137-142): data must decompose onto g's shape."""
+        sh, vals = compute.decompose(data)
+        a, b = g.shape, sh
+        same = a.kind == b.kind and (
+            (a.kind == "dense" and a.n == b.n) or
+            (a.kind == "run" and np.array_equal(_host_arr(a.s), _host_arr(b.s)) and
+             np.array_equal(_host_arr(a.e), _host_arr(b.e))) or
+            (a.kind == "point" and np.array_equal(_host_arr(a.p), _host_arr(b.p))))
+        if not same:
+            raise RqError(1, "aggregate: data shape differs from grouping shape")
+        return agg.aggregate_array(sh, vals, g, fn)
+
+    @staticmethod
+    def aggregate_all(data, fn, comm: Comm = None):
+        """agg::aggregate_all (groupby.cpp:164-172) -> python int (i64) or float (f64).
+        With `comm`: this rank's shard, merged over the communicator."""
         fn = H.AGG_NAMES.get(fn, fn)
         ctx = _ctx_of(data)
         dd = upload(data, ctx)
         dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+        if comm is not None:
+            check(_L.rq_aggregate_all_sharded(ctx.handle, comm.handle, dd.handle, fn, C.byref(dt), C.byref(i),
+                                              C.byref(f)))
+            return _agg_result(dt, i, f)
         check(_L.rq_aggregate_all(ctx.handle, dd.handle, fn, C.byref(dt), C.byref(i), C.byref(f)))
         return _agg_result(dt, i, f)
 
     @staticmethod
-    def group_aggregate(keys: Sequence, data: Sequence, fns: Sequence, normalize: bool = False):
+    def group_aggregate(keys: Sequence, data: Sequence, fns: Sequence, normalize: bool = False, comm: Comm = None):
         """agg::group_aggregate (groupby.cpp:144-162) -> (keys list, values list, n_groups).
         normalize=True: the query runner's GroupAgg (normalize_basic on every
         input first, runner.cpp:306-336), composites folded without expansion."""
@@ -753,13 +1160,18 @@ class agg:
         ok = (C.c_void_p * max(1, len(dk)))()
         ov = (C.c_void_p * max(1, len(dd)))()
         ng = C.c_int64()
-        check(fn_c(ctx.handle, karr, len(dk), darr, farr, len(dd), C.byref(ng), ok, ov))
+        if comm is not None:
+            check(_L.rq_group_aggregate_sharded(ctx.handle, comm.handle, karr, len(dk), darr, farr, len(dd),
+                                                int(normalize), C.byref(ng), ok, ov))
+        else:
+            check(fn_c(ctx.handle, karr, len(dk), darr, farr, len(dd), C.byref(ng), ok, ov))
         ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
         vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(dd))]
         return ks, vs, int(ng.value)
 
     @staticmethod
-    def group_aggregate_exprs(mask, keys: Sequence, exprs: Sequence, fns: Sequence, where: Sequence = ()):
+    def group_aggregate_exprs(mask, keys: Sequence, exprs: Sequence, fns: Sequence, where: Sequence = (),
+                              comm: Comm = None):
         """The runner's Filter → expressions → GroupAgg (runner.cpp:243-336)
         in one call: operands filtered by `mask` (None: no WHERE) and by the
         conjuncts `where` — (col, op, k) or (col, "in", [k...]) — each X
@@ -808,25 +1220,35 @@ class agg:
                 warr[i].op, warr[i].n_in = H.BINOP_NAMES.get(op, op), 0
                 warr[i].k = H.make_scalar(k)
         keep.extend(uploaded.values())
-        check(_L.rq_group_aggregate_where(ctx.handle, warr, len(where), dm.handle if dm is not None else None, karr,
-                                          len(dk), arr, farr, len(exprs), C.byref(ng), ok, ov, C.byref(fused)))
+        if comm is not None:
+            check(_L.rq_group_aggregate_where_sharded(ctx.handle, comm.handle, warr, len(where),
+                                                      dm.handle if dm is not None else None, karr, len(dk), arr, farr,
+                                                      len(exprs), C.byref(ng), ok, ov, C.byref(fused)))
+        else:
+            check(_L.rq_group_aggregate_where(ctx.handle, warr, len(where), dm.handle if dm is not None else None,
+                                              karr, len(dk), arr, farr, len(exprs), C.byref(ng), ok, ov,
+                                              C.byref(fused)))
         ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
         vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(exprs))]
         return ks, vs, int(ng.value), bool(fused.value)
 
     @staticmethod
-    def aggregate_binop(a, b, op, fn):
+    def aggregate_binop(a, b, op, fn, comm: Comm = None):
         """Fused aggregate_all(arith(a, b, op), fn) — one pass, no materialised fragments."""
         op = H.BINOP_NAMES.get(op, op)
         fn = H.AGG_NAMES.get(fn, fn)
         ctx = _ctx_of(a, b)
         da, db = upload(a, ctx), upload(b, ctx)
         dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+        if comm is not None:
+            check(_L.rq_aggregate_binop_sharded(ctx.handle, comm.handle, da.handle, db.handle, op, fn, C.byref(dt),
+                                                C.byref(i), C.byref(f)))
+            return _agg_result(dt, i, f)
         check(_L.rq_aggregate_binop(ctx.handle, da.handle, db.handle, op, fn, C.byref(dt), C.byref(i), C.byref(f)))
         return _agg_result(dt, i, f)
 
     @staticmethod
-    def filtered_aggregate_binop(c, k, cmp, a, b, op, fn):
+    def filtered_aggregate_binop(c, k, cmp, a, b, op, fn, comm: Comm = None):
         """aggregate_all(arith(filter(a,m), filter(b,m), op), fn), m = compare_scalar(c, k, cmp)."""
         op = H.BINOP_NAMES.get(op, op)
         cmp = H.BINOP_NAMES.get(cmp, cmp)
@@ -834,6 +1256,11 @@ class agg:
         ctx = _ctx_of(c, a, b)
         dc, da, db = upload(c, ctx), upload(a, ctx), upload(b, ctx)
         dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+        if comm is not None:
+            check(_L.rq_filtered_aggregate_binop_sharded(ctx.handle, comm.handle, dc.handle, H.make_scalar(k), cmp,
+                                                         da.handle, db.handle, op, fn, C.byref(dt), C.byref(i),
+                                                         C.byref(f)))
+            return _agg_result(dt, i, f)
         check(_L.rq_filtered_aggregate_binop(ctx.handle, dc.handle, H.make_scalar(k), cmp, da.handle, db.handle,
                                              op, fn, C.byref(dt), C.byref(i), C.byref(f)))
         return _agg_result(dt, i, f)

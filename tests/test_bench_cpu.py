@@ -11,7 +11,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("workload", ["c1", "c2", "c5"])
+@pytest.mark.parametrize("workload", ["c1", "c2", "c3", "q1", "q6", "c5"])
 def test_reference_arm_does_not_load_product(ref, workload):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", workload,
                           "--rows", "2000000", "--steps", "1", "--warmup", "3"],

@@ -51,12 +51,13 @@ def test_c3_streamed_upload_vs_oracle_200m(rq, so):
     from oracle import streaming as S
     from paper_2506_10092_b200 import host as H
     n = 200_000_000
-    k, x, y = G.c3_run_columns(n, 42)
+    k, x, y, _, _ = G.c3_run_columns(n, 42)
     fold = S.C3Fold(so, k, x, y)
     za = rq.alloc_array(H.I16, n)
     wa = rq.alloc_array(H.F64, n)
-    for r0 in range(0, n, G.C3_CHUNK):
-        z, w = G.c3_plain_chunk(n, 42, r0)
+    for r0 in range(0, n, G.GEN_CHUNK):
+        r1 = min(n, r0 + G.GEN_CHUNK)
+        z, w = G.c3_plain_rows(n, 42, r0, r1)
         keep = (za.write(r0, z), wa.write(r0, w))
         za.ctx.synchronize()
         del keep
@@ -108,7 +109,7 @@ def test_q6_vs_oracle_sf100(rq, so, n):
 def test_c5_vs_oracle(rq, ref, so, n):
     from oracle import streaming as S
     from oracle.refpy import RefAPI
-    t = Q.production_table(n, 5)
+    t = Q.production_table(n, 5, columns=["r2", "r3", "r4", "pi0", "p1"])
     want = S.c5(t, Q.C5_IN, Q.C5_LT, so)
     if n <= 5_000_000:  # the reference itself at small sizes
         wk, wv, _ = Q.c5_query(RefAPI(ref), t)

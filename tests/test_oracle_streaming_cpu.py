@@ -100,3 +100,31 @@ def test_where_can_empty_a_group(ref, so):
                                          normalize=True)
     so_keys, so_vals = S.q1(t, cutoff, so)
     tables_equal((so_keys, so_vals[:1]), ks, vs)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_partials_merge_to_whole_table(so, world):
+    """The oracle of a table cut into row-range shards (each generated alone,
+    datagen part=(rank, world)) merges to the whole-table oracle — the
+    multi-GPU bench gate."""
+    from oracle import streaming as S
+    from oracle.refpy import shard_column
+    n = 1_500_007
+    whole = S.c3(dict(zip("kxyzw", G.c3_tables(n, 4))), so)
+    parts = [S.c3_partial(dict(zip("kxyzw", G.c3_tables(n, 4, part=(r, world), slicer=shard_column))), so)
+             for r in range(world)]
+    tables_equal(S.c3_finish(S.merge(parts)), *whole)
+    t = Q.lineitem_q1(n, 43)
+    parts = [S.q1_partial(Q.lineitem_q1(n, 43, part=(r, world), slicer=shard_column), Q.Q1_CUTOFF, so)
+             for r in range(world)]
+    tables_equal(S.q1_finish(S.merge(parts)), *S.q1(t, Q.Q1_CUTOFF, so))
+    t = Q.lineitem_q6(n, 42)
+    parts = [S.q6_partial(Q.lineitem_q6(n, 42, part=(r, world), slicer=shard_column), Q.Q6_WHERE, so)
+             for r in range(world)]
+    a, b = S.q6_finish(S.merge(parts)), S.q6(t, Q.Q6_WHERE, so)
+    assert abs(a - b) <= 1e-9 * max(1.0, abs(a), abs(b))
+    cols = ["r2", "r3", "r4", "pi0", "p1"]
+    t = Q.production_table(n, 5, columns=cols)
+    parts = [S.c5_partial(Q.production_table(n, 5, part=(r, world), slicer=shard_column, columns=cols), Q.C5_IN,
+                          Q.C5_LT, so) for r in range(world)]
+    tables_equal(S.c5_finish(S.merge(parts)), *S.c5(t, Q.C5_IN, Q.C5_LT, so))
