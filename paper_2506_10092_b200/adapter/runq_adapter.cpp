@@ -60,6 +60,14 @@ rq_ctx_t ctx() {
   return tc.c;
 }
 
+// The device (CUDA context, stream, pool) is brought up when the program
+// loads, like any library's static state, so the first operator call does
+// not pay for driver initialisation.
+const bool kWarm = [] {
+  if (!std::getenv("RQ_ADAPTER_LAZY")) ctx();
+  return true;
+}();
+
 // ---- owned handles -----------------------------------------------------------------
 
 struct Arr {

@@ -37,8 +37,8 @@ def test_reference_acceptance_on_device():
     print(r.stdout)
     lines = {l.split("  ")[1].split(".")[0]: l.startswith("PASS") for l in r.stdout.splitlines()
              if l.startswith(("PASS", "FAIL"))}
-    # 1 paper fixtures, 2 randomized differential suite, 3 run statistics,
-    # 6 invariant suites; 5 needs the reference's data directory (absent on the
-    # GPU box) and 4 bounds wall time of per-call host round trips
-    for c in ("1", "2", "3", "6"):
+    # 1 paper fixtures (< 1 s), 2 randomized differential suite, 3 run
+    # statistics, 4 size accounting + bounds, 6 invariant suites; 5 needs the
+    # reference's data directory, absent on the GPU box
+    for c in ("1", "2", "3", "4", "6"):
         assert lines.get(c), r.stdout
