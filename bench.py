@@ -614,6 +614,7 @@ class C5(Q6):
         else:
             ks, vs, ng = Q.c5_query(rq, d)
         h = rq.download_all(list(ks) + list(vs))
+        self._sel = int(h[3].sum())  # selected rows (COUNT column): the measures are read only there
         return h[:1], h[1:]
 
     def oracle_partial(self, h):

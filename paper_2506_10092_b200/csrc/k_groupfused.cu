@@ -1405,6 +1405,175 @@ __global__ void k_xg_where(const __grid_constant__ XgPreds W, int64_t n, uint8_t
     flags[k] = pass ? 1 : 0;
   }
 }
+
+// ---- k-way segment table (joint alignment of every run list in one pass) ----
+//
+// The joint shape of the key runs, the WHERE columns' runs, the mask's runs
+// and the RLE operands' runs (align_many's left fold, align.cpp:233-254) is
+// the set of fragments [max_l s_l(r_l), min_l e_l(r_l)] over one run r_l per
+// list; every fragment ends at a run end of some list. So every run end x of
+// every list is a candidate fragment end: it is kept when every list covers x
+// (its run containing x starts at or before x), when no lower-numbered list
+// also ends a run at x (one owner per fragment), and when the WHERE conjuncts
+// pass on the lists' values at x. A candidate's position in the merged
+// (stable, list-index tie-broken) order of all run ends is Σ_l lower_bound(e_l, x)
+// plus the lower-numbered lists ending at x — known from the searches the
+// coverage test does anyway — so the fragments come out in row order without
+// a sort; two scans (kept flags, lengths) give every fragment's output slot
+// and covered-row offset.
+constexpr int KW_LISTS = 12;
+constexpr int64_t KW_MAX_ROWS = int64_t{1} << 40;  // the look-back scan carries 40-bit prefixes
+struct KwList {
+  const int64_t* s;
+  const int64_t* e;
+  int64_t n;
+  const void* v;  // run values (keys / predicate columns / RLE operands), or null
+  int dt;
+  int role;       // bits: 1 key, 2 predicate column, 4 RLE operand, 8 coverage only (mask / domain)
+  int cst;        // RLE operand: index of its per-fragment value array
+  int64_t kmin, stride;
+};
+struct KwPlan {
+  int nl;
+  KwList l[KW_LISTS];
+  int64_t start[KW_LISTS + 1];  // candidate index of each list's first run end
+  int np;
+  XgPred p[XG_PREDS];  // p.src = list index
+};
+
+__device__ __forceinline__ int64_t kw_lower_bound(const int64_t* __restrict__ e, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(e + mid) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint64_t kw_value_bits(const void* v, int dt, int64_t r) {
+  return dt_is_float_dev(dt) ? static_cast<uint64_t>(__double_as_longlong(ld_f64(v, dt, r)))
+                             : static_cast<uint64_t>(ld_i64(v, dt, r));
+}
+
+__device__ __forceinline__ bool kw_pass(const XgPred& P, uint64_t v) {
+  if (P.op >= 0) return xg_cmp1(v, P.flt, P.ki[0], P.kf[0], P.kflt[0], P.op);
+  for (int t = 0; t < P.n_in; ++t)
+    if (xg_cmp1(v, P.flt, P.ki[t], P.kf[t], P.kflt[t], RQ_EQ)) return true;
+  return false;
+}
+
+// One thread per run end. `kept` is zeroed beforehand: a candidate that
+// fails its own list's conjuncts, is not covered by some list, fails a
+// conjunct of a list already located, or is not its fragment's owner
+// returns early (most run ends of a selective WHERE never search the other
+// lists); a kept one writes its fragment at its merged rank and adds to the
+// (segments, covered rows) counters.
+__global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __restrict__ kept,
+                                  int64_t* __restrict__ seg_s, int64_t* __restrict__ seg_e,
+                                  int64_t* __restrict__ seg_slot, uint64_t* __restrict__ seg_cst,
+                                  unsigned long long* __restrict__ dims) {
+  const int64_t N = K.start[K.nl];
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < N;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int j = 0;
+    while (c >= K.start[j + 1]) ++j;
+    const KwList& J = K.l[j];
+    const int64_t i = c - K.start[j];
+    const int64_t x = __ldg(J.e + i);
+    bool keep = true;
+    for (int q = 0; q < K.np && keep; ++q)  // this list's own conjuncts first: no search needed
+      if (K.p[q].src == j) keep = kw_pass(K.p[q], kw_value_bits(J.v, J.dt, i));
+    if (!keep) continue;
+    int64_t rank = 0, start = __ldg(J.s + i);
+    int64_t r[KW_LISTS];
+    for (int l = 0; l < K.nl && keep; ++l) {
+      const KwList& L = K.l[l];
+      if (l == j) {
+        r[l] = i;
+        rank += i;
+        continue;
+      }
+      const int64_t rl = kw_lower_bound(L.e, L.n, x);
+      if (rl >= L.n || __ldg(L.s + rl) > x) keep = false;          // x not covered by list l
+      else if (l < j && __ldg(L.e + rl) == x) keep = false;        // a lower-numbered list owns this end
+      if (!keep) break;
+      start = max(start, __ldg(L.s + rl));
+      r[l] = rl;
+      rank += rl;
+      for (int q = 0; q < K.np && keep; ++q)
+        if (K.p[q].src == l) keep = kw_pass(K.p[q], kw_value_bits(L.v, L.dt, rl));
+    }
+    if (!keep) continue;
+    int64_t slot = 0;
+    for (int l = 0; l < K.nl; ++l) {
+      const KwList& L = K.l[l];
+      if (L.role & 1) slot += (ld_i64(L.v, L.dt, r[l]) - L.kmin) * L.stride;
+      if (L.role & 4) seg_cst[static_cast<int64_t>(L.cst) * N + rank] = kw_value_bits(L.v, L.dt, r[l]);
+    }
+    kept[rank] = 1;
+    seg_s[rank] = start;
+    seg_e[rank] = x;
+    seg_slot[rank] = slot;
+    // (segments, covered rows): one atomic pair per warp
+    const unsigned act = __activemask();
+    const unsigned long long len = static_cast<unsigned long long>(x - start + 1);
+    // len < 2^40: two 20-bit halves, each summed over <= 32 lanes without overflow
+    const unsigned long long wl =
+        __reduce_add_sync(act, static_cast<unsigned>(len & 0xfffffu)) +
+        (static_cast<unsigned long long>(__reduce_add_sync(act, static_cast<unsigned>(len >> 20))) << 20);
+    if ((threadIdx.x & 31) == __ffs(act) - 1) {
+      atomicAdd(dims, static_cast<unsigned long long>(__popc(act)));
+      atomicAdd(dims + 1, wl);
+    }
+  }
+}
+
+// kept candidates → the segment table (s, e, slot, cst, off) at their scanned
+// slots; the last thread writes (n segments, covered rows) to dims
+__global__ void k_kway_compact(int64_t N, int ncst, const int64_t* __restrict__ kept, const int64_t* __restrict__ exk,
+                               const int64_t* __restrict__ seg_s, const int64_t* __restrict__ seg_e,
+                               const int64_t* __restrict__ seg_slot, const uint64_t* __restrict__ seg_cst,
+                               int64_t* __restrict__ s, int64_t* __restrict__ e, int64_t* __restrict__ slot,
+                               uint64_t* __restrict__ cst) {
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < N;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!kept[c]) continue;
+    const int64_t o = exk[c];
+    s[o] = seg_s[c];
+    e[o] = seg_e[c];
+    slot[o] = seg_slot[c];
+    for (int j = 0; j < ncst; ++j) cst[static_cast<int64_t>(j) * N + o] = seg_cst[static_cast<int64_t>(j) * N + c];
+  }
+}
+
+// Plain+Index operand: the outliers inside each segment, found by a binary
+// search of the segment's start in the (sorted) outlier positions — the
+// query touches only the outliers of selected rows — replace the base's
+// decoded value (column.cpp:299-309); one add per segment (a segment has one
+// slot)
+__global__ void k_xg_outliers_seg(PlainSrc base, const int64_t* __restrict__ p, const void* __restrict__ v2, int v2dt,
+                                  int64_t n, const int64_t* __restrict__ ss, const int64_t* __restrict__ se,
+                                  const int64_t* __restrict__ seg_slot, int64_t nseg, int ne, int ei, int acc_f,
+                                  unsigned long long* __restrict__ tab) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nseg;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = ldg64(ss, k), b = ldg64(se, k);
+    int64_t i = kw_lower_bound(p, n, a);
+    if (i >= n || ldg64(p, i) > b) continue;
+    double fd = 0.0;
+    uint64_t id = 0;
+    for (; i < n; ++i) {
+      const int64_t pos = ldg64(p, i);
+      if (pos > b) break;
+      if (acc_f) fd += ld_f64(v2, v2dt, i) - plain_value<double>(base, pos);
+      else id += static_cast<uint64_t>(ld_i64(v2, v2dt, i)) - static_cast<uint64_t>(plain_value<int64_t>(base, pos));
+    }
+    const int64_t cell = ldg64(seg_slot, k) * ne + ei;
+    if (acc_f) atomicAdd(reinterpret_cast<double*>(tab) + cell, fd);
+    else atomicAdd(tab + cell, static_cast<unsigned long long>(id));
+  }
+}
 }  // namespace dev
 
 namespace {
@@ -1461,6 +1630,174 @@ void gather_many(const CtxPtr& ctx, const std::vector<DArr*>& arrs, const DArr& 
   std::vector<std::pair<DArr*, const DArr*>> items;
   for (DArr* a : arrs) items.push_back({a, &idx});
   gather_multi(ctx, items);
+}
+
+// Key slot layout without building the key runs: slot = Σ (key − min)·stride
+// over each key column's (cached) value range, first key most significant —
+// the dense slots of build_key / build_multi_key.
+bool key_layout(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKey& K) {
+  K.G = 1;
+  for (auto* k : keys) {
+    if (k->enc != RQ_ENC_RLE || dt_float(k->v.dt) || k->v.n == 0) return false;
+    auto mm = col_minmax(ctx, *k);
+    const int64_t range = mm.second - mm.first + 1;
+    if (range <= 0 || range > kFusedSlotLimit || K.G * range > kFusedSlotLimit) return false;
+    K.kmin.push_back(mm.first);
+    K.range.push_back(range);
+    K.kdt.push_back(k->v.dt);
+    K.G *= range;
+  }
+  K.stride.assign(keys.size(), 1);
+  int64_t st = 1;
+  for (size_t c = keys.size(); c-- > 0;) {
+    K.stride[c] = st;
+    st *= K.range[c];
+  }
+  return true;
+}
+
+// The segment table in one pass over every run list (k_kway_candidates):
+// s / e / slot / per-segment RLE-operand values / covered-row offsets, with
+// one readback (segment count, covered rows). Returns false when the lists
+// do not fit the kernel (the pairwise path then builds the table).
+bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, const DMask* mask,
+                   const std::vector<XPred>* preds, const std::vector<const DCol*>& rle_cols, int64_t total,
+                   GroupKey& K, DArr& s, DArr& e, DArr& slot, DArr& cst_all, DArr& off, int64_t& nseg,
+                   int64_t& ncov) {
+  if (total <= 0 || total >= dev::KW_MAX_ROWS) return false;
+  if (!key_layout(ctx, keys, K)) return false;
+  dev::KwPlan KP{};
+  std::vector<const DCol*> of_list;  // the column behind each list (null: mask / domain)
+  auto add = [&](const DArr& ls, const DArr& le, const DCol* col) -> int {
+    for (int l = 0; l < KP.nl; ++l)  // one list per column, whatever its roles
+      if (col && of_list[l] && (of_list[l] == col || (of_list[l]->v.raw() == col->v.raw() &&
+                                                      of_list[l]->e.raw() == col->e.raw())))
+        return l;
+    if (KP.nl >= dev::KW_LISTS) return -1;
+    dev::KwList& L = KP.l[KP.nl];
+    L.s = ls.pos();
+    L.e = le.pos();
+    L.n = le.n;
+    L.v = col ? col->v.raw() : nullptr;
+    L.dt = col ? col->v.dt : RQ_I64;
+    L.role = 0;
+    L.cst = -1;
+    of_list.push_back(col);
+    return KP.nl++;
+  };
+  for (size_t c = 0; c < keys.size(); ++c) {
+    const int l = add(keys[c]->s, keys[c]->e, keys[c]);
+    if (l < 0 || (KP.l[l].role & 1)) return false;  // the same column twice as a key
+    KP.l[l].role |= 1;
+    KP.l[l].kmin = K.kmin[c];
+    KP.l[l].stride = K.stride[c];
+  }
+  DArr ms, me;  // the mask's true rows as runs
+  if (mask) {
+    if (mask->enc == RQ_MASK_RLE) {
+      ms = mask->s;
+      me = mask->e;
+    } else if (mask->enc == RQ_MASK_PLAIN) {
+      plain_mask_to_rle(ctx, mask->bits, ms, me);
+    } else if (mask->enc == RQ_MASK_INDEX) {
+      ms = me = mask->p;
+    } else {
+      return false;
+    }
+    if (add(ms, me, nullptr) < 0) return false;
+  }
+  const size_t npred = preds ? preds->size() : 0;
+  for (size_t i = 0; i < npred; ++i) {
+    const XPred& q = (*preds)[i];
+    const int l = add(q.col->s, q.col->e, q.col);
+    if (l < 0) return false;
+    KP.l[l].role |= 2;
+    dev::XgPred& P = KP.p[KP.np++];
+    P.src = l;
+    P.flt = dt_float(q.col->v.dt) ? 1 : 0;
+    P.op = q.in.empty() ? q.op : -1;
+    const std::vector<Scalar> one{q.k};
+    const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
+    P.n_in = static_cast<int>(ks.size());
+    for (size_t j = 0; j < ks.size(); ++j) {
+      P.kflt[j] = ks[j].is_float ? 1 : 0;
+      P.ki[j] = ks[j].i;
+      P.kf[j] = ks[j].f;
+    }
+  }
+  for (size_t j = 0; j < rle_cols.size(); ++j) {
+    const int l = add(rle_cols[j]->s, rle_cols[j]->e, rle_cols[j]);
+    if (l < 0) return false;
+    if (KP.l[l].role & 4) return false;  // two operand slots on one list: pairwise path
+    KP.l[l].role |= 4;
+    KP.l[l].cst = static_cast<int>(j);
+  }
+  DArr dom_s, dom_e;
+  if (KP.nl == 0) {  // no run list at all: the whole domain is one segment
+    const int64_t z = 0, t1 = total - 1;
+    dom_s = upload_arr(ctx, RQ_I64, &z, 1);
+    dom_e = upload_arr(ctx, RQ_I64, &t1, 1);
+    add(dom_s, dom_e, nullptr);
+  }
+  // role bits → the kernel's roles (0 key, 1 predicate, 2 operand, 3 coverage): a
+  // list may carry several; the kernel reads them as bits too
+  for (int l = 0; l < KP.nl; ++l) {
+    KP.l[l].role = KP.l[l].role == 0 ? 8 : KP.l[l].role;
+    if (!(KP.l[l].role & 4)) KP.l[l].cst = -1;
+  }
+  KP.start[0] = 0;
+  for (int l = 0; l < KP.nl; ++l) KP.start[l + 1] = KP.start[l] + KP.l[l].n;
+  const int64_t N = KP.start[KP.nl];
+  const int ncst = static_cast<int>(rle_cols.size());
+  if (N == 0) {
+    s = alloc_arr(ctx, RQ_I64, 0);
+    e = alloc_arr(ctx, RQ_I64, 0);
+    slot = alloc_arr(ctx, RQ_I64, 0);
+    cst_all = alloc_arr(ctx, RQ_I64, 1);
+    off = alloc_arr(ctx, RQ_I64, 1);
+    nseg = ncov = 0;
+    return true;
+  }
+  DArr kept = alloc_arr(ctx, RQ_I64, N), cs = alloc_arr(ctx, RQ_I64, N), ce = alloc_arr(ctx, RQ_I64, N),
+       cslot = alloc_arr(ctx, RQ_I64, N), ccst = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst)),
+       dims = alloc_arr(ctx, RQ_I64, 2);
+  RQ_CUDA_CHECK(cudaMemsetAsync(kept.raw_mut(), 0, static_cast<size_t>(N) * 8, ctx->stream));
+  RQ_CUDA_CHECK(cudaMemsetAsync(dims.raw_mut(), 0, 16, ctx->stream));
+  dev::k_kway_candidates<<<grid_cap(ctx, N), 256, 0, ctx->stream>>>(
+      KP, kept.as<int64_t>(), cs.as<int64_t>(), ce.as<int64_t>(), cslot.as<int64_t>(), ccst.as<uint64_t>(),
+      dims.as<unsigned long long>());
+  launched(ctx);
+  DArr exk;
+  scan_exclusive_i64(ctx, kept, exk);
+  s = alloc_arr(ctx, RQ_I64, N);
+  e = alloc_arr(ctx, RQ_I64, N);
+  slot = alloc_arr(ctx, RQ_I64, N);
+  DArr cst_n = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst));
+  dev::k_kway_compact<<<grid_cap(ctx, N), 256, 0, ctx->stream>>>(N, ncst, kept.pos(), exk.pos(), cs.pos(), ce.pos(),
+                                                                 cslot.pos(), ccst.as<uint64_t>(), s.as<int64_t>(),
+                                                                 e.as<int64_t>(), slot.as<int64_t>(),
+                                                                 cst_n.as<uint64_t>());
+  launched(ctx);
+  const int64_t* h = ctx->readback(dims.raw(), 16);
+  nseg = h[0];
+  ncov = h[1];
+  s.n = e.n = slot.n = nseg;
+  // covered-row offsets of the kept segments (a scan over nseg, not N)
+  off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
+  if (nseg) {
+    DArr len = alloc_arr(ctx, RQ_I64, nseg + 1);
+    dev::k_xg_lengths<<<grid_cap(ctx, nseg + 1), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
+    launched(ctx);
+    scan_exclusive_i64(ctx, len, off);
+    off.n = nseg;
+  }
+  // the row kernels read operand j of segment k at cst[j * nseg + k]
+  cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * ncst));
+  if (ncst && nseg)
+    RQ_CUDA_CHECK(cudaMemcpy2DAsync(cst_all.raw_mut(), static_cast<size_t>(nseg) * 8, cst_n.raw(),
+                                    static_cast<size_t>(N) * 8, static_cast<size_t>(nseg) * 8, ncst,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  return true;
 }
 
 bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol*>& keys,
@@ -1549,141 +1886,148 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   P.ncst = static_cast<int>(rle_cols.size());
   for (size_t j = 0; j < rle_cols.size(); ++j) P.cst_f[j] = dt_float(rle_cols[j]->v.dt) ? 1 : 0;
 
-  // ---- segment table: keys ∩ mask ∩ RLE operands (align_many's joint shape) ----
-  auto stage = std::make_unique<KTimer>(ctx, "xg_keys");  // per-stage profile tags (no-ops unless profiling)
-  GroupKey K;
-  if (preK) {
-    K = *preK;
-  } else if (!keys.empty()) {
-    if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
-  } else {
-    if (total == 0) return false;
-    // one run [0, total) in slot 0 (one device fill: no host staging)
-    K.s = alloc_arr(ctx, RQ_I64, 1);
-    K.e = alloc_arr(ctx, RQ_I64, 1);
-    K.slot = alloc_arr(ctx, RQ_I64, 1);
-    dev::k_xg_fill3<<<1, 1, 0, ctx->stream>>>(K.s.as<int64_t>(), 0, K.e.as<int64_t>(), total - 1,
-                                              K.slot.as<int64_t>(), 0);
-    launched(ctx);
-    K.G = 1;
-  }
-  stage.reset();
+  // ---- segment table: keys ∩ mask ∩ WHERE ∩ RLE operands (align_many's joint shape) ----
   KTimer timer(ctx, "group_exprs");
-  stage = std::make_unique<KTimer>(ctx, "xg_where");
-  DArr s = K.s, e = K.e, slot = K.slot;
-  std::vector<DArr> cst;
-  if (mask) {
-    // the mask's true rows as runs: RLE as is, a plain byte mask through
-    // plain_mask_to_rle (primitives.cpp:349-360), index points as 1-row runs
-    DArr ms = mask->s, me = mask->e;
-    if (mask->enc == RQ_MASK_PLAIN) plain_mask_to_rle(ctx, mask->bits, ms, me);
-    else if (mask->enc == RQ_MASK_INDEX) ms = me = mask->p;
-    Intersection r = range_intersect(ctx, s, e, ms, me, true, false);
-    slot = gather(ctx, slot, r.idx1);
-    s = r.s;
-    e = r.e;
-  }
-  if (npred) {
-    // WHERE pushdown: the segments are intersected with each distinct
-    // predicate column's runs (fewest runs first) and the passing segments
-    // kept; before a column with many runs the segments are pruned by the
-    // conjuncts already evaluable, so the large intersection runs on the
-    // selected segments only.
-    std::vector<const DCol*> pcols;  // distinct predicate columns
-    std::vector<int> pcol_of(npred);
-    for (size_t i = 0; i < npred; ++i) {
-      const XPred& q = (*preds)[i];
-      int src = -1;
-      for (size_t j = 0; j < pcols.size(); ++j)
-        if (pcols[j] == q.col || (pcols[j]->v.raw() == q.col->v.raw() && pcols[j]->e.raw() == q.col->e.raw()))
-          src = static_cast<int>(j);
-      if (src < 0) {
-        pcols.push_back(q.col);
-        src = static_cast<int>(pcols.size()) - 1;
-      }
-      pcol_of[i] = src;
-    }
-    std::vector<int> order(pcols.size());
-    for (size_t j = 0; j < order.size(); ++j) order[j] = static_cast<int>(j);
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return pcols[x]->e.n < pcols[y]->e.n; });
-    std::vector<int> slot_of(pcols.size(), -1);  // predicate column -> its value array in pv
-    std::vector<DArr> pv;
-    // keep the segments passing every conjunct whose column is already joined in
-    auto prune = [&]() {
-      dev::XgPreds W{};
-      for (size_t i = 0; i < npred; ++i) {
-        const int src = slot_of[pcol_of[i]];
-        if (src < 0) continue;
-        const XPred& q = (*preds)[i];
-        dev::XgPred& P = W.p[W.n++];
-        P.src = src;
-        P.flt = dt_float(q.col->v.dt) ? 1 : 0;
-        P.op = q.in.empty() ? q.op : -1;
-        const std::vector<Scalar> one{q.k};
-        const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
-        P.n_in = static_cast<int>(ks.size());
-        for (size_t j = 0; j < ks.size(); ++j) {
-          P.kflt[j] = ks[j].is_float ? 1 : 0;
-          P.ki[j] = ks[j].i;
-          P.kf[j] = ks[j].f;
-        }
-      }
-      for (size_t j = 0; j < pv.size(); ++j) W.val[j] = reinterpret_cast<const uint64_t*>(pv[j].raw());
-      if (!s.n || !W.n) return;
-      DArr flags = alloc_arr(ctx, RQ_I8, s.n);
-      dev::k_xg_where<<<grid_cap(ctx, s.n), 256, 0, ctx->stream>>>(W, s.n, flags.as<uint8_t>());
+  GroupKey K;
+  DArr s, e, slot, cst_all, off;
+  int64_t nseg = 0, ncov = 0;
+  const bool kway = !preK && kway_segments(ctx, keys, mask, preds, rle_cols, total, K, s, e, slot, cst_all, off, nseg,
+                                           ncov);
+  if (!kway) {
+    auto stage = std::make_unique<KTimer>(ctx, "xg_keys");  // per-stage profile tags (no-ops unless profiling)
+    if (preK) {
+      K = *preK;
+    } else if (!keys.empty()) {
+      if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
+    } else {
+      if (total == 0) return false;
+      // one run [0, total) in slot 0 (one device fill: no host staging)
+      K.s = alloc_arr(ctx, RQ_I64, 1);
+      K.e = alloc_arr(ctx, RQ_I64, 1);
+      K.slot = alloc_arr(ctx, RQ_I64, 1);
+      dev::k_xg_fill3<<<1, 1, 0, ctx->stream>>>(K.s.as<int64_t>(), 0, K.e.as<int64_t>(), total - 1,
+                                                K.slot.as<int64_t>(), 0);
       launched(ctx);
-      DArr keep;
-      flagged_indices(ctx, flags, s.n, keep);
-      std::vector<DArr*> g{&s, &e, &slot};
-      for (auto& v : pv) g.push_back(&v);
-      gather_many(ctx, g, keep);
-    };
-    for (size_t oi = 0; oi < order.size(); ++oi) {
-      const DCol* col = pcols[order[oi]];
-      if (oi > 0 && col->e.n >= 65536 && s.n > 0 && col->e.n >= 16 * s.n) prune();
-      Intersection r = range_intersect(ctx, s, e, col->s, col->e, true, true);
-      DArr nv = col->v;  // segment tables through idx1, the column's values through idx2: one launch
-      std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
-      for (auto& v : pv) g.push_back({&v, &r.idx1});
-      g.push_back({&nv, &r.idx2});
-      gather_multi(ctx, g);
-      pv.push_back(nv);
-      slot_of[order[oi]] = static_cast<int>(pv.size()) - 1;
+      K.G = 1;
+    }
+    stage = std::make_unique<KTimer>(ctx, "xg_where");
+    s = K.s;
+    e = K.e;
+    slot = K.slot;
+    std::vector<DArr> cst;
+    if (mask) {
+      // the mask's true rows as runs: RLE as is, a plain byte mask through
+      // plain_mask_to_rle (primitives.cpp:349-360), index points as 1-row runs
+      DArr ms = mask->s, me = mask->e;
+      if (mask->enc == RQ_MASK_PLAIN) plain_mask_to_rle(ctx, mask->bits, ms, me);
+      else if (mask->enc == RQ_MASK_INDEX) ms = me = mask->p;
+      Intersection r = range_intersect(ctx, s, e, ms, me, true, false);
+      slot = gather(ctx, slot, r.idx1);
       s = r.s;
       e = r.e;
     }
-    prune();
+    if (npred) {
+      // WHERE pushdown: the segments are intersected with each distinct
+      // predicate column's runs (fewest runs first) and the passing segments
+      // kept; before a column with many runs the segments are pruned by the
+      // conjuncts already evaluable, so the large intersection runs on the
+      // selected segments only.
+      std::vector<const DCol*> pcols;  // distinct predicate columns
+      std::vector<int> pcol_of(npred);
+      for (size_t i = 0; i < npred; ++i) {
+        const XPred& q = (*preds)[i];
+        int src = -1;
+        for (size_t j = 0; j < pcols.size(); ++j)
+          if (pcols[j] == q.col || (pcols[j]->v.raw() == q.col->v.raw() && pcols[j]->e.raw() == q.col->e.raw()))
+            src = static_cast<int>(j);
+        if (src < 0) {
+          pcols.push_back(q.col);
+          src = static_cast<int>(pcols.size()) - 1;
+        }
+        pcol_of[i] = src;
+      }
+      std::vector<int> order(pcols.size());
+      for (size_t j = 0; j < order.size(); ++j) order[j] = static_cast<int>(j);
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return pcols[x]->e.n < pcols[y]->e.n; });
+      std::vector<int> slot_of(pcols.size(), -1);  // predicate column -> its value array in pv
+      std::vector<DArr> pv;
+      // keep the segments passing every conjunct whose column is already joined in
+      auto prune = [&]() {
+        dev::XgPreds W{};
+        for (size_t i = 0; i < npred; ++i) {
+          const int src = slot_of[pcol_of[i]];
+          if (src < 0) continue;
+          const XPred& q = (*preds)[i];
+          dev::XgPred& P = W.p[W.n++];
+          P.src = src;
+          P.flt = dt_float(q.col->v.dt) ? 1 : 0;
+          P.op = q.in.empty() ? q.op : -1;
+          const std::vector<Scalar> one{q.k};
+          const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
+          P.n_in = static_cast<int>(ks.size());
+          for (size_t j = 0; j < ks.size(); ++j) {
+            P.kflt[j] = ks[j].is_float ? 1 : 0;
+            P.ki[j] = ks[j].i;
+            P.kf[j] = ks[j].f;
+          }
+        }
+        for (size_t j = 0; j < pv.size(); ++j) W.val[j] = reinterpret_cast<const uint64_t*>(pv[j].raw());
+        if (!s.n || !W.n) return;
+        DArr flags = alloc_arr(ctx, RQ_I8, s.n);
+        dev::k_xg_where<<<grid_cap(ctx, s.n), 256, 0, ctx->stream>>>(W, s.n, flags.as<uint8_t>());
+        launched(ctx);
+        DArr keep;
+        flagged_indices(ctx, flags, s.n, keep);
+        std::vector<DArr*> g{&s, &e, &slot};
+        for (auto& v : pv) g.push_back(&v);
+        gather_many(ctx, g, keep);
+      };
+      for (size_t oi = 0; oi < order.size(); ++oi) {
+        const DCol* col = pcols[order[oi]];
+        if (oi > 0 && col->e.n >= 65536 && s.n > 0 && col->e.n >= 16 * s.n) prune();
+        Intersection r = range_intersect(ctx, s, e, col->s, col->e, true, true);
+        DArr nv = col->v;  // segment tables through idx1, the column's values through idx2: one launch
+        std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
+        for (auto& v : pv) g.push_back({&v, &r.idx1});
+        g.push_back({&nv, &r.idx2});
+        gather_multi(ctx, g);
+        pv.push_back(nv);
+        slot_of[order[oi]] = static_cast<int>(pv.size()) - 1;
+        s = r.s;
+        e = r.e;
+      }
+      prune();
+    }
+    stage = std::make_unique<KTimer>(ctx, "xg_operands");
+    for (const DCol* rc : rle_cols) {
+      Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
+      DArr nv = rc->v;
+      std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
+      for (auto& c : cst) g.push_back({&c, &r.idx1});
+      g.push_back({&nv, &r.idx2});
+      gather_multi(ctx, g);
+      cst.push_back(nv);
+      s = r.s;
+      e = r.e;
+    }
+    stage = std::make_unique<KTimer>(ctx, "xg_prep");
+    nseg = s.n;
+    cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * static_cast<int64_t>(cst.size())));
+    for (size_t j = 0; j < cst.size(); ++j)
+      if (nseg)
+        RQ_CUDA_CHECK(cudaMemcpyAsync(cst_all.as<int64_t>() + j * nseg, cst[j].raw(), nseg * 8,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+    off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
+    if (nseg) {
+      // lengths plus a trailing 0: the exclusive scan's last entry is the covered-row total
+      DArr len = alloc_arr(ctx, RQ_I64, nseg + 1);
+      dev::k_xg_lengths<<<grid_cap(ctx, nseg + 1), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
+      launched(ctx);
+      scan_exclusive_i64(ctx, len, off);
+      ncov = *ctx->readback(off.as<int64_t>() + nseg, 8);
+    }
   }
-  stage = std::make_unique<KTimer>(ctx, "xg_operands");
-  for (const DCol* rc : rle_cols) {
-    Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
-    DArr nv = rc->v;
-    std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
-    for (auto& c : cst) g.push_back({&c, &r.idx1});
-    g.push_back({&nv, &r.idx2});
-    gather_multi(ctx, g);
-    cst.push_back(nv);
-    s = r.s;
-    e = r.e;
-  }
-  stage = std::make_unique<KTimer>(ctx, "xg_prep");
-  const int64_t nseg = s.n;
-  DArr cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * static_cast<int64_t>(cst.size())));
-  for (size_t j = 0; j < cst.size(); ++j)
-    if (nseg)
-      RQ_CUDA_CHECK(cudaMemcpyAsync(cst_all.as<int64_t>() + j * nseg, cst[j].raw(), nseg * 8,
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
-  DArr off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
-  int64_t ncov = 0;
-  if (nseg) {
-    // lengths plus a trailing 0: the exclusive scan's last entry is the covered-row total
-    DArr len = alloc_arr(ctx, RQ_I64, nseg + 1);
-    dev::k_xg_lengths<<<grid_cap(ctx, nseg + 1), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
-    launched(ctx);
-    scan_exclusive_i64(ctx, len, off);
-    ncov = *ctx->readback(off.as<int64_t>() + nseg, 8);
-  }
+  auto stage = std::make_unique<KTimer>(ctx, "xg_prep");
   const int64_t G = K.G;
   const int64_t cells = G * P.ne;
   if (cells > (int64_t{1} << 26)) return false;
@@ -1717,15 +2061,13 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
     launched(ctx);
   }
-  for (auto& pe : pi_exprs) {  // Plain+Index: outliers inside segments
+  for (auto& pe : pi_exprs) {  // Plain+Index: outliers inside segments (located by search, not materialised)
     const DCol& c = *pe.second;
     if (c.p2.n == 0 || nseg == 0) continue;
-    PointsInRuns r = points_in_runs(ctx, c.p2, s, e, true, true);
-    if (r.p_out.n == 0) continue;
     const dev::XgExpr& X = P.e[pe.first];
-    dev::k_xg_outliers<<<grid_cap(ctx, r.p_out.n), 256, 0, ctx->stream>>>(
-        P.col[X.t[0].src], r.p_out.pos(), c.v2.raw(), c.v2.dt, r.idx_of.pos(), r.run_of.pos(), r.p_out.n,
-        slot.pos(), P.ne, pe.first, X.acc_f, tabp);
+    dev::k_xg_outliers_seg<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(
+        P.col[X.t[0].src], c.p2.pos(), c.v2.raw(), c.v2.dt, c.p2.n, s.pos(), e.pos(), slot.pos(), nseg, P.ne,
+        pe.first, X.acc_f, tabp);
     launched(ctx);
   }
   bool int_div = false;  // only integer division can raise (align.cpp:297-299)

@@ -101,7 +101,7 @@ def test_random_expressions_vs_reference(rq, ref, inst, row_kernel):
     p16 = H.PlainColumn(rng.integers(-3000, 3001, n).astype(np.int16), H.I32, None)
     pf = H.PlainColumn(rng.uniform(-50, 50, n))
     r = _rle(rng, n, 40, -9, 9)
-    pi = Q._plain_index(n, rng, 0.02)
+    pi = Q._plain_index(rng, n, 0.02)
     mcol = _rle(rng, n, 200, 0, 9)
     mask = rq.compute.compare_scalar(mcol, 6, "<") if inst % 2 == 0 else None
     hmask = ref.compare_scalar(mcol, 6, "<") if mask is not None else None
