@@ -1439,6 +1439,7 @@ struct KwPlan {
   int64_t start[KW_LISTS + 1];  // candidate index of each list's first run end
   int np;
   XgPred p[XG_PREDS];  // p.src = list index
+  int own[KW_LISTS];   // list l has conjuncts
 };
 
 __device__ __forceinline__ int64_t kw_lower_bound(const int64_t* __restrict__ e, int64_t n, int64_t x) {
@@ -1482,12 +1483,18 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __r
     const int64_t i = c - K.start[j];
     const int64_t x = __ldg(J.e + i);
     bool keep = true;
-    for (int q = 0; q < K.np && keep; ++q)  // this list's own conjuncts first: no search needed
-      if (K.p[q].src == j) keep = kw_pass(K.p[q], kw_value_bits(J.v, J.dt, i));
+    if (K.own[j]) {  // this list's own conjuncts first: no search needed
+      const uint64_t v = kw_value_bits(J.v, J.dt, i);
+#pragma unroll
+      for (int q = 0; q < XG_PREDS; ++q)
+        if (q < K.np && keep && K.p[q].src == j) keep = kw_pass(K.p[q], v);
+    }
     if (!keep) continue;
     int64_t rank = 0, start = __ldg(J.s + i);
     int64_t r[KW_LISTS];
-    for (int l = 0; l < K.nl && keep; ++l) {
+#pragma unroll
+    for (int l = 0; l < KW_LISTS; ++l) {  // unrolled: r[] stays in registers
+      if (l >= K.nl || !keep) break;
       const KwList& L = K.l[l];
       if (l == j) {
         r[l] = i;
@@ -1501,12 +1508,18 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __r
       start = max(start, __ldg(L.s + rl));
       r[l] = rl;
       rank += rl;
-      for (int q = 0; q < K.np && keep; ++q)
-        if (K.p[q].src == l) keep = kw_pass(K.p[q], kw_value_bits(L.v, L.dt, rl));
+      if (K.own[l]) {
+        const uint64_t v = kw_value_bits(L.v, L.dt, rl);
+#pragma unroll
+        for (int q = 0; q < XG_PREDS; ++q)
+          if (q < K.np && keep && K.p[q].src == l) keep = kw_pass(K.p[q], v);
+      }
     }
     if (!keep) continue;
     int64_t slot = 0;
-    for (int l = 0; l < K.nl; ++l) {
+#pragma unroll
+    for (int l = 0; l < KW_LISTS; ++l) {
+      if (l >= K.nl) break;
       const KwList& L = K.l[l];
       if (L.role & 1) slot += (ld_i64(L.v, L.dt, r[l]) - L.kmin) * L.stride;
       if (L.role & 4) seg_cst[static_cast<int64_t>(L.cst) * N + rank] = kw_value_bits(L.v, L.dt, r[l]);
@@ -1714,6 +1727,7 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
     KP.l[l].role |= 2;
     dev::XgPred& P = KP.p[KP.np++];
     P.src = l;
+    KP.own[l] = 1;
     P.flt = dt_float(q.col->v.dt) ? 1 : 0;
     P.op = q.in.empty() ? q.op : -1;
     const std::vector<Scalar> one{q.k};
