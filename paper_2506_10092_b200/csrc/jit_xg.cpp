@@ -70,7 +70,8 @@ Nvrtc& nvrtc() {
 const char* kPrelude = R"(
 typedef long long i64;
 typedef unsigned long long u64;
-struct XgSegs { const i64* s; const i64* e; const i64* off; const i64* slot; const u64* cst; i64 n; i64 ncov; };
+struct XgSegs { const i64* s; const i64* e; const i64* off; const i64* slot; const u64* cst; i64 n; i64 ncov;
+                double* dpart; i64 dcells; };
 struct XgCol { const void* v; i64 center; };
 struct XgK { i64 i[24]; double f[24]; };
 __device__ __forceinline__ i64 ldg64(const i64* p, i64 i) { return __ldg(p + i); }
@@ -326,8 +327,10 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
     const dev::XgExpr& X = P.e[e];
     if (!X.rows) continue;
     if (X.acc_f)
-      o << "        { const double t = wsum_d(a" << e << "); if (lane == 0 && t != 0.0) atomicAdd((double*)tab + slot * NE + "
-        << e << ", t); a" << e << " = 0.0; }\n";
+      o << "        { const double t = wsum_d(a" << e << ");\n"
+           "          if (S.dpart) { if (lane == 0) S.dpart[(c0_ / chunk) * S.dcells + slot * NE + " << e << "] += t; }\n"
+           "          else if (lane == 0 && t != 0.0) atomicAdd((double*)tab + slot * NE + " << e << ", t);\n"
+           "          a" << e << " = 0.0; }\n";
     else
       o << "        { const u64 t = wsum_u(a" << e << "); if (lane == 0 && t != 0ull) atomicAdd(tab + slot * NE + " << e
         << ", t); a" << e << " = 0ull; }\n";

@@ -618,7 +618,10 @@ void col_to_rows(const CtxPtr& ctx, const DCol& c, DArr& positions, DArr& values
 }
 
 DArr decode_full(const CtxPtr& ctx, const DCol& c) {
-  if (!col_full_coverage(ctx, c)) fail("decode_full: column has gaps; use to_rows");
+  // covered_rows() == total_size (column.cpp:311-314); RLE+Index: runs + points
+  const bool full = c.enc == RQ_ENC_RLE_INDEX ? covered_rows(ctx, c.s, c.e) + c.p2.n == c.total
+                                              : col_full_coverage(ctx, c);
+  if (!full) fail("decode_full: column has gaps; use to_rows");
   switch (c.enc) {
     case RQ_ENC_PLAIN: return decode_plain(ctx, c);
     case RQ_ENC_PLAIN_INDEX: return decode_plain_index(ctx, c);

@@ -440,6 +440,12 @@ GroupAggOut group_aggregate(const CtxPtr& ctx, const std::vector<const DCol*>& k
     const DArr& v = ma.values[nk + d];
     const int fn = fns[d];
     const bool flt = dt_float(v.dt);
+    if ((flt && fn == RQ_SUM) || fn == RQ_AVG || fn == RQ_STD || fn == RQ_VAR) {
+      // f64 sums folded per group in slot order (aggregate_array, k_boundary.cu):
+      // bit-identical to the reference's loop and from run to run
+      out.vals.push_back(gather(ctx, aggregate_array(ctx, ma.shape, v, gid, G, fn), present));
+      continue;
+    }
     int kind;
     unsigned long long init = 0;
     int32_t odt = RQ_F64;

@@ -989,8 +989,9 @@ __device__ __forceinline__ void xg_load4(const PlainSrc& s, int64_t row0, uint64
 }
 
 
+// dp (deterministic mode): this chunk's f64 partial table, written by lane 0 only
 __device__ __forceinline__ void xg_flush(const XgPlan& P, unsigned long long* tab, int64_t slot,
-                                         uint64_t (&acc)[XG_EXPRS]) {
+                                         uint64_t (&acc)[XG_EXPRS], double* dp) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int e = 0; e < XG_EXPRS; ++e) {
@@ -998,7 +999,11 @@ __device__ __forceinline__ void xg_flush(const XgPlan& P, unsigned long long* ta
     if (P.e[e].acc_f) {
       double v = __longlong_as_double(static_cast<long long>(acc[e]));
       v = warp_sum(v);
-      if (lane == 0 && v != 0.0) atomicAdd(reinterpret_cast<double*>(tab) + slot * P.ne + e, v);
+      if (dp) {
+        if (lane == 0) dp[slot * P.ne + e] += v;
+      } else if (lane == 0 && v != 0.0) {
+        atomicAdd(reinterpret_cast<double*>(tab) + slot * P.ne + e, v);
+      }
     } else {
       unsigned long long v = warp_sum(static_cast<unsigned long long>(acc[e]));
       if (lane == 0 && v != 0ull) atomicAdd(tab + slot * P.ne + e, v);
@@ -1177,7 +1182,7 @@ __global__ void __launch_bounds__(BLOCK)
       c = min(c1, off + (e - s + 1));
       // flush at segment ends where the slot changes, and at the chunk end
       const int64_t next_slot = (c < c1 && k + 1 < S.n) ? ldg64(S.slot, k + 1) : -1;
-      if (next_slot != slot) xg_flush(P, tab, slot, acc);
+      if (next_slot != slot) xg_flush(P, tab, slot, acc, S.dpart ? S.dpart + (c0 / chunk) * S.dcells : nullptr);
       __syncwarp();
       ++k;
     }
@@ -1301,6 +1306,7 @@ __global__ void k_xg_finish(const int64_t* __restrict__ slots, int64_t ng, int n
 struct XgFinish {
   int ne;
   int fn[XG_EXPRS];
+  int isf[XG_EXPRS];  // the table cell holds f64 bits (else a wrapping int64 sum)
   void* out[XG_EXPRS];
 };
 __global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_t* __restrict__ slots, int64_t ng,
@@ -1313,15 +1319,34 @@ __global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_
       const int fn = F.fn[ei];
       if (fn == RQ_COUNT) {
         static_cast<long long*>(F.out[ei])[i] = static_cast<long long>(c);
-      } else if (fn == RQ_AVG) {
-        static_cast<double*>(F.out[ei])[i] =
-            c ? __longlong_as_double(static_cast<long long>(tab[g * F.ne + ei])) / static_cast<double>(c)
-              : __longlong_as_double(0x7ff8000000000000ll);
+      } else if (fn == RQ_AVG) {  // f64(Σ) / count (groupby.cpp:103-106); an integer Σ is exact in int64
+        const unsigned long long t = tab[g * F.ne + ei];
+        const double sum = F.isf[ei] ? __longlong_as_double(static_cast<long long>(t))
+                                     : static_cast<double>(static_cast<long long>(t));
+        static_cast<double*>(F.out[ei])[i] = c ? sum / static_cast<double>(c) : __longlong_as_double(0x7ff8000000000000ll);
       } else {
         static_cast<unsigned long long*>(F.out[ei])[i] = tab[g * F.ne + ei];
       }
     }
   }
+}
+
+// deterministic f64 fold: cell blockIdx.x of every chunk's partial table,
+// a fixed strided split over the block's threads and a fixed-shape tree
+__global__ void k_xg_dfold(const double* __restrict__ dpart, int64_t nchunks, int64_t cells, int ne,
+                           const int* __restrict__ is_f, unsigned long long* __restrict__ tab) {
+  __shared__ double red[256];
+  const int64_t cell = blockIdx.x;
+  if (!is_f[cell % ne]) return;
+  double acc = 0.0;
+  for (int64_t q = threadIdx.x; q < nchunks; q += 256) acc += dpart[q * cells + cell];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tab[cell] = static_cast<unsigned long long>(__double_as_longlong(red[0]));
 }
 
 __global__ void k_xg_lengths(const int64_t* __restrict__ s, const int64_t* __restrict__ e, int64_t n,
@@ -1892,7 +1917,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       vf = vf || yf;
     }
     X.res_f = vf;
-    X.acc_f = (vf || fns[i] == RQ_AVG) ? 1 : 0;
+    X.acc_f = vf ? 1 : 0;  // integer results (AVG too) sum exactly in int64
   }
   // plain columns referenced by a Plain+Index expression are read as their base
   P.nc = static_cast<int>(plain_cols.size());
@@ -2049,9 +2074,11 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   DArr cnt = new_table(ctx, G, 0);
   int* err = reinterpret_cast<int*>(ctx->tickets + 2);  // zero between launches (reset after the check)
   dev::XgSegs S{s.pos(), e.pos(), off.pos(), slot.pos(), reinterpret_cast<const uint64_t*>(cst_all.raw()), nseg,
-                ncov};
+                ncov, nullptr, 0};
   auto* tabp = reinterpret_cast<unsigned long long*>(tab.raw_mut());
   auto* cntp = reinterpret_cast<unsigned long long*>(cnt.raw_mut());
+  DArr dpart;
+  int64_t dchunks = 0;
   if (nseg) {
     dev::k_xg_segs<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(P, S, tabp, cntp, err);
     launched(ctx);
@@ -2064,6 +2091,18 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     const int64_t warps = static_cast<int64_t>(ctx->sm_count) * 8 * (B / 32);
     int64_t chunk = (ncov + warps - 1) / warps;
     chunk = std::max<int64_t>(512, (chunk + 127) / 128 * 128);
+    // f64 row sums: per-chunk partial tables + a fixed-order fold, so two runs
+    // give bit-identical results (atomics only past the table budget)
+    bool any_f = false;
+    for (int i = 0; i < P.ne; ++i) any_f = any_f || (P.e[i].rows && P.e[i].acc_f);
+    const int64_t nchunks = (ncov + chunk - 1) / chunk;
+    if (any_f && nchunks * cells <= (int64_t{8} << 20)) {
+      dpart = alloc_arr(ctx, RQ_F64, nchunks * cells);
+      RQ_CUDA_CHECK(cudaMemsetAsync(dpart.raw_mut(), 0, static_cast<size_t>(nchunks * cells) * 8, ctx->stream));
+      S.dpart = dpart.as<double>();
+      S.dcells = cells;
+      dchunks = nchunks;
+    }
     const int64_t blocks = std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
                                              (ncov / chunk + (B / 32)) / (B / 32) + 1);
     constexpr size_t smem = dev::xg_rows_smem<B>();
@@ -2074,6 +2113,14 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
         !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks)))
       dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
     launched(ctx);
+    if (S.dpart) {
+      int isf[dev::XG_EXPRS] = {0};
+      for (int i = 0; i < P.ne; ++i) isf[i] = P.e[i].rows && P.e[i].acc_f;
+      DArr isf_d = upload_arr(ctx, RQ_I32, isf, P.ne);
+      dev::k_xg_dfold<<<static_cast<unsigned>(cells), 256, 0, ctx->stream>>>(S.dpart, dchunks, cells, P.ne,
+                                                                             isf_d.as<int>(), tabp);
+      launched(ctx);
+    }
   }
   for (auto& pe : pi_exprs) {  // Plain+Index: outliers inside segments (located by search, not materialised)
     const DCol& c = *pe.second;
@@ -2126,6 +2173,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     const int32_t odt = fn == RQ_COUNT ? RQ_I64 : (fn == RQ_AVG || P.e[i].res_f) ? RQ_F64 : RQ_I64;
     DArr res = alloc_arr(ctx, odt, ng);
     F.fn[i] = fn;
+    F.isf[i] = P.e[i].acc_f;
     F.out[i] = res.raw_mut();
     out.vals.push_back(res);
   }

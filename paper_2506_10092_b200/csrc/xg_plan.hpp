@@ -30,7 +30,7 @@ struct XgExpr {
   int nt;     // 1..3 terms
   int op[2];  // chain ops, left-deep: ((t0 op0 t1) op1 t2)
   XgTerm t[3];
-  int acc_f;  // accumulate in f64 (float result, or AVG)
+  int acc_f;  // accumulate in f64 (float result); integer results (AVG too) accumulate in int64
   int res_f;  // expression result is f64
   int rows;   // evaluated per row (references a plain column)
 };
@@ -51,6 +51,11 @@ struct XgSegs {
   const uint64_t* cst;  // [XG_CONSTS][nseg] RLE operand values (i64 / f64 bits)
   int64_t n;
   int64_t ncov;
+  // deterministic f64 sums: each chunk (a warp's covered-row range) writes its
+  // per-cell partial to dpart[chunk * dcells + cell] (no atomics); a fixed-
+  // order fold adds them up. Null: atomic adds (order-dependent last bits).
+  double* dpart;
+  int64_t dcells;
 };
 
 }  // namespace dev

@@ -313,10 +313,11 @@ class Shape:
         return cls(k, int(n.value), get(s), get(e), get(p))
 
     def _args(self, ctx):
-        h = lambda x: _arr_in(x, ctx).handle if x is not None else None  # noqa: E731
-        keep = [self.s, self.e, self.p]
+        """ctypes arguments (kind, n, s, e, p); the uploaded arrays stay alive
+        on the shape until the next call."""
+        self._dev = [_arr_in(x, ctx, np.int64) if x is not None else None for x in (self.s, self.e, self.p)]
         return (C.c_int32(self.KINDS.index(self.kind)), C.c_int64(int(self.n if self.kind == "dense" else 0)),
-                h(keep[0]), h(keep[1]), h(keep[2]))
+                *[d.handle if d is not None else None for d in self._dev])
 
     def __repr__(self):
         return f"Shape({self.kind}, n={self.n})"
