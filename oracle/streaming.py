@@ -325,10 +325,11 @@ def q1_partial(t: Dict[str, H.Column], cutoff: int, so: StreamingOracle = None) 
     sq = so.fold_runs(seg, t["l_quantity"])
     price = t["l_extendedprice"].values
     disc, tax = t["l_discount"], t["l_tax"]
-    assert disc.center is None and tax.center is None
+    # decoded value = stored + centre (column.cpp:283-297): 100 − disc = −stored + (100 − centre)
+    dc, tc = disc.center or 0, tax.center or 0
     sp = so.fold_plain_f64(seg, price)
-    sdp = so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100))
-    sch = so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100), f2=(tax.values, 1, 100))
+    sdp = so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100 - dc))
+    sch = so.fold_plain_f64(seg, price, f1=(disc.values, -1, 100 - dc), f2=(tax.values, 1, 100 + tc))
     sd = so.fold_plain_int(seg, disc)
     keep = cnt > 0
     keys, ints = _present(seg, cnt, seg.keys, [sq, sd, cnt])

@@ -18,8 +18,14 @@ linestatus {F,O} → 0..1, shipdate days since 1970 in [8036, 10561], quantity
 decimals as floats, here hundredths keep the sums exact), extendedprice f64.
 Tables are sorted per query as in the paper's Table 7:
 Q1 by (returnflag, linestatus, shipdate, quantity), Q6 by (quantity,
-discount, shipdate); low-cardinality sort keys are RLE, discount/tax narrow
-plain (i8), price plain f64 — what choose_encoding picks (ingest.cpp:217-271).
+discount, shipdate); low-cardinality sort keys are RLE, discount/tax
+plain-centered i8, price plain f64. At SF100 that is exactly what the
+device's choose_encoding (ingest.cpp:217-271; itself checked against the
+reference's) picks for each decoded column — tests/test_gpu_encode_choice.py
+runs it on the full 600M-row columns. (At SF1-SF10 the heuristic picks
+plain-centered for some sort keys whose runs are still short, e.g. Q6's
+shipdate below ~SF50; the generator keeps the SF100 encodings at every
+scale so the plan shape is the same.)
 """
 from __future__ import annotations
 
@@ -32,6 +38,7 @@ ROWS_PER_SF = 6_000_000
 SHIP_LO, SHIP_HI = 8036, 10561      # 1992-01-02 .. 1998-12-01
 Q6_LO, Q6_HI = 8766, 9131           # [1994-01-01, 1995-01-01)
 Q1_CUTOFF = 10471                   # 1998-09-02
+DISC_CENTER, TAX_CENTER = 5, 4      # choose_encoding's plain-centered centres (mid-range)
 
 
 def _rle_from_sorted(vals: np.ndarray, total: int) -> H.RleColumn:
@@ -118,16 +125,18 @@ def lineitem_q1(n: int, seed: int = 43, part=None, slicer=None):
     cat = lambda xs: np.concatenate([np.asarray(x) for x in xs])
     qty = _rle_from_counts(cat(qv), cat(qc), n)
     lo, hi = part_range(n, part, qty)
-    disc = positional(n, seed + 1, lo, hi, lambda r, m: r.integers(0, 11, m).astype(np.int8), np.int8)
-    tax = positional(n, seed + 2, lo, hi, lambda r, m: r.integers(0, 9, m).astype(np.int8), np.int8)
+    # plain-centered i8 (storage = value − centre), the heuristic's pick for
+    # these columns (tests/test_gpu_encode_choice.py)
+    disc = positional(n, seed + 1, lo, hi, lambda r, m: (r.integers(0, 11, m) - DISC_CENTER).astype(np.int8), np.int8)
+    tax = positional(n, seed + 2, lo, hi, lambda r, m: (r.integers(0, 9, m) - TAX_CENTER).astype(np.int8), np.int8)
     price = positional(n, seed + 3, lo, hi, lambda r, m: r.uniform(900.0, 105000.0, m), np.float64)
     return {
         "l_returnflag": cut(_rle_from_counts(cat(rfv), cat(rfc), n), lo, hi, slicer),
         "l_linestatus": cut(_rle_from_counts(cat(lsv), cat(lsc), n), lo, hi, slicer),
         "l_shipdate": cut(_rle_from_counts(cat(shv), cat(shc), n), lo, hi, slicer),
         "l_quantity": cut(qty, lo, hi, slicer),
-        "l_discount": H.PlainColumn(disc, H.I64),
-        "l_tax": H.PlainColumn(tax, H.I64),
+        "l_discount": H.PlainColumn(disc, H.I64, DISC_CENTER),
+        "l_tax": H.PlainColumn(tax, H.I64, TAX_CENTER),
         "l_extendedprice": H.PlainColumn(price),
     }
 
