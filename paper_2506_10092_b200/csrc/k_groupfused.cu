@@ -1333,11 +1333,14 @@ __global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_
 
 // deterministic f64 fold: cell blockIdx.x of every chunk's partial table,
 // a fixed strided split over the block's threads and a fixed-shape tree
-__global__ void k_xg_dfold(const double* __restrict__ dpart, int64_t nchunks, int64_t cells, int ne,
-                           const int* __restrict__ is_f, unsigned long long* __restrict__ tab) {
+struct XgIsF {
+  int f[XG_EXPRS];
+};
+__global__ void k_xg_dfold(const double* __restrict__ dpart, int64_t nchunks, int64_t cells, int ne, XgIsF is_f,
+                           unsigned long long* __restrict__ tab) {
   __shared__ double red[256];
   const int64_t cell = blockIdx.x;
-  if (!is_f[cell % ne]) return;
+  if (!is_f.f[cell % ne]) return;
   double acc = 0.0;
   for (int64_t q = threadIdx.x; q < nchunks; q += 256) acc += dpart[q * cells + cell];
   red[threadIdx.x] = acc;
@@ -2114,11 +2117,10 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
     launched(ctx);
     if (S.dpart) {
-      int isf[dev::XG_EXPRS] = {0};
-      for (int i = 0; i < P.ne; ++i) isf[i] = P.e[i].rows && P.e[i].acc_f;
-      DArr isf_d = upload_arr(ctx, RQ_I32, isf, P.ne);
-      dev::k_xg_dfold<<<static_cast<unsigned>(cells), 256, 0, ctx->stream>>>(S.dpart, dchunks, cells, P.ne,
-                                                                             isf_d.as<int>(), tabp);
+      dev::XgIsF isf{};  // by value: no host staging
+      for (int i = 0; i < P.ne; ++i) isf.f[i] = P.e[i].rows && P.e[i].acc_f;
+      dev::k_xg_dfold<<<static_cast<unsigned>(cells), 256, 0, ctx->stream>>>(S.dpart, dchunks, cells, P.ne, isf,
+                                                                             tabp);
       launched(ctx);
     }
   }
