@@ -478,7 +478,11 @@ bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S
   const char* mb = std::getenv("RQ_JIT_MINB");
   // the L2 prefetch pays on long segments (Q1: 1.20 -> 1.12 ms, C3's row pass
   // -4%) and costs on plans of many short selected segments (Q6: +20%)
-  const int pf = S.n > 0 && S.ncov / S.n >= 2048 ? prefetch_distance() : 0;
+  static const int64_t pf_min = [] {  // segment length from which the prefetch pays (RQ_JIT_PF_MIN)
+    const char* e = std::getenv("RQ_JIT_PF_MIN");
+    return e ? std::atoll(e) : int64_t{2048};
+  }();
+  const int pf = S.n > 0 && S.ncov / S.n >= pf_min ? prefetch_distance() : 0;
   const std::string sig = plan_signature(P, mb ? std::atoi(mb) : 3, pf);
   cudaKernel_t k = nullptr;
   {

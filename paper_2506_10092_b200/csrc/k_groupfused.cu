@@ -2099,7 +2099,8 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     bool any_f = false;
     for (int i = 0; i < P.ne; ++i) any_f = any_f || (P.e[i].rows && P.e[i].acc_f);
     const int64_t nchunks = (ncov + chunk - 1) / chunk;
-    if (any_f && nchunks * cells <= (int64_t{8} << 20)) {
+    static const bool nodet = std::getenv("RQ_XG_NODET") != nullptr;  // A/B knob: atomic f64 flushes
+    if (any_f && !nodet && nchunks * cells <= (int64_t{8} << 20)) {
       dpart = alloc_arr(ctx, RQ_F64, nchunks * cells);
       RQ_CUDA_CHECK(cudaMemsetAsync(dpart.raw_mut(), 0, static_cast<size_t>(nchunks * cells) * 8, ctx->stream));
       S.dpart = dpart.as<double>();
