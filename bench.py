@@ -333,12 +333,14 @@ class C1(Workload):
     tag = "pair_reduce"
 
     def describe(self):
-        return "C1: SUM(A+B) over two misaligned RLE i64 columns, L=64/96"
+        la, lb = getattr(self.args, "c1_runs", (64, 96))
+        return f"C1: SUM(A+B) over two misaligned RLE i64 columns, L={la}/{lb}"
 
     def gen(self, rows, seed, part=None, slicer=None):
         from paper_2506_10092_b200 import datagen as G
         from paper_2506_10092_b200 import sharding
-        a, b = G.c1_tables(rows, 64, 96, seed)
+        la, lb = getattr(self.args, "c1_runs", (64, 96))
+        a, b = G.c1_tables(rows, la, lb, seed)
         t = {"a": a, "b": b}
         return t if part is None else sharding.shard_table(t, part[0], part[1], snap="a")
 
@@ -722,6 +724,7 @@ def main():
     ap.add_argument("--rows", type=int, default=None,
                     help="logical rows per GPU (default 1B; SF100 = 600M for q6/q1; 750M for c5)")
     ap.add_argument("--variant", default="rle", choices=["rle", "narrow"])
+    ap.add_argument("--c1-runs", default="64,96", help="C1 mean run lengths of A,B (SURVEY §8d sweep: 16,24 / 64,96 / 1000,1500)")
     ap.add_argument("--path", default="fused", choices=["fused", "chain"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -730,6 +733,7 @@ def main():
                          "transport over gloo (several ranks may share a GPU: tests of the N>1 logic)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    args.c1_runs = tuple(int(x) for x in args.c1_runs.split(","))
     if args.rows is None:
         args.rows = {"q6": 600_000_000, "q1": 600_000_000, "c5": 750_000_000}.get(args.workload, 1_000_000_000)
     w = WORKLOADS[args.workload](args)
