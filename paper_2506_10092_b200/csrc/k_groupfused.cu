@@ -623,6 +623,10 @@ void fold_column(const CtxPtr& ctx, const GroupKey& K, const DCol& d, dev::GTabl
 
 DArr new_table(const CtxPtr& ctx, int64_t G, unsigned long long init) {
   DArr t = alloc_arr(ctx, RQ_I64, G);
+  if (init == 0) {  // a memset, not a kernel
+    if (G) RQ_CUDA_CHECK(cudaMemsetAsync(t.raw_mut(), 0, static_cast<size_t>(G) * 8, ctx->stream));
+    return t;
+  }
   dev::k_gk_init<<<grid_cap(ctx, G), 256, 0, ctx->stream>>>(reinterpret_cast<unsigned long long*>(t.raw_mut()), G, init);
   launched(ctx);
   return t;
@@ -1313,7 +1317,7 @@ __global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_
                                 const unsigned long long* __restrict__ tab, const unsigned long long* __restrict__ cnt) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < ng;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t g = ldg64(slots, i);
+    const int64_t g = slots ? ldg64(slots, i) : i;  // null: the slots are 0..ng-1 (no keys: one group)
     const unsigned long long c = cnt[g];
     for (int ei = 0; ei < F.ne; ++ei) {
       const int fn = F.fn[ei];
@@ -1618,13 +1622,6 @@ __global__ void k_xg_outliers_seg(PlainSrc base, const int64_t* __restrict__ p, 
 }  // namespace dev
 
 namespace {
-
-DArr xg_fill(const CtxPtr& ctx, int64_t v) {  // one-element device array
-  DArr a = alloc_arr(ctx, RQ_I64, 1);
-  dev::k_xg_fill1<<<1, 1, 0, ctx->stream>>>(a.as<int64_t>(), v);
-  launched(ctx);
-  return a;
-}
 
 // 16-B aligned base and room for the 8-row vector groups past the last row
 // (the generated kernel reads 8 rows per lane, the interpreted one 4)
@@ -2150,7 +2147,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   stage = std::make_unique<KTimer>(ctx, "xg_out");
   DArr present;
   if (keys.empty()) {
-    present = xg_fill(ctx, 0);
+    present.n = 1;  // one group (slot 0): finish reads no slot list
   } else {
     DArr flags = alloc_arr(ctx, RQ_I8, G);
     dev::k_gk_flags<<<grid_cap(ctx, G), 256, 0, ctx->stream>>>(reinterpret_cast<const unsigned long long*>(cnt.raw()),
@@ -2182,7 +2179,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   }
   if (ng) {
     dev::k_xg_finish_all<<<grid_cap(ctx, ng), 256, 0, ctx->stream>>>(
-        F, present.pos(), ng, reinterpret_cast<const unsigned long long*>(tab.raw()),
+        F, keys.empty() ? nullptr : present.pos(), ng, reinterpret_cast<const unsigned long long*>(tab.raw()),
         reinterpret_cast<const unsigned long long*>(cnt.raw()));
     launched(ctx);
   }
