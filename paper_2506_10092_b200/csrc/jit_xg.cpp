@@ -71,7 +71,7 @@ const char* kPrelude = R"(
 typedef long long i64;
 typedef unsigned long long u64;
 struct XgSegs { const i64* s; const i64* e; const i64* off; const i64* slot; const u64* cst; i64 n; i64 ncov;
-                double* dpart; i64 dcells; };
+                double* dpart; i64 dcells; const i64* dims; i64 cstride; };
 struct XgCol { const void* v; i64 center; };
 struct XgK { i64 i[24]; double f[24]; };
 __device__ __forceinline__ i64 ldg64(const i64* p, i64 i) { return __ldg(p + i); }
@@ -225,18 +225,24 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
   o << "  const i64 nwarps = ((i64)gridDim.x * 256) >> 5;\n  int lerr = 0;\n";
   for (int e = 0; e < P.ne; ++e)
     if (P.e[e].rows) o << "  " << (P.e[e].acc_f ? "double" : "u64") << " a" << e << " = 0;\n";
-  o << "  for (i64 c0_ = warp * chunk; c0_ < S.ncov; c0_ += nwarps * chunk) {\n"
-       "    const i64 c1_ = min(c0_ + chunk, S.ncov);\n"
-       "    i64 k = warp_lb(S.off, S.n, c0_ + 1) - 1;\n"
+  // (segments, covered rows) from the device when the table was built without a readback;
+  // chunk 0: derived from them as the host does (xg_chunk)
+  o << "  const i64 nseg_ = S.dims ? ldg64(S.dims, 0) : S.n, ncov_ = S.dims ? ldg64(S.dims, 1) : S.ncov;\n"
+       "  i64 chunk_ = chunk;\n"
+       "  if (chunk_ <= 0) { chunk_ = (ncov_ + nwarps - 1) / nwarps; chunk_ = (chunk_ + 127) / 128 * 128;"
+       " if (chunk_ < 512) chunk_ = 512; }\n";
+  o << "  for (i64 c0_ = warp * chunk_; c0_ < ncov_; c0_ += nwarps * chunk_) {\n"
+       "    const i64 c1_ = min(c0_ + chunk_, ncov_);\n"
+       "    i64 k = warp_lb(S.off, nseg_, c0_ + 1) - 1;\n"
        "    i64 c = c0_;\n"
        "    while (c < c1_) {\n"
        "      const i64 off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k);\n"
        "      const i64 slot = ldg64(S.slot, k);\n";
   for (int j = 0; j < P.ncst; ++j) {
     if (P.cst_f[j])
-      o << "      const double k" << j << " = __longlong_as_double((long long)__ldg(S.cst + " << j << " * S.n + k));\n";
+      o << "      const double k" << j << " = __longlong_as_double((long long)__ldg(S.cst + " << j << " * S.cstride + k));\n";
     else
-      o << "      const i64 k" << j << " = (i64)__ldg(S.cst + " << j << " * S.n + k);\n";
+      o << "      const i64 k" << j << " = (i64)__ldg(S.cst + " << j << " * S.cstride + k);\n";
   }
   o << "      const i64 r0 = s + (c - off);\n"
        "      const i64 r1 = min(e, s + (c1_ - off) - 1);\n"
@@ -321,14 +327,14 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
   }
   o << "        }\n      }\n";
   o << "      c = min(c1_, off + (e - s + 1));\n"
-       "      const i64 next_slot = (c < c1_ && k + 1 < S.n) ? ldg64(S.slot, k + 1) : -1;\n"
+       "      const i64 next_slot = (c < c1_ && k + 1 < nseg_) ? ldg64(S.slot, k + 1) : -1;\n"
        "      if (next_slot != slot) {\n";
   for (int e = 0; e < P.ne; ++e) {
     const dev::XgExpr& X = P.e[e];
     if (!X.rows) continue;
     if (X.acc_f)
       o << "        { const double t = wsum_d(a" << e << ");\n"
-           "          if (S.dpart) { if (lane == 0) S.dpart[(c0_ / chunk) * S.dcells + slot * NE + " << e << "] += t; }\n"
+           "          if (S.dpart) { if (lane == 0) S.dpart[(c0_ / chunk_) * S.dcells + slot * NE + " << e << "] += t; }\n"
            "          else if (lane == 0 && t != 0.0) atomicAdd((double*)tab + slot * NE + " << e << ", t);\n"
            "          a" << e << " = 0.0; }\n";
     else
@@ -470,7 +476,7 @@ void plan_literals(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<d
 }
 
 bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S, int64_t chunk,
-                   unsigned long long* tab, int64_t G, int* err, unsigned blocks) {
+                   unsigned long long* tab, int64_t G, int* err, unsigned blocks, int64_t avg_len) {
   std::vector<int64_t> ki;
   std::vector<double> kf;
   plan_literals(P, ki, kf);
@@ -482,7 +488,7 @@ bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S
     const char* e = std::getenv("RQ_JIT_PF_MIN");
     return e ? std::atoll(e) : int64_t{2048};
   }();
-  const int pf = S.n > 0 && S.ncov / S.n >= pf_min ? prefetch_distance() : 0;
+  const int pf = avg_len >= pf_min ? prefetch_distance() : 0;
   const std::string sig = plan_signature(P, mb ? std::atoi(mb) : 3, pf);
   cudaKernel_t k = nullptr;
   {

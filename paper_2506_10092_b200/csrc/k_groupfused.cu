@@ -1104,14 +1104,16 @@ __global__ void __launch_bounds__(BLOCK)
   uint64_t acc[XG_EXPRS];
 #pragma unroll
   for (int e = 0; e < XG_EXPRS; ++e) acc[e] = 0;
-  for (int64_t c0 = warp * chunk; c0 < S.ncov; c0 += nwarps * chunk) {
-    const int64_t c1 = min(c0 + chunk, S.ncov);
-    int64_t k = warp_lower_bound(S.off, S.n, c0 + 1) - 1;  // segment holding covered row c0
+  const int64_t nseg = S.dims ? ldg64(S.dims, 0) : S.n, ncov = S.dims ? ldg64(S.dims, 1) : S.ncov;
+  if (chunk <= 0) chunk = xg_chunk(ncov, nwarps);
+  for (int64_t c0 = warp * chunk; c0 < ncov; c0 += nwarps * chunk) {
+    const int64_t c1 = min(c0 + chunk, ncov);
+    int64_t k = warp_lower_bound(S.off, nseg, c0 + 1) - 1;  // segment holding covered row c0
     int64_t c = c0;
     while (c < c1) {
       const int64_t off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k);
       const int64_t slot = ldg64(S.slot, k);
-      if (lane < P.ncst) wk[lane] = __ldg(S.cst + lane * S.n + k);
+      if (lane < P.ncst) wk[lane] = __ldg(S.cst + lane * S.cstride + k);
       __syncwarp();
       const int64_t r0 = s + (c - off);
       const int64_t r1 = min(e, s + (c1 - off) - 1);
@@ -1185,7 +1187,7 @@ __global__ void __launch_bounds__(BLOCK)
       }
       c = min(c1, off + (e - s + 1));
       // flush at segment ends where the slot changes, and at the chunk end
-      const int64_t next_slot = (c < c1 && k + 1 < S.n) ? ldg64(S.slot, k + 1) : -1;
+      const int64_t next_slot = (c < c1 && k + 1 < nseg) ? ldg64(S.slot, k + 1) : -1;
       if (next_slot != slot) xg_flush(P, tab, slot, acc, S.dpart ? S.dpart + (c0 / chunk) * S.dcells : nullptr);
       __syncwarp();
       ++k;
@@ -1233,9 +1235,10 @@ __global__ void k_xg_segs(const __grid_constant__ XgPlan P, const __grid_constan
   // every lane of a warp runs the same number of iterations (warp-collective adds)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t first = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
-  for (int64_t base = first; base < S.n; base += stride) {
+  const int64_t nseg = S.dims ? ldg64(S.dims, 0) : S.n;
+  for (int64_t base = first; base < nseg; base += stride) {
     const int64_t k = base + (threadIdx.x & 31);
-    const bool ok = k < S.n;
+    const bool ok = k < nseg;
     const int64_t len = ok ? ldg64(S.e, k) - ldg64(S.s, k) + 1 : 0;
     const int64_t slot = ok ? ldg64(S.slot, k) : 0;
     xg_add_u64(cnt, slot, static_cast<uint64_t>(len));
@@ -1246,7 +1249,7 @@ __global__ void k_xg_segs(const __grid_constant__ XgPlan P, const __grid_constan
       int vf = 0;
       for (int ti = 0; ti < X.nt; ++ti) {
         const XgTerm& T = X.t[ti];
-        const uint64_t y = ok ? xg_term(T, __ldg(S.cst + (T.src - XG_COLS) * S.n + k), &lerr) : 0;
+        const uint64_t y = ok ? xg_term(T, __ldg(S.cst + (T.src - XG_COLS) * S.cstride + k), &lerr) : 0;
         const int yf = T.flt || (T.sop >= 0 && T.kflt);
         if (ti == 0) {
           v = y;
@@ -1465,13 +1468,25 @@ struct KwList {
   int cst;        // RLE operand: index of its per-fragment value array
   int64_t kmin, stride;
 };
+// A list's conjuncts on integer values folded on the host into one interval
+// and at most one value set (IN lists intersected; NE values excluded), so a
+// candidate tests two compares and a short set scan instead of interpreting
+// every conjunct (compare_scalar's f64 semantics are exact here: every float
+// literal is finite and below 2^52 in magnitude, kw_fold_conjuncts).
+struct KwConj {
+  int64_t lo, hi;  // lo <= v <= hi
+  int nset;
+  int set_in;      // 1: v must be in set; 0: v must not be
+  int64_t set[XG_IN];
+};
 struct KwPlan {
   int nl;
   KwList l[KW_LISTS];
   int64_t start[KW_LISTS + 1];  // candidate index of each list's first run end
   int np;
   XgPred p[XG_PREDS];  // p.src = list index
-  int own[KW_LISTS];   // list l has conjuncts
+  int own[KW_LISTS];   // list l has conjuncts: 1 folded (conj[l]), 2 interpreted (p[])
+  KwConj conj[KW_LISTS];
 };
 
 __device__ __forceinline__ int64_t kw_lower_bound(const int64_t* __restrict__ e, int64_t n, int64_t x) {
@@ -1489,11 +1504,31 @@ __device__ __forceinline__ uint64_t kw_value_bits(const void* v, int dt, int64_t
                              : static_cast<uint64_t>(ld_i64(v, dt, r));
 }
 
+__device__ __forceinline__ bool kw_conj(const KwConj& C, int64_t v) {
+  if (v < C.lo || v > C.hi) return false;
+  if (C.nset == 0) return true;
+  bool hit = false;
+#pragma unroll
+  for (int t = 0; t < XG_IN; ++t)
+    if (t < C.nset && C.set[t] == v) hit = true;
+  return hit == (C.set_in != 0);
+}
+
 __device__ __forceinline__ bool kw_pass(const XgPred& P, uint64_t v) {
   if (P.op >= 0) return xg_cmp1(v, P.flt, P.ki[0], P.kf[0], P.kflt[0], P.op);
   for (int t = 0; t < P.n_in; ++t)
     if (xg_cmp1(v, P.flt, P.ki[t], P.kf[t], P.kflt[t], RQ_EQ)) return true;
   return false;
+}
+
+// every conjunct of list l on value bits v
+__device__ __forceinline__ bool kw_own(const KwPlan& K, int l, uint64_t v) {
+  if (K.own[l] == 1) return kw_conj(K.conj[l], static_cast<int64_t>(v));
+  bool keep = true;
+#pragma unroll
+  for (int q = 0; q < XG_PREDS; ++q)
+    if (q < K.np && keep && K.p[q].src == l) keep = kw_pass(K.p[q], v);
+  return keep;
 }
 
 // One thread per run end. `kept` is zeroed beforehand: a candidate that
@@ -1502,10 +1537,12 @@ __device__ __forceinline__ bool kw_pass(const XgPred& P, uint64_t v) {
 // returns early (most run ends of a selective WHERE never search the other
 // lists); a kept one writes its fragment at its merged rank and adds to the
 // (segments, covered rows) counters.
-__global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __restrict__ kept,
+constexpr int KW_TILE = 2048;  // k_kway_select's tile (256 threads x 8 candidates)
+__global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __restrict__ kept,
                                   int64_t* __restrict__ seg_s, int64_t* __restrict__ seg_e,
                                   int64_t* __restrict__ seg_slot, uint64_t* __restrict__ seg_cst,
-                                  unsigned long long* __restrict__ dims) {
+                                  unsigned long long* __restrict__ dims, unsigned long long* __restrict__ tagg,
+                                  int64_t ntiles) {
   const int64_t N = K.start[K.nl];
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < N;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1515,12 +1552,7 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __r
     const int64_t i = c - K.start[j];
     const int64_t x = __ldg(J.e + i);
     bool keep = true;
-    if (K.own[j]) {  // this list's own conjuncts first: no search needed
-      const uint64_t v = kw_value_bits(J.v, J.dt, i);
-#pragma unroll
-      for (int q = 0; q < XG_PREDS; ++q)
-        if (q < K.np && keep && K.p[q].src == j) keep = kw_pass(K.p[q], v);
-    }
+    if (K.own[j]) keep = kw_own(K, j, kw_value_bits(J.v, J.dt, i));  // own conjuncts first: no search
     if (!keep) continue;
     int64_t rank = 0, start = __ldg(J.s + i);
     int64_t r[KW_LISTS];
@@ -1540,12 +1572,7 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __r
       start = max(start, __ldg(L.s + rl));
       r[l] = rl;
       rank += rl;
-      if (K.own[l]) {
-        const uint64_t v = kw_value_bits(L.v, L.dt, rl);
-#pragma unroll
-        for (int q = 0; q < XG_PREDS; ++q)
-          if (q < K.np && keep && K.p[q].src == l) keep = kw_pass(K.p[q], v);
-      }
+      if (K.own[l]) keep = kw_own(K, l, kw_value_bits(L.v, L.dt, rl));
     }
     if (!keep) continue;
     int64_t slot = 0;
@@ -1560,7 +1587,9 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __r
     seg_s[rank] = start;
     seg_e[rank] = x;
     seg_slot[rank] = slot;
-    // (segments, covered rows): one atomic pair per warp
+    // (segments, covered rows) in total and per k_kway_select tile of ranks
+    // (that kernel's tile offsets then come from a scan of these, not from a
+    // look-back chain): one atomic pair per warp and per tile the warp touches
     const unsigned act = __activemask();
     const unsigned long long len = static_cast<unsigned long long>(x - start + 1);
     // len < 2^40: two 20-bit halves, each summed over <= 32 lanes without overflow
@@ -1571,24 +1600,60 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, int64_t* __r
       atomicAdd(dims, static_cast<unsigned long long>(__popc(act)));
       atomicAdd(dims + 1, wl);
     }
+    const int64_t tile = rank / KW_TILE;
+    const unsigned peers = __match_any_sync(act, static_cast<unsigned long long>(tile));
+    const unsigned long long tl =
+        __reduce_add_sync(peers, static_cast<unsigned>(len & 0xfffffu)) +
+        (static_cast<unsigned long long>(__reduce_add_sync(peers, static_cast<unsigned>(len >> 20))) << 20);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) {
+      atomicAdd(tagg + tile, static_cast<unsigned long long>(__popc(peers)));
+      atomicAdd(tagg + ntiles + tile, tl);
+    }
   }
 }
 
-// kept candidates → the segment table (s, e, slot, cst, off) at their scanned
-// slots; the last thread writes (n segments, covered rows) to dims
-__global__ void k_kway_compact(int64_t N, int ncst, const int64_t* __restrict__ kept, const int64_t* __restrict__ exk,
-                               const int64_t* __restrict__ seg_s, const int64_t* __restrict__ seg_e,
-                               const int64_t* __restrict__ seg_slot, const uint64_t* __restrict__ seg_cst,
-                               int64_t* __restrict__ s, int64_t* __restrict__ e, int64_t* __restrict__ slot,
-                               uint64_t* __restrict__ cst) {
-  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < N;
-       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (!kept[c]) continue;
-    const int64_t o = exk[c];
-    s[o] = seg_s[c];
-    e[o] = seg_e[c];
-    slot[o] = seg_slot[c];
-    for (int j = 0; j < ncst; ++j) cst[static_cast<int64_t>(j) * N + o] = seg_cst[static_cast<int64_t>(j) * N + c];
+// kept candidates → the segment table: each tile's first slot and covered-row
+// offset come from the exclusive scan of the per-tile (count, rows) that
+// k_kway_candidates accumulated (tpre[t], tpre[ntiles + t] - tpre[ntiles]);
+// inside the tile a block scan places every kept fragment, written there
+// (s, e, slot, operand values at stride N, off). The totals stay on the
+// device (dims): nothing is read back before the row kernels run.
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK)
+    k_kway_select(int64_t N, int ncst, const uint8_t* __restrict__ kept, const int64_t* __restrict__ cs,
+                  const int64_t* __restrict__ ce, const int64_t* __restrict__ cslot, const uint64_t* __restrict__ ccst,
+                  const int64_t* __restrict__ tpre, int64_t ntiles, int64_t* __restrict__ s, int64_t* __restrict__ e,
+                  int64_t* __restrict__ slot, uint64_t* __restrict__ cst, int64_t* __restrict__ off) {
+  static_assert(BLOCK * ITEMS == KW_TILE, "tile of the per-tile aggregates");
+  __shared__ uint64_t wn[BLOCK / 32 + 1], wr[BLOCK / 32 + 1];
+  const int64_t base = (static_cast<int64_t>(blockIdx.x) * BLOCK + threadIdx.x) * ITEMS;
+  uint64_t len[ITEMS];
+  uint64_t cn = 0, cr = 0;
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t i = base + k;
+    const bool kk = i < N && kept[i];
+    len[k] = kk ? static_cast<uint64_t>(ldg64(ce, i) - ldg64(cs, i) + 1) : 0;
+    cn += kk;
+    cr += len[k];
+  }
+  uint64_t tn, tr;
+  uint64_t on = block_exclusive<BLOCK>(cn, tn, wn);
+  uint64_t orow = block_exclusive<BLOCK>(cr, tr, wr);
+  if (!cn) return;
+  on += static_cast<uint64_t>(ldg64(tpre, blockIdx.x));
+  orow += static_cast<uint64_t>(ldg64(tpre, ntiles + blockIdx.x) - ldg64(tpre, ntiles));
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    if (!len[k]) continue;
+    const int64_t i = base + k, o = static_cast<int64_t>(on);
+    s[o] = ldg64(cs, i);
+    e[o] = ldg64(ce, i);
+    slot[o] = ldg64(cslot, i);
+    for (int j = 0; j < ncst; ++j) cst[static_cast<int64_t>(j) * N + o] = __ldg(ccst + static_cast<int64_t>(j) * N + i);
+    off[o] = static_cast<int64_t>(orow);
+    ++on;
+    orow += len[k];
   }
 }
 
@@ -1599,8 +1664,9 @@ __global__ void k_kway_compact(int64_t N, int ncst, const int64_t* __restrict__ 
 // slot)
 __global__ void k_xg_outliers_seg(PlainSrc base, const int64_t* __restrict__ p, const void* __restrict__ v2, int v2dt,
                                   int64_t n, const int64_t* __restrict__ ss, const int64_t* __restrict__ se,
-                                  const int64_t* __restrict__ seg_slot, int64_t nseg, int ne, int ei, int acc_f,
-                                  unsigned long long* __restrict__ tab) {
+                                  const int64_t* __restrict__ seg_slot, int64_t nseg, const int64_t* __restrict__ dims,
+                                  int ne, int ei, int acc_f, unsigned long long* __restrict__ tab) {
+  if (dims) nseg = ldg64(dims, 0);
   for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nseg;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t a = ldg64(ss, k), b = ldg64(se, k);
@@ -1630,10 +1696,6 @@ bool xg_vec_ok(const DArr& a) {
   const size_t w = static_cast<size_t>(dt_width(a.dt));
   return (reinterpret_cast<uintptr_t>(a.buf->ptr) & 15) == 0 &&
          a.buf->cap >= static_cast<size_t>((a.n + 7) & ~int64_t(7)) * w;
-}
-
-DArr xg_const_bits(const CtxPtr& ctx, const DArr& v) {
-  return cast_values(ctx, v, dt_float(v.dt) ? RQ_F64 : RQ_I64);
 }
 
 // Several gathers in one launch, each array through its own index array (all
@@ -1694,15 +1756,112 @@ bool key_layout(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKe
   return true;
 }
 
-// The segment table in one pass over every run list (k_kway_candidates):
-// s / e / slot / per-segment RLE-operand values / covered-row offsets, with
-// one readback (segment count, covered rows). Returns false when the lists
-// do not fit the kernel (the pairwise path then builds the table).
+// Fold each list's conjuncts on integer values into KwConj (interval ∩ one
+// value set); lists whose values are float, or with a float literal that is
+// not finite or exceeds 2^52 in magnitude (where compare_scalar's f64
+// rounding could differ from an integer compare), stay interpreted.
+void kw_fold_conjuncts(dev::KwPlan& KP, const std::vector<int>& list_float) {
+  constexpr double LIM = 4503599627370496.0;  // 2^52
+  for (int l = 0; l < KP.nl; ++l) {
+    if (!KP.own[l]) continue;
+    KP.own[l] = 2;
+    if (list_float[static_cast<size_t>(l)]) continue;
+    int64_t lo = INT64_MIN, hi = INT64_MAX;
+    bool have_in = false, ok = true;
+    std::vector<int64_t> in, out;
+    for (int q = 0; q < KP.np && ok; ++q) {
+      const dev::XgPred& P = KP.p[q];
+      if (P.src != l) continue;
+      if (P.op >= 0) {
+        int64_t k = P.ki[0];
+        double kf = P.kf[0];
+        if (P.kflt[0] && !(std::isfinite(kf) && std::fabs(kf) < LIM)) {
+          ok = false;
+          break;
+        }
+        // the integer bound equivalent to x op k (x integral)
+        const bool integral = !P.kflt[0] || std::floor(kf) == kf;
+        const int64_t fl = P.kflt[0] ? static_cast<int64_t>(std::floor(kf)) : k;
+        const int64_t ce = P.kflt[0] ? static_cast<int64_t>(std::ceil(kf)) : k;
+        switch (P.op) {
+          case RQ_LT: if (ce == INT64_MIN) { lo = INT64_MAX; hi = INT64_MIN; } else hi = std::min(hi, ce - 1); break;
+          case RQ_LE: hi = std::min(hi, fl); break;
+          case RQ_GE: lo = std::max(lo, ce); break;
+          case RQ_GT: if (fl == INT64_MAX) { lo = INT64_MAX; hi = INT64_MIN; } else lo = std::max(lo, fl + 1); break;
+          case RQ_EQ:
+            if (!integral) { lo = INT64_MAX; hi = INT64_MIN; }
+            else { lo = std::max(lo, fl); hi = std::min(hi, fl); }
+            break;
+          case RQ_NE: if (integral) out.push_back(fl); break;
+          default: ok = false;
+        }
+      } else {
+        std::vector<int64_t> vals;
+        for (int t = 0; t < P.n_in; ++t) {
+          if (P.kflt[t]) {
+            const double kf = P.kf[t];
+            if (std::isnan(kf)) continue;  // never equal
+            if (!(std::isfinite(kf) && std::fabs(kf) < LIM)) { ok = false; break; }
+            if (std::floor(kf) != kf) continue;
+            vals.push_back(static_cast<int64_t>(kf));
+          } else {
+            vals.push_back(P.ki[t]);
+          }
+        }
+        if (!have_in) {
+          in = vals;
+          have_in = true;
+        } else {
+          std::vector<int64_t> keep;
+          for (int64_t v : in)
+            if (std::find(vals.begin(), vals.end(), v) != vals.end()) keep.push_back(v);
+          in.swap(keep);
+        }
+      }
+    }
+    if (!ok) continue;
+    dev::KwConj& C = KP.conj[l];
+    C.lo = lo;
+    C.hi = hi;
+    if (have_in) {
+      std::vector<int64_t> keep;
+      for (int64_t v : in)
+        if (v >= lo && v <= hi && std::find(out.begin(), out.end(), v) == out.end() &&
+            std::find(keep.begin(), keep.end(), v) == keep.end())
+          keep.push_back(v);
+      if (keep.empty()) {  // nothing passes
+        C.lo = 1;
+        C.hi = 0;
+      }
+      if (keep.size() > static_cast<size_t>(dev::XG_IN)) continue;
+      C.nset = static_cast<int>(keep.size());
+      C.set_in = 1;
+      for (size_t t = 0; t < keep.size(); ++t) C.set[t] = keep[t];
+    } else {
+      std::vector<int64_t> ex;
+      for (int64_t v : out)
+        if (v >= lo && v <= hi && std::find(ex.begin(), ex.end(), v) == ex.end()) ex.push_back(v);
+      if (ex.size() > static_cast<size_t>(dev::XG_IN)) continue;
+      C.nset = static_cast<int>(ex.size());
+      C.set_in = 0;
+      for (size_t t = 0; t < ex.size(); ++t) C.set[t] = ex[t];
+    }
+    KP.own[l] = 1;
+  }
+}
+
+// The segment table in one pass over every run list (k_kway_candidates +
+// k_kway_select): s / e / slot / per-segment RLE-operand values / covered-row
+// offsets, sized by their capacity `cap` (the candidate count) with the real
+// (segments, covered rows) left on the device in `dims` — no readback.
+// Returns false when the lists do not fit the kernel (the pairwise path then
+// builds the table).
 bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, const DMask* mask,
                    const std::vector<XPred>* preds, const std::vector<const DCol*>& rle_cols, int64_t total,
-                   GroupKey& K, DArr& s, DArr& e, DArr& slot, DArr& cst_all, DArr& off, int64_t& nseg,
-                   int64_t& ncov) {
+                   GroupKey& K, DArr& s, DArr& e, DArr& slot, DArr& cst_all, DArr& off, DArr& dims,
+                   int64_t& cap) {
   if (total <= 0 || total >= dev::KW_MAX_ROWS) return false;
+  auto host_timer = std::make_unique<KTimer>(ctx, "kw_host");  // the plan, up to the first launch
   if (!key_layout(ctx, keys, K)) return false;
   dev::KwPlan KP{};
   std::vector<const DCol*> of_list;  // the column behind each list (null: mask / domain)
@@ -1764,6 +1923,11 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
       P.kf[j] = ks[j].f;
     }
   }
+  {
+    std::vector<int> list_float(static_cast<size_t>(KP.nl), 0);
+    for (int l = 0; l < KP.nl; ++l) list_float[static_cast<size_t>(l)] = dt_float(KP.l[l].dt) ? 1 : 0;
+    kw_fold_conjuncts(KP, list_float);
+  }
   for (size_t j = 0; j < rle_cols.size(); ++j) {
     const int l = add(rle_cols[j]->s, rle_cols[j]->e, rle_cols[j]);
     if (l < 0) return false;
@@ -1787,55 +1951,41 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
   KP.start[0] = 0;
   for (int l = 0; l < KP.nl; ++l) KP.start[l + 1] = KP.start[l] + KP.l[l].n;
   const int64_t N = KP.start[KP.nl];
+  if (N + total >= dev::KW_MAX_ROWS) return false;  // the tile scan runs (counts | rows) as one 40-bit prefix
   const int ncst = static_cast<int>(rle_cols.size());
-  if (N == 0) {
-    s = alloc_arr(ctx, RQ_I64, 0);
-    e = alloc_arr(ctx, RQ_I64, 0);
-    slot = alloc_arr(ctx, RQ_I64, 0);
-    cst_all = alloc_arr(ctx, RQ_I64, 1);
-    off = alloc_arr(ctx, RQ_I64, 1);
-    nseg = ncov = 0;
-    return true;
-  }
-  DArr kept = alloc_arr(ctx, RQ_I64, N), cs = alloc_arr(ctx, RQ_I64, N), ce = alloc_arr(ctx, RQ_I64, N),
-       cslot = alloc_arr(ctx, RQ_I64, N), ccst = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst)),
-       dims = alloc_arr(ctx, RQ_I64, 2);
-  RQ_CUDA_CHECK(cudaMemsetAsync(kept.raw_mut(), 0, static_cast<size_t>(N) * 8, ctx->stream));
+  host_timer.reset();
+  dims = alloc_arr(ctx, RQ_I64, 2);
   RQ_CUDA_CHECK(cudaMemsetAsync(dims.raw_mut(), 0, 16, ctx->stream));
-  dev::k_kway_candidates<<<grid_cap(ctx, N), 256, 0, ctx->stream>>>(
-      KP, kept.as<int64_t>(), cs.as<int64_t>(), ce.as<int64_t>(), cslot.as<int64_t>(), ccst.as<uint64_t>(),
-      dims.as<unsigned long long>());
-  launched(ctx);
-  DArr exk;
-  scan_exclusive_i64(ctx, kept, exk);
+  // the table is sized by its capacity N (every candidate kept); the real
+  // (segments, covered rows) stay in `dims` on the device
   s = alloc_arr(ctx, RQ_I64, N);
   e = alloc_arr(ctx, RQ_I64, N);
   slot = alloc_arr(ctx, RQ_I64, N);
-  DArr cst_n = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst));
-  dev::k_kway_compact<<<grid_cap(ctx, N), 256, 0, ctx->stream>>>(N, ncst, kept.pos(), exk.pos(), cs.pos(), ce.pos(),
-                                                                 cslot.pos(), ccst.as<uint64_t>(), s.as<int64_t>(),
-                                                                 e.as<int64_t>(), slot.as<int64_t>(),
-                                                                 cst_n.as<uint64_t>());
+  off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N));
+  cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst));
+  cap = N;
+  if (N == 0) return true;
+  constexpr int B = 256, IT = dev::KW_TILE / 256;
+  const int64_t ntiles = (N + dev::KW_TILE - 1) / dev::KW_TILE;
+  // the per-tile (count, rows) aggregates, then the kept flags: one zeroing memset
+  const int64_t words = 2 * ntiles + (N + 7) / 8;
+  DArr zero = alloc_arr(ctx, RQ_I64, words), cs = alloc_arr(ctx, RQ_I64, N), ce = alloc_arr(ctx, RQ_I64, N),
+       cslot = alloc_arr(ctx, RQ_I64, N), ccst = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst));
+  RQ_CUDA_CHECK(cudaMemsetAsync(zero.raw_mut(), 0, static_cast<size_t>(words) * 8, ctx->stream));
+  auto* tagg = zero.as<unsigned long long>();
+  auto* kept = reinterpret_cast<uint8_t*>(tagg + 2 * ntiles);
+  dev::k_kway_candidates<<<grid_cap(ctx, N), 256, 0, ctx->stream>>>(
+      KP, kept, cs.as<int64_t>(), ce.as<int64_t>(), cslot.as<int64_t>(), ccst.as<uint64_t>(),
+      dims.as<unsigned long long>(), tagg, ntiles);
   launched(ctx);
-  const int64_t* h = ctx->readback(dims.raw(), 16);
-  nseg = h[0];
-  ncov = h[1];
-  s.n = e.n = slot.n = nseg;
-  // covered-row offsets of the kept segments (a scan over nseg, not N)
-  off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
-  if (nseg) {
-    DArr len = alloc_arr(ctx, RQ_I64, nseg + 1);
-    dev::k_xg_lengths<<<grid_cap(ctx, nseg + 1), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
-    launched(ctx);
-    scan_exclusive_i64(ctx, len, off);
-    off.n = nseg;
-  }
-  // the row kernels read operand j of segment k at cst[j * nseg + k]
-  cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * ncst));
-  if (ncst && nseg)
-    RQ_CUDA_CHECK(cudaMemcpy2DAsync(cst_all.raw_mut(), static_cast<size_t>(nseg) * 8, cst_n.raw(),
-                                    static_cast<size_t>(N) * 8, static_cast<size_t>(nseg) * 8, ncst,
-                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  DArr tv = zero;  // the aggregates (the buffer's head), then their exclusive scan
+  tv.n = 2 * ntiles;
+  DArr tpre;
+  scan_exclusive_i64(ctx, tv, tpre);
+  dev::k_kway_select<B, IT><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
+      N, ncst, kept, cs.pos(), ce.pos(), cslot.pos(), ccst.as<uint64_t>(), tpre.pos(), ntiles, s.as<int64_t>(),
+      e.as<int64_t>(), slot.as<int64_t>(), cst_all.as<uint64_t>(), off.as<int64_t>());
+  launched(ctx);
   return true;
 }
 
@@ -1843,6 +1993,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
               const std::vector<XExpr>& exprs, const std::vector<int>& fns, GroupAggOut& out,
               const GroupKey* preK, const std::vector<XPred>* preds) {
   if (exprs.size() > static_cast<size_t>(dev::XG_EXPRS) || keys.size() > 8) return false;
+  auto plan_timer = std::make_unique<KTimer>(ctx, "xg_plan");  // host-side planning (profiling only)
   const int64_t total = !keys.empty() ? keys[0]->total
                         : mask        ? mask->total
                                       : (exprs.empty() || exprs[0].terms.empty() ? -1 : exprs[0].terms[0].col->total);
@@ -1926,12 +2077,13 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   for (size_t j = 0; j < rle_cols.size(); ++j) P.cst_f[j] = dt_float(rle_cols[j]->v.dt) ? 1 : 0;
 
   // ---- segment table: keys ∩ mask ∩ WHERE ∩ RLE operands (align_many's joint shape) ----
+  plan_timer.reset();
   KTimer timer(ctx, "group_exprs");
   GroupKey K;
-  DArr s, e, slot, cst_all, off;
-  int64_t nseg = 0, ncov = 0;
-  const bool kway = !preK && kway_segments(ctx, keys, mask, preds, rle_cols, total, K, s, e, slot, cst_all, off, nseg,
-                                           ncov);
+  DArr s, e, slot, cst_all, off, dims;
+  int64_t nseg = 0, ncov = 0;  // host-known sizes (pairwise builder); the k-way one leaves them in dims
+  const bool kway = !preK && kway_segments(ctx, keys, mask, preds, rle_cols, total, K, s, e, slot, cst_all, off, dims,
+                                           nseg);
   if (!kway) {
     auto stage = std::make_unique<KTimer>(ctx, "xg_keys");  // per-stage profile tags (no-ops unless profiling)
     if (preK) {
@@ -2073,8 +2225,13 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   DArr tab = new_table(ctx, std::max<int64_t>(1, cells), 0);
   DArr cnt = new_table(ctx, G, 0);
   int* err = reinterpret_cast<int*>(ctx->tickets + 2);  // zero between launches (reset after the check)
-  dev::XgSegs S{s.pos(), e.pos(), off.pos(), slot.pos(), reinterpret_cast<const uint64_t*>(cst_all.raw()), nseg,
-                ncov, nullptr, 0};
+  // k-way: nseg is the table's capacity, the counts are read on the device
+  dev::XgSegs S{s.pos(), e.pos(), off.pos(),  slot.pos(), reinterpret_cast<const uint64_t*>(cst_all.raw()),
+                nseg,    ncov,    nullptr,    0,          kway ? dims.pos() : nullptr,
+                nseg};
+  // average covered segment length (the row kernel's prefetch choice): the
+  // k-way table's is estimated as rows per candidate
+  const int64_t avg_len = kway ? total / std::max<int64_t>(1, nseg) : ncov / std::max<int64_t>(1, nseg);
   auto* tabp = reinterpret_cast<unsigned long long*>(tab.raw_mut());
   auto* cntp = reinterpret_cast<unsigned long long*>(cnt.raw_mut());
   DArr dpart;
@@ -2086,16 +2243,16 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   bool any_rows = false;
   for (int i = 0; i < P.ne; ++i) any_rows = any_rows || P.e[i].rows;
   stage.reset();
-  if (any_rows && ncov > 0) {
+  if (any_rows && (kway ? nseg > 0 : ncov > 0)) {
     constexpr int B = 256;
     const int64_t warps = static_cast<int64_t>(ctx->sm_count) * 8 * (B / 32);
-    int64_t chunk = (ncov + warps - 1) / warps;
-    chunk = std::max<int64_t>(512, (chunk + 127) / 128 * 128);
+    // chunk 0: the kernel derives it from the device-side row count (same formula)
+    const int64_t chunk = kway ? 0 : dev::xg_chunk(ncov, warps);
     // f64 row sums: per-chunk partial tables + a fixed-order fold, so two runs
     // give bit-identical results (atomics only past the table budget)
     bool any_f = false;
     for (int i = 0; i < P.ne; ++i) any_f = any_f || (P.e[i].rows && P.e[i].acc_f);
-    const int64_t nchunks = (ncov + chunk - 1) / chunk;
+    const int64_t nchunks = kway ? warps : (ncov + chunk - 1) / chunk;  // k-way: the bound (zeros fold exactly)
     static const bool nodet = std::getenv("RQ_XG_NODET") != nullptr;  // A/B knob: atomic f64 flushes
     if (any_f && !nodet && nchunks * cells <= (int64_t{8} << 20)) {
       dpart = alloc_arr(ctx, RQ_F64, nchunks * cells);
@@ -2104,14 +2261,15 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       S.dcells = cells;
       dchunks = nchunks;
     }
-    const int64_t blocks = std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
-                                             (ncov / chunk + (B / 32)) / (B / 32) + 1);
+    const int64_t blocks = kway ? static_cast<int64_t>(ctx->sm_count) * 8
+                                : std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
+                                                    (ncov / chunk + (B / 32)) / (B / 32) + 1);
     constexpr size_t smem = dev::xg_rows_smem<B>();
     kernel_occupancy(ctx, dev::k_xg_rows<B>, B, smem);  // shared-memory opt-in on this device
     KTimer rows_timer(ctx, "xg_rows");
     const char* nojit = std::getenv("RQ_NO_JIT");
     if ((nojit && nojit[0] == '1') ||
-        !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks)))
+        !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks), avg_len))
       dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
     launched(ctx);
     if (S.dpart) {
@@ -2127,8 +2285,8 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     if (c.p2.n == 0 || nseg == 0) continue;
     const dev::XgExpr& X = P.e[pe.first];
     dev::k_xg_outliers_seg<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(
-        P.col[X.t[0].src], c.p2.pos(), c.v2.raw(), c.v2.dt, c.p2.n, s.pos(), e.pos(), slot.pos(), nseg, P.ne,
-        pe.first, X.acc_f, tabp);
+        P.col[X.t[0].src], c.p2.pos(), c.v2.raw(), c.v2.dt, c.p2.n, s.pos(), e.pos(), slot.pos(), nseg, S.dims,
+        P.ne, pe.first, X.acc_f, tabp);
     launched(ctx);
   }
   bool int_div = false;  // only integer division can raise (align.cpp:297-299)

@@ -48,15 +48,27 @@ struct XgSegs {
   const int64_t* e;
   const int64_t* off;   // exclusive prefix of segment lengths (covered rows)
   const int64_t* slot;
-  const uint64_t* cst;  // [XG_CONSTS][nseg] RLE operand values (i64 / f64 bits)
-  int64_t n;
-  int64_t ncov;
+  const uint64_t* cst;  // [XG_CONSTS][cstride] RLE operand values (i64 / f64 bits)
+  int64_t n;            // segments, or the table's capacity when `dims` is set
+  int64_t ncov;         // covered rows (unused when `dims` is set)
   // deterministic f64 sums: each chunk (a warp's covered-row range) writes its
   // per-cell partial to dpart[chunk * dcells + cell] (no atomics); a fixed-
   // order fold adds them up. Null: atomic adds (order-dependent last bits).
   double* dpart;
   int64_t dcells;
+  // device-resident (segments, covered rows) of a table built without a host
+  // readback (the k-way builder); null: n / ncov above
+  const int64_t* dims;
+  int64_t cstride;  // operand j of segment k at cst[j * cstride + k]
 };
+
+// rows per warp chunk of the row kernels: at least 512, a multiple of 128,
+// and at most `nwarps` chunks (the deterministic fold's partial tables)
+__host__ __device__ inline int64_t xg_chunk(int64_t ncov, int64_t nwarps) {
+  int64_t c = (ncov + nwarps - 1) / nwarps;
+  c = (c + 127) / 128 * 128;
+  return c < 512 ? 512 : c;
+}
 
 }  // namespace dev
 }  // namespace rqb

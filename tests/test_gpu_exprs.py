@@ -209,6 +209,42 @@ def test_where_pushdown_vs_reference(rq, ref, inst, row_kernel):
             assert_scalar(float(got) if isinstance(want, float) else int(got), want, f"expr {i}")
 
 
+_FOLD_CASES = [
+    # conjuncts on one integer run column, folded to interval ∩ value set
+    [("p1", "in", [1, 7.0, 7.5, 12, 29]), ("p1", "in", [7, 12, 13]), ("p2", ">", -2.5), ("p2", "<=", 3.9)],
+    [("p1", "==", 7.0), ("p2", "!=", 0), ("p2", "!=", 99)],
+    [("p1", "==", 7.5)],                                   # never equal: empty result
+    [("p1", ">=", 20), ("p1", "<", 10)],                    # contradictory interval
+    [("p1", "<", 1e300), ("p2", ">", -1e300)],              # out-of-range literals: interpreted
+    [("p1", "!=", 3), ("p1", "!=", 4), ("p1", "in", [3, 4, 5, 6])],
+    [("pf", "<", 5.0), ("p1", ">=", 10)],                   # float run values: interpreted
+    [("p2", ">=", -9223372036854775808), ("p1", "<=", 9223372036854775807)],
+]
+
+
+@pytest.mark.parametrize("case", range(len(_FOLD_CASES)))
+def test_where_folded_conjuncts_vs_reference(rq, ref, case):
+    """The segment table folds a list's integer conjuncts into one interval
+    and value set: float literals (integral or not), NE exclusions, IN lists
+    intersected, empty and unbounded ranges == compare_scalar's masks."""
+    rng = np.random.default_rng(1200 + case)
+    X = rq.X
+    n = 200_000
+    cols = {"p1": _rle(rng, n, 80, 0, 30), "p2": _rle(rng, n, 900, -5, 5)}
+    pf = _rle(rng, n, 500, 0, 10)
+    cols["pf"] = H.RleColumn(pf.v.astype(np.float64) + 0.25, pf.s, pf.e, n)
+    k1 = _rle(rng, n, 5_000, 0, 5)
+    v = H.PlainColumn(rng.integers(-100, 101, n).astype(np.int64))
+    where = [(cols[c], op, k) for c, op, k in _FOLD_CASES[case]]
+    exprs, fns = [X.col(v), X.count()], ["sum", "count"]
+    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [k1], exprs, fns, where=where)
+    assert fused
+    wk, wv, wng = _chain(ref, _ref_where_mask(ref, where), [k1], exprs, fns)
+    assert ng == wng
+    for g, w in zip(ks + vs, wk + wv):
+        assert_array(g, w)
+
+
 def test_where_on_plain_column_falls_back_to_mask(rq, ref):
     """A conjunct on a plain column cannot be evaluated per run segment: the
     call builds the runner's mask and still fuses the aggregation."""
