@@ -93,25 +93,28 @@ class ClockSampler:
 
     def _sample(self):
         nv = self.nv
-        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        clk = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-        for bit, name in self.REASONS.items():
-            if r & bit:
-                self.reasons.add(name)
+        self.samples.append((time.perf_counter(), clk, r))
 
     def _run(self):
         # every 10 ms: NVML queries take driver locks that delay the launches
         # and syncs of host-paced steps (Q6 / C5: 27 launches per 0.4 ms step)
-        while not self._stop.is_set():
+        while not self._stop.wait(0.01):
             self._sample()
-            self._stop.wait(0.01)
 
+    # The thread is started before the warm-up steps (its creation and first
+    # NVML calls stay out of short timed regions); the summary keeps the
+    # samples from 10 ms before the region to 10 ms after it.
     def __enter__(self):
         if self.ok:
             self._sample()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
+
+    def mark(self, start: bool):
+        setattr(self, "t0" if start else "t1", time.perf_counter())
 
     def __exit__(self, *a):
         if self.ok:
@@ -122,8 +125,11 @@ class ClockSampler:
     def summary(self):
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml-unavailable"]}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": float(self.max),
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        t0, t1 = getattr(self, "t0", -1e30), getattr(self, "t1", 1e30)
+        win = [x for x in self.samples if t0 - 0.01 <= x[0] <= t1 + 0.01] or self.samples
+        reasons = sorted({name for _, _, r in win for bit, name in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(statistics.median(c for _, c, _ in win)), "sm_max_mhz": float(self.max),
+                "reasons": reasons, "samples": len(win)}
 
 
 _PINNED = []  # keeps pinned host tensors alive
@@ -813,23 +819,31 @@ def main():
             dist.barrier()
 
     def timed(fn, steps, profile=False):
-        for _ in range(args.warmup):
-            fn()
-        barrier()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local)
         buf = (runq.C.c_char * 65536)()
         if profile:
+            # only the dominant kernel's region is timed live (two events per
+            # step): per-scope events would add their own cost to small queries.
+            # On from the warm-up on: the warm-up calls then build the same
+            # plan (and CUDA graph) the timed calls run.
+            runq._L.rq_ctx_profile_only(ctx.handle, profile.encode())
             runq._L.rq_ctx_set_profiling(ctx.handle, 1)
-            runq._L.rq_ctx_profile_report(ctx.handle, 1, buf, 65536)  # reset
-        l0 = ctx.launches
-        sampler = ClockSampler(local)
         with sampler:
+            for _ in range(args.warmup):
+                fn()
+            barrier()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            if profile:
+                runq._L.rq_ctx_profile_report(ctx.handle, 1, buf, 65536)  # reset: timed steps only
+            l0 = ctx.launches
+            sampler.mark(True)
             ev0.record(stream)
             for _ in range(steps):
                 fn()
             ev1.record(stream)
             ev1.synchronize()
+            sampler.mark(False)
         barrier()
         launches = ctx.launches - l0
         report = None
@@ -845,7 +859,8 @@ def main():
         return ms, launches, report, sampler.summary()
 
     # device-resident throughput (value) with live per-kernel event timing
-    ms, launches, report, clocks = timed(lambda: w.query(runq, dev, args.path, comm), args.steps, profile=True)
+    ms, launches, report, clocks = timed(lambda: w.query(runq, dev, args.path, comm), args.steps,
+                                         profile=w.tag or False)
     value = total / (ms / 1000.0)
 
     chain_ms = None

@@ -156,6 +156,8 @@ int64_t rq_ctx_launches(rq_ctx_t ctx);
 /* Per-kernel CUDA-event timing: when enabled, each tagged kernel launch is
  * bracketed by events on the context stream (SURVEY.md §5 tracing). */
 int rq_ctx_set_profiling(rq_ctx_t ctx, int32_t enable);
+/* Limit the profile to the comma-separated tags (NULL or "": every tag). */
+int rq_ctx_profile_only(rq_ctx_t ctx, const char* tags);
 /* JSON {"tag": {"ms": total, "count": launches}, ...} into buf (syncs). */
 int rq_ctx_profile_report(rq_ctx_t ctx, int32_t reset, char* buf, int64_t cap);
 

@@ -554,7 +554,46 @@ static int group_aggregate_exprs_api(rq_ctx_t c, const rq_pred* where, int32_t n
           },
           same_expr);
     } else {
-      r = group_aggregate_exprs(ctx, m, k, xs, f, &was_fused, pp);
+      // the plan's CUDA-graph key: handle ids, operators, literal bits, functions
+      std::string key = "gae";
+      auto add = [&](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+      auto add_s = [&](const rq_scalar& x) {
+        add(&x.is_float, sizeof x.is_float);
+        add(&x.i, sizeof x.i);
+        add(&x.f, sizeof x.f);
+      };
+      const uint64_t mu = mask ? mask->uid : 0;
+      add(&mu, 8);
+      for (int i = 0; i < n_keys; ++i) add(&keys[i]->uid, 8);
+      key += '|';
+      for (int i = 0; i < n_exprs; ++i) {
+        const rq_expr& x = exprs[i];
+        add(&x.n_terms, sizeof x.n_terms);
+        for (int t = 0; t < x.n_terms; ++t) {
+          add(&x.terms[t].col->uid, 8);
+          add(&x.terms[t].op, sizeof x.terms[t].op);
+          add(&x.terms[t].reversed, sizeof x.terms[t].reversed);
+          add_s(x.terms[t].k);
+          if (t > 0) add(&x.ops[t - 1], sizeof x.ops[t - 1]);
+        }
+        add(&fns[i], sizeof fns[i]);
+      }
+      key += '|';
+      for (int i = 0; i < n_where; ++i) {
+        add(&where[i].col->uid, 8);
+        add(&where[i].op, sizeof where[i].op);
+        add(&where[i].n_in, sizeof where[i].n_in);
+        add_s(where[i].k);
+        for (int j = 0; j < where[i].n_in; ++j) add_s(where[i].in_list[j]);
+      }
+      ctx->graph_key = std::move(key);
+      try {
+        r = group_aggregate_exprs(ctx, m, k, xs, f, &was_fused, pp);
+      } catch (...) {
+        ctx->graph_key.clear();
+        throw;
+      }
+      ctx->graph_key.clear();
     }
     if (fused) *fused = was_fused ? 1 : 0;
     if (n_groups) *n_groups = r.n_groups;

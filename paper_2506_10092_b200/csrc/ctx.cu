@@ -77,6 +77,7 @@ void Ctx::collect_profile() {
 Ctx::~Ctx() {
   cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  graphs.clear();  // their blocks go back through free() while the cache is alive
   for (auto& kv : block_cache)
     for (void* p : kv.second) cudaFree(p);
   for (auto& p : pending) {
@@ -123,6 +124,14 @@ void* Ctx::alloc(size_t bytes, size_t* cap) {
     }
   }
   void* p = nullptr;
+  if (capturing) {  // no allocation node in the graph: a plain allocation, kept by the graph
+    if (cudaMalloc(&p, c) != cudaSuccess) {
+      cudaGetLastError();
+      capture_broken = true;
+      throw RqError(RQ_RESOURCE, "device allocation during graph capture failed");
+    }
+    return p;
+  }
   cudaError_t err = cudaMallocAsync(&p, c, stream);
   if (err != cudaSuccess) {  // give the cached blocks back and retry once
     cudaGetLastError();
@@ -139,6 +148,10 @@ void* Ctx::alloc(size_t bytes, size_t* cap) {
 
 void Ctx::free(void* p, size_t cap) {
   if (!p) return;
+  if (capturing) {  // a captured kernel may still use it on every replay
+    capture_owned.push_back({p, cap});
+    return;
+  }
   if (cap && cap <= kCacheMaxBlock && cached_bytes + cap <= kCacheMaxBytes) {
     block_cache[cap].push_back(p);
     cached_bytes += cap;
@@ -159,6 +172,10 @@ void Ctx::release_cache() {
 // Stream synchronisation; under profiling its host wall time is recorded as
 // the pseudo-tag "host_sync_wait" (time the host spent blocked on the GPU).
 void Ctx::wait_stream() {
+  if (capturing) {  // a plan that syncs cannot be captured: the caller runs it uncaptured
+    capture_broken = true;
+    throw RqError(RQ_CUDA, "stream sync during graph capture");
+  }
   if (!profiling) {
     RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
     return;
@@ -199,7 +216,45 @@ uint32_t Ctx::next_epoch(int64_t tiles) {
   return epoch;
 }
 
+unsigned long long* Ctx::lookback_status(int64_t tiles, uint32_t* epoch_out) {
+  if (!capturing) {
+    *epoch_out = next_epoch(tiles);
+    return tile_status;
+  }
+  const size_t bytes = static_cast<size_t>(tiles + 1) * 8;
+  size_t cap = 0;
+  void* p = alloc(bytes, &cap);
+  capture_owned.push_back({p, cap});
+  RQ_CUDA_CHECK(cudaMemsetAsync(p, 0, bytes, stream));
+  *epoch_out = 1;
+  return static_cast<unsigned long long*>(p);
+}
+
+void Ctx::capture_cut(const char* tag, int kind) {
+  cudaGraph_t g = nullptr;
+  if (cudaStreamEndCapture(stream, &g) != cudaSuccess) {
+    cudaGetLastError();
+    capture_broken = true;
+  }
+  capture_steps.push_back({g, "", 0});
+  capture_steps.push_back({nullptr, tag, kind});
+  if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    capture_broken = true;
+  }
+}
+
+void Ctx::drop_graphs() {
+  if (graphs.empty()) return;
+  RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
+  graphs.clear();
+}
+
 void* Ctx::get_scratch(size_t bytes) {
+  if (capturing) {
+    capture_broken = true;
+    throw RqError(RQ_CUDA, "scratch resize during graph capture");
+  }
   if (bytes > scratch_bytes) {
     if (scratch) {
       RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
@@ -341,6 +396,24 @@ int rq_ctx_set_profiling(rq_ctx_t c, int32_t enable) {
     auto ctx = get_ctx(c);
     ctx->collect_profile();
     ctx->profiling = enable != 0;
+  });
+}
+
+int rq_ctx_profile_only(rq_ctx_t c, const char* tags) {
+  return api_guard([&] {
+    auto ctx = get_ctx(c);
+    ctx->collect_profile();
+    ctx->profile_only.clear();
+    std::string cur;
+    for (const char* q = tags ? tags : ""; ; ++q) {
+      if (*q == ',' || *q == 0) {
+        if (!cur.empty()) ctx->profile_only.push_back(cur);
+        cur.clear();
+        if (*q == 0) break;
+      } else {
+        cur += *q;
+      }
+    }
   });
 }
 

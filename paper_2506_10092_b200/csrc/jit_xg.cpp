@@ -71,7 +71,7 @@ const char* kPrelude = R"(
 typedef long long i64;
 typedef unsigned long long u64;
 struct XgSegs { const i64* s; const i64* e; const i64* off; const i64* slot; const u64* cst; i64 n; i64 ncov;
-                double* dpart; i64 dcells; const i64* dims; i64 cstride; };
+                double* dpart; i64 dcells; const i64* dims; i64 cstride; const i64* cstart; };
 struct XgCol { const void* v; i64 center; };
 struct XgK { i64 i[24]; double f[24]; };
 __device__ __forceinline__ i64 ldg64(const i64* p, i64 i) { return __ldg(p + i); }
@@ -207,6 +207,15 @@ int prefetch_distance() {
   return pf;
 }
 
+// software-pipelined segment bounds in the row loop (RQ_JIT_PIPE=0: off, A/B)
+bool pipeline_segments() {
+  static const bool on = [] {
+    const char* e = std::getenv("RQ_JIT_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // the source of a plan's kernel; literal slots are appended to ki / kf
 std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf, int pf) {
   std::ostringstream o;
@@ -233,11 +242,21 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
        " if (chunk_ < 512) chunk_ = 512; }\n";
   o << "  for (i64 c0_ = warp * chunk_; c0_ < ncov_; c0_ += nwarps * chunk_) {\n"
        "    const i64 c1_ = min(c0_ + chunk_, ncov_);\n"
-       "    i64 k = warp_lb(S.off, nseg_, c0_ + 1) - 1;\n"
-       "    i64 c = c0_;\n"
-       "    while (c < c1_) {\n"
-       "      const i64 off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k);\n"
-       "      const i64 slot = ldg64(S.slot, k);\n";
+       "    i64 k = S.cstart ? ldg64(S.cstart, c0_ / chunk_) : warp_lb(S.off, nseg_, c0_ + 1) - 1;\n"
+       "    i64 c = c0_;\n";
+  // short segments (no L2 prefetch): the next segment's bounds are loaded
+  // while this one's rows stream, so a segment costs one round trip, not two
+  const bool pipe = pf == 0 && pipeline_segments();
+  if (pipe)
+    o << "    i64 off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k), slot = ldg64(S.slot, k);\n"
+         "    while (c < c1_) {\n"
+         "      const bool more_ = k + 1 < nseg_;\n"
+         "      const i64 n_off = more_ ? ldg64(S.off, k + 1) : 0, n_s = more_ ? ldg64(S.s, k + 1) : 0;\n"
+         "      const i64 n_e = more_ ? ldg64(S.e, k + 1) : 0, n_slot = more_ ? ldg64(S.slot, k + 1) : -1;\n";
+  else
+    o << "    while (c < c1_) {\n"
+         "      const i64 off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k);\n"
+         "      const i64 slot = ldg64(S.slot, k);\n";
   for (int j = 0; j < P.ncst; ++j) {
     if (P.cst_f[j])
       o << "      const double k" << j << " = __longlong_as_double((long long)__ldg(S.cst + " << j << " * S.cstride + k));\n";
@@ -326,9 +345,12 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
         << (X.acc_f ? "(double)" : "(u64)") << "v" << e << "_" << u << ";\n";
   }
   o << "        }\n      }\n";
-  o << "      c = min(c1_, off + (e - s + 1));\n"
-       "      const i64 next_slot = (c < c1_ && k + 1 < nseg_) ? ldg64(S.slot, k + 1) : -1;\n"
-       "      if (next_slot != slot) {\n";
+  o << "      c = min(c1_, off + (e - s + 1));\n";
+  if (pipe)
+    o << "      const i64 next_slot = (c < c1_ && more_) ? n_slot : -1;\n";
+  else
+    o << "      const i64 next_slot = (c < c1_ && k + 1 < nseg_) ? ldg64(S.slot, k + 1) : -1;\n";
+  o << "      if (next_slot != slot) {\n";
   for (int e = 0; e < P.ne; ++e) {
     const dev::XgExpr& X = P.e[e];
     if (!X.rows) continue;
@@ -341,7 +363,8 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
       o << "        { const u64 t = wsum_u(a" << e << "); if (lane == 0 && t != 0ull) atomicAdd(tab + slot * NE + " << e
         << ", t); a" << e << " = 0ull; }\n";
   }
-  o << "      }\n      ++k;\n    }\n  }\n";
+  if (pipe) o << "      }\n      ++k;\n      off = n_off; s = n_s; e = n_e; slot = n_slot;\n    }\n  }\n";
+  else o << "      }\n      ++k;\n    }\n  }\n";
   o << "  if (lerr) atomicOr(err, 1);\n";
   o << "  if (in_smem) {\n    __syncthreads();\n    for (i64 i = threadIdx.x; i < cells; i += 256) {\n"
        "      const u64 v = stab[i];\n      if (!v) continue;\n      switch ((int)(i % NE)) {\n";
@@ -389,6 +412,10 @@ cudaKernel_t compile(const std::string& src) {
     std::fprintf(stderr, "runq_b200: K12 kernel compilation failed (interpreted kernel used):\n%s\n", log.c_str());
     N.destroy(&prog);
     C.failed[src] = true;
+    // RQ_JIT_STRICT=1 (the GPU test suite): a generator bug fails loudly
+    // instead of silently running the interpreted kernel
+    const char* strict = std::getenv("RQ_JIT_STRICT");
+    if (strict && strict[0] == '1') throw RqError(RQ_CUDA, "K12 kernel compilation failed:\n" + log);
     return nullptr;
   }
   size_t n = 0;
@@ -434,6 +461,7 @@ std::string plan_signature(const dev::XgPlan& P, int minb, int pf) {
   auto put = [&](int64_t v) { sig += std::to_string(v); sig += ','; };
   put(minb);
   put(pf);
+  put(pipeline_segments() ? 1 : 0);
   put(P.nc);
   for (int c = 0; c < P.nc; ++c) {
     put(P.col[c].dt);

@@ -122,6 +122,83 @@ __global__ void k_expand(const int64_t* __restrict__ off, int64_t nseg, int64_t 
   }
 }
 
+// Large groups (many elements per group, few groups): each warp folds a
+// contiguous range of the input in order into its own row of a partial table
+// (lanes of one group combined in lane order, then one plain add by the
+// leader); integer folds go straight to the output with atomics (exact in
+// any order). Row init: 0 / +inf / -inf for sum / min / max.
+__global__ void k_group_fold_warp(const void* __restrict__ v, int dt, const int64_t* __restrict__ idx, int64_t n,
+                                  int64_t G, int op, int flt, int64_t per_warp, double* __restrict__ fpart,
+                                  unsigned long long* __restrict__ iout) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  double* row = flt ? fpart + w * G : nullptr;
+  if (flt) {
+    const double init = op == 1 ? INFINITY : op == 2 ? -INFINITY : 0.0;
+    for (int64_t g = lane; g < G; g += 32) row[g] = init;
+    __syncwarp();
+  }
+  const int64_t a = w * per_warp, b = min(n, a + per_warp);
+  for (int64_t base = a; base < b; base += 32) {
+    const int64_t j = base + lane;
+    const bool ok = j < b;
+    const int64_t g = ok ? idx[j] : -1;
+    const unsigned same = __match_any_sync(FULL, static_cast<unsigned long long>(g));
+    const int leader = __ffs(same) - 1;
+    if (flt) {
+      const double x = ok ? ld_f64(v, dt, j) : 0.0;
+      double acc = op == 1 ? INFINITY : op == 2 ? -INFINITY : 0.0;
+      for (unsigned m = same; m; m &= m - 1) {
+        const double y = __shfl_sync(same, x, __ffs(m) - 1);
+        if (op == 0) acc += y;
+        else if (op == 1) acc = (y < acc) ? y : acc;
+        else acc = (acc < y) ? y : acc;
+      }
+      if (ok && lane == leader) {
+        if (op == 0) row[g] += acc;
+        else if (op == 1) row[g] = (acc < row[g]) ? acc : row[g];
+        else row[g] = (row[g] < acc) ? acc : row[g];
+      }
+      __syncwarp();
+    } else {
+      const int64_t x = !ok ? 0 : op == 3 ? 1 : ld_i64(v, dt, j);
+      if (op == 0 || op == 3) {
+        uint64_t acc = 0;
+        for (unsigned m = same; m; m &= m - 1) acc += static_cast<uint64_t>(__shfl_sync(same, x, __ffs(m) - 1));
+        if (ok && lane == leader) atomicAdd(iout + g, static_cast<unsigned long long>(acc));
+      } else if (ok) {
+        if (op == 1) atomicMin(reinterpret_cast<long long*>(iout) + g, static_cast<long long>(x));
+        else atomicMax(reinterpret_cast<long long*>(iout) + g, static_cast<long long>(x));
+      }
+    }
+  }
+}
+
+// the warps' rows folded per group in warp order (fixed: the same bits on every run)
+__global__ void k_group_fold_rows(const double* __restrict__ fpart, int64_t nw, int64_t G, int op,
+                                  double* __restrict__ out) {
+  __shared__ double red[256];
+  const int64_t g = blockIdx.x;
+  const double init = op == 1 ? INFINITY : op == 2 ? -INFINITY : 0.0;
+  double acc = init;
+  for (int64_t q = threadIdx.x; q < nw; q += 256) {
+    const double y = fpart[q * G + g];
+    if (op == 0) acc += y;
+    else if (op == 1) acc = (y < acc) ? y : acc;
+    else acc = (acc < y) ? y : acc;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) {
+      const double y = red[threadIdx.x + k], x = red[threadIdx.x];
+      red[threadIdx.x] = op == 0 ? x + y : op == 1 ? ((y < x) ? y : x) : ((x < y) ? y : x);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[g] = red[0];
+}
+
 // one thread per group: fold values[perm[k]] for k in [start[g], start[g+1])
 // in input order (scatter_loop, kernels.cpp:67-80)
 __global__ void k_scatter_seq(const void* __restrict__ v, int dt, const int64_t* __restrict__ perm,
@@ -359,6 +436,34 @@ DArr scatter_reduce(const CtxPtr& ctx, const DArr& values, const DArr& index, in
   const bool flt = dt_float(values.dt) && op != 3;
   DArr out = alloc_arr(ctx, flt ? RQ_F64 : RQ_I64, n_groups);
   if (n_groups == 0) return out;
+  // few large groups: warp-range folds (one thread per group would walk
+  // ~n / G elements serially); deterministic, within rounding of the
+  // input-order loop for f64 sums
+  const int64_t nw = static_cast<int64_t>(ctx->sm_count) * 8 * 8;
+  if (index.n >= (int64_t{1} << 20) && index.n / n_groups >= 4096 && nw * n_groups <= (int64_t{8} << 20)) {
+    const int64_t per = ((index.n + nw - 1) / nw + 31) / 32 * 32;
+    DArr fpart;
+    if (flt) {
+      fpart = alloc_arr(ctx, RQ_F64, nw * n_groups);
+    } else if (op == 0 || op == 3) {
+      RQ_CUDA_CHECK(cudaMemsetAsync(out.raw_mut(), 0, static_cast<size_t>(n_groups) * 8, ctx->stream));
+    } else {  // min / max identities (rare: a host copy and one sync)
+      std::vector<int64_t> h(static_cast<size_t>(n_groups), op == 1 ? INT64_MAX : INT64_MIN);
+      RQ_CUDA_CHECK(cudaMemcpyAsync(out.raw_mut(), h.data(), static_cast<size_t>(n_groups) * 8,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+      RQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // h leaves scope
+    }
+    dev::k_group_fold_warp<<<static_cast<unsigned>(nw / 8), 256, 0, ctx->stream>>>(
+        values.raw(), values.dt, index.pos(), index.n, n_groups, op, flt ? 1 : 0, per,
+        flt ? fpart.as<double>() : nullptr, flt ? nullptr : out.as<unsigned long long>());
+    launched(ctx);
+    if (flt) {
+      dev::k_group_fold_rows<<<static_cast<unsigned>(n_groups), 256, 0, ctx->stream>>>(fpart.as<double>(), nw,
+                                                                                      n_groups, op, out.as<double>());
+      launched(ctx);
+    }
+    return out;
+  }
   // stable sort of the element indices by group: each group's values in input order
   DArr keys = copy_prefix(ctx, index, index.n);
   DArr perm = iota(ctx, index.n);

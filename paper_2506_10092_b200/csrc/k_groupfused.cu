@@ -126,13 +126,22 @@ struct GTable {
   unsigned long long* g;  // global table (G slots)
   int64_t G;
   int64_t kmin;
+  // f64 sums (G_SUM_F / G_SQ): each warp adds into its own row part[warp * G]
+  // in its fixed item order, the rows are folded in warp order afterwards
+  // (k_gk_pfold) — the same bits on every run. Null: atomics.
+  double* part = nullptr;
 };
+
+template <int KIND>
+__device__ __forceinline__ constexpr bool g_fsum() {
+  return KIND == G_SUM_F || KIND == G_SQ;
+}
 
 constexpr int kSmemSlots = 4096;
 
 template <int KIND>
 __device__ __forceinline__ unsigned long long* g_table_begin(unsigned long long* smem, const GTable& t) {
-  if (t.G > kSmemSlots) return t.g;
+  if (t.G > kSmemSlots || (g_fsum<KIND>() && t.part)) return t.g;
   for (int64_t s = threadIdx.x; s < t.G; s += blockDim.x) smem[s] = g_identity<KIND>();
   __syncthreads();
   return smem;
@@ -140,7 +149,7 @@ __device__ __forceinline__ unsigned long long* g_table_begin(unsigned long long*
 
 template <int KIND>
 __device__ __forceinline__ void g_table_end(unsigned long long* smem, const GTable& t) {
-  if (t.G > kSmemSlots) return;
+  if (t.G > kSmemSlots || (g_fsum<KIND>() && t.part)) return;
   __syncthreads();
   using T = typename GTraits<KIND>::T;
   const unsigned long long idn = g_identity<KIND>();
@@ -196,6 +205,22 @@ __global__ void __launch_bounds__(BLOCK)
   T acc = g_zero<KIND>();
   int64_t cur = -1;  // current slot
   double mu = 0.0;
+  // deterministic f64 mode: this thread's flushes, in walk order (at most one
+  // per merge item plus the last), combined by the warp in lane order below
+  constexpr int NREC = g_fsum<KIND>() ? ITEMS + 1 : 1;
+  int64_t rslot[NREC];
+  T racc[NREC];
+  int nrec = 0;
+  const bool det = g_fsum<KIND>() && t.part;
+  auto flush = [&](int64_t sl, T a) {
+    if (det) {
+      rslot[nrec < NREC ? nrec : NREC - 1] = sl;
+      racc[nrec < NREC ? nrec : NREC - 1] = a;
+      ++nrec;
+    } else {
+      g_atomic<KIND>(tab, sl, a);
+    }
+  };
   tl.walk(sk, [&](int64_t i, int64_t j, bool takeA, int64_t key) {
     if (i >= m.na || j >= m.nb) return;
     // key run i starts after key run i-1's end; data run j starts at ds[j]
@@ -205,14 +230,39 @@ __global__ void __launch_bounds__(BLOCK)
     if (len <= 0) return;
     const int64_t slot = ld_i64(kv, kdt, i) - t.kmin;
     if (slot != cur) {
-      if (cur >= 0) g_atomic<KIND>(tab, cur, acc);
+      if (cur >= 0) flush(cur, acc);
       acc = g_zero<KIND>();
       cur = slot;
       if (KIND == G_SQ) mu = mean[slot];
     }
     g_fold<KIND>(acc, ld_as<T>(dv, ddt, j), len, mu);
   });
-  if (cur >= 0) g_atomic<KIND>(tab, cur, acc);
+  if (cur >= 0) flush(cur, acc);
+  if (det) {
+    // lane 0 walks the warp's records in (lane, record) order, adding runs of
+    // one slot in a register and each finished run into the warp's row
+    const int lane = threadIdx.x & 31;
+    double* row = t.part + ((static_cast<int64_t>(blockIdx.x) * BLOCK + threadIdx.x) >> 5) * t.G;
+    int64_t cs = -1;
+    double ca = 0.0;
+    for (int l = 0; l < 32; ++l) {
+      const int nl = __shfl_sync(FULL, nrec, l);
+#pragma unroll
+      for (int r = 0; r < NREC; ++r) {
+        const int64_t sl = __shfl_sync(FULL, rslot[r], l);
+        const double a = __shfl_sync(FULL, static_cast<double>(racc[r]), l);
+        if (lane == 0 && r < nl) {
+          if (sl != cs) {
+            if (cs >= 0) row[cs] += ca;
+            cs = sl;
+            ca = 0.0;
+          }
+          ca += a;
+        }
+      }
+    }
+    if (lane == 0 && cs >= 0) row[cs] += ca;
+  }
   g_table_end<KIND>(smem, t);
 }
 
@@ -351,7 +401,10 @@ __global__ void __launch_bounds__(256)
         T r = acc;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r = g_combine<KIND>(r, __shfl_xor_sync(FULL, r, o));
-        if (lane == 0 && slot >= 0) g_atomic<KIND>(tab, slot, r);
+        if (lane == 0 && slot >= 0) {
+          if (g_fsum<KIND>() && t.part) t.part[warp * t.G + slot] += static_cast<double>(r);
+          else g_atomic<KIND>(tab, slot, r);
+        }
         acc = g_zero<KIND>();
         ++kr;
         kstart = kr < nk ? ldg64(kst, kr) : INT64_MAX;
@@ -363,9 +416,28 @@ __global__ void __launch_bounds__(256)
     T r = acc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r = g_combine<KIND>(r, __shfl_xor_sync(FULL, r, o));
-    if (lane == 0 && slot >= 0) g_atomic<KIND>(tab, slot, r);
+    if (lane == 0 && slot >= 0) {
+      if (g_fsum<KIND>() && t.part) t.part[warp * t.G + slot] += static_cast<double>(r);
+      else g_atomic<KIND>(tab, slot, r);
+    }
   }
   g_table_end<KIND>(smem, t);
+}
+
+// the warps' rows of a deterministic f64 table folded per slot in warp order
+__global__ void k_gk_pfold(const double* __restrict__ part, int64_t rows, int64_t G,
+                           unsigned long long* __restrict__ tab) {
+  __shared__ double red[256];
+  const int64_t g = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t q = threadIdx.x; q < rows; q += 256) acc += part[q * G + g];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tab[g] = static_cast<unsigned long long>(__double_as_longlong(red[0]));
 }
 
 __global__ void k_gk_init(unsigned long long* __restrict__ t, int64_t G, unsigned long long v) {
@@ -641,7 +713,25 @@ DArr table_for(const CtxPtr& ctx, const GroupKey& K, const DCol& d, const double
   if (KIND == dev::G_MAX_F) init = 0xfff0000000000000ull;
   DArr tab = new_table(ctx, K.G, init);
   dev::GTable t{reinterpret_cast<unsigned long long*>(tab.raw_mut()), K.G, 0};
+  DArr part;
+  int64_t rows = 0;
+  if (KIND == dev::G_SUM_F || KIND == dev::G_SQ) {
+    // deterministic f64: one row per warp of the widest launch fold_column makes
+    rows = static_cast<int64_t>(ctx->sm_count) * 8 * 8;  // run_items' grid cap
+    if (d.enc == RQ_ENC_RLE || d.enc == RQ_ENC_RLE_INDEX)
+      rows = std::max<int64_t>(rows, (K.e.n + d.e.n + 2047) / 2048 * 8);  // run_rle: a warp per 256 merge items
+    if (rows * K.G <= (int64_t{8} << 20)) {
+      part = alloc_arr(ctx, RQ_F64, rows * K.G);
+      RQ_CUDA_CHECK(cudaMemsetAsync(part.raw_mut(), 0, static_cast<size_t>(rows * K.G) * 8, ctx->stream));
+      t.part = part.as<double>();
+    }
+  }
   fold_column<KIND>(ctx, K, d, t, mean);
+  if (t.part && K.G) {
+    dev::k_gk_pfold<<<static_cast<unsigned>(K.G), 256, 0, ctx->stream>>>(t.part, rows, K.G,
+                                                                        reinterpret_cast<unsigned long long*>(tab.raw_mut()));
+    launched(ctx);
+  }
   return tab;
 }
 
@@ -776,6 +866,11 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
       }
     }
   }
+  auto to_rows = [&](size_t i, size_t taken) {
+    const DCol& d = *data[i];
+    return kcov == total && (d.enc == RQ_ENC_PLAIN || d.enc == RQ_ENC_PLAIN_INDEX) &&
+           (fns[i] == RQ_SUM || fns[i] == RQ_AVG) && taken < 4;
+  };
   KTimer timer(ctx, "group_fused");
   // Plain / Plain+Index SUM and AVG over fully covered keys: one K12 row pass
   // streams all of them together (decode baked into the generated kernel)
@@ -787,8 +882,7 @@ bool group_aggregate_fused(const CtxPtr& ctx, const std::vector<const DCol*>& ke
     std::vector<int> xf;
     for (size_t i = 0; i < data.size(); ++i) {
       const DCol& d = *data[i];
-      if ((d.enc == RQ_ENC_PLAIN || d.enc == RQ_ENC_PLAIN_INDEX) && (fns[i] == RQ_SUM || fns[i] == RQ_AVG) &&
-          xe.size() < 4) {
+      if (to_rows(i, xe.size())) {
         XExpr x;
         XTerm t;
         t.col = &d;
@@ -1108,7 +1202,8 @@ __global__ void __launch_bounds__(BLOCK)
   if (chunk <= 0) chunk = xg_chunk(ncov, nwarps);
   for (int64_t c0 = warp * chunk; c0 < ncov; c0 += nwarps * chunk) {
     const int64_t c1 = min(c0 + chunk, ncov);
-    int64_t k = warp_lower_bound(S.off, nseg, c0 + 1) - 1;  // segment holding covered row c0
+    // segment holding covered row c0
+    int64_t k = S.cstart ? ldg64(S.cstart, c0 / chunk) : warp_lower_bound(S.off, nseg, c0 + 1) - 1;
     int64_t c = c0;
     while (c < c1) {
       const int64_t off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k);
@@ -1222,16 +1317,25 @@ __device__ __forceinline__ void xg_add_u64(unsigned long long* base, int64_t cel
   for (unsigned m = same; m; m &= m - 1) sum += __shfl_sync(same, v, __ffs(m) - 1);
   if ((threadIdx.x & 31) == __ffs(same) - 1 && sum) atomicAdd(base + cell, static_cast<unsigned long long>(sum));
 }
-__device__ __forceinline__ void xg_add_f64(double* base, int64_t cell, double v) {
+// f64 adds of a warp, lanes of one cell summed in lane order; then either an
+// atomic add (order-dependent last bits) or — `part` given — a plain add into
+// this warp's own partial-table row, folded over warps in a fixed order later
+// (k_xg_dfold): bit-identical run to run.
+__device__ __forceinline__ void xg_add_f64(double* base, int64_t cell, double v, double* part = nullptr) {
   const unsigned same = __match_any_sync(__activemask(), static_cast<unsigned long long>(cell));
   double sum = 0.0;
   for (unsigned m = same; m; m &= m - 1) sum += __shfl_sync(same, v, __ffs(m) - 1);
-  if ((threadIdx.x & 31) == __ffs(same) - 1 && sum != 0.0) atomicAdd(base + cell, sum);
+  if ((threadIdx.x & 31) != __ffs(same) - 1) return;
+  if (part) part[cell] += sum;
+  else if (sum != 0.0) atomicAdd(base + cell, sum);
 }
 
 __global__ void k_xg_segs(const __grid_constant__ XgPlan P, const __grid_constant__ XgSegs S, unsigned long long* __restrict__ tab,
-                          unsigned long long* __restrict__ cnt, int* __restrict__ err) {
+                          unsigned long long* __restrict__ cnt, int* __restrict__ err, double* __restrict__ part,
+                          int64_t cells) {
   int lerr = 0;
+  // this warp's row of the f64 partial table (null: atomics)
+  double* prow = part ? part + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * cells : nullptr;
   // every lane of a warp runs the same number of iterations (warp-collective adds)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t first = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
@@ -1260,7 +1364,8 @@ __global__ void k_xg_segs(const __grid_constant__ XgPlan P, const __grid_constan
         }
       }
       const int64_t cell = slot * P.ne + ei;
-      if (X.acc_f) xg_add_f64(reinterpret_cast<double*>(tab), cell, ok ? xg_f(v, vf) * static_cast<double>(len) : 0.0);
+      if (X.acc_f)
+        xg_add_f64(reinterpret_cast<double*>(tab), cell, ok ? xg_f(v, vf) * static_cast<double>(len) : 0.0, prow);
       else xg_add_u64(tab, cell, static_cast<uint64_t>(v) * static_cast<uint64_t>(len));
     }
   }
@@ -1343,20 +1448,34 @@ __global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_
 struct XgIsF {
   int f[XG_EXPRS];
 };
-__global__ void k_xg_dfold(const double* __restrict__ dpart, int64_t nchunks, int64_t cells, int ne, XgIsF is_f,
-                           unsigned long long* __restrict__ tab) {
-  __shared__ double red[256];
+constexpr int DFOLD_B = 512;
+__global__ void __launch_bounds__(DFOLD_B)
+    k_xg_dfold(const double* __restrict__ dpart, int64_t nchunks, int64_t cells, int ne, XgIsF is_f,
+               unsigned long long* __restrict__ tab, int add = 0) {
+  __shared__ double red[DFOLD_B];
   const int64_t cell = blockIdx.x;
   if (!is_f.f[cell % ne]) return;
-  double acc = 0.0;
-  for (int64_t q = threadIdx.x; q < nchunks; q += 256) acc += dpart[q * cells + cell];
-  red[threadIdx.x] = acc;
+  // four independent partial sums per thread (loads in flight), combined in
+  // a fixed order: the same bits on every run
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t q = threadIdx.x;
+  for (; q + 3 * DFOLD_B < nchunks; q += 4 * DFOLD_B) {
+    a0 += dpart[q * cells + cell];
+    a1 += dpart[(q + DFOLD_B) * cells + cell];
+    a2 += dpart[(q + 2 * DFOLD_B) * cells + cell];
+    a3 += dpart[(q + 3 * DFOLD_B) * cells + cell];
+  }
+  for (; q < nchunks; q += DFOLD_B) a0 += dpart[q * cells + cell];
+  red[threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
+  for (int w = DFOLD_B / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) tab[cell] = static_cast<unsigned long long>(__double_as_longlong(red[0]));
+  if (threadIdx.x == 0) {
+    const double v = add ? __longlong_as_double(static_cast<long long>(tab[cell])) + red[0] : red[0];
+    tab[cell] = static_cast<unsigned long long>(__double_as_longlong(v));
+  }
 }
 
 __global__ void k_xg_lengths(const int64_t* __restrict__ s, const int64_t* __restrict__ e, int64_t n,
@@ -1467,6 +1586,9 @@ struct KwList {
   int role;       // bits: 1 key, 2 predicate column, 4 RLE operand, 8 coverage only (mask / domain)
   int cst;        // RLE operand: index of its per-fragment value array
   int64_t kmin, stride;
+  const int64_t* dir;  // rank directory of e (null: whole-list search)
+  int dshift;
+  int64_t dnb;
 };
 // A list's conjuncts on integer values folded on the host into one interval
 // and at most one value set (IN lists intersected; NE values excluded), so a
@@ -1488,6 +1610,41 @@ struct KwPlan {
   int own[KW_LISTS];   // list l has conjuncts: 1 folded (conj[l]), 2 interpreted (p[])
   KwConj conj[KW_LISTS];
 };
+
+// Rank directory of a sorted array of row positions a[0, n) over [0, total):
+// dir[b] = lower_bound(a, b << shift) for b in [0, nb], so lower_bound(a, x)
+// lies in [dir[x >> shift], dir[(x >> shift) + 1]] — a search over the few
+// entries of one block instead of log2(n) dependent loads over the array.
+// Thread i writes the blocks whose first row falls in (a[i-1], a[i]].
+__global__ void k_rank_dir(const int64_t* __restrict__ a, int64_t n, int shift, int64_t nb,
+                           int64_t* __restrict__ dir) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b0 = i == 0 ? 0 : (ldg64(a, i - 1) >> shift) + 1;
+    const int64_t b1 = i == n ? nb : min(nb, ldg64(a, i) >> shift);
+    for (int64_t b = b0; b <= b1; ++b) dir[b] = i;
+  }
+}
+
+__device__ __forceinline__ int64_t kw_lower_bound_in(const int64_t* __restrict__ e, int64_t lo, int64_t hi,
+                                                     int64_t x) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(e + mid) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// lower_bound(e, x) through the directory when there is one (x >= 0)
+__device__ __forceinline__ int64_t kw_lower_bound_dir(const int64_t* __restrict__ e, int64_t n,
+                                                      const int64_t* __restrict__ dir, int shift, int64_t nb,
+                                                      int64_t x) {
+  if (!dir) return kw_lower_bound_in(e, 0, n, x);
+  const int64_t b = x >> shift;
+  if (b >= nb) return kw_lower_bound_in(e, ldg64(dir, nb), n, x);
+  return kw_lower_bound_in(e, ldg64(dir, b), ldg64(dir, b + 1), x);
+}
 
 __device__ __forceinline__ int64_t kw_lower_bound(const int64_t* __restrict__ e, int64_t n, int64_t x) {
   int64_t lo = 0, hi = n;
@@ -1565,7 +1722,7 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __r
         rank += i;
         continue;
       }
-      const int64_t rl = kw_lower_bound(L.e, L.n, x);
+      const int64_t rl = kw_lower_bound_dir(L.e, L.n, L.dir, L.dshift, L.dnb, x);
       if (rl >= L.n || __ldg(L.s + rl) > x) keep = false;          // x not covered by list l
       else if (l < j && __ldg(L.e + rl) == x) keep = false;        // a lower-numbered list owns this end
       if (!keep) break;
@@ -1623,7 +1780,8 @@ __global__ void __launch_bounds__(BLOCK)
     k_kway_select(int64_t N, int ncst, const uint8_t* __restrict__ kept, const int64_t* __restrict__ cs,
                   const int64_t* __restrict__ ce, const int64_t* __restrict__ cslot, const uint64_t* __restrict__ ccst,
                   const int64_t* __restrict__ tpre, int64_t ntiles, int64_t* __restrict__ s, int64_t* __restrict__ e,
-                  int64_t* __restrict__ slot, uint64_t* __restrict__ cst, int64_t* __restrict__ off) {
+                  int64_t* __restrict__ slot, uint64_t* __restrict__ cst, int64_t* __restrict__ off,
+                  const int64_t* __restrict__ dims, int64_t nwarps, int64_t* __restrict__ cstart) {
   static_assert(BLOCK * ITEMS == KW_TILE, "tile of the per-tile aggregates");
   __shared__ uint64_t wn[BLOCK / 32 + 1], wr[BLOCK / 32 + 1];
   const int64_t base = (static_cast<int64_t>(blockIdx.x) * BLOCK + threadIdx.x) * ITEMS;
@@ -1643,6 +1801,7 @@ __global__ void __launch_bounds__(BLOCK)
   if (!cn) return;
   on += static_cast<uint64_t>(ldg64(tpre, blockIdx.x));
   orow += static_cast<uint64_t>(ldg64(tpre, ntiles + blockIdx.x) - ldg64(tpre, ntiles));
+  const int64_t chunk = xg_chunk(ldg64(dims, 1), nwarps);  // the row kernels' chunk (same formula)
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     if (!len[k]) continue;
@@ -1652,6 +1811,9 @@ __global__ void __launch_bounds__(BLOCK)
     slot[o] = ldg64(cslot, i);
     for (int j = 0; j < ncst; ++j) cst[static_cast<int64_t>(j) * N + o] = __ldg(ccst + static_cast<int64_t>(j) * N + i);
     off[o] = static_cast<int64_t>(orow);
+    // the row chunks whose first covered row falls in this segment start here
+    const int64_t r0 = static_cast<int64_t>(orow), r1 = r0 + static_cast<int64_t>(len[k]) - 1;
+    for (int64_t q = (r0 + chunk - 1) / chunk; q <= r1 / chunk; ++q) cstart[q] = o;
     ++on;
     orow += len[k];
   }
@@ -1665,24 +1827,41 @@ __global__ void __launch_bounds__(BLOCK)
 __global__ void k_xg_outliers_seg(PlainSrc base, const int64_t* __restrict__ p, const void* __restrict__ v2, int v2dt,
                                   int64_t n, const int64_t* __restrict__ ss, const int64_t* __restrict__ se,
                                   const int64_t* __restrict__ seg_slot, int64_t nseg, const int64_t* __restrict__ dims,
-                                  int ne, int ei, int acc_f, unsigned long long* __restrict__ tab) {
+                                  const int64_t* __restrict__ pdir, int pshift, int64_t pnb, int ne, int ei, int acc_f,
+                                  unsigned long long* __restrict__ tab, double* __restrict__ part, int64_t cells) {
   if (dims) nseg = ldg64(dims, 0);
-  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nseg;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  double* prow = part ? part + w * cells : nullptr;
+  // one warp per segment (segments in order per warp): the lanes take the
+  // segment's outliers 32 at a time, so a segment costs one search and a few
+  // rounds of parallel loads instead of one serial walk per thread
+  for (int64_t k = w; k < nseg; k += nw) {
     const int64_t a = ldg64(ss, k), b = ldg64(se, k);
-    int64_t i = kw_lower_bound(p, n, a);
-    if (i >= n || ldg64(p, i) > b) continue;
+    const int64_t cell = ldg64(seg_slot, k) * ne + ei;
+    const int64_t i0 = kw_lower_bound_dir(p, n, pdir, pshift, pnb, a);
     double fd = 0.0;
     uint64_t id = 0;
-    for (; i < n; ++i) {
-      const int64_t pos = ldg64(p, i);
-      if (pos > b) break;
-      if (acc_f) fd += ld_f64(v2, v2dt, i) - plain_value<double>(base, pos);
-      else id += static_cast<uint64_t>(ld_i64(v2, v2dt, i)) - static_cast<uint64_t>(plain_value<int64_t>(base, pos));
+    for (int64_t i = i0 + lane;; i += 32) {
+      const int64_t pos = i < n ? ldg64(p, i) : INT64_MAX;
+      const bool in = pos <= b;
+      if (in) {
+        if (acc_f) fd += ld_f64(v2, v2dt, i) - plain_value<double>(base, pos);
+        else id += static_cast<uint64_t>(ld_i64(v2, v2dt, i)) - static_cast<uint64_t>(plain_value<int64_t>(base, pos));
+      }
+      if (!__all_sync(FULL, in)) break;  // the last lane passed the segment's end
     }
-    const int64_t cell = ldg64(seg_slot, k) * ne + ei;
-    if (acc_f) atomicAdd(reinterpret_cast<double*>(tab) + cell, fd);
-    else atomicAdd(tab + cell, static_cast<unsigned long long>(id));
+    if (acc_f) {
+      fd = warp_sum(fd);  // a fixed butterfly: the same bits on every run
+      if (lane == 0) {
+        if (prow) prow[cell] += fd;
+        else if (fd != 0.0) atomicAdd(reinterpret_cast<double*>(tab) + cell, fd);
+      }
+    } else {
+      id = warp_sum(id);
+      if (lane == 0 && id) atomicAdd(tab + cell, static_cast<unsigned long long>(id));
+    }
   }
 }
 }  // namespace dev
@@ -1754,6 +1933,23 @@ bool key_layout(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKe
     st *= K.range[c];
   }
   return true;
+}
+
+// The rank directory of a column's sorted positions (run ends or index
+// points), built on first use and kept on the column (columns are
+// immutable): blocks of about four to eight elements' average span.
+const DCol::RankDir& rank_dir(const CtxPtr& ctx, const DArr& a, int64_t total, DCol::RankDir& d) {
+  if (d.shift >= 0 || a.n == 0 || total <= 0) return d;
+  const int64_t avg = std::max<int64_t>(1, total / a.n);
+  int sh = 0;  // floor(log2(avg)) + 2: a block spans 4-8 average gaps
+  while (sh < 38 && (int64_t{1} << (sh + 1)) <= avg) ++sh;
+  sh += 2;
+  d.nb = ((total - 1) >> sh) + 1;
+  d.dir = alloc_arr(ctx, RQ_I64, d.nb + 1);
+  dev::k_rank_dir<<<grid_cap(ctx, a.n + 1), 256, 0, ctx->stream>>>(a.pos(), a.n, sh, d.nb, d.dir.as<int64_t>());
+  launched(ctx);
+  d.shift = sh;
+  return d;
 }
 
 // Fold each list's conjuncts on integer values into KwConj (interval ∩ one
@@ -1859,7 +2055,7 @@ void kw_fold_conjuncts(dev::KwPlan& KP, const std::vector<int>& list_float) {
 bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, const DMask* mask,
                    const std::vector<XPred>* preds, const std::vector<const DCol*>& rle_cols, int64_t total,
                    GroupKey& K, DArr& s, DArr& e, DArr& slot, DArr& cst_all, DArr& off, DArr& dims,
-                   int64_t& cap) {
+                   DArr& cstart, int64_t& cap) {
   if (total <= 0 || total >= dev::KW_MAX_ROWS) return false;
   auto host_timer = std::make_unique<KTimer>(ctx, "kw_host");  // the plan, up to the first launch
   if (!key_layout(ctx, keys, K)) return false;
@@ -1879,6 +2075,15 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
     L.dt = col ? col->v.dt : RQ_I64;
     L.role = 0;
     L.cst = -1;
+    L.dir = nullptr;
+    if (col) {
+      const DCol::RankDir& d = rank_dir(ctx, le, col->total, col->dir_e);
+      if (d.shift >= 0) {
+        L.dir = d.dir.pos();
+        L.dshift = d.shift;
+        L.dnb = d.nb;
+      }
+    }
     of_list.push_back(col);
     return KP.nl++;
   };
@@ -1963,6 +2168,8 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
   slot = alloc_arr(ctx, RQ_I64, N);
   off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N));
   cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst));
+  const int64_t nwarps = static_cast<int64_t>(ctx->sm_count) * 8 * 8;  // the row kernels' grid (xg_fused)
+  cstart = alloc_arr(ctx, RQ_I64, nwarps + 1);
   cap = N;
   if (N == 0) return true;
   constexpr int B = 256, IT = dev::KW_TILE / 256;
@@ -1984,8 +2191,189 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
   scan_exclusive_i64(ctx, tv, tpre);
   dev::k_kway_select<B, IT><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
       N, ncst, kept, cs.pos(), ce.pos(), cslot.pos(), ccst.as<uint64_t>(), tpre.pos(), ntiles, s.as<int64_t>(),
-      e.as<int64_t>(), slot.as<int64_t>(), cst_all.as<uint64_t>(), off.as<int64_t>());
+      e.as<int64_t>(), slot.as<int64_t>(), cst_all.as<uint64_t>(), off.as<int64_t>(), dims.pos(), nwarps,
+      cstart.as<int64_t>());
   launched(ctx);
+  return true;
+}
+
+// ---- CUDA graphs of repeated plans ------------------------------------------------
+//
+// A query plan re-run on the same user handles (the C API sets ctx->graph_key
+// from the handles' ids, the expressions, literals and functions) launches the
+// same kernels on the same columns. The launches from the segment table to the
+// row folds have no host readback when the k-way builder makes the table, so
+// the second such call captures them into a CUDA graph and later calls replay
+// it: one launch instead of ~10 (Q6 / C5 were host-paced). The graph keeps
+// every block its kernels touch (freed blocks are held, not recycled); the
+// accumulators it fills (tab, cnt) are read by the host-side tail of the call
+// as before. Profiled regions inside are event-record nodes that get fresh
+// events per replay. RQ_NO_GRAPH=1 disables it (A/B).
+struct XgGraph : Ctx::GraphEntry {
+  Ctx* ctx = nullptr;
+  int seen = 0;
+  bool capturable = true;
+  bool ready = false;
+  struct Step {
+    cudaGraphExec_t exec = nullptr;  // a piece, or a region boundary (tag, kind)
+    std::string tag;
+    int kind = 0;
+  };
+  std::vector<Step> steps;
+  std::vector<std::pair<void*, size_t>> owned;
+  GroupKey K;
+  void* tab = nullptr;
+  void* cnt = nullptr;
+  size_t tab_cap = 0, cnt_cap = 0;
+  int64_t tab_n = 0, cnt_n = 0;
+  int64_t nlaunch = 0;
+  ~XgGraph() override {
+    for (auto& st : steps)
+      if (st.exec) cudaGraphExecDestroy(st.exec);
+    for (auto& b : owned) ctx->free(b.first, b.second);
+  }
+  // launches the pieces in order; a profiled region's events go between them
+  void replay(Ctx& c) {
+    std::vector<std::pair<std::string, cudaEvent_t>> open;
+    for (auto& st : steps) {
+      if (st.exec) {
+        RQ_CUDA_CHECK(cudaGraphLaunch(st.exec, c.stream));
+      } else if (st.kind == 1) {
+        cudaEvent_t a = c.get_event();
+        RQ_CUDA_CHECK(cudaEventRecord(a, c.stream));
+        open.push_back({st.tag, a});
+      } else if (st.kind == 2 && !open.empty()) {
+        cudaEvent_t b = c.get_event();
+        RQ_CUDA_CHECK(cudaEventRecord(b, c.stream));
+        c.pending.push_back({open.back().first, open.back().second, b});
+        open.pop_back();
+      }
+    }
+    c.count_launch(static_cast<int>(nlaunch));
+  }
+};
+
+// a non-owning view of a block the graph keeps
+DArr graph_view(const CtxPtr& ctx, void* p, size_t cap, int64_t n) {
+  DArr a;
+  a.dt = RQ_I64;
+  a.n = n;
+  a.buf = std::make_shared<Buffer>();
+  a.buf->ctx = ctx;
+  a.buf->ptr = p;
+  a.buf->bytes = static_cast<size_t>(n) * 8;
+  a.buf->cap = cap;
+  a.buf->owned = false;
+  return a;
+}
+
+// Runs `middle` (returns 0: plan not fusable) directly, by capturing it, or by
+// replaying its graph; K / tab / cnt / kway are its outputs.
+template <class F>
+bool run_graph(const CtxPtr& ctx, bool allowed, F& middle, GroupKey& K, DArr& tab, DArr& cnt, bool& kway) {
+  std::string key;
+  key.swap(ctx->graph_key);  // consumed by the first fused pass of the call
+  static const bool off = std::getenv("RQ_NO_GRAPH") != nullptr;
+  if (key.empty() || off || !allowed) return middle() != 0;
+  if (ctx->profiling) {  // graphs captured with and without event nodes are distinct
+    key += "|prof";
+    for (const auto& t : ctx->profile_only) key += "," + t;
+  }
+  auto it = ctx->graphs.find(key);
+  if (it == ctx->graphs.end()) {
+    if (ctx->graphs.size() >= 16) ctx->drop_graphs();  // bounded: drop them all (after a sync)
+    auto fresh = std::make_shared<XgGraph>();
+    fresh->ctx = ctx.get();
+    it = ctx->graphs.emplace(key, fresh).first;
+  }
+  auto* g = static_cast<XgGraph*>(it->second.get());
+  if (g->ready) {  // replay
+    g->replay(*ctx);
+    K = g->K;
+    tab = graph_view(ctx, g->tab, g->tab_cap, g->tab_n);
+    cnt = graph_view(ctx, g->cnt, g->cnt_cap, g->cnt_n);
+    kway = true;
+    return true;
+  }
+  if (g->seen == 0 || !g->capturable) {  // first call: run it, note whether it can be captured
+    ++g->seen;
+    const bool ok = middle() != 0;
+    g->capturable = g->capturable && ok && kway;
+    return ok;
+  }
+  // second call: capture, then replay
+  ctx->capture_owned.clear();
+  ctx->capture_steps.clear();
+  ctx->capture_broken = false;
+  RQ_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+  ctx->capturing = true;
+  const int64_t l0 = ctx->launches;
+  int r = 0;
+  bool threw = false;
+  try {
+    r = middle();
+  } catch (...) {
+    threw = true;
+  }
+  ctx->capturing = false;
+  cudaGraph_t last = nullptr;
+  if (cudaStreamEndCapture(ctx->stream, &last) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->capture_broken = true;
+  }
+  ctx->capture_steps.push_back({last, "", 0});
+  bool ok = !threw && r == 1 && kway && !ctx->capture_broken;
+  std::vector<XgGraph::Step> steps;
+  for (auto& cs : ctx->capture_steps) {
+    if (cs.kind != 0) {
+      steps.push_back({nullptr, cs.tag, cs.kind});
+      continue;
+    }
+    size_t nn = 0;
+    if (!cs.g) {
+      ok = false;
+      continue;
+    }
+    if (ok && cudaGraphGetNodes(cs.g, nullptr, &nn) == cudaSuccess && nn > 0) {
+      cudaGraphExec_t ex = nullptr;
+      if (cudaGraphInstantiate(&ex, cs.g, 0) == cudaSuccess) steps.push_back({ex, "", 0});
+      else ok = false;
+    }
+    cudaGraphDestroy(cs.g);
+  }
+  ctx->capture_steps.clear();
+  if (!ok) {  // not capturable after all: release what the capture held, run it directly
+    cudaGetLastError();
+    for (auto& st : steps)
+      if (st.exec) cudaGraphExecDestroy(st.exec);
+    auto owned = std::move(ctx->capture_owned);
+    ctx->capture_owned.clear();
+    for (auto& b : owned) ctx->free(b.first, b.second);  // nothing ran: safe to recycle
+    g->capturable = false;
+    K = GroupKey();
+    tab = cnt = DArr();
+    return middle() != 0;
+  }
+  g->steps = std::move(steps);
+  g->owned = std::move(ctx->capture_owned);
+  ctx->capture_owned.clear();
+  g->nlaunch = ctx->launches - l0;
+  ctx->launches = l0;  // counted when the pieces run (replay)
+  g->K = K;  // the layout only: no arrays held (they would keep the context alive)
+  g->K.s = g->K.e = g->K.slot = DArr();
+  // the accumulators now belong to the graph; this call reads them through views
+  g->tab = tab.raw_mut();
+  g->tab_cap = tab.buf->cap;
+  g->tab_n = tab.n;
+  tab.buf->owned = false;
+  g->owned.push_back({g->tab, g->tab_cap});
+  g->cnt = cnt.raw_mut();
+  g->cnt_cap = cnt.buf->cap;
+  g->cnt_n = cnt.n;
+  cnt.buf->owned = false;
+  g->owned.push_back({g->cnt, g->cnt_cap});
+  g->ready = true;
+  g->replay(*ctx);
   return true;
 }
 
@@ -2080,215 +2468,259 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   plan_timer.reset();
   KTimer timer(ctx, "group_exprs");
   GroupKey K;
-  DArr s, e, slot, cst_all, off, dims;
-  int64_t nseg = 0, ncov = 0;  // host-known sizes (pairwise builder); the k-way one leaves them in dims
-  const bool kway = !preK && kway_segments(ctx, keys, mask, preds, rle_cols, total, K, s, e, slot, cst_all, off, dims,
-                                           nseg);
-  if (!kway) {
-    auto stage = std::make_unique<KTimer>(ctx, "xg_keys");  // per-stage profile tags (no-ops unless profiling)
-    if (preK) {
-      K = *preK;
-    } else if (!keys.empty()) {
-      if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return false;
-    } else {
-      if (total == 0) return false;
-      // one run [0, total) in slot 0 (one device fill: no host staging)
-      K.s = alloc_arr(ctx, RQ_I64, 1);
-      K.e = alloc_arr(ctx, RQ_I64, 1);
-      K.slot = alloc_arr(ctx, RQ_I64, 1);
-      dev::k_xg_fill3<<<1, 1, 0, ctx->stream>>>(K.s.as<int64_t>(), 0, K.e.as<int64_t>(), total - 1,
-                                                K.slot.as<int64_t>(), 0);
-      launched(ctx);
-      K.G = 1;
-    }
-    stage = std::make_unique<KTimer>(ctx, "xg_where");
-    s = K.s;
-    e = K.e;
-    slot = K.slot;
-    std::vector<DArr> cst;
-    if (mask) {
-      // the mask's true rows as runs: RLE as is, a plain byte mask through
-      // plain_mask_to_rle (primitives.cpp:349-360), index points as 1-row runs
-      DArr ms = mask->s, me = mask->e;
-      if (mask->enc == RQ_MASK_PLAIN) plain_mask_to_rle(ctx, mask->bits, ms, me);
-      else if (mask->enc == RQ_MASK_INDEX) ms = me = mask->p;
-      Intersection r = range_intersect(ctx, s, e, ms, me, true, false);
-      slot = gather(ctx, slot, r.idx1);
-      s = r.s;
-      e = r.e;
-    }
-    if (npred) {
-      // WHERE pushdown: the segments are intersected with each distinct
-      // predicate column's runs (fewest runs first) and the passing segments
-      // kept; before a column with many runs the segments are pruned by the
-      // conjuncts already evaluable, so the large intersection runs on the
-      // selected segments only.
-      std::vector<const DCol*> pcols;  // distinct predicate columns
-      std::vector<int> pcol_of(npred);
-      for (size_t i = 0; i < npred; ++i) {
-        const XPred& q = (*preds)[i];
-        int src = -1;
-        for (size_t j = 0; j < pcols.size(); ++j)
-          if (pcols[j] == q.col || (pcols[j]->v.raw() == q.col->v.raw() && pcols[j]->e.raw() == q.col->e.raw()))
-            src = static_cast<int>(j);
-        if (src < 0) {
-          pcols.push_back(q.col);
-          src = static_cast<int>(pcols.size()) - 1;
-        }
-        pcol_of[i] = src;
-      }
-      std::vector<int> order(pcols.size());
-      for (size_t j = 0; j < order.size(); ++j) order[j] = static_cast<int>(j);
-      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return pcols[x]->e.n < pcols[y]->e.n; });
-      std::vector<int> slot_of(pcols.size(), -1);  // predicate column -> its value array in pv
-      std::vector<DArr> pv;
-      // keep the segments passing every conjunct whose column is already joined in
-      auto prune = [&]() {
-        dev::XgPreds W{};
-        for (size_t i = 0; i < npred; ++i) {
-          const int src = slot_of[pcol_of[i]];
-          if (src < 0) continue;
-          const XPred& q = (*preds)[i];
-          dev::XgPred& P = W.p[W.n++];
-          P.src = src;
-          P.flt = dt_float(q.col->v.dt) ? 1 : 0;
-          P.op = q.in.empty() ? q.op : -1;
-          const std::vector<Scalar> one{q.k};
-          const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
-          P.n_in = static_cast<int>(ks.size());
-          for (size_t j = 0; j < ks.size(); ++j) {
-            P.kflt[j] = ks[j].is_float ? 1 : 0;
-            P.ki[j] = ks[j].i;
-            P.kf[j] = ks[j].f;
-          }
-        }
-        for (size_t j = 0; j < pv.size(); ++j) W.val[j] = reinterpret_cast<const uint64_t*>(pv[j].raw());
-        if (!s.n || !W.n) return;
-        DArr flags = alloc_arr(ctx, RQ_I8, s.n);
-        dev::k_xg_where<<<grid_cap(ctx, s.n), 256, 0, ctx->stream>>>(W, s.n, flags.as<uint8_t>());
+  DArr tab, cnt;
+  int* err = reinterpret_cast<int*>(ctx->tickets + 2);  // zero between launches (reset after the check)
+  bool kway = false;
+  // The plan's launches from the segment table to the row folds: no host
+  // readback when the k-way builder makes the table, so a repeated call on
+  // the same user handles replays them as one CUDA graph (run_graph below).
+  auto middle = [&]() -> int {
+    DArr s, e, slot, cst_all, off, dims, cstart;
+    int64_t nseg = 0, ncov = 0;  // host-known sizes (pairwise builder); the k-way one leaves them in dims
+    kway = !preK && kway_segments(ctx, keys, mask, preds, rle_cols, total, K, s, e, slot, cst_all, off, dims,
+                                  cstart, nseg);
+    if (!kway) {
+      auto stage = std::make_unique<KTimer>(ctx, "xg_keys");  // per-stage profile tags (no-ops unless profiling)
+      if (preK) {
+        K = *preK;
+      } else if (!keys.empty()) {
+        if (!(keys.size() == 1 ? build_key(ctx, keys, K) : build_multi_key(ctx, keys, K))) return 0;
+      } else {
+        if (total == 0) return 0;
+        // one run [0, total) in slot 0 (one device fill: no host staging)
+        K.s = alloc_arr(ctx, RQ_I64, 1);
+        K.e = alloc_arr(ctx, RQ_I64, 1);
+        K.slot = alloc_arr(ctx, RQ_I64, 1);
+        dev::k_xg_fill3<<<1, 1, 0, ctx->stream>>>(K.s.as<int64_t>(), 0, K.e.as<int64_t>(), total - 1,
+                                                  K.slot.as<int64_t>(), 0);
         launched(ctx);
-        DArr keep;
-        flagged_indices(ctx, flags, s.n, keep);
-        std::vector<DArr*> g{&s, &e, &slot};
-        for (auto& v : pv) g.push_back(&v);
-        gather_many(ctx, g, keep);
-      };
-      for (size_t oi = 0; oi < order.size(); ++oi) {
-        const DCol* col = pcols[order[oi]];
-        if (oi > 0 && col->e.n >= 65536 && s.n > 0 && col->e.n >= 16 * s.n) prune();
-        Intersection r = range_intersect(ctx, s, e, col->s, col->e, true, true);
-        DArr nv = col->v;  // segment tables through idx1, the column's values through idx2: one launch
-        std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
-        for (auto& v : pv) g.push_back({&v, &r.idx1});
-        g.push_back({&nv, &r.idx2});
-        gather_multi(ctx, g);
-        pv.push_back(nv);
-        slot_of[order[oi]] = static_cast<int>(pv.size()) - 1;
+        K.G = 1;
+      }
+      stage = std::make_unique<KTimer>(ctx, "xg_where");
+      s = K.s;
+      e = K.e;
+      slot = K.slot;
+      std::vector<DArr> cst;
+      if (mask) {
+        // the mask's true rows as runs: RLE as is, a plain byte mask through
+        // plain_mask_to_rle (primitives.cpp:349-360), index points as 1-row runs
+        DArr ms = mask->s, me = mask->e;
+        if (mask->enc == RQ_MASK_PLAIN) plain_mask_to_rle(ctx, mask->bits, ms, me);
+        else if (mask->enc == RQ_MASK_INDEX) ms = me = mask->p;
+        Intersection r = range_intersect(ctx, s, e, ms, me, true, false);
+        slot = gather(ctx, slot, r.idx1);
         s = r.s;
         e = r.e;
       }
-      prune();
+      if (npred) {
+        // WHERE pushdown: the segments are intersected with each distinct
+        // predicate column's runs (fewest runs first) and the passing segments
+        // kept; before a column with many runs the segments are pruned by the
+        // conjuncts already evaluable, so the large intersection runs on the
+        // selected segments only.
+        std::vector<const DCol*> pcols;  // distinct predicate columns
+        std::vector<int> pcol_of(npred);
+        for (size_t i = 0; i < npred; ++i) {
+          const XPred& q = (*preds)[i];
+          int src = -1;
+          for (size_t j = 0; j < pcols.size(); ++j)
+            if (pcols[j] == q.col || (pcols[j]->v.raw() == q.col->v.raw() && pcols[j]->e.raw() == q.col->e.raw()))
+              src = static_cast<int>(j);
+          if (src < 0) {
+            pcols.push_back(q.col);
+            src = static_cast<int>(pcols.size()) - 1;
+          }
+          pcol_of[i] = src;
+        }
+        std::vector<int> order(pcols.size());
+        for (size_t j = 0; j < order.size(); ++j) order[j] = static_cast<int>(j);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return pcols[x]->e.n < pcols[y]->e.n; });
+        std::vector<int> slot_of(pcols.size(), -1);  // predicate column -> its value array in pv
+        std::vector<DArr> pv;
+        // keep the segments passing every conjunct whose column is already joined in
+        auto prune = [&]() {
+          dev::XgPreds W{};
+          for (size_t i = 0; i < npred; ++i) {
+            const int src = slot_of[pcol_of[i]];
+            if (src < 0) continue;
+            const XPred& q = (*preds)[i];
+            dev::XgPred& P = W.p[W.n++];
+            P.src = src;
+            P.flt = dt_float(q.col->v.dt) ? 1 : 0;
+            P.op = q.in.empty() ? q.op : -1;
+            const std::vector<Scalar> one{q.k};
+            const std::vector<Scalar>& ks = q.in.empty() ? one : q.in;
+            P.n_in = static_cast<int>(ks.size());
+            for (size_t j = 0; j < ks.size(); ++j) {
+              P.kflt[j] = ks[j].is_float ? 1 : 0;
+              P.ki[j] = ks[j].i;
+              P.kf[j] = ks[j].f;
+            }
+          }
+          for (size_t j = 0; j < pv.size(); ++j) W.val[j] = reinterpret_cast<const uint64_t*>(pv[j].raw());
+          if (!s.n || !W.n) return;
+          DArr flags = alloc_arr(ctx, RQ_I8, s.n);
+          dev::k_xg_where<<<grid_cap(ctx, s.n), 256, 0, ctx->stream>>>(W, s.n, flags.as<uint8_t>());
+          launched(ctx);
+          DArr keep;
+          flagged_indices(ctx, flags, s.n, keep);
+          std::vector<DArr*> g{&s, &e, &slot};
+          for (auto& v : pv) g.push_back(&v);
+          gather_many(ctx, g, keep);
+        };
+        for (size_t oi = 0; oi < order.size(); ++oi) {
+          const DCol* col = pcols[order[oi]];
+          if (oi > 0 && col->e.n >= 65536 && s.n > 0 && col->e.n >= 16 * s.n) prune();
+          Intersection r = range_intersect(ctx, s, e, col->s, col->e, true, true);
+          DArr nv = col->v;  // segment tables through idx1, the column's values through idx2: one launch
+          std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
+          for (auto& v : pv) g.push_back({&v, &r.idx1});
+          g.push_back({&nv, &r.idx2});
+          gather_multi(ctx, g);
+          pv.push_back(nv);
+          slot_of[order[oi]] = static_cast<int>(pv.size()) - 1;
+          s = r.s;
+          e = r.e;
+        }
+        prune();
+      }
+      stage = std::make_unique<KTimer>(ctx, "xg_operands");
+      for (const DCol* rc : rle_cols) {
+        Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
+        DArr nv = rc->v;
+        std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
+        for (auto& c : cst) g.push_back({&c, &r.idx1});
+        g.push_back({&nv, &r.idx2});
+        gather_multi(ctx, g);
+        cst.push_back(nv);
+        s = r.s;
+        e = r.e;
+      }
+      stage = std::make_unique<KTimer>(ctx, "xg_prep");
+      nseg = s.n;
+      cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * static_cast<int64_t>(cst.size())));
+      for (size_t j = 0; j < cst.size(); ++j)
+        if (nseg)
+          RQ_CUDA_CHECK(cudaMemcpyAsync(cst_all.as<int64_t>() + j * nseg, cst[j].raw(), nseg * 8,
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+      off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
+      if (nseg) {
+        // lengths plus a trailing 0: the exclusive scan's last entry is the covered-row total
+        DArr len = alloc_arr(ctx, RQ_I64, nseg + 1);
+        dev::k_xg_lengths<<<grid_cap(ctx, nseg + 1), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
+        launched(ctx);
+        scan_exclusive_i64(ctx, len, off);
+        ncov = *ctx->readback(off.as<int64_t>() + nseg, 8);
+      }
     }
-    stage = std::make_unique<KTimer>(ctx, "xg_operands");
-    for (const DCol* rc : rle_cols) {
-      Intersection r = range_intersect(ctx, s, e, rc->s, rc->e, true, true);
-      DArr nv = rc->v;
-      std::vector<std::pair<DArr*, const DArr*>> g{{&slot, &r.idx1}};
-      for (auto& c : cst) g.push_back({&c, &r.idx1});
-      g.push_back({&nv, &r.idx2});
-      gather_multi(ctx, g);
-      cst.push_back(nv);
-      s = r.s;
-      e = r.e;
-    }
-    stage = std::make_unique<KTimer>(ctx, "xg_prep");
-    nseg = s.n;
-    cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg * static_cast<int64_t>(cst.size())));
-    for (size_t j = 0; j < cst.size(); ++j)
-      if (nseg)
-        RQ_CUDA_CHECK(cudaMemcpyAsync(cst_all.as<int64_t>() + j * nseg, cst[j].raw(), nseg * 8,
-                                      cudaMemcpyDeviceToDevice, ctx->stream));
-    off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, nseg));
+    auto stage = std::make_unique<KTimer>(ctx, "xg_prep");
+    const int64_t G = K.G;
+    const int64_t cells = G * P.ne;
+    if (cells > (int64_t{1} << 26)) return 0;
+    tab = new_table(ctx, std::max<int64_t>(1, cells), 0);
+    cnt = new_table(ctx, G, 0);
+    // k-way: nseg is the table's capacity, the counts are read on the device
+    dev::XgSegs S{s.pos(), e.pos(), off.pos(),  slot.pos(), reinterpret_cast<const uint64_t*>(cst_all.raw()),
+                  nseg,    ncov,    nullptr,    0,          kway ? dims.pos() : nullptr,
+                  nseg,    kway ? cstart.pos() : nullptr};
+    // average covered segment length (the row kernel's prefetch choice): the
+    // k-way table's is estimated as rows per candidate
+    const int64_t avg_len = kway ? total / std::max<int64_t>(1, nseg) : ncov / std::max<int64_t>(1, nseg);
+    auto* tabp = reinterpret_cast<unsigned long long*>(tab.raw_mut());
+    auto* cntp = reinterpret_cast<unsigned long long*>(cnt.raw_mut());
+    DArr dpart;
+    int64_t dchunks = 0;
+    // f64 expressions over RLE operands only: per-warp partial rows + a
+    // fixed-order fold (bit-identical results; atomics past the budget)
+    auto f64_part = [&](int blocks, DArr& part) -> double* {
+      const int64_t rows = static_cast<int64_t>(blocks) * 8;
+      if (rows * cells > (int64_t{8} << 20)) return nullptr;
+      part = alloc_arr(ctx, RQ_F64, rows * cells);
+      RQ_CUDA_CHECK(cudaMemsetAsync(part.raw_mut(), 0, static_cast<size_t>(rows * cells) * 8, ctx->stream));
+      return part.as<double>();
+    };
     if (nseg) {
-      // lengths plus a trailing 0: the exclusive scan's last entry is the covered-row total
-      DArr len = alloc_arr(ctx, RQ_I64, nseg + 1);
-      dev::k_xg_lengths<<<grid_cap(ctx, nseg + 1), 256, 0, ctx->stream>>>(s.pos(), e.pos(), nseg, len.as<int64_t>());
+      dev::XgIsF sf{};
+      bool any_sf = false;
+      for (int i = 0; i < P.ne; ++i) {
+        sf.f[i] = !P.e[i].rows && P.e[i].nt > 0 && P.e[i].acc_f;
+        any_sf = any_sf || sf.f[i];
+      }
+      const int gs = grid_cap(ctx, nseg);
+      DArr spart;
+      double* sp = any_sf ? f64_part(gs, spart) : nullptr;
+      dev::k_xg_segs<<<gs, 256, 0, ctx->stream>>>(P, S, tabp, cntp, err, sp, cells);
       launched(ctx);
-      scan_exclusive_i64(ctx, len, off);
-      ncov = *ctx->readback(off.as<int64_t>() + nseg, 8);
+      if (sp) {
+        dev::k_xg_dfold<<<static_cast<unsigned>(cells), dev::DFOLD_B, 0, ctx->stream>>>(sp, int64_t{gs} * 8, cells, P.ne, sf,
+                                                                               tabp);
+        launched(ctx);
+      }
     }
-  }
-  auto stage = std::make_unique<KTimer>(ctx, "xg_prep");
+    bool any_rows = false;
+    for (int i = 0; i < P.ne; ++i) any_rows = any_rows || P.e[i].rows;
+    stage.reset();
+    if (any_rows && (kway ? nseg > 0 : ncov > 0)) {
+      constexpr int B = 256;
+      const int64_t warps = static_cast<int64_t>(ctx->sm_count) * 8 * (B / 32);
+      // chunk 0: the kernel derives it from the device-side row count (same formula)
+      const int64_t chunk = kway ? 0 : dev::xg_chunk(ncov, warps);
+      // f64 row sums: per-chunk partial tables + a fixed-order fold, so two runs
+      // give bit-identical results (atomics only past the table budget)
+      bool any_f = false;
+      for (int i = 0; i < P.ne; ++i) any_f = any_f || (P.e[i].rows && P.e[i].acc_f);
+      const int64_t nchunks = kway ? warps : (ncov + chunk - 1) / chunk;  // k-way: the bound (zeros fold exactly)
+      static const bool nodet = std::getenv("RQ_XG_NODET") != nullptr;  // A/B knob: atomic f64 flushes
+      if (any_f && !nodet && nchunks * cells <= (int64_t{8} << 20)) {
+        dpart = alloc_arr(ctx, RQ_F64, nchunks * cells);
+        RQ_CUDA_CHECK(cudaMemsetAsync(dpart.raw_mut(), 0, static_cast<size_t>(nchunks * cells) * 8, ctx->stream));
+        S.dpart = dpart.as<double>();
+        S.dcells = cells;
+        dchunks = nchunks;
+      }
+      const int64_t blocks = kway ? static_cast<int64_t>(ctx->sm_count) * 8
+                                  : std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
+                                                      (ncov / chunk + (B / 32)) / (B / 32) + 1);
+      constexpr size_t smem = dev::xg_rows_smem<B>();
+      kernel_occupancy(ctx, dev::k_xg_rows<B>, B, smem);  // shared-memory opt-in on this device
+      KTimer rows_timer(ctx, "xg_rows");
+      const char* nojit = std::getenv("RQ_NO_JIT");
+      if ((nojit && nojit[0] == '1') ||
+          !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks), avg_len))
+        dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
+      launched(ctx);
+      if (S.dpart) {
+        dev::XgIsF isf{};  // by value: no host staging
+        for (int i = 0; i < P.ne; ++i) isf.f[i] = P.e[i].rows && P.e[i].acc_f;
+        dev::k_xg_dfold<<<static_cast<unsigned>(cells), dev::DFOLD_B, 0, ctx->stream>>>(S.dpart, dchunks, cells, P.ne, isf,
+                                                                               tabp);
+        launched(ctx);
+      }
+    }
+    for (auto& pe : pi_exprs) {  // Plain+Index: outliers inside segments (located by search, not materialised)
+      const DCol& c = *pe.second;
+      if (c.p2.n == 0 || nseg == 0) continue;
+      const dev::XgExpr& X = P.e[pe.first];
+      const DCol::RankDir& pd = rank_dir(ctx, c.p2, c.total, c.dir_p2);
+      const int gs = grid_cap(ctx, nseg * 32);  // a warp per segment
+      DArr opart;
+      double* op = X.acc_f ? f64_part(gs, opart) : nullptr;
+      dev::k_xg_outliers_seg<<<gs, 256, 0, ctx->stream>>>(
+          P.col[X.t[0].src], c.p2.pos(), c.v2.raw(), c.v2.dt, c.p2.n, s.pos(), e.pos(), slot.pos(), nseg, S.dims,
+          pd.shift >= 0 ? pd.dir.pos() : nullptr, pd.shift, pd.nb, P.ne, pe.first, X.acc_f, tabp, op, cells);
+      launched(ctx);
+      if (op) {  // added after the row pass's fold wrote the base sums
+        dev::XgIsF of{};
+        of.f[pe.first] = 1;
+        dev::k_xg_dfold<<<static_cast<unsigned>(cells), dev::DFOLD_B, 0, ctx->stream>>>(op, int64_t{gs} * 8, cells, P.ne, of,
+                                                                               tabp, 1);
+        launched(ctx);
+      }
+    }
+    return 1;
+  };
+  if (!run_graph(ctx, preK == nullptr, middle, K, tab, cnt, kway)) return false;
   const int64_t G = K.G;
-  const int64_t cells = G * P.ne;
-  if (cells > (int64_t{1} << 26)) return false;
-  DArr tab = new_table(ctx, std::max<int64_t>(1, cells), 0);
-  DArr cnt = new_table(ctx, G, 0);
-  int* err = reinterpret_cast<int*>(ctx->tickets + 2);  // zero between launches (reset after the check)
-  // k-way: nseg is the table's capacity, the counts are read on the device
-  dev::XgSegs S{s.pos(), e.pos(), off.pos(),  slot.pos(), reinterpret_cast<const uint64_t*>(cst_all.raw()),
-                nseg,    ncov,    nullptr,    0,          kway ? dims.pos() : nullptr,
-                nseg};
-  // average covered segment length (the row kernel's prefetch choice): the
-  // k-way table's is estimated as rows per candidate
-  const int64_t avg_len = kway ? total / std::max<int64_t>(1, nseg) : ncov / std::max<int64_t>(1, nseg);
-  auto* tabp = reinterpret_cast<unsigned long long*>(tab.raw_mut());
-  auto* cntp = reinterpret_cast<unsigned long long*>(cnt.raw_mut());
-  DArr dpart;
-  int64_t dchunks = 0;
-  if (nseg) {
-    dev::k_xg_segs<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(P, S, tabp, cntp, err);
-    launched(ctx);
-  }
-  bool any_rows = false;
-  for (int i = 0; i < P.ne; ++i) any_rows = any_rows || P.e[i].rows;
-  stage.reset();
-  if (any_rows && (kway ? nseg > 0 : ncov > 0)) {
-    constexpr int B = 256;
-    const int64_t warps = static_cast<int64_t>(ctx->sm_count) * 8 * (B / 32);
-    // chunk 0: the kernel derives it from the device-side row count (same formula)
-    const int64_t chunk = kway ? 0 : dev::xg_chunk(ncov, warps);
-    // f64 row sums: per-chunk partial tables + a fixed-order fold, so two runs
-    // give bit-identical results (atomics only past the table budget)
-    bool any_f = false;
-    for (int i = 0; i < P.ne; ++i) any_f = any_f || (P.e[i].rows && P.e[i].acc_f);
-    const int64_t nchunks = kway ? warps : (ncov + chunk - 1) / chunk;  // k-way: the bound (zeros fold exactly)
-    static const bool nodet = std::getenv("RQ_XG_NODET") != nullptr;  // A/B knob: atomic f64 flushes
-    if (any_f && !nodet && nchunks * cells <= (int64_t{8} << 20)) {
-      dpart = alloc_arr(ctx, RQ_F64, nchunks * cells);
-      RQ_CUDA_CHECK(cudaMemsetAsync(dpart.raw_mut(), 0, static_cast<size_t>(nchunks * cells) * 8, ctx->stream));
-      S.dpart = dpart.as<double>();
-      S.dcells = cells;
-      dchunks = nchunks;
-    }
-    const int64_t blocks = kway ? static_cast<int64_t>(ctx->sm_count) * 8
-                                : std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
-                                                    (ncov / chunk + (B / 32)) / (B / 32) + 1);
-    constexpr size_t smem = dev::xg_rows_smem<B>();
-    kernel_occupancy(ctx, dev::k_xg_rows<B>, B, smem);  // shared-memory opt-in on this device
-    KTimer rows_timer(ctx, "xg_rows");
-    const char* nojit = std::getenv("RQ_NO_JIT");
-    if ((nojit && nojit[0] == '1') ||
-        !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks), avg_len))
-      dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
-    launched(ctx);
-    if (S.dpart) {
-      dev::XgIsF isf{};  // by value: no host staging
-      for (int i = 0; i < P.ne; ++i) isf.f[i] = P.e[i].rows && P.e[i].acc_f;
-      dev::k_xg_dfold<<<static_cast<unsigned>(cells), 256, 0, ctx->stream>>>(S.dpart, dchunks, cells, P.ne, isf,
-                                                                             tabp);
-      launched(ctx);
-    }
-  }
-  for (auto& pe : pi_exprs) {  // Plain+Index: outliers inside segments (located by search, not materialised)
-    const DCol& c = *pe.second;
-    if (c.p2.n == 0 || nseg == 0) continue;
-    const dev::XgExpr& X = P.e[pe.first];
-    dev::k_xg_outliers_seg<<<grid_cap(ctx, nseg), 256, 0, ctx->stream>>>(
-        P.col[X.t[0].src], c.p2.pos(), c.v2.raw(), c.v2.dt, c.p2.n, s.pos(), e.pos(), slot.pos(), nseg, S.dims,
-        P.ne, pe.first, X.acc_f, tabp);
-    launched(ctx);
-  }
   bool int_div = false;  // only integer division can raise (align.cpp:297-299)
   for (int i = 0; i < P.ne; ++i)
     for (int t = 0; t < P.e[i].nt; ++t)
@@ -2302,7 +2734,7 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     }
   }
   // ---- outputs: present slots ascending (= ascending keys) ----
-  stage = std::make_unique<KTimer>(ctx, "xg_out");
+  auto stage = std::make_unique<KTimer>(ctx, "xg_out");
   DArr present;
   if (keys.empty()) {
     present.n = 1;  // one group (slot 0): finish reads no slot list
@@ -2428,6 +2860,9 @@ GroupAggOut group_aggregate_exprs(const CtxPtr& ctx, const DMask* mask, const st
     for (auto& x : exprs)
       for (auto& t : x.terms) fusable = fusable && col_full_coverage(ctx, *t.col);
   bool ok = fusable && xg_fused(ctx, mask, keys, exprs, fns, out, nullptr, has_preds ? preds : nullptr);
+  // the CUDA-graph key names this call's user handles: the passes below run on
+  // per-call arrays (a built mask) and must never replay a graph
+  ctx->graph_key.clear();
   if (ok) {
     if (fused) *fused = true;
     return out;

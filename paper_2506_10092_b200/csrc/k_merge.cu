@@ -105,8 +105,8 @@ int64_t merge_select(const CtxPtr& ctx, const int64_t* A, int64_t na, const int6
                      int64_t nb, const Policy& pol, const char* tag) {
   if (na + nb == 0) return 0;
   int64_t ntiles = (na + nb + MTILE - 1) / MTILE;
-  dev::LookBack lb{nullptr, ctx->next_epoch(ntiles)};
-  lb.status = ctx->tile_status;
+  dev::LookBack lb{nullptr, 0};
+  lb.status = ctx->lookback_status(ntiles, &lb.epoch);
   DArr part;
   int64_t* count;
   {
@@ -170,9 +170,8 @@ PointsInRuns points_in_runs(const CtxPtr& ctx, const DArr& p, const DArr& s, con
       // few points: independent binary searches beat streaming all runs
       constexpr int B = 256, IT = 4;
       const int64_t ntiles = (p.n + B * IT - 1) / (B * IT);
-      dev::LookBack lb{ctx->tile_status, 0};
-      lb.epoch = ctx->next_epoch(ntiles);
-      lb.status = ctx->tile_status;
+      dev::LookBack lb{nullptr, 0};
+      lb.status = ctx->lookback_status(ntiles, &lb.epoch);
       dev::k_points_in_runs_search<B, IT><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
           p.pos(), p.n, s.pos(), e.pos(), s.n, lb, po, ro, io, ctx->count_slot_dev());
       ctx->count_launch();

@@ -325,8 +325,8 @@ template <class Policy>
 int64_t run_select(const CtxPtr& ctx, int64_t n, const Policy& pol) {
   if (n == 0) return 0;
   const int64_t ntiles = (n + STILE - 1) / STILE;
-  dev::LookBack lb{nullptr, ctx->next_epoch(ntiles)};
-  lb.status = ctx->tile_status;
+  dev::LookBack lb{nullptr, 0};
+  lb.status = ctx->lookback_status(ntiles, &lb.epoch);
   dev::k_select<SB, SI, Policy><<<static_cast<unsigned>(ntiles), SB, 0, ctx->stream>>>(
       n, pol, lb, ctx->count_slot_dev());
   ctx->count_launch();
@@ -496,8 +496,8 @@ DArr scan_lengths(const CtxPtr& ctx, const DArr& s, const DArr& e, int64_t& tota
   constexpr int B = 256, IT = 8;
   DArr offs = alloc_arr(ctx, RQ_I64, s.n + 1);
   const int64_t ntiles = (s.n + B * IT - 1) / (B * IT);
-  dev::LookBack lb{nullptr, ctx->next_epoch(ntiles)};
-  lb.status = ctx->tile_status;
+  dev::LookBack lb{nullptr, 0};
+  lb.status = ctx->lookback_status(ntiles, &lb.epoch);
   int64_t* tot = offs.as<int64_t>() + s.n;
   dev::k_scan_lengths<B, IT><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
       s.pos(), e.pos(), s.n, lb, offs.as<int64_t>(), tot);

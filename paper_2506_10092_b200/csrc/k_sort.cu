@@ -248,8 +248,8 @@ void scan_exclusive_i64(const CtxPtr& ctx, const DArr& in, DArr& out) {
   out = alloc_arr(ctx, RQ_I64, in.n);
   if (in.n == 0) return;
   const int64_t ntiles = (in.n + B * IT - 1) / (B * IT);
-  dev::LookBack lb{nullptr, ctx->next_epoch(ntiles)};
-  lb.status = ctx->tile_status;
+  dev::LookBack lb{nullptr, 0};
+  lb.status = ctx->lookback_status(ntiles, &lb.epoch);
   dev::k_scan_i64<B, IT><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(in.pos(), in.n, lb,
                                                                              out.as<int64_t>());
   launched(ctx);

@@ -12,6 +12,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
@@ -110,6 +111,15 @@ struct Ctx {
     return *reinterpret_cast<volatile int64_t*>(static_cast<char*>(result_host) + 2048);
   }
   bool host_profiling = std::getenv("RQ_HOST_PROFILE") != nullptr;
+  // tags the profile records (empty: every tag) — a timed loop that needs one
+  // kernel's time pays two event records per step, not one pair per scope
+  std::vector<std::string> profile_only;
+  bool profile_wants(const char* tag) const {
+    if (profile_only.empty()) return true;
+    for (const auto& t : profile_only)
+      if (t == tag) return true;
+    return false;
+  }
   void add_host_stat(const std::string& tag, double ms) {
     for (auto& kv : kstats)
       if (kv.first == tag) {
@@ -134,8 +144,39 @@ struct Ctx {
   const int64_t* readback(const void* dev, size_t bytes);
   // Ensures tile_status can hold `tiles` entries; returns the epoch to use.
   uint32_t next_epoch(int64_t tiles);
+  // Look-back status words for a launch of `tiles` tiles: the shared
+  // epoch-tagged buffer, or — while a CUDA graph is being captured — a
+  // graph-owned buffer zeroed by a captured memset on every replay.
+  unsigned long long* lookback_status(int64_t tiles, uint32_t* epoch_out);
   void* get_scratch(size_t bytes);
   void count_launch(int n = 1) { launches += n; }
+
+  // ---- CUDA-graph capture of repeated query plans (k_groupfused.cu) ----
+  // While capturing, blocks freed are kept for the graph (capture_owned)
+  // instead of returning to the cache, cache misses use cudaMalloc (no
+  // stream-ordered allocation nodes), syncs / readbacks abort the capture,
+  // and profiled regions cut the capture into pieces (capture_cut).
+  bool capturing = false;
+  bool capture_broken = false;
+  std::vector<std::pair<void*, size_t>> capture_owned;
+  // a profiled region inside a capture cuts it: the graph is replayed as
+  // pieces with the region's events recorded between them (kind 0: piece,
+  // 1: region begins, 2: region ends)
+  struct CapStep {
+    cudaGraph_t g = nullptr;
+    std::string tag;
+    int kind = 0;
+  };
+  std::vector<CapStep> capture_steps;
+  void capture_cut(const char* tag, int kind);
+  // graph cache key of the current API call (set by the C API for calls on
+  // user handles only; consumed by the first fused pass of the call)
+  std::string graph_key;
+  struct GraphEntry {
+    virtual ~GraphEntry() = default;
+  };
+  std::unordered_map<std::string, std::shared_ptr<GraphEntry>> graphs;
+  void drop_graphs();  // syncs, then releases every cached graph and its blocks
 };
 
 using CtxPtr = std::shared_ptr<Ctx>;
@@ -158,14 +199,24 @@ struct KTimer {
   const char* tag;
   cudaEvent_t a = nullptr;
   std::chrono::steady_clock::time_point h0;
+  bool cut = false;  // region boundary of a graph being captured
   KTimer(const CtxPtr& ctx, const char* t) : c(ctx.get()), tag(t) {
-    if (c->profiling) {
+    if (c->profiling && c->profile_wants(t)) {
+      if (c->capturing) {
+        c->capture_cut(t, 1);
+        cut = true;
+        return;
+      }
       a = c->get_event();
       cudaEventRecord(a, c->stream);
       if (c->host_profiling) h0 = std::chrono::steady_clock::now();
     }
   }
   ~KTimer() {
+    if (cut) {
+      c->capture_cut(tag, 2);
+      return;
+    }
     if (a) {
       cudaEvent_t b = c->get_event();
       cudaEventRecord(b, c->stream);
@@ -238,6 +289,14 @@ struct DCol {
   // key builder — columns are immutable, so the facts stay valid)
   mutable bool has_minmax = false;
   mutable int64_t vmin = 0, vmax = 0;
+  // rank directories of the run ends (e) and of the index positions (p2):
+  // dir[b] = lower_bound(a, b << shift), built on first use (rank_dir)
+  struct RankDir {
+    DArr dir;
+    int shift = -1;
+    int64_t nb = 0;
+  };
+  mutable RankDir dir_e, dir_p2;
 
   int32_t value_type() const {  // column.cpp:88-97
     switch (enc) {
@@ -271,11 +330,21 @@ struct rq_ctx_s {
 struct rq_arr_s {
   rqb::DArr a;
 };
+namespace rqb {
+// handle ids: a graph cache key names the user handles of a call, never an
+// address a later handle could reuse
+inline uint64_t next_handle_uid() {
+  static std::atomic<uint64_t> n{0};
+  return ++n;
+}
+}  // namespace rqb
 struct rq_col_s {
   rqb::DCol c;
+  uint64_t uid = rqb::next_handle_uid();
 };
 struct rq_mask_s {
   rqb::DMask m;
+  uint64_t uid = rqb::next_handle_uid();
 };
 
 namespace rqb {

@@ -60,6 +60,9 @@ struct XgSegs {
   // readback (the k-way builder); null: n / ncov above
   const int64_t* dims;
   int64_t cstride;  // operand j of segment k at cst[j * cstride + k]
+  // k-way tables: the segment holding each row chunk's first covered row
+  // (chunk q starts at row q * xg_chunk(ncov, nwarps)); null: searched in off
+  const int64_t* cstart;
 };
 
 // rows per warp chunk of the row kernels: at least 512, a multiple of 128,

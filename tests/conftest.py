@@ -11,6 +11,9 @@ import sys
 
 import pytest
 
+# a K12 code-generator error fails the test instead of falling back silently
+os.environ.setdefault("RQ_JIT_STRICT", "1")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

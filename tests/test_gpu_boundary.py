@@ -78,6 +78,39 @@ def test_scatter_reduce_input_order(rq, op):
         rq.kernels.scatter_reduce(np.array([1.0, 2.0]), np.array([0, 5]), 3, "sum")
 
 
+@pytest.mark.parametrize("op", ["sum", "min", "max", "count"])
+def test_scatter_reduce_few_large_groups(rq, op):
+    """Few groups of millions of elements take the warp-range fold: integers
+    exact, f64 min / max exact, f64 sums within 1e-12 of the input-order
+    loop and bit-identical run to run."""
+    rng = np.random.default_rng(4)
+    n, G_ = 3_000_000, 5
+    idx = rng.integers(0, G_, n)
+    idx[idx == 3] = 2  # one empty group keeps the identity
+    for vals in (rng.normal(0, 1e6, n), rng.integers(-10 ** 12, 10 ** 12, n)):
+        got = rq.kernels.scatter_reduce(vals, idx, G_, op)
+        flt = vals.dtype.kind == "f" and op != "count"
+        if op == "sum":
+            want = np.array([vals[idx == g].sum() if flt else int(vals[idx == g].astype(object).sum())
+                             for g in range(G_)], np.float64 if flt else object)
+            if not flt:
+                want = np.array([int(w) & ((1 << 64) - 1) for w in want], np.uint64).astype(np.int64)
+        elif op == "count":
+            want = np.bincount(idx, minlength=G_).astype(np.int64)
+        else:
+            f = np.min if op == "min" else np.max
+            ident = (np.inf if op == "min" else -np.inf) if flt else \
+                (np.iinfo(np.int64).max if op == "min" else np.iinfo(np.int64).min)
+            want = np.array([f(vals[idx == g]) if (idx == g).any() else ident for g in range(G_)],
+                            np.float64 if flt else np.int64)
+        if flt and op == "sum":
+            np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-3)
+            again = rq.kernels.scatter_reduce(vals, idx, G_, op)
+            assert got.tobytes() == again.tobytes()
+        else:
+            assert np.array_equal(got, want), op
+
+
 def test_unique_gather_sort_adjacent(rq):
     rng = np.random.default_rng(4)
     a = rng.integers(0, 7, 5000).astype(np.int32)
