@@ -30,6 +30,7 @@ PROTOTYPES = {
     "rq_ctx_stream": (vp, [vp]),
     "rq_ctx_launches": (i64, [vp]),
     "rq_ctx_set_profiling": (C.c_int, [vp, i32]),
+    "rq_ctx_profile_only": (C.c_int, [vp, C.c_char_p]),
     "rq_ctx_profile_report": (C.c_int, [vp, i32, C.c_char_p, i64]),
     "rq_arr_upload": (C.c_int, [vp, i32, vp, i64, P(vp)]),
     "rq_arr_wrap_device": (C.c_int, [vp, i32, vp, i64, P(vp)]),

@@ -217,11 +217,9 @@ bool pipeline_segments() {
 }
 
 // the source of a plan's kernel; literal slots are appended to ki / kf
-std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf, int pf) {
+std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<double>& kf, int pf, int minb) {
   std::ostringstream o;
   o << kPrelude;
-  const char* mb = std::getenv("RQ_JIT_MINB");  // tuning knob: min resident CTAs per SM
-  const int minb = mb ? std::atoi(mb) : 3;
   o << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") xg_kernel(const XgSegs S, const i64 chunk, u64* gtab, "
        "const i64 G, int* err, const XgCol c0, const XgCol c1, const XgCol c2, const XgCol c3, const XgK K) {\n";
   o << "  constexpr int NE = " << P.ne << ";\n";
@@ -517,7 +515,11 @@ bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S
     return e ? std::atoll(e) : int64_t{2048};
   }();
   const int pf = avg_len >= pf_min ? prefetch_distance() : 0;
-  const std::string sig = plan_signature(P, mb ? std::atoi(mb) : 3, pf);
+  // resident CTAs per SM: 3 for long segments (Q1: 4 measured 1.48 vs 1.19 ms),
+  // 4 for short ones (Q6 row kernel 41 -> 36 µs; profiles/r2_ab_jit_pipe_minb.txt);
+  // RQ_JIT_MINB overrides
+  const int minb = mb ? std::atoi(mb) : pf ? 3 : 4;
+  const std::string sig = plan_signature(P, minb, pf);
   cudaKernel_t k = nullptr;
   {
     static std::mutex mu;
@@ -529,7 +531,7 @@ bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S
     } else {
       std::vector<int64_t> ki2;
       std::vector<double> kf2;
-      k = compile(gen_source(P, ki2, kf2, pf));
+      k = compile(gen_source(P, ki2, kf2, pf, minb));
       by_sig[sig] = k;  // nullptr too: a failed compilation is not retried
     }
   }
