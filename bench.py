@@ -294,6 +294,14 @@ class Workload:
     def cpu_sample(self, rows):
         return self.gen(rows, 42)
 
+    def prepared(self, make, rq, d, comm):
+        """The query's arguments marshalled once per table (agg.prepare_exprs,
+        the call a repeated query makes); a new table (the e2e path uploads
+        one per step) prepares again. Holds `d`, so its id cannot be reused."""
+        if getattr(self, "_plan_for", None) is not d or getattr(self, "_plan_comm", None) is not comm:
+            self._plan, self._plan_for, self._plan_comm = make(rq, d, comm), d, comm
+        return self._plan
+
 
 class C2(Workload):
     name = "c2"
@@ -504,7 +512,7 @@ class Q6(Workload):
     def query(self, rq, d, path, comm=None):
         from paper_2506_10092_b200 import queries as Q
         if path == "fused":
-            v, fused = Q.q6_fused(rq, d, comm)
+            v, fused = self.prepared(Q.q6_prepared, rq, d, comm)()
             assert fused, "q6: fused path not taken"
             return v
         return Q.q6(rq, d)
@@ -555,7 +563,7 @@ class Q1(Q6):
     def query(self, rq, d, path, comm=None):
         from paper_2506_10092_b200 import queries as Q
         if path == "fused":
-            (ks, vs, ng), fused = Q.q1_fused(rq, d, comm)
+            (ks, vs, ng), fused = self.prepared(Q.q1_prepared, rq, d, comm)()
             assert fused, "q1: fused path not taken"
         else:
             ks, vs, ng = Q.q1(rq, d)
@@ -618,7 +626,7 @@ class C5(Q6):
     def query(self, rq, d, path, comm=None):
         from paper_2506_10092_b200 import queries as Q
         if path == "fused":
-            (ks, vs, ng), fused = Q.c5_fused(rq, d, comm)
+            (ks, vs, ng), fused = self.prepared(Q.c5_prepared, rq, d, comm)()
             assert fused, "c5: fused path not taken"
         else:
             ks, vs, ng = Q.c5_query(rq, d)

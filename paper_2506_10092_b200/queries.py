@@ -270,28 +270,44 @@ Q6_WHERE = [("l_shipdate", ">=", Q6_LO), ("l_shipdate", "<", Q6_HI), ("l_discoun
             ("l_discount", "<=", 7), ("l_quantity", "<", 24)]
 
 
-def q6_fused(rq, t, comm=None):
+def q6_prepared(rq, t, comm=None):
     """WHERE pushed into the fused call (conjuncts on RLE columns are
-    evaluated per run segment; no mask is materialised). `comm`: this rank's
-    shard, merged over the communicator."""
+    evaluated per run segment; no mask is materialised), marshalled once:
+    calling the result runs the query (agg.prepare_exprs). `comm`: this
+    rank's shard, merged over the communicator."""
     X = rq.X
-    _, vs, _, fused = rq.agg.group_aggregate_exprs(
+    plan = rq.agg.prepare_exprs(
         None, [], [X.col(t["l_extendedprice"]).arith(X.col(t["l_discount"]), "*")], ["sum"],
-        where=[(t[c], op, k) for c, op, k in Q6_WHERE], **({"comm": comm} if comm is not None else {}))
-    v = vs[0]
-    return (float(v.download()[0]) if hasattr(v, "download") else float(v[0])), fused
+        where=[(t[c], op, k) for c, op, k in Q6_WHERE], comm=comm)
+
+    def run():
+        _, vs, _, fused = plan()
+        v = vs[0]
+        return (float(v.download()[0]) if hasattr(v, "download") else float(v[0])), fused
+    return run
 
 
-def q1_fused(rq, t, comm=None):
+def q6_fused(rq, t, comm=None):
+    return q6_prepared(rq, t, comm)()
+
+
+def q1_prepared(rq, t, comm=None):
     X = rq.X
     price, disc, tax, qty = (t[k] for k in ("l_extendedprice", "l_discount", "l_tax", "l_quantity"))
     disc_price = X.col(price).arith(X.col(disc).scalar(100, "-", True), "*")
     charge = disc_price.arith(X.col(tax).scalar(100, "+"), "*")
     exprs = [X.col(qty), X.col(price), disc_price, charge, X.col(qty), X.col(price), X.col(disc), X.count()]
-    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [t["l_returnflag"], t["l_linestatus"]], exprs, Q1_FNS,
-                                                     where=[(t["l_shipdate"], "<=", Q1_CUTOFF)],
-                                                     **({"comm": comm} if comm is not None else {}))
-    return (ks, vs, ng), fused
+    plan = rq.agg.prepare_exprs(None, [t["l_returnflag"], t["l_linestatus"]], exprs, Q1_FNS,
+                                where=[(t["l_shipdate"], "<=", Q1_CUTOFF)], comm=comm)
+
+    def run():
+        ks, vs, ng, fused = plan()
+        return (ks, vs, ng), fused
+    return run
+
+
+def q1_fused(rq, t, comm=None):
+    return q1_prepared(rq, t, comm)()
 
 
 def c5_mask(api, t):
@@ -303,10 +319,16 @@ def c5_mask(api, t):
     return M.and_mask(m_in, C.compare_scalar(t["r3"], C5_LT, "<"))
 
 
-def c5_fused(rq, t, comm=None):
+def c5_prepared(rq, t, comm=None):
     X = rq.X
-    ks, vs, ng, fused = rq.agg.group_aggregate_exprs(None, [t["r4"]],
-                                                     [X.col(t["pi0"]), X.col(t["p1"]), X.count()], C5_FNS,
-                                                     where=[(t["r2"], "in", C5_IN), (t["r3"], "<", C5_LT)],
-                                                     **({"comm": comm} if comm is not None else {}))
-    return (ks, vs, ng), fused
+    plan = rq.agg.prepare_exprs(None, [t["r4"]], [X.col(t["pi0"]), X.col(t["p1"]), X.count()], C5_FNS,
+                                where=[(t["r2"], "in", C5_IN), (t["r3"], "<", C5_LT)], comm=comm)
+
+    def run():
+        ks, vs, ng, fused = plan()
+        return (ks, vs, ng), fused
+    return run
+
+
+def c5_fused(rq, t, comm=None):
+    return c5_prepared(rq, t, comm)()

@@ -1178,60 +1178,15 @@ class agg:
         conjuncts `where` — (col, op, k) or (col, "in", [k...]) — each X
         expression evaluated, group_aggregate(normalize) over `keys` (empty:
         one global group). Returns (keys list, values list, n_groups, fused)."""
-        fns = [H.AGG_NAMES.get(f, f) for f in fns]
-        cols = [t[0] for x in exprs for t in x.terms] + [w[0] for w in where]
-        host = _is_host(*keys, *cols, *([mask] if mask is not None else []))
-        ctx = _ctx_of(*keys, *cols, *([mask] if mask is not None else []))
-        dm = upload(mask, ctx) if mask is not None else None
-        dk = [upload(k, ctx) for k in keys]
-        arr = (H.Expr * len(exprs))()
-        keep = [dm, dk]
-        uploaded = {}  # one device column per distinct operand object
+        return PreparedExprs(mask, keys, exprs, fns, where, comm)()
 
-        def up(c):
-            if id(c) not in uploaded:
-                uploaded[id(c)] = (c, upload(c, ctx))
-            return uploaded[id(c)][1]
-        for i, x in enumerate(exprs):
-            arr[i].n_terms = len(x.terms)
-            for j, op in enumerate(x.ops):
-                arr[i].ops[j] = op
-            for j, (c, op, rev, k) in enumerate(x.terms):
-                dc = up(c)
-                keep.append(dc)
-                arr[i].terms[j].col = dc.handle.value
-                arr[i].terms[j].op = op
-                arr[i].terms[j].reversed = int(rev)
-                arr[i].terms[j].k = H.make_scalar(k)
-        karr = (C.c_void_p * max(1, len(dk)))(*[k.handle.value for k in dk])
-        farr = (C.c_int32 * len(fns))(*fns)
-        ok = (C.c_void_p * max(1, len(dk)))()
-        ov = (C.c_void_p * len(exprs))()
-        ng, fused = C.c_int64(), C.c_int32()
-        warr = (H.Pred * max(1, len(where)))()
-        for i, w in enumerate(where):
-            col, op, k = w
-            warr[i].col = up(col).handle.value
-            if isinstance(op, str) and op.lower() == "in":
-                lst = (H.Scalar * len(k))(*[H.make_scalar(x) for x in k])
-                keep.append(lst)
-                warr[i].op, warr[i].n_in, warr[i].in_list = 0, len(k), lst
-                warr[i].k = H.make_scalar(0)
-            else:
-                warr[i].op, warr[i].n_in = H.BINOP_NAMES.get(op, op), 0
-                warr[i].k = H.make_scalar(k)
-        keep.extend(uploaded.values())
-        if comm is not None:
-            check(_L.rq_group_aggregate_where_sharded(ctx.handle, comm.handle, warr, len(where),
-                                                      dm.handle if dm is not None else None, karr, len(dk), arr, farr,
-                                                      len(exprs), C.byref(ng), ok, ov, C.byref(fused)))
-        else:
-            check(_L.rq_group_aggregate_where(ctx.handle, warr, len(where), dm.handle if dm is not None else None,
-                                              karr, len(dk), arr, farr, len(exprs), C.byref(ng), ok, ov,
-                                              C.byref(fused)))
-        ks = [_out(DeviceArray(C.c_void_p(ok[i]), ctx), host) for i in range(len(dk))]
-        vs = [_out(DeviceArray(C.c_void_p(ov[i]), ctx), host) for i in range(len(exprs))]
-        return ks, vs, int(ng.value), bool(fused.value)
+    @staticmethod
+    def prepare_exprs(mask, keys: Sequence, exprs: Sequence, fns: Sequence, where: Sequence = (),
+                      comm: Comm = None) -> "PreparedExprs":
+        """group_aggregate_exprs with its arguments marshalled once: calling
+        the result runs the query again (a repeated plan on the same device
+        handles is replayed by the library as one CUDA graph)."""
+        return PreparedExprs(mask, keys, exprs, fns, where, comm)
 
     @staticmethod
     def aggregate_binop(a, b, op, fn, comm: Comm = None):
@@ -1276,3 +1231,70 @@ def shard_host_column(col: H.Column, lo: int, hi: int) -> H.Column:
         return H.column_from_malloc_image(out)
     finally:
         _L.rq_host_column_free(C.byref(out))
+
+
+class PreparedExprs:
+    """rq_group_aggregate_where(_sharded) with its C arguments built once (the
+    device columns the plan names are uploaded once and kept alive)."""
+
+    def __init__(self, mask, keys: Sequence, exprs: Sequence, fns: Sequence, where: Sequence = (),
+                 comm: Comm = None):
+        fns = [H.AGG_NAMES.get(f, f) for f in fns]
+        cols = [t[0] for x in exprs for t in x.terms] + [w[0] for w in where]
+        self.host = _is_host(*keys, *cols, *([mask] if mask is not None else []))
+        ctx = self.ctx = _ctx_of(*keys, *cols, *([mask] if mask is not None else []))
+        dm = upload(mask, ctx) if mask is not None else None
+        dk = [upload(k, ctx) for k in keys]
+        arr = (H.Expr * len(exprs))()
+        keep = [dm, dk]
+        uploaded = {}  # one device column per distinct operand object
+
+        def up(c):
+            if id(c) not in uploaded:
+                uploaded[id(c)] = (c, upload(c, ctx))
+            return uploaded[id(c)][1]
+        for i, x in enumerate(exprs):
+            arr[i].n_terms = len(x.terms)
+            for j, op in enumerate(x.ops):
+                arr[i].ops[j] = op
+            for j, (c, op, rev, k) in enumerate(x.terms):
+                dc = up(c)
+                keep.append(dc)
+                arr[i].terms[j].col = dc.handle.value
+                arr[i].terms[j].op = op
+                arr[i].terms[j].reversed = int(rev)
+                arr[i].terms[j].k = H.make_scalar(k)
+        warr = (H.Pred * max(1, len(where)))()
+        for i, w in enumerate(where):
+            col, op, k = w
+            warr[i].col = up(col).handle.value
+            if isinstance(op, str) and op.lower() == "in":
+                lst = (H.Scalar * len(k))(*[H.make_scalar(x) for x in k])
+                keep.append(lst)
+                warr[i].op, warr[i].n_in, warr[i].in_list = 0, len(k), lst
+                warr[i].k = H.make_scalar(0)
+            else:
+                warr[i].op, warr[i].n_in = H.BINOP_NAMES.get(op, op), 0
+                warr[i].k = H.make_scalar(k)
+        keep.extend(uploaded.values())
+        self._keep = keep
+        self.nk, self.ne, self.nw = len(dk), len(exprs), len(where)
+        self._args = (warr, len(where), dm.handle if dm is not None else None,
+                      (C.c_void_p * max(1, len(dk)))(*[k.handle.value for k in dk]), len(dk), arr,
+                      (C.c_int32 * len(fns))(*fns), len(exprs))
+        self.comm = comm
+
+    def __call__(self):
+        ok = (C.c_void_p * max(1, self.nk))()
+        ov = (C.c_void_p * self.ne)()
+        ng, fused = C.c_int64(), C.c_int32()
+        warr, nw, dm, karr, nk, arr, farr, ne = self._args
+        if self.comm is not None:
+            check(_L.rq_group_aggregate_where_sharded(self.ctx.handle, self.comm.handle, warr, nw, dm, karr, nk, arr,
+                                                      farr, ne, C.byref(ng), ok, ov, C.byref(fused)))
+        else:
+            check(_L.rq_group_aggregate_where(self.ctx.handle, warr, nw, dm, karr, nk, arr, farr, ne, C.byref(ng), ok,
+                                              ov, C.byref(fused)))
+        ks = [_out(DeviceArray(C.c_void_p(ok[i]), self.ctx), self.host) for i in range(self.nk)]
+        vs = [_out(DeviceArray(C.c_void_p(ov[i]), self.ctx), self.host) for i in range(self.ne)]
+        return ks, vs, int(ng.value), bool(fused.value)

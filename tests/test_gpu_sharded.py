@@ -180,7 +180,13 @@ class _Sharded:
         class agg:
             @staticmethod
             def group_aggregate_exprs(*a, **kw):
+                kw.pop("comm", None)
                 return rq.agg.group_aggregate_exprs(*a, comm=comm, **kw)
+
+            @staticmethod
+            def prepare_exprs(*a, **kw):
+                kw.pop("comm", None)
+                return rq.agg.prepare_exprs(*a, comm=comm, **kw)
         self.agg = agg
 
 
