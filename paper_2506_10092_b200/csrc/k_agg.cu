@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <type_traits>
 
 #include "merge_walk.cuh"
 #include "rq_internal.hpp"
@@ -542,26 +543,40 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
           int64_t ka = x < na_t ? wAe[x] : INT64_MAX;
           int64_t kb = y < nbi ? wB[y] : INT64_MAX;
           T va = wAv[x], vb = vB[y];
-          for (int it = d; it < dend; ++it) {
-            const bool takeA = ka <= kb;
-            const int64_t key = takeA ? ka : kb;
-            const int64_t len = key - prev;  // 0 on a tie: no fragment
-            if (KIND == 2) {
-              cnt += len;
-            } else if (KIND == 0 && OP != RQ_DIV) {
-              const T r = swap ? arith_t<T>(vb, va, OP, &lerr) : arith_t<T>(va, vb, OP, &lerr);
-              isum += static_cast<uint64_t>(static_cast<int64_t>(r)) * static_cast<uint64_t>(len);
-            } else {
-              fold(va, vb, len);
+          // a tile spanning < 2^32 rows has fragment lengths that fit 32 bits:
+          // the integer sum then multiplies 64 x 32 bits (one IMAD fewer per
+          // fragment) and takes the length from the keys' low words
+          auto walk = [&](auto narrow) {
+            constexpr bool N32 = decltype(narrow)::value;
+            for (int it = d; it < dend; ++it) {
+              const bool takeA = ka <= kb;
+              const int64_t key = takeA ? ka : kb;
+              if (KIND == 0 && OP != RQ_DIV && N32) {
+                const uint32_t len32 = static_cast<uint32_t>(key) - static_cast<uint32_t>(prev);
+                const T r = swap ? arith_t<T>(vb, va, OP, &lerr) : arith_t<T>(va, vb, OP, &lerr);
+                isum += static_cast<uint64_t>(static_cast<int64_t>(r)) * len32;
+              } else {
+                const int64_t len = key - prev;  // 0 on a tie: no fragment
+                if (KIND == 2) {
+                  cnt += len;
+                } else if (KIND == 0 && OP != RQ_DIV) {
+                  const T r = swap ? arith_t<T>(vb, va, OP, &lerr) : arith_t<T>(va, vb, OP, &lerr);
+                  isum += static_cast<uint64_t>(static_cast<int64_t>(r)) * static_cast<uint64_t>(len);
+                } else {
+                  fold(va, vb, len);
+                }
+              }
+              prev = key;
+              x += takeA ? 1 : 0;
+              y += takeA ? 0 : 1;
+              ka = x < na_t ? wAe[x] : INT64_MAX;
+              kb = y < nbi ? wB[y] : INT64_MAX;
+              va = wAv[x];
+              vb = vB[y];
             }
-            prev = key;
-            x += takeA ? 1 : 0;
-            y += takeA ? 0 : 1;
-            ka = x < na_t ? wAe[x] : INT64_MAX;
-            kb = y < nbi ? wB[y] : INT64_MAX;
-            va = wAv[x];
-            vb = vB[y];
-          }
+          };
+          if (r_hi - r_lo < (int64_t{1} << 32)) walk(std::true_type{});
+          else walk(std::false_type{});
         }
       } else {
         // slow path (the covering run is past the staged window): driver
