@@ -53,6 +53,7 @@ cudaEvent_t Ctx::get_event() {
 }
 
 void Ctx::collect_profile() {
+  while (!graph_timers_unread.empty()) read_graph_timer(graph_timers_unread.front().a);
   if (pending.empty()) return;
   RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
   for (auto& p : pending) {
@@ -77,6 +78,7 @@ void Ctx::collect_profile() {
 Ctx::~Ctx() {
   cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  graph_timers_unread.clear();
   graphs.clear();  // their blocks go back through free() while the cache is alive
   for (auto& kv : block_cache)
     for (void* p : kv.second) cudaFree(p);
@@ -230,23 +232,23 @@ unsigned long long* Ctx::lookback_status(int64_t tiles, uint32_t* epoch_out) {
   return static_cast<unsigned long long*>(p);
 }
 
-void Ctx::capture_cut(const char* tag, int kind) {
-  cudaGraph_t g = nullptr;
-  if (cudaStreamEndCapture(stream, &g) != cudaSuccess) {
-    cudaGetLastError();
-    capture_broken = true;
-  }
-  capture_steps.push_back({g, "", 0});
-  capture_steps.push_back({nullptr, tag, kind});
-  if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
-    cudaGetLastError();
-    capture_broken = true;
+void Ctx::read_graph_timer(cudaEvent_t a) {
+  for (size_t i = 0; i < graph_timers_unread.size(); ++i) {
+    const CapTimer t = graph_timers_unread[i];
+    if (t.a != a) continue;
+    RQ_CUDA_CHECK(cudaEventSynchronize(t.b));
+    float ms = 0;
+    RQ_CUDA_CHECK(cudaEventElapsedTime(&ms, t.a, t.b));
+    add_host_stat(t.tag, ms);  // (tag, ms, +1 launch) like a pending pair
+    graph_timers_unread.erase(graph_timers_unread.begin() + static_cast<std::ptrdiff_t>(i));
+    return;
   }
 }
 
 void Ctx::drop_graphs() {
   if (graphs.empty()) return;
   RQ_CUDA_CHECK(cudaStreamSynchronize(stream));
+  collect_profile();  // reads the graphs' unread timers before their events go
   graphs.clear();
 }
 

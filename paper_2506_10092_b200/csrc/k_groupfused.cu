@@ -2207,19 +2207,15 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
 // it: one launch instead of ~10 (Q6 / C5 were host-paced). The graph keeps
 // every block its kernels touch (freed blocks are held, not recycled); the
 // accumulators it fills (tab, cnt) are read by the host-side tail of the call
-// as before. Profiled regions inside are event-record nodes that get fresh
-// events per replay. RQ_NO_GRAPH=1 disables it (A/B).
+// as before. A profiled region inside is a pair of event nodes; each replay's
+// time is read before the next replay re-records them. RQ_NO_GRAPH=1
+// disables graphs (A/B).
 struct XgGraph : Ctx::GraphEntry {
   Ctx* ctx = nullptr;
   int seen = 0;
   bool capturable = true;
-  bool ready = false;
-  struct Step {
-    cudaGraphExec_t exec = nullptr;  // a piece, or a region boundary (tag, kind)
-    std::string tag;
-    int kind = 0;
-  };
-  std::vector<Step> steps;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Ctx::CapTimer> timers;  // event nodes of the profiled regions (owned)
   std::vector<std::pair<void*, size_t>> owned;
   GroupKey K;
   void* tab = nullptr;
@@ -2228,27 +2224,19 @@ struct XgGraph : Ctx::GraphEntry {
   int64_t tab_n = 0, cnt_n = 0;
   int64_t nlaunch = 0;
   ~XgGraph() override {
-    for (auto& st : steps)
-      if (st.exec) cudaGraphExecDestroy(st.exec);
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto& t : timers) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
     for (auto& b : owned) ctx->free(b.first, b.second);
   }
-  // launches the pieces in order; a profiled region's events go between them
+  // one launch; the previous run's region times are read first (the replay
+  // re-records the same events)
   void replay(Ctx& c) {
-    std::vector<std::pair<std::string, cudaEvent_t>> open;
-    for (auto& st : steps) {
-      if (st.exec) {
-        RQ_CUDA_CHECK(cudaGraphLaunch(st.exec, c.stream));
-      } else if (st.kind == 1) {
-        cudaEvent_t a = c.get_event();
-        RQ_CUDA_CHECK(cudaEventRecord(a, c.stream));
-        open.push_back({st.tag, a});
-      } else if (st.kind == 2 && !open.empty()) {
-        cudaEvent_t b = c.get_event();
-        RQ_CUDA_CHECK(cudaEventRecord(b, c.stream));
-        c.pending.push_back({open.back().first, open.back().second, b});
-        open.pop_back();
-      }
-    }
+    for (auto& t : timers) c.read_graph_timer(t.a);
+    RQ_CUDA_CHECK(cudaGraphLaunch(exec, c.stream));
+    for (auto& t : timers) c.graph_timers_unread.push_back(t);
     c.count_launch(static_cast<int>(nlaunch));
   }
 };
@@ -2287,7 +2275,7 @@ bool run_graph(const CtxPtr& ctx, bool allowed, F& middle, GroupKey& K, DArr& ta
     it = ctx->graphs.emplace(key, fresh).first;
   }
   auto* g = static_cast<XgGraph*>(it->second.get());
-  if (g->ready) {  // replay
+  if (g->exec) {  // replay
     g->replay(*ctx);
     K = g->K;
     tab = graph_view(ctx, g->tab, g->tab_cap, g->tab_n);
@@ -2303,7 +2291,7 @@ bool run_graph(const CtxPtr& ctx, bool allowed, F& middle, GroupKey& K, DArr& ta
   }
   // second call: capture, then replay
   ctx->capture_owned.clear();
-  ctx->capture_steps.clear();
+  ctx->capture_timers.clear();
   ctx->capture_broken = false;
   RQ_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
   ctx->capturing = true;
@@ -2316,36 +2304,24 @@ bool run_graph(const CtxPtr& ctx, bool allowed, F& middle, GroupKey& K, DArr& ta
     threw = true;
   }
   ctx->capturing = false;
-  cudaGraph_t last = nullptr;
-  if (cudaStreamEndCapture(ctx->stream, &last) != cudaSuccess) {
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamEndCapture(ctx->stream, &graph) != cudaSuccess) {
     cudaGetLastError();
     ctx->capture_broken = true;
   }
-  ctx->capture_steps.push_back({last, "", 0});
-  bool ok = !threw && r == 1 && kway && !ctx->capture_broken;
-  std::vector<XgGraph::Step> steps;
-  for (auto& cs : ctx->capture_steps) {
-    if (cs.kind != 0) {
-      steps.push_back({nullptr, cs.tag, cs.kind});
-      continue;
-    }
-    size_t nn = 0;
-    if (!cs.g) {
-      ok = false;
-      continue;
-    }
-    if (ok && cudaGraphGetNodes(cs.g, nullptr, &nn) == cudaSuccess && nn > 0) {
-      cudaGraphExec_t ex = nullptr;
-      if (cudaGraphInstantiate(&ex, cs.g, 0) == cudaSuccess) steps.push_back({ex, "", 0});
-      else ok = false;
-    }
-    cudaGraphDestroy(cs.g);
-  }
-  ctx->capture_steps.clear();
+  cudaGraphExec_t exec = nullptr;
+  const bool ok = !threw && r == 1 && kway && !ctx->capture_broken && graph &&
+                  cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  auto timers = std::move(ctx->capture_timers);
+  ctx->capture_timers.clear();
   if (!ok) {  // not capturable after all: release what the capture held, run it directly
     cudaGetLastError();
-    for (auto& st : steps)
-      if (st.exec) cudaGraphExecDestroy(st.exec);
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto& t : timers) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
     auto owned = std::move(ctx->capture_owned);
     ctx->capture_owned.clear();
     for (auto& b : owned) ctx->free(b.first, b.second);  // nothing ran: safe to recycle
@@ -2354,11 +2330,12 @@ bool run_graph(const CtxPtr& ctx, bool allowed, F& middle, GroupKey& K, DArr& ta
     tab = cnt = DArr();
     return middle() != 0;
   }
-  g->steps = std::move(steps);
+  g->exec = exec;
+  g->timers = std::move(timers);
   g->owned = std::move(ctx->capture_owned);
   ctx->capture_owned.clear();
   g->nlaunch = ctx->launches - l0;
-  ctx->launches = l0;  // counted when the pieces run (replay)
+  ctx->launches = l0;  // counted when the graph runs (replay)
   g->K = K;  // the layout only: no arrays held (they would keep the context alive)
   g->K.s = g->K.e = g->K.slot = DArr();
   // the accumulators now belong to the graph; this call reads them through views
@@ -2372,7 +2349,6 @@ bool run_graph(const CtxPtr& ctx, bool allowed, F& middle, GroupKey& K, DArr& ta
   g->cnt_n = cnt.n;
   cnt.buf->owned = false;
   g->owned.push_back({g->cnt, g->cnt_cap});
-  g->ready = true;
   g->replay(*ctx);
   return true;
 }

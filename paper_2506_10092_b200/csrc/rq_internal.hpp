@@ -155,20 +155,20 @@ struct Ctx {
   // While capturing, blocks freed are kept for the graph (capture_owned)
   // instead of returning to the cache, cache misses use cudaMalloc (no
   // stream-ordered allocation nodes), syncs / readbacks abort the capture,
-  // and profiled regions cut the capture into pieces (capture_cut).
+  // and profiled regions record graph-owned events (capture_timers).
   bool capturing = false;
   bool capture_broken = false;
   std::vector<std::pair<void*, size_t>> capture_owned;
-  // a profiled region inside a capture cuts it: the graph is replayed as
-  // pieces with the region's events recorded between them (kind 0: piece,
-  // 1: region begins, 2: region ends)
-  struct CapStep {
-    cudaGraph_t g = nullptr;
+  // a profiled region inside a capture records two events of its own (event
+  // nodes of the graph, re-recorded by every replay); a replay's times are
+  // read just before the next replay re-records them, or by collect_profile
+  struct CapTimer {
     std::string tag;
-    int kind = 0;
+    cudaEvent_t a, b;
   };
-  std::vector<CapStep> capture_steps;
-  void capture_cut(const char* tag, int kind);
+  std::vector<CapTimer> capture_timers;
+  std::vector<CapTimer> graph_timers_unread;
+  void read_graph_timer(cudaEvent_t a);  // the unread run of the timer starting with event a, if any
   // graph cache key of the current API call (set by the C API for calls on
   // user handles only; consumed by the first fused pass of the call)
   std::string graph_key;
@@ -199,22 +199,26 @@ struct KTimer {
   const char* tag;
   cudaEvent_t a = nullptr;
   std::chrono::steady_clock::time_point h0;
-  bool cut = false;  // region boundary of a graph being captured
+  bool captured = false;  // events owned by a graph being captured
   KTimer(const CtxPtr& ctx, const char* t) : c(ctx.get()), tag(t) {
     if (c->profiling && c->profile_wants(t)) {
-      if (c->capturing) {
-        c->capture_cut(t, 1);
-        cut = true;
-        return;
+      captured = c->capturing;
+      if (captured) {  // an event-record node of the graph (External: not a capture-internal join point)
+        cudaEventCreate(&a);
+        cudaEventRecordWithFlags(a, c->stream, cudaEventRecordExternal);
+      } else {
+        a = c->get_event();
+        cudaEventRecord(a, c->stream);
       }
-      a = c->get_event();
-      cudaEventRecord(a, c->stream);
       if (c->host_profiling) h0 = std::chrono::steady_clock::now();
     }
   }
   ~KTimer() {
-    if (cut) {
-      c->capture_cut(tag, 2);
+    if (a && captured) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecordWithFlags(b, c->stream, cudaEventRecordExternal);
+      c->capture_timers.push_back({tag, a, b});
       return;
     }
     if (a) {
