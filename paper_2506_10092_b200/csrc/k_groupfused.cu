@@ -1663,12 +1663,11 @@ __device__ __forceinline__ uint64_t kw_value_bits(const void* v, int dt, int64_t
 
 __device__ __forceinline__ bool kw_conj(const KwConj& C, int64_t v) {
   if (v < C.lo || v > C.hi) return false;
-  if (C.nset == 0) return true;
-  bool hit = false;
-#pragma unroll
-  for (int t = 0; t < XG_IN; ++t)
-    if (t < C.nset && C.set[t] == v) hit = true;
-  return hit == (C.set_in != 0);
+  // the set's own length bounds the scan (IN (3, 17, 42): three compares,
+  // not XG_IN guarded ones)
+  for (int t = 0; t < C.nset; ++t)
+    if (C.set[t] == v) return C.set_in != 0;
+  return C.set_in == 0;
 }
 
 __device__ __forceinline__ bool kw_pass(const XgPred& P, uint64_t v) {
@@ -1770,8 +1769,10 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __r
 }
 
 // kept candidates → the segment table: each tile's first slot and covered-row
-// offset come from the exclusive scan of the per-tile (count, rows) that
-// k_kway_candidates accumulated (tpre[t], tpre[ntiles + t] - tpre[ntiles]);
+// offset come from the per-tile (count, rows) that k_kway_candidates
+// accumulated — summed over the earlier tiles by the block itself when there
+// are few tiles, else from their exclusive scan (tpre[t], tpre[ntiles + t] -
+// tpre[ntiles]);
 // inside the tile a block scan places every kept fragment, written there
 // (s, e, slot, operand values at stride N, off). The totals stay on the
 // device (dims): nothing is read back before the row kernels run.
@@ -1779,7 +1780,8 @@ template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK)
     k_kway_select(int64_t N, int ncst, const uint8_t* __restrict__ kept, const int64_t* __restrict__ cs,
                   const int64_t* __restrict__ ce, const int64_t* __restrict__ cslot, const uint64_t* __restrict__ ccst,
-                  const int64_t* __restrict__ tpre, int64_t ntiles, int64_t* __restrict__ s, int64_t* __restrict__ e,
+                  const int64_t* __restrict__ tpre, const int64_t* __restrict__ tagg, int64_t ntiles,
+                  int64_t* __restrict__ s, int64_t* __restrict__ e,
                   int64_t* __restrict__ slot, uint64_t* __restrict__ cst, int64_t* __restrict__ off,
                   const int64_t* __restrict__ dims, int64_t nwarps, int64_t* __restrict__ cstart) {
   static_assert(BLOCK * ITEMS == KW_TILE, "tile of the per-tile aggregates");
@@ -1798,9 +1800,27 @@ __global__ void __launch_bounds__(BLOCK)
   uint64_t tn, tr;
   uint64_t on = block_exclusive<BLOCK>(cn, tn, wn);
   uint64_t orow = block_exclusive<BLOCK>(cr, tr, wr);
+  __shared__ uint64_t base_n, base_r;
+  if (!tpre) {  // few tiles: this tile's prefix is the sum of the earlier tiles' aggregates
+    uint64_t pn = 0, pr = 0;
+    for (int64_t q = threadIdx.x; q < blockIdx.x; q += BLOCK) {
+      pn += static_cast<uint64_t>(ldg64(tagg, q));
+      pr += static_cast<uint64_t>(ldg64(tagg, ntiles + q));
+    }
+    pn = block_sum<BLOCK>(pn, wn);
+    pr = block_sum<BLOCK>(pr, wr);
+    if (threadIdx.x == 0) {
+      base_n = pn;
+      base_r = pr;
+    }
+  } else if (threadIdx.x == 0) {
+    base_n = static_cast<uint64_t>(ldg64(tpre, blockIdx.x));
+    base_r = static_cast<uint64_t>(ldg64(tpre, ntiles + blockIdx.x) - ldg64(tpre, ntiles));
+  }
+  __syncthreads();
   if (!cn) return;
-  on += static_cast<uint64_t>(ldg64(tpre, blockIdx.x));
-  orow += static_cast<uint64_t>(ldg64(tpre, ntiles + blockIdx.x) - ldg64(tpre, ntiles));
+  on += base_n;
+  orow += base_r;
   const int64_t chunk = xg_chunk(ldg64(dims, 1), nwarps);  // the row kernels' chunk (same formula)
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
@@ -1941,9 +1961,13 @@ bool key_layout(const CtxPtr& ctx, const std::vector<const DCol*>& keys, GroupKe
 const DCol::RankDir& rank_dir(const CtxPtr& ctx, const DArr& a, int64_t total, DCol::RankDir& d) {
   if (d.shift >= 0 || a.n == 0 || total <= 0) return d;
   const int64_t avg = std::max<int64_t>(1, total / a.n);
-  int sh = 0;  // floor(log2(avg)) + 2: a block spans 4-8 average gaps
+  static const int extra = [] {  // RQ_DIR_SHIFT (A/B): log2 of average gaps per block
+    const char* e = std::getenv("RQ_DIR_SHIFT");
+    return e ? std::atoi(e) : 2;
+  }();
+  int sh = 0;  // floor(log2(avg)) + extra: a block spans 2^extra .. 2^(extra+1) average gaps
   while (sh < 38 && (int64_t{1} << (sh + 1)) <= avg) ++sh;
-  sh += 2;
+  sh = std::max(0, sh + extra);
   d.nb = ((total - 1) >> sh) + 1;
   d.dir = alloc_arr(ctx, RQ_I64, d.nb + 1);
   dev::k_rank_dir<<<grid_cap(ctx, a.n + 1), 256, 0, ctx->stream>>>(a.pos(), a.n, sh, d.nb, d.dir.as<int64_t>());
@@ -2185,12 +2209,13 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
       KP, kept, cs.as<int64_t>(), ce.as<int64_t>(), cslot.as<int64_t>(), ccst.as<uint64_t>(),
       dims.as<unsigned long long>(), tagg, ntiles);
   launched(ctx);
-  DArr tv = zero;  // the aggregates (the buffer's head), then their exclusive scan
+  DArr tv = zero;  // the aggregates (the buffer's head), then — many tiles — their exclusive scan
   tv.n = 2 * ntiles;
   DArr tpre;
-  scan_exclusive_i64(ctx, tv, tpre);
+  if (ntiles > 2048) scan_exclusive_i64(ctx, tv, tpre);
   dev::k_kway_select<B, IT><<<static_cast<unsigned>(ntiles), B, 0, ctx->stream>>>(
-      N, ncst, kept, cs.pos(), ce.pos(), cslot.pos(), ccst.as<uint64_t>(), tpre.pos(), ntiles, s.as<int64_t>(),
+      N, ncst, kept, cs.pos(), ce.pos(), cslot.pos(), ccst.as<uint64_t>(), tpre.n ? tpre.pos() : nullptr,
+      tv.pos(), ntiles, s.as<int64_t>(),
       e.as<int64_t>(), slot.as<int64_t>(), cst_all.as<uint64_t>(), off.as<int64_t>(), dims.pos(), nwarps,
       cstart.as<int64_t>());
   launched(ctx);
