@@ -407,6 +407,11 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     int64_t jb = 0, b_lo = 0;
     int b_est = BW, b_n = 0;
     int hw0 = BW + 8, hw1 = BW + 8;  // per stage: entries [hw, BW + 8) still hold the pad
+    // start-up search inputs loaded together: the end before the CTA's first
+    // A run and B's last end (interpolation round of warp_lower_bound_pair)
+    const int64_t a_first = t_begin * static_cast<int64_t>(ta);
+    const int64_t r_lo0 = t_begin < t_end && a_first > 0 ? ldg64(Ae, a_first - 1) : -1;
+    const int64_t b_last = nb > 0 ? ldg64(Be, nb - 1) : -1;
     for (int64_t t = t_begin; t < t_end; ++t) {
       const int st = static_cast<int>((t - t_begin) & 1);
       const uint32_t use = static_cast<uint32_t>((t - t_begin) >> 1);
@@ -437,8 +442,8 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
       }
       // (2) the other list's window: chained from tile t-1's landed window
       if (t == t_begin) {
-        const int64_t r_lo = a0 > 0 ? ldg64(Ae, a0 - 1) : -1;
-        jb = warp_lower_bound(Be, nb, r_lo + 1);
+        int64_t unused;
+        warp_lower_bound_pair(Be, nb, b_last, r_lo0 + 1, nullptr, 0, -1, 0, jb, unused);
       } else {
         mbar_wait(&full[st ^ 1], ((t - 1 - t_begin) >> 1) & 1);  // tile t-1 landed
         const int pst = st ^ 1;

@@ -588,6 +588,9 @@ __global__ void __launch_bounds__(BLOCK, 4)
     for (int i = 0; i < NS; ++i) hwA[i] = AW + 8, hwC[i] = CW + 8;
     int a_est = AW, c_est = CW, a_n = 0, c_n = 0;
     int64_t pf = t_begin < t_end ? ldg64(P, t_begin * TILE) : 0;
+    // last run ends (interpolation round of the start-up search), loaded beside pf
+    const int64_t a_last = x.n > 0 ? ldg64(x.e, x.n - 1) : -1;
+    const int64_t c_last = HAS_C && c.n > 0 ? ldg64(c.e, c.n - 1) : -1;
     for (int64_t t = t_begin; t < t_end; ++t) {
       const int st = static_cast<int>((t - t_begin) % NS);
       const uint32_t use = static_cast<uint32_t>((t - t_begin) / NS);
@@ -595,8 +598,8 @@ __global__ void __launch_bounds__(BLOCK, 4)
       const int64_t p_first = pf;
       if (t + 1 < t_end) pf = ldg64(P, (t + 1) * TILE);
       if (t == t_begin) {
-        a_cur = warp_lower_bound(x.e, x.n, p_first);
-        if (HAS_C) c_cur = warp_lower_bound(c.e, c.n, p_first);
+        warp_lower_bound_pair(x.e, x.n, a_last, p_first, HAS_C ? c.e : nullptr, HAS_C ? c.n : 0, c_last,
+                              p_first, a_cur, c_cur);
       } else {
         mbar_wait(&full[pst], ((t - 1 - t_begin) / NS) & 1);  // tile t-1 landed
         const int ra = smem_lb_pow2<AW>(sA(pst), AW, p_first);
