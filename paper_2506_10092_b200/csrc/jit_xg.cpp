@@ -501,6 +501,28 @@ void plan_literals(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vector<d
   }
 }
 
+// Row-kernel CTAs per SM, the grid its covered-row chunks are cut for (the
+// k-way segment table's chunk-start entries use the same count), always a
+// whole number of waves of resident CTAs: plans of short segments run ONE
+// wave (Q6 row kernel 36.4 -> 29.5 µs, C5 37.5 -> 33.4 µs; 2 waves of small
+// chunks paid a segment-bound start-up per chunk), long-segment plans 4 waves
+// of 3 (Q1 1.198 -> 1.181 ms, C3 2.14 -> 2.07 ms against the former 8 = 2.67
+// waves; profiles/r2_ab_bps.txt). RQ_XG_BPS overrides.
+int xg_row_blocks_per_sm(int64_t avg_len) {
+  static const int env = [] {
+    const char* e = std::getenv("RQ_XG_BPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0) return env;
+  static const int64_t pf_min = [] {
+    const char* e = std::getenv("RQ_JIT_PF_MIN");
+    return e ? std::atoll(e) : int64_t{2048};
+  }();
+  if (avg_len >= pf_min) return 12;  // the long-segment kernel keeps 3 CTAs per SM
+  const char* mb = std::getenv("RQ_JIT_MINB");
+  return mb && std::atoi(mb) > 0 ? std::atoi(mb) : 4;  // = the short-segment kernel's resident CTAs
+}
+
 bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S, int64_t chunk,
                    unsigned long long* tab, int64_t G, int* err, unsigned blocks, int64_t avg_len) {
   std::vector<int64_t> ki;

@@ -537,8 +537,8 @@ __device__ __forceinline__ void load_keys(const int64_t* __restrict__ P, int64_t
   }
 }
 
-template <int BLOCK, int ITEMS, int AW, int CW, int NS, class T, int OP, int CK, bool SAME>
-__global__ void __launch_bounds__(BLOCK, 4)
+template <int BLOCK, int ITEMS, int AW, int CW, int NS, class T, int OP, int CK, bool SAME, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
     k_points_filtered_reduce_tma(const int64_t* __restrict__ P, const void* __restrict__ yv, int ydt,
                                  int64_t np, XSpec x, CSpec c, int64_t ntiles, int swap,
                                  AggPart* __restrict__ parts, unsigned* __restrict__ ticket,
@@ -871,7 +871,28 @@ void launch1(int op, int ck, const CtxPtr& ctx, const FusedLaunch& f) {
 }
 
 // ---- persistent TMA path ----
-constexpr int TB = 256, TI = 4, TAW = 2048, TCW = 512, TNS = 2;  // 3 stages measured slower (3 CTAs/SM)
+// (overridable at build time for A/B sweeps: -DRQ_C2_TB=… etc.)
+#ifndef RQ_C2_TB
+#define RQ_C2_TB 256
+#endif
+#ifndef RQ_C2_TI
+#define RQ_C2_TI 4
+#endif
+#ifndef RQ_C2_TAW
+#define RQ_C2_TAW 2048
+#endif
+#ifndef RQ_C2_TCW
+#define RQ_C2_TCW 512
+#endif
+#ifndef RQ_C2_TNS
+#define RQ_C2_TNS 2
+#endif
+#ifndef RQ_C2_MINB
+#define RQ_C2_MINB 4
+#endif
+constexpr int TB = RQ_C2_TB, TI = RQ_C2_TI, TAW = RQ_C2_TAW, TCW = RQ_C2_TCW;
+constexpr int TNS = RQ_C2_TNS;  // 3 stages measured slower (3 CTAs/SM)
+constexpr int TMINB = RQ_C2_MINB;
 using TmaSmem = dev::C2Stage<TAW, TCW>;
 constexpr size_t TMA_SMEM = TNS * TmaSmem::BYTES;
 
@@ -892,8 +913,8 @@ template <class T, int OP, int CK>
 int64_t launch_tma3(const CtxPtr& ctx, const TmaLaunch& f, bool dry) {
   const int32_t tdt = std::is_same<T, double>::value ? RQ_F64 : RQ_I64;
   const bool same = f.xs.dt == tdt && f.y->v.dt == tdt;
-  auto k_same = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, true>;
-  auto k_gen = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, false>;
+  auto k_same = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, true, TMINB>;
+  auto k_gen = dev::k_points_filtered_reduce_tma<TB, TI, TAW, TCW, TNS, T, OP, CK, false, TMINB>;
   const int occ = kernel_occupancy(ctx, same ? k_same : k_gen, TB, TMA_SMEM);
   int64_t grid = static_cast<int64_t>(ctx->sm_count) * occ;
   if (grid > f.ntiles) grid = f.ntiles;

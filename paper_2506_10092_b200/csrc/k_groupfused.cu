@@ -2192,7 +2192,8 @@ bool kway_segments(const CtxPtr& ctx, const std::vector<const DCol*>& keys, cons
   slot = alloc_arr(ctx, RQ_I64, N);
   off = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N));
   cst_all = alloc_arr(ctx, RQ_I64, std::max<int64_t>(1, N * ncst));
-  const int64_t nwarps = static_cast<int64_t>(ctx->sm_count) * 8 * 8;  // the row kernels' grid (xg_fused)
+  // the row kernels' grid (xg_fused: same average-length estimate, total / capacity)
+  const int64_t nwarps = static_cast<int64_t>(ctx->sm_count) * xg_row_blocks_per_sm(total / std::max<int64_t>(1, N)) * 8;
   cstart = alloc_arr(ctx, RQ_I64, nwarps + 1);
   cap = N;
   if (N == 0) return true;
@@ -2663,7 +2664,8 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
     stage.reset();
     if (any_rows && (kway ? nseg > 0 : ncov > 0)) {
       constexpr int B = 256;
-      const int64_t warps = static_cast<int64_t>(ctx->sm_count) * 8 * (B / 32);
+      const int bps = xg_row_blocks_per_sm(avg_len);
+      const int64_t warps = static_cast<int64_t>(ctx->sm_count) * bps * (B / 32);
       // chunk 0: the kernel derives it from the device-side row count (same formula)
       const int64_t chunk = kway ? 0 : dev::xg_chunk(ncov, warps);
       // f64 row sums: per-chunk partial tables + a fixed-order fold, so two runs
@@ -2679,8 +2681,8 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
         S.dcells = cells;
         dchunks = nchunks;
       }
-      const int64_t blocks = kway ? static_cast<int64_t>(ctx->sm_count) * 8
-                                  : std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * 8,
+      const int64_t blocks = kway ? static_cast<int64_t>(ctx->sm_count) * bps
+                                  : std::min<int64_t>(static_cast<int64_t>(ctx->sm_count) * bps,
                                                       (ncov / chunk + (B / 32)) / (B / 32) + 1);
       constexpr size_t smem = dev::xg_rows_smem<B>();
       kernel_occupancy(ctx, dev::k_xg_rows<B>, B, smem);  // shared-memory opt-in on this device

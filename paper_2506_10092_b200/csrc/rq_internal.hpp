@@ -584,6 +584,7 @@ struct XgSegs;
 }  // namespace dev
 // jit_xg.cpp: run-time specialised K12 row kernel (NVRTC)
 bool xg_jit_available();
+int xg_row_blocks_per_sm(int64_t avg_len);
 bool xg_jit_launch(const CtxPtr& ctx, const dev::XgPlan& P, const dev::XgSegs& S, int64_t chunk,
                    unsigned long long* tab, int64_t G, int* err, unsigned blocks, int64_t avg_len);
 // WHERE conjunct for the pushdown form: `col op k`, or `col IN (in)` when
