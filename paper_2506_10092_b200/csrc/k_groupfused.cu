@@ -1700,6 +1700,12 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __r
                                   unsigned long long* __restrict__ dims, unsigned long long* __restrict__ tagg,
                                   int64_t ntiles) {
   const int64_t N = K.start[K.nl];
+  // (segments, covered rows) summed per block in shared memory, one global
+  // atomic pair per block: every warp's pair on the same two addresses
+  // serialised in L2
+  __shared__ unsigned long long s_dims[2];
+  if (threadIdx.x < 2) s_dims[threadIdx.x] = 0;
+  __syncthreads();
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < N;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int j = 0;
@@ -1753,8 +1759,8 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __r
         __reduce_add_sync(act, static_cast<unsigned>(len & 0xfffffu)) +
         (static_cast<unsigned long long>(__reduce_add_sync(act, static_cast<unsigned>(len >> 20))) << 20);
     if ((threadIdx.x & 31) == __ffs(act) - 1) {
-      atomicAdd(dims, static_cast<unsigned long long>(__popc(act)));
-      atomicAdd(dims + 1, wl);
+      atomicAdd(&s_dims[0], static_cast<unsigned long long>(__popc(act)));
+      atomicAdd(&s_dims[1], wl);
     }
     const int64_t tile = rank / KW_TILE;
     const unsigned peers = __match_any_sync(act, static_cast<unsigned long long>(tile));
@@ -1766,6 +1772,8 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __r
       atomicAdd(tagg + ntiles + tile, tl);
     }
   }
+  __syncthreads();
+  if (threadIdx.x < 2 && s_dims[threadIdx.x]) atomicAdd(dims + threadIdx.x, s_dims[threadIdx.x]);
 }
 
 // kept candidates → the segment table: each tile's first slot and covered-row
