@@ -1784,8 +1784,21 @@ __global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __r
 // inside the tile a block scan places every kept fragment, written there
 // (s, e, slot, operand values at stride N, off). The totals stay on the
 // device (dims): nothing is read back before the row kernels run.
+// floor(a / b) for 0 <= a < 2^53, b > 0, without the 64-bit division
+// sequence (~70 instructions): the double quotient is within one of the
+// answer, one correction step each way
+__device__ __forceinline__ int64_t div_floor_pos(int64_t a, int64_t b, double inv_b) {
+  int64_t q = static_cast<int64_t>(static_cast<double>(a) * inv_b);
+  if (q * b > a) --q;
+  else if ((q + 1) * b <= a) ++q;
+  return q;
+}
+
+// 5 resident CTAs per SM (<= 51 registers): the placement of a k-way table
+// of up to 740 tiles runs in one wave (Q6: 684 tiles, C5: 458; at 72
+// registers only 3 fitted and both ran a second, nearly empty wave)
 template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, 5)
     k_kway_select(int64_t N, int ncst, const uint8_t* __restrict__ kept, const int64_t* __restrict__ cs,
                   const int64_t* __restrict__ ce, const int64_t* __restrict__ cslot, const uint64_t* __restrict__ ccst,
                   const int64_t* __restrict__ tpre, const int64_t* __restrict__ tagg, int64_t ntiles,
@@ -1795,15 +1808,15 @@ __global__ void __launch_bounds__(BLOCK)
   static_assert(BLOCK * ITEMS == KW_TILE, "tile of the per-tile aggregates");
   __shared__ uint64_t wn[BLOCK / 32 + 1], wr[BLOCK / 32 + 1];
   const int64_t base = (static_cast<int64_t>(blockIdx.x) * BLOCK + threadIdx.x) * ITEMS;
-  uint64_t len[ITEMS];
+  unsigned keep = 0;  // kept items as bits (lengths re-derived from the reloaded s / e below)
   uint64_t cn = 0, cr = 0;
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
     const int64_t i = base + k;
     const bool kk = i < N && kept[i];
-    len[k] = kk ? static_cast<uint64_t>(ldg64(ce, i) - ldg64(cs, i) + 1) : 0;
+    keep |= kk ? 1u << k : 0u;
     cn += kk;
-    cr += len[k];
+    cr += kk ? static_cast<uint64_t>(ldg64(ce, i) - ldg64(cs, i) + 1) : 0;
   }
   uint64_t tn, tr;
   uint64_t on = block_exclusive<BLOCK>(cn, tn, wn);
@@ -1830,20 +1843,24 @@ __global__ void __launch_bounds__(BLOCK)
   on += base_n;
   orow += base_r;
   const int64_t chunk = xg_chunk(ldg64(dims, 1), nwarps);  // the row kernels' chunk (same formula)
+  const double inv_chunk = 1.0 / static_cast<double>(chunk);
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
-    if (!len[k]) continue;
+    if (!((keep >> k) & 1u)) continue;
     const int64_t i = base + k, o = static_cast<int64_t>(on);
-    s[o] = ldg64(cs, i);
-    e[o] = ldg64(ce, i);
+    const int64_t si = ldg64(cs, i), ei = ldg64(ce, i);
+    const uint64_t len = static_cast<uint64_t>(ei - si + 1);
+    s[o] = si;
+    e[o] = ei;
     slot[o] = ldg64(cslot, i);
     for (int j = 0; j < ncst; ++j) cst[static_cast<int64_t>(j) * N + o] = __ldg(ccst + static_cast<int64_t>(j) * N + i);
     off[o] = static_cast<int64_t>(orow);
     // the row chunks whose first covered row falls in this segment start here
-    const int64_t r0 = static_cast<int64_t>(orow), r1 = r0 + static_cast<int64_t>(len[k]) - 1;
-    for (int64_t q = (r0 + chunk - 1) / chunk; q <= r1 / chunk; ++q) cstart[q] = o;
+    const int64_t r0 = static_cast<int64_t>(orow), r1 = r0 + static_cast<int64_t>(len) - 1;
+    const int64_t q1 = div_floor_pos(r1, chunk, inv_chunk);
+    for (int64_t q = div_floor_pos(r0 + chunk - 1, chunk, inv_chunk); q <= q1; ++q) cstart[q] = o;
     ++on;
-    orow += len[k];
+    orow += len;
   }
 }
 
