@@ -1694,7 +1694,15 @@ __device__ __forceinline__ bool kw_own(const KwPlan& K, int l, uint64_t v) {
 // lists); a kept one writes its fragment at its merged rank and adds to the
 // (segments, covered rows) counters.
 constexpr int KW_TILE = 2048;  // k_kway_select's tile (256 threads x 8 candidates)
-__global__ void k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __restrict__ kept,
+// 8 resident CTAs per SM (32 registers, the per-list run indices partly in
+// local memory): the pass is a set of dependent search chains, so warps in
+// flight beat registers — C5 0.221 -> 0.206 ms per query against the
+// compiler's 64-register / 4-CTA choice, Q6 unchanged
+// (profiles/r2b_ab_kway_candidates.txt; 5 and 6 CTAs in between)
+#ifndef RQ_KW_MINB
+#define RQ_KW_MINB 8
+#endif
+__global__ void __launch_bounds__(256, RQ_KW_MINB) k_kway_candidates(const __grid_constant__ KwPlan K, uint8_t* __restrict__ kept,
                                   int64_t* __restrict__ seg_s, int64_t* __restrict__ seg_e,
                                   int64_t* __restrict__ seg_slot, uint64_t* __restrict__ seg_cst,
                                   unsigned long long* __restrict__ dims, unsigned long long* __restrict__ tagg,
