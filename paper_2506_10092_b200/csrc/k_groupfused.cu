@@ -1443,6 +1443,61 @@ __global__ void k_xg_finish_all(const __grid_constant__ XgFinish F, const int64_
   }
 }
 
+// The keyed output stage in ONE block (tables of up to XG_TAIL_MAX slots):
+// present slots (count > 0) ranked by a block scan over contiguous slot
+// ranges, keys decoded from the slot (ascending slot = ascending key) and
+// every expression's result written at the slot's rank, the group count into
+// *ng. Replaces flags → select (size readback) → keys → finish: the host
+// reads the count once, after all the work is queued.
+constexpr int XG_TAIL_B = 1024;
+constexpr int64_t XG_TAIL_MAX = 32768;
+struct XgTailKeys {
+  int nk;
+  int dt[8];
+  int64_t kmin[8], stride[8], range[8];
+  void* out[8];
+};
+__global__ void __launch_bounds__(XG_TAIL_B)
+    k_xg_tail(const __grid_constant__ XgFinish F, const __grid_constant__ XgTailKeys KT, int64_t G,
+              const unsigned long long* __restrict__ tab, const unsigned long long* __restrict__ cnt,
+              int64_t* __restrict__ ng) {
+  __shared__ int64_t wt[XG_TAIL_B / 32 + 1];
+  const int64_t per = (G + XG_TAIL_B - 1) / XG_TAIL_B;
+  const int64_t g0 = min(G, threadIdx.x * per), g1 = min(G, g0 + per);
+  int64_t mine = 0;
+  for (int64_t g = g0; g < g1; ++g) mine += cnt[g] > 0;
+  int64_t total;
+  int64_t i = block_exclusive<XG_TAIL_B>(mine, total, wt);
+  if (threadIdx.x == 0) *ng = total;
+  for (int64_t g = g0; g < g1; ++g) {
+    const unsigned long long c = cnt[g];
+    if (!c) continue;
+    for (int k = 0; k < KT.nk; ++k) {
+      const int64_t key = KT.kmin[k] + (g / KT.stride[k]) % KT.range[k];
+      switch (KT.dt[k]) {
+        case RQ_I8: static_cast<int8_t*>(KT.out[k])[i] = static_cast<int8_t>(key); break;
+        case RQ_I16: static_cast<int16_t*>(KT.out[k])[i] = static_cast<int16_t>(key); break;
+        case RQ_I32: static_cast<int32_t*>(KT.out[k])[i] = static_cast<int32_t>(key); break;
+        default: static_cast<int64_t*>(KT.out[k])[i] = key; break;
+      }
+    }
+    for (int ei = 0; ei < F.ne; ++ei) {  // k_xg_finish_all's conventions (groupby.cpp:67-135)
+      const int fn = F.fn[ei];
+      if (fn == RQ_COUNT) {
+        static_cast<long long*>(F.out[ei])[i] = static_cast<long long>(c);
+      } else if (fn == RQ_AVG) {
+        const unsigned long long t = tab[g * F.ne + ei];
+        const double sum = F.isf[ei] ? __longlong_as_double(static_cast<long long>(t))
+                                     : static_cast<double>(static_cast<long long>(t));
+        static_cast<double*>(F.out[ei])[i] = sum / static_cast<double>(c);
+      } else {
+        static_cast<unsigned long long*>(F.out[ei])[i] = tab[g * F.ne + ei];
+      }
+    }
+    ++i;
+  }
+}
+
 // deterministic f64 fold: cell blockIdx.x of every chunk's partial table,
 // a fixed strided split over the block's threads and a fixed-shape tree
 struct XgIsF {
@@ -2771,6 +2826,47 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
   }
   // ---- outputs: present slots ascending (= ascending keys) ----
   auto stage = std::make_unique<KTimer>(ctx, "xg_out");
+  static const bool no_tail = std::getenv("RQ_XG_NO_TAIL") != nullptr;  // A/B knob: the multi-launch tail
+  if (!keys.empty() && keys.size() <= 8 && G <= dev::XG_TAIL_MAX && !no_tail) {
+    dev::XgTailKeys KT{};
+    KT.nk = static_cast<int>(keys.size());
+    for (size_t c = 0; c < keys.size(); ++c) {
+      DArr kout = alloc_arr(ctx, K.kdt[c], G);  // capacity: every slot present
+      KT.dt[c] = K.kdt[c];
+      KT.kmin[c] = K.kmin[c];
+      KT.stride[c] = K.stride[c];
+      KT.range[c] = K.range[c];
+      KT.out[c] = kout.raw_mut();
+      out.keys.push_back(kout);
+    }
+    dev::XgFinish F{};
+    F.ne = P.ne;
+    for (int i = 0; i < P.ne; ++i) {
+      const int fn = fns[static_cast<size_t>(i)];
+      const int32_t odt = fn == RQ_COUNT ? RQ_I64 : (fn == RQ_AVG || P.e[i].res_f) ? RQ_F64 : RQ_I64;
+      DArr res = alloc_arr(ctx, odt, G);
+      F.fn[i] = fn;
+      F.isf[i] = P.e[i].acc_f;
+      F.out[i] = res.raw_mut();
+      out.vals.push_back(res);
+    }
+    DArr ngd = alloc_arr(ctx, RQ_I64, 1);
+    dev::k_xg_tail<<<1, dev::XG_TAIL_B, 0, ctx->stream>>>(F, KT, G, reinterpret_cast<const unsigned long long*>(tab.raw()),
+                                                          reinterpret_cast<const unsigned long long*>(cnt.raw()),
+                                                          ngd.as<int64_t>());
+    launched(ctx);
+    const int64_t ng = ctx->readback(ngd.raw(), 8)[0];
+    out.n_groups = ng;
+    for (auto& a : out.keys) {
+      a.n = ng;
+      if (ng == 0) a.buf.reset();
+    }
+    for (auto& a : out.vals) {
+      a.n = ng;
+      if (ng == 0) a.buf.reset();
+    }
+    return true;
+  }
   DArr present;
   if (keys.empty()) {
     present.n = 1;  // one group (slot 0): finish reads no slot list
