@@ -139,8 +139,49 @@ std::string wrap(int logical, const std::string& x) {
   }
 }
 
-// loads + decode of column c for the lane's ROWS rows into x<c>_<u>
-void gen_load(std::ostringstream& o, int c, const dev::PlainSrc& s) {
+// the vector type and count of column c's raw loads for the lane's ROWS rows
+struct RawLoad {
+  const char* vt;  // vector type
+  const char* et;  // element pointer type
+  int n;           // loads (16-B or 8-B vectors)
+};
+RawLoad raw_load(int dt) {
+  switch (dt) {
+    case RQ_I8: return {"uint2", "signed char", 1};
+    case RQ_I16: return {"uint4", "short", 1};
+    case RQ_I32: return {"int4", "int", 2};
+    case RQ_F32: return {"float4", "float", 2};
+    case RQ_F64: return {"double2", "double", 4};
+    default: return {"longlong2", "i64", 4};
+  }
+}
+std::string wname(int c, int dt, int q) {
+  const RawLoad L = raw_load(dt);
+  return L.n == 1 ? "w" + std::to_string(c) : "w" + std::to_string(c) + "_" + std::to_string(q);
+}
+
+// raw vector loads of column c at row `rowv` into w<c>[_q]<suffix>; with a
+// guard, a lane past the window's end loads nothing (zero vectors)
+void gen_raw_loads(std::ostringstream& o, int c, const dev::PlainSrc& s, const std::string& rowv,
+                   const std::string& suffix, const std::string& guard) {
+  const RawLoad L = raw_load(s.dt);
+  for (int q = 0; q < L.n; ++q) {
+    const std::string ld = std::string("__ldg((const ") + L.vt + "*)((const " + L.et + "*)c" + std::to_string(c) +
+                           ".v + " + rowv + ")" + (L.n == 1 ? "" : " + " + std::to_string(q)) + ")";
+    o << "    const " << L.vt << " " << wname(c, s.dt, q) << suffix << " = "
+      << (guard.empty() ? ld : "(" + guard + ") ? " + ld + " : " + L.vt + "{}") << ";\n";
+  }
+}
+
+// w<c>[_q] = w<c>[_q]<suffix> (the window's loads under the names the decode uses)
+void gen_alias(std::ostringstream& o, int c, const dev::PlainSrc& s, const std::string& suffix) {
+  const RawLoad L = raw_load(s.dt);
+  for (int q = 0; q < L.n; ++q)
+    o << "    const " << L.vt << " " << wname(c, s.dt, q) << " = " << wname(c, s.dt, q) << suffix << ";\n";
+}
+
+// decode of column c's loaded vectors into x<c>_<u>
+void gen_decode(std::ostringstream& o, int c, const dev::PlainSrc& s) {
   const std::string p = "c" + std::to_string(c);
   auto raw = [&](int u) -> std::string {
     switch (s.dt) {
@@ -155,33 +196,6 @@ void gen_load(std::ostringstream& o, int c, const dev::PlainSrc& s) {
       default: return std::string("w") + std::to_string(c) + "_" + std::to_string(u / 2) + (u % 2 ? ".y" : ".x");
     }
   };
-  switch (s.dt) {
-    case RQ_I8:
-      o << "    const uint2 w" << c << " = __ldg((const uint2*)((const signed char*)" << p << ".v + row));\n";
-      break;
-    case RQ_I16:
-      o << "    const uint4 w" << c << " = __ldg((const uint4*)((const short*)" << p << ".v + row));\n";
-      break;
-    case RQ_I32:
-      for (int q = 0; q < 2; ++q)
-        o << "    const int4 w" << c << "_" << q << " = __ldg((const int4*)((const int*)" << p << ".v + row) + " << q
-          << ");\n";
-      break;
-    case RQ_F32:
-      for (int q = 0; q < 2; ++q)
-        o << "    const float4 w" << c << "_" << q << " = __ldg((const float4*)((const float*)" << p << ".v + row) + "
-          << q << ");\n";
-      break;
-    case RQ_F64:
-      for (int q = 0; q < 4; ++q)
-        o << "    const double2 w" << c << "_" << q << " = __ldg((const double2*)((const double*)" << p
-          << ".v + row) + " << q << ");\n";
-      break;
-    default:
-      for (int q = 0; q < 4; ++q)
-        o << "    const longlong2 w" << c << "_" << q << " = __ldg((const longlong2*)((const i64*)" << p
-          << ".v + row) + " << q << ");\n";
-  }
   const bool fstore = s.dt == RQ_F32 || s.dt == RQ_F64;
   for (int u = 0; u < ROWS; ++u) {
     std::string v = raw(u);
@@ -195,6 +209,18 @@ void gen_load(std::ostringstream& o, int c, const dev::PlainSrc& s) {
     }
     o << "    const " << ty(s.flt) << " x" << c << "_" << u << " = " << v << ";\n";
   }
+}
+
+// windows of 32 x ROWS rows a short-segment row loop loads before it
+// computes (RQ_JIT_UNROLL=2: both windows' loads issued first). Measured
+// slower at the 64-register cap — Q6's row kernel 31 -> 35 µs, C5's 34 ->
+// 36 µs (profiles/r2b_ab_jit_unroll.txt) — so one window per trip stays.
+int window_unroll() {
+  static const int u = [] {
+    const char* e = std::getenv("RQ_JIT_UNROLL");
+    return e && std::atoi(e) == 2 ? 2 : 1;
+  }();
+  return u;
 }
 
 // windows ahead the row loop prefetches into L2 (RQ_JIT_PF, default 1; 0 = off;
@@ -245,6 +271,7 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
   // short segments (no L2 prefetch): the next segment's bounds are loaded
   // while this one's rows stream, so a segment costs one round trip, not two
   const bool pipe = pf == 0 && pipeline_segments();
+  const int unroll = pf == 0 ? window_unroll() : 1;  // long segments: the L2 prefetch instead
   if (pipe)
     o << "    i64 off = ldg64(S.off, k), s = ldg64(S.s, k), e = ldg64(S.e, k), slot = ldg64(S.slot, k);\n"
          "    while (c < c1_) {\n"
@@ -263,7 +290,7 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
   }
   o << "      const i64 r0 = s + (c - off);\n"
        "      const i64 r1 = min(e, s + (c1_ - off) - 1);\n"
-       "      for (i64 b = r0 & ~(i64)" << (ROWS - 1) << "; b <= r1; b += " << 32 * ROWS << ") {\n";
+       "      for (i64 b = r0 & ~(i64)" << (ROWS - 1) << "; b <= r1; b += " << 32 * ROWS * unroll << ") {\n";
   // L2 prefetch of the window PF windows ahead, one 128-B line per lane and
   // column: more bytes in flight per warp without holding them in registers
   if (pf > 0 && P.nc > 0) {
@@ -278,12 +305,6 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
     }
     o << "          }\n        }\n";
   }
-  o << "        const i64 row = b + lane * " << ROWS << ";\n"
-       "        if (row > r1) continue;\n";
-  // loads
-  std::ostringstream ld;
-  for (int c = 0; c < P.nc; ++c) gen_load(ld, c, P.col[c]);
-  o << ld.str();
   // expression values per row, then the accumulation (guarded form for partial windows)
   auto lit = [&](const dev::XgTerm& t) -> std::string {
     if (t.kflt) {
@@ -299,6 +320,9 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
     if (!X.rows) continue;
     for (int t = 0; t < X.nt; ++t) lits[static_cast<size_t>(e)].push_back(X.t[t].sop >= 0 ? lit(X.t[t]) : "");
   }
+  // one window's decode + expressions + accumulation at `row` (loads named w<c>[_q])
+  std::ostringstream body;
+  for (int c = 0; c < P.nc; ++c) gen_decode(body, c, P.col[c]);
   for (int e = 0; e < P.ne; ++e) {
     const dev::XgExpr& X = P.e[e];
     if (!X.rows) continue;
@@ -324,25 +348,43 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
           vf = vf || xf;
         }
       }
-      o << "        const " << ty(vf) << " v" << e << "_" << u << " = " << v << ";\n";
+      body << "        const " << ty(vf) << " v" << e << "_" << u << " = " << v << ";\n";
     }
   }
-  o << "        if (row >= r0 && row + " << ROWS - 1 << " <= r1) {\n";
+  body << "        if (row >= r0 && row + " << ROWS - 1 << " <= r1) {\n";
   for (int e = 0; e < P.ne; ++e) {
     const dev::XgExpr& X = P.e[e];
     if (!X.rows) continue;
     for (int u = 0; u < ROWS; ++u)
-      o << "          a" << e << " += " << (X.acc_f ? "(double)" : "(u64)") << "v" << e << "_" << u << ";\n";
+      body << "          a" << e << " += " << (X.acc_f ? "(double)" : "(u64)") << "v" << e << "_" << u << ";\n";
   }
-  o << "        } else {\n";
+  body << "        } else {\n";
   for (int e = 0; e < P.ne; ++e) {
     const dev::XgExpr& X = P.e[e];
     if (!X.rows) continue;
     for (int u = 0; u < ROWS; ++u)
-      o << "          if (row + " << u << " >= r0 && row + " << u << " <= r1) a" << e << " += "
-        << (X.acc_f ? "(double)" : "(u64)") << "v" << e << "_" << u << ";\n";
+      body << "          if (row + " << u << " >= r0 && row + " << u << " <= r1) a" << e << " += "
+           << (X.acc_f ? "(double)" : "(u64)") << "v" << e << "_" << u << ";\n";
   }
-  o << "        }\n      }\n";
+  body << "        }\n";
+  if (unroll == 1) {
+    o << "        const i64 row = b + lane * " << ROWS << ";\n"
+         "        if (row > r1) continue;\n";
+    for (int c = 0; c < P.nc; ++c) gen_raw_loads(o, c, P.col[c], "row", "", "");
+    o << body.str() << "      }\n";
+  } else {
+    // both windows' loads issued before either is used: two round trips in
+    // flight per warp on segments of a few hundred rows
+    o << "        const i64 rw0_ = b + lane * " << ROWS << ", rw1_ = rw0_ + " << 32 * ROWS << ";\n";
+    for (int c = 0; c < P.nc; ++c) gen_raw_loads(o, c, P.col[c], "rw0_", "_A", "rw0_ <= r1");
+    for (int c = 0; c < P.nc; ++c) gen_raw_loads(o, c, P.col[c], "rw1_", "_B", "rw1_ <= r1");
+    for (int w = 0; w < 2; ++w) {
+      o << "        if (rw" << w << "_ <= r1) {\n        const i64 row = rw" << w << "_;\n";
+      for (int c = 0; c < P.nc; ++c) gen_alias(o, c, P.col[c], w ? "_B" : "_A");
+      o << body.str() << "        }\n";
+    }
+    o << "      }\n";
+  }
   o << "      c = min(c1_, off + (e - s + 1));\n";
   if (pipe)
     o << "      const i64 next_slot = (c < c1_ && more_) ? n_slot : -1;\n";
@@ -460,6 +502,7 @@ std::string plan_signature(const dev::XgPlan& P, int minb, int pf) {
   put(minb);
   put(pf);
   put(pipeline_segments() ? 1 : 0);
+  put(pf == 0 ? window_unroll() : 1);
   put(P.nc);
   for (int c = 0; c < P.nc; ++c) {
     put(P.col[c].dt);
