@@ -328,8 +328,9 @@ class C2(Workload):
         return alg_bytes(h["a"]) + alg_bytes(h["b"]) + alg_bytes(h["c"])
 
     def query(self, rq, d, path, comm=None):
-        if path == "fused":
-            return rq.agg.filtered_aggregate_binop(d["c"], self.k, "<", d["a"], d["b"], "*", "sum", comm=comm)
+        if path == "fused":  # arguments marshalled once per table (agg.prepare_filtered_binop)
+            return self.prepared(lambda rq_, t, cm: rq_.agg.prepare_filtered_binop(t["c"], self.k, "<", t["a"], t["b"],
+                                                                                  "*", "sum", comm=cm), rq, d, comm)()
         m = rq.compute.compare_scalar(d["c"], self.k, "<")
         return rq.agg.aggregate_all(rq.compute.arith(rq.compute.filter(d["a"], m), rq.compute.filter(d["b"], m), "*"),
                                     "sum", comm=comm)
@@ -362,8 +363,9 @@ class C1(Workload):
         return alg_bytes(h["a"]) + alg_bytes(h["b"])
 
     def query(self, rq, d, path, comm=None):
-        if path == "fused":
-            return rq.agg.aggregate_binop(d["a"], d["b"], "+", "sum", comm=comm)
+        if path == "fused":  # arguments marshalled once per table (agg.prepare_binop)
+            return self.prepared(lambda rq_, t, cm: rq_.agg.prepare_binop(t["a"], t["b"], "+", "sum", comm=cm),
+                                 rq, d, comm)()
         return rq.agg.aggregate_all(rq.compute.arith(d["a"], d["b"], "+"), "sum", comm=comm)
 
     def oracle_partial(self, h):

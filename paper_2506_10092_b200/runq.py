@@ -1222,6 +1222,55 @@ class agg:
         return _agg_result(dt, i, f)
 
 
+def _prepared_call(fnc, args, keep, dt, i, f):
+    """A fused scalar call with its ctypes arguments built once: calling it
+    runs the query again on the same device handles (`keep` holds them)."""
+    def run():
+        check(fnc(*args))
+        return _agg_result(dt, i, f)
+    run.handles = keep
+    return run
+
+
+def prepare_binop(a, b, op, fn, comm: Comm = None):
+    """agg.aggregate_binop with its arguments marshalled once (the call a
+    repeated query makes): returns a callable running rq_aggregate_binop(_sharded)."""
+    op = H.BINOP_NAMES.get(op, op)
+    fn = H.AGG_NAMES.get(fn, fn)
+    ctx = _ctx_of(a, b)
+    da, db = upload(a, ctx), upload(b, ctx)
+    dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+    out = (C.byref(dt), C.byref(i), C.byref(f))
+    if comm is not None:
+        return _prepared_call(_L.rq_aggregate_binop_sharded,
+                              (ctx.handle, comm.handle, da.handle, db.handle, op, fn) + out, (da, db, comm), dt, i, f)
+    return _prepared_call(_L.rq_aggregate_binop, (ctx.handle, da.handle, db.handle, op, fn) + out, (da, db), dt, i, f)
+
+
+def prepare_filtered_binop(c, k, cmp, a, b, op, fn, comm: Comm = None):
+    """agg.filtered_aggregate_binop with its arguments marshalled once:
+    returns a callable running rq_filtered_aggregate_binop(_sharded)."""
+    op = H.BINOP_NAMES.get(op, op)
+    cmp = H.BINOP_NAMES.get(cmp, cmp)
+    fn = H.AGG_NAMES.get(fn, fn)
+    ctx = _ctx_of(c, a, b)
+    dc, da, db = upload(c, ctx), upload(a, ctx), upload(b, ctx)
+    ks = H.make_scalar(k)
+    dt, i, f = C.c_int32(), C.c_int64(), C.c_double()
+    out = (C.byref(dt), C.byref(i), C.byref(f))
+    if comm is not None:
+        return _prepared_call(_L.rq_filtered_aggregate_binop_sharded,
+                              (ctx.handle, comm.handle, dc.handle, ks, cmp, da.handle, db.handle, op, fn) + out,
+                              (dc, da, db, ks, comm), dt, i, f)
+    return _prepared_call(_L.rq_filtered_aggregate_binop,
+                          (ctx.handle, dc.handle, ks, cmp, da.handle, db.handle, op, fn) + out, (dc, da, db, ks),
+                          dt, i, f)
+
+
+agg.prepare_binop = staticmethod(prepare_binop)
+agg.prepare_filtered_binop = staticmethod(prepare_filtered_binop)
+
+
 def shard_host_column(col: H.Column, lo: int, hi: int) -> H.Column:
     """rq_shard_host_column: rows [lo, hi) as a standalone shard (host only)."""
     img, keep = H.column_image(col)
