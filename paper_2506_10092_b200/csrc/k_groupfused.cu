@@ -2729,7 +2729,13 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       RQ_CUDA_CHECK(cudaMemsetAsync(part.raw_mut(), 0, static_cast<size_t>(rows * cells) * 8, ctx->stream));
       return part.as<double>();
     };
-    if (nseg) {
+    // keyless plans of row-evaluated SUMs read neither the per-slot row counts
+    // nor any per-segment term: no segment pass (Q6: one launch less)
+    static const bool always_segs = std::getenv("RQ_XG_ALWAYS_SEGS") != nullptr;  // A/B knob
+    bool need_segs = always_segs || !keys.empty();
+    for (int i = 0; i < P.ne; ++i)
+      need_segs = need_segs || !P.e[i].rows || P.e[i].nt == 0 || fns[static_cast<size_t>(i)] != RQ_SUM;
+    if (nseg && need_segs) {
       dev::XgIsF sf{};
       bool any_sf = false;
       for (int i = 0; i < P.ne; ++i) {
