@@ -71,7 +71,8 @@ const char* kPrelude = R"(
 typedef long long i64;
 typedef unsigned long long u64;
 struct XgSegs { const i64* s; const i64* e; const i64* off; const i64* slot; const u64* cst; i64 n; i64 ncov;
-                double* dpart; i64 dcells; const i64* dims; i64 cstride; const i64* cstart; };
+                double* dpart; i64 dcells; const i64* dims; i64 cstride; const i64* cstart;
+                unsigned* fticket; i64 fchunks; unsigned fmask; };
 struct XgCol { const void* v; i64 center; };
 struct XgK { i64 i[24]; double f[24]; };
 __device__ __forceinline__ i64 ldg64(const i64* p, i64 i) { return __ldg(p + i); }
@@ -415,7 +416,37 @@ std::string gen_source(const dev::XgPlan& P, std::vector<int64_t>& ki, std::vect
     else
       o << "        case " << e << ": atomicAdd(gtab + i, v); break;\n";
   }
-  o << "        default: break;\n      }\n    }\n  }\n}\n";
+  o << "        default: break;\n      }\n    }\n  }\n";
+  // the last CTA folds the per-chunk f64 partials in a fixed order (same
+  // bits every run): chunk-strided sums per thread, then a fixed tree
+  o << "  if (S.fticket) {\n"
+       "    __shared__ bool last_;\n"
+       "    __threadfence();\n    __syncthreads();\n"
+       "    if (threadIdx.x == 0) last_ = atomicInc(S.fticket, gridDim.x - 1) == gridDim.x - 1;\n"
+       "    __syncthreads();\n"
+       "    if (last_) {\n"
+       "      __threadfence();\n"
+       "      double* red = (double*)stab;\n"
+       "      for (i64 cell = 0; cell < S.dcells; ++cell) {\n"
+       "        if (!((S.fmask >> (int)(cell % NE)) & 1u)) continue;\n"
+       "        double f0 = 0.0, f1 = 0.0;\n"
+       "        i64 q = threadIdx.x;\n"
+       "        for (; q + 256 < S.fchunks; q += 512) {\n"
+       "          f0 += __ldcg(S.dpart + q * S.dcells + cell);\n"
+       "          f1 += __ldcg(S.dpart + (q + 256) * S.dcells + cell);\n"
+       "        }\n"
+       "        if (q < S.fchunks) f0 += __ldcg(S.dpart + q * S.dcells + cell);\n"
+       "        red[threadIdx.x] = f0 + f1;\n"
+       "        __syncthreads();\n"
+       "        for (int w = 128; w > 0; w >>= 1) {\n"
+       "          if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];\n"
+       "          __syncthreads();\n"
+       "        }\n"
+       "        if (threadIdx.x == 0) ((double*)gtab)[cell] = red[0];\n"
+       "        __syncthreads();\n"
+       "      }\n"
+       "    }\n"
+       "  }\n}\n";
   return o.str();
 }
 

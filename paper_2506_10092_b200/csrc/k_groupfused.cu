@@ -2782,11 +2782,28 @@ bool xg_fused(const CtxPtr& ctx, const DMask* mask, const std::vector<const DCol
       kernel_occupancy(ctx, dev::k_xg_rows<B>, B, smem);  // shared-memory opt-in on this device
       KTimer rows_timer(ctx, "xg_rows");
       const char* nojit = std::getenv("RQ_NO_JIT");
-      if ((nojit && nojit[0] == '1') ||
-          !xg_jit_launch(ctx, P, S, chunk, tabp, G, err, static_cast<unsigned>(blocks), avg_len))
-        dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
+      bool folded = false;  // the generated kernel's last CTA folded dpart
+      bool jit_ran = false;
+      if (!(nojit && nojit[0] == '1')) {
+        dev::XgSegs SJ = S;
+        // few f64 cells (Q6: one): fold inside the row kernel, no k_xg_dfold
+        // launch; many cells (Q1: 48) keep the one-block-per-cell fold
+        static const bool no_kfold = std::getenv("RQ_XG_NO_KFOLD") != nullptr;  // A/B knob
+        unsigned fmask = 0;
+        int nf = 0;
+        for (int i = 0; i < P.ne; ++i)
+          if (P.e[i].rows && P.e[i].acc_f) fmask |= 1u << i, ++nf;
+        if (S.dpart && !no_kfold && G * nf <= 4) {
+          SJ.fticket = ctx->tickets + 8;
+          SJ.fchunks = dchunks;
+          SJ.fmask = fmask;
+        }
+        jit_ran = xg_jit_launch(ctx, P, SJ, chunk, tabp, G, err, static_cast<unsigned>(blocks), avg_len);
+        folded = jit_ran && SJ.fticket != nullptr;
+      }
+      if (!jit_ran) dev::k_xg_rows<B><<<static_cast<unsigned>(blocks), B, smem, ctx->stream>>>(P, S, chunk, tabp, G, err);
       launched(ctx);
-      if (S.dpart) {
+      if (S.dpart && !folded) {
         dev::XgIsF isf{};  // by value: no host staging
         for (int i = 0; i < P.ne; ++i) isf.f[i] = P.e[i].rows && P.e[i].acc_f;
         dev::k_xg_dfold<<<static_cast<unsigned>(cells), dev::DFOLD_B, 0, ctx->stream>>>(S.dpart, dchunks, cells, P.ne, isf,

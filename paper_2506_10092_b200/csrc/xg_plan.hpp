@@ -63,6 +63,12 @@ struct XgSegs {
   // k-way tables: the segment holding each row chunk's first covered row
   // (chunk q starts at row q * xg_chunk(ncov, nwarps)); null: searched in off
   const int64_t* cstart;
+  // generated row kernel only: the f64 fold of dpart done by the last CTA to
+  // finish (ticket wraps back to 0) for the expressions in fmask, instead of a
+  // separate k_xg_dfold launch; null: no in-kernel fold
+  unsigned* fticket;
+  int64_t fchunks;
+  unsigned fmask;
 };
 
 // rows per warp chunk of the row kernels: at least 512, a multiple of 128,
