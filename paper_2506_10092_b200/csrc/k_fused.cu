@@ -517,7 +517,8 @@ struct C2Stage {
   static constexpr size_t A_OFF = 0;
   static constexpr size_t C_OFF = A_OFF + A_CAP * 8;
   static constexpr size_t CV_OFF = C_OFF + C_CAP * 8;
-  static constexpr size_t BYTES = CV_OFF + C_CAP * 8;
+  static constexpr size_t F_OFF = CV_OFF + C_CAP * 8;  // C's predicate per staged run (producer-written)
+  static constexpr size_t BYTES = F_OFF + ((C_CAP + 15) & ~15);
 };
 
 template <int BLOCK, int ITEMS>
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   constexpr bool HAS_C = CK != C_PLAIN;
   using S = C2Stage<AW, CW>;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[NS], empty[NS];
+  __shared__ uint64_t full[NS], empty[NS], ready[NS];
   __shared__ int64_t s_lo[NS][2];  // [stage][A, C] first staged run
   __shared__ int s_n[NS][2];       // [stage][A, C] staged runs
 
@@ -559,11 +560,13 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   auto sA = [&](int st) { return reinterpret_cast<int64_t*>(smem + st * S::BYTES + S::A_OFF); };
   auto sC = [&](int st) { return reinterpret_cast<int64_t*>(smem + st * S::BYTES + S::C_OFF); };
   auto sCv = [&](int st) { return smem + st * S::BYTES + S::CV_OFF; };
+  auto sF = [&](int st) { return smem + st * S::BYTES + S::F_OFF; };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 32);  // every producer lane arrives (releasing its own stores)
       mbar_init(&empty[i], NCW);
+      mbar_init(&ready[i], 32);  // producer lanes, after C's predicate flags of the landed stage
     }
   }
   __syncthreads();
@@ -602,6 +605,11 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                               p_first, a_cur, c_cur);
       } else {
         mbar_wait(&full[pst], ((t - 1 - t_begin) / NS) & 1);  // tile t-1 landed
+        // C's predicate once per staged run of tile t-1 (the consumers read a
+        // flag byte per point instead of comparing the value), then publish
+        if (HAS_C)
+          for (int i = lane; i < c_n; i += 32) sF(pst)[i] = c_smem_pass(c, sCv(pst), i) ? 1 : 0;
+        mbar_arrive(&ready[pst]);
         const int ra = smem_lb_pow2<AW>(sA(pst), AW, p_first);
         int64_t an = a_lo16 + ra;
         if (ra >= a_n && an < x.n) an += warp_lower_bound(x.e + an, x.n - an, p_first);
@@ -669,6 +677,13 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       }
       __syncwarp();
     }
+    if (t_begin < t_end) {  // the last tile's flags
+      const int lst = static_cast<int>((t_end - 1 - t_begin) % NS);
+      mbar_wait(&full[lst], ((t_end - 1 - t_begin) / NS) & 1);
+      if (HAS_C)
+        for (int i = lane; i < c_n; i += 32) sF(lst)[i] = c_smem_pass(c, sCv(lst), i) ? 1 : 0;
+      mbar_arrive(&ready[lst]);
+    }
   } else {
     // ---- consumer warps: ITEMS consecutive points per lane ---------------------
     const int i0 = ((wid - 1) * 32 + lane) * ITEMS;
@@ -680,7 +695,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       const int64_t tbase = t * TILE;
       const int npt = static_cast<int>(np - tbase < TILE ? np - tbase : TILE);
       if (t + 1 < t_end) load_keys<BLOCK, ITEMS>(P, np, tbase + TILE + i0, nxt);
-      mbar_wait(&full[st], use & 1u);
+      mbar_wait(&ready[st], use & 1u);  // landed (the producer saw `full`) and flagged
       const int64_t a16 = s_lo[st][0], c16 = s_lo[st][1];
       const int na = s_n[st][0], nc = s_n[st][1];
       const int64_t* wA = sA(st);
@@ -734,7 +749,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
             if (cr < c.n) cr = lb_window(c.e, cr, c.n, p);
             pass = pass && cr < c.n && (CK == C_RLE_GAPLESS || ldg64(c.s, cr) <= p) && c_run_pass(c, cr);
           } else {
-            pass = pass && (CK == C_RLE_GAPLESS || ldg64(c.s, cr) <= p) && c_smem_pass(c, sCv(st), rc[k]);
+            pass = pass && (CK == C_RLE_GAPLESS || ldg64(c.s, cr) <= p) && sF(st)[rc[k]];
           }
         }
         take[k] = pass;
